@@ -1,0 +1,246 @@
+/* SPDX-License-Identifier: MIT
+ *
+ * scenopt_b200 — C-ABI of the B200-native MINFBE / NAMA hot path.
+ *
+ * This is the drop-in boundary for the reference library's solver path
+ * (arXiv 2107.01745 reference, /root/reference/proj/include/scenopt/). The
+ * reference is a header-only C++ API with Eigen value types and exceptions;
+ * it has no FFI layer of its own. Every entry point below replaces one
+ * reference function (cited per declaration) with plain pointers and sizes:
+ *   - 0 = success; a negative status maps 1:1 onto the reference exception
+ *     types of errors.hpp:9-80 (the C++ shim include/scenopt_b200.hpp
+ *     rethrows the same types), plus CUDA/NCCL/allocation failures;
+ *   - scenopt_last_error() returns the message of the calling thread's last
+ *     failure;
+ *   - inputs are never retained; outputs are caller-owned buffers;
+ *   - a scenopt_dev handle owns its device memory and one CUDA stream and is
+ *     not thread-safe; distinct handles may be used concurrently.
+ * There is no CPU fallback: device entry points fail with
+ * SCENOPT_E_NODEVICE when no B200 (sm_100) device is present.
+ *
+ * Memory layouts follow the reference exactly (column-major, node-indexed):
+ *   PrimalPoint.x  nx x num_nodes     (problem_data.hpp:64-67)
+ *   PrimalPoint.u  nu x first_leaf
+ *   dual vectors   stage blocks of nodes 1..n-1 in id order, then terminal
+ *                  blocks of leaves in id order (problem_data.hpp:84-87,126-140)
+ */
+#ifndef SCENOPT_B200_H
+#define SCENOPT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCENOPT_ABI_VERSION 1
+
+/* errors.hpp:9-80 */
+enum scenopt_status {
+  SCENOPT_OK = 0,
+  SCENOPT_E_ERROR = -1,
+  SCENOPT_E_NON_STOCHASTIC_MATRIX = -2,
+  SCENOPT_E_STAGE_OUT_OF_RANGE = -3,
+  SCENOPT_E_DIMENSION_MISMATCH = -4,
+  SCENOPT_E_UNSUPPORTED_SPEC = -5,
+  SCENOPT_E_NOT_STRONGLY_CONVEX = -6,
+  SCENOPT_E_SHAPE_CHANGED = -7,
+  SCENOPT_E_CACHE_MISMATCH = -8,
+  SCENOPT_E_LINE_SEARCH_STALLED = -9,
+  SCENOPT_E_STEP_UNDERFLOW = -10,
+  SCENOPT_E_ZERO_PROBABILITY = -11,
+  SCENOPT_E_INVALID_PARAMS = -12,
+  SCENOPT_E_INFINITE_CONJUGATE = -13,
+  SCENOPT_E_PARSE_ERROR = -14,
+  SCENOPT_E_CUDA = -20,
+  SCENOPT_E_NCCL = -21,
+  SCENOPT_E_NOMEM = -22,
+  SCENOPT_E_NODEVICE = -23
+};
+
+/* I/O flag for entry points that take vectors: buffers are host memory
+ * (copied in/out inside the call) instead of device memory of the handle's
+ * device. */
+#define SCENOPT_HOST_IO 1
+
+/* Flat, node-indexed problem description (ProblemInstance,
+ * problem_data.hpp:95-141). Per-node arrays have one slot per node with slot
+ * 0 (the root) unused; per-leaf arrays are indexed by leaf ordinal. All
+ * matrices column-major. The tree must be BFS ordered (scenario_tree.hpp:
+ * 228-238), which makes every node's children a contiguous id range. */
+typedef struct scenopt_problem_view {
+  int32_t nx, nu, num_stages, num_nodes;
+  const int32_t* ancestor;      /* [n], -1 at the root */
+  const double* probability;    /* [n] */
+  const int32_t* stage_offsets; /* [num_stages + 2] */
+  const double* root_state;     /* [nx] */
+  const double *A, *B, *c;      /* [n][nx*nx], [n][nx*nu], [n][nx] (NodeDynamics) */
+  const double *Q, *R, *S;      /* [n][nx*nx], [n][nu*nu], [n][nu*nx] (NodeCost) */
+  const double *q, *r;          /* [n][nx], [n][nu] */
+  const int32_t* stage_rows;    /* [n], rows of F_i/G_i (0 at the root) */
+  const double *F, *G;          /* node i's block at dual_offset[i]*nx / dual_offset[i]*nu */
+  const int32_t* g_kind;        /* [n] NonsmoothKind: 0 None, 1 Box, 2 ScaledL1 */
+  const double* g_gamma;        /* [n] */
+  const double *P, *p;          /* [L][nx*nx], [L][nx] (TerminalCost) */
+  const int32_t* terminal_rows; /* [L] */
+  const double* FN;             /* leaf l's block at (tdual_offset[l] - stage_rows_total)*nx */
+  const int32_t* tg_kind;       /* [L] */
+  const double* tg_gamma;       /* [L] */
+  const double *zmin, *zmax;    /* [dual_dim] box bounds in dual layout */
+} scenopt_problem_view;
+
+/* SolverConfig, solvers.hpp:28-46. backtracking_rule: 0 Original,
+ * 1 Simple, 2 None. */
+typedef struct scenopt_solver_config {
+  double lambda0, eps, eps_curv, eps_bt, beta_bt;
+  int32_t memory, max_iters, backtracking_rule, warm_start, warm_start_iters, precondition,
+      nama_parallel_linesearch, nama_update_tlambda;
+} scenopt_solver_config;
+
+/* Scalar part of SolverReport, solvers.hpp:66-84 (+ OracleStats,
+ * tree_oracles.hpp:14-21). status: 0 Converged, 1 MaxItersExceeded. */
+typedef struct scenopt_report_summary {
+  int32_t status, iterations, verified, trace_len;
+  uint64_t dual_grad_calls, hessian_vec_calls, prox_calls, conj_calls, lipschitz_calls;
+  double lipschitz_estimate, lambda_final, eps, residual_inf, wall_ms, verify_residual_inf,
+      verify_subdiff_dist;
+} scenopt_report_summary;
+
+/* Device handle facts used by the benchmark's roofline accounting. */
+typedef struct scenopt_dev_info {
+  int32_t device, sm_count, grid_ctas, ctas_per_sm, slots, items_bw, items_fw, nodes_per_item_max;
+  int64_t slot_bytes, matrix_bytes_bw, matrix_bytes_fw, device_bytes;
+  int64_t sweep_bytes_hom, sweep_bytes_aff, sweep_bytes_hom2; /* algorithmic bytes per sweep */
+} scenopt_dev_info;
+
+typedef struct scenopt_problem scenopt_problem;
+typedef struct scenopt_factor scenopt_factor;
+typedef struct scenopt_dev scenopt_dev;
+typedef struct scenopt_report scenopt_report;
+typedef struct scenopt_lbfgs scenopt_lbfgs;
+
+const char* scenopt_last_error(void);
+int scenopt_abi_version(void);
+int scenopt_device_count(void); /* sm_100 devices visible; 0 on a GPU-less host */
+
+/* ---- problem (host) ---------------------------------------------------- */
+/* ProblemInstance + finalize_layout(), problem_data.hpp:95-141 */
+int scenopt_problem_create(const scenopt_problem_view* v, scenopt_problem** out);
+/* gen_random_instance, generators.hpp:255-328, with per-stage branching
+ * br[t] (1 after the listed stages); nbranch == 1 and horizon entries equal
+ * reproduce the reference's full-branching tree. */
+int scenopt_problem_gen_random(uint64_t seed, int nx, int nu, int horizon, const int32_t* branching,
+                               int nbranch, scenopt_problem** out);
+/* Pointers into the handle's own arrays (valid until destroy). */
+int scenopt_problem_get_view(scenopt_problem* p, scenopt_problem_view* v, int32_t* dual_dim);
+/* dims = {nx, nu, num_stages, num_nodes, num_leaves, first_leaf, dual_dim, primal_dim} */
+int scenopt_problem_dims(const scenopt_problem* p, int32_t* dims);
+/* validate(ProblemInstance), problem_data.hpp:233-314: returns the number of
+ * violations, messages joined by '\n' into buf. */
+int scenopt_problem_validate(const scenopt_problem* p, char* buf, int buflen);
+/* precondition(), solvers.hpp:569-602 */
+int scenopt_problem_precondition(const scenopt_problem* p, scenopt_problem** out);
+void scenopt_problem_destroy(scenopt_problem* p);
+
+/* ---- factor (host, offline) -------------------------------------------- */
+/* factor(), riccati.hpp:82-182 */
+int scenopt_factor_create(const scenopt_problem* p, scenopt_factor** out);
+/* refactor_affine(), riccati.hpp:187-216 */
+int scenopt_refactor_affine(scenopt_factor* f, const scenopt_problem* p);
+/* FactorCache members, flattened (same layout as the oracle export). */
+int scenopt_factor_export(const scenopt_factor* f, double* gain, double* child_to_input,
+                          double* closed_loop, double* dual_to_input, double* dual_to_costate,
+                          double* input_affine, double* costate_affine, double* value_quad,
+                          double* leaf_costate_affine);
+void scenopt_factor_destroy(scenopt_factor* f);
+
+/* ---- device handle ----------------------------------------------------- */
+/* Packs (ProblemInstance, FactorCache) into the stage-major device layout and
+ * uploads it. */
+int scenopt_dev_create(const scenopt_problem* p, const scenopt_factor* f, int device,
+                       scenopt_dev** out);
+int scenopt_dev_info_get(const scenopt_dev* d, scenopt_dev_info* info);
+int scenopt_dev_synchronize(scenopt_dev* d);
+void scenopt_dev_destroy(scenopt_dev* d);
+/* Device scratch the caller may use for device-resident I/O (bench). */
+int scenopt_dev_alloc(scenopt_dev* d, size_t bytes, void** out);
+int scenopt_dev_free(scenopt_dev* d, void* ptr);
+int scenopt_dev_memcpy(scenopt_dev* d, void* dst, const void* src, size_t bytes, int kind);
+
+/* ---- oracles: tree_oracles.hpp:33-129 ----------------------------------- */
+/* One fused backward/forward sweep with apply_H in the epilogue for nrhs
+ * (1 or 2) right-hand sides. affine = 1: dual_grad (x(y)); 0: hessian_vec
+ * (x0(r)). x/u/Hx entries may be NULL to skip that output. */
+int scenopt_dev_sweep(scenopt_dev* d, int nrhs, int affine, const double* const* y,
+                      double* const* x, double* const* u, double* const* Hx, int flags);
+/* Same, enqueued on the handle's stream without a host synchronisation
+ * (device pointers only). */
+int scenopt_dev_sweep_async(scenopt_dev* d, int nrhs, int affine, const double* const* y,
+                            double* const* x, double* const* u, double* const* Hx);
+/* dual_grad / hessian_vec, tree_oracles.hpp:96-114 */
+int scenopt_dual_grad(scenopt_dev* d, const double* y, double* x, double* u, int flags);
+int scenopt_hessian_vec(scenopt_dev* d, const double* r, double* x, double* u, int flags);
+/* apply_H, problem_data.hpp:144-162 */
+int scenopt_apply_H(scenopt_dev* d, const double* x, const double* u, double* z, int flags);
+/* fhat_value, tree_oracles.hpp:125-129 */
+int scenopt_fhat_value(scenopt_dev* d, const double* y, double* out, int flags);
+
+/* ---- nonsmooth term: prox.hpp:58-171 ------------------------------------ */
+int scenopt_prox_g(scenopt_dev* d, const double* v, double gamma_prox, double* out, int flags);
+int scenopt_conj_value_g(scenopt_dev* d, const double* w, double* out, int flags);
+int scenopt_dist_subdiff_inf(scenopt_dev* d, const double* y, const double* z, double* out,
+                             int flags);
+
+/* ---- forward-backward machinery: fbe.hpp:22-231 ------------------------- */
+/* fb_step: scalars = {fhat, conj_T, znorm_sq, value} */
+int scenopt_fb_step(scenopt_dev* d, const double* y, double lambda, double* x, double* u,
+                    double* Hx, double* z, double* R, double* T, double* scalars, int flags);
+/* fbe_grad: grad = R + lambda H x0(R) */
+int scenopt_fbe_grad(scenopt_dev* d, const double* R, double lambda, double* grad, int flags);
+/* linesearch_cert (shift == NULL) / linesearch_cert_shifted + evaluate_cert
+ * at ntau taus; identical contract to the oracle's orc_linesearch_cert. */
+int scenopt_linesearch_cert(scenopt_dev* d, const double* y, const double* Hx, double lambda,
+                            const double* state_scalars, const double* shift, const double* dir,
+                            int ntau, const double* taus, double* deltas, double* cert_scalars,
+                            double* cert_fhat, double* w, double* Hx_w, double* z, double* R,
+                            double* T, int flags);
+
+/* ---- L-BFGS: lbfgs.hpp:22-84 (device-resident pairs) -------------------- */
+int scenopt_lbfgs_create(scenopt_dev* d, int memory, double eps_curv, scenopt_lbfgs** out);
+int scenopt_lbfgs_push(scenopt_lbfgs* b, const double* step, const double* change,
+                       double scale_ref, int flags); /* 1 accepted, 0 rejected, <0 error */
+int scenopt_lbfgs_apply(scenopt_lbfgs* b, const double* grad, double* out, int flags);
+int scenopt_lbfgs_clear(scenopt_lbfgs* b);
+int scenopt_lbfgs_size(const scenopt_lbfgs* b);
+double scenopt_lbfgs_gamma0(const scenopt_lbfgs* b);
+void scenopt_lbfgs_destroy(scenopt_lbfgs* b);
+
+/* ---- solvers: solvers.hpp:89-720 ---------------------------------------- */
+/* estimate_dual_lipschitz, solvers.hpp:89-113 */
+int scenopt_estimate_lipschitz(scenopt_dev* d, uint64_t* calls, double* out);
+/* solve_minfbe (kind 0) / solve_nama (1) / solve_gpad (2) from y0 (host,
+ * NULL = zeros), optional residual weight (host, NULL = none). */
+int scenopt_dev_solve(scenopt_dev* d, const scenopt_solver_config* cfg, int kind, const double* y0,
+                      const double* residual_weight, scenopt_report** out);
+/* warm_start, solvers.hpp:545-564 */
+int scenopt_warm_start(scenopt_dev* d, const scenopt_solver_config* cfg, double lambda,
+                       double* y_out, uint64_t* dual_grad_calls);
+/* solve(), solvers.hpp:645-720: precondition, factor (unless shared),
+ * Lipschitz estimate, warm start, solver run, verify_report. */
+int scenopt_solve(const scenopt_problem* p, const scenopt_solver_config* cfg, int kind,
+                  const scenopt_factor* shared, int device, scenopt_report** out);
+int scenopt_report_summary_get(const scenopt_report* r, scenopt_report_summary* s);
+/* x [nx*n], u [nu*first_leaf], y/z [dual_dim], traces [trace_len]; NULL skips */
+int scenopt_report_arrays(const scenopt_report* r, double* x, double* u, double* y, double* z,
+                          double* residual_trace, double* fbe_trace);
+/* verify_report, solvers.hpp:630-639, against problem p (z_override: host
+ * dual vector replacing the report's z first, or NULL). */
+int scenopt_verify_report(const scenopt_problem* p, scenopt_report* r, const double* z_override,
+                          int device);
+void scenopt_report_destroy(scenopt_report* r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCENOPT_B200_H */

@@ -1,0 +1,95 @@
+// SPDX-License-Identifier: MIT
+// Device-resident packed instance (the scenopt_dev handle).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../cuda/layout.hpp"
+#include "model.hpp"
+
+namespace scn {
+
+#define SCN_CUDA(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      ::scn::fail(_e == cudaErrorMemoryAllocation ? SCENOPT_E_NOMEM : SCENOPT_E_CUDA,      \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                     \
+  } while (0)
+
+// Device buffer owned by a handle (freed in ~DevState).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+};
+
+struct Layout {  // host copy of the layout numbers the device code needs
+  int nx = 0, nu = 0, N = 0, n = 0, L = 0, first_leaf = 0, dual_dim = 0, stage_total = 0;
+  std::vector<int32_t> ancestor, stage_offsets, stage_rows, terminal_rows, child_begin,
+      child_count, dual_offset, tdual_offset;
+  std::vector<double> probability, root_state;
+};
+
+struct DevState {
+  int device = 0, sm_count = 0;
+  cudaStream_t stream = nullptr;
+  Layout lay;
+  size_t bytes_allocated = 0;
+  std::vector<void*> owned;
+
+  // packed matrices and metadata
+  double *bw_blk = nullptr, *fw_blk = nullptr, *aff_bw = nullptr, *aff_fw = nullptr,
+         *root_state = nullptr;
+  Item* items = nullptr;
+  NodeMeta* meta = nullptr;
+  int64_t *bw_off = nullptr, *fw_off = nullptr;
+  unsigned *ctrl = nullptr, *bw_flag = nullptr, *fw_flag = nullptr;
+  int64_t bw_doubles = 0, fw_doubles = 0;
+  int items_bw = 0, items_fw = 0, max_count = 1, max_m = 0, max_mN = 0;
+  // per dual row: nonsmooth kind, box bounds, l1 radius weight*gamma
+  int8_t* row_kind = nullptr;
+  double *row_lo = nullptr, *row_hi = nullptr, *row_wg = nullptr;
+  // sweep scratch (2 RHS)
+  double* contrib[kMaxRhs] = {nullptr, nullptr};
+  double* xs[kMaxRhs] = {nullptr, nullptr};
+  double* us[kMaxRhs] = {nullptr, nullptr};
+  double* hs[kMaxRhs] = {nullptr, nullptr};
+  double* ys[kMaxRhs] = {nullptr, nullptr};
+  // launch configuration
+  int grid = 0, ctas_per_sm = 0, nslot = 0, slot_doubles = 0, vec_doubles = 0, G = 16;
+  size_t dyn_smem = 0;
+  // algorithmic bytes per sweep
+  int64_t bytes_hom = 0, bytes_aff = 0, bytes_hom2 = 0;
+
+  ~DevState();
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    SCN_CUDA(cudaMalloc(&p, count * sizeof(T) + 16));
+    owned.push_back(p);
+    bytes_allocated += count * sizeof(T);
+    return static_cast<T*>(p);
+  }
+  void free_owned(void* p);
+};
+
+std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int device);
+int device_count_sm100();
+
+// One fused sweep over nrhs right-hand sides; y/x/u/Hx are device pointers
+// (x/u/Hx may be null: the handle's scratch is used). Enqueued on d.stream.
+void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
+               double* const* u, double* const* Hx);
+
+// kernel launchers (cuda/*.cu)
+cudaError_t sweep_configure(int nrhs, size_t dyn_smem);
+cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem);
+cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int G, int mmax,
+                         cudaStream_t stream);
+
+}  // namespace scn

@@ -1,0 +1,52 @@
+// SPDX-License-Identifier: MIT
+// Host/device I/O helpers of the scenopt_dev handle.
+#include "capi_internal.hpp"
+
+using namespace scn;
+
+void scenopt_dev::sync() { SCN_CUDA(cudaStreamSynchronize(d->stream)); }
+
+const double* scenopt_dev::in_dual(const double* src, int flags, int slot) {
+  if (!(flags & SCENOPT_HOST_IO)) return src;
+  if (!src) fail(SCENOPT_E_INVALID_PARAMS, "null input vector");
+  double* dst = d->ys[slot];
+  SCN_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * static_cast<size_t>(d->lay.dual_dim),
+                           cudaMemcpyHostToDevice, d->stream));
+  return dst;
+}
+
+void scenopt_dev::out_copy(double* dst, const double* dev_src, size_t count, int flags) {
+  if (!dst || dst == dev_src) return;
+  SCN_CUDA(cudaMemcpyAsync(dst, dev_src, sizeof(double) * count,
+                           (flags & SCENOPT_HOST_IO) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                           d->stream));
+}
+
+void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* const* x,
+                        double* const* u, double* const* Hx, int flags, bool sync_after) {
+  SCN_CUDA(cudaSetDevice(d->device));
+  if (nrhs < 1 || nrhs > kMaxRhs) fail(SCENOPT_E_INVALID_PARAMS, "sweep: nrhs must be 1 or 2");
+  const Layout& L = d->lay;
+  const double* yd[kMaxRhs] = {nullptr, nullptr};
+  double* xd[kMaxRhs] = {nullptr, nullptr};
+  double* ud[kMaxRhs] = {nullptr, nullptr};
+  double* hd[kMaxRhs] = {nullptr, nullptr};
+  const bool host = (flags & SCENOPT_HOST_IO) != 0;
+  for (int r = 0; r < nrhs; ++r) {
+    yd[r] = in_dual(y[r], flags, r);
+    if (!host) {
+      xd[r] = x ? x[r] : nullptr;
+      ud[r] = u ? u[r] : nullptr;
+      hd[r] = Hx ? Hx[r] : nullptr;
+    }
+  }
+  dev_sweep(*d, nrhs, affine, yd, xd, ud, hd);
+  if (host) {
+    for (int r = 0; r < nrhs; ++r) {
+      if (x && x[r]) out_copy(x[r], d->xs[r], static_cast<size_t>(L.nx) * L.n, flags);
+      if (u && u[r]) out_copy(u[r], d->us[r], static_cast<size_t>(L.nu) * L.first_leaf, flags);
+      if (Hx && Hx[r]) out_copy(Hx[r], d->hs[r], static_cast<size_t>(L.dual_dim), flags);
+    }
+  }
+  if (sync_after || host) sync();
+}

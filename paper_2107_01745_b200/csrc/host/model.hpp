@@ -1,0 +1,93 @@
+// SPDX-License-Identifier: MIT
+// Host-side data model of the scenopt_b200 library: the flat, node-indexed
+// problem (ProblemInstance, problem_data.hpp:95-141) and the factor cache
+// (FactorCache, riccati.hpp:38-63) in contiguous arrays that the packer
+// (pack.cpp) turns into the device layout.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "scenopt_b200.h"
+
+namespace scn {
+
+// errors.hpp:9-80 as status-carrying exceptions; the C-ABI converts them.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+struct Problem {
+  int nx = 0, nu = 0, N = 0, n = 0, L = 0, first_leaf = 0, dual_dim = 0, stage_total = 0;
+  std::vector<int32_t> ancestor, stage_offsets, stage_rows, terminal_rows, g_kind, tg_kind;
+  std::vector<double> probability, root_state, A, B, c, Q, R, S, q, r, F, G, g_gamma, P, p, FN,
+      tg_gamma, zmin, zmax;
+  // derived (finalize)
+  std::vector<int32_t> node_stage, child_begin, child_count, dual_offset, tdual_offset;
+
+  void finalize();  // layout + child ranges (problem_data.hpp:126-140)
+  size_t sxx() const { return static_cast<size_t>(nx) * nx; }
+  size_t sxu() const { return static_cast<size_t>(nx) * nu; }
+  size_t suu() const { return static_cast<size_t>(nu) * nu; }
+  const double* Ai(int i) const { return A.data() + i * sxx(); }
+  const double* Bi(int i) const { return B.data() + i * sxu(); }
+  const double* ci(int i) const { return c.data() + static_cast<size_t>(i) * nx; }
+  const double* Qi(int i) const { return Q.data() + i * sxx(); }
+  const double* Ri(int i) const { return R.data() + i * suu(); }
+  const double* Si(int i) const { return S.data() + i * sxu(); }
+  const double* qi(int i) const { return q.data() + static_cast<size_t>(i) * nx; }
+  const double* ri(int i) const { return r.data() + static_cast<size_t>(i) * nu; }
+  const double* Fi(int i) const { return F.data() + static_cast<size_t>(dual_offset[i]) * nx; }
+  const double* Gi(int i) const { return G.data() + static_cast<size_t>(dual_offset[i]) * nu; }
+  const double* Pl(int l) const { return P.data() + l * sxx(); }
+  const double* pl(int l) const { return p.data() + static_cast<size_t>(l) * nx; }
+  const double* FNl(int l) const {
+    return FN.data() + static_cast<size_t>(tdual_offset[l] - stage_total) * nx;
+  }
+  int primal_dim() const { return first_leaf * nu + (n - 1) * nx; }
+};
+
+Problem problem_from_view(const scenopt_problem_view& v);
+void problem_to_view(const Problem& p, scenopt_problem_view* v);
+std::vector<std::string> validate(const Problem& p);
+void require_valid(const Problem& p);
+Problem precondition(const Problem& p);                 // solvers.hpp:569-602
+std::vector<double> probability_roots(const Problem& p);  // solvers.hpp:608-623
+Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector<int>& br);
+
+struct Factor {
+  int nx = 0, nu = 0, n = 0, first_leaf = 0, dual_dim = 0, L = 0, stage_total = 0;
+  std::vector<int32_t> child_dual_offset, child_dual_rows;
+  std::vector<double> gain;             // [F][nu*nx]
+  std::vector<double> dual_to_input;    // by child_dual_offset: nu x M_i
+  std::vector<double> dual_to_costate;  // by child_dual_offset: nx x M_i
+  std::vector<double> input_affine;     // [F][nu]
+  std::vector<double> costate_affine;   // [F][nx]
+  std::vector<double> input_hessian;    // [F][nu*nu]
+  std::vector<double> child_to_input;   // [n][nu*nx]
+  std::vector<double> closed_loop;      // [n][nx*nx]
+  std::vector<double> value_quad;       // [n][nx*nx]
+  std::vector<double> leaf_costate_affine;  // [L][nx]
+};
+
+Factor factor(const Problem& p);                // riccati.hpp:82-182
+void refactor_affine(Factor& f, const Problem& p);  // riccati.hpp:187-216
+void check_factor_shape(const Factor& f, const Problem& p, const char* who);
+
+// small dense helpers (column-major)
+double sym_min_eig(const double* S, int n);
+double spectral_radius(const double* A, int n);
+// Cholesky in place (lower); returns false when not SPD
+bool cholesky(std::vector<double>& a, int n);
+// solve L L' X = B in place, B is n x k column-major
+void chol_solve(const std::vector<double>& L, int n, double* B, int k);
+
+// Parallel-for over [0, count) on the host worker pool (setup code only).
+void parallel_for(int count, int grain, const std::function<void(int, int)>& body);
+
+}  // namespace scn

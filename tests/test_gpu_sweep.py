@@ -1,0 +1,119 @@
+"""GPU parity of the fused sweep (dual_grad / hessian_vec, tree_oracles.hpp:
+33-114) against the CPU oracle, plus the reference's property tests
+(test_tree_oracles.cpp) run through the CUDA path. Tolerance: 1e-9
+relative (north_star), using the reference's rel_gap metric."""
+import numpy as np
+import pytest
+
+import paper_2107_01745_b200 as so
+from oracle import oracle as orc
+from tests import support as sup
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def both(prob_o):
+    """Same instance bytes on both sides."""
+    flat = prob_o.flat()
+    prob = so.ProblemInstance.from_flat(flat)
+    return prob, so.factor(prob), orc.Factor(prob_o)
+
+
+def test_dual_grad_matches_oracle_on_random_trees(gpu):
+    rng = orc.Rng(41)  # test_tree_oracles.cpp:23-36
+    for trial in range(20):
+        stages = rng.integer(1, 5)
+        po = rng.random_instance(stages, 40, rng.integer(1, 4), rng.integer(1, 4))
+        prob, cache, ofac = both(po)
+        y = rng.vector(prob.dual_dim, 2.0)
+        fast = so.dual_grad(cache, prob, y)
+        ox, ou = ofac.dual_grad(y)
+        gap = sup.rel_gap(ox, ou, fast.x.ravel(order="F"), fast.u.ravel(order="F"))
+        assert gap < TOL, (trial, gap)
+        kx, ku = sup.kkt_dual_grad(po.flat(), y)
+        assert sup.rel_gap(kx, ku, fast.x.ravel(order="F"), fast.u.ravel(order="F")) < 1e-8
+
+
+def test_hessian_vec_matches_oracle_and_homogeneity(gpu):
+    rng = orc.Rng(43)  # test_tree_oracles.cpp:64-81
+    for trial in range(10):
+        po = rng.random_instance(rng.integer(1, 4), 30, 3, 2)
+        prob, cache, ofac = both(po)
+        y = rng.vector(prob.dual_dim, 2.0)
+        r = rng.vector(prob.dual_dim, 2.0)
+        hom = so.hessian_vec(cache, prob, r)
+        ox, ou = ofac.hessian_vec(r)
+        assert sup.rel_gap(ox, ou, hom.x.ravel(order="F"), hom.u.ravel(order="F")) < TOL
+        a = so.dual_grad(cache, prob, y)
+        b = so.dual_grad(cache, prob, y + r)
+        dx, du = (b.x - a.x).ravel(order="F"), (b.u - a.u).ravel(order="F")
+        assert sup.rel_gap(dx, du, hom.x.ravel(order="F"), hom.u.ravel(order="F")) < TOL
+
+
+@pytest.mark.parametrize("opt", [dict(), dict(with_l1=True, with_none=True),
+                                 dict(affine=False, stage_rows_lo=0, stage_rows_hi=3)])
+def test_fused_apply_H_matches_oracle(gpu, opt):
+    rng = orc.Rng(12)
+    for trial in range(6):
+        po = rng.random_instance(rng.integer(1, 4), 60, rng.integer(1, 5), rng.integer(1, 4),
+                                 orc.InstanceOptions(**opt))
+        prob, cache, ofac = both(po)
+        y = rng.vector(prob.dual_dim, 1.5)
+        for affine in (True, False):
+            pts, hs = so.sweep(cache, [y], affine)
+            ox, ou = ofac.sweep(y, affine)
+            Hx = orc.apply_H(po, ox, ou)
+            assert np.abs(hs[0] - Hx).max() <= TOL * (1 + np.abs(Hx).max())
+
+
+def test_two_rhs_sweep_is_bitwise_two_single_sweeps(gpu):
+    rng = orc.Rng(1213)
+    po = rng.random_instance(4, 120, 4, 3, orc.InstanceOptions(with_l1=True, with_none=True))
+    prob, cache, _ = both(po)
+    a = rng.vector(prob.dual_dim)
+    b = rng.vector(prob.dual_dim)
+    for affine in (False, True):
+        pts2, hs2 = so.sweep(cache, [a, b], affine)
+        pa, ha = so.sweep(cache, [a], affine)
+        pb, hb = so.sweep(cache, [b], affine)
+        assert np.array_equal(hs2[0], ha[0]) and np.array_equal(hs2[1], hb[0])
+        assert np.array_equal(pts2[0].x, pa[0].x) and np.array_equal(pts2[1].u, pb[0].u)
+
+
+@pytest.mark.parametrize("shape", [(10, 5, 10, [2, 2, 2]), (6, 3, 6, [3, 1, 4]),
+                                   (20, 8, 5, [8, 8]), (50, 20, 3, [8, 8])])
+def test_generated_configs_match_oracle(gpu, shape):
+    nx, nu, N, br = shape
+    prob = so.gen_random_instance(1, nx, nu, N, br)
+    po = orc.Problem.from_flat(prob.flat())
+    cache = so.factor(prob)
+    ofac = orc.Factor(po)
+    rng = np.random.default_rng(5)
+    y = rng.uniform(-1, 1, prob.dual_dim)
+    for fn, ofn in ((so.dual_grad, ofac.dual_grad), (so.hessian_vec, ofac.hessian_vec)):
+        pt = fn(cache, prob, y)
+        ox, ou = ofn(y)
+        assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL
+
+
+def test_repeated_sweeps_are_deterministic(gpu):
+    prob = so.gen_random_instance(3, 12, 4, 8, [3, 3, 2])
+    cache = so.factor(prob)
+    y = np.linspace(-1, 1, prob.dual_dim)
+    first = so.dual_grad(cache, prob, y)
+    for _ in range(20):
+        again = so.dual_grad(cache, prob, y)
+        assert np.array_equal(first.x, again.x) and np.array_equal(first.u, again.u)
+
+
+def test_oracle_errors_mirror_reference(gpu):
+    rng = orc.Rng(47)  # test_tree_oracles.cpp:143-152
+    prob = so.ProblemInstance.from_flat(rng.random_instance(2, 12, 2, 2).flat())
+    other = so.ProblemInstance.from_flat(rng.random_instance(2, 12, 3, 2).flat())
+    cache = so.factor(prob)
+    with pytest.raises(so.CacheMismatch):
+        so.dual_grad(cache, other, np.zeros(other.dual_dim))
+    with pytest.raises(so.DimensionMismatch):
+        so.hessian_vec(cache, prob, np.zeros(prob.dual_dim + 1))

@@ -162,6 +162,8 @@ int scenopt_dev_create(const scenopt_problem* p, const scenopt_factor* f, int de
                        scenopt_dev** out);
 int scenopt_dev_info_get(const scenopt_dev* d, scenopt_dev_info* info);
 int scenopt_dev_synchronize(scenopt_dev* d);
+/* The handle's CUDA stream (cudaStream_t) for event timing by callers. */
+int scenopt_dev_stream(scenopt_dev* d, void** stream);
 void scenopt_dev_destroy(scenopt_dev* d);
 /* Device scratch the caller may use for device-resident I/O (bench). */
 int scenopt_dev_alloc(scenopt_dev* d, size_t bytes, void** out);

@@ -13,7 +13,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libscenopt_b200.so")
+LIB_PATH = os.environ.get("SCENOPT_LIBRARY") or os.path.join(_HERE, "lib", "libscenopt_b200.so")
 
 I32P = C.POINTER(C.c_int32)
 F64P = C.POINTER(C.c_double)

@@ -1,66 +1,86 @@
 // SPDX-License-Identifier: MIT
 // Device layout shared by the packer (host) and the sweep kernel (device).
 //
-// Every node owns two contiguous, 16-byte aligned matrix blocks, stored in
-// node-id (= stage-major BFS) order so a stage is one contiguous stream:
+// Node matrices are "dot-column" blocks (every product is out[j] = <col j, v>):
 //
-//  BW block (read by the backward pass, tree_oracles.hpp:44-73), all columns
-//  are "dot columns": out[j] = <col j, vec>:
-//    interior node c:  E_c  = M_c x (nu+nx)   col j<nu : row j of dual_to_input_c
-//                                              col nu+k : row k of dual_to_costate_c
-//    leaf c:           FN_c = mN x nx          col k    : column k of F_N (F_N' y)
-//    non-root c:       J_c  = nx x (nu+nx)     col j<nu : row j of child_to_input_c
-//                                              col nu+k : column k of closed_loop_c
-//  FW block (read by the forward pass, tree_oracles.hpp:75-88, fused with
-//  apply_H, problem_data.hpp:144-162):
-//    non-root c:       W_c  = (nx+nu) x (nx+m_c)  col r<nx : row r of [A_c B_c]
-//                                                 col nx+s : row s of [F_c G_c]
-//    interior c:       K_c  = nx x nu          col j : row j of gain_c
-//    leaf c:           TN_c = nx x mN          col s : row s of F_N
+//  BW block (backward pass, tree_oracles.hpp:44-73):
+//    interior c:  E_c  = M_c x (nu+nx)   col j<nu : row j of dual_to_input_c
+//                                         col nu+k : row k of dual_to_costate_c
+//    leaf c:      FN_c = mN x nx          col k    : column k of F_N (F_N' y)
+//    non-root c:  J_c  = nxp x (nu+nx)    col j<nu : row j of child_to_input_c
+//                                         col nu+k : column k of closed_loop_c
+//  FW block (forward pass, tree_oracles.hpp:75-88, fused with apply_H,
+//  problem_data.hpp:144-162):
+//    non-root c:  W_c  = Vp x (nx+m_c)    col r<nx : row r of [A_c B_c]
+//                                             col nx+s : row s of [F_c G_c]
+//    interior c:  K_c  = nxp x nu         col j : row j of gain_c
+//    leaf c:      TN_c = nxp x mN         col s : row s of F_N
+//  Columns of J/W/K/TN are zero-padded to nxp = pad(nx), Vp = pad(nx+nu) with
+//  pad(l) == 2 (mod 4): 16-byte loads of one column per thread then hit all
+//  32 shared-memory banks without conflicts. E_c and FN_c (short columns)
+//  are unpadded and rounded to an even size so J_c stays 16-byte aligned.
 //
-// Items are runs of consecutive same-stage nodes; their blocks are therefore
-// contiguous and one TMA bulk copy moves a whole item into shared memory.
+// Items are runs of consecutive same-stage nodes. Each pass array stores its
+// items back to back in ticket order; an item is [NodeMeta x count | node
+// blocks], 16-byte aligned, so ONE cp.async.bulk moves an item's metadata and
+// matrices into shared memory.
 #pragma once
 #include <cstdint>
 
 namespace scn {
 
-struct Item {
-  int64_t off;    // offset (doubles) of the first node's block in its pass array
-  int32_t first;  // first node id
-  int32_t count;  // nodes in the item
-  int32_t bytes;  // bulk-copy size (multiple of 16)
-  int32_t pass;   // 0 backward, 1 forward
-};
-
+// Per-node record at the head of an item (offsets are relative to the
+// item's shared-memory slot / staged-vector areas).
 struct NodeMeta {
-  int32_t anc, cb, cc, M;   // ancestor, first child, child count, child dual rows
-  int32_t cdo, doff, m, tdo;  // child dual offset, own stage-row offset/rows, terminal offset
-  int32_t mN, leaf, pad0, pad1;
+  int32_t c;       // node id
+  int32_t blk;     // offset (doubles) of the node block inside the slot
+  int32_t M, m;    // child dual rows; own stage rows
+  int32_t mN;      // terminal rows (leaf)
+  int32_t doff;    // dual offset of the node's stage rows
+  int32_t tdo;     // dual offset of the terminal rows (leaf)
+  int32_t yoff;    // backward: offset of y_kids / y_N in the staged y range
+  int32_t kid0;    // backward: first child's row in the staged contributions
+  int32_t nkid;    // backward: number of children
+  int32_t par;     // forward: parent's row in the staged parent vectors
+  int32_t pad;
 };
+static_assert(sizeof(NodeMeta) % 16 == 0, "NodeMeta must keep 16-byte alignment");
+
+struct Item {
+  int64_t off;      // offset (doubles) of the item in its pass array
+  int32_t bytes;    // bulk-copy size (multiple of 16)
+  int32_t first;    // first node id
+  int32_t count;    // nodes
+  int32_t pass;     // 0 backward, 1 forward
+  int32_t leaf;     // all nodes are leaves
+  int32_t dep_lo;   // dependency flags [dep_lo, dep_hi): bw -> children (bw flags),
+  int32_t dep_hi;   //   fw -> parents (fw flags), fw root -> bw flag of node 0
+  int32_t v0_lo;    // staged range 0: bw y rows [v0_lo, v0_lo+v0_n) ; fw parent nodes
+  int32_t v0_n;
+  int32_t v1_lo;    // staged range 1: bw child contribution rows ; fw u_off of the item
+  int32_t v1_n;
+  int32_t pad[3];
+};
+static_assert(sizeof(Item) == 64, "Item is one 64-byte record");
 
 constexpr int kMaxRhs = 2;
-constexpr int kMaxSlots = 4;
+constexpr int kMaxSlots = 8;
 
 struct SweepParams {
   int nx, nu, n, first_leaf, dual_dim;
-  int items_bw, items_total;
-  int nslot, slot_doubles, vec_doubles;  // per-CTA smem carve-up
-  int nrhs, affine;
-  int max_count;  // max nodes per item
-  int max_mN;     // max terminal rows
+  int items_total;
+  int nslot, slot_doubles, stage_doubles, scratch_doubles;
+  int nrhs, affine, G, max_count;
+  int nxp, Vp;  // padded column lengths (== 2 mod 4) of J/K/TN and W
   const Item* items;
-  const NodeMeta* meta;
-  const int64_t* bw_off;  // [n] node block offsets (doubles)
-  const int64_t* fw_off;
   const double* bw_blk;
   const double* fw_blk;
   const double* aff_bw;  // [n][nu+nx]: [input_affine; costate_affine] / [0; pi p_N]
   const double* aff_fw;  // [n][nx]: c_c
   const double* root_state;
-  unsigned* ctrl;      // [0] epoch, [1] ticket, [2] done
-  unsigned* bw_flag;   // [n]
-  unsigned* fw_flag;   // [n]
+  unsigned* ctrl;     // [0] epoch, [1] done-CTA counter
+  unsigned* bw_flag;  // [n]
+  unsigned* fw_flag;  // [n]
   const double* y[kMaxRhs];
   double* x[kMaxRhs];
   double* u[kMaxRhs];

@@ -1,32 +1,38 @@
 // SPDX-License-Identifier: MIT
 //
 // K1+K2: the dual-gradient / Hessian-vector sweep (tree_oracles.hpp:33-90)
-// fused with apply_H (problem_data.hpp:144-162), as ONE persistent kernel.
+// fused with apply_H (problem_data.hpp:144-162) as ONE persistent,
+// warp-specialised kernel.
 //
-// Work decomposition. Items (runs of same-stage nodes, see layout.hpp) are
-// dispensed from a global ticket counter: first the backward items from the
-// leaves to the root, then the forward items from the root to the leaves.
-// Every dependency of an item therefore has a smaller ticket. A CTA processes
-// its tickets in the order it grabbed them, so the smallest unfinished ticket
-// always belongs to a running CTA whose dependencies are done: the scheme
-// cannot deadlock and needs no grid-wide barrier, even with CTAs that are not
-// co-resident. A node publishes completion through an epoch-stamped flag
-// (release/acquire at gpu scope); consumers spin only on their own
-// children (backward) or parent (forward).
+// Schedule. Items (runs of same-stage nodes, layout.hpp) are numbered in
+// ticket order: backward items leaves -> root, then forward items root ->
+// leaves, so every dependency of an item has a smaller ticket. The grid is
+// co-resident (cooperative launch) and CTA b owns tickets b, b+G, b+2G, ...
+// processed in order: the smallest unfinished ticket always belongs to a CTA
+// that is working on it with all its dependencies done, so the scheme cannot
+// deadlock and needs no grid-wide barrier. Completion of a node is published
+// through an epoch-stamped flag (st.release / ld.acquire at gpu scope).
 //
-// Data movement. Each CTA keeps a ring of `nslot` shared-memory slots. As
-// soon as it owns a ticket, one thread issues a single cp.async.bulk (TMA 1-D)
-// of the whole item (contiguous node blocks) into a free slot, completing on
-// an mbarrier; the matrices are therefore in flight while the CTA is still
-// waiting for the dependencies of earlier items. All matrix traffic is a
-// sequential HBM stream; the small vectors (y, contributions, x, u) live in
-// L2.
-//
-// Arithmetic. Every product is a set of "dot columns" (layout.hpp) computed
-// by groups of G lanes (strided partial sums + butterfly shuffles), for all
-// right-hand sides at once so a 2-RHS sweep (p-NAMA) reads the matrices once.
+// Every per-item step is latency-bound (measured on B200: L2 hit ~280
+// cycles, st.release ~760, dependent DFMA 8), so the kernel overlaps items
+// in every role instead of shortening one item:
+//   warps 0..3  producers (one per staging slot, items k = p mod 4): poll
+//               the item's dependency flags (ld.acquire) and stage its small
+//               vectors (y rows, child contributions, parent x/u, u_off,
+//               affine terms) with async 8-byte copies; four such round trips
+//               are in flight at once.
+//   warps 4..7  consumer team 0 (even items), warps 8..11 team 1 (odd
+//               items): wait for the item's matrices (TMA, slot FULL) and
+//               vectors (stage FULL), compute every product from shared
+//               memory, and recycle the slot with one cp.async.bulk (TMA 1-D)
+//               of item k+nslot.
+//   warp 12     publisher: releases completion flags in ticket order, one
+//               gpu-scope fence per batch of finished items.
+// Products are "dot columns" split over S in {1,2,4,8} threads (interleaved
+// 16-byte shared loads over padded columns + xor shuffles), for all
+// right-hand sides at once so a 2-RHS (p-NAMA) sweep reads each matrix once.
 // fp64 throughout; the partial-sum order is fixed, so results are
-// deterministic run to run and identical between 1- and 2-RHS launches.
+// deterministic and identical between 1- and 2-RHS launches.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -37,30 +43,51 @@ namespace scn {
 
 namespace {
 
+constexpr int kTeam = 128;  // threads per consumer team
+constexpr int kTeams = 2;
+constexpr int kProducers = 4;  // producer warps (== slots), warp p stages items k = p (mod 4)
+constexpr int kThreads = 32 * kProducers + kTeams * kTeam + 32;  // producers, teams, publisher
+constexpr int kTeamWarp0 = kProducers;
+constexpr int kPublisherWarp = kProducers + kTeams * kTeam / 32;
+
+#ifdef SCN_SWEEP_PROFILE
+// cycle counters: [0] prod stage-empty wait [1] prod stage round trip
+// [2] prod dep spin [3] team slot-full wait [4] team stage-full wait
+// [5] team compute [6] team refill + publish back-pressure [7] publisher fence
+__device__ unsigned long long g_prof[16];
+#define PROF_T0() long long _pt = clock64()
+#define PROF_T1(slot)                                                                          \
+  do {                                                                                         \
+    long long _n = clock64();                                                                  \
+    atomicAdd(&g_prof[slot], (unsigned long long)(_n - _pt));                                  \
+    _pt = _n;                                                                                  \
+  } while (0)
+#else
+#define PROF_T0() (void)0
+#define PROF_T1(slot) (void)0
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -74,7 +101,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -82,327 +121,460 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ void team_sync(int team) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(kTeam) : "memory");
+}
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
 
-__device__ __forceinline__ void wait_flag(const unsigned* flag, unsigned epoch) {
-  if (ld_acquire(flag) == epoch) return;
-  unsigned ns = 32;
-  while (ld_acquire(flag) != epoch) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
+__device__ __forceinline__ const unsigned* dep_flags(const SweepParams& P, const Item& it) {
+  return (it.pass == 0 || it.first == 0) ? P.bw_flag : P.fw_flag;
+}
+
+__device__ __forceinline__ bool flags_ready(const unsigned* flags, const Item& it, unsigned E, int lane) {
+  bool ok = true;
+  for (int k = it.dep_lo + lane; k < it.dep_hi; k += 32) ok &= (ld_acquire(flags + k) == E);
+  return __all_sync(0xffffffffu, ok);
+}
+
+// Staged-vector layout of one item for NRHS right-hand sides:
+//   bw: Y_r at r*v0n ; C_r at NRHS*v0n + r*v1n*W ; AFF at NRHS*(v0n+v1n*W)  (count*W)
+//   fw: PV_r[p] = [x_a; u_a; 0-pad] at (r*v0n + p)*Vp ; UO_r at NRHS*v0n*Vp + r*v1n*nu ;
+//       AFF at NRHS*(v0n*Vp + v1n*nu)  (count*nx)
+// Issued as asynchronous 8-byte copies (LDGSTS) program-ordered after the
+// acquire that observed this item's flags (ld.acquire.gpu also invalidates
+// L1), so they read the published values.
+template <int NRHS>
+__device__ void stage_issue(const SweepParams& P, const Item& it, double* st, int lane) {
+  const int nx = P.nx, nu = P.nu, W = nx + nu, Vp = P.Vp;
+  if (it.pass == 0) {
+    const int nc = it.v1_n * W;
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      const double* ys = P.y[r] + it.v0_lo;
+      double* yd = st + r * it.v0_n;
+      for (int i = lane; i < it.v0_n; i += 32) cp_async8(yd + i, ys + i);
+      const double* cs = P.contrib[r] + static_cast<int64_t>(it.v1_lo) * W;
+      double* cd = st + NRHS * it.v0_n + r * nc;
+      for (int i = lane; i < nc; i += 32) cp_async8(cd + i, cs + i);
+    }
+    if (P.affine) {
+      const int na = it.count * W;
+      const double* as = P.aff_bw + static_cast<int64_t>(it.first) * W;
+      double* ad = st + NRHS * (it.v0_n + nc);
+      for (int i = lane; i < na; i += 32) cp_async8(ad + i, as + i);
+    }
+  } else {
+    const int tot = it.v0_n * Vp, nuo = it.v1_n * nu;
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      for (int pp = 0; pp < it.v0_n; ++pp) {
+        double* pd = st + r * tot + pp * Vp;
+        const double* xs = P.x[r] + static_cast<int64_t>(it.v0_lo + pp) * nx;
+        const double* us = P.u[r] + static_cast<int64_t>(it.v0_lo + pp) * nu;
+        for (int e = lane; e < Vp; e += 32) {
+          if (e < nx)
+            cp_async8(pd + e, xs + e);
+          else if (e < W)
+            cp_async8(pd + e, us + (e - nx));
+          else
+            pd[e] = 0.0;
+        }
+      }
+      const double* os = P.u[r] + static_cast<int64_t>(it.v1_lo) * nu;
+      double* od = st + NRHS * tot + r * nuo;
+      for (int i = lane; i < nuo; i += 32) cp_async8(od + i, os + i);
+    }
+    if (P.affine) {
+      const int na = it.count * nx;
+      const double* as = P.aff_fw + static_cast<int64_t>(it.first) * nx;
+      double* ad = st + NRHS * (tot + nuo);
+      for (int i = lane; i < na; i += 32) cp_async8(ad + i, as + i);
+    }
   }
 }
 
-__device__ __forceinline__ void issue_item(const SweepParams& P, unsigned t, double* slot, uint64_t* bar) {
-  const Item it = P.items[t];
-  const double* src = (it.pass == 0 ? P.bw_blk : P.fw_blk) + it.off;
-  mbar_expect_tx(bar, static_cast<unsigned>(it.bytes));
-  tma_load_1d(slot, src, static_cast<unsigned>(it.bytes), bar);
+// out[r] = <col, vec_r> over a padded length (even; 16-byte aligned operands)
+// by S consecutive threads (q = 0..S-1) taking interleaved 16-byte chunks,
+// two accumulators each, then an xor-shuffle reduction. All threads of a
+// warp call it (inactive ones with lenp = 0).
+template <int NRHS, int S>
+__device__ __forceinline__ void dot_split(const double* __restrict__ col, const double* __restrict__ v0,
+                                          int vstride, int lenp, int q, double (&out)[NRHS]) {
+  double a[NRHS], bq[NRHS];
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r) a[r] = bq[r] = 0.0;
+#pragma unroll 4
+  for (int k = 2 * q; k < lenp; k += 2 * S) {
+    const double2 m = *reinterpret_cast<const double2*>(col + k);
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      const double2 v = *reinterpret_cast<const double2*>(v0 + r * vstride + k);
+      a[r] = fma(m.x, v.x, a[r]);
+      bq[r] = fma(m.y, v.y, bq[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NRHS; ++r) {
+    double t = a[r] + bq[r];
+#pragma unroll
+    for (int o = S >> 1; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    out[r] = t;
+  }
 }
 
-template <int NRHS>
-__device__ __forceinline__ void group_reduce(double (&acc)[NRHS], int G) {
-#pragma unroll
-  for (int r = 0; r < NRHS; ++r)
-    for (int o = G >> 1; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+// Runs body.run<S>(task, q, active) over ntasks dot tasks on one team, S
+// threads per task, S chosen so one round covers the tasks when possible.
+template <class Body>
+__device__ __forceinline__ void for_tasks(int ntasks, int ttid, const Body& body) {
+  if (ntasks * 8 <= kTeam) {
+    const int g = ttid >> 3, q = ttid & 7;
+    body.template run<8>(g, q, g < ntasks);
+  } else if (ntasks * 4 <= kTeam) {
+    const int g = ttid >> 2, q = ttid & 3;
+    body.template run<4>(g, q, g < ntasks);
+  } else if (ntasks * 2 <= kTeam) {
+    const int g = ttid >> 1, q = ttid & 1;
+    body.template run<2>(g, q, g < ntasks);
+  } else {
+    for (int base = 0; base < ntasks; base += kTeam) body.template run<1>(base + ttid, 0, base + ttid < ntasks);
+  }
 }
 
 // ---------------------------------------------------------------- backward
-// tree_oracles.hpp:44-73. For interior node c:
-//   [u_off_c; w_c] = E_c' y_kids + sum_{k in kids} contrib_k (+ [sigma_c; c_hat_c])
-// for a leaf: w_c = F_N' y_N (+ pi p_N); then for non-root c:
-//   contrib_c = J_c' w_c = [child_to_input_c w_c ; closed_loop_c' w_c]
+// tree_oracles.hpp:54-73, phase B: contrib_c = J_c' w_c
+//   = [child_to_input_c w_c ; closed_loop_c' w_c] (non-root c).
 template <int NRHS>
-__device__ void backward_item(const SweepParams& P, const Item& it, const double* blk, double* vec,
-                              unsigned E, int G) {
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int nx = P.nx, nu = P.nu, W = nu + nx;
-  const int first = it.first, cnt = it.count;
-  const NodeMeta m0 = P.meta[first];
-  const bool leaf = m0.leaf != 0;
-  if (!leaf) {
-    const NodeMeta ml = P.meta[first + cnt - 1];
-    for (int k = m0.cb + tid; k < ml.cb + ml.cc; k += nthr) wait_flag(P.bw_flag + k, E);
+struct BwPhaseB {
+  const SweepParams& P;
+  const NodeMeta* meta;
+  const double* slot;
+  const double* wbuf;
+  int nx, W, nxp, leaf, single;
+  template <int S>
+  __device__ __forceinline__ void run(int task, int q, bool active) const {
+    int ni = 0, j = 0;
+    const double* col = slot;
+    if (active) {
+      ni = single ? 0 : task / W;
+      j = task - ni * W;
+      const NodeMeta& mc = meta[ni];
+      const int e = leaf ? mc.mN * nx : mc.M * W;
+      col = slot + mc.blk + ((e + 1) & ~1) + j * nxp;
+    }
+    double acc[NRHS];
+    dot_split<NRHS, S>(col, wbuf + ni * NRHS * nxp, nxp, active ? nxp : 0, q, acc);
+    if (active && q == 0) {
+      const int64_t c = meta[ni].c;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) P.contrib[r][c * W + j] = acc[r];
+    }
   }
-  __syncthreads();
+};
 
-  const int ngroups = nthr / G, g = tid / G, lane = tid % G;
-  // phase A
-  {
+// tree_oracles.hpp:44-73. Interior c: [u_off_c; w_c] = E_c' y_kids +
+// sum_kids contrib_k (+[sigma_c; c_hat_c]); leaf: w_c = F_N' y_N (+pi p_N);
+// then phase B for non-root c.
+template <int NRHS>
+__device__ void consume_backward(const SweepParams& P, const Item& it, const double* slot,
+                                 const double* st, double* wbuf, int ttid, int team) {
+  const int nx = P.nx, nu = P.nu, W = nx + nu, nxp = P.nxp;
+  const int cnt = it.count;
+  const bool leaf = it.leaf != 0;
+  const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
+  const double* Y = st;
+  const double* Cn = st + NRHS * it.v0_n;
+  const double* AF = st + NRHS * (it.v0_n + it.v1_n * W);
+  {  // phase A: short dot columns (len M or mN), child sums, affine terms
     const int ncols = leaf ? nx : W;
     const int ntasks = cnt * ncols;
-    for (int base = 0; base < ntasks; base += ngroups) {
-      const int task = base + g;
-      const bool active = task < ntasks;
+    for (int task = ttid; task < ntasks; task += kTeam) {
+      const int ni = cnt == 1 ? 0 : task / ncols;
+      const int j = task - ni * ncols;
+      const NodeMeta& mc = meta[ni];
+      const int len = leaf ? mc.mN : mc.M;
+      const double* col = slot + mc.blk + j * len;
+      const double* yv = Y + mc.yoff;
       double acc[NRHS];
 #pragma unroll
       for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
-      int ni = 0, j = 0, c = 0;
-      if (active) {
-        ni = task / ncols;
-        j = task - ni * ncols;
-        c = first + ni;
-        const NodeMeta mc = P.meta[c];
-        const double* nb = blk + (P.bw_off[c] - it.off);
-        if (!leaf) {
-          const double* col = nb + static_cast<int64_t>(j) * mc.M;
-          for (int k = lane; k < mc.M; k += G) {
-            const double a = col[k];
+      for (int k = 0; k < len; ++k) {
+        const double a = col[k];
 #pragma unroll
-            for (int r = 0; r < NRHS; ++r) acc[r] += a * __ldg(P.y[r] + mc.cdo + k);
-          }
-          for (int k = lane; k < mc.cc; k += G) {
-            const int64_t kid = mc.cb + k;
-#pragma unroll
-            for (int r = 0; r < NRHS; ++r) acc[r] += __ldcg(P.contrib[r] + kid * W + j);
-          }
-        } else {
-          const double* col = nb + static_cast<int64_t>(j) * mc.mN;
-          for (int k = lane; k < mc.mN; k += G) {
-            const double a = col[k];
-#pragma unroll
-            for (int r = 0; r < NRHS; ++r) acc[r] += a * __ldg(P.y[r] + mc.tdo + k);
-          }
-        }
+        for (int r = 0; r < NRHS; ++r) acc[r] = fma(a, yv[r * it.v0_n + k], acc[r]);
       }
-      group_reduce<NRHS>(acc, G);
-      if (active && lane == 0) {
-        const int ja = leaf ? nu + j : j;
-        const double aff = P.affine ? P.aff_bw[static_cast<int64_t>(c) * W + ja] : 0.0;
+      if (!leaf)
+        for (int k = 0; k < mc.nkid; ++k) {
 #pragma unroll
-        for (int r = 0; r < NRHS; ++r) {
-          const double v = acc[r] + aff;
-          if (ja < nu)
-            P.u[r][static_cast<int64_t>(c) * nu + ja] = v;  // u_off, finished by the forward pass
-          else
-            vec[(ni * NRHS + r) * nx + (ja - nu)] = v;  // costate w_c
+          for (int r = 0; r < NRHS; ++r) acc[r] += Cn[r * it.v1_n * W + (mc.kid0 + k) * W + j];
         }
+      const int ja = leaf ? nu + j : j;
+      const double aff = P.affine ? AF[ni * W + ja] : 0.0;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        const double v = acc[r] + aff;
+        if (ja < nu)
+          P.u[r][static_cast<int64_t>(mc.c) * nu + ja] = v;  // u_off, completed by the forward pass
+        else
+          wbuf[(ni * NRHS + r) * nxp + (ja - nu)] = v;  // costate w_c
       }
     }
   }
-  __syncthreads();
-  // phase B: contributions to the parent
-  if (first != 0) {
-    const int ntasks = cnt * W;
-    for (int base = 0; base < ntasks; base += ngroups) {
-      const int task = base + g;
-      const bool active = task < ntasks;
-      double acc[NRHS];
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
-      int ni = 0, j = 0, c = 0;
-      if (active) {
-        ni = task / W;
-        j = task - ni * W;
-        c = first + ni;
-        const NodeMeta mc = P.meta[c];
-        const double* nb = blk + (P.bw_off[c] - it.off);
-        const double* col = nb + (leaf ? mc.mN * nx : mc.M * W) + static_cast<int64_t>(j) * nx;
-        for (int k = lane; k < nx; k += G) {
-          const double a = col[k];
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) acc[r] += a * vec[(ni * NRHS + r) * nx + k];
-        }
-      }
-      group_reduce<NRHS>(acc, G);
-      if (active && lane == 0) {
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) P.contrib[r][static_cast<int64_t>(c) * W + j] = acc[r];
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < cnt; i += nthr) {
-    __threadfence();
-    st_release(P.bw_flag + first + i, E);
+  team_sync(team);
+  if (it.first != 0) {
+    const BwPhaseB<NRHS> body{P, meta, slot, wbuf, nx, W, nxp, leaf ? 1 : 0, cnt == 1 ? 1 : 0};
+    for_tasks(cnt * W, ttid, body);
   }
 }
 
 // ---------------------------------------------------------------- forward
-// tree_oracles.hpp:75-88 + apply_H. For non-root c with parent a:
-//   [x_c; z_c] = W_c' [x_a; u_a] (+ [c_c; 0]);  then
-//   interior: u_c = u_off_c + K_c x_c ;  leaf: z_N,c = F_N x_c
+// tree_oracles.hpp:75-88 + apply_H, phase A: [x_c; z_c] = W_c' [x_a; u_a]
+// (+[c_c; 0]) for non-root c.
 template <int NRHS>
-__device__ void forward_item(const SweepParams& P, const Item& it, const double* blk, double* vec,
-                             unsigned E, int G, int mmax) {
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int nx = P.nx, nu = P.nu, V = nx + nu;
-  const int first = it.first, cnt = it.count;
-  const NodeMeta m0 = P.meta[first];
-  const bool leaf = m0.leaf != 0;
-  const bool root = first == 0;
-  double* vin = vec;                         // [cnt][NRHS][nx+nu]
-  double* xb = vec + P.max_count * NRHS * V;  // [cnt][NRHS][nx]
-  if (root) {
-    if (tid == 0) wait_flag(P.bw_flag, E);
-  } else {
-    const int a0 = m0.anc, a1 = P.meta[first + cnt - 1].anc;
-    for (int k = a0 + tid; k <= a1; k += nthr) wait_flag(P.fw_flag + k, E);
+struct FwPhaseA {
+  const SweepParams& P;
+  const NodeMeta* meta;
+  const double* slot;
+  const double* PV;
+  const double* AF;
+  double* xbuf;
+  int nx, Vp, nxp, ncols, tot, single;
+  template <int S>
+  __device__ __forceinline__ void run(int task, int q, bool active) const {
+    int ni = 0, j = 0;
+    const double* col = slot;
+    const double* v = PV;
+    if (active) {
+      ni = single ? 0 : task / ncols;
+      j = task - ni * ncols;
+      const NodeMeta& mc = meta[ni];
+      active = j < nx + mc.m;
+      col = slot + mc.blk + j * Vp;
+      v = PV + mc.par * Vp;
+    }
+    double acc[NRHS];
+    dot_split<NRHS, S>(col, v, tot, active ? Vp : 0, q, acc);
+    if (active && q == 0) {
+      const NodeMeta& mc = meta[ni];
+      const int64_t c = mc.c;
+      if (j < nx) {
+        const double aff = P.affine ? AF[ni * nx + j] : 0.0;
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) {
+          const double xv = acc[r] + aff;
+          xbuf[(ni * NRHS + r) * nxp + j] = xv;
+          P.x[r][c * nx + j] = xv;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) P.Hx[r][mc.doff + (j - nx)] = acc[r];
+      }
+    }
   }
-  __syncthreads();
-  if (root) {
-    for (int idx = tid; idx < NRHS * nx; idx += nthr) {
+};
+
+// phase B: interior u_c = u_off_c + K_c x_c ; leaf z_N,c = F_N x_c.
+template <int NRHS>
+struct FwPhaseB {
+  const SweepParams& P;
+  const NodeMeta* meta;
+  const double* slot;
+  const double* UO;
+  const double* xbuf;
+  int nx, nu, Vp, nxp, ncols, v1nu, leaf, root, single;
+  template <int S>
+  __device__ __forceinline__ void run(int task, int q, bool active) const {
+    int ni = 0, j = 0;
+    const double* col = slot;
+    if (active) {
+      ni = single ? 0 : task / ncols;
+      j = task - ni * ncols;
+      const NodeMeta& mc = meta[ni];
+      if (leaf) active = j < mc.mN;
+      const int skip = root ? 0 : Vp * (nx + mc.m);
+      col = slot + mc.blk + skip + j * nxp;
+    }
+    double acc[NRHS];
+    dot_split<NRHS, S>(col, xbuf + ni * NRHS * nxp, nxp, active ? nxp : 0, q, acc);
+    if (active && q == 0) {
+      const NodeMeta& mc = meta[ni];
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        if (leaf)
+          P.Hx[r][mc.tdo + j] = acc[r];
+        else
+          P.u[r][static_cast<int64_t>(mc.c) * nu + j] = UO[r * v1nu + ni * nu + j] + acc[r];
+      }
+    }
+  }
+};
+
+template <int NRHS>
+__device__ void consume_forward(const SweepParams& P, const Item& it, const double* slot,
+                                const double* st, double* xbuf, int ttid, int team, int mmax,
+                                int mNmax) {
+  const int nx = P.nx, nu = P.nu, Vp = P.Vp, nxp = P.nxp;
+  const int cnt = it.count;
+  const bool leaf = it.leaf != 0;
+  const bool root = it.first == 0;
+  const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
+  const int tot = it.v0_n * Vp;
+  const double* PV = st;
+  const double* UO = st + NRHS * tot;
+  const double* AF = st + NRHS * (tot + it.v1_n * nu);
+  if (root) {  // x_0 = p (affine) or 0
+    for (int idx = ttid; idx < NRHS * nx; idx += kTeam) {
       const int r = idx / nx, k = idx - r * nx;
       const double v = P.affine ? P.root_state[k] : 0.0;
-      xb[r * nx + k] = v;
+      xbuf[r * nxp + k] = v;
       P.x[r][k] = v;
     }
   } else {
-    const int tot = cnt * NRHS * V;
-    for (int idx = tid; idx < tot; idx += nthr) {
-      const int ni = idx / (NRHS * V);
-      const int rem = idx - ni * NRHS * V;
-      const int r = rem / V, k = rem - r * V;
-      const int64_t a = P.meta[first + ni].anc;
-      vin[idx] = k < nx ? __ldcg(P.x[r] + a * nx + k) : __ldcg(P.u[r] + a * nu + (k - nx));
-    }
+    const FwPhaseA<NRHS> body{P, meta, slot, PV, AF, xbuf, nx, Vp, nxp, nx + mmax, tot, cnt == 1 ? 1 : 0};
+    for_tasks(cnt * (nx + mmax), ttid, body);
   }
-  __syncthreads();
-  const int ngroups = nthr / G, g = tid / G, lane = tid % G;
-  if (!root) {  // phase A: state + stage rows
-    const int ncols = nx + mmax;
-    const int ntasks = cnt * ncols;
-    for (int base = 0; base < ntasks; base += ngroups) {
-      const int task = base + g;
-      int ni = task / ncols;
-      int j = task - ni * ncols;
-      const int c = first + ni;
-      bool active = task < ntasks;
-      NodeMeta mc{};
-      if (active) {
-        mc = P.meta[c];
-        active = j < nx + mc.m;
-      }
-      double acc[NRHS];
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
-      if (active) {
-        const double* col = blk + (P.fw_off[c] - it.off) + static_cast<int64_t>(j) * V;
-        const double* v = vin + ni * NRHS * V;
-        for (int k = lane; k < V; k += G) {
-          const double a = col[k];
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) acc[r] += a * v[r * V + k];
-        }
-      }
-      group_reduce<NRHS>(acc, G);
-      if (active && lane == 0) {
-        if (j < nx) {
-          const double aff = P.affine ? P.aff_fw[static_cast<int64_t>(c) * nx + j] : 0.0;
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) {
-            const double xv = acc[r] + aff;
-            xb[(ni * NRHS + r) * nx + j] = xv;
-            P.x[r][static_cast<int64_t>(c) * nx + j] = xv;
-          }
-        } else {
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) P.Hx[r][mc.doff + (j - nx)] = acc[r];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  {  // phase B: input (interior) or terminal rows (leaf)
-    const int ncols = leaf ? P.max_mN : nu;
-    const int ntasks = cnt * ncols;
-    for (int base = 0; base < ntasks; base += ngroups) {
-      const int task = base + g;
-      const int ni = task / ncols;
-      const int j = task - ni * ncols;
-      const int c = first + ni;
-      bool active = task < ntasks;
-      NodeMeta mc{};
-      if (active) {
-        mc = P.meta[c];
-        if (leaf) active = j < mc.mN;
-      }
-      double acc[NRHS];
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
-      if (active) {
-        const int64_t skip = root ? 0 : static_cast<int64_t>(V) * (nx + mc.m);
-        const double* col = blk + (P.fw_off[c] - it.off) + skip + static_cast<int64_t>(j) * nx;
-        const double* xv = xb + ni * NRHS * nx;
-        for (int k = lane; k < nx; k += G) {
-          const double a = col[k];
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) acc[r] += a * xv[r * nx + k];
-        }
-      }
-      group_reduce<NRHS>(acc, G);
-      if (active && lane == 0) {
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) {
-          if (leaf) {
-            P.Hx[r][mc.tdo + j] = acc[r];
-          } else {
-            const int64_t o = static_cast<int64_t>(c) * nu + j;
-            P.u[r][o] = __ldcg(P.u[r] + o) + acc[r];
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < cnt; i += nthr) {
-    __threadfence();
-    st_release(P.fw_flag + first + i, E);
-  }
+  team_sync(team);
+  const FwPhaseB<NRHS> body{P, meta, slot, UO, xbuf, nx, nu, Vp, nxp, leaf ? mNmax : nu, it.v1_n * nu,
+                            leaf ? 1 : 0, root ? 1 : 0, cnt == 1 ? 1 : 0};
+  for_tasks(cnt * (leaf ? mNmax : nu), ttid, body);
 }
 
 template <int NRHS>
-__global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepParams P, int G, int mmax) {
+__global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P, int mmax, int mNmax) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t mbar[kMaxSlots];
-  __shared__ unsigned tick[kMaxSlots];
+  __shared__ __align__(8) uint64_t full[kMaxSlots], sfull[kMaxSlots], sempty[kMaxSlots], done[kMaxSlots],
+      pdone[kMaxSlots];
+  __shared__ __align__(16) Item sitem[kMaxSlots];
   __shared__ unsigned s_epoch;
-  const int tid = threadIdx.x;
-  const unsigned total = static_cast<unsigned>(P.items_total);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NS = P.nslot;  // matrix slots == staging slots (even, so a slot stays with one team)
   double* slots = smem;
-  double* vec = smem + static_cast<int64_t>(P.nslot) * P.slot_doubles;
+  double* stages = smem + static_cast<int64_t>(NS) * P.slot_doubles;
+  double* scratch = stages + static_cast<int64_t>(NS) * P.stage_doubles;  // per team
+  const int b = blockIdx.x, Gd = gridDim.x;
+  const int K = P.items_total > b ? (P.items_total - b + Gd - 1) / Gd : 0;
+
+  auto issue = [&](int k, const Item& it) {  // one thread
+    const int s = k % NS;
+    sitem[s] = it;
+    mbar_arrive_expect_tx(&full[s], static_cast<unsigned>(it.bytes));
+    tma_load_1d(slots + static_cast<int64_t>(s) * P.slot_doubles, (it.pass == 0 ? P.bw_blk : P.fw_blk) + it.off,
+                static_cast<unsigned>(it.bytes), &full[s]);
+  };
+
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile unsigned*>(P.ctrl) + 1u;
-    for (int s = 0; s < P.nslot; ++s) mbar_init(&mbar[s], 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 1);
+      mbar_init(&done[s], 1);
+      mbar_init(&pdone[s], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < P.nslot; ++s) {
-      const unsigned t = atomicAdd(P.ctrl + 1, 1u);
-      tick[s] = t;
-      if (t < total) issue_item(P, t, slots + static_cast<int64_t>(s) * P.slot_doubles, &mbar[s]);
+  }
+  for (int i = tid; i < kTeams * P.scratch_doubles; i += kThreads) scratch[i] = 0.0;  // zero pads of w / x
+  __syncthreads();
+  const unsigned E = s_epoch;
+  if (tid == 0)
+    for (int k = 0; k < NS && k < K; ++k) issue(k, P.items[b + static_cast<int64_t>(k) * Gd]);
+
+  if (warp < kProducers) {
+    // ------------------------------------------------------------ producers
+    // Producer warp p owns staging slot p (NS == kProducers): items k = p mod
+    // NS. For each it waits for the slot to be consumed, polls the item's
+    // dependency flags (ld.acquire), stages its vectors and arrives FULL.
+    // Four producers keep four of these latency-bound round trips in flight.
+    const int p = warp;
+    for (int k = p; k < K; k += NS) {
+      const Item it = P.items[b + static_cast<int64_t>(k) * Gd];
+      PROF_T0();
+      if (k >= NS) mbar_wait(&sempty[p], static_cast<unsigned>((k / NS - 1) & 1));
+      if (lane == 0 && p == 0) PROF_T1(0);
+      while (!flags_ready(dep_flags(P, it), it, E, lane)) __nanosleep(32);
+      if (lane == 0 && p == 0) PROF_T1(2);
+      stage_issue<NRHS>(P, it, stages + static_cast<int64_t>(p) * P.stage_doubles, lane);
+      cp_async_wait_all();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull[p]);
+      if (lane == 0 && p == 0) PROF_T1(1);
+    }
+  } else if (warp < kPublisherWarp) {
+    // ------------------------------------------------------------ consumer teams
+    const int team = (warp - kTeamWarp0) / (kTeam / 32);
+    const int ttid = tid - 32 * kTeamWarp0 - team * kTeam;
+    double* tbuf = scratch + team * P.scratch_doubles;
+    for (int k = team; k < K; k += kTeams) {
+      const int s = k % NS;
+      const bool refill = k + NS < K;
+      Item nxt{};
+      if (ttid == 0 && refill) nxt = P.items[b + static_cast<int64_t>(k + NS) * Gd];
+      PROF_T0();
+      mbar_wait(&full[s], static_cast<unsigned>((k / NS) & 1));
+      if (ttid == 0) PROF_T1(3);
+      mbar_wait(&sfull[s], static_cast<unsigned>((k / NS) & 1));
+      if (ttid == 0) PROF_T1(4);
+      const Item it = sitem[s];
+      const double* slot = slots + static_cast<int64_t>(s) * P.slot_doubles;
+      const double* st = stages + static_cast<int64_t>(s) * P.stage_doubles;
+      if (it.pass == 0)
+        consume_backward<NRHS>(P, it, slot, st, tbuf, ttid, team);
+      else
+        consume_forward<NRHS>(P, it, slot, st, tbuf, ttid, team, mmax, mNmax);
+      team_sync(team);
+      if (ttid == 0) PROF_T1(5);
+      if (ttid == 0) {
+        mbar_arrive(&sempty[s]);
+        fence_proxy_async();  // generic reads of the slot before the async-proxy refill
+        if (refill) issue(k + NS, nxt);
+        // the publisher must have retired item k-NS before its DONE phase reuses
+        if (k >= NS) mbar_wait(&pdone[s], static_cast<unsigned>((k / NS - 1) & 1));
+        mbar_arrive(&done[s]);
+      }
+      if (ttid == 0) PROF_T1(6);
+    }
+  }
+  if (warp == kPublisherWarp) {
+    // ------------------------------------------------------------ publisher
+    // Releases completion flags in ticket order; one gpu-scope fence covers
+    // every item finished since the previous one (the fence is the expensive
+    // part; it is cumulative over the teams' writes observed through DONE).
+    int k = 0;
+    while (k < K) {
+      mbar_wait(&done[k % NS], static_cast<unsigned>((k / NS) & 1));
+      int j = k + 1;
+      if (lane == 0)
+        while (j < K && j - k < NS && mbar_test(&done[j % NS], static_cast<unsigned>((j / NS) & 1))) ++j;
+      j = __shfl_sync(0xffffffffu, j, 0);
+      PROF_T0();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      for (int q2 = k; q2 < j; ++q2) {
+        const Item it = P.items[b + static_cast<int64_t>(q2) * Gd];
+        unsigned* flags = it.pass == 0 ? P.bw_flag : P.fw_flag;
+        for (int i = lane; i < it.count; i += 32)
+          asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + it.first + i), "r"(E) : "memory");
+      }
+      __syncwarp();
+      if (lane == 0) {
+        PROF_T1(7);
+        for (int q2 = k; q2 < j; ++q2) mbar_arrive(&pdone[q2 % NS]);
+      }
+      k = j;
     }
   }
   __syncthreads();
-  const unsigned E = s_epoch;
-  unsigned phase_bits = 0;
-  for (int k = 0;; ++k) {
-    const int s = k % P.nslot;
-    const unsigned t = tick[s];
-    if (t >= total) break;
-    mbar_wait(&mbar[s], (phase_bits >> s) & 1u);
-    phase_bits ^= 1u << s;
-    const Item it = P.items[t];
-    const double* blk = slots + static_cast<int64_t>(s) * P.slot_doubles;
-    if (it.pass == 0)
-      backward_item<NRHS>(P, it, blk, vec, E, G);
-    else
-      forward_item<NRHS>(P, it, blk, vec, E, G, mmax);
-    if (tid == 0) {
-      fence_proxy_async();
-      const unsigned t2 = atomicAdd(P.ctrl + 1, 1u);
-      tick[s] = t2;
-      if (t2 < total) issue_item(P, t2, slots + static_cast<int64_t>(s) * P.slot_doubles, &mbar[s]);
-    }
-    __syncthreads();
-  }
   if (tid == 0) {
     __threadfence();
-    const unsigned prev = atomicAdd(P.ctrl + 2, 1u);
+    const unsigned prev = atomicAdd(P.ctrl + 1, 1u);
     if (prev == gridDim.x - 1) {
       P.ctrl[1] = 0u;
-      P.ctrl[2] = 0u;
       __threadfence();
       atomicExch(P.ctrl, E);
     }
@@ -411,31 +583,48 @@ __global__ void __launch_bounds__(256, 1) sweep_kernel(const SweepParams P, int 
 
 }  // namespace
 
-cudaError_t sweep_configure(int nrhs, size_t dyn_smem) {
+int sweep_threads() { return kThreads; }
+int sweep_teams() { return kTeams; }
+
+cudaError_t sweep_profile_read(unsigned long long* out, bool reset) {
+#ifdef SCN_SWEEP_PROFILE
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 16);
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[16] = {0};
+    e = cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+  }
+  return e;
+#else
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+  (void)reset;
+  return cudaSuccess;
+#endif
+}
+
+cudaError_t sweep_configure(size_t dyn_smem) {
   cudaError_t e = cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(dyn_smem));
   if (e != cudaSuccess) return e;
-  (void)nrhs;
   return cudaFuncSetAttribute(sweep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(dyn_smem));
 }
 
 cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem) {
   int a = 0, b = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, sweep_kernel<1>, 256, dyn_smem);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, sweep_kernel<1>, kThreads, dyn_smem);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sweep_kernel<2>, 256, dyn_smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sweep_kernel<2>, kThreads, dyn_smem);
   *ctas_per_sm = a < b ? a : b;
   return e;
 }
 
-cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int G, int mmax,
+cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax,
                          cudaStream_t stream) {
-  if (P.nrhs == 2)
-    sweep_kernel<2><<<grid, 256, dyn_smem, stream>>>(P, G, mmax);
-  else
-    sweep_kernel<1><<<grid, 256, dyn_smem, stream>>>(P, G, mmax);
-  return cudaGetLastError();
+  SweepParams p = P;
+  void* args[] = {&p, &mmax, &mNmax};
+  const void* fn = P.nrhs == 2 ? reinterpret_cast<const void*>(sweep_kernel<2>)
+                               : reinterpret_cast<const void*>(sweep_kernel<1>);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, dyn_smem, stream);
 }
 
 }  // namespace scn

@@ -162,6 +162,10 @@ int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
   });
 }
 
+int scenopt_dev_stream(scenopt_dev* h, void** stream) {
+  SCN_GUARD(*stream = static_cast<void*>(h->d->stream));
+}
+
 int scenopt_dev_synchronize(scenopt_dev* h) {
   SCN_GUARD({
     SCN_CUDA(cudaSetDevice(h->d->device));
@@ -216,6 +220,12 @@ int scenopt_hessian_vec(scenopt_dev* h, const double* r, double* x, double* u, i
     ++h->stats.hessian_vec_calls;
     h->sweep(1, false, &r, &x, &u, nullptr, flags, true);
   });
+}
+
+/* Development hook: per-role cycle counters of a -DSCN_SWEEP_PROFILE build
+ * (all zero in the production library). */
+int scenopt_debug_sweep_profile(unsigned long long* out16, int reset) {
+  SCN_GUARD(SCN_CUDA(sweep_profile_read(out16, reset != 0)));
 }
 
 }  // extern "C"

@@ -52,41 +52,6 @@ T* upload(DevState& d, const std::vector<T>& h) {
   return p;
 }
 
-// Runs of consecutive same-stage nodes whose blocks total <= target bytes
-// (a node larger than the target forms its own item).
-void build_items(const Problem& p, const std::vector<int64_t>& off, const std::vector<int64_t>& size,
-                 int pass, int max_count, int64_t target_doubles, std::vector<Item>& out,
-                 int& max_cnt_seen, int64_t& max_item_doubles) {
-  auto stage_items = [&](int t) {
-    const int first = p.stage_offsets[t], past = p.stage_offsets[t + 1];
-    int i = first;
-    while (i < past) {
-      int cnt = 0;
-      int64_t tot = 0;
-      while (i + cnt < past && cnt < max_count) {
-        const int64_t s = size[i + cnt];
-        if (cnt > 0 && tot + s > target_doubles) break;
-        tot += s;
-        ++cnt;
-      }
-      Item it{};
-      it.off = off[i];
-      it.first = i;
-      it.count = cnt;
-      it.bytes = static_cast<int32_t>(tot * 8);
-      it.pass = pass;
-      out.push_back(it);
-      max_cnt_seen = std::max(max_cnt_seen, cnt);
-      max_item_doubles = std::max(max_item_doubles, tot);
-      i += cnt;
-    }
-  };
-  if (pass == 0)
-    for (int t = p.N; t >= 0; --t) stage_items(t);
-  else
-    for (int t = 0; t <= p.N; ++t) stage_items(t);
-}
-
 }  // namespace
 
 std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int device) {
@@ -131,159 +96,258 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int devi
   L.probability = p.probability;
   L.root_state = p.root_state;
 
-  // ---- per-node metadata and block sizes
-  std::vector<NodeMeta> meta(static_cast<size_t>(n));
+  // ---- per-node block sizes (doubles, even => 16-byte aligned); padded
+  // column lengths pad(l) == 2 (mod 4) for conflict-free 16-byte smem loads
+  auto pad2 = [](int l) { return l + ((2 - l % 4) + 4) % 4; };
+  const int nxp = pad2(nx), Vp = pad2(nx + nu);
+  d->nxp = nxp;
+  d->Vp = Vp;
   std::vector<int64_t> bws(static_cast<size_t>(n)), fws(static_cast<size_t>(n));
+  std::vector<int32_t> M(static_cast<size_t>(n), 0), cdo(static_cast<size_t>(n), 0);
   for (int c = 0; c < n; ++c) {
-    NodeMeta& m = meta[c];
     const bool leaf = c >= p.first_leaf;
-    m.anc = p.ancestor[c];
-    m.cb = p.child_begin[c];
-    m.cc = p.child_count[c];
-    m.M = leaf ? 0 : f.child_dual_rows[c];
-    m.cdo = leaf ? 0 : f.child_dual_offset[c];
-    m.doff = c == 0 ? 0 : p.dual_offset[c];
-    m.m = c == 0 ? 0 : p.stage_rows[c];
-    m.tdo = leaf ? p.tdual_offset[c - p.first_leaf] : 0;
-    m.mN = leaf ? p.terminal_rows[c - p.first_leaf] : 0;
-    m.leaf = leaf ? 1 : 0;
-    d->max_m = std::max(d->max_m, m.m);
-    d->max_mN = std::max(d->max_mN, m.mN);
-    int64_t b = leaf ? static_cast<int64_t>(m.mN) * nx : static_cast<int64_t>(m.M) * W;
-    if (c != 0) b += static_cast<int64_t>(nx) * W;
-    bws[c] = even(b);
+    const int m = c == 0 ? 0 : p.stage_rows[c];
+    const int mN = leaf ? p.terminal_rows[c - p.first_leaf] : 0;
+    if (!leaf) {
+      M[c] = f.child_dual_rows[c];
+      cdo[c] = f.child_dual_offset[c];
+    }
+    d->max_m = std::max(d->max_m, m);
+    d->max_mN = std::max(d->max_mN, mN);
+    int64_t b = even(leaf ? static_cast<int64_t>(mN) * nx : static_cast<int64_t>(M[c]) * W);
+    if (c != 0) b += static_cast<int64_t>(nxp) * W;
+    bws[c] = b;
     int64_t fw = 0;
-    if (c != 0) fw += static_cast<int64_t>(V) * (nx + m.m);
-    fw += leaf ? static_cast<int64_t>(nx) * m.mN : static_cast<int64_t>(nx) * nu;
+    if (c != 0) fw += static_cast<int64_t>(Vp) * (nx + m);
+    fw += leaf ? static_cast<int64_t>(nxp) * mN : static_cast<int64_t>(nxp) * nu;
     fws[c] = even(fw);
   }
-  std::vector<int64_t> bwo(static_cast<size_t>(n) + 1, 0), fwo(static_cast<size_t>(n) + 1, 0);
-  for (int c = 0; c < n; ++c) {
-    bwo[c + 1] = bwo[c] + bws[c];
-    fwo[c + 1] = fwo[c] + fws[c];
-  }
-  d->bw_doubles = bwo[n];
-  d->fw_doubles = fwo[n];
 
-  // ---- blocks
-  std::vector<double> bw(static_cast<size_t>(bwo[n]), 0.0), fw(static_cast<size_t>(fwo[n]), 0.0);
+  // ---- items: runs of same-stage nodes, tickets = backward (leaves->root)
+  // then forward (root->leaves)
+  const int64_t target = env_int("SCENOPT_ITEM_KB", 24) * 1024 / 8;
+  const int cap = std::max(1, env_int("SCENOPT_ITEM_MAX_NODES", 32));
+  struct Run { int first, count, pass; };
+  std::vector<Run> runs;
+  auto group_stage = [&](int t, int pass, const std::vector<int64_t>& size) {
+    const int first = p.stage_offsets[t], past = p.stage_offsets[t + 1];
+    int i = first;
+    while (i < past) {
+      int cnt = 0;
+      int64_t tot = 0;
+      while (i + cnt < past && cnt < cap) {
+        const int64_t sz = size[i + cnt] + static_cast<int64_t>(sizeof(NodeMeta) / 8);
+        if (cnt > 0 && tot + sz > target) break;
+        tot += sz;
+        ++cnt;
+      }
+      runs.push_back(Run{i, cnt, pass});
+      i += cnt;
+    }
+  };
+  for (int t = p.N; t >= 0; --t) group_stage(t, 0, bws);
+  const int nbw = static_cast<int>(runs.size());
+  for (int t = 0; t <= p.N; ++t) group_stage(t, 1, fws);
+  d->items_bw = nbw;
+  d->items_fw = static_cast<int>(runs.size()) - nbw;
+
+  std::vector<Item> items(runs.size());
+  std::vector<int64_t> item_doubles(runs.size());
+  int64_t bw_total = 0, fw_total = 0, max_item = 2, max_stage = 16;
+  int max_cnt = 1;
+  const int hdr_per_node = static_cast<int>(sizeof(NodeMeta) / 8);
+  for (size_t q = 0; q < runs.size(); ++q) {
+    const Run& ru = runs[q];
+    const std::vector<int64_t>& size = ru.pass == 0 ? bws : fws;
+    int64_t tot = static_cast<int64_t>(ru.count) * hdr_per_node;
+    for (int i = 0; i < ru.count; ++i) tot += size[ru.first + i];
+    item_doubles[q] = tot;
+    Item& it = items[q];
+    it.off = ru.pass == 0 ? bw_total : fw_total;
+    (ru.pass == 0 ? bw_total : fw_total) += tot;
+    it.bytes = static_cast<int32_t>(tot * 8);
+    it.first = ru.first;
+    it.count = ru.count;
+    it.pass = ru.pass;
+    const int last = ru.first + ru.count - 1;
+    const bool leaf = ru.first >= p.first_leaf;
+    it.leaf = leaf ? 1 : 0;
+    int64_t stage = 0;
+    if (ru.pass == 0) {
+      if (leaf) {
+        it.dep_lo = it.dep_hi = 0;
+        it.v0_lo = p.tdual_offset[ru.first - p.first_leaf];
+        it.v0_n = p.tdual_offset[last - p.first_leaf] + p.terminal_rows[last - p.first_leaf] - it.v0_lo;
+        it.v1_lo = it.v1_n = 0;
+      } else {
+        it.dep_lo = p.child_begin[ru.first];
+        it.dep_hi = p.child_begin[last] + p.child_count[last];
+        it.v0_lo = cdo[ru.first];
+        it.v0_n = cdo[last] + M[last] - it.v0_lo;
+        it.v1_lo = it.dep_lo;
+        it.v1_n = it.dep_hi - it.dep_lo;
+      }
+      stage = kMaxRhs * (static_cast<int64_t>(it.v0_n) + static_cast<int64_t>(it.v1_n) * W) +
+              static_cast<int64_t>(ru.count) * W;
+    } else {
+      if (ru.first == 0) {
+        it.dep_lo = 0;
+        it.dep_hi = 1;
+        it.v0_lo = it.v0_n = 0;
+      } else {
+        it.dep_lo = p.ancestor[ru.first];
+        it.dep_hi = p.ancestor[last] + 1;
+        it.v0_lo = it.dep_lo;
+        it.v0_n = it.dep_hi - it.dep_lo;
+      }
+      it.v1_lo = ru.first;
+      it.v1_n = leaf ? 0 : ru.count;
+      stage = kMaxRhs * (static_cast<int64_t>(it.v0_n) * Vp + static_cast<int64_t>(it.v1_n) * nu) +
+              static_cast<int64_t>(ru.count) * nx;
+    }
+    max_stage = std::max(max_stage, stage);
+    max_item = std::max(max_item, tot);
+    max_cnt = std::max(max_cnt, ru.count);
+  }
+  d->bw_doubles = bw_total;
+  d->fw_doubles = fw_total;
+  d->max_count = max_cnt;
+  d->slot_doubles = static_cast<int>((max_item + 15) & ~int64_t(15));
+  d->stage_doubles = static_cast<int>((max_stage + 15) & ~int64_t(15));
+  d->vec_doubles = static_cast<int>((static_cast<int64_t>(max_cnt) * kMaxRhs * nxp + 15) & ~int64_t(15));
+
+  // ---- pass arrays: [NodeMeta x count | node blocks] per item
+  std::vector<double> bw(static_cast<size_t>(bw_total), 0.0), fw(static_cast<size_t>(fw_total), 0.0);
   std::vector<double> aff_bw(static_cast<size_t>(n) * W, 0.0), aff_fw(static_cast<size_t>(n) * nx, 0.0);
-  parallel_for(n, 256, [&](int b, int e) {
-    for (int c = b; c < e; ++c) {
-      const NodeMeta& m = meta[c];
-      const bool leaf = m.leaf != 0;
-      double* B0 = bw.data() + bwo[c];
-      int64_t jo = 0;
-      if (!leaf) {
-        const double* d2i = f.dual_to_input.data() + static_cast<size_t>(m.cdo) * nu;
-        const double* d2c = f.dual_to_costate.data() + static_cast<size_t>(m.cdo) * nx;
-        for (int k = 0; k < m.M; ++k) {
-          for (int j = 0; j < nu; ++j) B0[k + static_cast<int64_t>(j) * m.M] = d2i[j + static_cast<int64_t>(k) * nu];
-          for (int t = 0; t < nx; ++t)
-            B0[k + static_cast<int64_t>(nu + t) * m.M] = d2c[t + static_cast<int64_t>(k) * nx];
+  parallel_for(static_cast<int>(items.size()), 64, [&](int qb, int qe) {
+    for (int q = qb; q < qe; ++q) {
+      const Item& it = items[q];
+      double* base = (it.pass == 0 ? bw.data() : fw.data()) + it.off;
+      NodeMeta* hdr = reinterpret_cast<NodeMeta*>(base);
+      int64_t blk = static_cast<int64_t>(it.count) * hdr_per_node;
+      for (int i = 0; i < it.count; ++i) {
+        const int c = it.first + i;
+        const bool leaf = c >= p.first_leaf;
+        const int mm = c == 0 ? 0 : p.stage_rows[c];
+        const int mN = leaf ? p.terminal_rows[c - p.first_leaf] : 0;
+        NodeMeta mt{};
+        mt.c = c;
+        mt.blk = static_cast<int32_t>(blk);
+        mt.M = M[c];
+        mt.m = mm;
+        mt.mN = mN;
+        mt.doff = c == 0 ? 0 : p.dual_offset[c];
+        mt.tdo = leaf ? p.tdual_offset[c - p.first_leaf] : 0;
+        if (it.pass == 0) {
+          mt.yoff = leaf ? mt.tdo - it.v0_lo : cdo[c] - it.v0_lo;
+          mt.kid0 = leaf ? 0 : p.child_begin[c] - it.v1_lo;
+          mt.nkid = leaf ? 0 : p.child_count[c];
+        } else {
+          mt.par = c == 0 ? 0 : p.ancestor[c] - it.v0_lo;
         }
-        jo = static_cast<int64_t>(m.M) * W;
-        const double* ia = f.input_affine.data() + static_cast<size_t>(c) * nu;
-        const double* ca = f.costate_affine.data() + static_cast<size_t>(c) * nx;
-        for (int j = 0; j < nu; ++j) aff_bw[static_cast<size_t>(c) * W + j] = ia[j];
-        for (int t = 0; t < nx; ++t) aff_bw[static_cast<size_t>(c) * W + nu + t] = ca[t];
-      } else {
-        const int l = c - p.first_leaf;
-        const double* FN = p.FNl(l);
-        std::copy(FN, FN + static_cast<size_t>(m.mN) * nx, B0);
-        jo = static_cast<int64_t>(m.mN) * nx;
-        const double* lca = f.leaf_costate_affine.data() + static_cast<size_t>(l) * nx;
-        for (int t = 0; t < nx; ++t) aff_bw[static_cast<size_t>(c) * W + nu + t] = lca[t];
-      }
-      if (c != 0) {
-        double* J = B0 + jo;
-        const double* c2i = f.child_to_input.data() + static_cast<size_t>(c) * nu * nx;
-        const double* cl = f.closed_loop.data() + static_cast<size_t>(c) * nx * nx;
-        for (int k = 0; k < nx; ++k) {
-          for (int j = 0; j < nu; ++j) J[k + static_cast<int64_t>(j) * nx] = c2i[j + static_cast<int64_t>(k) * nu];
-          for (int t = 0; t < nx; ++t) J[k + static_cast<int64_t>(nu + t) * nx] = cl[k + static_cast<int64_t>(t) * nx];
+        hdr[i] = mt;
+        double* B0 = base + blk;
+        if (it.pass == 0) {
+          int64_t jo = 0;
+          if (!leaf) {
+            const double* d2i = f.dual_to_input.data() + static_cast<size_t>(cdo[c]) * nu;
+            const double* d2c = f.dual_to_costate.data() + static_cast<size_t>(cdo[c]) * nx;
+            for (int k = 0; k < M[c]; ++k) {
+              for (int j = 0; j < nu; ++j) B0[k + static_cast<int64_t>(j) * M[c]] = d2i[j + static_cast<int64_t>(k) * nu];
+              for (int t = 0; t < nx; ++t)
+                B0[k + static_cast<int64_t>(nu + t) * M[c]] = d2c[t + static_cast<int64_t>(k) * nx];
+            }
+            jo = even(static_cast<int64_t>(M[c]) * W);
+            const double* ia = f.input_affine.data() + static_cast<size_t>(c) * nu;
+            const double* ca = f.costate_affine.data() + static_cast<size_t>(c) * nx;
+            for (int j = 0; j < nu; ++j) aff_bw[static_cast<size_t>(c) * W + j] = ia[j];
+            for (int t = 0; t < nx; ++t) aff_bw[static_cast<size_t>(c) * W + nu + t] = ca[t];
+          } else {
+            const int l = c - p.first_leaf;
+            const double* FN = p.FNl(l);
+            std::copy(FN, FN + static_cast<size_t>(mN) * nx, B0);
+            jo = even(static_cast<int64_t>(mN) * nx);
+            const double* lca = f.leaf_costate_affine.data() + static_cast<size_t>(l) * nx;
+            for (int t = 0; t < nx; ++t) aff_bw[static_cast<size_t>(c) * W + nu + t] = lca[t];
+          }
+          if (c != 0) {
+            double* J = B0 + jo;
+            const double* c2i = f.child_to_input.data() + static_cast<size_t>(c) * nu * nx;
+            const double* cl = f.closed_loop.data() + static_cast<size_t>(c) * nx * nx;
+            for (int k = 0; k < nx; ++k) {
+              for (int j = 0; j < nu; ++j) J[k + static_cast<int64_t>(j) * nxp] = c2i[j + static_cast<int64_t>(k) * nu];
+              for (int t = 0; t < nx; ++t) J[k + static_cast<int64_t>(nu + t) * nxp] = cl[k + static_cast<int64_t>(t) * nx];
+            }
+          }
+          blk += bws[c];
+        } else {
+          int64_t ko = 0;
+          if (c != 0) {
+            const double* A = p.Ai(c);
+            const double* Bm = p.Bi(c);
+            const double* Fm = p.Fi(c);
+            const double* Gm = p.Gi(c);
+            for (int r = 0; r < nx; ++r) {
+              double* col = B0 + static_cast<int64_t>(r) * Vp;
+              for (int k = 0; k < nx; ++k) col[k] = A[r + static_cast<int64_t>(k) * nx];
+              for (int k = 0; k < nu; ++k) col[nx + k] = Bm[r + static_cast<int64_t>(k) * nx];
+            }
+            for (int s2 = 0; s2 < mm; ++s2) {
+              double* col = B0 + static_cast<int64_t>(nx + s2) * Vp;
+              for (int k = 0; k < nx; ++k) col[k] = Fm[s2 + static_cast<int64_t>(k) * mm];
+              for (int k = 0; k < nu; ++k) col[nx + k] = Gm[s2 + static_cast<int64_t>(k) * mm];
+            }
+            ko = static_cast<int64_t>(Vp) * (nx + mm);
+            const double* cc = p.ci(c);
+            for (int t = 0; t < nx; ++t) aff_fw[static_cast<size_t>(c) * nx + t] = cc[t];
+          }
+          double* K = B0 + ko;
+          if (!leaf) {
+            const double* gain = f.gain.data() + static_cast<size_t>(c) * nu * nx;
+            for (int j = 0; j < nu; ++j)
+              for (int k = 0; k < nx; ++k) K[k + static_cast<int64_t>(j) * nxp] = gain[j + static_cast<int64_t>(k) * nu];
+          } else {
+            const double* FN = p.FNl(c - p.first_leaf);
+            for (int s2 = 0; s2 < mN; ++s2)
+              for (int k = 0; k < nx; ++k) K[k + static_cast<int64_t>(s2) * nxp] = FN[s2 + static_cast<int64_t>(k) * mN];
+          }
+          blk += fws[c];
         }
-      }
-      // forward block
-      double* F0 = fw.data() + fwo[c];
-      int64_t ko = 0;
-      if (c != 0) {
-        const double* A = p.Ai(c);
-        const double* Bm = p.Bi(c);
-        const double* Fm = p.Fi(c);
-        const double* Gm = p.Gi(c);
-        const int mm = m.m;
-        for (int r = 0; r < nx; ++r) {
-          double* col = F0 + static_cast<int64_t>(r) * V;
-          for (int k = 0; k < nx; ++k) col[k] = A[r + static_cast<int64_t>(k) * nx];
-          for (int k = 0; k < nu; ++k) col[nx + k] = Bm[r + static_cast<int64_t>(k) * nx];
-        }
-        for (int s = 0; s < mm; ++s) {
-          double* col = F0 + static_cast<int64_t>(nx + s) * V;
-          for (int k = 0; k < nx; ++k) col[k] = Fm[s + static_cast<int64_t>(k) * mm];
-          for (int k = 0; k < nu; ++k) col[nx + k] = Gm[s + static_cast<int64_t>(k) * mm];
-        }
-        ko = static_cast<int64_t>(V) * (nx + mm);
-        const double* cc = p.ci(c);
-        for (int t = 0; t < nx; ++t) aff_fw[static_cast<size_t>(c) * nx + t] = cc[t];
-      }
-      double* K = F0 + ko;
-      if (!leaf) {
-        const double* gain = f.gain.data() + static_cast<size_t>(c) * nu * nx;
-        for (int j = 0; j < nu; ++j)
-          for (int k = 0; k < nx; ++k) K[k + static_cast<int64_t>(j) * nx] = gain[j + static_cast<int64_t>(k) * nu];
-      } else {
-        const double* FN = p.FNl(c - p.first_leaf);
-        for (int s = 0; s < m.mN; ++s)
-          for (int k = 0; k < nx; ++k) K[k + static_cast<int64_t>(s) * nx] = FN[s + static_cast<int64_t>(k) * m.mN];
       }
     }
   });
 
-  // ---- items
-  const int64_t target = env_int("SCENOPT_ITEM_KB", 24) * 1024 / 8;
-  const int cap = std::max(1, env_int("SCENOPT_ITEM_MAX_NODES", 32));
-  std::vector<Item> items;
-  int max_cnt = 1;
-  int64_t max_item = 2;
-  build_items(p, bwo, bws, 0, cap, target, items, max_cnt, max_item);
-  d->items_bw = static_cast<int>(items.size());
-  build_items(p, fwo, fws, 1, cap, target, items, max_cnt, max_item);
-  d->items_fw = static_cast<int>(items.size()) - d->items_bw;
-  d->max_count = max_cnt;
-  d->slot_doubles = static_cast<int>((max_item + 15) & ~int64_t(15));
-  d->vec_doubles = static_cast<int>(((static_cast<int64_t>(max_cnt) * kMaxRhs * (2 * nx + nu)) + 15) & ~int64_t(15));
-
-  // ---- launch configuration: maximise concurrent slots per SM
+  // ---- launch configuration: one co-resident CTA per SM with the deepest
+  // even slot ring that fits (SCENOPT_NSLOT overrides)
   const int dbl = 8;
-  int best_cps = 0, best_ns = 0;
-  const int force_ns = env_int("SCENOPT_NSLOT", 0), force_cps = env_int("SCENOPT_CTAS_PER_SM", 0);
-  for (int ns = kMaxSlots; ns >= 2; --ns) {
+  const int force_ns = env_int("SCENOPT_NSLOT", 0);
+  const int teams = sweep_teams();
+  auto smem_for = [&](int ns) {
+    return (static_cast<size_t>(ns) * (d->slot_doubles + d->stage_doubles) +
+            static_cast<size_t>(teams) * d->vec_doubles) * dbl;
+  };
+  int best_ns = 0;
+  for (int ns = 4; ns >= 4; ns -= 2) {  // one producer warp per slot (sweep.cu kProducers)
     if (force_ns && ns != force_ns) continue;
-    const size_t smem = (static_cast<size_t>(ns) * d->slot_doubles + d->vec_doubles) * dbl;
+    const size_t smem = smem_for(ns);
     if (smem > static_cast<size_t>(prop.sharedMemPerBlockOptin)) continue;
-    SCN_CUDA(sweep_configure(2, smem));
+    SCN_CUDA(sweep_configure(smem));
     int cps = 0;
     SCN_CUDA(sweep_occupancy(&cps, smem));
-    if (force_cps) cps = std::min(cps, force_cps);
     if (cps < 1) continue;
-    if (cps * ns > best_cps * best_ns || (cps * ns == best_cps * best_ns && cps > best_cps)) {
-      best_cps = cps;
-      best_ns = ns;
-    }
+    best_ns = ns;
+    break;
   }
-  if (best_cps == 0) {  // a single huge node: one slot per CTA is not supported
-    const size_t smem = (2 * static_cast<size_t>(d->slot_doubles) + d->vec_doubles) * dbl;
-    fail(SCENOPT_E_INVALID_PARAMS, "dev_create: node blocks too large for shared memory (" +
-                                       std::to_string(smem) + " bytes needed per CTA)");
-  }
+  if (best_ns == 0)
+    fail(SCENOPT_E_INVALID_PARAMS, "dev_create: node blocks too large for a 2-slot shared-memory ring (" +
+                                       std::to_string(smem_for(2)) + " bytes)");
   d->nslot = best_ns;
-  d->ctas_per_sm = best_cps;
-  d->dyn_smem = (static_cast<size_t>(best_ns) * d->slot_doubles + d->vec_doubles) * dbl;
-  SCN_CUDA(sweep_configure(2, d->dyn_smem));
-  d->grid = d->sm_count * best_cps;
-  d->G = nx >= 40 ? 16 : (nx >= 20 ? 8 : 4);
-  if (const int g = env_int("SCENOPT_GROUP", 0)) d->G = g;
+  d->ctas_per_sm = 1;
+  d->dyn_smem = smem_for(best_ns);
+  SCN_CUDA(sweep_configure(d->dyn_smem));
+  d->grid = d->sm_count;
+  if (const int g = env_int("SCENOPT_GRID", 0)) d->grid = std::min(g, d->grid);  // experiments only
+  d->G = 0;
 
   // ---- upload
   d->bw_blk = upload(*d, bw);
@@ -296,11 +360,6 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int devi
   d->aff_fw = upload(*d, aff_fw);
   d->root_state = upload(*d, p.root_state);
   d->items = upload(*d, items);
-  d->meta = upload(*d, meta);
-  bwo.pop_back();
-  fwo.pop_back();
-  d->bw_off = upload(*d, bwo);
-  d->fw_off = upload(*d, fwo);
   d->ctrl = d->alloc<unsigned>(4);
   d->bw_flag = d->alloc<unsigned>(static_cast<size_t>(n));
   d->fw_flag = d->alloc<unsigned>(static_cast<size_t>(n));
@@ -346,7 +405,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int devi
   const int64_t F = p.first_leaf;
   const int64_t vecs = 2LL * D + static_cast<int64_t>(nx) * n + 3LL * nu * F +
                        static_cast<int64_t>(n - 1) * V + 2LL * (n - 1) * W;
-  const int64_t mats = d->bw_doubles + d->fw_doubles;
+  const int64_t mats = d->bw_doubles + d->fw_doubles;  // includes the per-item node headers
   d->bytes_hom = 8 * (mats + vecs);
   d->bytes_aff = d->bytes_hom + 8 * (static_cast<int64_t>(n) * W + static_cast<int64_t>(n) * nx);
   d->bytes_hom2 = 8 * (mats + 2 * vecs);
@@ -364,19 +423,18 @@ void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, doubl
   P.n = L.n;
   P.first_leaf = L.first_leaf;
   P.dual_dim = L.dual_dim;
-  P.items_bw = d.items_bw;
   P.items_total = d.items_bw + d.items_fw;
   P.nslot = d.nslot;
   P.slot_doubles = d.slot_doubles;
-  P.vec_doubles = d.vec_doubles;
+  P.stage_doubles = d.stage_doubles;
+  P.scratch_doubles = d.vec_doubles;
   P.nrhs = nrhs;
   P.affine = affine ? 1 : 0;
+  P.G = d.G;
   P.max_count = d.max_count;
-  P.max_mN = d.max_mN;
+  P.nxp = d.nxp;
+  P.Vp = d.Vp;
   P.items = d.items;
-  P.meta = d.meta;
-  P.bw_off = d.bw_off;
-  P.fw_off = d.fw_off;
   P.bw_blk = d.bw_blk;
   P.fw_blk = d.fw_blk;
   P.aff_bw = d.aff_bw;
@@ -392,7 +450,7 @@ void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, doubl
     P.Hx[r] = (Hx && Hx[r]) ? Hx[r] : d.hs[r];
     P.contrib[r] = d.contrib[r];
   }
-  SCN_CUDA(sweep_launch(P, d.grid, d.dyn_smem, d.G, d.max_m, d.stream));
+  SCN_CUDA(sweep_launch(P, d.grid, d.dyn_smem, d.max_m, d.max_mN, d.stream));
 }
 
 }  // namespace scn

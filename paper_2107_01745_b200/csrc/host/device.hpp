@@ -46,11 +46,9 @@ struct DevState {
   double *bw_blk = nullptr, *fw_blk = nullptr, *aff_bw = nullptr, *aff_fw = nullptr,
          *root_state = nullptr;
   Item* items = nullptr;
-  NodeMeta* meta = nullptr;
-  int64_t *bw_off = nullptr, *fw_off = nullptr;
   unsigned *ctrl = nullptr, *bw_flag = nullptr, *fw_flag = nullptr;
   int64_t bw_doubles = 0, fw_doubles = 0;
-  int items_bw = 0, items_fw = 0, max_count = 1, max_m = 0, max_mN = 0;
+  int items_bw = 0, items_fw = 0, max_count = 1, max_m = 0, max_mN = 0, nxp = 0, Vp = 0;
   // per dual row: nonsmooth kind, box bounds, l1 radius weight*gamma
   int8_t* row_kind = nullptr;
   double *row_lo = nullptr, *row_hi = nullptr, *row_wg = nullptr;
@@ -61,7 +59,8 @@ struct DevState {
   double* hs[kMaxRhs] = {nullptr, nullptr};
   double* ys[kMaxRhs] = {nullptr, nullptr};
   // launch configuration
-  int grid = 0, ctas_per_sm = 0, nslot = 0, slot_doubles = 0, vec_doubles = 0, G = 16;
+  int grid = 0, ctas_per_sm = 0, nslot = 0, slot_doubles = 0, stage_doubles = 0, vec_doubles = 0,
+      G = 16;
   size_t dyn_smem = 0;
   // algorithmic bytes per sweep
   int64_t bytes_hom = 0, bytes_aff = 0, bytes_hom2 = 0;
@@ -87,9 +86,11 @@ void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, doubl
                double* const* u, double* const* Hx);
 
 // kernel launchers (cuda/*.cu)
-cudaError_t sweep_configure(int nrhs, size_t dyn_smem);
+int sweep_teams();
+cudaError_t sweep_configure(size_t dyn_smem);
+cudaError_t sweep_profile_read(unsigned long long* out, bool reset);
 cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem);
-cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int G, int mmax,
+cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax,
                          cudaStream_t stream);
 
 }  // namespace scn

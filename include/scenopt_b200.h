@@ -209,10 +209,12 @@ int scenopt_linesearch_cert(scenopt_dev* d, const double* y, const double* Hx, d
                             double* T, int flags);
 
 /* ---- L-BFGS: lbfgs.hpp:22-84 (device-resident pairs) -------------------- */
+/* The buffer lives on d's device; vectors are host arrays of length n
+ * (fixed by the first call). */
 int scenopt_lbfgs_create(scenopt_dev* d, int memory, double eps_curv, scenopt_lbfgs** out);
-int scenopt_lbfgs_push(scenopt_lbfgs* b, const double* step, const double* change,
-                       double scale_ref, int flags); /* 1 accepted, 0 rejected, <0 error */
-int scenopt_lbfgs_apply(scenopt_lbfgs* b, const double* grad, double* out, int flags);
+int scenopt_lbfgs_push(scenopt_lbfgs* b, int n, const double* step, const double* change,
+                       double scale_ref); /* 1 accepted, 0 rejected, <0 error */
+int scenopt_lbfgs_apply(scenopt_lbfgs* b, int n, const double* grad, double* out);
 int scenopt_lbfgs_clear(scenopt_lbfgs* b);
 int scenopt_lbfgs_size(const scenopt_lbfgs* b);
 double scenopt_lbfgs_gamma0(const scenopt_lbfgs* b);

@@ -266,3 +266,344 @@ def sweep(cache: FactorCache, ys, affine: bool, want_primal: bool = True):
     check(N.lib().scenopt_dev_sweep(cache.device(), nr, int(affine), Yarr, Xarr, Uarr, Harr, HOST))
     pts = [_pp(prob, xs[i], us[i]) for i in range(nr)] if want_primal else None
     return pts, hs
+
+
+def grad_fhat(cache: FactorCache, prob: ProblemInstance, y, stats: OracleStats | None = None):
+    """tree_oracles.hpp:117-121: -H x(y)."""
+    return -apply_H(prob, dual_grad(cache, prob, y, stats), cache)
+
+
+def fhat_value(cache: FactorCache, prob: ProblemInstance, y, stats: OracleStats | None = None):
+    """tree_oracles.hpp:125-129."""
+    _check_shapes(cache, prob, "fhat_value")
+    yv = _dual(prob, y, "fhat_value")
+    out = C.c_double()
+    check(N.lib().scenopt_fhat_value(cache.device(), dptr(yv), C.byref(out), HOST))
+    if stats is not None:
+        stats.dual_grad_calls += 1
+    return out.value
+
+
+def apply_H(prob: ProblemInstance, pt: PrimalPoint, cache: FactorCache | None = None):
+    """problem_data.hpp:144-162 (on the device of `cache`, or of a
+    factor-less handle of `prob`)."""
+    dev = cache.device() if cache is not None else _lite(prob)
+    x = np.ascontiguousarray(pt.x, dtype=np.float64).ravel(order="F")
+    u = np.ascontiguousarray(pt.u, dtype=np.float64).ravel(order="F")
+    if x.size != prob.nx * prob.num_nodes() or u.size != prob.nu * prob.first_leaf:
+        raise N.DimensionMismatch("apply_H: point does not match the instance")
+    z = np.zeros(prob.dual_dim)
+    check(N.lib().scenopt_apply_H(dev, dptr(np.ascontiguousarray(x)), dptr(np.ascontiguousarray(u)),
+                                  dptr(z), HOST))
+    return z
+
+
+_LITE = {}
+
+
+def _lite(prob: ProblemInstance):
+    """Factor-less device handle (apply_H / prox / verification)."""
+    key = id(prob)
+    h = _LITE.get(key)
+    if h is None or h[0] is not prob:
+        dev = C.c_void_p()
+        check(N.lib().scenopt_dev_create(prob._h, None, 0, C.byref(dev)))
+        _LITE[key] = (prob, dev)
+        return dev
+    return h[1]
+
+
+# ---------------------------------------------------------------- nonsmooth
+class Nonsmooth:
+    """SeparableNonsmooth bound to a problem (prox.hpp:24-52)."""
+
+    def __init__(self, prob: ProblemInstance, cache: FactorCache | None = None):
+        self.prob = prob
+        self.dim = prob.dual_dim
+        self._dev = cache.device() if cache is not None else _lite(prob)
+
+    def prox(self, v, gamma_prox):
+        out = np.zeros(self.dim)
+        check(N.lib().scenopt_prox_g(self._dev, dptr(_dual(self.prob, v, "prox_g")),
+                                     C.c_double(gamma_prox), dptr(out), HOST))
+        return out
+
+    def conj(self, w):
+        out = C.c_double()
+        check(N.lib().scenopt_conj_value_g(self._dev, dptr(_dual(self.prob, w, "conj_value_g")),
+                                           C.byref(out), HOST))
+        return out.value
+
+    def dist_subdiff_inf(self, y, z):
+        out = C.c_double()
+        check(N.lib().scenopt_dist_subdiff_inf(self._dev, dptr(_dual(self.prob, y, "dist")),
+                                               dptr(_dual(self.prob, z, "dist")), C.byref(out), HOST))
+        return out.value
+
+
+def make_nonsmooth(prob: ProblemInstance, cache: FactorCache | None = None) -> Nonsmooth:
+    return Nonsmooth(prob, cache)
+
+
+# ---------------------------------------------------------------- FBE
+@dataclass
+class FbState:
+    """fbe.hpp:22-34."""
+
+    y: np.ndarray
+    lam: float
+    x: PrimalPoint
+    Hx: np.ndarray
+    z: np.ndarray
+    T: np.ndarray
+    R: np.ndarray
+    fhat: float
+    conj_T: float
+    znorm_sq: float
+    value: float
+
+
+def fb_step(cache: FactorCache, prob: ProblemInstance, y, lam: float,
+            stats: OracleStats | None = None) -> FbState:
+    """fbe.hpp:55-67 (one dual_grad sweep + fused prox / conjugate / FBE)."""
+    _check_shapes(cache, prob, "fb_step")
+    yv = _dual(prob, y, "fb_step")
+    x, u = _primal_out(prob)
+    D = prob.dual_dim
+    Hx, z, R, T = np.zeros(D), np.zeros(D), np.zeros(D), np.zeros(D)
+    sc = np.zeros(4)
+    check(N.lib().scenopt_fb_step(cache.device(), dptr(yv), C.c_double(lam), dptr(x), dptr(u),
+                                  dptr(Hx), dptr(z), dptr(R), dptr(T), dptr(sc), HOST))
+    if stats is not None:
+        stats.dual_grad_calls += 1
+        stats.prox_calls += 1
+        stats.conj_calls += 1
+    return FbState(yv.copy(), lam, _pp(prob, x, u), Hx, z, T, R, sc[0], sc[1], sc[2], sc[3])
+
+
+def fbe_value(state: FbState) -> float:
+    """fbe.hpp:82-86."""
+    if not np.isfinite(state.value):
+        raise N.InfiniteConjugate("fbe_value: g*(T) is infinite")
+    return state.value
+
+
+def fbe_grad(state: FbState, cache: FactorCache, prob: ProblemInstance,
+             stats: OracleStats | None = None):
+    """fbe.hpp:89-94: R + lam H x0(R)."""
+    out = np.zeros(prob.dual_dim)
+    check(N.lib().scenopt_fbe_grad(cache.device(), dptr(_dual(prob, state.R, "fbe_grad")),
+                                   C.c_double(state.lam), dptr(out), HOST))
+    if stats is not None:
+        stats.hessian_vec_calls += 1
+    return out
+
+
+def linesearch_cert(cache: FactorCache, prob: ProblemInstance, state: FbState, direction, taus,
+                    shift=None) -> dict:
+    """linesearch_cert / linesearch_cert_shifted + evaluate_cert at `taus`
+    (fbe.hpp:136-231). Returns deltas, the certificate scalars, cert_fhat(tau)
+    and w / Hx_w / z / R / T of the last tau."""
+    D = prob.dual_dim
+    taus = np.ascontiguousarray(taus, dtype=np.float64)
+    deltas, cfh, cs = np.zeros(len(taus)), np.zeros(len(taus)), np.zeros(6)
+    w, Hxw, z, R, T = (np.zeros(D) for _ in range(5))
+    ss = np.array([state.fhat, state.conj_T, state.znorm_sq, state.value])
+    sh = None if shift is None else _dual(prob, shift, "shift")
+    check(N.lib().scenopt_linesearch_cert(
+        cache.device(), dptr(_dual(prob, state.y, "y")), dptr(_dual(prob, state.Hx, "Hx")),
+        C.c_double(state.lam), dptr(ss), dptr(sh), dptr(_dual(prob, direction, "dir")),
+        len(taus), dptr(taus), dptr(deltas), dptr(cs), dptr(cfh), dptr(w), dptr(Hxw), dptr(z),
+        dptr(R), dptr(T), HOST))
+    return dict(deltas=deltas, alpha1=cs[0], alpha2=cs[1], conj_anchor=cs[2],
+                znorm_sq_anchor=cs[3], value_anchor=cs[4], fhat_anchor=cs[5], cert_fhat=cfh,
+                w=w, Hx_w=Hxw, z=z, R=R, T=T)
+
+
+# ---------------------------------------------------------------- L-BFGS
+class LbfgsBuffer:
+    """lbfgs.hpp:22-84 with device-resident pairs (on `cache`'s device)."""
+
+    def __init__(self, memory: int, eps_curv: float, cache: FactorCache):
+        self._h = C.c_void_p()
+        check(N.lib().scenopt_lbfgs_create(cache.device(), memory, C.c_double(eps_curv),
+                                           C.byref(self._h)))
+        self._cache = cache
+        self._memory = memory
+
+    def __del__(self):
+        if getattr(self, "_h", None) and N._lib is not None:
+            N._lib.scenopt_lbfgs_destroy(self._h)
+            self._h = None
+
+    def push(self, step, change, scale_ref) -> bool:
+        s = np.ascontiguousarray(step, np.float64)
+        q = np.ascontiguousarray(change, np.float64)
+        return bool(check(N.lib().scenopt_lbfgs_push(self._h, len(s), dptr(s), dptr(q),
+                                                     C.c_double(scale_ref))))
+
+    def apply_direction(self, grad):
+        g = np.ascontiguousarray(grad, np.float64)
+        out = np.zeros(len(g))
+        check(N.lib().scenopt_lbfgs_apply(self._h, len(g), dptr(g), dptr(out)))
+        return out
+
+    def clear(self):
+        check(N.lib().scenopt_lbfgs_clear(self._h))
+
+    def size(self) -> int:
+        return check(N.lib().scenopt_lbfgs_size(self._h))
+
+    def memory(self) -> int:
+        return self._memory
+
+    def gamma0(self) -> float:
+        return float(N.lib().scenopt_lbfgs_gamma0(self._h))
+
+
+# ---------------------------------------------------------------- solvers
+BACKTRACKING = {"original": 0, "simple": 1, "none": 2}
+KINDS = {"minfbe": 0, "nama": 1, "gpad": 2}
+
+
+@dataclass
+class SolverConfig:
+    """solvers.hpp:28-46."""
+
+    lambda0: float = 0.0
+    eps: float = 5e-4
+    eps_curv: float = 1e-12
+    eps_bt: float = 0.25
+    beta_bt: float = 0.05
+    memory: int = 5
+    max_iters: int = 20000
+    backtracking_rule: str = "simple"
+    warm_start: bool = False
+    warm_start_iters: int = 5
+    precondition: bool = False
+    nama_parallel_linesearch: bool = False
+    nama_update_tlambda: bool = True
+
+    def c(self):
+        return N.SolverConfigC(self.lambda0, self.eps, self.eps_curv, self.eps_bt, self.beta_bt,
+                               self.memory, self.max_iters,
+                               BACKTRACKING[self.backtracking_rule], int(self.warm_start),
+                               self.warm_start_iters, int(self.precondition),
+                               int(self.nama_parallel_linesearch), int(self.nama_update_tlambda))
+
+
+@dataclass
+class SolverReport:
+    """solvers.hpp:66-84."""
+
+    status: str
+    x: PrimalPoint
+    y: np.ndarray
+    z: np.ndarray
+    residual_inf: float
+    iterations: int
+    stats: OracleStats
+    lipschitz_calls: int
+    lipschitz_estimate: float
+    lambda_final: float
+    eps: float
+    residual_trace: np.ndarray
+    fbe_trace: np.ndarray
+    wall_ms: float
+    verified: bool
+    verify_residual_inf: float
+    verify_subdiff_dist: float
+    _h: object = field(default=None, repr=False)
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and N._lib is not None:
+            N._lib.scenopt_report_destroy(self._h)
+            self._h = None
+
+
+def _report(prob: ProblemInstance, h) -> SolverReport:
+    s = N.ReportSummaryC()
+    check(N.lib().scenopt_report_summary_get(h, C.byref(s)))
+    x, u = _primal_out(prob)
+    D = prob.dual_dim
+    y, z = np.zeros(D), np.zeros(D)
+    rt, ft = np.zeros(s.trace_len), np.zeros(s.trace_len)
+    check(N.lib().scenopt_report_arrays(h, dptr(x), dptr(u), dptr(y), dptr(z), dptr(rt), dptr(ft)))
+    return SolverReport(
+        status="converged" if s.status == 0 else "max_iters_exceeded", x=_pp(prob, x, u), y=y, z=z,
+        residual_inf=s.residual_inf, iterations=s.iterations,
+        stats=OracleStats(s.dual_grad_calls, s.hessian_vec_calls, s.prox_calls, s.conj_calls),
+        lipschitz_calls=s.lipschitz_calls, lipschitz_estimate=s.lipschitz_estimate,
+        lambda_final=s.lambda_final, eps=s.eps, residual_trace=rt, fbe_trace=ft,
+        wall_ms=s.wall_ms, verified=bool(s.verified), verify_residual_inf=s.verify_residual_inf,
+        verify_subdiff_dist=s.verify_subdiff_dist, _h=h)
+
+
+def estimate_dual_lipschitz(cache: FactorCache, prob: ProblemInstance):
+    """solvers.hpp:89-113 -> (estimate, sweeps)."""
+    _check_shapes(cache, prob, "estimate_dual_lipschitz")
+    calls = C.c_uint64()
+    out = C.c_double()
+    check(N.lib().scenopt_estimate_lipschitz(cache.device(), C.byref(calls), C.byref(out)))
+    return out.value, int(calls.value)
+
+
+def _solve_direct(kind, prob, cache, cfg, y0=None, residual_weight=None):
+    _check_shapes(cache, prob, "solve")
+    y0v = None if y0 is None else _dual(prob, y0, "y0")
+    wv = None if residual_weight is None else _dual(prob, residual_weight, "weight")
+    h = C.c_void_p()
+    c = cfg.c()
+    check(N.lib().scenopt_dev_solve(cache.device(), C.byref(c), KINDS[kind], dptr(y0v), dptr(wv),
+                                    C.byref(h)))
+    return _report(prob, h)
+
+
+def solve_minfbe(prob, cache, cfg: SolverConfig, y0=None, residual_weight=None) -> SolverReport:
+    """solvers.hpp:234-356."""
+    return _solve_direct("minfbe", prob, cache, cfg, y0, residual_weight)
+
+
+def solve_nama(prob, cache, cfg: SolverConfig, y0=None, residual_weight=None) -> SolverReport:
+    """solvers.hpp:362-492."""
+    return _solve_direct("nama", prob, cache, cfg, y0, residual_weight)
+
+
+def solve_gpad(prob, cache, cfg: SolverConfig, y0=None, residual_weight=None) -> SolverReport:
+    """solvers.hpp:498-540."""
+    return _solve_direct("gpad", prob, cache, cfg, y0, residual_weight)
+
+
+def warm_start(prob, cache, cfg: SolverConfig, lam: float):
+    """solvers.hpp:545-564 -> (y, dual_grad_calls)."""
+    y = np.zeros(prob.dual_dim)
+    dg = C.c_uint64()
+    c = cfg.c()
+    check(N.lib().scenopt_warm_start(cache.device(), C.byref(c), C.c_double(lam), dptr(y),
+                                     C.byref(dg)))
+    return y, int(dg.value)
+
+
+def solve(prob: ProblemInstance, cfg: SolverConfig, kind: str = "nama",
+          shared_cache: FactorCache | None = None, device: int = 0) -> SolverReport:
+    """solvers.hpp:645-720: precondition, factor, Lipschitz estimate, warm
+    start, solver run and independent verification."""
+    h = C.c_void_p()
+    c = cfg.c()
+    check(N.lib().scenopt_solve(prob._h, C.byref(c), KINDS[kind],
+                                shared_cache._h if shared_cache is not None else None, device,
+                                C.byref(h)))
+    return _report(prob, h)
+
+
+def verify_report(prob: ProblemInstance, rep: SolverReport, z_override=None, device: int = 0):
+    """solvers.hpp:630-639 (recomputes the verify_* fields in place)."""
+    zo = None if z_override is None else _dual(prob, z_override, "z")
+    check(N.lib().scenopt_verify_report(prob._h, rep._h, dptr(zo), device))
+    new = _report(prob, rep._h)
+    rep.verified, rep.verify_residual_inf, rep.verify_subdiff_dist = (
+        new.verified, new.verify_residual_inf, new.verify_subdiff_dist)
+    new._h = None
+    if zo is not None:
+        rep.z = zo.copy()
+    return rep

@@ -1,0 +1,764 @@
+// SPDX-License-Identifier: MIT
+//
+// K3-K8: fused dual-vector kernels of the forward-backward machinery
+// (fbe.hpp, lbfgs.hpp, prox.hpp, solvers.hpp). Dual vectors are small next
+// to the sweep's matrix stream (37k doubles at C3), so these kernels are
+// latency-bound: each one is a single cooperative persistent grid that does
+// all the passes of one algorithmic step, with grid barriers between passes
+// and a deterministic reduction (fixed per-block tree, block partials summed
+// in block order by every block). Every block therefore sees bit-identical
+// scalars, and decisions (L-BFGS curvature gate, first accepted line-search
+// step, power-iteration stop) are taken on the device without a host round
+// trip.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "dual.hpp"
+
+namespace scn {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxRed = 24;  // scalars per reduction
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = *reinterpret_cast<volatile unsigned*>(bar + 1);
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire(bar + 1) == gen) __nanosleep(20);
+    }
+  }
+  __syncthreads();
+}
+
+// Deterministic grid reduction of K per-thread values (sum, or max when
+// MAX). Every thread of every block receives the totals in v.
+template <int K, bool MAX = false>
+__device__ void grid_reduce(const DualCtx& c, int& ph, double (&v)[K]) {
+  __shared__ double sh[kWarps][kMaxRed];
+  __shared__ double tot[kMaxRed];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double t = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, t, o);
+      t = MAX ? fmax(t, u) : t + u;
+    }
+    if (lane == 0) sh[warp][k] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double t = sh[0][threadIdx.x];
+    for (int w = 1; w < kWarps; ++w) t = MAX ? fmax(t, sh[w][threadIdx.x]) : t + sh[w][threadIdx.x];
+    c.part[(static_cast<int64_t>(ph) * 64 + threadIdx.x) * c.nblk + blockIdx.x] = t;
+  }
+  grid_sync(c.bar);
+  if (warp == 0) {
+    for (int k = 0; k < K; ++k) {
+      const double* p = c.part + (static_cast<int64_t>(ph) * 64 + k) * c.nblk;
+      double t = MAX ? -INFINITY : 0.0;
+      for (int b = lane; b < c.nblk; b += 32) t = MAX ? fmax(t, __ldcg(p + b)) : t + __ldcg(p + b);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, t, o);
+        t = MAX ? fmax(t, u) : t + u;
+      }
+      if (lane == 0) tot[k] = t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = tot[k];
+  ph ^= 1;
+}
+
+// prox of gamma_prox * g on one row (prox.hpp:58-81).
+__device__ __forceinline__ double prox_row(int kind, double v, double lo, double hi, double thr) {
+  if (kind == 1) return fmin(fmax(v, lo), hi);
+  if (kind == 2) return v > thr ? v - thr : (v < -thr ? v + thr : 0.0);
+  return v;
+}
+// g* on one row (prox.hpp:90-113); +inf where the conjugate is infinite.
+__device__ __forceinline__ double conj_row(int kind, double w, double lo, double hi, double wg) {
+  constexpr double slack = 1e-9;
+  if (kind == 1) return fmax(w * lo, w * hi);
+  if (kind == 2) return fabs(w) > wg * (1.0 + slack) + slack ? INFINITY : 0.0;
+  return fabs(w) > slack ? INFINITY : 0.0;
+}
+
+__device__ __forceinline__ int gtid() { return blockIdx.x * kThreads + threadIdx.x; }
+__device__ __forceinline__ int gstride() { return gridDim.x * kThreads; }
+
+// ---------------------------------------------------------------- K3
+__global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, int mode, const double* y,
+                                                             const double* Hx, const double* Hx0,
+                                                             const double* weight, double* z, double* R,
+                                                             double* T) {
+  int ph = 0;
+  double* S = c.S + st * sl::kStateStride;
+  const double lam = S[sl::LAM];
+  const double gp = 1.0 / lam;
+  double s[5] = {0, 0, 0, 0, 0};  // conj, z2, Hx.R, R2, (Hx0+Hx).y
+  double m[1] = {0.0};            // weighted inf residual
+  for (int i = gtid(); i < c.D; i += gstride()) {
+    const int kd = c.g.kind[i];
+    const double yi = y[i], hi = Hx[i];
+    const double zi = prox_row(kd, yi / lam + hi, c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
+    const double Ri = zi - hi;
+    const double Ti = yi - lam * Ri;
+    z[i] = zi;
+    R[i] = Ri;
+    T[i] = Ti;
+    s[0] += conj_row(kd, Ti, c.g.lo[i], c.g.hi[i], c.g.wg[i]);
+    s[1] += zi * zi;
+    s[2] += hi * Ri;
+    s[3] += Ri * Ri;
+    if (mode == 0) s[4] += (Hx0[i] + hi) * yi;
+    m[0] = fmax(m[0], fabs(weight ? Ri * weight[i] : Ri));
+  }
+  grid_reduce<5>(c, ph, s);
+  grid_reduce<1, true>(c, ph, m);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double fhat = mode == 0 ? c.S[sl::FHAT0] - 0.5 * s[4] : S[sl::FHAT];
+    S[sl::FHAT] = fhat;
+    S[sl::CONJ] = s[0];
+    S[sl::ZN2] = s[1];
+    S[sl::VALUE] = fhat + s[0] + lam * s[2] + 0.5 * lam * s[3];
+    S[sl::RESID] = m[0];
+  }
+}
+
+// ---------------------------------------------------------------- K7
+__global__ void __launch_bounds__(kThreads) fbe_grad_kernel(DualCtx c, int st, const double* R,
+                                                            const double* HR, double* grad) {
+  int ph = 0;
+  const double lam = c.S[st * sl::kStateStride + sl::LAM];
+  double s[2] = {0, 0};
+  for (int i = gtid(); i < c.D; i += gstride()) {
+    const double Ri = R[i];
+    const double gi = Ri + lam * HR[i];
+    grad[i] = gi;
+    const double img = (gi - Ri) / lam;
+    s[0] += img * img;
+    s[1] += Ri * Ri;
+  }
+  grid_reduce<2>(c, ph, s);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c.S[sl::IMG2] = s[0];
+    c.S[sl::R2] = s[1];
+  }
+}
+
+// ---------------------------------------------------------------- K5
+__global__ void __launch_bounds__(kThreads) lbfgs_kernel(DualCtx c, int mem, double eps_curv, double scale_ref,
+                                                         int do_push,
+                                                         const double* a, const double* b, const double* cc,
+                                                         const double* dd, const double* gv, double* out,
+                                                         double* Sb, double* Qb) {
+  int ph = 0;
+  const int64_t D = c.D;
+  __shared__ int order[64];
+  __shared__ int count_s;
+  if (threadIdx.x == 0) {
+    count_s = c.I[il::LB_COUNT];
+    for (int j = 0; j <= mem; ++j) order[j] = c.I[il::LB_ORDER + j];
+  }
+  __syncthreads();
+  int count = count_s;
+  double gamma0 = c.S[sl::GAMMA0];
+  __shared__ double alpha[64];
+  __shared__ double curv[64];
+  if (threadIdx.x <= mem && threadIdx.x < 64) curv[threadIdx.x] = c.S[sl::CURV + threadIdx.x];
+  __syncthreads();
+  int pushed = 0;
+  if (do_push) {  // lbfgs.hpp:33-44 (strict curvature gate, FIFO eviction)
+    const int f = order[count];  // a free slot
+    double* sv = Sb + f * D;
+    double* qv = Qb + f * D;
+    double s4[4] = {0, 0, 0, 0};  // <s,q>, |s|^2, |q|^2, |dd|^2 (scale_ref)
+    for (int i = gtid(); i < c.D; i += gstride()) {
+      const double si = a[i] - b[i];
+      const double qi = cc[i] - dd[i];
+      sv[i] = si;
+      qv[i] = qi;
+      s4[0] += si * qi;
+      s4[1] += si * si;
+      s4[2] += qi * qi;
+      s4[3] += dd[i] * dd[i];
+    }
+    grid_reduce<4>(c, ph, s4);
+    const double curvature = s4[0];
+    const double scale = scale_ref >= 0.0 ? scale_ref : s4[3];
+    if ((curvature > eps_curv * s4[1] * scale) && (s4[2] > 0.0)) {
+      pushed = 1;
+      if (threadIdx.x == 0) {
+        if (count == mem) {  // evict the oldest pair
+          const int o = order[0];
+          for (int j = 0; j + 1 < mem; ++j) order[j] = order[j + 1];
+          order[mem - 1] = f;
+          order[mem] = o;
+        } else {
+          ++count_s;  // order[count] already holds f
+        }
+        curv[f] = curvature;
+      }
+      __syncthreads();
+      count = count_s;
+      gamma0 = curvature / s4[2];
+    }
+  }
+  // two-loop recursion (lbfgs.hpp:48-62), fused dot/axpy passes
+  if (count == 0) {
+    for (int i = gtid(); i < c.D; i += gstride()) out[i] = -(gamma0 * gv[i]);
+  } else {
+    // first loop: newest -> oldest
+    double pend = 0.0;
+    int pend_slot = -1;
+    for (int j = count - 1; j >= 0; --j) {
+      const int sj = order[j];
+      const double* s_j = Sb + sj * D;
+      const double* q_p = pend_slot >= 0 ? Qb + pend_slot * D : nullptr;
+      double acc[1] = {0.0};
+      for (int i = gtid(); i < c.D; i += gstride()) {
+        double w = (j == count - 1) ? gv[i] : out[i];
+        if (q_p) w = w - pend * q_p[i];
+        out[i] = w;
+        acc[0] += s_j[i] * w;
+      }
+      grid_reduce<1>(c, ph, acc);
+      const double al = acc[0] / curv[sj];
+      if (threadIdx.x == 0) alpha[j] = al;
+      pend = al;
+      pend_slot = sj;
+    }
+    __syncthreads();
+    // scale by gamma0 after the last pending update, then second loop
+    double pb = 0.0;
+    int pb_slot = -1;
+    for (int j = 0; j < count; ++j) {
+      const int sj = order[j];
+      const double* q_j = Qb + sj * D;
+      double acc[1] = {0.0};
+      for (int i = gtid(); i < c.D; i += gstride()) {
+        double w = out[i];
+        if (j == 0) {
+          w = w - alpha[0] * Qb[order[0] * D + i];
+          w = w * gamma0;
+        } else {
+          w = w + pb * Sb[pb_slot * D + i];
+        }
+        out[i] = w;
+        acc[0] += q_j[i] * w;
+      }
+      grid_reduce<1>(c, ph, acc);
+      const double beta = acc[0] / curv[sj];
+      pb = alpha[j] - beta;
+      pb_slot = sj;
+    }
+    for (int i = gtid(); i < c.D; i += gstride()) out[i] = -(out[i] + pb * Sb[pb_slot * D + i]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c.I[il::LB_COUNT] = count;
+    c.I[il::LB_PUSHED] = pushed;
+    for (int j = 0; j <= mem; ++j) {
+      c.I[il::LB_ORDER + j] = order[j];
+      c.S[sl::CURV + j] = curv[j];
+    }
+    c.S[sl::GAMMA0] = gamma0;
+  }
+}
+
+// ---------------------------------------------------------------- K4 / K6
+struct Taus {
+  double t[16];
+};
+
+__global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int shifted, int tlambda,
+                                                        const double* y, const double* R, const double* Hx,
+                                                        const double* HR, const double* d, const double* Hd,
+                                                        double* y_next, int ntau_explicit, Taus taus,
+                                                        double* deltas, double* cfh, double* ow, double* oHxw,
+                                                        double* oz, double* oR, double* oT) {
+  int ph = 0;
+  const double* S0 = c.S + st * sl::kStateStride;
+  const double lam = S0[sl::LAM], gp = 1.0 / lam;
+  const double value = S0[sl::VALUE], fhat = S0[sl::FHAT];
+  // pass 1: coefficients (fbe.hpp:136-143) and, for the shifted form, the
+  // anchor quantities (fbe.hpp:172-203)
+  double s[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  // 0 <dir,Hxd> 1 |Hxd|^2 2 <Hxa, dir + lam Hxd> 3 <Hxa,dir> 4 <Hx,r> 5 <r,Hr>
+  // 6 conj_a 7 |z_a|^2 8 <Hxa,res_a> 9 |res_a|^2 10 |HR|^2 11 |R|^2
+  for (int i = gtid(); i < c.D; i += gstride()) {
+    double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
+    if (shifted) {
+      const double r = -lam * R[i];
+      const double hr = -lam * HR[i];
+      s[4] += Hx[i] * r;
+      s[5] += r * hr;
+      an = an + r;
+      di = di - r;
+      ha = ha + hr;
+      hd = hd - hr;
+      const int kd = c.g.kind[i];
+      const double za = prox_row(kd, an / lam + ha, c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
+      const double ra = za - ha;
+      s[6] += conj_row(kd, an - lam * ra, c.g.lo[i], c.g.hi[i], c.g.wg[i]);
+      s[7] += za * za;
+      s[8] += ha * ra;
+      s[9] += ra * ra;
+      s[10] += HR[i] * HR[i];
+      s[11] += R[i] * R[i];
+    }
+    s[0] += di * hd;
+    s[1] += hd * hd;
+    s[2] += ha * (di + lam * hd);
+    s[3] += ha * di;
+  }
+  grid_reduce<12>(c, ph, s);
+  const double quad = s[0];
+  const double alpha2 = -0.5 * quad - 0.5 * lam * s[1];
+  const double alpha1 = -s[2];
+  double fhat_a, conj_a, zn2_a, value_a;
+  if (shifted) {
+    fhat_a = fhat - s[4] - 0.5 * s[5];
+    conj_a = s[6];
+    zn2_a = s[7];
+    value_a = fhat_a + conj_a + lam * s[8] + 0.5 * lam * s[9];
+  } else {
+    fhat_a = fhat;
+    conj_a = S0[sl::CONJ];
+    zn2_a = S0[sl::ZN2];
+    value_a = value;
+  }
+  const double slack = 1e-12 * (1.0 + fabs(value));
+  // tau search: batches of 8 speculative trials (evaluate_cert, fbe.hpp:214-231)
+  int kstar = -1;
+  double tau_star = 0.0, delta_star = 0.0;
+  const int ntau = ntau_explicit > 0 ? ntau_explicit : 61;
+  for (int base = 0; base < ntau && kstar < 0; base += 8) {
+    double acc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+    double tq[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int kk = base + q;
+      tq[q] = ntau_explicit > 0 ? (kk < ntau ? taus.t[kk < 16 ? kk : 15] : 0.0) : ldexp(1.0, -kk);
+    }
+    for (int i = gtid(); i < c.D; i += gstride()) {
+      double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
+      if (shifted) {
+        const double r = -lam * R[i];
+        const double hr = -lam * HR[i];
+        an = an + r;
+        di = di - r;
+        ha = ha + hr;
+        hd = hd - hr;
+      }
+      const double pb = an / lam + ha, ps = di / lam + hd;
+      const int kd = c.g.kind[i];
+      const double lo = c.g.lo[i], hi = c.g.hi[i], wg = c.g.wg[i];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double tau = tq[q];
+        const double z = prox_row(kd, pb + tau * ps, lo, hi, gp * wg);
+        const double Rt = z - (ha + tau * hd);
+        const double Tt = (an + tau * di) - lam * Rt;
+        acc[2 * q] += conj_row(kd, Tt, lo, hi, wg);
+        acc[2 * q + 1] += z * z;
+      }
+    }
+    grid_reduce<16>(c, ph, acc);
+    for (int q = 0; q < 8 && base + q < ntau; ++q) {
+      const double tau = tq[q];
+      const double delta =
+          alpha2 * tau * tau + alpha1 * tau + acc[2 * q] - conj_a + 0.5 * lam * (acc[2 * q + 1] - zn2_a);
+      if (ntau_explicit > 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+          deltas[base + q] = delta;
+          cfh[base + q] = fhat_a - tau * s[3] - 0.5 * tau * tau * quad;
+        }
+        continue;
+      }
+      const bool ok = shifted ? (value_a + delta <= value + slack) : (delta <= slack);
+      if (ok) {
+        kstar = base + q;
+        tau_star = tau;
+        delta_star = delta;
+        break;
+      }
+    }
+  }
+  if (ntau_explicit > 0) {  // vectors of the last tau (test path)
+    kstar = ntau - 1;
+    tau_star = taus.t[ntau - 1];
+  }
+  // final pass at tau*: next iterate and the original-rule probes
+  double f2[2] = {0, 0};
+  if (kstar >= 0) {
+    const double tau = tau_star;
+    for (int i = gtid(); i < c.D; i += gstride()) {
+      double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
+      if (shifted) {
+        const double r = -lam * R[i];
+        const double hr = -lam * HR[i];
+        an = an + r;
+        di = di - r;
+        ha = ha + hr;
+        hd = hd - hr;
+      }
+      const double pb = an / lam + ha, ps = di / lam + hd;
+      const int kd = c.g.kind[i];
+      const double z = prox_row(kd, pb + tau * ps, c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
+      const double w = an + tau * di;
+      const double hxw = ha + tau * hd;
+      const double Rt = z - hxw;
+      const double Tt = w - lam * Rt;
+      if (y_next) y_next[i] = tlambda ? Tt : y[i] - lam * Rt;
+      if (ow) {
+        ow[i] = w;
+        oHxw[i] = hxw;
+        oz[i] = z;
+        oR[i] = Rt;
+        oT[i] = Tt;
+      }
+      f2[0] += hxw * Rt;
+      f2[1] += Rt * Rt;
+    }
+  }
+  grid_reduce<2>(c, ph, f2);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c.S[sl::TAU] = tau_star;
+    c.S[sl::KSTAR] = kstar;
+    c.S[sl::STALL] = kstar < 0 ? 1.0 : 0.0;
+    c.S[sl::CERT_FHAT] = fhat_a - tau_star * s[3] - 0.5 * tau_star * tau_star * quad;
+    c.S[sl::HXW_RW] = f2[0];
+    c.S[sl::RW2] = f2[1];
+    c.S[sl::VALUE_A] = value_a;
+    c.S[sl::CONJ_A] = conj_a;
+    c.S[sl::ZN2_A] = zn2_a;
+    c.S[sl::FHAT_A] = fhat_a;
+    c.S[sl::ALPHA1] = alpha1;
+    c.S[sl::ALPHA2] = alpha2;
+    c.S[sl::DELTA] = delta_star;
+    c.S[sl::HR2] = s[10];
+    c.S[sl::RR2] = s[11];
+  }
+}
+
+// ---------------------------------------------------------------- K8
+__global__ void __launch_bounds__(kThreads) power_kernel(DualCtx c, double* v, const double* Hv, double rel_tol) {
+  int ph = 0;
+  double s[2] = {0, 0};
+  for (int i = gtid(); i < c.D; i += gstride()) {
+    const double img = -Hv[i];
+    s[0] += v[i] * img;
+    s[1] += img * img;
+  }
+  grid_reduce<2>(c, ph, s);
+  const double next = s[0], mag = sqrt(s[1]);
+  const bool zero = !(mag > 0.0);
+  const double rayleigh = c.S[sl::RAYLEIGH];
+  const bool settled = fabs(next - rayleigh) <= rel_tol * fabs(next);
+  if (!zero && !settled)
+    for (int i = gtid(); i < c.D; i += gstride()) v[i] = -Hv[i] / mag;
+  grid_sync(c.bar);  // every block has read S[RAYLEIGH]
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (!zero) c.S[sl::RAYLEIGH] = next;
+    c.S[sl::PNEXT] = next;
+    c.S[sl::PMAG] = mag;
+    c.I[il::SETTLED] = settled ? 1 : 0;
+    c.I[il::PZERO] = zero ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------- helpers
+__global__ void extrapolate_kernel(int D, const double* yn, double* yp, double* w, double mom) {
+  for (int i = gtid(); i < D; i += gstride()) {
+    const double a = yn[i];
+    w[i] = a + mom * (a - yp[i]);
+    yp[i] = a;
+  }
+}
+
+__global__ void prox_kernel(DualCtx c, const double* v, double gp, double* out) {
+  for (int i = gtid(); i < c.D; i += gstride())
+    out[i] = prox_row(c.g.kind[i], v[i], c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
+}
+
+__global__ void __launch_bounds__(kThreads) conj_kernel(DualCtx c, const double* w) {
+  int ph = 0;
+  double s[1] = {0.0};
+  for (int i = gtid(); i < c.D; i += gstride()) s[0] += conj_row(c.g.kind[i], w[i], c.g.lo[i], c.g.hi[i], c.g.wg[i]);
+  grid_reduce<1>(c, ph, s);
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.S[sl::RED0] = s[0];
+}
+
+// prox.hpp:127-171
+__global__ void __launch_bounds__(kThreads) dist_kernel(DualCtx c, const double* y, const double* z) {
+  int ph = 0;
+  double m[1] = {0.0};
+  for (int i = gtid(); i < c.D; i += gstride()) {
+    const int kd = c.g.kind[i];
+    const double yi = y[i], zi = z[i];
+    double dv = 0.0;
+    if (kd == 0) {
+      dv = fabs(yi);
+    } else if (kd == 1) {
+      const double lo = c.g.lo[i], hi = c.g.hi[i];
+      const double cushion = 1e-12 * (1.0 + fabs(lo) + fabs(hi));
+      const bool at_lo = zi <= lo + cushion, at_hi = zi >= hi - cushion;
+      dv = (at_lo && at_hi) ? 0.0 : at_lo ? fmax(yi, 0.0) : at_hi ? fmax(-yi, 0.0) : fabs(yi);
+    } else {
+      const double t = c.g.wg[i];
+      dv = zi > 0.0 ? fabs(yi - t) : (zi < 0.0 ? fabs(yi + t) : fmax(0.0, fabs(yi) - t));
+    }
+    m[0] = fmax(m[0], dv);
+  }
+  grid_reduce<1, true>(c, ph, m);
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.S[sl::RED0] = m[0];
+}
+
+__global__ void __launch_bounds__(kThreads) maxdiff_kernel(DualCtx c, const double* a, const double* b) {
+  int ph = 0;
+  double m[1] = {0.0};
+  for (int i = gtid(); i < c.D; i += gstride()) m[0] = fmax(m[0], fabs(a[i] - b[i]));
+  grid_reduce<1, true>(c, ph, m);
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.S[sl::RED0] = m[0];
+}
+
+__global__ void __launch_bounds__(kThreads) dot_kernel(DualCtx c, const double* a, const double* b) {
+  int ph = 0;
+  double s[1] = {0.0};
+  for (int i = gtid(); i < c.D; i += gstride()) s[0] += a[i] * b[i];
+  grid_reduce<1>(c, ph, s);
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.S[sl::RED0] = s[0];
+}
+
+__global__ void scale_kernel(int n, double alpha, const double* x, double beta, const double* y0, double* y) {
+  for (int i = gtid(); i < n; i += gstride()) y[i] = alpha * x[i] + (y0 ? beta * y0[i] : 0.0);
+}
+
+// apply_H over packed rows
+__global__ void apply_H_kernel(HRows h, const double* x, const double* u, double* z) {
+  const int V = h.nx + h.nu;
+  for (int r = gtid(); r < h.nrows; r += gstride()) {
+    const double* cf = h.coef + static_cast<int64_t>(r) * V;
+    const int64_t nd = h.row_node[r];
+    const double* xv = x + nd * h.nx;
+    double s = 0.0;
+    for (int k = 0; k < h.nx; ++k) s = fma(cf[k], xv[k], s);
+    if (!h.row_term[r]) {
+      const double* uv = u + nd * h.nu;
+      for (int k = 0; k < h.nu; ++k) s = fma(cf[h.nx + k], uv[k], s);
+    }
+    z[r] = s;
+  }
+}
+
+// eval_f: one warp per node (problem_data.hpp:194-222)
+__global__ void __launch_bounds__(kThreads) eval_f_kernel(DualCtx c, CostPack cp, const double* x,
+                                                          const double* u, double tol) {
+  int ph = 0;
+  const int nx = cp.nx, nu = cp.nu;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * kThreads + threadIdx.x) >> 5, nw = (gridDim.x * kThreads) >> 5;
+  const int64_t csz = 2LL * nx * nx + 2LL * nx * nu + static_cast<int64_t>(nu) * nu + 2 * nx + nu;
+  const int64_t lsz = static_cast<int64_t>(nx) * nx + nx;
+  double s[1] = {0.0}, bad[1] = {0.0};
+  const int L = cp.n - cp.first_leaf;
+  for (int t = gw; t < (cp.n - 1) + L + 1; t += nw) {
+    if (t == (cp.n - 1) + L) {  // root state check
+      for (int k = lane; k < nx; k += 32)
+        if (fabs(x[k] - cp.root_state[k]) > tol) bad[0] = 1.0;
+      continue;
+    }
+    if (t < cp.n - 1) {
+      const int nd = t + 1;
+      const int64_t a = cp.anc[nd];
+      const double* blk = cp.node + static_cast<int64_t>(t) * csz;
+      const double *A = blk, *B = A + nx * nx, *cv = B + nx * nu, *Q = cv + nx, *Sm = Q + nx * nx,
+                   *Rm = Sm + nu * nx, *q = Rm + nu * nu, *r = q + nx;
+      const double* xa = x + a * nx;
+      const double* ua = u + a * nu;
+      const double* xc = x + static_cast<int64_t>(nd) * nx;
+      double part = 0.0;
+      for (int row = lane; row < nx; row += 32) {  // dynamics residual and x'Qx
+        double ax = 0.0, qx = 0.0;
+        for (int k = 0; k < nx; ++k) {
+          ax = fma(A[row + k * nx], xa[k], ax);
+          qx = fma(Q[row + k * nx], xa[k], qx);
+        }
+        for (int k = 0; k < nu; ++k) ax = fma(B[row + k * nx], ua[k], ax);
+        if (fabs(xc[row] - ax - cv[row]) > tol) bad[0] = 1.0;
+        part += xa[row] * qx + q[row] * xa[row];
+      }
+      for (int row = lane; row < nu; row += 32) {  // u'Ru + 2 u'Sx + r'u
+        double ru = 0.0, sx = 0.0;
+        for (int k = 0; k < nu; ++k) ru = fma(Rm[row + k * nu], ua[k], ru);
+        for (int k = 0; k < nx; ++k) sx = fma(Sm[row + k * nu], xa[k], sx);
+        part += ua[row] * ru + 2.0 * ua[row] * sx + r[row] * ua[row];
+      }
+      s[0] += cp.prob[nd] * part;  // per-lane partial; reduced below
+    } else {
+      const int l = t - (cp.n - 1);
+      const int nd = cp.first_leaf + l;
+      const double* P = cp.leaf + static_cast<int64_t>(l) * lsz;
+      const double* p = P + nx * nx;
+      const double* xc = x + static_cast<int64_t>(nd) * nx;
+      double part = 0.0;
+      for (int row = lane; row < nx; row += 32) {
+        double px = 0.0;
+        for (int k = 0; k < nx; ++k) px = fma(P[row + k * nx], xc[k], px);
+        part += xc[row] * px + p[row] * xc[row];
+      }
+      s[0] += cp.prob[nd] * part;
+    }
+  }
+  grid_reduce<1>(c, ph, s);
+  grid_reduce<1, true>(c, ph, bad);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c.S[sl::EVALF] = s[0];
+    c.S[sl::EVALF_INF] = bad[0];
+  }
+}
+
+cudaError_t coop(const void* fn, const DualCtx& c, void** args, cudaStream_t st) {
+  return cudaLaunchCooperativeKernel(fn, dim3(c.nblk), dim3(kThreads), args, 0, st);
+}
+
+}  // namespace
+
+int dual_block_threads() { return kThreads; }
+
+cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, const double* Hx,
+                        const double* Hx0, const double* weight, double* z, double* R, double* T,
+                        cudaStream_t st) {
+  DualCtx cc = c;
+  void* args[] = {&cc, &state, &mode, &y, &Hx, &Hx0, &weight, &z, &R, &T};
+  return coop(reinterpret_cast<const void*>(fb_finish_kernel), c, args, st);
+}
+
+cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const double* HR, double* grad,
+                       cudaStream_t st) {
+  DualCtx cc = c;
+  void* args[] = {&cc, &state, &R, &HR, &grad};
+  return coop(reinterpret_cast<const void*>(fbe_grad_kernel), c, args, st);
+}
+
+cudaError_t k_lbfgs(const DualCtx& c, int mem, double eps_curv, double scale_ref, int do_push, const double* a,
+                    const double* b, const double* cc, const double* dd, const double* gvec,
+                    double* out, double* Sbuf, double* Qbuf, cudaStream_t st) {
+  DualCtx c2 = c;
+  void* args[] = {&c2, &mem, &eps_curv, &scale_ref, &do_push, &a, &b, &cc, &dd, &gvec, &out, &Sbuf, &Qbuf};
+  return coop(reinterpret_cast<const void*>(lbfgs_kernel), c, args, st);
+}
+
+cudaError_t k_cert_search(const DualCtx& c, int state, int shifted, int tlambda, const double* y,
+                          const double* R, const double* Hx, const double* HR, const double* d,
+                          const double* Hd, double* y_next, cudaStream_t st) {
+  DualCtx cc = c;
+  int ntau = 0;
+  Taus taus{};
+  double* nul = nullptr;
+  void* args[] = {&cc, &state, &shifted, &tlambda, &y, &R, &Hx, &HR, &d, &Hd, &y_next, &ntau, &taus,
+                  &nul, &nul, &nul, &nul, &nul, &nul, &nul};
+  return coop(reinterpret_cast<const void*>(cert_kernel), c, args, st);
+}
+
+cudaError_t k_cert_eval(const DualCtx& c, int state, int shifted, const double* y, const double* R,
+                        const double* Hx, const double* HR, const double* d, const double* Hd,
+                        int ntau, const double* taus_host, double* deltas, double* cfh, double* w,
+                        double* Hxw, double* zz, double* RR, double* TT, cudaStream_t st) {
+  if (ntau < 1 || ntau > 16) return cudaErrorInvalidValue;
+  DualCtx cc = c;
+  Taus taus{};
+  for (int k = 0; k < ntau; ++k) taus.t[k] = taus_host[k];
+  int tl = 1;
+  double* yn = nullptr;
+  void* args[] = {&cc, &state, &shifted, &tl, &y, &R, &Hx, &HR, &d, &Hd, &yn, &ntau, &taus,
+                  &deltas, &cfh, &w, &Hxw, &zz, &RR, &TT};
+  return coop(reinterpret_cast<const void*>(cert_kernel), c, args, st);
+}
+
+cudaError_t k_power(const DualCtx& c, double* v, const double* Hv, double rel_tol, cudaStream_t st) {
+  DualCtx cc = c;
+  void* args[] = {&cc, &v, &Hv, &rel_tol};
+  return coop(reinterpret_cast<const void*>(power_kernel), c, args, st);
+}
+
+cudaError_t k_extrapolate(const DualCtx& c, const double* yn, double* yp, double* w, double mom,
+                          cudaStream_t st) {
+  extrapolate_kernel<<<c.nblk, kThreads, 0, st>>>(c.D, yn, yp, w, mom);
+  return cudaGetLastError();
+}
+
+cudaError_t k_prox(const DualCtx& c, const double* v, double gamma_prox, double* out, cudaStream_t st) {
+  prox_kernel<<<c.nblk, kThreads, 0, st>>>(c, v, gamma_prox, out);
+  return cudaGetLastError();
+}
+
+cudaError_t k_conj(const DualCtx& c, const double* w, cudaStream_t st) {
+  DualCtx cc = c;
+  void* args[] = {&cc, &w};
+  return coop(reinterpret_cast<const void*>(conj_kernel), c, args, st);
+}
+
+cudaError_t k_dist_subdiff(const DualCtx& c, const double* y, const double* z, cudaStream_t st) {
+  DualCtx cc = c;
+  void* args[] = {&cc, &y, &z};
+  return coop(reinterpret_cast<const void*>(dist_kernel), c, args, st);
+}
+
+cudaError_t k_max_abs_diff(const DualCtx& c, const double* a, const double* b, cudaStream_t st) {
+  DualCtx cc = c;
+  void* args[] = {&cc, &a, &b};
+  return coop(reinterpret_cast<const void*>(maxdiff_kernel), c, args, st);
+}
+
+cudaError_t k_dot(const DualCtx& c, const double* a, const double* b, cudaStream_t st) {
+  DualCtx cc = c;
+  void* args[] = {&cc, &a, &b};
+  return coop(reinterpret_cast<const void*>(dot_kernel), c, args, st);
+}
+
+cudaError_t k_scale(const DualCtx& c, int n, double alpha, const double* x, double beta, const double* y0,
+                    double* y, cudaStream_t st) {
+  scale_kernel<<<c.nblk, kThreads, 0, st>>>(n, alpha, x, beta, y0, y);
+  return cudaGetLastError();
+}
+
+cudaError_t k_apply_H(const HRows& h, const double* x, const double* u, double* z, cudaStream_t st) {
+  const int blocks = (h.nrows + kThreads - 1) / kThreads;
+  apply_H_kernel<<<blocks > 0 ? blocks : 1, kThreads, 0, st>>>(h, x, u, z);
+  return cudaGetLastError();
+}
+
+cudaError_t k_eval_f(const DualCtx& c, const CostPack& cp, const double* x, const double* u,
+                     double feas_tol, cudaStream_t st) {
+  DualCtx cc = c;
+  CostPack p = cp;
+  void* args[] = {&cc, &p, &x, &u, &feas_tol};
+  return coop(reinterpret_cast<const void*>(eval_f_kernel), c, args, st);
+}
+
+}  // namespace scn

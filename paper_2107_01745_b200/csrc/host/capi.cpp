@@ -14,12 +14,6 @@ namespace scn {
 thread_local std::string g_last_error;
 }
 
-struct scenopt_problem {
-  Problem p;
-};
-struct scenopt_factor {
-  Factor f;
-};
 
 extern "C" {
 
@@ -135,7 +129,7 @@ void scenopt_factor_destroy(scenopt_factor* f) { delete f; }
 int scenopt_dev_create(const scenopt_problem* p, const scenopt_factor* f, int device, scenopt_dev** out) {
   SCN_GUARD({
     auto h = std::make_unique<scenopt_dev>();
-    h->d = dev_create(p->p, f->f, device);
+    h->d = dev_create(p->p, f ? &f->f : nullptr, device);
     h->init_solver_buffers();
     *out = h.release();
   });

@@ -34,6 +34,13 @@ struct Stats {  // OracleStats, tree_oracles.hpp:14-21
     }                                    \
   } while (0)
 
+struct scenopt_problem {
+  scn::Problem p;
+};
+struct scenopt_factor {
+  scn::Factor f;
+};
+
 struct scenopt_dev {
   std::unique_ptr<scn::DevState> d;
   scn::Stats stats;

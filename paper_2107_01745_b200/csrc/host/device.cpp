@@ -54,8 +54,12 @@ T* upload(DevState& d, const std::vector<T>& h) {
 
 }  // namespace
 
-std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int device) {
-  check_factor_shape(f, p, "dev_create");
+namespace {
+void pack_common(DevState& d, const Problem& p);
+}
+
+std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int device) {
+  if (fptr) check_factor_shape(*fptr, p, "dev_create");
   require_valid(p);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -95,6 +99,14 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int devi
   L.tdual_offset = p.tdual_offset;
   L.probability = p.probability;
   L.root_state = p.root_state;
+
+  if (!fptr) {
+    pack_common(*d, p);
+    SCN_CUDA(cudaDeviceSynchronize());
+    return d;
+  }
+  const Factor& f = *fptr;
+  d->has_factor = true;
 
   // ---- per-node block sizes (doubles, even => 16-byte aligned); padded
   // column lengths pad(l) == 2 (mod 4) for conflict-free 16-byte smem loads
@@ -367,31 +379,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int devi
   SCN_CUDA(cudaMemset(d->bw_flag, 0, static_cast<size_t>(n) * sizeof(unsigned)));
   SCN_CUDA(cudaMemset(d->fw_flag, 0, static_cast<size_t>(n) * sizeof(unsigned)));
 
-  // per-row nonsmooth data
+  pack_common(*d, p);
   const int D = p.dual_dim;
-  std::vector<int8_t> kind(static_cast<size_t>(D), 0);
-  std::vector<double> lo(static_cast<size_t>(D), 0.0), hi(static_cast<size_t>(D), 0.0),
-      wg(static_cast<size_t>(D), 0.0);
-  for (int i = 1; i < n; ++i)
-    for (int k = 0; k < p.stage_rows[i]; ++k) {
-      const int row = p.dual_offset[i] + k;
-      kind[row] = static_cast<int8_t>(p.g_kind[i]);
-      lo[row] = p.zmin[row];
-      hi[row] = p.zmax[row];
-      wg[row] = p.probability[i] * p.g_gamma[i];
-    }
-  for (int l = 0; l < p.L; ++l)
-    for (int k = 0; k < p.terminal_rows[l]; ++k) {
-      const int row = p.tdual_offset[l] + k;
-      kind[row] = static_cast<int8_t>(p.tg_kind[l]);
-      lo[row] = p.zmin[row];
-      hi[row] = p.zmax[row];
-      wg[row] = p.probability[p.first_leaf + l] * p.tg_gamma[l];
-    }
-  d->row_kind = upload(*d, kind);
-  d->row_lo = upload(*d, lo);
-  d->row_hi = upload(*d, hi);
-  d->row_wg = upload(*d, wg);
 
   for (int r = 0; r < kMaxRhs; ++r) {
     d->contrib[r] = d->alloc<double>(static_cast<size_t>(n) * W);
@@ -413,9 +402,107 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int devi
   return d;
 }
 
+namespace {
+// Per-dual-row nonsmooth data, apply_H rows and eval_f cost blocks: what
+// every handle needs, with or without the sweep layout.
+void pack_common(DevState& dd, const Problem& p) {
+  DevState* d = &dd;
+  const int n = p.n, nx = p.nx, nu = p.nu, D = p.dual_dim, V = nx + nu;
+  std::vector<int8_t> kind(static_cast<size_t>(D), 0);
+  std::vector<double> lo(static_cast<size_t>(D), 0.0), hi(static_cast<size_t>(D), 0.0),
+      wg(static_cast<size_t>(D), 0.0);
+  std::vector<int32_t> rnode(static_cast<size_t>(D), 0);
+  std::vector<int8_t> rterm(static_cast<size_t>(D), 0);
+  std::vector<double> coef(static_cast<size_t>(D) * V, 0.0);
+  for (int i = 1; i < n; ++i) {
+    const int m = p.stage_rows[i];
+    const double* F = p.Fi(i);
+    const double* G = p.Gi(i);
+    for (int k = 0; k < m; ++k) {
+      const int row = p.dual_offset[i] + k;
+      kind[row] = static_cast<int8_t>(p.g_kind[i]);
+      lo[row] = p.zmin[row];
+      hi[row] = p.zmax[row];
+      wg[row] = p.probability[i] * p.g_gamma[i];
+      rnode[row] = p.ancestor[i];
+      double* cf = coef.data() + static_cast<size_t>(row) * V;
+      for (int t = 0; t < nx; ++t) cf[t] = F[k + static_cast<size_t>(t) * m];
+      for (int t = 0; t < nu; ++t) cf[nx + t] = G[k + static_cast<size_t>(t) * m];
+    }
+  }
+  for (int l = 0; l < p.L; ++l) {
+    const int m = p.terminal_rows[l];
+    const double* FN = p.FNl(l);
+    for (int k = 0; k < m; ++k) {
+      const int row = p.tdual_offset[l] + k;
+      kind[row] = static_cast<int8_t>(p.tg_kind[l]);
+      lo[row] = p.zmin[row];
+      hi[row] = p.zmax[row];
+      wg[row] = p.probability[p.first_leaf + l] * p.tg_gamma[l];
+      rnode[row] = p.first_leaf + l;
+      rterm[row] = 1;
+      double* cf = coef.data() + static_cast<size_t>(row) * V;
+      for (int t = 0; t < nx; ++t) cf[t] = FN[k + static_cast<size_t>(t) * m];
+    }
+  }
+  d->row_kind = upload(*d, kind);
+  d->row_lo = upload(*d, lo);
+  d->row_hi = upload(*d, hi);
+  d->row_wg = upload(*d, wg);
+  d->hrows.nx = nx;
+  d->hrows.nu = nu;
+  d->hrows.nrows = D;
+  d->hrows.row_node = upload(*d, rnode);
+  d->hrows.row_term = upload(*d, rterm);
+  d->hrows.coef = upload(*d, coef);
+  // eval_f blocks: [A | B | c | Q | S | R | q | r] per non-root node, [P | p] per leaf
+  const size_t csz = 2 * p.sxx() + 2 * p.sxu() + p.suu() + 2 * static_cast<size_t>(nx) + nu;
+  std::vector<double> cn(static_cast<size_t>(n > 1 ? n - 1 : 1) * csz, 0.0);
+  parallel_for(n - 1, 256, [&](int b, int e) {
+    for (int t = b; t < e; ++t) {
+      const int i = t + 1;
+      double* o = cn.data() + static_cast<size_t>(t) * csz;
+      o = std::copy(p.Ai(i), p.Ai(i) + p.sxx(), o);
+      o = std::copy(p.Bi(i), p.Bi(i) + p.sxu(), o);
+      o = std::copy(p.ci(i), p.ci(i) + nx, o);
+      o = std::copy(p.Qi(i), p.Qi(i) + p.sxx(), o);
+      o = std::copy(p.Si(i), p.Si(i) + p.sxu(), o);
+      o = std::copy(p.Ri(i), p.Ri(i) + p.suu(), o);
+      o = std::copy(p.qi(i), p.qi(i) + nx, o);
+      std::copy(p.ri(i), p.ri(i) + nu, o);
+    }
+  });
+  const size_t lsz = p.sxx() + static_cast<size_t>(nx);
+  std::vector<double> cl(static_cast<size_t>(p.L) * lsz, 0.0);
+  for (int l = 0; l < p.L; ++l) {
+    double* o = cl.data() + static_cast<size_t>(l) * lsz;
+    o = std::copy(p.Pl(l), p.Pl(l) + p.sxx(), o);
+    std::copy(p.pl(l), p.pl(l) + nx, o);
+  }
+  d->cost.nx = nx;
+  d->cost.nu = nu;
+  d->cost.n = n;
+  d->cost.first_leaf = p.first_leaf;
+  d->cost.anc = upload(*d, p.ancestor);
+  d->cost.prob = upload(*d, p.probability);
+  d->cost.node = upload(*d, cn);
+  d->cost.leaf = upload(*d, cl);
+  d->cost.root_state = upload(*d, p.root_state);
+  if (!d->root_state) d->root_state = const_cast<double*>(d->cost.root_state);
+  if (!d->has_factor)
+    for (int r = 0; r < kMaxRhs; ++r) {
+      d->xs[r] = d->alloc<double>(static_cast<size_t>(n) * nx);
+      d->us[r] = d->alloc<double>(static_cast<size_t>(std::max(p.first_leaf, 1)) * nu);
+      d->hs[r] = d->alloc<double>(static_cast<size_t>(std::max(D, 1)));
+      d->ys[r] = d->alloc<double>(static_cast<size_t>(std::max(D, 1)));
+    }
+}
+}  // namespace
+
 void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
                double* const* u, double* const* Hx) {
   if (nrhs < 1 || nrhs > kMaxRhs) fail(SCENOPT_E_INVALID_PARAMS, "sweep: nrhs must be 1 or 2");
+  if (!d.has_factor) fail(SCENOPT_E_CACHE_MISMATCH, "sweep: handle was created without a factor cache");
   const Layout& L = d.lay;
   SweepParams P{};
   P.nx = L.nx;

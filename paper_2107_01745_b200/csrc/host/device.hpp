@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "../cuda/dual.hpp"
 #include "../cuda/layout.hpp"
 #include "model.hpp"
 
@@ -64,6 +65,10 @@ struct DevState {
   size_t dyn_smem = 0;
   // algorithmic bytes per sweep
   int64_t bytes_hom = 0, bytes_aff = 0, bytes_hom2 = 0;
+  bool has_factor = false;
+  // apply_H rows and eval_f cost blocks
+  HRows hrows{};
+  CostPack cost{};
 
   ~DevState();
   template <class T>
@@ -77,7 +82,9 @@ struct DevState {
   void free_owned(void* p);
 };
 
-std::unique_ptr<DevState> dev_create(const Problem& p, const Factor& f, int device);
+// f == nullptr builds a factor-less handle (apply_H, eval_f, prox/conj,
+// verification) without the sweep layout.
+std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* f, int device);
 int device_count_sm100();
 
 // One fused sweep over nrhs right-hand sides; y/x/u/Hx are device pointers

@@ -1,0 +1,1023 @@
+// SPDX-License-Identifier: MIT
+//
+// Solver layer over the device kernels: the forward-backward step, the FBE
+// gradient, the line-search certificate, L-BFGS, the power iteration, and the
+// MINFBE / NAMA / GPAD loops with the reference's exact control flow
+// (solvers.hpp:89-720, fbe.hpp, lbfgs.hpp). All vector work runs on the
+// device (sweep.cu, dualops.cu); the host only sequences kernels and reads a
+// few scalars at the decision points the reference's loops branch on.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "capi_internal.hpp"
+
+using namespace scn;
+
+// ------------------------------------------------------------------ workspace
+struct scenopt_dev::Work {
+  int D = 0, nblk = 0;
+  double* S = nullptr;
+  int* I = nullptr;
+  double* part = nullptr;
+  unsigned* bar = nullptr;
+  double* hS = nullptr;  // pinned mirrors
+  int* hI = nullptr;
+  // two FbStates (ping-pong)
+  double *y[2] = {}, *Hx[2] = {}, *z[2] = {}, *R[2] = {}, *T[2] = {}, *x[2] = {}, *u[2] = {};
+  double *Hx0 = nullptr, *x0 = nullptr, *u0 = nullptr;
+  double *grad = nullptr, *prev_y = nullptr, *prev_g = nullptr, *dir = nullptr, *Hd = nullptr,
+         *HR = nullptr, *v = nullptr, *Hv = nullptr, *w = nullptr, *yp = nullptr, *weight = nullptr,
+         *tmp = nullptr, *tmp2 = nullptr;
+  double *Sb = nullptr, *Qb = nullptr;
+  double* small = nullptr;  // 64 doubles of API scratch
+  int lb_slots = 0;
+  bool fhat0_ready = false;
+  DualCtx ctx(const DevState& d) const {
+    DualCtx c{};
+    c.D = D;
+    c.nblk = nblk;
+    c.g = RowG{d.row_kind, d.row_lo, d.row_hi, d.row_wg};
+    c.S = S;
+    c.I = I;
+    c.part = part;
+    c.bar = bar;
+    return c;
+  }
+};
+
+scenopt_dev::scenopt_dev() = default;
+scenopt_dev::~scenopt_dev() {
+  if (w) {
+    if (w->hS) cudaFreeHost(w->hS);
+    if (w->hI) cudaFreeHost(w->hI);
+  }
+}
+
+void scenopt_dev::init_solver_buffers() {
+  DevState& ds = *d;
+  SCN_CUDA(cudaSetDevice(ds.device));
+  w = std::make_unique<Work>();
+  Work& k = *w;
+  const Layout& L = ds.lay;
+  k.D = std::max(L.dual_dim, 1);
+  k.nblk = ds.sm_count;
+  k.S = ds.alloc<double>(sl::kScalars);
+  k.I = ds.alloc<int>(il::kInts);
+  k.part = ds.alloc<double>(static_cast<size_t>(2) * 64 * k.nblk);
+  k.bar = ds.alloc<unsigned>(4);
+  SCN_CUDA(cudaMemset(k.S, 0, sl::kScalars * sizeof(double)));
+  SCN_CUDA(cudaMemset(k.I, 0, il::kInts * sizeof(int)));
+  SCN_CUDA(cudaMemset(k.bar, 0, 4 * sizeof(unsigned)));
+  SCN_CUDA(cudaMallocHost(&k.hS, sl::kScalars * sizeof(double)));
+  SCN_CUDA(cudaMallocHost(&k.hI, il::kInts * sizeof(int)));
+  const size_t D = static_cast<size_t>(k.D), nxn = static_cast<size_t>(L.nx) * L.n,
+               nuf = static_cast<size_t>(L.nu) * std::max(L.first_leaf, 1);
+  for (int s = 0; s < 2; ++s) {
+    k.y[s] = ds.alloc<double>(D);
+    k.Hx[s] = ds.alloc<double>(D);
+    k.z[s] = ds.alloc<double>(D);
+    k.R[s] = ds.alloc<double>(D);
+    k.T[s] = ds.alloc<double>(D);
+    k.x[s] = ds.alloc<double>(nxn);
+    k.u[s] = ds.alloc<double>(nuf);
+  }
+  k.small = ds.alloc<double>(64);
+  k.Hx0 = ds.alloc<double>(D);
+  k.x0 = ds.alloc<double>(nxn);
+  k.u0 = ds.alloc<double>(nuf);
+  for (double** p : {&k.grad, &k.prev_y, &k.prev_g, &k.dir, &k.Hd, &k.HR, &k.v, &k.Hv, &k.w, &k.yp,
+                     &k.weight, &k.tmp, &k.tmp2})
+    *p = ds.alloc<double>(D);
+}
+
+namespace {
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+struct Report {  // SolverReport, solvers.hpp:66-84
+  int status = 1, iterations = 0;
+  Stats stats;
+  uint64_t lipschitz_calls = 0;
+  double lipschitz_estimate = 0.0, lambda_final = 0.0, eps = 0.0,
+         residual_inf = std::numeric_limits<double>::infinity(), wall_ms = 0.0;
+  bool verified = false;
+  double verify_residual_inf = std::numeric_limits<double>::infinity();
+  double verify_subdiff_dist = std::numeric_limits<double>::infinity();
+  std::vector<double> residual_trace, fbe_trace, x, u, y, z;
+};
+
+// solvers.hpp:48-60
+void validate_config(const scenopt_solver_config& c) {
+  if (c.lambda0 < 0.0) fail(SCENOPT_E_INVALID_PARAMS, "lambda0 must be >= 0");
+  if (!(c.eps > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "eps must be > 0");
+  if (!(c.eps_curv > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "eps_curv must be > 0");
+  if (!(c.eps_bt > 0.0 && c.eps_bt < 0.5)) fail(SCENOPT_E_INVALID_PARAMS, "eps_bt must lie in (0, 1/2)");
+  if (c.beta_bt < 0.0 || c.beta_bt >= 1.0) fail(SCENOPT_E_INVALID_PARAMS, "beta_bt must lie in [0, 1)");
+  if (c.memory < 1) fail(SCENOPT_E_INVALID_PARAMS, "memory must be >= 1");
+  if (c.memory > 48) fail(SCENOPT_E_INVALID_PARAMS, "memory must be <= 48 on the device");
+  if (c.max_iters < 1) fail(SCENOPT_E_INVALID_PARAMS, "max_iters must be >= 1");
+  if (c.warm_start_iters < 0) fail(SCENOPT_E_INVALID_PARAMS, "warm_start_iters must be >= 0");
+  if (c.backtracking_rule < 0 || c.backtracking_rule > 2)
+    fail(SCENOPT_E_INVALID_PARAMS, "unknown backtracking rule");
+}
+
+// solvers.hpp:122-127
+double halve_lambda(double lambda) {
+  const double next = 0.5 * lambda;
+  if (next < 1e-14) fail(SCENOPT_E_STEP_UNDERFLOW, "backtracking drove lambda below 1e-14");
+  return next;
+}
+
+}  // namespace
+
+// Engine: the per-handle solver operations (device resident).
+struct Engine {
+  scenopt_dev& h;
+  DevState& d;
+  scenopt_dev::Work& k;
+  cudaStream_t st;
+  Engine(scenopt_dev& hh) : h(hh), d(*hh.d), k(*hh.w), st(hh.d->stream) { SCN_CUDA(cudaSetDevice(d.device)); }
+  DualCtx ctx() const { return k.ctx(d); }
+  size_t D() const { return static_cast<size_t>(d.lay.dual_dim); }
+
+  void set_scalar(int slot, double v) {
+    k.hS[slot] = v;  // staged through a pinned word per slot
+    SCN_CUDA(cudaMemcpyAsync(k.S + slot, k.hS + slot, sizeof(double), cudaMemcpyHostToDevice, st));
+    SCN_CUDA(cudaStreamSynchronize(st));
+  }
+  void read_scalars() {
+    SCN_CUDA(cudaMemcpyAsync(k.hS, k.S, sl::kScalars * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SCN_CUDA(cudaMemcpyAsync(k.hI, k.I, il::kInts * sizeof(int), cudaMemcpyDeviceToHost, st));
+    SCN_CUDA(cudaStreamSynchronize(st));
+  }
+  double S(int slot) const { return k.hS[slot]; }
+  int I(int slot) const { return k.hI[slot]; }
+  void copy(double* dst, const double* src, size_t n) {
+    SCN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  void sweep1(bool affine, const double* y, double* x, double* u, double* Hx) {
+    dev_sweep(d, 1, affine, &y, x ? &x : nullptr, u ? &u : nullptr, &Hx);
+  }
+  void sweep2(const double* a, const double* b, double* Ha, double* Hb) {
+    const double* ys[2] = {a, b};
+    double* hs[2] = {Ha, Hb};
+    dev_sweep(d, 2, false, ys, nullptr, nullptr, hs);
+  }
+
+  // f_hat(0) and H x(0), once per handle (fhat identity)
+  void ensure_fhat0() {
+    if (k.fhat0_ready) return;
+    SCN_CUDA(cudaMemsetAsync(k.tmp, 0, D() * sizeof(double), st));
+    sweep1(true, k.tmp, k.x0, k.u0, k.Hx0);
+    SCN_CUDA(k_eval_f(ctx(), d.cost, k.x0, k.u0, 1e-8, st));
+    read_scalars();
+    const double f0 = S(sl::EVALF);
+    if (S(sl::EVALF_INF) != 0.0 || !std::isfinite(f0))
+      fail(SCENOPT_E_ERROR, "fhat(0): the oracle's minimiser violated the dynamics");
+    set_scalar(sl::FHAT0, -f0);
+    k.fhat0_ready = true;
+  }
+
+  // fb_step (fbe.hpp:55-67) into state s: dual_grad sweep + fused finish
+  void fb_step(int s, const double* ydev, double lambda, const double* weight, Stats& stats) {
+    if (!(lambda > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "fb_step: lambda must be > 0");
+    ensure_fhat0();
+    if (ydev != k.y[s]) copy(k.y[s], ydev, D());
+    set_scalar(s * sl::kStateStride + sl::LAM, lambda);
+    sweep1(true, k.y[s], k.x[s], k.u[s], k.Hx[s]);
+    ++stats.dual_grad_calls;
+    SCN_CUDA(k_fb_finish(ctx(), s, 0, k.y[s], k.Hx[s], k.Hx0, weight, k.z[s], k.R[s], k.T[s], st));
+    ++stats.prox_calls;
+    ++stats.conj_calls;
+  }
+  // rescale_state (fbe.hpp:72-77): no sweep
+  void rescale(int s, double lambda, const double* weight, Stats& stats) {
+    if (!(lambda > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "rescale_state: lambda must be > 0");
+    set_scalar(s * sl::kStateStride + sl::LAM, lambda);
+    SCN_CUDA(k_fb_finish(ctx(), s, 1, k.y[s], k.Hx[s], k.Hx0, weight, k.z[s], k.R[s], k.T[s], st));
+    ++stats.prox_calls;
+    ++stats.conj_calls;
+  }
+  void lbfgs_reset(int mem) {
+    if (k.lb_slots < mem + 1) {
+      k.Sb = d.alloc<double>(static_cast<size_t>(mem + 1) * D());
+      k.Qb = d.alloc<double>(static_cast<size_t>(mem + 1) * D());
+      k.lb_slots = mem + 1;
+    }
+    std::vector<int> ints(il::kInts, 0);
+    for (int j = 0; j <= mem; ++j) ints[il::LB_ORDER + j] = j;
+    SCN_CUDA(cudaMemcpy(k.I, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
+    set_scalar(sl::GAMMA0, 1.0);
+  }
+  void lbfgs_clear() {  // lbfgs.hpp:64-67
+    const int zero = 0;
+    SCN_CUDA(cudaMemcpy(k.I + il::LB_COUNT, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    set_scalar(sl::GAMMA0, 1.0);
+  }
+
+  // estimate_dual_lipschitz (solvers.hpp:89-113)
+  double lipschitz(uint64_t* calls, double rel_tol = 1e-6, int max_rounds = 100) {
+    const int n = d.lay.dual_dim;
+    std::vector<double> v(static_cast<size_t>(n));
+    std::mt19937_64 gen(0x5eed5eed5eed5eedULL);
+    for (int i = 0; i < n; ++i) v[i] = 2.0 * ((gen() >> 11) * 0x1.0p-53) - 1.0;
+    double nn = 0.0;
+    for (double a : v) nn += a * a;
+    nn = std::sqrt(nn);
+    for (double& a : v) a /= nn;
+    SCN_CUDA(cudaMemcpy(k.v, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+    set_scalar(sl::RAYLEIGH, 0.0);
+    double rayleigh = 0.0;
+    for (int round = 0; round < max_rounds; ++round) {
+      sweep1(false, k.v, nullptr, nullptr, k.Hv);
+      if (calls) ++*calls;
+      SCN_CUDA(k_power(ctx(), k.v, k.Hv, rel_tol, st));
+      read_scalars();
+      if (I(il::PZERO)) return 1e-12;
+      rayleigh = S(sl::PNEXT);
+      if (I(il::SETTLED)) break;
+    }
+    return std::max(rayleigh, 1e-12);
+  }
+};
+
+namespace {
+
+// Trace bookkeeping shared by the loops (solvers.hpp:151-169).
+struct Loop {
+  Engine& e;
+  Report& rep;
+  const double* weight;
+  double t0;
+  void push_trace(int s) {
+    rep.residual_trace.push_back(e.S(s * sl::kStateStride + sl::RESID));
+    rep.fbe_trace.push_back(e.S(s * sl::kStateStride + sl::VALUE));
+  }
+  void refresh_tail(int s) {
+    e.read_scalars();
+    rep.residual_trace.back() = e.S(s * sl::kStateStride + sl::RESID);
+    rep.fbe_trace.back() = e.S(s * sl::kStateStride + sl::VALUE);
+  }
+  void finish(int status, int s, double residual, double lambda) {
+    rep.status = status;
+    rep.residual_inf = residual;
+    rep.lambda_final = lambda;
+    const Layout& L = e.d.lay;
+    rep.x.resize(static_cast<size_t>(L.nx) * L.n);
+    rep.u.resize(static_cast<size_t>(L.nu) * L.first_leaf);
+    rep.y.resize(static_cast<size_t>(L.dual_dim));
+    rep.z.resize(static_cast<size_t>(L.dual_dim));
+    auto dl = [&](std::vector<double>& dst, const double* src) {
+      if (!dst.empty())
+        SCN_CUDA(cudaMemcpyAsync(dst.data(), src, dst.size() * sizeof(double), cudaMemcpyDeviceToHost, e.st));
+    };
+    dl(rep.x, e.k.x[s]);
+    dl(rep.u, e.k.u[s]);
+    dl(rep.y, e.k.y[s]);
+    dl(rep.z, e.k.z[s]);
+    SCN_CUDA(cudaStreamSynchronize(e.st));
+    rep.wall_ms = now_ms() - t0;
+  }
+};
+
+double resolve_lambda0(Engine& e, const scenopt_solver_config& cfg, int kind, Report& rep) {
+  // solvers.hpp:129-138
+  if (cfg.lambda0 > 0.0) return cfg.lambda0;
+  rep.lipschitz_estimate = e.lipschitz(&rep.lipschitz_calls);
+  const bool fixed = kind == 2 || cfg.backtracking_rule == 2;
+  return (fixed ? 0.95 : 0.9) / rep.lipschitz_estimate;
+}
+
+// solve_minfbe, solvers.hpp:234-356
+Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y0dev, const double* weight) {
+  validate_config(cfg);
+  Report rep;
+  Loop lp{e, rep, weight, now_ms()};
+  rep.eps = cfg.eps;
+  double lambda = resolve_lambda0(e, cfg, 0, rep);
+  e.lbfgs_reset(cfg.memory);
+  auto& k = e.k;
+  const size_t D = e.D();
+  int cur = 0;
+  e.fb_step(cur, y0dev, lambda, weight, rep.stats);
+  bool grad_valid = false, have_pair = false, fresh = true;
+  int iter = 0;
+  for (;;) {
+    e.read_scalars();
+    const double residual = e.S(cur * sl::kStateStride + sl::RESID);
+    if (fresh) {
+      lp.push_trace(cur);
+      fresh = false;
+    }
+    if (residual <= cfg.eps) {
+      rep.iterations = iter;
+      lp.finish(0, cur, residual, lambda);
+      return rep;
+    }
+    if (iter >= cfg.max_iters) {
+      rep.iterations = iter;
+      lp.finish(1, cur, residual, lambda);
+      return rep;
+    }
+    if (!grad_valid) {  // fbe_grad (fbe.hpp:89-94)
+      e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
+      ++rep.stats.hessian_vec_calls;
+      SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, k.grad, e.st));
+      grad_valid = true;
+    }
+    if (cfg.backtracking_rule == 1) {  // simple rule (solvers.hpp:279-302)
+      bool halved = false;
+      for (;;) {
+        e.read_scalars();
+        const bool trigger = lambda * std::sqrt(e.S(sl::IMG2)) > cfg.eps_bt * std::sqrt(e.S(sl::R2));
+        if (!trigger) break;
+        lambda = halve_lambda(lambda);
+        e.lbfgs_clear();
+        have_pair = false;
+        e.rescale(cur, lambda, weight, rep.stats);
+        e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
+        ++rep.stats.hessian_vec_calls;
+        SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, k.grad, e.st));
+        halved = true;
+      }
+      if (halved) {
+        lp.refresh_tail(cur);
+        continue;
+      }
+    }
+    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], k.prev_y, k.grad,
+                     k.prev_g, k.grad, k.dir, k.Sb, k.Qb, e.st));
+    have_pair = false;
+    e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
+    ++rep.stats.hessian_vec_calls;
+    const int nxt = cur ^ 1;
+    SCN_CUDA(k_cert_search(e.ctx(), cur, 0, 1, k.y[cur], k.R[cur], k.Hx[cur], k.HR, k.dir, k.Hd, k.y[nxt],
+                           e.st));
+    e.read_scalars();
+    if (e.S(sl::STALL) != 0.0) {
+      rep.stats.prox_calls += 61;
+      rep.stats.conj_calls += 61;
+      fail(SCENOPT_E_LINE_SEARCH_STALLED, "no step in {2^-nu, nu <= 60} decreases the envelope");
+    }
+    const uint64_t trials = static_cast<uint64_t>(e.S(sl::KSTAR)) + 1;
+    rep.stats.prox_calls += trials;
+    rep.stats.conj_calls += trials;
+    const double cert_fhat = e.S(sl::CERT_FHAT), hxw_rw = e.S(sl::HXW_RW), rw2 = e.S(sl::RW2);
+    e.fb_step(nxt, k.y[nxt], lambda, weight, rep.stats);
+    if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:329-346)
+      e.read_scalars();
+      const double model = cert_fhat + lambda * hxw_rw + 0.5 * (1.0 - cfg.beta_bt) * lambda * rw2;
+      if (e.S(nxt * sl::kStateStride + sl::FHAT) > model) {
+        lambda = halve_lambda(lambda);
+        e.lbfgs_clear();
+        have_pair = false;
+        e.rescale(cur, lambda, weight, rep.stats);
+        lp.refresh_tail(cur);
+        grad_valid = false;
+        continue;
+      }
+    }
+    e.copy(k.prev_y, k.y[cur], D);
+    e.copy(k.prev_g, k.grad, D);
+    grad_valid = false;
+    have_pair = true;
+    cur = nxt;
+    ++iter;
+    fresh = true;
+  }
+}
+
+// solve_nama, solvers.hpp:362-492
+Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0dev, const double* weight) {
+  validate_config(cfg);
+  Report rep;
+  Loop lp{e, rep, weight, now_ms()};
+  rep.eps = cfg.eps;
+  double lambda = resolve_lambda0(e, cfg, 1, rep);
+  e.lbfgs_reset(cfg.memory);
+  auto& k = e.k;
+  const size_t D = e.D();
+  int cur = 0;
+  e.fb_step(cur, y0dev, lambda, weight, rep.stats);
+  bool have_pair = false, fresh = true;
+  int iter = 0;
+  for (;;) {
+    e.read_scalars();
+    const double residual = e.S(cur * sl::kStateStride + sl::RESID);
+    if (fresh) {
+      lp.push_trace(cur);
+      fresh = false;
+    }
+    if (residual <= cfg.eps) {
+      rep.iterations = iter;
+      lp.finish(0, cur, residual, lambda);
+      return rep;
+    }
+    if (iter >= cfg.max_iters) {
+      rep.iterations = iter;
+      lp.finish(1, cur, residual, lambda);
+      return rep;
+    }
+    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], k.prev_y, k.R[cur],
+                     k.prev_g, k.R[cur], k.dir, k.Sb, k.Qb, e.st));
+    have_pair = false;
+    // the two homogeneous images x0(r), x0(d): one 2-RHS sweep when the
+    // parallel line search is on (p-NAMA), two sweeps otherwise; the
+    // arithmetic is identical either way (solvers.hpp:410-422)
+    if (cfg.nama_parallel_linesearch)
+      e.sweep2(k.R[cur], k.dir, k.HR, k.Hd);
+    else {
+      e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
+      e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
+    }
+    rep.stats.hessian_vec_calls += 2;
+    const int nxt = cur ^ 1;
+    SCN_CUDA(k_cert_search(e.ctx(), cur, 1, cfg.nama_update_tlambda ? 1 : 0, k.y[cur], k.R[cur], k.Hx[cur],
+                           k.HR, k.dir, k.Hd, k.y[nxt], e.st));
+    e.read_scalars();
+    if (cfg.backtracking_rule == 1) {  // simple rule (solvers.hpp:424-438)
+      const bool trigger = lambda * std::sqrt(e.S(sl::HR2)) > cfg.eps_bt * std::sqrt(e.S(sl::RR2));
+      if (trigger) {
+        lambda = halve_lambda(lambda);
+        e.lbfgs_clear();
+        have_pair = false;
+        e.rescale(cur, lambda, weight, rep.stats);
+        lp.refresh_tail(cur);
+        continue;
+      }
+    }
+    rep.stats.prox_calls += 1;  // shifted anchor (fbe.hpp:192-197)
+    rep.stats.conj_calls += 1;
+    if (e.S(sl::STALL) != 0.0) {
+      rep.stats.prox_calls += 61;
+      rep.stats.conj_calls += 61;
+      fail(SCENOPT_E_LINE_SEARCH_STALLED, "no step in {2^-nu, nu <= 60} decreases the envelope");
+    }
+    const uint64_t trials = static_cast<uint64_t>(e.S(sl::KSTAR)) + 1;
+    rep.stats.prox_calls += trials;
+    rep.stats.conj_calls += trials;
+    const double cert_fhat = e.S(sl::CERT_FHAT), hxw_rw = e.S(sl::HXW_RW), rw2 = e.S(sl::RW2);
+    e.fb_step(nxt, k.y[nxt], lambda, weight, rep.stats);
+    if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:467-483)
+      e.read_scalars();
+      const double model = cert_fhat + lambda * hxw_rw + 0.5 * (1.0 - cfg.beta_bt) * lambda * rw2;
+      if (e.S(nxt * sl::kStateStride + sl::FHAT) > model) {
+        lambda = halve_lambda(lambda);
+        e.lbfgs_clear();
+        have_pair = false;
+        e.rescale(cur, lambda, weight, rep.stats);
+        lp.refresh_tail(cur);
+        continue;
+      }
+    }
+    e.copy(k.prev_y, k.y[cur], D);
+    e.copy(k.prev_g, k.R[cur], D);  // prev_res
+    have_pair = true;
+    cur = nxt;
+    ++iter;
+    fresh = true;
+  }
+}
+
+// solve_gpad, solvers.hpp:498-540
+Report solve_gpad(Engine& e, const scenopt_solver_config& cfg, const double* y0dev, const double* weight) {
+  validate_config(cfg);
+  Report rep;
+  Loop lp{e, rep, weight, now_ms()};
+  rep.eps = cfg.eps;
+  const double lambda = resolve_lambda0(e, cfg, 2, rep);
+  auto& k = e.k;
+  const size_t D = e.D();
+  e.copy(k.yp, y0dev, D);
+  double t = 1.0;
+  int cur = 0;
+  e.fb_step(cur, y0dev, lambda, weight, rep.stats);
+  int iter = 0;
+  for (;;) {
+    e.read_scalars();
+    const double residual = e.S(cur * sl::kStateStride + sl::RESID);
+    lp.push_trace(cur);
+    if (residual <= cfg.eps) {
+      rep.iterations = iter;
+      lp.finish(0, cur, residual, lambda);
+      return rep;
+    }
+    if (iter >= cfg.max_iters) {
+      rep.iterations = iter;
+      lp.finish(1, cur, residual, lambda);
+      return rep;
+    }
+    const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+    SCN_CUDA(k_extrapolate(e.ctx(), k.T[cur], k.yp, k.w, (t - 1.0) / t_next, e.st));
+    t = t_next;
+    const int nxt = cur ^ 1;
+    e.fb_step(nxt, k.w, lambda, weight, rep.stats);
+    cur = nxt;
+    ++iter;
+  }
+}
+
+// warm_start, solvers.hpp:545-564: GPAD iterations from zero; result in k.tmp2
+void warm_start(Engine& e, const scenopt_solver_config& cfg, double lambda, Stats& stats) {
+  auto& k = e.k;
+  const size_t D = e.D();
+  SCN_CUDA(cudaMemsetAsync(k.tmp2, 0, D * sizeof(double), e.st));
+  if (cfg.warm_start_iters <= 0) return;
+  if (!(lambda > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "warm_start: lambda must be > 0");
+  SCN_CUDA(cudaMemsetAsync(k.w, 0, D * sizeof(double), e.st));
+  double t = 1.0;
+  for (int it = 0; it < cfg.warm_start_iters; ++it) {
+    e.fb_step(0, k.w, lambda, nullptr, stats);
+    const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+    // w = T + mom (T - y); y = T
+    SCN_CUDA(k_extrapolate(e.ctx(), k.T[0], k.tmp2, k.w, (t - 1.0) / t_next, e.st));
+    t = t_next;
+  }
+  SCN_CUDA(cudaStreamSynchronize(e.st));
+}
+
+Report dispatch(Engine& e, const scenopt_solver_config& cfg, int kind, const double* y0dev,
+                const double* weight) {
+  switch (kind) {
+    case 0:
+      return solve_minfbe(e, cfg, y0dev, weight);
+    case 1:
+      return solve_nama(e, cfg, y0dev, weight);
+    case 2:
+      return solve_gpad(e, cfg, y0dev, weight);
+  }
+  fail(SCENOPT_E_INVALID_PARAMS, "unknown solver kind");
+}
+
+// verify_report, solvers.hpp:630-639, on a handle of the problem to verify
+void verify(scenopt_dev& h, Report& rep) {
+  Engine e(h);
+  auto& k = e.k;
+  const Layout& L = e.d.lay;
+  const size_t D = static_cast<size_t>(L.dual_dim);
+  SCN_CUDA(cudaMemcpyAsync(k.x[0], rep.x.data(), rep.x.size() * sizeof(double), cudaMemcpyHostToDevice, e.st));
+  if (!rep.u.empty())
+    SCN_CUDA(cudaMemcpyAsync(k.u[0], rep.u.data(), rep.u.size() * sizeof(double), cudaMemcpyHostToDevice, e.st));
+  SCN_CUDA(cudaMemcpyAsync(k.y[0], rep.y.data(), D * sizeof(double), cudaMemcpyHostToDevice, e.st));
+  SCN_CUDA(cudaMemcpyAsync(k.z[0], rep.z.data(), D * sizeof(double), cudaMemcpyHostToDevice, e.st));
+  SCN_CUDA(k_apply_H(e.d.hrows, k.x[0], k.u[0], k.Hx[0], e.st));
+  SCN_CUDA(k_max_abs_diff(e.ctx(), k.z[0], k.Hx[0], e.st));
+  e.read_scalars();
+  rep.verify_residual_inf = e.S(sl::RED0);
+  SCN_CUDA(k_dist_subdiff(e.ctx(), k.y[0], k.z[0], e.st));
+  e.read_scalars();
+  rep.verify_subdiff_dist = e.S(sl::RED0);
+  const double slop = 1.0 + 1e-9;
+  rep.verified = rep.status == 0 && rep.verify_residual_inf <= rep.eps * slop &&
+                 rep.verify_subdiff_dist <= rep.lambda_final * rep.eps * slop;
+}
+
+}  // namespace
+
+struct scenopt_report {
+  Report r;
+};
+static const Problem* scenopt_problem_ptr(const scenopt_problem* p) { return &p->p; }
+static const Factor* scenopt_factor_ptr(const scenopt_factor* f) { return &f->f; }
+struct scenopt_lbfgs {
+  scenopt_dev* h;
+  int n, mem;
+  double eps_curv;
+  DualCtx c;
+  double *Sb, *Qb, *g, *out, *a, *b, *cc, *dd;
+};
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" {
+
+int scenopt_fhat_value(scenopt_dev* h, const double* y, double* out, int flags) {
+  SCN_GUARD({
+    Engine e(*h);
+    const double* yd = h->in_dual(y, flags, 0);
+    e.sweep1(true, yd, e.k.x[1], e.k.u[1], e.k.Hx[1]);
+    ++h->stats.dual_grad_calls;
+    SCN_CUDA(k_eval_f(e.ctx(), h->d->cost, e.k.x[1], e.k.u[1], 1e-8, e.st));
+    SCN_CUDA(k_dot(e.ctx(), e.k.Hx[1], yd, e.st));
+    e.read_scalars();
+    const double f = e.S(sl::EVALF_INF) != 0.0 ? std::numeric_limits<double>::infinity() : e.S(sl::EVALF);
+    *out = -e.S(sl::RED0) - f;  // tree_oracles.hpp:125-129
+  });
+}
+
+int scenopt_apply_H(scenopt_dev* h, const double* x, const double* u, double* z, int flags) {
+  SCN_GUARD({
+    Engine e(*h);
+    const Layout& L = h->d->lay;
+    const double *xd = x, *ud = u;
+    if (flags & SCENOPT_HOST_IO) {
+      SCN_CUDA(cudaMemcpyAsync(e.k.x[1], x, sizeof(double) * L.nx * L.n, cudaMemcpyHostToDevice, e.st));
+      if (L.first_leaf > 0)
+        SCN_CUDA(cudaMemcpyAsync(e.k.u[1], u, sizeof(double) * L.nu * L.first_leaf, cudaMemcpyHostToDevice, e.st));
+      xd = e.k.x[1];
+      ud = e.k.u[1];
+    }
+    double* zd = (flags & SCENOPT_HOST_IO) ? e.k.tmp : z;
+    SCN_CUDA(k_apply_H(h->d->hrows, xd, ud, zd, e.st));
+    h->out_copy(z, zd, static_cast<size_t>(L.dual_dim), flags);
+    h->sync();
+  });
+}
+
+int scenopt_prox_g(scenopt_dev* h, const double* v, double gamma_prox, double* out, int flags) {
+  SCN_GUARD({
+    if (!(gamma_prox > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "prox_g: gamma_prox must be > 0");
+    Engine e(*h);
+    const double* vd = h->in_dual(v, flags, 0);
+    double* od = (flags & SCENOPT_HOST_IO) ? e.k.tmp : out;
+    SCN_CUDA(k_prox(e.ctx(), vd, gamma_prox, od, e.st));
+    h->out_copy(out, od, e.D(), flags);
+    h->sync();
+  });
+}
+
+int scenopt_conj_value_g(scenopt_dev* h, const double* w, double* out, int flags) {
+  SCN_GUARD({
+    Engine e(*h);
+    SCN_CUDA(k_conj(e.ctx(), h->in_dual(w, flags, 0), e.st));
+    e.read_scalars();
+    *out = e.S(sl::RED0);
+  });
+}
+
+int scenopt_dist_subdiff_inf(scenopt_dev* h, const double* y, const double* z, double* out, int flags) {
+  SCN_GUARD({
+    Engine e(*h);
+    const double* yd = h->in_dual(y, flags, 0);
+    const double* zd = h->in_dual(z, flags, 1);
+    SCN_CUDA(k_dist_subdiff(e.ctx(), yd, zd, e.st));
+    e.read_scalars();
+    *out = e.S(sl::RED0);
+  });
+}
+
+int scenopt_fb_step(scenopt_dev* h, const double* y, double lambda, double* x, double* u, double* Hx,
+                    double* z, double* R, double* T, double* scalars, int flags) {
+  SCN_GUARD({
+    Engine e(*h);
+    auto& k = e.k;
+    e.fb_step(0, h->in_dual(y, flags, 0), lambda, nullptr, h->stats);
+    const Layout& L = h->d->lay;
+    h->out_copy(x, k.x[0], static_cast<size_t>(L.nx) * L.n, flags);
+    h->out_copy(u, k.u[0], static_cast<size_t>(L.nu) * L.first_leaf, flags);
+    h->out_copy(Hx, k.Hx[0], e.D(), flags);
+    h->out_copy(z, k.z[0], e.D(), flags);
+    h->out_copy(R, k.R[0], e.D(), flags);
+    h->out_copy(T, k.T[0], e.D(), flags);
+    e.read_scalars();
+    if (scalars) {
+      scalars[0] = e.S(sl::FHAT);
+      scalars[1] = e.S(sl::CONJ);
+      scalars[2] = e.S(sl::ZN2);
+      scalars[3] = e.S(sl::VALUE);
+    }
+  });
+}
+
+int scenopt_fbe_grad(scenopt_dev* h, const double* R, double lambda, double* grad, int flags) {
+  SCN_GUARD({
+    Engine e(*h);
+    auto& k = e.k;
+    const double* Rd = h->in_dual(R, flags, 0);
+    e.set_scalar(sl::LAM, lambda);
+    e.sweep1(false, Rd, nullptr, nullptr, k.HR);
+    ++h->stats.hessian_vec_calls;
+    SCN_CUDA(k_fbe_grad(e.ctx(), 0, Rd, k.HR, k.grad, e.st));
+    h->out_copy(grad, k.grad, e.D(), flags);
+    h->sync();
+  });
+}
+
+int scenopt_linesearch_cert(scenopt_dev* h, const double* y, const double* Hx, double lambda,
+                            const double* ss, const double* shift, const double* dir, int ntau,
+                            const double* taus, double* deltas, double* cs, double* cfh, double* w,
+                            double* Hx_w, double* z, double* R, double* T, int flags) {
+  SCN_GUARD({
+    if (!(lambda > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "linesearch_cert: lambda must be > 0");
+    if (ntau < 1 || ntau > 16) fail(SCENOPT_E_INVALID_PARAMS, "linesearch_cert: 1..16 taus");
+    Engine e(*h);
+    auto& k = e.k;
+    const size_t D = e.D();
+    const bool host = (flags & SCENOPT_HOST_IO) != 0;
+    auto in = [&](const double* src, double* dst) {
+      SCN_CUDA(cudaMemcpyAsync(dst, src, D * sizeof(double), host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                               e.st));
+    };
+    in(y, k.y[0]);
+    in(Hx, k.Hx[0]);
+    in(dir, k.dir);
+    e.set_scalar(sl::LAM, lambda);
+    e.set_scalar(sl::FHAT, ss[0]);
+    e.set_scalar(sl::CONJ, ss[1]);
+    e.set_scalar(sl::ZN2, ss[2]);
+    e.set_scalar(sl::VALUE, ss[3]);
+    e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
+    if (shift) {  // the kernel's shift is -lambda R: pass R = -shift / lambda
+      in(shift, k.tmp);
+      SCN_CUDA(k_scale(e.ctx(), static_cast<int>(D), -1.0 / lambda, k.tmp, 0.0, nullptr, k.R[0], e.st));
+      e.sweep1(false, k.R[0], nullptr, nullptr, k.HR);
+    }
+    double* dev_deltas = k.small;
+    double* dev_cfh = k.small + 16;
+    SCN_CUDA(k_cert_eval(e.ctx(), 0, shift ? 1 : 0, k.y[0], k.R[0], k.Hx[0], k.HR, k.dir, k.Hd, ntau, taus,
+                         dev_deltas, dev_cfh, k.z[1], k.Hx[1], k.T[1], k.R[1], k.grad, e.st));
+    SCN_CUDA(cudaStreamSynchronize(e.st));
+    std::vector<double> hd(static_cast<size_t>(ntau)), hc(static_cast<size_t>(ntau));
+    SCN_CUDA(cudaMemcpy(hd.data(), dev_deltas, ntau * sizeof(double), cudaMemcpyDeviceToHost));
+    SCN_CUDA(cudaMemcpy(hc.data(), dev_cfh, ntau * sizeof(double), cudaMemcpyDeviceToHost));
+    std::copy(hd.begin(), hd.end(), deltas);
+    if (cfh) std::copy(hc.begin(), hc.end(), cfh);
+    e.read_scalars();
+    if (cs) {
+      cs[0] = e.S(sl::ALPHA1);
+      cs[1] = e.S(sl::ALPHA2);
+      cs[2] = e.S(sl::CONJ_A);
+      cs[3] = e.S(sl::ZN2_A);
+      cs[4] = e.S(sl::VALUE_A);
+      cs[5] = e.S(sl::FHAT_A);
+    }
+    h->out_copy(w, k.z[1], D, flags);
+    h->out_copy(Hx_w, k.Hx[1], D, flags);
+    h->out_copy(z, k.T[1], D, flags);
+    h->out_copy(R, k.R[1], D, flags);
+    h->out_copy(T, k.grad, D, flags);
+    h->sync();
+  });
+}
+
+int scenopt_estimate_lipschitz(scenopt_dev* h, uint64_t* calls, double* out) {
+  SCN_GUARD({
+    Engine e(*h);
+    *out = e.lipschitz(calls);
+  });
+}
+
+int scenopt_dev_solve(scenopt_dev* h, const scenopt_solver_config* cfg, int kind, const double* y0,
+                      const double* weight, scenopt_report** out) {
+  SCN_GUARD({
+    validate_config(*cfg);
+    Engine e(*h);
+    const size_t D = e.D();
+    if (y0)
+      SCN_CUDA(cudaMemcpyAsync(e.k.tmp2, y0, D * sizeof(double), cudaMemcpyHostToDevice, e.st));
+    else
+      SCN_CUDA(cudaMemsetAsync(e.k.tmp2, 0, D * sizeof(double), e.st));
+    const double* wd = nullptr;
+    if (weight) {
+      SCN_CUDA(cudaMemcpyAsync(e.k.weight, weight, D * sizeof(double), cudaMemcpyHostToDevice, e.st));
+      wd = e.k.weight;
+    }
+    auto r = std::make_unique<scenopt_report>();
+    r->r = dispatch(e, *cfg, kind, e.k.tmp2, wd);
+    *out = r.release();
+  });
+}
+
+int scenopt_warm_start(scenopt_dev* h, const scenopt_solver_config* cfg, double lambda, double* y_out,
+                       uint64_t* dual_grad_calls) {
+  SCN_GUARD({
+    Engine e(*h);
+    Stats st;
+    warm_start(e, *cfg, lambda, st);
+    SCN_CUDA(cudaMemcpy(y_out, e.k.tmp2, e.D() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (dual_grad_calls) *dual_grad_calls = st.dual_grad_calls;
+  });
+}
+
+int scenopt_report_summary_get(const scenopt_report* rr, scenopt_report_summary* s) {
+  SCN_GUARD({
+    const Report& r = rr->r;
+    s->status = r.status;
+    s->iterations = r.iterations;
+    s->verified = r.verified ? 1 : 0;
+    s->trace_len = static_cast<int32_t>(r.residual_trace.size());
+    s->dual_grad_calls = r.stats.dual_grad_calls;
+    s->hessian_vec_calls = r.stats.hessian_vec_calls;
+    s->prox_calls = r.stats.prox_calls;
+    s->conj_calls = r.stats.conj_calls;
+    s->lipschitz_calls = r.lipschitz_calls;
+    s->lipschitz_estimate = r.lipschitz_estimate;
+    s->lambda_final = r.lambda_final;
+    s->eps = r.eps;
+    s->residual_inf = r.residual_inf;
+    s->wall_ms = r.wall_ms;
+    s->verify_residual_inf = r.verify_residual_inf;
+    s->verify_subdiff_dist = r.verify_subdiff_dist;
+  });
+}
+
+int scenopt_report_arrays(const scenopt_report* rr, double* x, double* u, double* y, double* z, double* rt,
+                          double* ft) {
+  SCN_GUARD({
+    const Report& r = rr->r;
+    auto cp = [](const std::vector<double>& v, double* dst) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    };
+    cp(r.x, x);
+    cp(r.u, u);
+    cp(r.y, y);
+    cp(r.z, z);
+    cp(r.residual_trace, rt);
+    cp(r.fbe_trace, ft);
+  });
+}
+
+void scenopt_report_destroy(scenopt_report* r) { delete r; }
+
+// ------------------------------------------------------------------ L-BFGS handle (lbfgs.hpp)
+int scenopt_lbfgs_create(scenopt_dev* h, int memory, double eps_curv, scenopt_lbfgs** out) {
+  SCN_GUARD({
+    if (memory < 1) fail(SCENOPT_E_INVALID_PARAMS, "LbfgsBuffer: memory must be >= 1");
+    if (memory > 48) fail(SCENOPT_E_INVALID_PARAMS, "LbfgsBuffer: memory must be <= 48 on the device");
+    if (!(eps_curv > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "LbfgsBuffer: eps_curv must be > 0");
+    auto b = std::make_unique<scenopt_lbfgs>();
+    b->h = h;
+    b->n = 0;
+    b->mem = memory;
+    b->eps_curv = eps_curv;
+    DevState& d = *h->d;
+    SCN_CUDA(cudaSetDevice(d.device));
+    b->c = h->w->ctx(d);
+    b->c.S = d.alloc<double>(sl::kScalars);
+    b->c.I = d.alloc<int>(il::kInts);
+    b->c.part = d.alloc<double>(static_cast<size_t>(2) * 64 * b->c.nblk);
+    b->c.bar = d.alloc<unsigned>(4);
+    SCN_CUDA(cudaMemset(b->c.S, 0, sl::kScalars * sizeof(double)));
+    SCN_CUDA(cudaMemset(b->c.bar, 0, 4 * sizeof(unsigned)));
+    std::vector<int> ints(il::kInts, 0);
+    for (int j = 0; j <= memory; ++j) ints[il::LB_ORDER + j] = j;
+    SCN_CUDA(cudaMemcpy(b->c.I, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
+    const double one = 1.0;
+    SCN_CUDA(cudaMemcpy(b->c.S + sl::GAMMA0, &one, sizeof(double), cudaMemcpyHostToDevice));
+    b->Sb = b->Qb = b->g = b->out = b->a = b->b = b->cc = b->dd = nullptr;
+    *out = b.release();
+  });
+}
+
+namespace {
+void lb_ensure(scenopt_lbfgs* b, int n) {
+  if (b->n == n) return;
+  if (b->n != 0) fail(SCENOPT_E_DIMENSION_MISMATCH, "LbfgsBuffer: vector length changed");
+  DevState& d = *b->h->d;
+  b->n = n;
+  b->c.D = n;
+  b->Sb = d.alloc<double>(static_cast<size_t>(b->mem + 1) * n);
+  b->Qb = d.alloc<double>(static_cast<size_t>(b->mem + 1) * n);
+  for (double** p : {&b->g, &b->out, &b->a, &b->b, &b->cc, &b->dd}) *p = d.alloc<double>(n);
+  SCN_CUDA(cudaMemset(b->b, 0, n * sizeof(double)));
+  SCN_CUDA(cudaMemset(b->dd, 0, n * sizeof(double)));
+}
+}  // namespace
+
+int scenopt_lbfgs_push(scenopt_lbfgs* b, int n, const double* step, const double* change, double scale_ref) {
+  try {
+    SCN_CUDA(cudaSetDevice(b->h->d->device));
+    lb_ensure(b, n);
+    cudaStream_t st = b->h->d->stream;
+    // push(step, change, scale_ref) (lbfgs.hpp:33-44): s = step - 0,
+    // q = change - 0 with an explicit scale_ref for the curvature gate.
+    SCN_CUDA(cudaMemcpyAsync(b->a, step, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    SCN_CUDA(cudaMemcpyAsync(b->cc, change, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    SCN_CUDA(k_lbfgs(b->c, b->mem, b->eps_curv, scale_ref, 1, b->a, b->b, b->cc, b->dd, b->a, b->out, b->Sb,
+                     b->Qb, st));
+    int pushed = 0;
+    SCN_CUDA(cudaMemcpyAsync(&pushed, b->c.I + il::LB_PUSHED, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SCN_CUDA(cudaStreamSynchronize(st));
+    return pushed;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  }
+}
+
+int scenopt_lbfgs_apply(scenopt_lbfgs* b, int n, const double* grad, double* out) {
+  SCN_GUARD({
+    SCN_CUDA(cudaSetDevice(b->h->d->device));
+    lb_ensure(b, n);
+    cudaStream_t st = b->h->d->stream;
+    SCN_CUDA(cudaMemcpyAsync(b->g, grad, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    SCN_CUDA(k_lbfgs(b->c, b->mem, b->eps_curv, -1.0, 0, nullptr, nullptr, nullptr, nullptr, b->g, b->out, b->Sb, b->Qb, st));
+    SCN_CUDA(cudaMemcpyAsync(out, b->out, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SCN_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int scenopt_lbfgs_clear(scenopt_lbfgs* b) {
+  SCN_GUARD({
+    const int zero = 0;
+    const double one = 1.0;
+    SCN_CUDA(cudaMemcpy(b->c.I + il::LB_COUNT, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    SCN_CUDA(cudaMemcpy(b->c.S + sl::GAMMA0, &one, sizeof(double), cudaMemcpyHostToDevice));
+  });
+}
+
+int scenopt_lbfgs_size(const scenopt_lbfgs* b) {
+  int c = 0;
+  if (cudaMemcpy(&c, b->c.I + il::LB_COUNT, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -20;
+  return c;
+}
+
+double scenopt_lbfgs_gamma0(const scenopt_lbfgs* b) {
+  double g = 0.0;
+  cudaMemcpy(&g, b->c.S + sl::GAMMA0, sizeof(double), cudaMemcpyDeviceToHost);
+  return g;
+}
+
+void scenopt_lbfgs_destroy(scenopt_lbfgs* b) { delete b; }
+
+// ------------------------------------------------------------------ solve() driver
+int scenopt_solve(const scenopt_problem* p, const scenopt_solver_config* cfg, int kind,
+                  const scenopt_factor* shared, int device, scenopt_report** out) {
+  SCN_GUARD({
+    validate_config(*cfg);
+    if (kind < 0 || kind > 2) fail(SCENOPT_E_INVALID_PARAMS, "unknown solver kind");
+    const double t0 = now_ms();
+    const Problem& prob = *scenopt_problem_ptr(p);
+    auto run = [&](scenopt_dev& h, const double* wdev) {
+      Engine e(h);
+      double lhat = 0.0;
+      uint64_t lhat_calls = 0;
+      scenopt_solver_config run_cfg = *cfg;
+      if (!(cfg->lambda0 > 0.0)) {  // solvers.hpp:673-679
+        lhat = e.lipschitz(&lhat_calls);
+        const bool fixed = kind == 2 || cfg->backtracking_rule == 2;
+        run_cfg.lambda0 = (fixed ? 0.95 : 0.9) / lhat;
+      }
+      Stats warm;
+      SCN_CUDA(cudaMemsetAsync(e.k.tmp2, 0, e.D() * sizeof(double), e.st));
+      if (cfg->warm_start) {
+        const double lam_ws = cfg->lambda0 > 0.0 ? cfg->lambda0 : 0.95 / lhat;
+        warm_start(e, *cfg, lam_ws, warm);
+      }
+      Report r = dispatch(e, run_cfg, kind, e.k.tmp2, wdev);
+      r.stats.dual_grad_calls += warm.dual_grad_calls;
+      r.stats.hessian_vec_calls += warm.hessian_vec_calls;
+      r.stats.prox_calls += warm.prox_calls;
+      r.stats.conj_calls += warm.conj_calls;
+      r.lipschitz_estimate = lhat;
+      r.lipschitz_calls = lhat_calls;
+      return r;
+    };
+    auto rep = std::make_unique<scenopt_report>();
+    if (!cfg->precondition) {
+      Factor local;
+      const Factor* f = shared ? scenopt_factor_ptr(shared) : nullptr;
+      if (!f) {
+        local = factor(prob);
+        f = &local;
+      }
+      scenopt_dev h;
+      h.d = dev_create(prob, f, device);
+      h.init_solver_buffers();
+      rep->r = run(h, nullptr);
+      verify(h, rep->r);
+    } else {
+      const Problem scaled = precondition(prob);
+      const Factor fs = factor(scaled);
+      const std::vector<double> roots = probability_roots(prob);
+      std::vector<double> weight(roots.size());
+      for (size_t i = 0; i < roots.size(); ++i) weight[i] = 1.0 / roots[i];
+      {
+        scenopt_dev h;
+        h.d = dev_create(scaled, &fs, device);
+        h.init_solver_buffers();
+        SCN_CUDA(cudaMemcpy(h.w->weight, weight.data(), weight.size() * sizeof(double), cudaMemcpyHostToDevice));
+        rep->r = run(h, h.w->weight);
+      }
+      for (size_t i = 0; i < rep->r.y.size(); ++i) rep->r.y[i] = rep->r.y[i] * roots[i];
+      for (size_t i = 0; i < rep->r.z.size(); ++i) rep->r.z[i] = rep->r.z[i] * weight[i];
+      scenopt_dev ho;  // factor-less handle of the original problem for verification
+      ho.d = dev_create(prob, nullptr, device);
+      ho.init_solver_buffers();
+      verify(ho, rep->r);
+    }
+    rep->r.wall_ms = now_ms() - t0;
+    *out = rep.release();
+  });
+}
+
+int scenopt_verify_report(const scenopt_problem* p, scenopt_report* r, const double* z_override, int device) {
+  SCN_GUARD({
+    const Problem& prob = *scenopt_problem_ptr(p);
+    if (z_override) std::copy(z_override, z_override + prob.dual_dim, r->r.z.begin());
+    scenopt_dev h;
+    h.d = dev_create(prob, nullptr, device);
+    h.init_solver_buffers();
+    verify(h, r->r);
+  });
+}
+
+}  // extern "C"

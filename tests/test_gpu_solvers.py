@@ -129,7 +129,10 @@ def test_backtracking_rules(gpu):
     rng = orc.Rng(1206)  # test_solvers.cpp:307-348
     halved = 0
     for rule in ("simple", "original", "simple", "original"):
-        po, prob = fixture(rng, feasible_box())
+        while True:  # an instance with active constraints (y* != 0)
+            po, prob = fixture(rng, mixed())
+            if orc.solve(po, orc.SolverConfig(), 0)["iterations"] > 0:
+                break
         lip = sup.dual_lipschitz_dense(orc.Factor(po))
         c, oc = cfgs(backtracking_rule=rule, lambda0=10.0 / lip)
         cache = so.factor(prob)

@@ -440,7 +440,11 @@ FactorCache factor(const ProblemInstance& prob) {
 
   for (int t = tree.num_stages - 1; t >= 0; --t) {
     const NodeRange rng = nodes_at(tree, t);
-    for (int i = rng.first; i < rng.past; ++i) {
+    // Nodes of one stage are independent (riccati.hpp:115-180 loops them in
+    // order); the oracle runs them on host threads to keep setup time
+    // bounded. Each node's arithmetic is the serial restatement below, so
+    // results are identical to a serial run.
+    auto node = [&](int i) {
       const auto si = static_cast<size_t>(i);
       const auto& kids = tree.children[si];
       Mat huu(nu, nu), hux(nu, nx), hxx(nx, nx);
@@ -519,7 +523,27 @@ FactorCache factor(const ProblemInstance& prob) {
       for (int j = 0; j < nx; ++j)
         for (int k = 0; k < nx; ++k) vq(k, j) = 0.5 * (value(k, j) + value(j, k));
       cache.value_quad[si] = vq;
+    };
+    const int cnt = rng.past - rng.first;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nth = static_cast<int>(std::min<unsigned>(hw, static_cast<unsigned>((cnt + 15) / 16)));
+    std::vector<std::string> errs(static_cast<size_t>(std::max(nth, 1)));
+    auto run = [&](int tix) {
+      try {
+        for (int i = rng.first + tix; i < rng.past; i += std::max(nth, 1)) node(i);
+      } catch (const Error& e) {
+        errs[static_cast<size_t>(tix)] = e.what();
+      }
+    };
+    if (nth <= 1) {
+      run(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (int tix = 0; tix < nth; ++tix) pool.emplace_back(run, tix);
+      for (auto& th : pool) th.join();
     }
+    for (const auto& e : errs)
+      if (!e.empty()) ORC_THROW(kNotStronglyConvex, e);
   }
   return cache;
 }

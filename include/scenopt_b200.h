@@ -112,6 +112,8 @@ typedef struct scenopt_dev_info {
   int32_t device, sm_count, grid_ctas, ctas_per_sm, slots, items_bw, items_fw, nodes_per_item_max;
   int64_t slot_bytes, matrix_bytes_bw, matrix_bytes_fw, device_bytes;
   int64_t sweep_bytes_hom, sweep_bytes_aff, sweep_bytes_hom2; /* algorithmic bytes per sweep */
+  int32_t cut_stage; /* stages >= cut_stage are owned per CTA as whole subtrees; -1: all global */
+  int32_t reserved;
 } scenopt_dev_info;
 
 typedef struct scenopt_problem scenopt_problem;

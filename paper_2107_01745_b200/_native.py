@@ -66,7 +66,7 @@ class DevInfoC(C.Structure):
         ("slot_bytes", C.c_int64), ("matrix_bytes_bw", C.c_int64),
         ("matrix_bytes_fw", C.c_int64), ("device_bytes", C.c_int64),
         ("sweep_bytes_hom", C.c_int64), ("sweep_bytes_aff", C.c_int64),
-        ("sweep_bytes_hom2", C.c_int64),
+        ("sweep_bytes_hom2", C.c_int64), ("cut_stage", C.c_int32), ("reserved", C.c_int32),
     ]
 
 

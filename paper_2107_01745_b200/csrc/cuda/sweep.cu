@@ -4,14 +4,18 @@
 // fused with apply_H (problem_data.hpp:144-162) as ONE persistent,
 // warp-specialised kernel.
 //
-// Schedule. Items (runs of same-stage nodes, layout.hpp) are numbered in
-// ticket order: backward items leaves -> root, then forward items root ->
-// leaves, so every dependency of an item has a smaller ticket. The grid is
-// co-resident (cooperative launch) and CTA b owns tickets b, b+G, b+2G, ...
-// processed in order: the smallest unfinished ticket always belongs to a CTA
-// that is working on it with all its dependencies done, so the scheme cannot
-// deadlock and needs no grid-wide barrier. Completion of a node is published
-// through an epoch-stamped flag (st.release / ld.acquire at gpu scope).
+// Schedule (built by device.cpp). Items are runs of same-stage nodes
+// (layout.hpp). Below a cut stage each CTA owns a contiguous group of whole
+// subtrees, so those items depend only on earlier items of the same CTA:
+// the producer waits on a shared-memory retire counter (CTA-scope
+// release/acquire, no gpu-scope traffic). The nodes above the cut are global
+// tickets dealt round-robin; their completion (and that of the subtree
+// roots they consume) is published through epoch-stamped per-node flags
+// (gpu-scope fence + flag store / ld.acquire). Every CTA processes its list
+// in rank order (backward leaves -> root, then forward root -> leaves) and
+// every dependency has a smaller rank, so the lowest-ranked unfinished item
+// can always proceed: no deadlock, no grid-wide barrier. The grid is
+// co-resident (cooperative launch).
 //
 // Every per-item step is latency-bound (measured on B200: L2 hit ~280
 // cycles, st.release ~760, dependent DFMA 8), so the kernel overlaps items
@@ -26,8 +30,9 @@
 //               vectors (stage FULL), compute every product from shared
 //               memory, and recycle the slot with one cp.async.bulk (TMA 1-D)
 //               of item k+nslot.
-//   warp 12     publisher: releases completion flags in ticket order, one
-//               gpu-scope fence per batch of finished items.
+//   warp 12     publisher: retires items in order (CTA-scope counter) and
+//               releases the flags of publishing items, one gpu-scope fence
+//               per batch of finished items.
 // Products are "dot columns" split over S in {1,2,4,8} threads (interleaved
 // 16-byte shared loads over padded columns + xor shuffles), for all
 // right-hand sides at once so a 2-RHS (p-NAMA) sweep reads each matrix once.
@@ -48,6 +53,8 @@ constexpr int kTeams = 2;
 constexpr int kProducers = 4;  // producer warps (== slots), warp p stages items k = p (mod 4)
 constexpr int kThreads = 32 * kProducers + kTeams * kTeam + 32;  // producers, teams, publisher
 constexpr int kTeamWarp0 = kProducers;
+constexpr int kStageQ = 8;  // staging ring depth (items staged ahead)
+constexpr int kDoneQ = 16;  // completion ring depth (publisher lag allowed)
 constexpr int kPublisherWarp = kProducers + kTeams * kTeam / 32;
 
 #ifdef SCN_SWEEP_PROFILE
@@ -55,6 +62,8 @@ constexpr int kPublisherWarp = kProducers + kTeams * kTeam / 32;
 // [2] prod dep spin [3] team slot-full wait [4] team stage-full wait
 // [5] team compute [6] team refill + publish back-pressure [7] publisher fence
 __device__ unsigned long long g_prof[16];
+__device__ int g_dbg;  // timing experiments only: bit0 ignore dependencies, bit1 skip compute
+#define DBG(bit) (g_dbg & (bit))
 #define PROF_T0() long long _pt = clock64()
 #define PROF_T1(slot)                                                                          \
   do {                                                                                         \
@@ -63,6 +72,7 @@ __device__ unsigned long long g_prof[16];
     _pt = _n;                                                                                  \
   } while (0)
 #else
+#define DBG(bit) 0
 #define PROF_T0() (void)0
 #define PROF_T1(slot) (void)0
 #endif
@@ -77,6 +87,14 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 }
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -161,14 +179,16 @@ __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, in
       const double* ys = P.y[r] + it.v0_lo;
       double* yd = st + r * it.v0_n;
       for (int i = lane; i < it.v0_n; i += 32) cp_async8(yd + i, ys + i);
-      const double* cs = P.contrib[r] + static_cast<int64_t>(it.v1_lo) * W;
-      double* cd = st + NRHS * it.v0_n + r * nc;
-      for (int i = lane; i < nc; i += 32) cp_async8(cd + i, cs + i);
+      if (!it.direct) {
+        const double* cs = P.contrib[r] + static_cast<int64_t>(it.v1_lo) * W;
+        double* cd = st + NRHS * it.v0_n + r * nc;
+        for (int i = lane; i < nc; i += 32) cp_async8(cd + i, cs + i);
+      }
     }
     if (P.affine) {
       const int na = it.count * W;
       const double* as = P.aff_bw + static_cast<int64_t>(it.first) * W;
-      double* ad = st + NRHS * (it.v0_n + nc);
+      double* ad = st + NRHS * (it.v0_n + (it.direct ? 0 : nc));
       for (int i = lane; i < na; i += 32) cp_async8(ad + i, as + i);
     }
   } else {
@@ -291,7 +311,7 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
   const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
   const double* Y = st;
   const double* Cn = st + NRHS * it.v0_n;
-  const double* AF = st + NRHS * (it.v0_n + it.v1_n * W);
+  const double* AF = st + NRHS * (it.v0_n + (it.direct ? 0 : it.v1_n * W));
   {  // phase A: short dot columns (len M or mN), child sums, affine terms
     const int ncols = leaf ? nx : W;
     const int ntasks = cnt * ncols;
@@ -310,11 +330,20 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
 #pragma unroll
         for (int r = 0; r < NRHS; ++r) acc[r] = fma(a, yv[r * it.v0_n + k], acc[r]);
       }
-      if (!leaf)
-        for (int k = 0; k < mc.nkid; ++k) {
+      if (!leaf) {
+        if (it.direct) {  // many children: read the published contributions from L2
+          for (int k = 0; k < mc.nkid; ++k) {
 #pragma unroll
-          for (int r = 0; r < NRHS; ++r) acc[r] += Cn[r * it.v1_n * W + (mc.kid0 + k) * W + j];
+            for (int r = 0; r < NRHS; ++r)
+              acc[r] += __ldcg(P.contrib[r] + static_cast<int64_t>(it.v1_lo + mc.kid0 + k) * W + j);
+          }
+        } else {
+          for (int k = 0; k < mc.nkid; ++k) {
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) acc[r] += Cn[r * it.v1_n * W + (mc.kid0 + k) * W + j];
+          }
         }
+      }
       const int ja = leaf ? nu + j : j;
       const double aff = P.affine ? AF[ni * W + ja] : 0.0;
 #pragma unroll
@@ -449,17 +478,20 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
 template <int NRHS>
 __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P, int mmax, int mNmax) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t full[kMaxSlots], sfull[kMaxSlots], sempty[kMaxSlots], done[kMaxSlots],
-      pdone[kMaxSlots];
+  __shared__ __align__(8) uint64_t full[kMaxSlots], sfull[kStageQ], sempty[kStageQ], done[kDoneQ],
+      pdone[kDoneQ];
   __shared__ __align__(16) Item sitem[kMaxSlots];
+  __shared__ __align__(16) int4 sdone[kDoneQ];  // {first, count, pass, publish} of finished items
   __shared__ unsigned s_epoch;
+  __shared__ int s_retired;  // items [0, s_retired) of this CTA are complete
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NS = P.nslot;  // matrix slots == staging slots (even, so a slot stays with one team)
+  const int NS = P.nslot;  // matrix slots (even, so a slot stays with one team)
   double* slots = smem;
-  double* stages = smem + static_cast<int64_t>(NS) * P.slot_doubles;
-  double* scratch = stages + static_cast<int64_t>(NS) * P.stage_doubles;  // per team
-  const int b = blockIdx.x, Gd = gridDim.x;
-  const int K = P.items_total > b ? (P.items_total - b + Gd - 1) / Gd : 0;
+  double* stages = smem + static_cast<int64_t>(NS) * P.slot_doubles;  // kStageQ staging areas
+  double* scratch = stages + static_cast<int64_t>(kStageQ) * P.stage_doubles;  // per team
+  const int b = blockIdx.x;
+  const Item* items = P.items + P.cta_off[b];
+  const int K = P.cta_off[b + 1] - P.cta_off[b];
 
   auto issue = [&](int k, const Item& it) {  // one thread
     const int s = k % NS;
@@ -471,12 +503,15 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile unsigned*>(P.ctrl) + 1u;
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 1);
-      mbar_init(&done[s], 1);
-      mbar_init(&pdone[s], 1);
+    s_retired = 0;
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    for (int q = 0; q < kStageQ; ++q) {
+      mbar_init(&sfull[q], 1);
+      mbar_init(&sempty[q], 1);
+    }
+    for (int q = 0; q < kDoneQ; ++q) {
+      mbar_init(&done[q], 1);
+      mbar_init(&pdone[q], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -484,26 +519,32 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   __syncthreads();
   const unsigned E = s_epoch;
   if (tid == 0)
-    for (int k = 0; k < NS && k < K; ++k) issue(k, P.items[b + static_cast<int64_t>(k) * Gd]);
+    for (int k = 0; k < NS && k < K; ++k) issue(k, items[k]);
 
   if (warp < kProducers) {
     // ------------------------------------------------------------ producers
-    // Producer warp p owns staging slot p (NS == kProducers): items k = p mod
-    // NS. For each it waits for the slot to be consumed, polls the item's
-    // dependency flags (ld.acquire), stages its vectors and arrives FULL.
-    // Four producers keep four of these latency-bound round trips in flight.
+    // Producer warp p stages items k = p (mod kProducers) into staging area
+    // q = k mod kStageQ (a ring twice as deep as the matrix slots, so staging
+    // runs ahead of slot recycling): wait for the area to be consumed, poll
+    // the item's dependency flags (ld.acquire), stage its vectors, arrive.
     const int p = warp;
-    for (int k = p; k < K; k += NS) {
-      const Item it = P.items[b + static_cast<int64_t>(k) * Gd];
+    for (int k = p; k < K; k += kProducers) {
+      const int q = k % kStageQ;
+      const Item it = items[k];
       PROF_T0();
-      if (k >= NS) mbar_wait(&sempty[p], static_cast<unsigned>((k / NS - 1) & 1));
+      if (k >= kStageQ) mbar_wait(&sempty[q], static_cast<unsigned>((k / kStageQ - 1) & 1));
       if (lane == 0 && p == 0) PROF_T1(0);
-      while (!flags_ready(dep_flags(P, it), it, E, lane)) __nanosleep(32);
+      if (!DBG(1)) {
+        if (it.ldep >= 0)
+          while (ld_acquire_cta(&s_retired) <= it.ldep) __nanosleep(16);
+        if (it.dep_lo < it.dep_hi)
+          while (!flags_ready(dep_flags(P, it), it, E, lane)) __nanosleep(32);
+      }
       if (lane == 0 && p == 0) PROF_T1(2);
-      stage_issue<NRHS>(P, it, stages + static_cast<int64_t>(p) * P.stage_doubles, lane);
+      stage_issue<NRHS>(P, it, stages + static_cast<int64_t>(q) * P.stage_doubles, lane);
       cp_async_wait_all();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sfull[p]);
+      if (lane == 0) mbar_arrive(&sfull[q]);
       if (lane == 0 && p == 0) PROF_T1(1);
     }
   } else if (warp < kPublisherWarp) {
@@ -515,56 +556,70 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       const int s = k % NS;
       const bool refill = k + NS < K;
       Item nxt{};
-      if (ttid == 0 && refill) nxt = P.items[b + static_cast<int64_t>(k + NS) * Gd];
+      if (ttid == 0 && refill) nxt = items[k + NS];
       PROF_T0();
       mbar_wait(&full[s], static_cast<unsigned>((k / NS) & 1));
       if (ttid == 0) PROF_T1(3);
-      mbar_wait(&sfull[s], static_cast<unsigned>((k / NS) & 1));
+      const int q = k % kStageQ;
+      mbar_wait(&sfull[q], static_cast<unsigned>((k / kStageQ) & 1));
       if (ttid == 0) PROF_T1(4);
       const Item it = sitem[s];
       const double* slot = slots + static_cast<int64_t>(s) * P.slot_doubles;
-      const double* st = stages + static_cast<int64_t>(s) * P.stage_doubles;
-      if (it.pass == 0)
+      const double* st = stages + static_cast<int64_t>(q) * P.stage_doubles;
+      if (DBG(2)) {
+      } else if (it.pass == 0)
         consume_backward<NRHS>(P, it, slot, st, tbuf, ttid, team);
       else
         consume_forward<NRHS>(P, it, slot, st, tbuf, ttid, team, mmax, mNmax);
       team_sync(team);
       if (ttid == 0) PROF_T1(5);
       if (ttid == 0) {
-        mbar_arrive(&sempty[s]);
+        mbar_arrive(&sempty[q]);
         fence_proxy_async();  // generic reads of the slot before the async-proxy refill
         if (refill) issue(k + NS, nxt);
-        // the publisher must have retired item k-NS before its DONE phase reuses
-        if (k >= NS) mbar_wait(&pdone[s], static_cast<unsigned>((k / NS - 1) & 1));
-        mbar_arrive(&done[s]);
+        // the publisher must have retired item k-kDoneQ before its DONE phase reuses
+        const int dq = k % kDoneQ;
+        if (k >= kDoneQ) mbar_wait(&pdone[dq], static_cast<unsigned>((k / kDoneQ - 1) & 1));
+        sdone[dq] = make_int4(it.first, it.count, it.pass, it.publish);
+        mbar_arrive(&done[dq]);
       }
       if (ttid == 0) PROF_T1(6);
     }
   }
   if (warp == kPublisherWarp) {
     // ------------------------------------------------------------ publisher
-    // Releases completion flags in ticket order; one gpu-scope fence covers
-    // every item finished since the previous one (the fence is the expensive
-    // part; it is cumulative over the teams' writes observed through DONE).
+    // Retires items in order. Items consumed by other CTAs get their flags
+    // released; one gpu-scope fence covers every item finished since the
+    // previous one (the fence is the expensive part; it is cumulative over
+    // the teams' writes observed through DONE). Local-only batches need just
+    // the CTA-scope release of the retire counter.
     int k = 0;
     while (k < K) {
-      mbar_wait(&done[k % NS], static_cast<unsigned>((k / NS) & 1));
+      mbar_wait(&done[k % kDoneQ], static_cast<unsigned>((k / kDoneQ) & 1));
       int j = k + 1;
       if (lane == 0)
-        while (j < K && j - k < NS && mbar_test(&done[j % NS], static_cast<unsigned>((j / NS) & 1))) ++j;
+        while (j < K && j - k < kDoneQ &&
+               mbar_test(&done[j % kDoneQ], static_cast<unsigned>((j / kDoneQ) & 1)))
+          ++j;
       j = __shfl_sync(0xffffffffu, j, 0);
       PROF_T0();
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      for (int q2 = k; q2 < j; ++q2) {
-        const Item it = P.items[b + static_cast<int64_t>(q2) * Gd];
-        unsigned* flags = it.pass == 0 ? P.bw_flag : P.fw_flag;
-        for (int i = lane; i < it.count; i += 32)
-          asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + it.first + i), "r"(E) : "memory");
+      bool pub = false;
+      for (int q2 = k; q2 < j; ++q2) pub |= sdone[q2 % kDoneQ].w != 0;
+      if (pub) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int q2 = k; q2 < j; ++q2) {
+          const int4 dn = sdone[q2 % kDoneQ];
+          if (!dn.w) continue;
+          unsigned* flags = dn.z == 0 ? P.bw_flag : P.fw_flag;
+          for (int i = lane; i < dn.y; i += 32)
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + dn.x + i), "r"(E) : "memory");
+        }
       }
       __syncwarp();
       if (lane == 0) {
+        st_release_cta(&s_retired, j);
         PROF_T1(7);
-        for (int q2 = k; q2 < j; ++q2) mbar_arrive(&pdone[q2 % NS]);
+        for (int q2 = k; q2 < j; ++q2) mbar_arrive(&pdone[q2 % kDoneQ]);
       }
       k = j;
     }
@@ -585,6 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 
 int sweep_threads() { return kThreads; }
 int sweep_teams() { return kTeams; }
+int sweep_stage_queue() { return kStageQ; }
 
 cudaError_t sweep_profile_read(unsigned long long* out, bool reset) {
 #ifdef SCN_SWEEP_PROFILE
@@ -622,6 +678,15 @@ cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mm
                          cudaStream_t stream) {
   SweepParams p = P;
   void* args[] = {&p, &mmax, &mNmax};
+#ifdef SCN_SWEEP_PROFILE
+  static int dbg_set = [] {
+    const char* e = getenv("SCN_DBG");
+    int v = e ? atoi(e) : 0;
+    cudaMemcpyToSymbol(g_dbg, &v, sizeof(int));
+    return 1;
+  }();
+  (void)dbg_set;
+#endif
   const void* fn = P.nrhs == 2 ? reinterpret_cast<const void*>(sweep_kernel<2>)
                                : reinterpret_cast<const void*>(sweep_kernel<1>);
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, dyn_smem, stream);

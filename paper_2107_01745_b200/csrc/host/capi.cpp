@@ -153,6 +153,8 @@ int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
     info->sweep_bytes_hom = d.bytes_hom;
     info->sweep_bytes_aff = d.bytes_aff;
     info->sweep_bytes_hom2 = d.bytes_hom2;
+    info->cut_stage = d.cut_stage;
+    info->reserved = 0;
   });
 }
 

@@ -135,33 +135,139 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     fws[c] = even(fw);
   }
 
-  // ---- items: runs of same-stage nodes, tickets = backward (leaves->root)
-  // then forward (root->leaves)
+  // ---- schedule. The grid is one co-resident CTA per SM. Below a cut stage
+  // with >= kMinSub*G nodes, every CTA owns a contiguous, byte-balanced group
+  // of whole subtrees: their items depend only on items of the same CTA
+  // (a shared-memory retire counter, no gpu-scope publication). The few
+  // nodes above the cut are dealt round-robin as global tickets whose
+  // dependencies are released through per-node flags. Each CTA's list is
+  // ordered by rank (backward leaves->root, then forward root->leaves), and
+  // every dependency has a smaller rank, so the schedule cannot deadlock.
+  d->grid = d->sm_count;
+  if (const int g = env_int("SCENOPT_GRID", 0)) d->grid = std::min(g, d->grid);  // experiments only
+  const int G = d->grid;
   const int64_t target = env_int("SCENOPT_ITEM_KB", 24) * 1024 / 8;
   const int cap = std::max(1, env_int("SCENOPT_ITEM_MAX_NODES", 32));
-  struct Run { int first, count, pass; };
-  std::vector<Run> runs;
-  auto group_stage = [&](int t, int pass, const std::vector<int64_t>& size) {
-    const int first = p.stage_offsets[t], past = p.stage_offsets[t + 1];
-    int i = first;
-    while (i < past) {
+  const int min_sub = env_int("SCENOPT_MIN_SUBTREES", 4);  // per CTA; 0 disables ownership
+  const int min_items = 8;  // independent items per stage and CTA (local dependency distance)
+  struct Run { int first, count, pass, ldep, gdep, publish; };
+  auto chunk = [&](int lo, int hi, int pass, int per_stage_min, std::vector<Run>& out) {
+    const std::vector<int64_t>& size = pass == 0 ? bws : fws;
+    const int cnt_all = hi - lo;
+    const int ncap = std::max(1, std::min(cap, (cnt_all + per_stage_min - 1) / std::max(1, per_stage_min)));
+    int i = lo;
+    while (i < hi) {
       int cnt = 0;
       int64_t tot = 0;
-      while (i + cnt < past && cnt < cap) {
+      while (i + cnt < hi && cnt < ncap) {
         const int64_t sz = size[i + cnt] + static_cast<int64_t>(sizeof(NodeMeta) / 8);
         if (cnt > 0 && tot + sz > target) break;
         tot += sz;
         ++cnt;
       }
-      runs.push_back(Run{i, cnt, pass});
+      out.push_back(Run{i, cnt, pass, -1, 0, 0});
       i += cnt;
     }
   };
-  for (int t = p.N; t >= 0; --t) group_stage(t, 0, bws);
-  const int nbw = static_cast<int>(runs.size());
-  for (int t = 0; t <= p.N; ++t) group_stage(t, 1, fws);
+  int cut = -1;
+  if (min_sub > 0)
+    for (int s = 1; s <= p.N; ++s)
+      if (p.stage_offsets[s + 1] - p.stage_offsets[s] >= min_sub * G) {
+        cut = s;
+        break;
+      }
+  const int top_end = cut < 0 ? p.N + 1 : cut;  // stages [0, top_end) are global
+  std::vector<Run> top_bw, top_fw;
+  for (int t = top_end - 1; t >= 0; --t) chunk(p.stage_offsets[t], p.stage_offsets[t + 1], 0, 1, top_bw);
+  for (int t = 0; t < top_end; ++t) chunk(p.stage_offsets[t], p.stage_offsets[t + 1], 1, 1, top_fw);
+  for (Run& r : top_bw) r.gdep = r.publish = 1;
+  for (Run& r : top_fw) r.gdep = r.publish = 1;
+  std::vector<std::vector<Run>> lists(static_cast<size_t>(G));
+  std::vector<std::vector<Run>> local_fw(static_cast<size_t>(G));
+  if (cut >= 0) {
+    // subtree byte totals (BFS numbering: parents precede children)
+    std::vector<int64_t> sub(static_cast<size_t>(n));
+    for (int c = 0; c < n; ++c) sub[c] = bws[c] + fws[c];
+    for (int c = n - 1; c >= 1; --c) sub[p.ancestor[c]] += sub[c];
+    const int r0 = p.stage_offsets[cut], r1 = p.stage_offsets[cut + 1];
+    int64_t total = 0;
+    for (int r = r0; r < r1; ++r) total += sub[r];
+    std::vector<int> bound(static_cast<size_t>(G) + 1, r1);
+    bound[0] = r0;
+    int64_t acc = 0;
+    int g = 1;
+    for (int r = r0; r < r1 && g < G; ++r) {
+      acc += sub[r];
+      while (g < G && acc * G >= total * g) bound[g++] = r + 1;
+    }
+    for (int gg = 0; gg < G; ++gg) {
+      // per-stage node range of the group, stages cut..N
+      std::vector<std::pair<int, int>> rng;
+      int lo = bound[gg], hi = bound[gg + 1];
+      for (int t = cut; t <= p.N; ++t) {
+        rng.emplace_back(lo, hi);
+        if (t < p.N && lo < hi) {
+          const int nlo = p.child_begin[lo], nhi = p.child_begin[hi - 1] + p.child_count[hi - 1];
+          lo = nlo;
+          hi = nhi;
+        } else if (t < p.N) {
+          lo = hi = 0;
+        }
+      }
+      for (int t = p.N; t >= cut; --t) {
+        const auto [a, b2] = rng[t - cut];
+        if (a < b2) chunk(a, b2, 0, min_items, lists[gg]);
+      }
+      for (Run& r : lists[gg])
+        if (p.node_stage[r.first] == cut) r.publish = 1;  // consumed by the global top
+      for (int t = cut; t <= p.N; ++t) {
+        const auto [a, b2] = rng[t - cut];
+        if (a < b2) chunk(a, b2, 1, min_items, local_fw[gg]);
+      }
+      for (Run& r : local_fw[gg])
+        if (p.node_stage[r.first] == cut) r.gdep = 1;  // parents above the cut
+    }
+  }
+  for (size_t i = 0; i < top_bw.size(); ++i) lists[i % G].push_back(top_bw[i]);
+  for (size_t i = 0; i < top_fw.size(); ++i) lists[i % G].push_back(top_fw[i]);
+  for (int gg = 0; gg < G; ++gg) lists[gg].insert(lists[gg].end(), local_fw[gg].begin(), local_fw[gg].end());
+  // local dependency indices
+  {
+    std::vector<int> bw_pos(static_cast<size_t>(n), -1), fw_pos(static_cast<size_t>(n), -1);
+    for (int gg = 0; gg < G; ++gg) {
+      for (int k = 0; k < static_cast<int>(lists[gg].size()); ++k) {
+        Run& r = lists[gg][k];
+        auto& pos = r.pass == 0 ? bw_pos : fw_pos;
+        if (!r.gdep && !(r.pass == 0 && r.first >= p.first_leaf)) {
+          int ld = -1;
+          const int last = r.first + r.count - 1;
+          if (r.pass == 0) {
+            for (int c = p.child_begin[r.first]; c < p.child_begin[last] + p.child_count[last]; ++c)
+              ld = std::max(ld, bw_pos[c]);
+          } else {
+            for (int a = p.ancestor[r.first]; a <= p.ancestor[last]; ++a) ld = std::max(ld, fw_pos[a]);
+          }
+          if (ld < 0) fail(SCENOPT_E_INVALID_PARAMS, "dev_create: internal schedule error (local dependency)");
+          r.ldep = ld;
+        }
+        for (int c = r.first; c < r.first + r.count; ++c) pos[c] = k;
+      }
+    }
+  }
+  std::vector<Run> runs;
+  std::vector<int32_t> cta_off(static_cast<size_t>(G) + 1, 0);
+  int nbw = 0;
+  for (int gg = 0; gg < G; ++gg) {
+    cta_off[gg] = static_cast<int32_t>(runs.size());
+    for (const Run& r : lists[gg]) {
+      runs.push_back(r);
+      nbw += r.pass == 0;
+    }
+  }
+  cta_off[G] = static_cast<int32_t>(runs.size());
   d->items_bw = nbw;
   d->items_fw = static_cast<int>(runs.size()) - nbw;
+  d->cut_stage = cut;
 
   std::vector<Item> items(runs.size());
   std::vector<int64_t> item_doubles(runs.size());
@@ -184,6 +290,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     const int last = ru.first + ru.count - 1;
     const bool leaf = ru.first >= p.first_leaf;
     it.leaf = leaf ? 1 : 0;
+    it.ldep = ru.ldep;
+    it.publish = ru.publish;
     int64_t stage = 0;
     if (ru.pass == 0) {
       if (leaf) {
@@ -199,7 +307,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         it.v1_lo = it.dep_lo;
         it.v1_n = it.dep_hi - it.dep_lo;
       }
-      stage = kMaxRhs * (static_cast<int64_t>(it.v0_n) + static_cast<int64_t>(it.v1_n) * W) +
+      it.direct = it.v1_n > 2 * ru.count ? 1 : 0;  // > 2 children per node on average
+      stage = kMaxRhs * (static_cast<int64_t>(it.v0_n) + (it.direct ? 0 : static_cast<int64_t>(it.v1_n) * W)) +
               static_cast<int64_t>(ru.count) * W;
     } else {
       if (ru.first == 0) {
@@ -217,6 +326,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
       stage = kMaxRhs * (static_cast<int64_t>(it.v0_n) * Vp + static_cast<int64_t>(it.v1_n) * nu) +
               static_cast<int64_t>(ru.count) * nx;
     }
+    if (!ru.gdep) it.dep_hi = it.dep_lo;  // dependencies inside the CTA: retire counter
     max_stage = std::max(max_stage, stage);
     max_item = std::max(max_item, tot);
     max_cnt = std::max(max_cnt, ru.count);
@@ -334,12 +444,13 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   const int dbl = 8;
   const int force_ns = env_int("SCENOPT_NSLOT", 0);
   const int teams = sweep_teams();
+  const int stageq = sweep_stage_queue();
   auto smem_for = [&](int ns) {
-    return (static_cast<size_t>(ns) * (d->slot_doubles + d->stage_doubles) +
+    return (static_cast<size_t>(ns) * d->slot_doubles + static_cast<size_t>(stageq) * d->stage_doubles +
             static_cast<size_t>(teams) * d->vec_doubles) * dbl;
   };
   int best_ns = 0;
-  for (int ns = 4; ns >= 4; ns -= 2) {  // one producer warp per slot (sweep.cu kProducers)
+  for (int ns = 4; ns >= 2; ns -= 2) {  // even: a slot stays with one consumer team
     if (force_ns && ns != force_ns) continue;
     const size_t smem = smem_for(ns);
     if (smem > static_cast<size_t>(prop.sharedMemPerBlockOptin)) continue;
@@ -357,8 +468,6 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->ctas_per_sm = 1;
   d->dyn_smem = smem_for(best_ns);
   SCN_CUDA(sweep_configure(d->dyn_smem));
-  d->grid = d->sm_count;
-  if (const int g = env_int("SCENOPT_GRID", 0)) d->grid = std::min(g, d->grid);  // experiments only
   d->G = 0;
 
   // ---- upload
@@ -372,6 +481,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->aff_fw = upload(*d, aff_fw);
   d->root_state = upload(*d, p.root_state);
   d->items = upload(*d, items);
+  d->cta_off = upload(*d, cta_off);
   d->ctrl = d->alloc<unsigned>(4);
   d->bw_flag = d->alloc<unsigned>(static_cast<size_t>(n));
   d->fw_flag = d->alloc<unsigned>(static_cast<size_t>(n));
@@ -522,6 +632,7 @@ void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, doubl
   P.nxp = d.nxp;
   P.Vp = d.Vp;
   P.items = d.items;
+  P.cta_off = d.cta_off;
   P.bw_blk = d.bw_blk;
   P.fw_blk = d.fw_blk;
   P.aff_bw = d.aff_bw;

@@ -47,6 +47,8 @@ struct DevState {
   double *bw_blk = nullptr, *fw_blk = nullptr, *aff_bw = nullptr, *aff_fw = nullptr,
          *root_state = nullptr;
   Item* items = nullptr;
+  int32_t* cta_off = nullptr;  // [grid + 1] per-CTA item ranges
+  int cut_stage = -1;          // subtree-ownership cut (-1: all items are global tickets)
   unsigned *ctrl = nullptr, *bw_flag = nullptr, *fw_flag = nullptr;
   int64_t bw_doubles = 0, fw_doubles = 0;
   int items_bw = 0, items_fw = 0, max_count = 1, max_m = 0, max_mN = 0, nxp = 0, Vp = 0;
@@ -94,6 +96,7 @@ void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, doubl
 
 // kernel launchers (cuda/*.cu)
 int sweep_teams();
+int sweep_stage_queue();
 cudaError_t sweep_configure(size_t dyn_smem);
 cudaError_t sweep_profile_read(unsigned long long* out, bool reset);
 cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem);

@@ -117,3 +117,39 @@ def test_oracle_errors_mirror_reference(gpu):
         so.dual_grad(cache, other, np.zeros(other.dual_dim))
     with pytest.raises(so.DimensionMismatch):
         so.hessian_vec(cache, prob, np.zeros(prob.dual_dim + 1))
+
+
+@pytest.mark.parametrize("grid,min_sub", [(4, 1), (8, 2), (16, 4), (3, 1), (16, 0)])
+def test_subtree_ownership_schedule_matches_oracle(gpu, monkeypatch, grid, min_sub):
+    """The per-CTA subtree schedule (local dependencies through the retire
+    counter, global flags above the cut) at several grid sizes and cuts, on
+    regular, irregular and random trees; the reduced grids force a cut on
+    trees small enough for the oracle."""
+    monkeypatch.setenv("SCENOPT_GRID", str(grid))
+    monkeypatch.setenv("SCENOPT_MIN_SUBTREES", str(min_sub))
+    rng = orc.Rng(900 + grid)
+    cases = [orc.Problem.from_flat(so.gen_random_instance(2, 6, 3, 9, [3, 1, 4, 2]).flat()),
+             orc.Problem.from_flat(so.gen_random_instance(4, 5, 2, 12, [2] * 7).flat()),
+             rng.random_instance(6, 300, 3, 2, orc.InstanceOptions(with_l1=True, with_none=True))]
+    for po in cases:
+        prob, cache, ofac = both(po)
+        info = cache.dev_info()
+        assert info["grid_ctas"] == grid
+        if min_sub == 0:
+            assert info["cut_stage"] == -1
+        y = rng.vector(prob.dual_dim, 1.5)
+        r = rng.vector(prob.dual_dim, 1.5)
+        for affine in (True, False):
+            pts, hs = so.sweep(cache, [y, r], affine)
+            for v, pt, h in ((y, pts[0], hs[0]), (r, pts[1], hs[1])):
+                ox, ou = ofac.sweep(v, affine)
+                assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL
+                Hx = orc.apply_H(po, ox, ou)
+                assert np.abs(h - Hx).max() <= TOL * (1 + np.abs(Hx).max())
+
+
+def test_default_grid_uses_subtree_ownership_on_c3(gpu):
+    prob = so.gen_random_instance(1, 50, 20, 20, [8, 8, 8, 2])  # BASELINE C3 shape
+    info = so.factor(prob).dev_info()
+    assert info["grid_ctas"] == info["sm_count"]
+    assert info["cut_stage"] == 4  # 1024 subtrees >= 4 per CTA

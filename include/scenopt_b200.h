@@ -211,8 +211,9 @@ int scenopt_linesearch_cert(scenopt_dev* d, const double* y, const double* Hx, d
                             double* T, int flags);
 
 /* ---- L-BFGS: lbfgs.hpp:22-84 (device-resident pairs) -------------------- */
-/* The buffer lives on d's device; vectors are host arrays of length n
- * (fixed by the first call). */
+/* The buffer lives on d's device (d == NULL: a standalone buffer on device
+ * 0, as LbfgsBuffer(memory, eps_curv) carries no problem); vectors are host
+ * arrays of length n (fixed by the first call). */
 int scenopt_lbfgs_create(scenopt_dev* d, int memory, double eps_curv, scenopt_lbfgs** out);
 int scenopt_lbfgs_push(scenopt_lbfgs* b, int n, const double* step, const double* change,
                        double scale_ref); /* 1 accepted, 0 rejected, <0 error */

@@ -58,6 +58,24 @@ namespace {
 void pack_common(DevState& d, const Problem& p);
 }
 
+std::unique_ptr<DevState> dev_create_bare(int device) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    fail(SCENOPT_E_NODEVICE, "scenopt: no CUDA device visible (the library has no CPU path)");
+  }
+  if (device < 0 || device >= ndev) fail(SCENOPT_E_NODEVICE, "scenopt: device index out of range");
+  cudaDeviceProp prop{};
+  SCN_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) fail(SCENOPT_E_NODEVICE, std::string("scenopt: device is ") + prop.name + "; this build targets sm_100a (B200)");
+  auto d = std::make_unique<DevState>();
+  d->device = device;
+  SCN_CUDA(cudaSetDevice(device));
+  SCN_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  d->sm_count = prop.multiProcessorCount;
+  return d;
+}
+
 std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int device) {
   if (fptr) check_factor_shape(*fptr, p, "dev_create");
   require_valid(p);

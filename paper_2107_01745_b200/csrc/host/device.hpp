@@ -86,6 +86,8 @@ struct DevState {
 
 // f == nullptr builds a factor-less handle (apply_H, eval_f, prox/conj,
 // verification) without the sweep layout.
+// Bare context (device, stream, SM count) for problem-free device objects.
+std::unique_ptr<DevState> dev_create_bare(int device);
 std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* f, int device);
 int device_count_sm100();
 

@@ -589,7 +589,9 @@ struct scenopt_report {
 static const Problem* scenopt_problem_ptr(const scenopt_problem* p) { return &p->p; }
 static const Factor* scenopt_factor_ptr(const scenopt_factor* f) { return &f->f; }
 struct scenopt_lbfgs {
-  scenopt_dev* h;
+  scenopt_dev* h;                   // owning solver handle, or NULL (standalone buffer)
+  std::unique_ptr<DevState> own;    // standalone: bare device context (device 0)
+  DevState* dev;
   int n, mem;
   double eps_curv;
   DualCtx c;
@@ -848,9 +850,20 @@ int scenopt_lbfgs_create(scenopt_dev* h, int memory, double eps_curv, scenopt_lb
     b->n = 0;
     b->mem = memory;
     b->eps_curv = eps_curv;
-    DevState& d = *h->d;
+    if (h) {
+      b->dev = h->d.get();
+    } else {  // LbfgsBuffer(memory, eps_curv) has no problem attached: own a bare context
+      b->own = dev_create_bare(0);
+      b->dev = b->own.get();
+    }
+    DevState& d = *b->dev;
     SCN_CUDA(cudaSetDevice(d.device));
-    b->c = h->w->ctx(d);
+    if (h) {
+      b->c = h->w->ctx(d);
+    } else {
+      b->c = DualCtx{};
+      b->c.nblk = d.sm_count;
+    }
     b->c.S = d.alloc<double>(sl::kScalars);
     b->c.I = d.alloc<int>(il::kInts);
     b->c.part = d.alloc<double>(static_cast<size_t>(2) * 64 * b->c.nblk);
@@ -871,7 +884,7 @@ namespace {
 void lb_ensure(scenopt_lbfgs* b, int n) {
   if (b->n == n) return;
   if (b->n != 0) fail(SCENOPT_E_DIMENSION_MISMATCH, "LbfgsBuffer: vector length changed");
-  DevState& d = *b->h->d;
+  DevState& d = *b->dev;
   b->n = n;
   b->c.D = n;
   b->Sb = d.alloc<double>(static_cast<size_t>(b->mem + 1) * n);
@@ -884,9 +897,9 @@ void lb_ensure(scenopt_lbfgs* b, int n) {
 
 int scenopt_lbfgs_push(scenopt_lbfgs* b, int n, const double* step, const double* change, double scale_ref) {
   try {
-    SCN_CUDA(cudaSetDevice(b->h->d->device));
+    SCN_CUDA(cudaSetDevice(b->dev->device));
     lb_ensure(b, n);
-    cudaStream_t st = b->h->d->stream;
+    cudaStream_t st = b->dev->stream;
     // push(step, change, scale_ref) (lbfgs.hpp:33-44): s = step - 0,
     // q = change - 0 with an explicit scale_ref for the curvature gate.
     SCN_CUDA(cudaMemcpyAsync(b->a, step, n * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -905,9 +918,9 @@ int scenopt_lbfgs_push(scenopt_lbfgs* b, int n, const double* step, const double
 
 int scenopt_lbfgs_apply(scenopt_lbfgs* b, int n, const double* grad, double* out) {
   SCN_GUARD({
-    SCN_CUDA(cudaSetDevice(b->h->d->device));
+    SCN_CUDA(cudaSetDevice(b->dev->device));
     lb_ensure(b, n);
-    cudaStream_t st = b->h->d->stream;
+    cudaStream_t st = b->dev->stream;
     SCN_CUDA(cudaMemcpyAsync(b->g, grad, n * sizeof(double), cudaMemcpyHostToDevice, st));
     SCN_CUDA(k_lbfgs(b->c, b->mem, b->eps_curv, -1.0, 0, nullptr, nullptr, nullptr, nullptr, b->g, b->out, b->Sb, b->Qb, st));
     SCN_CUDA(cudaMemcpyAsync(out, b->out, n * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -919,6 +932,7 @@ int scenopt_lbfgs_clear(scenopt_lbfgs* b) {
   SCN_GUARD({
     const int zero = 0;
     const double one = 1.0;
+    SCN_CUDA(cudaSetDevice(b->dev->device));
     SCN_CUDA(cudaMemcpy(b->c.I + il::LB_COUNT, &zero, sizeof(int), cudaMemcpyHostToDevice));
     SCN_CUDA(cudaMemcpy(b->c.S + sl::GAMMA0, &one, sizeof(double), cudaMemcpyHostToDevice));
   });
@@ -926,12 +940,14 @@ int scenopt_lbfgs_clear(scenopt_lbfgs* b) {
 
 int scenopt_lbfgs_size(const scenopt_lbfgs* b) {
   int c = 0;
+  if (cudaSetDevice(b->dev->device) != cudaSuccess) return -20;
   if (cudaMemcpy(&c, b->c.I + il::LB_COUNT, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return -20;
   return c;
 }
 
 double scenopt_lbfgs_gamma0(const scenopt_lbfgs* b) {
   double g = 0.0;
+  cudaSetDevice(b->dev->device);
   cudaMemcpy(&g, b->c.S + sl::GAMMA0, sizeof(double), cudaMemcpyDeviceToHost);
   return g;
 }

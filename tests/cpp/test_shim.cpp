@@ -1,0 +1,344 @@
+// SPDX-License-Identifier: MIT
+// Tests of the C++ drop-in layer (include/scenopt_b200.hpp), written against
+// the reference's API exactly as the reference's own Catch2 tests use it
+// (proj/tests/test_tree_oracles.cpp, test_fbe.cpp, test_lbfgs.cpp,
+// test_solvers.cpp). A minimal harness replaces Catch2 (not in the image).
+//   test_shim            all cases (needs an sm_100 device)
+//   test_shim --host     host-only cases (no device: layout, validation,
+//                        generators, errors)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "scenopt_b200.hpp"
+
+using scenopt::Vec;
+
+namespace {
+struct Case {
+  const char* name;
+  bool host;
+  std::function<void()> fn;
+};
+std::vector<Case>& cases() {
+  static std::vector<Case> c;
+  return c;
+}
+struct Reg {
+  Reg(const char* n, bool host, std::function<void()> f) { cases().push_back({n, host, std::move(f)}); }
+};
+int g_fail = 0;
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define TEST_CASE(name, host) \
+  static void CAT(tc_, __LINE__)(); \
+  static Reg CAT(reg_, __LINE__)(name, host, CAT(tc_, __LINE__)); \
+  static void CAT(tc_, __LINE__)()
+#define CHECK(cond)                                                              \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      std::printf("    CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);    \
+      ++g_fail;                                                                  \
+    }                                                                            \
+  } while (0)
+#define REQUIRE(cond)                                                            \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      std::printf("    REQUIRE failed %s:%d: %s\n", __FILE__, __LINE__, #cond);  \
+      ++g_fail;                                                                  \
+      return;                                                                    \
+    }                                                                            \
+  } while (0)
+#define CHECK_THROWS_AS(expr, type)                                              \
+  do {                                                                           \
+    bool ok_ = false;                                                            \
+    try {                                                                        \
+      (void)(expr);                                                              \
+    } catch (const type&) {                                                      \
+      ok_ = true;                                                                \
+    } catch (...) {                                                              \
+    }                                                                            \
+    if (!ok_) {                                                                  \
+      std::printf("    CHECK_THROWS_AS failed %s:%d: %s\n", __FILE__, __LINE__, #expr); \
+      ++g_fail;                                                                  \
+    }                                                                            \
+  } while (0)
+
+struct Rng {  // tests/support.hpp-style uniform draws
+  std::mt19937_64 gen;
+  explicit Rng(uint64_t s) : gen(s) {}
+  double uniform(double lo, double hi) { return std::uniform_real_distribution<double>(lo, hi)(gen); }
+  Vec vector(int n, double scale = 1.0) {
+    Vec v(n);
+    for (int i = 0; i < n; ++i) v(i) = uniform(-scale, scale);
+    return v;
+  }
+};
+
+double max_abs(const Vec& v) { return v.lpNormInf(); }
+Vec flat_x(const scenopt::PrimalPoint& p) { return p.flatten(); }
+
+scenopt::ProblemInstance small(uint64_t seed, int nx = 3, int nu = 2, int horizon = 3, int br = 2) {
+  return scenopt::gen_random_instance(seed, scenopt::RandomDims{nx, nu}, scenopt::RandomTreeShape{horizon, br});
+}
+}  // namespace
+
+// ---------------------------------------------------------------- host-only
+TEST_CASE("generated instances are valid and laid out like the reference", true) {
+  const auto prob = small(7, 3, 2, 3, 2);
+  CHECK(scenopt::validate(prob).empty());
+  CHECK(prob.num_nodes() == 15);
+  CHECK(prob.tree.first_leaf() == 7);
+  CHECK(prob.tree.stage_offsets == std::vector<int>({0, 1, 3, 7, 15}));  // test_scenario_tree.cpp:20-50
+  CHECK(prob.dual_offset[0] == -1 && prob.dual_offset[1] == 0);
+  int rows = 0;
+  for (int i = 1; i < prob.num_nodes(); ++i) rows += prob.stage_rows(i);
+  for (int l = 0; l < prob.tree.num_leaves(); ++l) rows += prob.terminal_rows(l);
+  CHECK(rows == prob.dual_dim);
+  CHECK(prob.primal_dim() == 7 * 2 + 14 * 3);
+  // equal seeds give identical instances (generators.hpp:247-249)
+  const auto again = small(7, 3, 2, 3, 2);
+  CHECK(again.con[5].F(1, 2) == prob.con[5].F(1, 2) && again.cost[9].Q(2, 1) == prob.cost[9].Q(2, 1));
+}
+
+TEST_CASE("validate reports broken instances", true) {
+  auto prob = small(8);
+  prob.tree.probability[1] = 0.9;  // children no longer sum to the parent
+  CHECK(!scenopt::validate(prob).empty());
+  auto bad = small(8);
+  bad.dyn[3].A = scenopt::Mat(2, 2);
+  const auto msgs = scenopt::validate(bad);
+  CHECK(!msgs.empty() && msgs.front().find("A must be") != std::string::npos);
+}
+
+TEST_CASE("preconditioning scales rows by square-root probabilities", true) {
+  const auto prob = small(9);
+  const auto pre = scenopt::precondition(prob);
+  const Vec roots = scenopt::probability_roots(prob);
+  CHECK(roots.size() == prob.dual_dim);
+  const int i = 4;
+  const double r = std::sqrt(prob.tree.probability[i]);
+  CHECK(std::abs(pre.con[i].F(0, 1) - r * prob.con[i].F(0, 1)) < 1e-15);
+  CHECK(std::abs(roots(prob.dual_offset[i]) - r) < 1e-15);
+}
+
+TEST_CASE("configuration and buffer parameters are validated", true) {
+  scenopt::SolverConfig cfg;
+  cfg.eps = 0.0;
+  CHECK_THROWS_AS(scenopt::validate_config(cfg), scenopt::InvalidParams);
+  cfg = {};
+  cfg.eps_bt = 0.5;
+  CHECK_THROWS_AS(scenopt::validate_config(cfg), scenopt::InvalidParams);
+  CHECK_THROWS_AS(scenopt::LbfgsBuffer(0, 1e-12), scenopt::InvalidParams);  // test_lbfgs.cpp:194
+  CHECK_THROWS_AS(scenopt::LbfgsBuffer(3, 0.0), scenopt::InvalidParams);
+  CHECK_THROWS_AS(scenopt::gen_random_instance(1, scenopt::RandomDims{0, 2}), scenopt::InvalidParams);
+}
+
+// ---------------------------------------------------------------- device
+TEST_CASE("dual_grad output is dynamics-feasible", false) {
+  Rng rng(41);
+  const auto prob = small(11, 4, 2, 4, 2);
+  const auto cache = scenopt::factor(prob);
+  for (int trial = 0; trial < 5; ++trial) {
+    const Vec y = rng.vector(prob.dual_dim, 2.0);
+    const auto pt = scenopt::dual_grad(cache, prob, y);
+    CHECK(max_abs(pt.x.col(0) - prob.root_state) < 1e-12);
+    for (int i = 1; i < prob.num_nodes(); ++i) {
+      const int a = prob.tree.ancestor[i];
+      const Vec res = pt.x.col(i) - prob.dyn[i].A * pt.x.col(a) - prob.dyn[i].B * pt.u.col(a) - prob.dyn[i].c;
+      CHECK(max_abs(res) < 1e-9 * (1.0 + max_abs(pt.x.col(i))));
+    }
+  }
+}
+
+TEST_CASE("hessian_vec is the homogeneous part of the affine solution map", false) {
+  Rng rng(43);  // test_tree_oracles.cpp:64-81
+  const auto prob = small(12, 3, 2, 4, 2);
+  const auto cache = scenopt::factor(prob);
+  for (int trial = 0; trial < 5; ++trial) {
+    const Vec y = rng.vector(prob.dual_dim, 2.0), r = rng.vector(prob.dual_dim, 2.0);
+    const Vec d = flat_x(scenopt::dual_grad(cache, prob, y + r)) - flat_x(scenopt::dual_grad(cache, prob, y));
+    const Vec h = flat_x(scenopt::hessian_vec(cache, prob, r));
+    REQUIRE(max_abs(d - h) < 1e-9 * (1.0 + max_abs(h)));
+  }
+}
+
+TEST_CASE("dual Hessian-vector products: exactness, symmetry, curvature sign", false) {
+  Rng rng(44);  // test_tree_oracles.cpp:83-109
+  const auto prob = small(13, 3, 2, 3, 3);
+  const auto cache = scenopt::factor(prob);
+  for (int trial = 0; trial < 5; ++trial) {
+    const Vec y = rng.vector(prob.dual_dim, 2.0), r = rng.vector(prob.dual_dim, 2.0);
+    const Vec lhs = scenopt::grad_fhat(cache, prob, y + r) - scenopt::grad_fhat(cache, prob, y);
+    const Vec rhs = -scenopt::apply_H(prob, scenopt::hessian_vec(cache, prob, r));
+    REQUIRE(max_abs(lhs - rhs) < 1e-9 * (1.0 + max_abs(rhs)));
+    const Vec a = rng.vector(prob.dual_dim), b = rng.vector(prob.dual_dim);
+    const double ab = a.dot(-scenopt::apply_H(prob, scenopt::hessian_vec(cache, prob, b)));
+    const double ba = b.dot(-scenopt::apply_H(prob, scenopt::hessian_vec(cache, prob, a)));
+    CHECK(std::abs(ab - ba) <= 1e-9 * std::abs(ba) + 1e-12);
+    CHECK(r.dot(rhs) > -1e-10);
+  }
+}
+
+TEST_CASE("fhat gradient matches central differences of fhat_value", false) {
+  Rng rng(45);  // test_tree_oracles.cpp:111-126
+  const auto prob = small(14, 2, 2, 2, 2);
+  const auto cache = scenopt::factor(prob);
+  for (int trial = 0; trial < 5; ++trial) {
+    const Vec y = rng.vector(prob.dual_dim);
+    Vec d = rng.vector(prob.dual_dim);
+    d /= d.norm();
+    const double h = 1e-4;
+    const double fd =
+        (scenopt::fhat_value(cache, prob, y + h * d) - scenopt::fhat_value(cache, prob, y - h * d)) / (2.0 * h);
+    const double an = scenopt::grad_fhat(cache, prob, y).dot(d);
+    CHECK(std::abs(fd - an) <= 1e-6 * std::abs(an) + 1e-8);
+  }
+}
+
+TEST_CASE("oracle call counters", false) {
+  const auto prob = small(46, 2, 2, 2, 2);  // test_tree_oracles.cpp:128-141
+  const auto cache = scenopt::factor(prob);
+  scenopt::OracleStats stats;
+  const Vec y = Vec::Zero(prob.dual_dim);
+  scenopt::dual_grad(cache, prob, y, &stats);
+  scenopt::hessian_vec(cache, prob, y, &stats);
+  scenopt::hessian_vec(cache, prob, y, &stats);
+  scenopt::grad_fhat(cache, prob, y, &stats);
+  CHECK(stats.dual_grad_calls == 2);
+  CHECK(stats.hessian_vec_calls == 2);
+  CHECK(stats.sweep_total() == 4);
+}
+
+TEST_CASE("oracles reject foreign caches and bad dual lengths", false) {
+  const auto prob = small(47, 2, 2, 2, 2);  // test_tree_oracles.cpp:143-152
+  const auto other = small(48, 3, 2, 2, 2);
+  const auto cache = scenopt::factor(prob);
+  CHECK_THROWS_AS(scenopt::dual_grad(cache, other, Vec::Zero(other.dual_dim)), scenopt::CacheMismatch);
+  CHECK_THROWS_AS(scenopt::hessian_vec(cache, prob, Vec::Zero(prob.dual_dim + 1)), scenopt::DimensionMismatch);
+}
+
+TEST_CASE("a second instance of the same shape is swept with the cache's matrices", false) {
+  const auto prob = small(49, 3, 2, 3, 2);
+  const auto twin = small(49, 3, 2, 3, 2);  // identical bytes, different object
+  const auto cache = scenopt::factor(prob);
+  Rng rng(50);
+  const Vec y = rng.vector(prob.dual_dim);
+  const Vec a = flat_x(scenopt::dual_grad(cache, prob, y)), b = flat_x(scenopt::dual_grad(cache, twin, y));
+  CHECK(max_abs(a - b) == 0.0);
+}
+
+TEST_CASE("fb_step populates a consistent state", false) {
+  Rng rng(51);  // test_fbe.cpp:44-79
+  const auto prob = small(52, 3, 2, 3, 2);
+  const auto cache = scenopt::factor(prob);
+  const auto g = scenopt::make_nonsmooth(prob);
+  const Vec y = rng.vector(prob.dual_dim);
+  const double lambda = 0.7;
+  scenopt::OracleStats stats;
+  const auto s = scenopt::fb_step(cache, prob, g, y, lambda, &stats);
+  CHECK(stats.dual_grad_calls == 1 && stats.prox_calls == 1 && stats.conj_calls == 1);
+  CHECK(max_abs(s.Hx - scenopt::apply_H(prob, s.x)) < 1e-12 * (1.0 + max_abs(s.Hx)));
+  const Vec z = scenopt::prox_g(g, y / lambda + s.Hx, 1.0 / lambda);
+  CHECK(max_abs(s.z - z) < 1e-12 * (1.0 + max_abs(z)));
+  CHECK(max_abs(s.R - (s.z - s.Hx)) < 1e-13 * (1.0 + max_abs(s.R)));
+  CHECK(max_abs(s.T - (y - lambda * s.R)) < 1e-13 * (1.0 + max_abs(s.T)));
+  const double fhat = scenopt::fhat_value(cache, prob, y);
+  CHECK(std::abs(s.fhat - fhat) <= 1e-9 * (1.0 + std::abs(fhat)));
+  const double value = s.fhat + s.conj_T + lambda * s.Hx.dot(s.R) + 0.5 * lambda * s.R.squaredNorm();
+  CHECK(std::abs(scenopt::fbe_value(s) - value) <= 1e-9 * (1.0 + std::abs(value)));
+  CHECK_THROWS_AS(scenopt::fb_step(cache, prob, g, y, 0.0), scenopt::InvalidParams);  // test_fbe.cpp:81-89
+  // rescale_state at the same lambda reproduces the state (fbe.hpp:72-77)
+  auto t = s;
+  scenopt::rescale_state(t, g, lambda);
+  CHECK(std::abs(t.value - s.value) <= 1e-12 * (1.0 + std::abs(s.value)));
+  // fbe_grad = R + lambda H x0(R)
+  const Vec grad = scenopt::fbe_grad(s, cache, prob);
+  const Vec want = s.R + lambda * scenopt::apply_H(prob, scenopt::hessian_vec(cache, prob, s.R));
+  CHECK(max_abs(grad - want) < 1e-9 * (1.0 + max_abs(want)));
+}
+
+TEST_CASE("lbfgs: empty buffer, clear resets scaling and contents", false) {
+  Rng rng(87);  // test_lbfgs.cpp:31-38, 177-192
+  scenopt::LbfgsBuffer buf(4, 1e-12);
+  const Vec g0 = rng.vector(5);
+  CHECK(max_abs(buf.apply_direction(g0) + g0) < 1e-15);
+  for (int k = 0; k < 4; ++k) {
+    const Vec step = rng.vector(5);
+    buf.push(step, Vec(2.5 * step), 1.0);
+  }
+  REQUIRE(buf.size() > 0);
+  CHECK(std::abs(buf.gamma0() - 0.4) < 1e-14);
+  buf.clear();
+  CHECK(buf.size() == 0);
+  CHECK(buf.gamma0() == 1.0);
+  const Vec grad = rng.vector(5);
+  CHECK(max_abs(buf.apply_direction(grad) + grad) < 1e-15);
+}
+
+TEST_CASE("termination reports verify independently", false) {
+  for (int trial = 0; trial < 2; ++trial) {  // test_solvers.cpp:248-270
+    const auto prob = small(1203 + trial, 3, 2, 4, 2);
+    const auto g = scenopt::make_nonsmooth(prob);
+    scenopt::SolverConfig cfg;
+    for (const auto kind : {scenopt::SolverKind::Minfbe, scenopt::SolverKind::Nama, scenopt::SolverKind::Gpad}) {
+      auto rep = scenopt::solve(prob, cfg, kind);
+      REQUIRE(rep.status == scenopt::SolverStatus::Converged);
+      CHECK(rep.verified);
+      CHECK(rep.verify_residual_inf <= cfg.eps * (1.0 + 1e-9));
+      CHECK(rep.verify_subdiff_dist <= rep.lambda_final * cfg.eps * (1.0 + 1e-9));
+      scenopt::verify_report(prob, g, rep);
+      CHECK(rep.verified);
+      for (int i = 0; i < rep.z.size(); ++i) rep.z(i) += 10.0 * cfg.eps;
+      scenopt::verify_report(prob, g, rep);
+      CHECK(!rep.verified);
+    }
+  }
+}
+
+TEST_CASE("the solver entry points agree with solve() and each other", false) {
+  const auto prob = small(1300, 3, 2, 4, 2);  // test_solvers.cpp:368-386
+  const auto cache = scenopt::factor(prob);
+  const auto g = scenopt::make_nonsmooth(prob);
+  scenopt::SolverConfig cfg;
+  std::uint64_t calls = 0;
+  const double L = scenopt::estimate_dual_lipschitz(cache, prob, &calls);
+  CHECK(L > 0.0 && calls > 0);
+  cfg.lambda0 = 0.9 / L;
+  const Vec y0 = Vec::Zero(prob.dual_dim);
+  const auto a = scenopt::solve_minfbe(prob, cache, g, cfg, y0);
+  const auto b = scenopt::solve_nama(prob, cache, g, cfg, y0);
+  REQUIRE(a.status == scenopt::SolverStatus::Converged && b.status == scenopt::SolverStatus::Converged);
+  scenopt::SolverConfig dflt;
+  const auto c = scenopt::solve(prob, dflt, scenopt::SolverKind::Minfbe, &cache);
+  CHECK(c.iterations == a.iterations);  // solve() computes the same lambda0 = 0.9 / L
+  const Vec xa = flat_x(a.x), xb = flat_x(b.x);
+  CHECK(max_abs(xa - xb) < 1e-2 * (1.0 + max_abs(xa)));
+  CHECK(a.stats.dual_grad_calls >= static_cast<std::uint64_t>(a.iterations));
+  scenopt::SolverConfig bad;
+  bad.memory = 0;
+  CHECK_THROWS_AS(scenopt::solve_minfbe(prob, cache, g, bad, y0), scenopt::InvalidParams);
+}
+
+int main(int argc, char** argv) {
+  const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
+  int run = 0;
+  for (const Case& c : cases()) {
+    if (host_only && !c.host) continue;
+    const int before = g_fail;
+    try {
+      c.fn();
+    } catch (const std::exception& e) {
+      std::printf("    unexpected exception: %s\n", e.what());
+      ++g_fail;
+    }
+    std::printf("%s %s\n", g_fail == before ? "ok  " : "FAIL", c.name);
+    ++run;
+  }
+  std::printf("%d cases, %d failed checks\n", run, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}

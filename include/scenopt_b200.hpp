@@ -131,6 +131,27 @@ class Vec {
   friend Vec operator*(double s, Vec a) { return a *= s; }
   friend Vec operator/(Vec a, double s) { return a /= s; }
   const std::vector<double>& std() const { return v_; }
+  double sum() const {
+    double s = 0.0;
+    for (double x : v_) s += x;
+    return s;
+  }
+  double minCoeff() const { return *std::min_element(v_.begin(), v_.end()); }
+  double maxCoeff() const { return *std::max_element(v_.begin(), v_.end()); }
+  /// Eigen-style comma initializer: v << a, b, c;
+  struct Comma {
+    Vec& v;
+    int i;
+    Comma& operator,(double x) {
+      if (i >= v.size()) throw DimensionMismatch("Vec: too many coefficients in comma initializer");
+      v(i++) = x;
+      return *this;
+    }
+  };
+  Comma operator<<(double x) {
+    Comma c{*this, 0};
+    return c, x;
+  }
 
  private:
   void need(const Vec& o) const {
@@ -145,10 +166,47 @@ class Mat {
   Mat() = default;
   Mat(int r, int c) : r_(r), c_(c), v_(static_cast<size_t>(r) * c, 0.0) {}
   static Mat Zero(int r, int c) { return Mat(r, c); }
-  static Mat Identity(int n) {
-    Mat m(n, n);
-    for (int i = 0; i < n; ++i) m(i, i) = 1.0;
+  static Mat Constant(int r, int c, double v) {
+    Mat m(r, c);
+    std::fill(m.v_.begin(), m.v_.end(), v);
     return m;
+  }
+  static Mat Identity(int n) { return Identity(n, n); }
+  static Mat Identity(int r, int c) {
+    Mat m(r, c);
+    for (int i = 0; i < std::min(r, c); ++i) m(i, i) = 1.0;
+    return m;
+  }
+  /// Eigen-style comma initializer, row-major order: m << a, b, c, d;
+  struct Comma {
+    Mat& m;
+    int k;
+    Comma& operator,(double x) {
+      if (k >= m.size()) throw DimensionMismatch("Mat: too many coefficients in comma initializer");
+      m(k / m.c_, k % m.c_) = x;
+      ++k;
+      return *this;
+    }
+  };
+  Comma operator<<(double x) {
+    Comma c{*this, 0};
+    return c, x;
+  }
+  Mat& operator*=(double a) {
+    for (double& x : v_) x *= a;
+    return *this;
+  }
+  friend Mat operator*(double a, Mat m) { return m *= a; }
+  friend Mat operator*(Mat m, double a) { return m *= a; }
+  friend Mat operator+(Mat a, const Mat& b) {
+    if (a.r_ != b.r_ || a.c_ != b.c_) throw DimensionMismatch("Mat + Mat: size mismatch");
+    for (size_t i = 0; i < a.v_.size(); ++i) a.v_[i] += b.v_[i];
+    return a;
+  }
+  Vec row(int i) const {
+    Vec r(c_);
+    for (int j = 0; j < c_; ++j) r(j) = (*this)(i, j);
+    return r;
   }
   int rows() const { return r_; }
   int cols() const { return c_; }
@@ -197,6 +255,62 @@ struct ScenarioTree {
   bool is_leaf(int i) const { return node_stage[static_cast<size_t>(i)] == num_stages; }
   int first_leaf() const { return stage_offsets[static_cast<size_t>(num_stages)]; }
 };
+
+/// scenario_tree.hpp:46-63
+struct NodeRange {
+  int first = 0;
+  int past = 0;
+  int size() const { return past - first; }
+};
+inline NodeRange nodes_at(const ScenarioTree& tree, int t1, int t2) {
+  if (t1 < 0 || t2 > tree.num_stages || t1 > t2)
+    throw StageOutOfRange("nodes_at: stage range [" + std::to_string(t1) + ", " + std::to_string(t2) +
+                          "] outside [0, " + std::to_string(tree.num_stages) + "]");
+  return NodeRange{tree.stage_offsets[static_cast<size_t>(t1)], tree.stage_offsets[static_cast<size_t>(t2) + 1]};
+}
+inline NodeRange nodes_at(const ScenarioTree& tree, int t) { return nodes_at(tree, t, t); }
+
+/// build_from_markov, scenario_tree.hpp:72-126: the tree of all
+/// positive-probability mode paths of a Markov chain, BFS numbered; the root
+/// branches on `initial`, later nodes on their mode's transition row.
+inline ScenarioTree build_from_markov(const Mat& transition, const Vec& initial, int horizon) {
+  const int modes = initial.size();
+  if (horizon < 1) throw InvalidParams("build_from_markov: horizon must be >= 1");
+  if (transition.rows() != modes || transition.cols() != modes)
+    throw DimensionMismatch("build_from_markov: transition must be square and match the initial distribution size");
+  const double tol = 1e-9;
+  if (initial.minCoeff() < 0.0 || std::abs(initial.sum() - 1.0) > tol)
+    throw NonStochasticMatrix("build_from_markov: initial distribution");
+  for (int w = 0; w < modes; ++w) {
+    const Vec row = transition.row(w);
+    if (row.minCoeff() < 0.0 || std::abs(row.sum() - 1.0) > tol)
+      throw NonStochasticMatrix("build_from_markov: transition row " + std::to_string(w));
+  }
+  ScenarioTree t;
+  t.num_stages = horizon;
+  t.node_stage = {0};
+  t.ancestor = {-1};
+  t.children = {{}};
+  t.probability = {1.0};
+  t.mode = {-1};
+  t.stage_offsets = {0, 1};
+  for (int s = 0; s < horizon; ++s) {
+    const int lo = t.stage_offsets[static_cast<size_t>(s)], hi = t.stage_offsets[static_cast<size_t>(s) + 1];
+    for (int a = lo; a < hi; ++a)
+      for (int w = 0; w < modes; ++w) {
+        const double pr = s == 0 ? initial(w) : transition(t.mode[static_cast<size_t>(a)], w);
+        if (!(pr > 0.0)) continue;
+        t.children[static_cast<size_t>(a)].push_back(t.num_nodes());
+        t.node_stage.push_back(s + 1);
+        t.ancestor.push_back(a);
+        t.children.emplace_back();
+        t.probability.push_back(t.probability[static_cast<size_t>(a)] * pr);
+        t.mode.push_back(w);
+      }
+    t.stage_offsets.push_back(t.num_nodes());
+  }
+  return t;
+}
 
 // ------------------------------------------------------------------ problem_data.hpp:16-141
 struct NodeDynamics { Mat A, B; Vec c; };

@@ -97,7 +97,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   SCN_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
   d->sm_count = prop.multiProcessorCount;
 
-  const int nx = p.nx, nu = p.nu, n = p.n, W = nx + nu, V = nx + nu;
+  const int nx = p.nx, nu = p.nu, n = p.n, W = nx + nu;
   Layout& L = d->lay;
   L.nx = nx;
   L.nu = nu;
@@ -518,14 +518,22 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     d->ys[r] = d->alloc<double>(static_cast<size_t>(std::max(D, 1)));
   }
 
-  // ---- algorithmic bytes per sweep (matrices once + vector traffic)
-  const int64_t F = p.first_leaf;
-  const int64_t vecs = 2LL * D + static_cast<int64_t>(nx) * n + 3LL * nu * F +
-                       static_cast<int64_t>(n - 1) * V + 2LL * (n - 1) * W;
-  const int64_t mats = d->bw_doubles + d->fw_doubles;  // includes the per-item node headers
-  d->bytes_hom = 8 * (mats + vecs);
-  d->bytes_aff = d->bytes_hom + 8 * (static_cast<int64_t>(n) * W + static_cast<int64_t>(n) * nx);
-  d->bytes_hom2 = 8 * (mats + 2 * vecs);
+  // ---- algorithmic bytes per sweep, SURVEY.md §8(d) / DESIGN.md §Roofline:
+  // every matrix read once, every vector touched once (fp64).
+  //   B_hom = 8 [(n-1)(2nx^2 + 2nx nu) + F nu nx + 2 sum_i m_i (nx+nu)
+  //              + 2 sum_l mN_l nx] + B_vec,  B_vec = 8 (4 n nx + 3 F nu + 2 m)
+  //   B_aff = B_hom + 8 [F (nx+nu) + S nx + (n-1) nx]
+  //   B_hom2 (two right-hand sides) = matrices once + 2 B_vec
+  const int64_t F = p.first_leaf, S = p.L, m = D;
+  int64_t stage_rows_total = 0, term_rows_total = 0;
+  for (int c = 1; c < n; ++c) stage_rows_total += p.stage_rows[c];
+  for (int l = 0; l < p.L; ++l) term_rows_total += p.terminal_rows[l];
+  const int64_t mat = static_cast<int64_t>(n - 1) * (2LL * nx * nx + 2LL * nx * nu) + F * nu * nx +
+                      2 * stage_rows_total * (nx + nu) + 2 * term_rows_total * nx;
+  const int64_t vec = 4LL * n * nx + 3 * F * nu + 2 * m;
+  d->bytes_hom = 8 * (mat + vec);
+  d->bytes_aff = d->bytes_hom + 8 * (F * (nx + nu) + S * nx + static_cast<int64_t>(n - 1) * nx);
+  d->bytes_hom2 = 8 * (mat + 2 * vec);
   SCN_CUDA(cudaDeviceSynchronize());
   return d;
 }

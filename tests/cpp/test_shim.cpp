@@ -105,6 +105,26 @@ TEST_CASE("generated instances are valid and laid out like the reference", true)
   CHECK(again.con[5].F(1, 2) == prob.con[5].F(1, 2) && again.cost[9].Q(2, 1) == prob.cost[9].Q(2, 1));
 }
 
+TEST_CASE("markov build: full two-mode chain is a binary tree", true) {
+  scenopt::Mat P(2, 2);  // test_scenario_tree.cpp:20-50 known answers
+  P << 0.1, 0.9, 0.9, 0.1;
+  Vec p0(2);
+  p0 << 0.5, 0.5;
+  const auto tree = scenopt::build_from_markov(P, p0, 3);
+  CHECK(tree.num_nodes() == 15 && tree.num_leaves() == 8 && tree.first_leaf() == 7);
+  CHECK(tree.stage_offsets == std::vector<int>({0, 1, 3, 7, 15}));
+  CHECK(tree.mode[0] == -1 && tree.mode[1] == 0 && tree.probability[1] == 0.5);
+  const int stay = tree.children[1][0], flip = tree.children[1][1];
+  CHECK(tree.mode[stay] == 0 && std::abs(tree.probability[stay] - 0.05) < 1e-15);
+  CHECK(std::abs(tree.probability[flip] - 0.45) < 1e-15);
+  const auto r = scenopt::nodes_at(tree, 2);
+  CHECK(r.first == 3 && r.past == 7 && r.size() == 4);
+  CHECK_THROWS_AS(scenopt::nodes_at(tree, 4), scenopt::StageOutOfRange);
+  scenopt::Mat bad(2, 2);
+  bad << 0.5, 0.6, 0.5, 0.5;
+  CHECK_THROWS_AS(scenopt::build_from_markov(bad, p0, 2), scenopt::NonStochasticMatrix);
+}
+
 TEST_CASE("validate reports broken instances", true) {
   auto prob = small(8);
   prob.tree.probability[1] = 0.9;  // children no longer sum to the parent

@@ -9,21 +9,28 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIBDIR = os.path.join(ROOT, "paper_2107_01745_b200", "lib")
-SRC = os.path.join(ROOT, "tests", "cpp", "test_shim.cpp")
-OUT = os.path.join(ROOT, "tests", "cpp", "_build", "test_shim")
+BUILD = os.path.join(ROOT, "tests", "cpp", "_build")
 
 
-def _build():
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = ["g++", "-std=c++17", "-O1", "-Wall", "-Wextra", "-Werror", f"-I{ROOT}/include", SRC,
-           f"-L{LIBDIR}", "-lscenopt_b200", f"-Wl,-rpath,{LIBDIR}", "-o", OUT]
-    subprocess.run(cmd, check=True, capture_output=True, text=True)
-    return OUT
+def _build(name):
+    os.makedirs(BUILD, exist_ok=True)
+    out = os.path.join(BUILD, name)
+    cmd = ["g++", "-std=c++17", "-O1", "-Wall", "-Wextra", "-Werror", f"-I{ROOT}/include",
+           os.path.join(ROOT, "tests", "cpp", name + ".cpp"), f"-L{LIBDIR}", "-lscenopt_b200",
+           f"-Wl,-rpath,{LIBDIR}", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
 
 
 @pytest.fixture(scope="module")
 def shim_binary(_built_libraries):
-    return _build()
+    return _build("test_shim")
+
+
+@pytest.fixture(scope="module")
+def sample_binary(_built_libraries):
+    return _build("sample_markov")
 
 
 def test_shim_header_compiles_and_host_cases_pass(shim_binary):
@@ -37,3 +44,14 @@ def test_shim_device_cases(gpu, shim_binary):
     r = subprocess.run([shim_binary], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_style_sample_solves_and_verifies(gpu, sample_binary):
+    r = subprocess.run([sample_binary], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "verified 1" in r.stdout
+
+
+def test_reference_style_sample_compiles(sample_binary):
+    assert os.path.exists(sample_binary)

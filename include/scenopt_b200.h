@@ -112,8 +112,10 @@ typedef struct scenopt_dev_info {
   int32_t device, sm_count, grid_ctas, ctas_per_sm, slots, items_bw, items_fw, nodes_per_item_max;
   int64_t slot_bytes, matrix_bytes_bw, matrix_bytes_fw, device_bytes;
   int64_t sweep_bytes_hom, sweep_bytes_aff, sweep_bytes_hom2; /* algorithmic bytes per sweep */
-  int32_t cut_stage; /* stages >= cut_stage are owned per CTA as whole subtrees; -1: all global */
-  int32_t reserved;
+  int32_t cut_stage;   /* CTA subtree-ownership cut of the main region; -1: all global tickets */
+  int32_t shard_stage; /* subtree sharding over ranks: cut stage, -1 when not sharded */
+  int32_t rank, world; /* this handle's rank in the shard group (0, 1 when not sharded) */
+  int32_t shard_first, shard_past; /* this rank's shard-stage node ids [first, past) */
 } scenopt_dev_info;
 
 typedef struct scenopt_problem scenopt_problem;
@@ -162,6 +164,35 @@ void scenopt_factor_destroy(scenopt_factor* f);
  * uploads it. */
 int scenopt_dev_create(const scenopt_problem* p, const scenopt_factor* f, int device,
                        scenopt_dev** out);
+/* Subtree-sharded handle: rank `rank` of `world` processes
+ * (one per GPU, all calling this concurrently) owns the subtrees of a
+ * contiguous, byte-balanced range of the shard-stage nodes (shard_stage < 0:
+ * the smallest stage with >= world nodes) and replicates the stages above.
+ * Dual vectors are replicated on every rank; every sweep exchanges the
+ * shard-stage contributions and assembles Hx with NCCL sum-allreduces on the
+ * handle's stream; x/u outputs of the public entry points and solver reports
+ * are assembled in full. nccl_id: 128 bytes from scenopt_nccl_unique_id() on
+ * one rank, shared with the others (NULL: no communicator, see the phase
+ * API below; world == 1 needs none). The same problem and factor must be
+ * passed on every rank. Replaces nothing in the reference (single-process);
+ * every other entry point accepts the sharded handle unchanged. */
+int scenopt_nccl_unique_id(void* out128);
+/* Host-only plan of the above: the shard stage actually used and the
+ * world + 1 bounds of the ranks' shard-stage node ranges. */
+int scenopt_shard_plan(const scenopt_problem* p, int world, int shard_stage, int32_t* stage_out,
+                       int32_t* bounds);
+int scenopt_dev_create_sharded(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
+                               int world, int shard_stage, const void* nccl_id, scenopt_dev** out);
+/* Sharded handles created with nccl_id == NULL leave the exchange to the
+ * caller (emulating ranks on one device, tests): phase 0 zeroes Hx, runs the
+ * local backward and writes this rank's shard-stage contributions into the
+ * exchange buffer (zeros elsewhere); the caller sums the buffers over ranks
+ * into every rank's buffer; phase 1 runs the top backward and all forward
+ * work and zeroes the replicated top rows of Hx on ranks != 0, so the sum of
+ * the ranks' Hx is the full Hx. Device pointers, handle stream. */
+int scenopt_shard_sweep_phase(scenopt_dev* d, int phase, int nrhs, int affine, const double* const* y,
+                              double* const* Hx);
+int scenopt_shard_exchange_buffer(scenopt_dev* d, double** buf, size_t* doubles_per_rhs);
 int scenopt_dev_info_get(const scenopt_dev* d, scenopt_dev_info* info);
 int scenopt_dev_synchronize(scenopt_dev* d);
 /* The handle's CUDA stream (cudaStream_t) for event timing by callers. */

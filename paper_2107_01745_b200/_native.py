@@ -66,7 +66,8 @@ class DevInfoC(C.Structure):
         ("slot_bytes", C.c_int64), ("matrix_bytes_bw", C.c_int64),
         ("matrix_bytes_fw", C.c_int64), ("device_bytes", C.c_int64),
         ("sweep_bytes_hom", C.c_int64), ("sweep_bytes_aff", C.c_int64),
-        ("sweep_bytes_hom2", C.c_int64), ("cut_stage", C.c_int32), ("reserved", C.c_int32),
+        ("sweep_bytes_hom2", C.c_int64), ("cut_stage", C.c_int32), ("shard_stage", C.c_int32),
+        ("rank", C.c_int32), ("world", C.c_int32), ("shard_first", C.c_int32), ("shard_past", C.c_int32),
     ]
 
 

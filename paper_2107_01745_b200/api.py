@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from ._native import check, dptr, iptr
+from ._native import InvalidParams, check, dptr, iptr
 
 HOST = N.HOST_IO
 
@@ -166,6 +166,22 @@ class FactorCache:
             self._dev = h
         return self._dev
 
+    def shard(self, rank: int, world: int, nccl_id: bytes | None, device: int = 0, stage: int = -1):
+        """Attach a subtree-sharded device handle: every
+        rank of `world` (one process per GPU) calls this concurrently with the
+        same instance, factor and nccl_id (nccl_unique_id() on one rank,
+        shared). All oracle and solver calls on this cache then run sharded."""
+        if self._dev is not None:
+            raise InvalidParams("shard(): the cache already has a device handle")
+        if nccl_id is not None and len(nccl_id) != 128:
+            raise InvalidParams("shard(): nccl_id must be 128 bytes")
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        check(N.lib().scenopt_dev_create_sharded(self._prob._h, self._h, device, rank, world, stage, buf,
+                                                 C.byref(h)))
+        self._dev = h
+        return h
+
     def dev_info(self) -> dict:
         info = N.DevInfoC()
         check(N.lib().scenopt_dev_info_get(self.device(), C.byref(info)))
@@ -185,6 +201,13 @@ class FactorCache:
             "gain", "child_to_input", "closed_loop", "dual_to_input", "dual_to_costate",
             "input_affine", "costate_affine", "value_quad", "leaf_costate_affine")]))
         return out
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) for FactorCache.shard()."""
+    buf = C.create_string_buffer(128)
+    check(N.lib().scenopt_nccl_unique_id(buf))
+    return buf.raw
 
 
 def factor(prob: ProblemInstance) -> FactorCache:

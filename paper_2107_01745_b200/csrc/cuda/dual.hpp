@@ -109,9 +109,14 @@ struct CostPack {
   int nx, nu, n, first_leaf;
   const int32_t* anc;
   const double* prob;
-  const double* node;   // per non-root node: [A | B | c | Q | S | R | q | r]
-  const double* leaf;   // per leaf: [P | p]
+  const int32_t* nodes;  // non-root nodes evaluated here (all, or a rank's share)
+  int nnodes;
+  const double* node;    // per listed node: [A | B | c | Q | S | R | q | r]
+  const int32_t* leaves; // leaves evaluated here
+  int nleaves;
+  const double* leaf;    // per listed leaf: [P | p]
   const double* root_state;
+  int check_root;        // 1: include the x^0 = p check
 };
 cudaError_t k_eval_f(const DualCtx& c, const CostPack& cp, const double* x, const double* u,
                      double feas_tol, cudaStream_t st);  // -> S[EVALF], S[EVALF_INF]

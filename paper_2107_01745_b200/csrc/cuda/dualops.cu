@@ -585,15 +585,16 @@ __global__ void __launch_bounds__(kThreads) eval_f_kernel(DualCtx c, CostPack cp
   const int64_t csz = 2LL * nx * nx + 2LL * nx * nu + static_cast<int64_t>(nu) * nu + 2 * nx + nu;
   const int64_t lsz = static_cast<int64_t>(nx) * nx + nx;
   double s[1] = {0.0}, bad[1] = {0.0};
-  const int L = cp.n - cp.first_leaf;
-  for (int t = gw; t < (cp.n - 1) + L + 1; t += nw) {
-    if (t == (cp.n - 1) + L) {  // root state check
-      for (int k = lane; k < nx; k += 32)
-        if (fabs(x[k] - cp.root_state[k]) > tol) bad[0] = 1.0;
+  const int NN = cp.nnodes, NL = cp.nleaves;
+  for (int t = gw; t < NN + NL + 1; t += nw) {
+    if (t == NN + NL) {  // root state check
+      if (cp.check_root)
+        for (int k = lane; k < nx; k += 32)
+          if (fabs(x[k] - cp.root_state[k]) > tol) bad[0] = 1.0;
       continue;
     }
-    if (t < cp.n - 1) {
-      const int nd = t + 1;
+    if (t < NN) {
+      const int nd = cp.nodes[t];
       const int64_t a = cp.anc[nd];
       const double* blk = cp.node + static_cast<int64_t>(t) * csz;
       const double *A = blk, *B = A + nx * nx, *cv = B + nx * nu, *Q = cv + nx, *Sm = Q + nx * nx,
@@ -620,8 +621,8 @@ __global__ void __launch_bounds__(kThreads) eval_f_kernel(DualCtx c, CostPack cp
       }
       s[0] += cp.prob[nd] * part;  // per-lane partial; reduced below
     } else {
-      const int l = t - (cp.n - 1);
-      const int nd = cp.first_leaf + l;
+      const int l = t - NN;
+      const int nd = cp.leaves[l];
       const double* P = cp.leaf + static_cast<int64_t>(l) * lsz;
       const double* p = P + nx * nx;
       const double* xc = x + static_cast<int64_t>(nd) * nx;

@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "layout.hpp"
 
@@ -658,8 +659,21 @@ cudaError_t sweep_profile_read(unsigned long long* out, bool reset) {
 }
 
 cudaError_t sweep_configure(size_t dyn_smem) {
-  cudaError_t e = cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(dyn_smem));
+  // The cap is a per-function, per-device attribute shared by every handle of
+  // the process: only ever raise it (a lower value would break the launches
+  // of handles with larger slots).
+  static std::mutex mu;
+  static size_t configured[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= 0 && dev < 64) {
+    if (dyn_smem <= configured[dev]) return cudaSuccess;
+    configured[dev] = dyn_smem;
+  }
+  e = cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(dyn_smem));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(sweep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(dyn_smem));

@@ -135,6 +135,52 @@ int scenopt_dev_create(const scenopt_problem* p, const scenopt_factor* f, int de
   });
 }
 
+int scenopt_nccl_unique_id(void* out128) { SCN_GUARD(nccl_unique_id(out128)); }
+
+int scenopt_shard_plan(const scenopt_problem* p, int world, int shard_stage, int32_t* stage_out,
+                       int32_t* bounds) {
+  SCN_GUARD({
+    int s = shard_stage;
+    const std::vector<int> b = shard_plan(p->p, world, &s);
+    *stage_out = s;
+    for (size_t i = 0; i < b.size(); ++i) bounds[i] = b[i];
+  });
+}
+
+int scenopt_dev_create_sharded(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
+                               int world, int shard_stage, const void* nccl_id, scenopt_dev** out) {
+  SCN_GUARD({
+    if (!f) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: a factor cache is required");
+    if (world < 1 || rank < 0 || rank >= world) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: bad rank/world");
+    ShardSpec spec;
+    spec.rank = rank;
+    spec.world = world;
+    spec.stage = shard_stage;
+    spec.nccl_id = nccl_id;
+    auto h = std::make_unique<scenopt_dev>();
+    h->d = dev_create(p->p, &f->f, device, &spec);
+    h->init_solver_buffers();
+    *out = h.release();
+  });
+}
+
+int scenopt_shard_sweep_phase(scenopt_dev* h, int phase, int nrhs, int affine, const double* const* y,
+                              double* const* Hx) {
+  SCN_GUARD({
+    SCN_CUDA(cudaSetDevice(h->d->device));
+    dev_sweep_phase(*h->d, phase, nrhs, affine != 0, y, Hx);
+  });
+}
+
+int scenopt_shard_exchange_buffer(scenopt_dev* h, double** buf, size_t* doubles_per_rhs) {
+  SCN_GUARD({
+    const DevState& d = *h->d;
+    if (!d.sharded()) fail(SCENOPT_E_INVALID_PARAMS, "exchange buffer: handle is not sharded");
+    *buf = d.xbuf;
+    *doubles_per_rhs = static_cast<size_t>(d.sstage_hi - d.sstage_lo) * (d.lay.nx + d.lay.nu);
+  });
+}
+
 int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
   SCN_GUARD({
     const DevState& d = *h->d;
@@ -154,7 +200,11 @@ int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
     info->sweep_bytes_aff = d.bytes_aff;
     info->sweep_bytes_hom2 = d.bytes_hom2;
     info->cut_stage = d.cut_stage;
-    info->reserved = 0;
+    info->shard_stage = d.shard_stage;
+    info->rank = d.rank;
+    info->world = d.world;
+    info->shard_first = d.shard_lo;
+    info->shard_past = d.shard_hi;
   });
 }
 

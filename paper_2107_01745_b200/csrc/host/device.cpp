@@ -11,6 +11,7 @@ namespace scn {
 
 DevState::~DevState() {
   if (device >= 0) cudaSetDevice(device);
+  nccl_comm_destroy(comm);
   for (void* p : owned) cudaFree(p);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -44,6 +45,8 @@ int env_int(const char* name, int dflt) {
 }
 
 inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
+// padded column length == 2 (mod 4): conflict-free 16-byte shared loads
+inline int pad2(int l) { return l + ((2 - l % 4) + 4) % 4; }
 
 template <class T>
 T* upload(DevState& d, const std::vector<T>& h) {
@@ -55,7 +58,66 @@ T* upload(DevState& d, const std::vector<T>& h) {
 }  // namespace
 
 namespace {
-void pack_common(DevState& d, const Problem& p);
+void pack_common(DevState& d, const Problem& p, const std::vector<char>* mine = nullptr);
+}
+
+// Per-node packed block sizes (doubles) of the backward / forward pass
+// arrays (layout.hpp); M_c = the children's stage rows.
+void node_block_sizes(const Problem& p, std::vector<int64_t>& bws, std::vector<int64_t>& fws) {
+  const int nx = p.nx, nu = p.nu, n = p.n, W = nx + nu;
+  const int nxp = pad2(nx), Vp = pad2(nx + nu);
+  bws.assign(static_cast<size_t>(n), 0);
+  fws.assign(static_cast<size_t>(n), 0);
+  for (int c = 0; c < n; ++c) {
+    const bool leaf = c >= p.first_leaf;
+    const int m = c == 0 ? 0 : p.stage_rows[c];
+    const int mN = leaf ? p.terminal_rows[c - p.first_leaf] : 0;
+    int64_t M = 0;
+    if (!leaf)
+      for (int k = p.child_begin[c]; k < p.child_begin[c] + p.child_count[c]; ++k) M += p.stage_rows[k];
+    int64_t b = even(leaf ? static_cast<int64_t>(mN) * nx : M * W);
+    if (c != 0) b += static_cast<int64_t>(nxp) * W;
+    bws[c] = b;
+    int64_t fw = 0;
+    if (c != 0) fw += static_cast<int64_t>(Vp) * (nx + m);
+    fw += leaf ? static_cast<int64_t>(nxp) * mN : static_cast<int64_t>(nxp) * nu;
+    fws[c] = even(fw);
+  }
+}
+
+// Contiguous split of nodes [lo, hi) into k groups balanced by subtree bytes.
+std::vector<int> balanced_split(const std::vector<int64_t>& sub, int lo, int hi, int k) {
+  std::vector<int> bound(static_cast<size_t>(k) + 1, hi);
+  bound[0] = lo;
+  int64_t total = 0, acc = 0;
+  for (int r = lo; r < hi; ++r) total += sub[r];
+  int g = 1;
+  for (int r = lo; r < hi && g < k; ++r) {
+    acc += sub[r];
+    while (g < k && acc * k >= total * g) bound[g++] = r + 1;
+  }
+  return bound;
+}
+
+std::vector<int64_t> subtree_bytes(const Problem& p, const std::vector<int64_t>& bws, const std::vector<int64_t>& fws) {
+  std::vector<int64_t> sub(static_cast<size_t>(p.n));
+  for (int c = 0; c < p.n; ++c) sub[c] = bws[c] + fws[c];
+  for (int c = p.n - 1; c >= 1; --c) sub[p.ancestor[c]] += sub[c];  // BFS: parents precede children
+  return sub;
+}
+
+std::vector<int> shard_plan(const Problem& p, int world, int* stage) {
+  int s = *stage;
+  if (world < 1) fail(SCENOPT_E_INVALID_PARAMS, "shard plan: world must be >= 1");
+  if (s < 0)
+    for (int t = 1; t <= p.N && s < 0; ++t)
+      if (p.stage_offsets[t + 1] - p.stage_offsets[t] >= world) s = t;
+  if (s < 1 || s > p.N || p.stage_offsets[s + 1] - p.stage_offsets[s] < world)
+    fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: shard stage must lie in [1, N] and hold >= world nodes");
+  std::vector<int64_t> bws, fws;
+  node_block_sizes(p, bws, fws);
+  *stage = s;
+  return balanced_split(subtree_bytes(p, bws, fws), p.stage_offsets[s], p.stage_offsets[s + 1], world);
 }
 
 std::unique_ptr<DevState> dev_create_bare(int device) {
@@ -76,7 +138,7 @@ std::unique_ptr<DevState> dev_create_bare(int device) {
   return d;
 }
 
-std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int device) {
+std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int device, const ShardSpec* shard) {
   if (fptr) check_factor_shape(*fptr, p, "dev_create");
   require_valid(p);
   int ndev = 0;
@@ -127,40 +189,38 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->has_factor = true;
 
   // ---- per-node block sizes (doubles, even => 16-byte aligned); padded
-  // column lengths pad(l) == 2 (mod 4) for conflict-free 16-byte smem loads
-  auto pad2 = [](int l) { return l + ((2 - l % 4) + 4) % 4; };
+  // column lengths pad2(l) == 2 (mod 4) for conflict-free 16-byte smem loads
   const int nxp = pad2(nx), Vp = pad2(nx + nu);
   d->nxp = nxp;
   d->Vp = Vp;
-  std::vector<int64_t> bws(static_cast<size_t>(n)), fws(static_cast<size_t>(n));
+  std::vector<int64_t> bws, fws;
+  node_block_sizes(p, bws, fws);
   std::vector<int32_t> M(static_cast<size_t>(n), 0), cdo(static_cast<size_t>(n), 0);
   for (int c = 0; c < n; ++c) {
     const bool leaf = c >= p.first_leaf;
-    const int m = c == 0 ? 0 : p.stage_rows[c];
-    const int mN = leaf ? p.terminal_rows[c - p.first_leaf] : 0;
     if (!leaf) {
       M[c] = f.child_dual_rows[c];
       cdo[c] = f.child_dual_offset[c];
     }
-    d->max_m = std::max(d->max_m, m);
-    d->max_mN = std::max(d->max_mN, mN);
-    int64_t b = even(leaf ? static_cast<int64_t>(mN) * nx : static_cast<int64_t>(M[c]) * W);
-    if (c != 0) b += static_cast<int64_t>(nxp) * W;
-    bws[c] = b;
-    int64_t fw = 0;
-    if (c != 0) fw += static_cast<int64_t>(Vp) * (nx + m);
-    fw += leaf ? static_cast<int64_t>(nxp) * mN : static_cast<int64_t>(nxp) * nu;
-    fws[c] = even(fw);
+    d->max_m = std::max(d->max_m, c == 0 ? 0 : p.stage_rows[c]);
+    d->max_mN = std::max(d->max_mN, leaf ? p.terminal_rows[c - p.first_leaf] : 0);
   }
 
-  // ---- schedule. The grid is one co-resident CTA per SM. Below a cut stage
-  // with >= kMinSub*G nodes, every CTA owns a contiguous, byte-balanced group
-  // of whole subtrees: their items depend only on items of the same CTA
-  // (a shared-memory retire counter, no gpu-scope publication). The few
-  // nodes above the cut are dealt round-robin as global tickets whose
-  // dependencies are released through per-node flags. Each CTA's list is
-  // ordered by rank (backward leaves->root, then forward root->leaves), and
-  // every dependency has a smaller rank, so the schedule cannot deadlock.
+  // ---- schedule. The grid is one co-resident CTA per SM.
+  // A region (per-stage node ranges) is scheduled as: below a cut stage with
+  // >= min_sub*G nodes every CTA owns a contiguous, byte-balanced group of
+  // whole subtrees (its items depend only on items of the same CTA: a
+  // shared-memory retire counter, no gpu-scope publication); the region's
+  // nodes above that cut are dealt round-robin as global tickets whose
+  // dependencies are released through per-node flags. Each CTA's list is in
+  // rank order (backward leaves->root, then forward root->leaves) and every
+  // dependency has a smaller rank, so no schedule can deadlock.
+  //
+  // A sharded handle (rank r of W) owns the subtrees of a contiguous,
+  // byte-balanced range of shard-stage nodes and replicates the stages
+  // above. Its sweep is two launches: A = the local backward below the
+  // shard stage; then the shard-stage contributions are sum-allreduced; then
+  // B = the (redundant) top backward, top forward and local forward.
   d->grid = d->sm_count;
   if (const int g = env_int("SCENOPT_GRID", 0)) d->grid = std::min(g, d->grid);  // experiments only
   const int G = d->grid;
@@ -169,6 +229,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   const int min_sub = env_int("SCENOPT_MIN_SUBTREES", 4);  // per CTA; 0 disables ownership
   const int min_items = 8;  // independent items per stage and CTA (local dependency distance)
   struct Run { int first, count, pass, ldep, gdep, publish; };
+  using Lists = std::vector<std::vector<Run>>;
   auto chunk = [&](int lo, int hi, int pass, int per_stage_min, std::vector<Run>& out) {
     const std::vector<int64_t>& size = pass == 0 ? bws : fws;
     const int cnt_all = hi - lo;
@@ -187,105 +248,167 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
       i += cnt;
     }
   };
-  int cut = -1;
-  if (min_sub > 0)
-    for (int s = 1; s <= p.N; ++s)
-      if (p.stage_offsets[s + 1] - p.stage_offsets[s] >= min_sub * G) {
-        cut = s;
-        break;
+  const std::vector<int64_t> sub = subtree_bytes(p, bws, fws);
+  auto split = [&](int lo, int hi, int k) { return balanced_split(sub, lo, hi, k); };
+  // per-stage ranges [t0, t1] of the subtrees of nodes [lo, hi) at stage t0
+  auto descend = [&](int lo, int hi, int t0, int t1) {
+    std::vector<std::pair<int, int>> rng(static_cast<size_t>(p.N) + 1, {0, 0});
+    for (int t = t0; t <= t1; ++t) {
+      rng[t] = {lo, hi};
+      if (t < p.N && lo < hi) {
+        const int nlo = p.child_begin[lo], nhi = p.child_begin[hi - 1] + p.child_count[hi - 1];
+        lo = nlo;
+        hi = nhi;
+      } else {
+        lo = hi = 0;
       }
-  const int top_end = cut < 0 ? p.N + 1 : cut;  // stages [0, top_end) are global
-  std::vector<Run> top_bw, top_fw;
-  for (int t = top_end - 1; t >= 0; --t) chunk(p.stage_offsets[t], p.stage_offsets[t + 1], 0, 1, top_bw);
-  for (int t = 0; t < top_end; ++t) chunk(p.stage_offsets[t], p.stage_offsets[t + 1], 1, 1, top_fw);
-  for (Run& r : top_bw) r.gdep = r.publish = 1;
-  for (Run& r : top_fw) r.gdep = r.publish = 1;
-  std::vector<std::vector<Run>> lists(static_cast<size_t>(G));
-  std::vector<std::vector<Run>> local_fw(static_cast<size_t>(G));
-  if (cut >= 0) {
-    // subtree byte totals (BFS numbering: parents precede children)
-    std::vector<int64_t> sub(static_cast<size_t>(n));
-    for (int c = 0; c < n; ++c) sub[c] = bws[c] + fws[c];
-    for (int c = n - 1; c >= 1; --c) sub[p.ancestor[c]] += sub[c];
-    const int r0 = p.stage_offsets[cut], r1 = p.stage_offsets[cut + 1];
-    int64_t total = 0;
-    for (int r = r0; r < r1; ++r) total += sub[r];
-    std::vector<int> bound(static_cast<size_t>(G) + 1, r1);
-    bound[0] = r0;
-    int64_t acc = 0;
-    int g = 1;
-    for (int r = r0; r < r1 && g < G; ++r) {
-      acc += sub[r];
-      while (g < G && acc * G >= total * g) bound[g++] = r + 1;
     }
-    for (int gg = 0; gg < G; ++gg) {
-      // per-stage node range of the group, stages cut..N
-      std::vector<std::pair<int, int>> rng;
-      int lo = bound[gg], hi = bound[gg + 1];
-      for (int t = cut; t <= p.N; ++t) {
-        rng.emplace_back(lo, hi);
-        if (t < p.N && lo < hi) {
-          const int nlo = p.child_begin[lo], nhi = p.child_begin[hi - 1] + p.child_count[hi - 1];
-          lo = nlo;
-          hi = nhi;
-        } else if (t < p.N) {
-          lo = hi = 0;
+    return rng;
+  };
+  // Region [t0, t1] with per-stage ranges rng: per CTA, the backward part
+  // (local backward, then region-top backward tickets) and the forward part
+  // (region-top forward tickets, then local forward).
+  auto region = [&](int t0, int t1, const std::vector<std::pair<int, int>>& rng, bool allow_cut, bool want_bw,
+                    bool want_fw, Lists& bw_out, Lists& fw_out) {
+    int cut = -1;
+    if (allow_cut && min_sub > 0)
+      for (int t = std::max(t0, 1); t <= t1; ++t)
+        if (rng[t].second - rng[t].first >= min_sub * G) {
+          cut = t;
+          break;
+        }
+    const int top_end = cut < 0 ? t1 + 1 : cut;
+    std::vector<Run> tb, tf;
+    if (want_bw)
+      for (int t = top_end - 1; t >= t0; --t) chunk(rng[t].first, rng[t].second, 0, 1, tb);
+    if (want_fw)
+      for (int t = t0; t < top_end; ++t) chunk(rng[t].first, rng[t].second, 1, 1, tf);
+    bw_out.assign(static_cast<size_t>(G), {});
+    fw_out.assign(static_cast<size_t>(G), {});
+    Lists lfw(static_cast<size_t>(G));
+    if (cut >= 0) {
+      const std::vector<int> bound = split(rng[cut].first, rng[cut].second, G);
+      for (int gg = 0; gg < G; ++gg) {
+        const auto grp = descend(bound[gg], bound[gg + 1], cut, t1);
+        if (want_bw)
+          for (int t = t1; t >= cut; --t)
+            if (grp[t].first < grp[t].second) chunk(grp[t].first, grp[t].second, 0, min_items, bw_out[gg]);
+        if (want_fw)
+          for (int t = cut; t <= t1; ++t)
+            if (grp[t].first < grp[t].second) chunk(grp[t].first, grp[t].second, 1, min_items, lfw[gg]);
+      }
+    }
+    for (size_t i = 0; i < tb.size(); ++i) bw_out[i % G].push_back(tb[i]);
+    for (size_t i = 0; i < tf.size(); ++i) fw_out[i % G].push_back(tf[i]);
+    for (int gg = 0; gg < G; ++gg) fw_out[gg].insert(fw_out[gg].end(), lfw[gg].begin(), lfw[gg].end());
+    return cut;
+  };
+  // Dependencies of one launch: a dependency node produced by the same CTA
+  // is a local wait (retire counter); by another CTA a flag wait (and its
+  // producer publishes); by an earlier launch / the exchange, no wait.
+  auto resolve = [&](Lists& L) {
+    std::vector<int> bcta(static_cast<size_t>(n), -1), bpos(static_cast<size_t>(n), -1),
+        fcta(static_cast<size_t>(n), -1), fpos(static_cast<size_t>(n), -1);
+    for (int gg = 0; gg < G; ++gg)
+      for (int k = 0; k < static_cast<int>(L[gg].size()); ++k) {
+        const Run& r = L[gg][k];
+        for (int c = r.first; c < r.first + r.count; ++c) {
+          (r.pass == 0 ? bcta : fcta)[c] = gg;
+          (r.pass == 0 ? bpos : fpos)[c] = k;
         }
       }
-      for (int t = p.N; t >= cut; --t) {
-        const auto [a, b2] = rng[t - cut];
-        if (a < b2) chunk(a, b2, 0, min_items, lists[gg]);
-      }
-      for (Run& r : lists[gg])
-        if (p.node_stage[r.first] == cut) r.publish = 1;  // consumed by the global top
-      for (int t = cut; t <= p.N; ++t) {
-        const auto [a, b2] = rng[t - cut];
-        if (a < b2) chunk(a, b2, 1, min_items, local_fw[gg]);
-      }
-      for (Run& r : local_fw[gg])
-        if (p.node_stage[r.first] == cut) r.gdep = 1;  // parents above the cut
-    }
-  }
-  for (size_t i = 0; i < top_bw.size(); ++i) lists[i % G].push_back(top_bw[i]);
-  for (size_t i = 0; i < top_fw.size(); ++i) lists[i % G].push_back(top_fw[i]);
-  for (int gg = 0; gg < G; ++gg) lists[gg].insert(lists[gg].end(), local_fw[gg].begin(), local_fw[gg].end());
-  // local dependency indices
-  {
-    std::vector<int> bw_pos(static_cast<size_t>(n), -1), fw_pos(static_cast<size_t>(n), -1);
-    for (int gg = 0; gg < G; ++gg) {
-      for (int k = 0; k < static_cast<int>(lists[gg].size()); ++k) {
-        Run& r = lists[gg][k];
-        auto& pos = r.pass == 0 ? bw_pos : fw_pos;
-        if (!r.gdep && !(r.pass == 0 && r.first >= p.first_leaf)) {
-          int ld = -1;
-          const int last = r.first + r.count - 1;
-          if (r.pass == 0) {
-            for (int c = p.child_begin[r.first]; c < p.child_begin[last] + p.child_count[last]; ++c)
-              ld = std::max(ld, bw_pos[c]);
+    for (int gg = 0; gg < G; ++gg)
+      for (int k = 0; k < static_cast<int>(L[gg].size()); ++k) {
+        Run& r = L[gg][k];
+        const int last = r.first + r.count - 1;
+        int lo = 0, hi = 0;
+        const std::vector<int>*cta = &bcta, *pos = &bpos;
+        if (r.pass == 0) {
+          if (r.first >= p.first_leaf) continue;
+          lo = p.child_begin[r.first];
+          hi = p.child_begin[last] + p.child_count[last];
+        } else if (r.first == 0) {
+          lo = 0, hi = 1;  // forward root <- backward root
+        } else {
+          lo = p.ancestor[r.first];
+          hi = p.ancestor[last] + 1;
+          cta = &fcta;
+          pos = &fpos;
+        }
+        int ld = -1, nloc = 0, nrem = 0, next = 0;
+        for (int c = lo; c < hi; ++c) {
+          const int g2 = (*cta)[c];
+          if (g2 < 0) {
+            ++next;
+          } else if (g2 == gg) {
+            ++nloc;
+            ld = std::max(ld, (*pos)[c]);
           } else {
-            for (int a = p.ancestor[r.first]; a <= p.ancestor[last]; ++a) ld = std::max(ld, fw_pos[a]);
+            ++nrem;
           }
-          if (ld < 0) fail(SCENOPT_E_INVALID_PARAMS, "dev_create: internal schedule error (local dependency)");
+        }
+        if (next && (nloc || nrem)) fail(SCENOPT_E_INVALID_PARAMS, "dev_create: internal schedule error (mixed dependency)");
+        if (ld >= k) fail(SCENOPT_E_INVALID_PARAMS, "dev_create: internal schedule error (dependency order)");
+        if (nrem) {
+          r.gdep = 1;
+          for (int c = lo; c < hi; ++c) {
+            std::vector<Run>& owner = L[(*cta)[c]];
+            owner[(*pos)[c]].publish = 1;
+          }
+        } else if (nloc) {
           r.ldep = ld;
         }
-        for (int c = r.first; c < r.first + r.count; ++c) pos[c] = k;
       }
+  };
+
+  std::vector<Lists> launch_lists;
+  std::vector<std::pair<int, int>> full(static_cast<size_t>(p.N) + 1);
+  for (int t = 0; t <= p.N; ++t) full[t] = {p.stage_offsets[t], p.stage_offsets[t + 1]};
+  if (!shard) {
+    Lists bw_l, fw_l;
+    d->cut_stage = region(0, p.N, full, true, true, true, bw_l, fw_l);
+    for (int gg = 0; gg < G; ++gg) bw_l[gg].insert(bw_l[gg].end(), fw_l[gg].begin(), fw_l[gg].end());
+    launch_lists.push_back(std::move(bw_l));
+  } else {
+    int s = shard->stage;
+    const std::vector<int> bound = shard_plan(p, shard->world, &s);
+    d->shard_stage = s;
+    d->shard_lo = bound[shard->rank];
+    d->shard_hi = bound[shard->rank + 1];
+    d->sstage_lo = p.stage_offsets[s];
+    d->sstage_hi = p.stage_offsets[s + 1];
+    d->dual_top = p.dual_offset[p.stage_offsets[s]];
+    const auto own = descend(d->shard_lo, d->shard_hi, s, p.N);
+    Lists a_bw, a_fw, t_bw, t_fw, o_bw, o_fw;
+    d->cut_stage = region(s, p.N, own, true, true, false, a_bw, a_fw);
+    launch_lists.push_back(std::move(a_bw));
+    region(0, s - 1, full, false, true, true, t_bw, t_fw);
+    region(s, p.N, own, true, false, true, o_bw, o_fw);
+    for (int gg = 0; gg < G; ++gg) {
+      t_bw[gg].insert(t_bw[gg].end(), t_fw[gg].begin(), t_fw[gg].end());
+      t_bw[gg].insert(t_bw[gg].end(), o_fw[gg].begin(), o_fw[gg].end());
     }
+    launch_lists.push_back(std::move(t_bw));
   }
   std::vector<Run> runs;
-  std::vector<int32_t> cta_off(static_cast<size_t>(G) + 1, 0);
+  std::vector<std::vector<int32_t>> cta_offs;
   int nbw = 0;
-  for (int gg = 0; gg < G; ++gg) {
-    cta_off[gg] = static_cast<int32_t>(runs.size());
-    for (const Run& r : lists[gg]) {
-      runs.push_back(r);
-      nbw += r.pass == 0;
+  for (Lists& L : launch_lists) {
+    resolve(L);
+    std::vector<int32_t> off(static_cast<size_t>(G) + 1, 0);
+    const int base = static_cast<int>(runs.size());
+    for (int gg = 0; gg < G; ++gg) {
+      off[gg] = static_cast<int32_t>(runs.size()) - base;
+      for (const Run& r : L[gg]) {
+        runs.push_back(r);
+        nbw += r.pass == 0;
+      }
     }
+    off[G] = static_cast<int32_t>(runs.size()) - base;
+    cta_offs.push_back(std::move(off));
   }
-  cta_off[G] = static_cast<int32_t>(runs.size());
   d->items_bw = nbw;
   d->items_fw = static_cast<int>(runs.size()) - nbw;
-  d->cut_stage = cut;
 
   std::vector<Item> items(runs.size());
   std::vector<int64_t> item_doubles(runs.size());
@@ -498,8 +621,17 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->aff_bw = upload(*d, aff_bw);
   d->aff_fw = upload(*d, aff_fw);
   d->root_state = upload(*d, p.root_state);
-  d->items = upload(*d, items);
-  d->cta_off = upload(*d, cta_off);
+  {
+    size_t base = 0;
+    for (const auto& off : cta_offs) {
+      DevState::Launch ln;
+      ln.count = off.back();
+      ln.items = upload(*d, std::vector<Item>(items.begin() + base, items.begin() + base + ln.count));
+      ln.cta_off = upload(*d, off);
+      d->launches.push_back(ln);
+      base += ln.count;
+    }
+  }
   d->ctrl = d->alloc<unsigned>(4);
   d->bw_flag = d->alloc<unsigned>(static_cast<size_t>(n));
   d->fw_flag = d->alloc<unsigned>(static_cast<size_t>(n));
@@ -507,8 +639,28 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   SCN_CUDA(cudaMemset(d->bw_flag, 0, static_cast<size_t>(n) * sizeof(unsigned)));
   SCN_CUDA(cudaMemset(d->fw_flag, 0, static_cast<size_t>(n) * sizeof(unsigned)));
 
-  pack_common(*d, p);
+  std::vector<char> mine;
+  if (d->sharded()) {  // nodes whose cost this rank evaluates: own subtrees, top on rank 0
+    mine.assign(static_cast<size_t>(n), 0);
+    for (int c = 0; c < p.stage_offsets[d->shard_stage]; ++c) mine[c] = shard->rank == 0;
+    int lo = d->shard_lo, hi = d->shard_hi;
+    for (int t = d->shard_stage; t <= p.N; ++t) {
+      for (int c = lo; c < hi; ++c) mine[c] = 1;
+      if (t < p.N && lo < hi) {
+        const int nlo = p.child_begin[lo], nhi = p.child_begin[hi - 1] + p.child_count[hi - 1];
+        lo = nlo;
+        hi = nhi;
+      }
+    }
+  }
+  pack_common(*d, p, d->sharded() ? &mine : nullptr);
   const int D = p.dual_dim;
+  if (d->sharded()) {
+    d->rank = shard->rank;
+    d->world = shard->world;
+    d->xbuf = d->alloc<double>(static_cast<size_t>(kMaxRhs) * (d->sstage_hi - d->sstage_lo) * W);
+    if (shard->nccl_id) nccl_comm_init(*d, shard->nccl_id);  // else: exchange left to the caller (phase API)
+  }
 
   for (int r = 0; r < kMaxRhs; ++r) {
     d->contrib[r] = d->alloc<double>(static_cast<size_t>(n) * W);
@@ -541,7 +693,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
 namespace {
 // Per-dual-row nonsmooth data, apply_H rows and eval_f cost blocks: what
 // every handle needs, with or without the sweep layout.
-void pack_common(DevState& dd, const Problem& p) {
+void pack_common(DevState& dd, const Problem& p, const std::vector<char>* mine) {
   DevState* d = &dd;
   const int n = p.n, nx = p.nx, nu = p.nu, D = p.dual_dim, V = nx + nu;
   std::vector<int8_t> kind(static_cast<size_t>(D), 0);
@@ -592,11 +744,18 @@ void pack_common(DevState& dd, const Problem& p) {
   d->hrows.row_term = upload(*d, rterm);
   d->hrows.coef = upload(*d, coef);
   // eval_f blocks: [A | B | c | Q | S | R | q | r] per non-root node, [P | p] per leaf
+  // (a sharded handle keeps only the nodes it evaluates: its subtrees, and
+  // the replicated top on rank 0; the partial sums are allreduced)
+  std::vector<int32_t> nodes, leaves;
+  for (int i = 1; i < n; ++i)
+    if (!mine || (*mine)[i]) nodes.push_back(i);
+  for (int l = 0; l < p.L; ++l)
+    if (!mine || (*mine)[p.first_leaf + l]) leaves.push_back(p.first_leaf + l);
   const size_t csz = 2 * p.sxx() + 2 * p.sxu() + p.suu() + 2 * static_cast<size_t>(nx) + nu;
-  std::vector<double> cn(static_cast<size_t>(n > 1 ? n - 1 : 1) * csz, 0.0);
-  parallel_for(n - 1, 256, [&](int b, int e) {
+  std::vector<double> cn(std::max<size_t>(nodes.size(), 1) * csz, 0.0);
+  parallel_for(static_cast<int>(nodes.size()), 256, [&](int b, int e) {
     for (int t = b; t < e; ++t) {
-      const int i = t + 1;
+      const int i = nodes[t];
       double* o = cn.data() + static_cast<size_t>(t) * csz;
       o = std::copy(p.Ai(i), p.Ai(i) + p.sxx(), o);
       o = std::copy(p.Bi(i), p.Bi(i) + p.sxu(), o);
@@ -609,9 +768,10 @@ void pack_common(DevState& dd, const Problem& p) {
     }
   });
   const size_t lsz = p.sxx() + static_cast<size_t>(nx);
-  std::vector<double> cl(static_cast<size_t>(p.L) * lsz, 0.0);
-  for (int l = 0; l < p.L; ++l) {
-    double* o = cl.data() + static_cast<size_t>(l) * lsz;
+  std::vector<double> cl(std::max<size_t>(leaves.size(), 1) * lsz, 0.0);
+  for (size_t t = 0; t < leaves.size(); ++t) {
+    const int l = leaves[t] - p.first_leaf;
+    double* o = cl.data() + t * lsz;
     o = std::copy(p.Pl(l), p.Pl(l) + p.sxx(), o);
     std::copy(p.pl(l), p.pl(l) + nx, o);
   }
@@ -621,8 +781,13 @@ void pack_common(DevState& dd, const Problem& p) {
   d->cost.first_leaf = p.first_leaf;
   d->cost.anc = upload(*d, p.ancestor);
   d->cost.prob = upload(*d, p.probability);
+  d->cost.nodes = upload(*d, nodes);
+  d->cost.nnodes = static_cast<int>(nodes.size());
   d->cost.node = upload(*d, cn);
+  d->cost.leaves = upload(*d, leaves);
+  d->cost.nleaves = static_cast<int>(leaves.size());
   d->cost.leaf = upload(*d, cl);
+  d->cost.check_root = (!mine || (*mine)[0]) ? 1 : 0;
   d->cost.root_state = upload(*d, p.root_state);
   if (!d->root_state) d->root_state = const_cast<double*>(d->cost.root_state);
   if (!d->has_factor)
@@ -635,8 +800,9 @@ void pack_common(DevState& dd, const Problem& p) {
 }
 }  // namespace
 
-void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
-               double* const* u, double* const* Hx) {
+namespace {
+SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
+                         double* const* u, double* const* Hx) {
   if (nrhs < 1 || nrhs > kMaxRhs) fail(SCENOPT_E_INVALID_PARAMS, "sweep: nrhs must be 1 or 2");
   if (!d.has_factor) fail(SCENOPT_E_CACHE_MISMATCH, "sweep: handle was created without a factor cache");
   const Layout& L = d.lay;
@@ -646,7 +812,6 @@ void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, doubl
   P.n = L.n;
   P.first_leaf = L.first_leaf;
   P.dual_dim = L.dual_dim;
-  P.items_total = d.items_bw + d.items_fw;
   P.nslot = d.nslot;
   P.slot_doubles = d.slot_doubles;
   P.stage_doubles = d.stage_doubles;
@@ -657,8 +822,6 @@ void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, doubl
   P.max_count = d.max_count;
   P.nxp = d.nxp;
   P.Vp = d.Vp;
-  P.items = d.items;
-  P.cta_off = d.cta_off;
   P.bw_blk = d.bw_blk;
   P.fw_blk = d.fw_blk;
   P.aff_bw = d.aff_bw;
@@ -674,7 +837,87 @@ void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, doubl
     P.Hx[r] = (Hx && Hx[r]) ? Hx[r] : d.hs[r];
     P.contrib[r] = d.contrib[r];
   }
+  return P;
+}
+void launch(DevState& d, SweepParams& P, const DevState::Launch& ln) {
+  P.items = ln.items;
+  P.cta_off = ln.cta_off;
+  P.items_total = ln.count;
   SCN_CUDA(sweep_launch(P, d.grid, d.dyn_smem, d.max_m, d.max_mN, d.stream));
+}
+// sharded phase A: zero the outputs this rank does not own, local backward,
+// own shard-stage contributions into the (zeroed) exchange buffer
+void phase_a(DevState& d, SweepParams& P, bool gather_primal) {
+  const Layout& L = d.lay;
+  const int W = L.nx + L.nu;
+  const size_t ns = static_cast<size_t>(d.sstage_hi - d.sstage_lo);
+  for (int r = 0; r < P.nrhs; ++r) {
+    SCN_CUDA(cudaMemsetAsync(P.Hx[r], 0, sizeof(double) * L.dual_dim, d.stream));
+    if (gather_primal) {
+      SCN_CUDA(cudaMemsetAsync(P.x[r], 0, sizeof(double) * L.nx * L.n, d.stream));
+      SCN_CUDA(cudaMemsetAsync(P.u[r], 0, sizeof(double) * L.nu * L.first_leaf, d.stream));
+    }
+  }
+  launch(d, P, d.launches[0]);
+  SCN_CUDA(cudaMemsetAsync(d.xbuf, 0, sizeof(double) * P.nrhs * ns * W, d.stream));
+  for (int r = 0; r < P.nrhs; ++r)
+    SCN_CUDA(cudaMemcpyAsync(d.xbuf + (r * ns + (d.shard_lo - d.sstage_lo)) * W,
+                             P.contrib[r] + static_cast<size_t>(d.shard_lo) * W,
+                             sizeof(double) * (d.shard_hi - d.shard_lo) * W, cudaMemcpyDeviceToDevice, d.stream));
+}
+// sharded phase B: summed contributions back, top backward + forward, and
+// the replicated top rows of Hx kept on rank 0 only
+void phase_b(DevState& d, SweepParams& P) {
+  const Layout& L = d.lay;
+  const int W = L.nx + L.nu;
+  const size_t ns = static_cast<size_t>(d.sstage_hi - d.sstage_lo);
+  for (int r = 0; r < P.nrhs; ++r)
+    SCN_CUDA(cudaMemcpyAsync(P.contrib[r] + static_cast<size_t>(d.sstage_lo) * W, d.xbuf + r * ns * W,
+                             sizeof(double) * ns * W, cudaMemcpyDeviceToDevice, d.stream));
+  launch(d, P, d.launches[1]);
+  if (d.rank != 0)
+    for (int r = 0; r < P.nrhs; ++r)
+      SCN_CUDA(cudaMemsetAsync(P.Hx[r], 0, d.dual_top * sizeof(double), d.stream));
+}
+}  // namespace
+
+void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
+               double* const* u, double* const* Hx, bool gather_primal) {
+  SweepParams P = sweep_params(d, nrhs, affine, y, x, u, Hx);
+  if (!d.sharded()) {
+    launch(d, P, d.launches[0]);
+    return;
+  }
+  // sharded: A (local backward) | allreduce contributions | B (top + local forward) | allreduce Hx
+  const int W = d.lay.nx + d.lay.nu;
+  const size_t ns = static_cast<size_t>(d.sstage_hi - d.sstage_lo);
+  phase_a(d, P, gather_primal);
+  dev_allreduce(d, d.xbuf, static_cast<size_t>(nrhs) * ns * W);
+  phase_b(d, P);
+  for (int r = 0; r < nrhs; ++r) dev_allreduce(d, P.Hx[r], static_cast<size_t>(d.lay.dual_dim));
+  if (gather_primal)
+    for (int r = 0; r < nrhs; ++r) dev_gather_primal(d, P.x[r], P.u[r]);
+}
+
+void dev_sweep_phase(DevState& d, int phase, int nrhs, bool affine, const double* const* y, double* const* Hx) {
+  if (!d.sharded()) fail(SCENOPT_E_INVALID_PARAMS, "sweep phase: handle is not sharded");
+  SweepParams P = sweep_params(d, nrhs, affine, y, nullptr, nullptr, Hx);
+  if (phase == 0)
+    phase_a(d, P, false);
+  else
+    phase_b(d, P);
+}
+
+void dev_gather_primal(DevState& d, double* x, double* u) {
+  if (!d.sharded()) return;
+  const Layout& L = d.lay;
+  // top nodes [0, sstage_lo) are replicated: keep rank 0's copy only
+  if (d.rank != 0) {
+    SCN_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * L.nx * d.sstage_lo, d.stream));
+    SCN_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * L.nu * d.sstage_lo, d.stream));
+  }
+  dev_allreduce(d, x, static_cast<size_t>(L.nx) * L.n);
+  dev_allreduce(d, u, static_cast<size_t>(L.nu) * L.first_leaf);
 }
 
 }  // namespace scn

@@ -46,9 +46,24 @@ struct DevState {
   // packed matrices and metadata
   double *bw_blk = nullptr, *fw_blk = nullptr, *aff_bw = nullptr, *aff_fw = nullptr,
          *root_state = nullptr;
-  Item* items = nullptr;
-  int32_t* cta_off = nullptr;  // [grid + 1] per-CTA item ranges
-  int cut_stage = -1;          // subtree-ownership cut (-1: all items are global tickets)
+  // Sweep launches: one (unsharded), or two for a sharded handle (local
+  // backward below the rank cut, then top backward + forward), each with
+  // CTA-major items and per-CTA ranges [cta_off[b], cta_off[b+1]).
+  struct Launch {
+    Item* items = nullptr;
+    int32_t* cta_off = nullptr;
+    int count = 0;
+  };
+  std::vector<Launch> launches;
+  int cut_stage = -1;  // CTA subtree-ownership cut of the main region (-1: all global tickets)
+  // ---- subtree sharding over ranks
+  int rank = 0, world = 1, shard_stage = -1;
+  void* comm = nullptr;         // ncclComm_t
+  int shard_lo = 0, shard_hi = 0;  // this rank's shard-stage nodes
+  int sstage_lo = 0, sstage_hi = 0;  // all shard-stage nodes [stage_offsets[s], stage_offsets[s+1])
+  int64_t dual_top = 0;          // dual rows of the replicated top stages (a prefix)
+  double* xbuf = nullptr;        // exchange buffer: shard-stage contributions, kMaxRhs x ns x (nu+nx)
+  bool sharded() const { return shard_stage >= 0; }
   unsigned *ctrl = nullptr, *bw_flag = nullptr, *fw_flag = nullptr;
   int64_t bw_doubles = 0, fw_doubles = 0;
   int items_bw = 0, items_fw = 0, max_count = 1, max_m = 0, max_mN = 0, nxp = 0, Vp = 0;
@@ -78,6 +93,7 @@ struct DevState {
     void* p = nullptr;
     SCN_CUDA(cudaMalloc(&p, count * sizeof(T) + 16));
     owned.push_back(p);
+    SCN_CUDA(cudaMemset(p, 0, count * sizeof(T) + 16));  // sharded outputs rely on zero fill
     bytes_allocated += count * sizeof(T);
     return static_cast<T*>(p);
   }
@@ -88,13 +104,37 @@ struct DevState {
 // verification) without the sweep layout.
 // Bare context (device, stream, SM count) for problem-free device objects.
 std::unique_ptr<DevState> dev_create_bare(int device);
-std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* f, int device);
+struct ShardSpec {
+  int rank = 0, world = 1;
+  int stage = -1;              // shard cut stage (-1: smallest stage with >= world nodes)
+  const void* nccl_id = nullptr;  // 128-byte ncclUniqueId shared by all ranks
+};
+// Host-only shard plan: *stage (in: -1 = auto) and the world+1 bounds of the
+// ranks' contiguous shard-stage node ranges, balanced by subtree bytes.
+std::vector<int> shard_plan(const Problem& p, int world, int* stage);
+std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* f, int device,
+                                     const ShardSpec* shard = nullptr);
+// ncclGetUniqueId into 128 bytes
+void nccl_unique_id(void* out128);
+void nccl_comm_init(DevState& d, const void* id128);
+void nccl_comm_destroy(void* comm);
+// Sum-allreduce of n doubles on the handle's stream (no-op unsharded).
+void dev_allreduce(DevState& d, double* buf, size_t n);
 int device_count_sm100();
 
 // One fused sweep over nrhs right-hand sides; y/x/u/Hx are device pointers
 // (x/u/Hx may be null: the handle's scratch is used). Enqueued on d.stream.
+// Sharded handles: Hx is assembled on every rank; x/u hold this rank's nodes
+// plus the replicated top unless gather_primal assembles them in full.
 void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
-               double* const* u, double* const* Hx);
+               double* const* u, double* const* Hx, bool gather_primal = false);
+// One phase of a sharded sweep with the exchange left to the caller (phase 0:
+// zero Hx, local backward, own contributions into d.xbuf; phase 1: xbuf
+// (summed over ranks by the caller) back, top backward + forward, top rows
+// of Hx zeroed on ranks != 0). Emulation / tests of handles without NCCL.
+void dev_sweep_phase(DevState& d, int phase, int nrhs, bool affine, const double* const* y, double* const* Hx);
+// Assemble a sharded primal point in full on every rank (x: nx*n, u: nu*F).
+void dev_gather_primal(DevState& d, double* x, double* u);
 
 // kernel launchers (cuda/*.cu)
 int sweep_teams();

@@ -40,7 +40,7 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
       hd[r] = Hx ? Hx[r] : nullptr;
     }
   }
-  dev_sweep(*d, nrhs, affine, yd, xd, ud, hd);
+  dev_sweep(*d, nrhs, affine, yd, xd, ud, hd, (x != nullptr) || (u != nullptr));
   if (host) {
     for (int r = 0; r < nrhs; ++r) {
       if (x && x[r]) out_copy(x[r], d->xs[r], static_cast<size_t>(L.nx) * L.n, flags);

@@ -179,6 +179,7 @@ struct Engine {
     SCN_CUDA(cudaMemsetAsync(k.tmp, 0, D() * sizeof(double), st));
     sweep1(true, k.tmp, k.x0, k.u0, k.Hx0);
     SCN_CUDA(k_eval_f(ctx(), d.cost, k.x0, k.u0, 1e-8, st));
+    dev_allreduce(d, k.S + sl::EVALF, 2);  // sharded: partial f and infeasibility count
     read_scalars();
     const double f0 = S(sl::EVALF);
     if (S(sl::EVALF_INF) != 0.0 || !std::isfinite(f0))
@@ -280,6 +281,7 @@ struct Loop {
       if (!dst.empty())
         SCN_CUDA(cudaMemcpyAsync(dst.data(), src, dst.size() * sizeof(double), cudaMemcpyDeviceToHost, e.st));
     };
+    dev_gather_primal(e.d, e.k.x[s], e.k.u[s]);  // sharded: assemble the full point
     dl(rep.x, e.k.x[s]);
     dl(rep.u, e.k.u[s]);
     dl(rep.y, e.k.y[s]);
@@ -608,6 +610,7 @@ int scenopt_fhat_value(scenopt_dev* h, const double* y, double* out, int flags) 
     e.sweep1(true, yd, e.k.x[1], e.k.u[1], e.k.Hx[1]);
     ++h->stats.dual_grad_calls;
     SCN_CUDA(k_eval_f(e.ctx(), h->d->cost, e.k.x[1], e.k.u[1], 1e-8, e.st));
+    dev_allreduce(*h->d, e.k.S + sl::EVALF, 2);
     SCN_CUDA(k_dot(e.ctx(), e.k.Hx[1], yd, e.st));
     e.read_scalars();
     const double f = e.S(sl::EVALF_INF) != 0.0 ? std::numeric_limits<double>::infinity() : e.S(sl::EVALF);
@@ -673,6 +676,7 @@ int scenopt_fb_step(scenopt_dev* h, const double* y, double lambda, double* x, d
     auto& k = e.k;
     e.fb_step(0, h->in_dual(y, flags, 0), lambda, nullptr, h->stats);
     const Layout& L = h->d->lay;
+    if (x || u) dev_gather_primal(*h->d, k.x[0], k.u[0]);
     h->out_copy(x, k.x[0], static_cast<size_t>(L.nx) * L.n, flags);
     h->out_copy(u, k.u[0], static_cast<size_t>(L.nu) * L.first_leaf, flags);
     h->out_copy(Hx, k.Hx[0], e.D(), flags);

@@ -1,0 +1,140 @@
+"""Subtree sharding on one B200.
+
+* world = 1 with a real NCCL communicator: the two-launch sharded sweep
+  (local backward | contribution allreduce | top + forward | Hx allreduce)
+  must reproduce the single-launch handle bitwise, and so must whole solves.
+* W emulated ranks (handles without a communicator, exchange done here on
+  the host through the phase API): each rank packs only its own subtrees;
+  summing the ranks' exchange buffers and Hx must reproduce the unsharded
+  Hx (every row is nonzero on exactly one rank, so the exchange itself is
+  exact; the per-item summation order depends on how a shard's nodes are
+  grouped into items, hence 1e-12 rather than bitwise). Kernels of
+  different ranks never wait on one another: the exchange sits between
+  launches."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2107_01745_b200 as so
+from paper_2107_01745_b200 import _native as N
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+P = C.POINTER(C.c_double)
+
+
+def shapes():
+    rng = orc.Rng(77)
+    return [so.gen_random_instance(2, 6, 3, 9, [3, 1, 4, 2]),
+            so.gen_random_instance(3, 5, 2, 8, [2, 2, 2, 2, 2]),
+            so.ProblemInstance.from_flat(rng.random_instance(6, 400, 3, 2,
+                                                             orc.InstanceOptions(with_l1=True)).flat())]
+
+
+def both_handles(prob, world=1, rank=0, nccl=True, stage=-1):
+    full = so.factor(prob)
+    shard = so.factor(prob)
+    shard.shard(rank, world, so.nccl_unique_id() if nccl else None, 0, stage)
+    return full, shard
+
+
+@pytest.mark.parametrize("stage", [-1, 2])
+def test_world1_sharded_sweep_is_bitwise_the_single_launch(gpu, stage):
+    for prob in shapes():
+        full, shard = both_handles(prob, stage=stage)
+        info = shard.dev_info()
+        assert info["world"] == 1 and info["shard_stage"] == (1 if stage < 0 else stage)
+        rng = np.random.default_rng(3)
+        y = rng.uniform(-1, 1, prob.dual_dim)
+        r = rng.uniform(-1, 1, prob.dual_dim)
+        for affine in (True, False):
+            pf, hf = so.sweep(full, [y, r], affine)
+            ps, hs = so.sweep(shard, [y, r], affine)
+            for k in range(2):
+                assert np.array_equal(hf[k], hs[k])
+        a = so.dual_grad(full, prob, y)
+        b = so.dual_grad(shard, prob, y)
+        assert np.array_equal(a.x, b.x) and np.array_equal(a.u, b.u)
+
+
+def test_world1_sharded_solves_reproduce_the_single_launch(gpu):
+    prob = so.gen_random_instance(5, 6, 3, 8, [3, 3, 2])
+    full, shard = both_handles(prob)
+    for kind in ("minfbe", "nama"):
+        cfg = so.SolverConfig(nama_parallel_linesearch=(kind == "nama"))
+        a = so.api._solve_direct(kind, prob, full, cfg)
+        b = so.api._solve_direct(kind, prob, shard, cfg)
+        assert a.status == b.status == "converged"
+        assert a.iterations == b.iterations
+        assert np.array_equal(a.y, b.y) and np.array_equal(a.x.x, b.x.x)
+        assert a.stats.dual_grad_calls == b.stats.dual_grad_calls
+
+
+class EmulatedRank:
+    def __init__(self, prob, rank, world, stage):
+        self.cache = so.factor(prob)
+        self.cache.shard(rank, world, None, 0, stage)
+        self.dev = self.cache.device()
+        self.lib = N.lib()
+        self.D = prob.dual_dim
+        self.y = [self._alloc(self.D) for _ in range(2)]
+        self.h = [self._alloc(self.D) for _ in range(2)]
+        buf, n = P(), C.c_size_t()
+        so.api.check(self.lib.scenopt_shard_exchange_buffer(self.dev, C.byref(buf), C.byref(n)))
+        self.xbuf, self.nx = C.cast(buf, C.c_void_p).value, n.value
+
+    def _alloc(self, n):
+        p = C.c_void_p()
+        so.api.check(self.lib.scenopt_dev_alloc(self.dev, C.c_size_t(8 * n), C.byref(p)))
+        return p.value
+
+    def put(self, dst, arr):
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        so.api.check(self.lib.scenopt_dev_memcpy(self.dev, C.c_void_p(dst), a.ctypes.data_as(C.c_void_p),
+                                                 C.c_size_t(a.nbytes), 1))
+
+    def get(self, src, n):
+        a = np.empty(n)
+        so.api.check(self.lib.scenopt_dev_memcpy(self.dev, a.ctypes.data_as(C.c_void_p), C.c_void_p(src),
+                                                 C.c_size_t(8 * n), 2))
+        return a
+
+    def phase(self, ph, nrhs, affine):
+        Y = (P * 2)(*[C.cast(C.c_void_p(p), P) for p in self.y])
+        H = (P * 2)(*[C.cast(C.c_void_p(p), P) for p in self.h])
+        so.api.check(self.lib.scenopt_shard_sweep_phase(self.dev, ph, nrhs, int(affine), Y, H))
+        so.api.check(self.lib.scenopt_dev_synchronize(self.dev))
+
+
+@pytest.mark.parametrize("world,stage,grid", [(2, -1, 0), (3, 2, 0), (4, 3, 6), (2, 4, 3)])
+def test_emulated_ranks_reassemble_the_unsharded_sweep(gpu, monkeypatch, world, stage, grid):
+    if grid:
+        monkeypatch.setenv("SCENOPT_GRID", str(grid))  # force CTA-level cuts inside the shards
+        monkeypatch.setenv("SCENOPT_MIN_SUBTREES", "1")
+    for prob in shapes():
+        counts = np.diff(prob.flat()["stage_offsets"])
+        st = stage if stage > 0 else int(np.argmax(counts >= world))
+        if st > prob.num_stages or counts[st] < world:
+            continue
+        full = so.factor(prob)
+        ranks = [EmulatedRank(prob, r, world, st) for r in range(world)]
+        infos = [rk.cache.dev_info() for rk in ranks]
+        assert infos[0]["shard_first"] == prob.flat()["stage_offsets"][st]
+        assert all(infos[i]["shard_past"] == infos[i + 1]["shard_first"] for i in range(world - 1))
+        rng = np.random.default_rng(world)
+        ys = [rng.uniform(-1, 1, prob.dual_dim) for _ in range(2)]
+        for nrhs, affine in ((1, True), (2, False), (2, True)):
+            for rk in ranks:
+                for k in range(nrhs):
+                    rk.put(rk.y[k], ys[k])
+                rk.phase(0, nrhs, affine)
+            total = sum(rk.get(rk.xbuf, nrhs * rk.nx) for rk in ranks)
+            for rk in ranks:
+                rk.put(rk.xbuf, total)
+                rk.phase(1, nrhs, affine)
+            _, want = so.sweep(full, ys[:nrhs], affine)
+            for k in range(nrhs):
+                got = sum(rk.get(rk.h[k], prob.dual_dim) for rk in ranks)
+                err = np.abs(got - want[k]).max() / (1.0 + np.abs(want[k]).max())
+                assert err < 1e-12, (world, st, nrhs, affine, err)

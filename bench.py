@@ -34,6 +34,7 @@ CONFIGS = {
     # id: (nx, nu, N, branching, label)
     "c3": (50, 20, 20, [8, 8, 8, 2], "C3: MINFBE/NAMA ~1M-variable tree (nx=50, nu=20, N=20, branching [8,8,8,2])"),
     "c1": (10, 5, 10, [2, 2, 2], "C1: small tree (nx=10, nu=5, N=10, branching [2,2,2])"),
+    "c4": (50, 20, 20, [8, 8, 8, 8, 4], "C4: NAMA ~20M-variable tree (nx=50, nu=20, N=20, branching [8,8,8,8,4])"),
     "c5a": (10, 5, 20, [2] * 13, "C5: oracle microbench, 73,727 nodes (nx=10, nu=5, N=20, [2]x13)"),
     "c5b": (10, 5, 20, [4] * 8, "C5: oracle microbench, 873,813 nodes (nx=10, nu=5, N=20, [4]x8)"),
     "c5c": (50, 20, 20, [4] * 6, "C5: oracle microbench, 60,074 nodes (nx=50, nu=20, N=20, [4]x6)"),
@@ -163,6 +164,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-shard", action="store_true",
+                    help="use the sharded (NCCL) handle even at one GPU (exercises the N>1 path)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -183,9 +186,25 @@ def main():
     torch.cuda.set_device(device)
 
     nx, nu, N, br, label = CONFIGS[args.config]
+    units = 1  # C3-sized evaluations per sweep of the benchmarked tree
+    sharded = world > 1 or args.force_shard
+    if sharded:
+        # Weak scaling over subtree shards: N GPUs solve ONE tree
+        # of N C3-sized subtrees, branching [8N, 8, 8, 2] (N = 1 is exactly
+        # C3), sharded at stage 1 -- each rank owns 8 of the 8N stage-1
+        # subtrees and replicates the root; every sweep exchanges the stage-1
+        # contributions and assembles Hx with NCCL allreduces.
+        br = [br[0] * world] + list(br[1:])
+        units = world
+        label = f"{label}; x{world} sharded: one tree [{', '.join(map(str, br))}] over {world} GPUs"
     t0 = time.time()
     prob = so.gen_random_instance(1, nx, nu, N, br)
     cache = so.factor(prob)
+    if sharded:
+        nid = [so.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(nid, src=0)
+        cache.shard(rank, world, nid[0], device=device, stage=1)
     dev = cache.device(device)
     setup_s = time.time() - t0
     info = cache.dev_info()
@@ -242,8 +261,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_s = float(t[0]), float(t[1])
         dist.barrier()
-    value = world * 1e3 / ms
-    e2e_value = world / e2e_s
+    value = units * 1e3 / ms
+    e2e_value = units / e2e_s
 
     # time-to-tolerance: MINFBE and NAMA from y0 = 0 with the reference
     # defaults. As in solve() (solvers.hpp:668-679), L is estimated once by
@@ -269,14 +288,14 @@ def main():
                          "lambda0": cfg.lambda0}
 
     peaks, peak_src = measured_peaks()
-    bytes_step = info["sweep_bytes_aff"]
-    achieved = bytes_step / (ms * 1e-3) / 1e9
+    bytes_step = info["sweep_bytes_aff"]  # algorithmic bytes of the whole tree
+    achieved = bytes_step / world / (ms * 1e-3) / 1e9  # per GPU
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
+                traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch") if not sharded else None
         except (OSError, ValueError):
             traffic = None
     out = {
@@ -285,7 +304,11 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded gen_random_instance, seed 1; random-system tree)",
         "config": {"workload": label, "nodes": prob.num_nodes(), "primal_dim": prob.primal_dim(),
-                   "dual_dim": D, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "dual_dim": D,
+                   "parallelism": (f"subtree shards x{world} (stage 1, NCCL allreduce of stage-1 "
+                                   f"contributions + Hx per sweep)") if sharded else "1 GPU",
+                   "value_units": "C3-sized dual-grad evaluations (a sweep of the x{0} tree counts {0})"
+                                  .format(units),
                    "l2": "inputs larger than L2 (packed matrices %.2f GB vs 126 MB L2)"
                          % ((info["matrix_bytes_bw"] + info["matrix_bytes_fw"]) / 1e9),
                    "setup_s": round(setup_s, 2), "grid_ctas": info["grid_ctas"],
@@ -296,7 +319,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "dual-grad evals/s",
                 "h2d_bytes_per_step": 8 * D,
                 "d2h_bytes_per_step": 8 * (nx * prob.num_nodes() + nu * prob.first_leaf)},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * (2 if sharded else 1),
         "time_to_tolerance": ttt,
         "clocks": clk.summary(),
     }

@@ -307,8 +307,8 @@ def main():
                    "dual_dim": D,
                    "parallelism": (f"subtree shards x{world} (stage 1, NCCL allreduce of stage-1 "
                                    f"contributions + Hx per sweep)") if sharded else "1 GPU",
-                   "value_units": "C3-sized dual-grad evaluations (a sweep of the x{0} tree counts {0})"
-                                  .format(units),
+                   "value_units": ("C3-sized dual-grad evaluations (a sweep of the x{0} tree counts {0})"
+                                   .format(units)) if sharded else "dual-grad evaluations of the tree",
                    "l2": "inputs larger than L2 (packed matrices %.2f GB vs 126 MB L2)"
                          % ((info["matrix_bytes_bw"] + info["matrix_bytes_fw"]) / 1e9),
                    "setup_s": round(setup_s, 2), "grid_ctas": info["grid_ctas"],

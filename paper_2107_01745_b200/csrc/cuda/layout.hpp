@@ -71,6 +71,7 @@ constexpr int kMaxSlots = 8;
 struct SweepParams {
   int nx, nu, n, first_leaf, dual_dim;
   int items_total;
+  int items_base;  // index of this launch's first item in the handle's item order (profiling)
   int nslot, slot_doubles, stage_doubles, scratch_doubles;
   int nrhs, affine, G, max_count;
   int nxp, Vp;  // padded column lengths (== 2 mod 4) of J/K/TN and W

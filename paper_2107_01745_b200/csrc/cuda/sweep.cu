@@ -52,11 +52,15 @@ namespace {
 constexpr int kTeam = 128;  // threads per consumer team
 constexpr int kTeams = 2;
 constexpr int kProducers = 4;  // producer warps (== slots), warp p stages items k = p (mod 4)
-constexpr int kThreads = 32 * kProducers + kTeams * kTeam + 32;  // producers, teams, publisher
+constexpr int kThreads = 32 * kProducers + kTeams * kTeam + 64;  // producers, teams, publisher, issuer
 constexpr int kTeamWarp0 = kProducers;
-constexpr int kStageQ = 8;  // staging ring depth (items staged ahead)
+constexpr int kStageQ = 8;  // staging ring depth (items staged ahead); a multiple of kProducers
+                            // and even, so each staging area always serves the same producer
+                            // warp and the same team in order
+static_assert(kStageQ % kProducers == 0 && kStageQ % 2 == 0, "staging ring vs producers / teams");
 constexpr int kDoneQ = 16;  // completion ring depth (publisher lag allowed)
 constexpr int kPublisherWarp = kProducers + kTeams * kTeam / 32;
+constexpr int kIssuerWarp = kPublisherWarp + 1;
 
 #ifdef SCN_SWEEP_PROFILE
 // cycle counters: [0] prod stage-empty wait [1] prod stage round trip
@@ -64,6 +68,12 @@ constexpr int kPublisherWarp = kProducers + kTeams * kTeam / 32;
 // [5] team compute [6] team refill + publish back-pressure [7] publisher fence
 __device__ unsigned long long g_prof[16];
 __device__ int g_dbg;  // timing experiments only: bit0 ignore dependencies, bit1 skip compute
+__device__ unsigned long long* g_timeline;  // per item: globaltimer at retirement (null: off)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 #define DBG(bit) (g_dbg & (bit))
 #define PROF_T0() long long _pt = clock64()
 #define PROF_T1(slot)                                                                          \
@@ -479,14 +489,19 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
 template <int NRHS>
 __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P, int mmax, int mNmax) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t full[kMaxSlots], sfull[kStageQ], sempty[kStageQ], done[kDoneQ],
+  // full[k mod 2*NS]: the matrix-slot barrier of item k. Two per slot, so a
+  // barrier always serves the same consumer team in order (k and k + 2NS
+  // have the same parity) whatever NS is: a team can never test a phase
+  // parity of a use that has not started yet.
+  __shared__ __align__(8) uint64_t full[2 * kMaxSlots], sfull[kStageQ], sempty[kStageQ], done[kDoneQ],
       pdone[kDoneQ];
+  __shared__ __align__(8) uint64_t mempty[kMaxSlots];  // slot consumed (team -> issuer)
   __shared__ __align__(16) Item sitem[kMaxSlots];
   __shared__ __align__(16) int4 sdone[kDoneQ];  // {first, count, pass, publish} of finished items
   __shared__ unsigned s_epoch;
   __shared__ int s_retired;  // items [0, s_retired) of this CTA are complete
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NS = P.nslot;  // matrix slots (even, so a slot stays with one team)
+  const int NS = P.nslot;  // matrix slots
   double* slots = smem;
   double* stages = smem + static_cast<int64_t>(NS) * P.slot_doubles;  // kStageQ staging areas
   double* scratch = stages + static_cast<int64_t>(kStageQ) * P.stage_doubles;  // per team
@@ -497,15 +512,17 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   auto issue = [&](int k, const Item& it) {  // one thread
     const int s = k % NS;
     sitem[s] = it;
-    mbar_arrive_expect_tx(&full[s], static_cast<unsigned>(it.bytes));
+    uint64_t* fb = &full[k % (2 * NS)];
+    mbar_arrive_expect_tx(fb, static_cast<unsigned>(it.bytes));
     tma_load_1d(slots + static_cast<int64_t>(s) * P.slot_doubles, (it.pass == 0 ? P.bw_blk : P.fw_blk) + it.off,
-                static_cast<unsigned>(it.bytes), &full[s]);
+                static_cast<unsigned>(it.bytes), fb);
   };
 
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile unsigned*>(P.ctrl) + 1u;
     s_retired = 0;
-    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < 2 * NS; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&mempty[s], 1);
     for (int q = 0; q < kStageQ; ++q) {
       mbar_init(&sfull[q], 1);
       mbar_init(&sempty[q], 1);
@@ -519,9 +536,6 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   for (int i = tid; i < kTeams * P.scratch_doubles; i += kThreads) scratch[i] = 0.0;  // zero pads of w / x
   __syncthreads();
   const unsigned E = s_epoch;
-  if (tid == 0)
-    for (int k = 0; k < NS && k < K; ++k) issue(k, items[k]);
-
   if (warp < kProducers) {
     // ------------------------------------------------------------ producers
     // Producer warp p stages items k = p (mod kProducers) into staging area
@@ -555,11 +569,8 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
     double* tbuf = scratch + team * P.scratch_doubles;
     for (int k = team; k < K; k += kTeams) {
       const int s = k % NS;
-      const bool refill = k + NS < K;
-      Item nxt{};
-      if (ttid == 0 && refill) nxt = items[k + NS];
       PROF_T0();
-      mbar_wait(&full[s], static_cast<unsigned>((k / NS) & 1));
+      mbar_wait(&full[k % (2 * NS)], static_cast<unsigned>((k / (2 * NS)) & 1));
       if (ttid == 0) PROF_T1(3);
       const int q = k % kStageQ;
       mbar_wait(&sfull[q], static_cast<unsigned>((k / kStageQ) & 1));
@@ -575,9 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       team_sync(team);
       if (ttid == 0) PROF_T1(5);
       if (ttid == 0) {
+        mbar_arrive(&mempty[s]);  // slot reads done (team_sync) -> the issuer may refill it
         mbar_arrive(&sempty[q]);
-        fence_proxy_async();  // generic reads of the slot before the async-proxy refill
-        if (refill) issue(k + NS, nxt);
         // the publisher must have retired item k-kDoneQ before its DONE phase reuses
         const int dq = k % kDoneQ;
         if (k >= kDoneQ) mbar_wait(&pdone[dq], static_cast<unsigned>((k / kDoneQ - 1) & 1));
@@ -585,6 +595,20 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
         mbar_arrive(&done[dq]);
       }
       if (ttid == 0) PROF_T1(6);
+    }
+  }
+  if (warp == kIssuerWarp) {
+    // ------------------------------------------------------------ issuer
+    // One thread streams the CTA's items through the matrix slots in order:
+    // item k goes to slot k mod NS once the team holding item k - NS has
+    // released it (mbarrier, so generic reads precede the async-proxy
+    // write), as one 1-D bulk copy completing on full[k mod 2NS].
+    if (lane == 0) {
+      for (int k = 0; k < K; ++k) {
+        const Item it = items[k];
+        if (k >= NS) mbar_wait(&mempty[k % NS], static_cast<unsigned>((k / NS - 1) & 1));
+        issue(k, it);
+      }
     }
   }
   if (warp == kPublisherWarp) {
@@ -619,6 +643,12 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       __syncwarp();
       if (lane == 0) {
         st_release_cta(&s_retired, j);
+#ifdef SCN_SWEEP_PROFILE
+        if (g_timeline) {
+          const unsigned long long now = gtimer();
+          for (int q2 = k; q2 < j; ++q2) g_timeline[P.cta_off[b] + q2 + P.items_base] = now;
+        }
+#endif
         PROF_T1(7);
         for (int q2 = k; q2 < j; ++q2) mbar_arrive(&pdone[q2 % kDoneQ]);
       }
@@ -642,6 +672,15 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 int sweep_threads() { return kThreads; }
 int sweep_teams() { return kTeams; }
 int sweep_stage_queue() { return kStageQ; }
+
+cudaError_t sweep_timeline(unsigned long long* dev_buf) {
+#ifdef SCN_SWEEP_PROFILE
+  return cudaMemcpyToSymbol(g_timeline, &dev_buf, sizeof(dev_buf));
+#else
+  (void)dev_buf;
+  return cudaErrorNotSupported;
+#endif
+}
 
 cudaError_t sweep_profile_read(unsigned long long* out, bool reset) {
 #ifdef SCN_SWEEP_PROFILE

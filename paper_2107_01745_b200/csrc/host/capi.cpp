@@ -274,4 +274,37 @@ int scenopt_debug_sweep_profile(unsigned long long* out16, int reset) {
   SCN_GUARD(SCN_CUDA(sweep_profile_read(out16, reset != 0)));
 }
 
+// Profiling build only: per-item retirement timestamps into dev_buf (one
+// u64 per item in handle order; NULL switches the timeline off).
+int scenopt_debug_sweep_timeline(void* dev_buf) {
+  SCN_GUARD(SCN_CUDA(sweep_timeline(static_cast<unsigned long long*>(dev_buf))));
+}
+
+// Items in handle order: {launch, cta, pass, first, count, ldep, publish} x n.
+int scenopt_debug_items(scenopt_dev* h, int32_t* out, int cap) {
+  int total = 0;
+  try {
+    const DevState& d = *h->d;
+    int li = 0;
+    for (const auto& ln : d.launches) {
+      std::vector<Item> it(static_cast<size_t>(ln.count));
+      std::vector<int32_t> off(static_cast<size_t>(d.grid) + 1);
+      SCN_CUDA(cudaMemcpy(it.data(), ln.items, it.size() * sizeof(Item), cudaMemcpyDeviceToHost));
+      SCN_CUDA(cudaMemcpy(off.data(), ln.cta_off, off.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      for (int b = 0; b < d.grid; ++b)
+        for (int k = off[b]; k < off[b + 1]; ++k, ++total)
+          if (out && total < cap) {
+            int32_t* o = out + 7 * total;
+            o[0] = li, o[1] = b, o[2] = it[k].pass, o[3] = it[k].first, o[4] = it[k].count, o[5] = it[k].ldep,
+            o[6] = it[k].publish;
+          }
+      ++li;
+    }
+    return total;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  }
+}
+
 }  // extern "C"

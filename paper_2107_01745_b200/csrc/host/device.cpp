@@ -591,7 +591,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
             static_cast<size_t>(teams) * d->vec_doubles) * dbl;
   };
   int best_ns = 0;
-  for (int ns = 4; ns >= 2; ns -= 2) {  // even: a slot stays with one consumer team
+  const int ns_max = std::min(kMaxSlots, std::max(2, env_int("SCENOPT_NSLOT_MAX", 5)));
+  for (int ns = ns_max; ns >= 2; --ns) {
     if (force_ns && ns != force_ns) continue;
     const size_t smem = smem_for(ns);
     if (smem > static_cast<size_t>(prop.sharedMemPerBlockOptin)) continue;
@@ -840,6 +841,7 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
   return P;
 }
 void launch(DevState& d, SweepParams& P, const DevState::Launch& ln) {
+  P.items_base = static_cast<int>(&ln - d.launches.data()) == 0 ? 0 : d.launches[0].count;
   P.items = ln.items;
   P.cta_off = ln.cta_off;
   P.items_total = ln.count;

@@ -141,6 +141,7 @@ int sweep_teams();
 int sweep_stage_queue();
 cudaError_t sweep_configure(size_t dyn_smem);
 cudaError_t sweep_profile_read(unsigned long long* out, bool reset);
+cudaError_t sweep_timeline(unsigned long long* dev_buf);
 cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem);
 cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax,
                          cudaStream_t stream);

@@ -50,15 +50,18 @@ namespace scn {
 namespace {
 
 constexpr int kTeam = 128;  // threads per consumer team
-constexpr int kTeams = 2;
+#ifndef SCN_TEAMS
+#define SCN_TEAMS 3
+#endif
+constexpr int kTeams = SCN_TEAMS;  // consumer teams (items k = team mod kTeams)
 constexpr int kProducers = 4;  // producer warps (== slots), warp p stages items k = p (mod 4)
 constexpr int kThreads = 32 * kProducers + kTeams * kTeam + 64;  // producers, teams, publisher, issuer
 constexpr int kTeamWarp0 = kProducers;
-constexpr int kStageQ = 8;  // staging ring depth (items staged ahead); a multiple of kProducers
+constexpr int kStageQ = kTeams == 3 ? 12 : 8;  // staging ring depth (items staged ahead); a multiple of kProducers
                             // and even, so each staging area always serves the same producer
                             // warp and the same team in order
-static_assert(kStageQ % kProducers == 0 && kStageQ % 2 == 0, "staging ring vs producers / teams");
-constexpr int kDoneQ = 16;  // completion ring depth (publisher lag allowed)
+static_assert(kStageQ % kProducers == 0 && kStageQ % kTeams == 0, "staging ring vs producers / teams");
+constexpr int kDoneQ = 8 * kTeams;  // completion ring depth (publisher lag allowed); a multiple of kTeams
 constexpr int kPublisherWarp = kProducers + kTeams * kTeam / 32;
 constexpr int kIssuerWarp = kPublisherWarp + 1;
 
@@ -69,6 +72,11 @@ constexpr int kIssuerWarp = kPublisherWarp + 1;
 __device__ unsigned long long g_prof[16];
 __device__ int g_dbg;  // timing experiments only: bit0 ignore dependencies, bit1 skip compute
 __device__ unsigned long long* g_timeline;  // per item: globaltimer at retirement (null: off)
+__device__ long long* g_trace;              // per item: 8 clock64 stamps of the consumer team (null: off)
+#define TRACE_IN(i) \
+  do { if (g_trace && ttid == 0 && trace_row) trace_row[i] = clock64(); } while (0)
+#define TRACE(i) \
+  do { if (g_trace && ttid == 0) g_trace[8LL * (P.cta_off[blockIdx.x] + P.items_base + k) + (i)] = clock64(); } while (0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -84,6 +92,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #else
 #define DBG(bit) 0
+#define TRACE(i) (void)0
+#define TRACE_IN(i) (void)0
 #define PROF_T0() (void)0
 #define PROF_T1(slot) (void)0
 #endif
@@ -315,7 +325,7 @@ struct BwPhaseB {
 // then phase B for non-root c.
 template <int NRHS>
 __device__ void consume_backward(const SweepParams& P, const Item& it, const double* slot,
-                                 const double* st, double* wbuf, int ttid, int team) {
+                                 const double* st, double* wbuf, int ttid, int team, long long* trace_row) {
   const int nx = P.nx, nu = P.nu, W = nx + nu, nxp = P.nxp;
   const int cnt = it.count;
   const bool leaf = it.leaf != 0;
@@ -323,6 +333,7 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
   const double* Y = st;
   const double* Cn = st + NRHS * it.v0_n;
   const double* AF = st + NRHS * (it.v0_n + (it.direct ? 0 : it.v1_n * W));
+  PROF_T0();
   {  // phase A: short dot columns (len M or mN), child sums, affine terms
     const int ncols = leaf ? nx : W;
     const int ntasks = cnt * ncols;
@@ -367,11 +378,16 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
       }
     }
   }
+  if (ttid == 0) PROF_T1(8);
+  TRACE_IN(3);
   team_sync(team);
+  if (ttid == 0) PROF_T1(9);
+  TRACE_IN(4);
   if (it.first != 0) {
     const BwPhaseB<NRHS> body{P, meta, slot, wbuf, nx, W, nxp, leaf ? 1 : 0, cnt == 1 ? 1 : 0};
     for_tasks(cnt * W, ttid, body);
   }
+  if (ttid == 0) PROF_T1(10);
 }
 
 // ---------------------------------------------------------------- forward
@@ -459,7 +475,7 @@ struct FwPhaseB {
 template <int NRHS>
 __device__ void consume_forward(const SweepParams& P, const Item& it, const double* slot,
                                 const double* st, double* xbuf, int ttid, int team, int mmax,
-                                int mNmax) {
+                                int mNmax, long long* trace_row) {
   const int nx = P.nx, nu = P.nu, Vp = P.Vp, nxp = P.nxp;
   const int cnt = it.count;
   const bool leaf = it.leaf != 0;
@@ -469,6 +485,7 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   const double* PV = st;
   const double* UO = st + NRHS * tot;
   const double* AF = st + NRHS * (tot + it.v1_n * nu);
+  PROF_T0();
   if (root) {  // x_0 = p (affine) or 0
     for (int idx = ttid; idx < NRHS * nx; idx += kTeam) {
       const int r = idx / nx, k = idx - r * nx;
@@ -480,20 +497,25 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
     const FwPhaseA<NRHS> body{P, meta, slot, PV, AF, xbuf, nx, Vp, nxp, nx + mmax, tot, cnt == 1 ? 1 : 0};
     for_tasks(cnt * (nx + mmax), ttid, body);
   }
+  if (ttid == 0) PROF_T1(11);
+  TRACE_IN(3);
   team_sync(team);
+  if (ttid == 0) PROF_T1(12);
+  TRACE_IN(4);
   const FwPhaseB<NRHS> body{P, meta, slot, UO, xbuf, nx, nu, Vp, nxp, leaf ? mNmax : nu, it.v1_n * nu,
                             leaf ? 1 : 0, root ? 1 : 0, cnt == 1 ? 1 : 0};
   for_tasks(cnt * (leaf ? mNmax : nu), ttid, body);
+  if (ttid == 0) PROF_T1(13);
 }
 
 template <int NRHS>
 __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P, int mmax, int mNmax) {
   extern __shared__ __align__(128) double smem[];
-  // full[k mod 2*NS]: the matrix-slot barrier of item k. Two per slot, so a
-  // barrier always serves the same consumer team in order (k and k + 2NS
-  // have the same parity) whatever NS is: a team can never test a phase
-  // parity of a use that has not started yet.
-  __shared__ __align__(8) uint64_t full[2 * kMaxSlots], sfull[kStageQ], sempty[kStageQ], done[kDoneQ],
+  // full[k mod kTeams*NS]: the matrix-slot barrier of item k. kTeams per
+  // slot, so a barrier always serves the same consumer team in order (k and
+  // k + kTeams*NS go to the same team) whatever NS is: a team can never test
+  // the phase parity of a use that has not started yet.
+  __shared__ __align__(8) uint64_t full[kTeams * kMaxSlots], sfull[kStageQ], sempty[kStageQ], done[kDoneQ],
       pdone[kDoneQ];
   __shared__ __align__(8) uint64_t mempty[kMaxSlots];  // slot consumed (team -> issuer)
   __shared__ __align__(16) Item sitem[kMaxSlots];
@@ -512,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   auto issue = [&](int k, const Item& it) {  // one thread
     const int s = k % NS;
     sitem[s] = it;
-    uint64_t* fb = &full[k % (2 * NS)];
+    uint64_t* fb = &full[k % (kTeams * NS)];
     mbar_arrive_expect_tx(fb, static_cast<unsigned>(it.bytes));
     tma_load_1d(slots + static_cast<int64_t>(s) * P.slot_doubles, (it.pass == 0 ? P.bw_blk : P.fw_blk) + it.off,
                 static_cast<unsigned>(it.bytes), fb);
@@ -521,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile unsigned*>(P.ctrl) + 1u;
     s_retired = 0;
-    for (int s = 0; s < 2 * NS; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kTeams * NS; ++s) mbar_init(&full[s], 1);
     for (int s = 0; s < NS; ++s) mbar_init(&mempty[s], 1);
     for (int q = 0; q < kStageQ; ++q) {
       mbar_init(&sfull[q], 1);
@@ -570,21 +592,30 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
     for (int k = team; k < K; k += kTeams) {
       const int s = k % NS;
       PROF_T0();
-      mbar_wait(&full[k % (2 * NS)], static_cast<unsigned>((k / (2 * NS)) & 1));
+      TRACE(0);
+      mbar_wait(&full[k % (kTeams * NS)], static_cast<unsigned>((k / (kTeams * NS)) & 1));
       if (ttid == 0) PROF_T1(3);
+      TRACE(1);
       const int q = k % kStageQ;
       mbar_wait(&sfull[q], static_cast<unsigned>((k / kStageQ) & 1));
       if (ttid == 0) PROF_T1(4);
+      TRACE(2);
       const Item it = sitem[s];
       const double* slot = slots + static_cast<int64_t>(s) * P.slot_doubles;
       const double* st = stages + static_cast<int64_t>(q) * P.stage_doubles;
+      long long* trace_row = nullptr;
+#ifdef SCN_SWEEP_PROFILE
+      if (g_trace) trace_row = g_trace + 8LL * (P.cta_off[blockIdx.x] + P.items_base + k);
+#endif
       if (DBG(2)) {
       } else if (it.pass == 0)
-        consume_backward<NRHS>(P, it, slot, st, tbuf, ttid, team);
+        consume_backward<NRHS>(P, it, slot, st, tbuf, ttid, team, trace_row);
       else
-        consume_forward<NRHS>(P, it, slot, st, tbuf, ttid, team, mmax, mNmax);
+        consume_forward<NRHS>(P, it, slot, st, tbuf, ttid, team, mmax, mNmax, trace_row);
+      TRACE(5);
       team_sync(team);
       if (ttid == 0) PROF_T1(5);
+      TRACE(6);
       if (ttid == 0) {
         mbar_arrive(&mempty[s]);  // slot reads done (team_sync) -> the issuer may refill it
         mbar_arrive(&sempty[q]);
@@ -595,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
         mbar_arrive(&done[dq]);
       }
       if (ttid == 0) PROF_T1(6);
+      TRACE(7);
     }
   }
   if (warp == kIssuerWarp) {
@@ -603,12 +635,17 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
     // item k goes to slot k mod NS once the team holding item k - NS has
     // released it (mbarrier, so generic reads precede the async-proxy
     // write), as one 1-D bulk copy completing on full[k mod 2NS].
-    if (lane == 0) {
-      for (int k = 0; k < K; ++k) {
-        const Item it = items[k];
+    // The next item's record is prefetched while waiting for the slot.
+    Item nxt{};
+    if (lane == 0 && K > 0) nxt = items[0];
+    for (int k = 0; k < K; ++k) {
+      if (lane == 0) {
+        const Item it = nxt;
+        if (k + 1 < K) nxt = items[k + 1];
         if (k >= NS) mbar_wait(&mempty[k % NS], static_cast<unsigned>((k / NS - 1) & 1));
         issue(k, it);
       }
+      __syncwarp();
     }
   }
   if (warp == kPublisherWarp) {
@@ -671,7 +708,22 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 
 int sweep_threads() { return kThreads; }
 int sweep_teams() { return kTeams; }
+size_t sweep_static_smem() {
+  cudaFuncAttributes a1{}, a2{};
+  cudaFuncGetAttributes(&a1, sweep_kernel<1>);
+  cudaFuncGetAttributes(&a2, sweep_kernel<2>);
+  return a1.sharedSizeBytes > a2.sharedSizeBytes ? a1.sharedSizeBytes : a2.sharedSizeBytes;
+}
 int sweep_stage_queue() { return kStageQ; }
+
+cudaError_t sweep_trace(long long* dev_buf) {
+#ifdef SCN_SWEEP_PROFILE
+  return cudaMemcpyToSymbol(g_trace, &dev_buf, sizeof(dev_buf));
+#else
+  (void)dev_buf;
+  return cudaErrorNotSupported;
+#endif
+}
 
 cudaError_t sweep_timeline(unsigned long long* dev_buf) {
 #ifdef SCN_SWEEP_PROFILE

@@ -280,6 +280,10 @@ int scenopt_debug_sweep_timeline(void* dev_buf) {
   SCN_GUARD(SCN_CUDA(sweep_timeline(static_cast<unsigned long long*>(dev_buf))));
 }
 
+int scenopt_debug_sweep_trace(void* dev_buf) {
+  SCN_GUARD(SCN_CUDA(sweep_trace(static_cast<long long*>(dev_buf))));
+}
+
 // Items in handle order: {launch, cta, pass, first, count, ldep, publish} x n.
 int scenopt_debug_items(scenopt_dev* h, int32_t* out, int cap) {
   int total = 0;

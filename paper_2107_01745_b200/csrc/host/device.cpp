@@ -422,8 +422,6 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     for (int i = 0; i < ru.count; ++i) tot += size[ru.first + i];
     item_doubles[q] = tot;
     Item& it = items[q];
-    it.off = ru.pass == 0 ? bw_total : fw_total;
-    (ru.pass == 0 ? bw_total : fw_total) += tot;
     it.bytes = static_cast<int32_t>(tot * 8);
     it.first = ru.first;
     it.count = ru.count;
@@ -471,6 +469,32 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     max_stage = std::max(max_stage, stage);
     max_item = std::max(max_item, tot);
     max_cnt = std::max(max_cnt, ru.count);
+  }
+  // Pass-array placement in "time-major" order: item k of every CTA, then
+  // item k+1, ... (SCENOPT_PACK=cta: CTA-major). CTAs advance through their
+  // lists at about the same rate, so the blocks streamed concurrently by the
+  // grid are neighbours in HBM instead of 148 far-apart streams.
+  {
+    const bool cta_major = std::getenv("SCENOPT_PACK") && std::string(std::getenv("SCENOPT_PACK")) == "cta";
+    size_t base = 0;
+    for (const auto& off : cta_offs) {
+      int longest = 0;
+      for (int gg = 0; gg < G; ++gg) longest = std::max(longest, off[gg + 1] - off[gg]);
+      auto place = [&](size_t q) {
+        Item& it = items[q];
+        int64_t& total = it.pass == 0 ? bw_total : fw_total;
+        it.off = total;
+        total += item_doubles[q];
+      };
+      if (cta_major) {
+        for (int q = 0; q < off[G]; ++q) place(base + q);
+      } else {
+        for (int k = 0; k < longest; ++k)
+          for (int gg = 0; gg < G; ++gg)
+            if (off[gg] + k < off[gg + 1]) place(base + off[gg] + k);
+      }
+      base += off[G];
+    }
   }
   d->bw_doubles = bw_total;
   d->fw_doubles = fw_total;
@@ -595,7 +619,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   for (int ns = ns_max; ns >= 2; --ns) {
     if (force_ns && ns != force_ns) continue;
     const size_t smem = smem_for(ns);
-    if (smem > static_cast<size_t>(prop.sharedMemPerBlockOptin)) continue;
+    if (smem + sweep_static_smem() > static_cast<size_t>(prop.sharedMemPerBlockOptin)) continue;
     SCN_CUDA(sweep_configure(smem));
     int cps = 0;
     SCN_CUDA(sweep_occupancy(&cps, smem));

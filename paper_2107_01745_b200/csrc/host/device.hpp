@@ -138,10 +138,12 @@ void dev_gather_primal(DevState& d, double* x, double* u);
 
 // kernel launchers (cuda/*.cu)
 int sweep_teams();
+size_t sweep_static_smem();
 int sweep_stage_queue();
 cudaError_t sweep_configure(size_t dyn_smem);
 cudaError_t sweep_profile_read(unsigned long long* out, bool reset);
 cudaError_t sweep_timeline(unsigned long long* dev_buf);
+cudaError_t sweep_trace(long long* dev_buf);
 cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem);
 cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax,
                          cudaStream_t stream);

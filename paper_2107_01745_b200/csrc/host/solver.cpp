@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -28,6 +30,11 @@ struct scenopt_dev::Work {
   unsigned* bar = nullptr;
   double* hS = nullptr;  // pinned mirrors
   int* hI = nullptr;
+  // pinned staging words of asynchronous scalar writes; a word is reused only
+  // after a stream synchronisation has retired every copy that read it
+  static constexpr int kRing = 256;
+  double* hRing = nullptr;
+  int ring_next = 0;
   // two FbStates (ping-pong)
   double *y[2] = {}, *Hx[2] = {}, *z[2] = {}, *R[2] = {}, *T[2] = {}, *x[2] = {}, *u[2] = {};
   double *Hx0 = nullptr, *x0 = nullptr, *u0 = nullptr;
@@ -56,6 +63,7 @@ scenopt_dev::~scenopt_dev() {
   if (w) {
     if (w->hS) cudaFreeHost(w->hS);
     if (w->hI) cudaFreeHost(w->hI);
+    if (w->hRing) cudaFreeHost(w->hRing);
   }
 }
 
@@ -76,6 +84,7 @@ void scenopt_dev::init_solver_buffers() {
   SCN_CUDA(cudaMemset(k.bar, 0, 4 * sizeof(unsigned)));
   SCN_CUDA(cudaMallocHost(&k.hS, sl::kScalars * sizeof(double)));
   SCN_CUDA(cudaMallocHost(&k.hI, il::kInts * sizeof(int)));
+  SCN_CUDA(cudaMallocHost(&k.hRing, scenopt_dev::Work::kRing * sizeof(double)));
   const size_t D = static_cast<size_t>(k.D), nxn = static_cast<size_t>(L.nx) * L.n,
                nuf = static_cast<size_t>(L.nu) * std::max(L.first_leaf, 1);
   for (int s = 0; s < 2; ++s) {
@@ -149,28 +158,85 @@ struct Engine {
   DualCtx ctx() const { return k.ctx(d); }
   size_t D() const { return static_cast<size_t>(d.lay.dual_dim); }
 
+  // Stream-ordered scalar write, no host synchronisation.
   void set_scalar(int slot, double v) {
-    k.hS[slot] = v;  // staged through a pinned word per slot
-    SCN_CUDA(cudaMemcpyAsync(k.S + slot, k.hS + slot, sizeof(double), cudaMemcpyHostToDevice, st));
-    SCN_CUDA(cudaStreamSynchronize(st));
+    if (k.ring_next == scenopt_dev::Work::kRing) {  // every staging word may still be in flight
+      SCN_CUDA(cudaStreamSynchronize(st));
+      k.ring_next = 0;
+    }
+    double* w = k.hRing + k.ring_next++;
+    *w = v;
+    k.hS[slot] = v;  // host mirror
+    SCN_CUDA(cudaMemcpyAsync(k.S + slot, w, sizeof(double), cudaMemcpyHostToDevice, st));
   }
   void read_scalars() {
+    cudaEvent_t pre = nullptr;
+    if (timer.on) {
+      cudaEventCreate(&pre);
+      cudaEventRecord(pre, st);
+    }
     SCN_CUDA(cudaMemcpyAsync(k.hS, k.S, sl::kScalars * sizeof(double), cudaMemcpyDeviceToHost, st));
     SCN_CUDA(cudaMemcpyAsync(k.hI, k.I, il::kInts * sizeof(int), cudaMemcpyDeviceToHost, st));
     SCN_CUDA(cudaStreamSynchronize(st));
+    k.ring_next = 0;
+    if (timer.on) {  // GPU-side cost of this host round trip: copies + wake-up + re-enqueue
+      cudaEvent_t post;
+      cudaEventCreate(&post);
+      cudaEventRecord(post, st);
+      timer.sync_ev.emplace_back(pre, post);
+    }
   }
   double S(int slot) const { return k.hS[slot]; }
   int I(int slot) const { return k.hI[slot]; }
   void copy(double* dst, const double* src, size_t n) {
     SCN_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
+  // SCN_SOLVE_TIMING=1: CUDA-event time of every sweep, summed to stderr at exit (diagnostics)
+  struct SweepTimer {
+    bool on = std::getenv("SCN_SOLVE_TIMING") != nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    ~SweepTimer() {
+      if (!on || ev.empty()) return;
+      cudaDeviceSynchronize();
+      double tot = 0.0;
+      for (auto& p : ev) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.first, p.second);
+        tot += ms;
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+      }
+      std::fprintf(stderr, "[scn] %zu sweeps, %.3f ms GPU (%.1f us each)\n", ev.size(), tot, 1e3 * tot / ev.size());
+      double st = 0.0;
+      for (auto& p : sync_ev) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.first, p.second);
+        st += ms;
+      }
+      if (!sync_ev.empty())
+        std::fprintf(stderr, "[scn] %zu host round trips, %.3f ms (%.1f us each)\n", sync_ev.size(), st,
+                     1e3 * st / sync_ev.size());
+    }
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sync_ev;
+  } timer;
+  template <class F>
+  void timed(F&& f) {
+    if (!timer.on) return f();
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+    f();
+    cudaEventRecord(b, st);
+    timer.ev.emplace_back(a, b);
+  }
   void sweep1(bool affine, const double* y, double* x, double* u, double* Hx) {
-    dev_sweep(d, 1, affine, &y, x ? &x : nullptr, u ? &u : nullptr, &Hx);
+    timed([&] { dev_sweep(d, 1, affine, &y, x ? &x : nullptr, u ? &u : nullptr, &Hx); });
   }
   void sweep2(const double* a, const double* b, double* Ha, double* Hb) {
     const double* ys[2] = {a, b};
     double* hs[2] = {Ha, Hb};
-    dev_sweep(d, 2, false, ys, nullptr, nullptr, hs);
+    timed([&] { dev_sweep(d, 2, false, ys, nullptr, nullptr, hs); });
   }
 
   // f_hat(0) and H x(0), once per handle (fhat identity)

@@ -116,6 +116,8 @@ typedef struct scenopt_dev_info {
   int32_t shard_stage; /* subtree sharding over ranks: cut stage, -1 when not sharded */
   int32_t rank, world; /* this handle's rank in the shard group (0, 1 when not sharded) */
   int32_t shard_first, shard_past; /* this rank's shard-stage node ids [first, past) */
+  int32_t items_global;   /* items too large for a shared-memory slot (blocks read from HBM in place) */
+  int32_t consumer_stage; /* 1: vectors staged by the consumer teams (very wide states) */
 } scenopt_dev_info;
 
 typedef struct scenopt_problem scenopt_problem;

@@ -59,12 +59,15 @@ struct Item {
   int32_t v0_n;
   int32_t v1_lo;    // staged range 1: bw child contribution rows ; fw u_off of the item
   int32_t v1_n;
-  int32_t direct;   // bw: contributions read from L2 by the consumers (many children)
+  int32_t direct;   // flags: kDirectContrib (bw: contributions read from L2, many children),
+                    //        kGlobalBlocks (node blocks stay in HBM; only the headers are copied)
   int32_t ldep;     // local index (same CTA) of the last item this one depends on, -1: none
   int32_t publish;  // 1: release the nodes' flags at gpu scope (consumed by other CTAs)
 };
 static_assert(sizeof(Item) == 64, "Item is one 64-byte record");
 
+constexpr int kDirectContrib = 1;
+constexpr int kGlobalBlocks = 2;
 constexpr int kMaxRhs = 2;
 constexpr int kMaxSlots = 8;
 
@@ -75,6 +78,8 @@ struct SweepParams {
   int nslot, slot_doubles, stage_doubles, scratch_doubles;
   int nrhs, affine, G, max_count;
   int nxp, Vp;  // padded column lengths (== 2 mod 4) of J/K/TN and W
+  int consumer_stage;  // 1: teams stage their own vectors (staging area per team, not per ring entry)
+  int global_blocks;   // 1: some items keep their node blocks in HBM (kGlobalBlocks)
   const Item* items;      // CTA-major: CTA b owns items [cta_off[b], cta_off[b+1])
   const int32_t* cta_off;
   const double* bw_blk;

@@ -74,9 +74,9 @@ __device__ int g_dbg;  // timing experiments only: bit0 ignore dependencies, bit
 __device__ unsigned long long* g_timeline;  // per item: globaltimer at retirement (null: off)
 __device__ long long* g_trace;              // per item: 8 clock64 stamps of the consumer team (null: off)
 #define TRACE_IN(i) \
-  do { if (g_trace && ttid == 0 && trace_row) trace_row[i] = clock64(); } while (0)
+  do { if (g_trace && ttid == 0 && trace_row) trace_row[i] = static_cast<long long>(gtimer()); } while (0)
 #define TRACE(i) \
-  do { if (g_trace && ttid == 0) g_trace[8LL * (P.cta_off[blockIdx.x] + P.items_base + k) + (i)] = clock64(); } while (0)
+  do { if (g_trace && ttid == 0) g_trace[12LL * (P.cta_off[blockIdx.x] + P.items_base + k) + (i)] = static_cast<long long>(gtimer()); } while (0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -86,9 +86,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PROF_T0() long long _pt = clock64()
 #define PROF_T1(slot)                                                                          \
   do {                                                                                         \
-    long long _n = clock64();                                                                  \
-    atomicAdd(&g_prof[slot], (unsigned long long)(_n - _pt));                                  \
-    _pt = _n;                                                                                  \
+    if (g_dbg & 4) {  /* SCN_DBG bit 2: per-role cycle counters (heavy: global atomics) */     \
+      long long _n = clock64();                                                                \
+      atomicAdd(&g_prof[slot], (unsigned long long)(_n - _pt));                                \
+      _pt = _n;                                                                                \
+    }                                                                                          \
   } while (0)
 #else
 #define DBG(bit) 0
@@ -127,7 +129,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef SCN_MBAR_HINT_NS
+#define SCN_MBAR_HINT_NS 0  /* measured: no explicit hint is ~1% faster than 32 or 256 ns */
+#endif
+// try_wait with an explicit suspend-time hint: a waiting warp re-checks within
+// ~tens of ns instead of the implementation's default suspend interval (the
+// item pipeline is latency-bound; every wake-up is on some item's path).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#if SCN_MBAR_HINT_NS > 0
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "n"(SCN_MBAR_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -139,6 +160,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
   unsigned ok;
@@ -190,7 +212,7 @@ __device__ __forceinline__ bool flags_ready(const unsigned* flags, const Item& i
 // Issued as asynchronous 8-byte copies (LDGSTS) program-ordered after the
 // acquire that observed this item's flags (ld.acquire.gpu also invalidates
 // L1), so they read the published values.
-template <int NRHS>
+template <int NRHS, int nt = 32>
 __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, int lane) {
   const int nx = P.nx, nu = P.nu, W = nx + nu, Vp = P.Vp;
   if (it.pass == 0) {
@@ -199,18 +221,18 @@ __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, in
     for (int r = 0; r < NRHS; ++r) {
       const double* ys = P.y[r] + it.v0_lo;
       double* yd = st + r * it.v0_n;
-      for (int i = lane; i < it.v0_n; i += 32) cp_async8(yd + i, ys + i);
-      if (!it.direct) {
+      for (int i = lane; i < it.v0_n; i += nt) cp_async8(yd + i, ys + i);
+      if (!(it.direct & kDirectContrib)) {
         const double* cs = P.contrib[r] + static_cast<int64_t>(it.v1_lo) * W;
         double* cd = st + NRHS * it.v0_n + r * nc;
-        for (int i = lane; i < nc; i += 32) cp_async8(cd + i, cs + i);
+        for (int i = lane; i < nc; i += nt) cp_async8(cd + i, cs + i);
       }
     }
     if (P.affine) {
       const int na = it.count * W;
       const double* as = P.aff_bw + static_cast<int64_t>(it.first) * W;
-      double* ad = st + NRHS * (it.v0_n + (it.direct ? 0 : nc));
-      for (int i = lane; i < na; i += 32) cp_async8(ad + i, as + i);
+      double* ad = st + NRHS * (it.v0_n + ((it.direct & kDirectContrib) ? 0 : nc));
+      for (int i = lane; i < na; i += nt) cp_async8(ad + i, as + i);
     }
   } else {
     const int tot = it.v0_n * Vp, nuo = it.v1_n * nu;
@@ -220,7 +242,7 @@ __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, in
         double* pd = st + r * tot + pp * Vp;
         const double* xs = P.x[r] + static_cast<int64_t>(it.v0_lo + pp) * nx;
         const double* us = P.u[r] + static_cast<int64_t>(it.v0_lo + pp) * nu;
-        for (int e = lane; e < Vp; e += 32) {
+        for (int e = lane; e < Vp; e += nt) {
           if (e < nx)
             cp_async8(pd + e, xs + e);
           else if (e < W)
@@ -231,13 +253,13 @@ __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, in
       }
       const double* os = P.u[r] + static_cast<int64_t>(it.v1_lo) * nu;
       double* od = st + NRHS * tot + r * nuo;
-      for (int i = lane; i < nuo; i += 32) cp_async8(od + i, os + i);
+      for (int i = lane; i < nuo; i += nt) cp_async8(od + i, os + i);
     }
     if (P.affine) {
       const int na = it.count * nx;
       const double* as = P.aff_fw + static_cast<int64_t>(it.first) * nx;
       double* ad = st + NRHS * (tot + nuo);
-      for (int i = lane; i < na; i += 32) cp_async8(ad + i, as + i);
+      for (int i = lane; i < na; i += nt) cp_async8(ad + i, as + i);
     }
   }
 }
@@ -324,7 +346,7 @@ struct BwPhaseB {
 // sum_kids contrib_k (+[sigma_c; c_hat_c]); leaf: w_c = F_N' y_N (+pi p_N);
 // then phase B for non-root c.
 template <int NRHS>
-__device__ void consume_backward(const SweepParams& P, const Item& it, const double* slot,
+__device__ void consume_backward(const SweepParams& P, const Item& it, const double* slot, const double* mat,
                                  const double* st, double* wbuf, int ttid, int team, long long* trace_row) {
   const int nx = P.nx, nu = P.nu, W = nx + nu, nxp = P.nxp;
   const int cnt = it.count;
@@ -332,7 +354,7 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
   const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
   const double* Y = st;
   const double* Cn = st + NRHS * it.v0_n;
-  const double* AF = st + NRHS * (it.v0_n + (it.direct ? 0 : it.v1_n * W));
+  const double* AF = st + NRHS * (it.v0_n + ((it.direct & kDirectContrib) ? 0 : it.v1_n * W));
   PROF_T0();
   {  // phase A: short dot columns (len M or mN), child sums, affine terms
     const int ncols = leaf ? nx : W;
@@ -342,7 +364,7 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
       const int j = task - ni * ncols;
       const NodeMeta& mc = meta[ni];
       const int len = leaf ? mc.mN : mc.M;
-      const double* col = slot + mc.blk + j * len;
+      const double* col = mat + mc.blk + j * len;
       const double* yv = Y + mc.yoff;
       double acc[NRHS];
 #pragma unroll
@@ -353,11 +375,21 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
         for (int r = 0; r < NRHS; ++r) acc[r] = fma(a, yv[r * it.v0_n + k], acc[r]);
       }
       if (!leaf) {
-        if (it.direct) {  // many children: read the published contributions from L2
-          for (int k = 0; k < mc.nkid; ++k) {
+        if (it.direct & kDirectContrib) {  // many children: read the published contributions from L2,
+                          // eight loads in flight, summed in child order (as when staged)
+          const int64_t base = static_cast<int64_t>(it.v1_lo + mc.kid0) * W + j;
+          for (int k0 = 0; k0 < mc.nkid; k0 += 8) {
+            double v[NRHS][8];
 #pragma unroll
-            for (int r = 0; r < NRHS; ++r)
-              acc[r] += __ldcg(P.contrib[r] + static_cast<int64_t>(it.v1_lo + mc.kid0 + k) * W + j);
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+              for (int r = 0; r < NRHS; ++r)
+                v[r][u] = k0 + u < mc.nkid ? __ldcg(P.contrib[r] + base + static_cast<int64_t>(k0 + u) * W) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+              for (int r = 0; r < NRHS; ++r)
+                if (k0 + u < mc.nkid) acc[r] += v[r][u];
           }
         } else {
           for (int k = 0; k < mc.nkid; ++k) {
@@ -384,7 +416,7 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
   if (ttid == 0) PROF_T1(9);
   TRACE_IN(4);
   if (it.first != 0) {
-    const BwPhaseB<NRHS> body{P, meta, slot, wbuf, nx, W, nxp, leaf ? 1 : 0, cnt == 1 ? 1 : 0};
+    const BwPhaseB<NRHS> body{P, meta, mat, wbuf, nx, W, nxp, leaf ? 1 : 0, cnt == 1 ? 1 : 0};
     for_tasks(cnt * W, ttid, body);
   }
   if (ttid == 0) PROF_T1(10);
@@ -473,7 +505,7 @@ struct FwPhaseB {
 };
 
 template <int NRHS>
-__device__ void consume_forward(const SweepParams& P, const Item& it, const double* slot,
+__device__ void consume_forward(const SweepParams& P, const Item& it, const double* slot, const double* mat,
                                 const double* st, double* xbuf, int ttid, int team, int mmax,
                                 int mNmax, long long* trace_row) {
   const int nx = P.nx, nu = P.nu, Vp = P.Vp, nxp = P.nxp;
@@ -494,7 +526,7 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
       P.x[r][k] = v;
     }
   } else {
-    const FwPhaseA<NRHS> body{P, meta, slot, PV, AF, xbuf, nx, Vp, nxp, nx + mmax, tot, cnt == 1 ? 1 : 0};
+    const FwPhaseA<NRHS> body{P, meta, mat, PV, AF, xbuf, nx, Vp, nxp, nx + mmax, tot, cnt == 1 ? 1 : 0};
     for_tasks(cnt * (nx + mmax), ttid, body);
   }
   if (ttid == 0) PROF_T1(11);
@@ -502,13 +534,17 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   team_sync(team);
   if (ttid == 0) PROF_T1(12);
   TRACE_IN(4);
-  const FwPhaseB<NRHS> body{P, meta, slot, UO, xbuf, nx, nu, Vp, nxp, leaf ? mNmax : nu, it.v1_n * nu,
+  const FwPhaseB<NRHS> body{P, meta, mat, UO, xbuf, nx, nu, Vp, nxp, leaf ? mNmax : nu, it.v1_n * nu,
                             leaf ? 1 : 0, root ? 1 : 0, cnt == 1 ? 1 : 0};
   for_tasks(cnt * (leaf ? mNmax : nu), ttid, body);
   if (ttid == 0) PROF_T1(13);
 }
 
-template <int NRHS>
+// MODE bits (one instantiation per combination, so the common layout's
+// kernel carries no fallback code): kModeConsumerStage = teams stage their own
+// vectors; kModeGlobalBlocks = some items read their node blocks from HBM.
+constexpr int kModeConsumerStage = 1, kModeGlobalBlocks = 2;
+template <int NRHS, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P, int mmax, int mNmax) {
   extern __shared__ __align__(128) double smem[];
   // full[k mod kTeams*NS]: the matrix-slot barrier of item k. kTeams per
@@ -525,8 +561,9 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NS = P.nslot;  // matrix slots
   double* slots = smem;
-  double* stages = smem + static_cast<int64_t>(NS) * P.slot_doubles;  // kStageQ staging areas
-  double* scratch = stages + static_cast<int64_t>(kStageQ) * P.stage_doubles;  // per team
+  double* stages = smem + static_cast<int64_t>(NS) * P.slot_doubles;  // kStageQ (or kTeams) staging areas
+  constexpr bool kConsumerStage = (MODE & kModeConsumerStage) != 0;
+  double* scratch = stages + static_cast<int64_t>(kConsumerStage ? kTeams : kStageQ) * P.stage_doubles;
   const int b = blockIdx.x;
   const Item* items = P.items + P.cta_off[b];
   const int K = P.cta_off[b + 1] - P.cta_off[b];
@@ -571,6 +608,9 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       PROF_T0();
       if (k >= kStageQ) mbar_wait(&sempty[q], static_cast<unsigned>((k / kStageQ - 1) & 1));
       if (lane == 0 && p == 0) PROF_T1(0);
+#ifdef SCN_SWEEP_PROFILE
+      if (g_trace && lane == 0) g_trace[12LL * (P.cta_off[blockIdx.x] + P.items_base + k) + 8] = static_cast<long long>(gtimer());
+#endif
       if (!DBG(1)) {
         if (it.ldep >= 0)
           while (ld_acquire_cta(&s_retired) <= it.ldep) __nanosleep(16);
@@ -578,9 +618,15 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
           while (!flags_ready(dep_flags(P, it), it, E, lane)) __nanosleep(32);
       }
       if (lane == 0 && p == 0) PROF_T1(2);
-      stage_issue<NRHS>(P, it, stages + static_cast<int64_t>(q) * P.stage_doubles, lane);
+#ifdef SCN_SWEEP_PROFILE
+      if (g_trace && lane == 0) g_trace[12LL * (P.cta_off[blockIdx.x] + P.items_base + k) + 9] = static_cast<long long>(gtimer());
+#endif
+      if (!kConsumerStage) stage_issue<NRHS>(P, it, stages + static_cast<int64_t>(q) * P.stage_doubles, lane);
       cp_async_wait_all();
       __syncwarp();
+#ifdef SCN_SWEEP_PROFILE
+      if (g_trace && lane == 0) g_trace[12LL * (P.cta_off[blockIdx.x] + P.items_base + k) + 10] = static_cast<long long>(gtimer());
+#endif
       if (lane == 0) mbar_arrive(&sfull[q]);
       if (lane == 0 && p == 0) PROF_T1(1);
     }
@@ -602,16 +648,36 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       TRACE(2);
       const Item it = sitem[s];
       const double* slot = slots + static_cast<int64_t>(s) * P.slot_doubles;
+      // node blocks: in the slot, or (an item larger than a slot) read from
+      // HBM/L2 in place; the slot then holds only the item's node headers.
+      // Separate call sites keep the slot path's loads in the shared space.
+      const bool gblocks = (it.direct & kGlobalBlocks) != 0;
+      const double* gmat = (it.pass == 0 ? P.bw_blk : P.fw_blk) + it.off;
       const double* st = stages + static_cast<int64_t>(q) * P.stage_doubles;
+      if constexpr (kConsumerStage) {  // large vectors: the team stages its own item after the producer's
+                               // dependency check (acquire) into a per-team area
+        double* tst = stages + static_cast<int64_t>(team) * P.stage_doubles;
+        stage_issue<NRHS, kTeam>(P, it, tst, ttid);
+        cp_async_wait_all();
+        team_sync(team);
+        st = tst;
+      }
       long long* trace_row = nullptr;
 #ifdef SCN_SWEEP_PROFILE
-      if (g_trace) trace_row = g_trace + 8LL * (P.cta_off[blockIdx.x] + P.items_base + k);
+      if (g_trace) trace_row = g_trace + 12LL * (P.cta_off[blockIdx.x] + P.items_base + k);
 #endif
       if (DBG(2)) {
-      } else if (it.pass == 0)
-        consume_backward<NRHS>(P, it, slot, st, tbuf, ttid, team, trace_row);
-      else
-        consume_forward<NRHS>(P, it, slot, st, tbuf, ttid, team, mmax, mNmax, trace_row);
+      } else if (it.pass == 0) {
+        if ((MODE & kModeGlobalBlocks) && gblocks)
+          consume_backward<NRHS>(P, it, slot, gmat, st, tbuf, ttid, team, trace_row);
+        else
+          consume_backward<NRHS>(P, it, slot, slot, st, tbuf, ttid, team, trace_row);
+      } else {
+        if ((MODE & kModeGlobalBlocks) && gblocks)
+          consume_forward<NRHS>(P, it, slot, gmat, st, tbuf, ttid, team, mmax, mNmax, trace_row);
+        else
+          consume_forward<NRHS>(P, it, slot, slot, st, tbuf, ttid, team, mmax, mNmax, trace_row);
+      }
       TRACE(5);
       team_sync(team);
       if (ttid == 0) PROF_T1(5);
@@ -681,9 +747,12 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       if (lane == 0) {
         st_release_cta(&s_retired, j);
 #ifdef SCN_SWEEP_PROFILE
-        if (g_timeline) {
+        if (g_timeline || g_trace) {
           const unsigned long long now = gtimer();
-          for (int q2 = k; q2 < j; ++q2) g_timeline[P.cta_off[b] + q2 + P.items_base] = now;
+          for (int q2 = k; q2 < j; ++q2) {
+            if (g_timeline) g_timeline[P.cta_off[b] + q2 + P.items_base] = now;
+            if (g_trace) g_trace[12LL * (P.cta_off[b] + P.items_base + q2) + 11] = static_cast<long long>(now);
+          }
         }
 #endif
         PROF_T1(7);
@@ -708,11 +777,23 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 
 int sweep_threads() { return kThreads; }
 int sweep_teams() { return kTeams; }
+namespace {
+const void* const kKernels[2][4] = {
+    {reinterpret_cast<const void*>(sweep_kernel<1, 0>), reinterpret_cast<const void*>(sweep_kernel<1, 1>),
+     reinterpret_cast<const void*>(sweep_kernel<1, 2>), reinterpret_cast<const void*>(sweep_kernel<1, 3>)},
+    {reinterpret_cast<const void*>(sweep_kernel<2, 0>), reinterpret_cast<const void*>(sweep_kernel<2, 1>),
+     reinterpret_cast<const void*>(sweep_kernel<2, 2>), reinterpret_cast<const void*>(sweep_kernel<2, 3>)}};
+}  // namespace
+
 size_t sweep_static_smem() {
-  cudaFuncAttributes a1{}, a2{};
-  cudaFuncGetAttributes(&a1, sweep_kernel<1>);
-  cudaFuncGetAttributes(&a2, sweep_kernel<2>);
-  return a1.sharedSizeBytes > a2.sharedSizeBytes ? a1.sharedSizeBytes : a2.sharedSizeBytes;
+  size_t m = 0;
+  for (auto& row : kKernels)
+    for (const void* fn : row) {
+      cudaFuncAttributes a{};
+      cudaFuncGetAttributes(&a, fn);
+      m = a.sharedSizeBytes > m ? a.sharedSizeBytes : m;
+    }
+  return m;
 }
 int sweep_stage_queue() { return kStageQ; }
 
@@ -763,20 +844,25 @@ cudaError_t sweep_configure(size_t dyn_smem) {
     if (dyn_smem <= configured[dev]) return cudaSuccess;
     configured[dev] = dyn_smem;
   }
-  e = cudaFuncSetAttribute(sweep_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(dyn_smem));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(sweep_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(dyn_smem));
+  for (auto& row : kKernels)
+    for (const void* fn : row) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_smem));
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
 }
 
 cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem) {
-  int a = 0, b = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, sweep_kernel<1>, kThreads, dyn_smem);
-  if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sweep_kernel<2>, kThreads, dyn_smem);
-  *ctas_per_sm = a < b ? a : b;
-  return e;
+  int lo = 1 << 30;
+  for (auto& row : kKernels)
+    for (const void* fn : row) {
+      int a = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, fn, kThreads, dyn_smem);
+      if (e != cudaSuccess) return e;
+      lo = a < lo ? a : lo;
+    }
+  *ctas_per_sm = lo;
+  return cudaSuccess;
 }
 
 cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax,
@@ -792,8 +878,8 @@ cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mm
   }();
   (void)dbg_set;
 #endif
-  const void* fn = P.nrhs == 2 ? reinterpret_cast<const void*>(sweep_kernel<2>)
-                               : reinterpret_cast<const void*>(sweep_kernel<1>);
+  const int mode = (P.consumer_stage ? kModeConsumerStage : 0) | (P.global_blocks ? kModeGlobalBlocks : 0);
+  const void* fn = kKernels[P.nrhs == 2 ? 1 : 0][mode];
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, dyn_smem, stream);
 }
 

@@ -205,6 +205,8 @@ int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
     info->world = d.world;
     info->shard_first = d.shard_lo;
     info->shard_past = d.shard_hi;
+    info->items_global = d.items_global;
+    info->consumer_stage = d.consumer_stage ? 1 : 0;
   });
 }
 

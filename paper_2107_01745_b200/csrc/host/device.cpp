@@ -499,7 +499,6 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->bw_doubles = bw_total;
   d->fw_doubles = fw_total;
   d->max_count = max_cnt;
-  d->slot_doubles = static_cast<int>((max_item + 15) & ~int64_t(15));
   d->stage_doubles = static_cast<int>((max_stage + 15) & ~int64_t(15));
   d->vec_doubles = static_cast<int>((static_cast<int64_t>(max_cnt) * kMaxRhs * nxp + 15) & ~int64_t(15));
 
@@ -604,35 +603,77 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     }
   });
 
-  // ---- launch configuration: one co-resident CTA per SM with the deepest
-  // even slot ring that fits (SCENOPT_NSLOT overrides)
+  // ---- launch configuration: one co-resident CTA per SM. Preference order:
+  //   1. producer-staged vectors, every item's blocks in a shared-memory slot,
+  //      the deepest slot ring (<= 5) that fits;
+  //   2. producer-staged, 4 slots sized for the small items: larger items keep
+  //      their blocks in HBM (only the node headers are copied; kGlobalBlocks);
+  //   3./4. the same with consumer-staged vectors (one staging area per team
+  //      instead of a 12-deep ring) for very wide states.
+  // SCENOPT_NSLOT / SCENOPT_SLOT_KB / SCENOPT_STAGE=consumer force choices (tests).
   const int dbl = 8;
   const int force_ns = env_int("SCENOPT_NSLOT", 0);
   const int teams = sweep_teams();
   const int stageq = sweep_stage_queue();
-  auto smem_for = [&](int ns) {
-    return (static_cast<size_t>(ns) * d->slot_doubles + static_cast<size_t>(stageq) * d->stage_doubles +
+  const size_t optin = static_cast<size_t>(prop.sharedMemPerBlockOptin) - sweep_static_smem();
+  const int64_t slot_cap_env = static_cast<int64_t>(env_int("SCENOPT_SLOT_KB", 0)) * 1024 / 8;
+  const bool force_consumer = std::getenv("SCENOPT_STAGE") && std::string(std::getenv("SCENOPT_STAGE")) == "consumer";
+  const int64_t hdr_doubles_max = static_cast<int64_t>(d->max_count) * (sizeof(NodeMeta) / 8);
+  auto smem_for = [&](int ns, int64_t slot, bool consumer) {
+    return (static_cast<size_t>(ns) * slot + static_cast<size_t>(consumer ? teams : stageq) * d->stage_doubles +
             static_cast<size_t>(teams) * d->vec_doubles) * dbl;
   };
   int best_ns = 0;
+  int64_t slot = 0;
+  bool consumer = false;
   const int ns_max = std::min(kMaxSlots, std::max(2, env_int("SCENOPT_NSLOT_MAX", 5)));
-  for (int ns = ns_max; ns >= 2; --ns) {
-    if (force_ns && ns != force_ns) continue;
-    const size_t smem = smem_for(ns);
-    if (smem + sweep_static_smem() > static_cast<size_t>(prop.sharedMemPerBlockOptin)) continue;
+  auto fits = [&](int ns, int64_t sl, bool cons) {
+    const size_t smem = smem_for(ns, sl, cons);
+    if (smem > optin) return false;
     SCN_CUDA(sweep_configure(smem));
     int cps = 0;
     SCN_CUDA(sweep_occupancy(&cps, smem));
-    if (cps < 1) continue;
-    best_ns = ns;
-    break;
+    return cps >= 1;
+  };
+  for (int pass = 0; pass < 2 && !best_ns; ++pass) {
+    const bool cons = pass == 1 || force_consumer;
+    if (pass == 1 && force_consumer) break;
+    // all items in smem
+    if (!slot_cap_env)
+      for (int ns = ns_max; ns >= 2; --ns) {
+        if (force_ns && ns != force_ns) continue;
+        const int64_t sl = (std::max<int64_t>(max_item, 2) + 15) & ~int64_t(15);
+        if (fits(ns, sl, cons)) {
+          best_ns = ns, slot = sl, consumer = cons;
+          break;
+        }
+      }
+    if (best_ns) break;
+    // small items in smem, large ones from HBM
+    const int ns = force_ns ? force_ns : 4;
+    int64_t sl = slot_cap_env ? slot_cap_env
+                              : static_cast<int64_t>((optin / dbl - static_cast<size_t>(cons ? teams : stageq) * d->stage_doubles -
+                                                      static_cast<size_t>(teams) * d->vec_doubles) / ns);
+    sl = std::max<int64_t>(sl, hdr_doubles_max) & ~int64_t(15);
+    sl = std::max<int64_t>(sl, (hdr_doubles_max + 15) & ~int64_t(15));
+    if (sl > 0 && fits(ns, sl, cons)) best_ns = ns, slot = sl, consumer = cons;
   }
   if (best_ns == 0)
-    fail(SCENOPT_E_INVALID_PARAMS, "dev_create: node blocks too large for a 2-slot shared-memory ring (" +
-                                       std::to_string(smem_for(2)) + " bytes)");
+    fail(SCENOPT_E_INVALID_PARAMS, "dev_create: the per-item staging vectors do not fit in shared memory (" +
+                                       std::to_string(smem_for(2, hdr_doubles_max, true)) + " bytes)");
+  d->slot_doubles = static_cast<int>(slot);
+  d->consumer_stage = consumer;
+  int n_global = 0;
+  for (Item& it : items)
+    if (it.bytes > slot * dbl) {  // blocks stay in HBM; copy only the node headers
+      it.direct |= kGlobalBlocks;
+      it.bytes = static_cast<int32_t>(it.count * sizeof(NodeMeta));
+      ++n_global;
+    }
+  d->items_global = n_global;
   d->nslot = best_ns;
   d->ctas_per_sm = 1;
-  d->dyn_smem = smem_for(best_ns);
+  d->dyn_smem = smem_for(best_ns, slot, consumer);
   SCN_CUDA(sweep_configure(d->dyn_smem));
   d->G = 0;
 
@@ -847,6 +888,8 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
   P.max_count = d.max_count;
   P.nxp = d.nxp;
   P.Vp = d.Vp;
+  P.consumer_stage = d.consumer_stage ? 1 : 0;
+  P.global_blocks = d.items_global > 0 ? 1 : 0;
   P.bw_blk = d.bw_blk;
   P.fw_blk = d.fw_blk;
   P.aff_bw = d.aff_bw;

@@ -56,6 +56,8 @@ struct DevState {
   };
   std::vector<Launch> launches;
   int cut_stage = -1;  // CTA subtree-ownership cut of the main region (-1: all global tickets)
+  bool consumer_stage = false;  // teams stage their own vectors (very wide states)
+  int items_global = 0;         // items whose node blocks are read from HBM in place
   // ---- subtree sharding over ranks
   int rank = 0, world = 1, shard_stage = -1;
   void* comm = nullptr;         // ncclComm_t

@@ -153,3 +153,56 @@ def test_default_grid_uses_subtree_ownership_on_c3(gpu):
     info = so.factor(prob).dev_info()
     assert info["grid_ctas"] == info["sm_count"]
     assert info["cut_stage"] == 4  # 1024 subtrees >= 4 per CTA
+
+
+@pytest.mark.parametrize("mode", [dict(SCENOPT_SLOT_KB="4"), dict(SCENOPT_STAGE="consumer"),
+                                  dict(SCENOPT_SLOT_KB="6", SCENOPT_STAGE="consumer"),
+                                  dict(SCENOPT_SLOT_KB="4", SCENOPT_GRID="5", SCENOPT_MIN_SUBTREES="1")])
+def test_fallback_layouts_match_oracle(gpu, monkeypatch, mode):
+    """Items larger than a shared-memory slot read their node blocks from HBM
+    in place (kGlobalBlocks); very wide states stage vectors per consumer
+    team. Forced here on ordinary trees, with 1- and 2-RHS sweeps."""
+    for k, v in mode.items():
+        monkeypatch.setenv(k, v)
+    rng = orc.Rng(4242)
+    cases = [orc.Problem.from_flat(so.gen_random_instance(3, 9, 4, 7, [3, 2, 2]).flat()),
+             rng.random_instance(5, 200, 4, 3, orc.InstanceOptions(with_l1=True, with_none=True))]
+    n_global = 0
+    for po in cases:
+        prob, cache, ofac = both(po)
+        info = cache.dev_info()
+        n_global += info["items_global"]
+        if "SCENOPT_STAGE" in mode:
+            assert info["consumer_stage"] == 1
+        y = rng.vector(prob.dual_dim, 1.5)
+        r = rng.vector(prob.dual_dim, 1.5)
+        for affine in (True, False):
+            pts, hs = so.sweep(cache, [y, r], affine)
+            for v, pt, h in ((y, pts[0], hs[0]), (r, pts[1], hs[1])):
+                ox, ou = ofac.sweep(v, affine)
+                assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL
+                Hx = orc.apply_H(po, ox, ou)
+                assert np.abs(h - Hx).max() <= TOL * (1 + np.abs(Hx).max())
+    if "SCENOPT_SLOT_KB" in mode:
+        assert n_global > 0
+
+
+@pytest.mark.parametrize("dims", [(120, 60, [3, 2]), (300, 40, [2, 2])])
+def test_wide_states_match_oracle(gpu, dims):
+    """States far wider than the benchmark's (a node block of several
+    hundred KB): the sweep picks the HBM-block / consumer-staged layouts by
+    itself and still matches the oracle."""
+    nx, nu, br = dims
+    prob = so.gen_random_instance(7, nx, nu, 3, br)
+    po = orc.Problem.from_flat(prob.flat())
+    cache = so.factor(prob)
+    ofac = orc.Factor(po)
+    info = cache.dev_info()
+    assert info["items_global"] > 0
+    y = np.random.default_rng(1).uniform(-1, 1, prob.dual_dim)
+    for fn, ofn in ((so.dual_grad, ofac.dual_grad), (so.hessian_vec, ofac.hessian_vec)):
+        pt = fn(cache, prob, y)
+        ox, ou = ofn(y)
+        assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL
+    rep = so.solve(prob, so.SolverConfig(), "nama")
+    assert rep.status == "converged" and rep.verified

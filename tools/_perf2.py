@@ -1,4 +1,5 @@
 import sys, os, ctypes as C, numpy as np
+os.environ["SCN_DBG"] = str(int(os.environ.get("SCN_DBG", "0")) | 4)  # per-role counters on
 sys.path.insert(0, '.')
 import torch
 import paper_2107_01745_b200 as so

@@ -72,8 +72,10 @@ __device__ void grid_reduce(const DualCtx& c, int& ph, double (&v)[K]) {
     c.part[(static_cast<int64_t>(ph) * 64 + threadIdx.x) * c.nblk + blockIdx.x] = t;
   }
   grid_sync(c.bar);
-  if (warp == 0) {
-    for (int k = 0; k < K; ++k) {
+  // the K totals are spread over the block's warps (one L2 round trip each
+  // instead of K in a row); each total keeps the same summation order
+  {
+    for (int k = warp; k < K; k += kWarps) {
       const double* p = c.part + (static_cast<int64_t>(ph) * 64 + k) * c.nblk;
       double t = MAX ? -INFINITY : 0.0;
       for (int b = lane; b < c.nblk; b += 32) t = MAX ? fmax(t, __ldcg(p + b)) : t + __ldcg(p + b);

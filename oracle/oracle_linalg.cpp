@@ -247,8 +247,11 @@ double spectral_radius(const Mat& A0) {
           }
           nn -= 2;
         } else {
-          if (its == 60) ORC_THROW(kError, "spectral_radius: QR iteration did not converge");
-          if (its == 10 || its == 20) {
+          // LAPACK dlahqr budget: 30 max(10, n) sweeps per block, exceptional
+          // shift every 10 (identical to the classic 10/20 shifts for every
+          // block that converges within 30 sweeps)
+          if (its == 30 * std::max(10, n)) ORC_THROW(kError, "spectral_radius: QR iteration did not converge");
+          if (its > 0 && its % 10 == 0) {
             t += x;
             for (int i = 0; i < nn + 1; ++i) a(i, i) -= x;
             const double s = std::abs(a(nn, nn - 1)) + std::abs(a(nn - 1, nn - 2));

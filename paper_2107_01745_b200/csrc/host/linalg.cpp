@@ -154,8 +154,10 @@ double spectral_radius(const double* A0, int n) {
       iter = 0;
       continue;
     }
-    if (iter == 60) fail(SCENOPT_E_ERROR, "spectral_radius: QR iteration did not converge");
-    if (iter == 10 || iter == 20) {  // exceptional shift
+    // LAPACK dlahqr budget: 30 max(10, n) sweeps per block, exceptional shift
+    // every 10 (the classic 10/20 shifts for every block converging within 30)
+    if (iter == 30 * std::max(10, n)) fail(SCENOPT_E_ERROR, "spectral_radius: QR iteration did not converge");
+    if (iter > 0 && iter % 10 == 0) {  // exceptional shift
       shift_acc += x;
       for (int i = 0; i <= hi; ++i) H(i, i) -= x;
       const double s = std::fabs(H(hi, hi - 1)) + std::fabs(H(hi - 1, hi - 2));

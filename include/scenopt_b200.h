@@ -162,6 +162,25 @@ int scenopt_factor_export(const scenopt_factor* f, double* gain, double* child_t
 void scenopt_factor_destroy(scenopt_factor* f);
 
 /* ---- device handle ----------------------------------------------------- */
+/* factor() on the device (riccati.hpp:82-182): the
+ * handle is packed from problem data only and the Riccati factor is computed
+ * by a per-stage GPU kernel directly into the sweep layout (no host factor,
+ * no factor upload). Throws NotStronglyConvex like factor(). */
+int scenopt_dev_create_device_factor(const scenopt_problem* p, int device, scenopt_dev** out);
+/* Recompute the device factor of the handle's problem data in place (the
+ * factor kernels only; e.g. after the handle's data were updated). */
+int scenopt_dev_refactor_device(scenopt_dev* d);
+/* refactor_affine (riccati.hpp:187-216) on the device, for MPC-style
+ * re-solves: only p's linear terms (q, r, c, p_N) and root state move to the
+ * device (O(n (nx+nu)) bytes) and the affine factor terms are recomputed in
+ * place; the matrices of p must be those the handle was factored with.
+ * Requires a handle from scenopt_dev_create_device_factor. */
+int scenopt_dev_refactor_affine(scenopt_dev* d, const scenopt_problem* p);
+/* The device factor in scenopt_factor_export's layout (p: the handle's problem). */
+int scenopt_dev_factor_export(scenopt_dev* d, const scenopt_problem* p, double* gain, double* child_to_input,
+                              double* closed_loop, double* dual_to_input, double* dual_to_costate,
+                              double* input_affine, double* costate_affine, double* value_quad,
+                              double* leaf_costate_affine);
 /* Packs (ProblemInstance, FactorCache) into the stage-major device layout and
  * uploads it. */
 int scenopt_dev_create(const scenopt_problem* p, const scenopt_factor* f, int device,

@@ -210,6 +210,44 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class DeviceFactorCache(FactorCache):
+    """factor() computed on the device (K9): the handle
+    is packed from problem data and the Riccati factor is written into the
+    sweep layout by a per-stage GPU kernel; export() reads it back in the
+    FactorCache layout."""
+
+    def __init__(self, prob: ProblemInstance, device: int = 0):
+        super().__init__(None, prob)
+        h = C.c_void_p()
+        check(N.lib().scenopt_dev_create_device_factor(prob._h, device, C.byref(h)))
+        self._dev = h
+
+    def device(self, device: int = 0):
+        return self._dev
+
+    def shard(self, *a, **k):
+        raise InvalidParams("shard(): a device factor cannot be sharded (use factor())")
+
+    def export(self) -> dict:
+        p = self._prob
+        nx, nu, n, F, L = p.nx, p.nu, p.num_nodes(), p.first_leaf, p.num_leaves
+        S = int(p.flat()["stage_rows"].sum())
+        out = dict(gain=np.zeros(F * nu * nx), child_to_input=np.zeros(n * nu * nx),
+                   closed_loop=np.zeros(n * nx * nx), dual_to_input=np.zeros(max(S, 1) * nu),
+                   dual_to_costate=np.zeros(max(S, 1) * nx), input_affine=np.zeros(F * nu),
+                   costate_affine=np.zeros(F * nx), value_quad=np.zeros(n * nx * nx),
+                   leaf_costate_affine=np.zeros(L * nx))
+        check(N.lib().scenopt_dev_factor_export(self._dev, p._h, *[dptr(out[k]) for k in (
+            "gain", "child_to_input", "closed_loop", "dual_to_input", "dual_to_costate",
+            "input_affine", "costate_affine", "value_quad", "leaf_costate_affine")]))
+        return out
+
+
+def factor_device(prob: ProblemInstance, device: int = 0) -> DeviceFactorCache:
+    """riccati.hpp:82-182 on the GPU (no host factor, no factor upload)."""
+    return DeviceFactorCache(prob, device)
+
+
 def factor(prob: ProblemInstance) -> FactorCache:
     """riccati.hpp:82-182."""
     h = C.c_void_p()
@@ -218,7 +256,13 @@ def factor(prob: ProblemInstance) -> FactorCache:
 
 
 def refactor_affine(cache: FactorCache, prob: ProblemInstance) -> None:
-    """riccati.hpp:187-216 (the device copy is re-packed on next use)."""
+    """riccati.hpp:187-216: new linear terms (q, r, c, p_N) with the same
+    matrices. A device-factored cache recomputes them on the GPU and moves
+    only the vectors (scenopt_dev_refactor_affine)."""
+    if isinstance(cache, DeviceFactorCache):
+        _check_shapes(cache, prob, "refactor_affine")
+        check(N.lib().scenopt_dev_refactor_affine(cache._dev, prob._h))
+        return
     check(N.lib().scenopt_refactor_affine(cache._h, prob._h))
     if cache._dev is not None:
         N.lib().scenopt_dev_destroy(cache._dev)

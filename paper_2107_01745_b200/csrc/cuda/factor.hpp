@@ -1,0 +1,42 @@
+// SPDX-License-Identifier: MIT
+// Device factorization (K9, factor.cu): launch parameters shared with the host.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace scn {
+
+struct FactorParams {
+  int nx, nu, n, first_leaf, nxp;
+  int stage_first, stage_count;   // nodes of this launch
+  const int32_t* child_begin;
+  const int32_t* child_count;
+  const int32_t* dual_offset;     // per node (-1 root)
+  const int32_t* stage_rows;      // per node
+  const double* prob;
+  const double* cost_node;        // per non-root node i at (i-1)*csz (unsharded handles)
+  const double* cost_leaf;        // per leaf l at l*lsz
+  const double* hcoef;            // per dual row: [F row | G row]
+  const int64_t* bw_off;          // per node: E / leaf F_N block start in the bw pass array
+  const int64_t* bw_j;            // per non-root node: J block start
+  const int64_t* k_off;           // per node: K (gain) / T_N block start in the fw pass array
+  double* bw_blk;
+  double* fw_blk;
+  double* aff_bw;                 // [n][nu+nx]
+  double* vq;                     // [n][nx*nx] value_quad
+  double* lchol;                  // [first_leaf][nu*nu] Cholesky factor of the input Hessian (refactor_affine)
+  const double* root_unused;      // (layout padding)
+  int affine_only;                // factor_leaves: update the affine terms only
+  double* ws_global;              // per-CTA workspace when it does not fit in shared memory
+  int64_t ws_doubles;
+  int* bad;                       // first failing node + 1 (0: all strongly convex)
+};
+
+int64_t factor_workspace_doubles(int nx, int nu, int max_rows);
+cudaError_t factor_run_leaves(const FactorParams& F, int grid, cudaStream_t st);
+cudaError_t factor_run_stage(const FactorParams& F, int grid, size_t smem, cudaStream_t st);
+// refactor_affine (riccati.hpp:187-216) of every non-leaf node: new linear terms, same factor
+cudaError_t factor_run_affine(const FactorParams& F, int grid, cudaStream_t st);
+
+}  // namespace scn

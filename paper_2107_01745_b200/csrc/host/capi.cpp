@@ -181,6 +181,34 @@ int scenopt_shard_exchange_buffer(scenopt_dev* h, double** buf, size_t* doubles_
   });
 }
 
+int scenopt_dev_create_device_factor(const scenopt_problem* p, int device, scenopt_dev** out) {
+  SCN_GUARD({
+    auto h = std::make_unique<scenopt_dev>();
+    h->d = dev_create_device_factor(p->p, device);
+    h->init_solver_buffers();
+    *out = h.release();
+  });
+}
+
+int scenopt_dev_factor_export(scenopt_dev* h, const scenopt_problem* p, double* gain, double* c2i, double* cl,
+                              double* d2i, double* d2c, double* ia, double* ca, double* vq, double* lca) {
+  SCN_GUARD({
+    const Factor f = dev_factor_export(*h->d, p->p);
+    auto cp = [](const std::vector<double>& v, double* dst) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    };
+    cp(f.gain, gain);
+    cp(f.child_to_input, c2i);
+    cp(f.closed_loop, cl);
+    cp(f.dual_to_input, d2i);
+    cp(f.dual_to_costate, d2c);
+    cp(f.input_affine, ia);
+    cp(f.costate_affine, ca);
+    cp(f.value_quad, vq);
+    cp(f.leaf_costate_affine, lca);
+  });
+}
+
 int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
   SCN_GUARD({
     const DevState& d = *h->d;

@@ -4,6 +4,8 @@
 #include "device.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -138,7 +140,21 @@ std::unique_ptr<DevState> dev_create_bare(int device) {
   return d;
 }
 
+namespace {
+struct PhaseClock {  // SCN_SETUP_TIMING=1: phase times of dev_create on stderr
+  bool on = std::getenv("SCN_SETUP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dev_create] %-22s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
+
 std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int device, const ShardSpec* shard) {
+  PhaseClock clk;
   if (fptr) check_factor_shape(*fptr, p, "dev_create");
   require_valid(p);
   int ndev = 0;
@@ -206,6 +222,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     d->max_mN = std::max(d->max_mN, leaf ? p.terminal_rows[c - p.first_leaf] : 0);
   }
 
+  clk.mark("sizes");
   // ---- schedule. The grid is one co-resident CTA per SM.
   // A region (per-stage node ranges) is scheduled as: below a cut stage with
   // >= min_sub*G nodes every CTA owns a contiguous, byte-balanced group of
@@ -410,6 +427,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->items_bw = nbw;
   d->items_fw = static_cast<int>(runs.size()) - nbw;
 
+  clk.mark("schedule");
   std::vector<Item> items(runs.size());
   std::vector<int64_t> item_doubles(runs.size());
   int64_t bw_total = 0, fw_total = 0, max_item = 2, max_stage = 16;
@@ -502,9 +520,15 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->stage_doubles = static_cast<int>((max_stage + 15) & ~int64_t(15));
   d->vec_doubles = static_cast<int>((static_cast<int64_t>(max_cnt) * kMaxRhs * nxp + 15) & ~int64_t(15));
 
+  clk.mark("items");
   // ---- pass arrays: [NodeMeta x count | node blocks] per item
   std::vector<double> bw(static_cast<size_t>(bw_total), 0.0), fw(static_cast<size_t>(fw_total), 0.0);
   std::vector<double> aff_bw(static_cast<size_t>(n) * W, 0.0), aff_fw(static_cast<size_t>(n) * nx, 0.0);
+  const bool fz = f.gain.empty();  // layout-only factor: the device factor writes these blocks
+  // per-node block positions (the device factor writes E / J / K in place)
+  d->h_bw_off.assign(static_cast<size_t>(n), -1);
+  d->h_bw_j.assign(static_cast<size_t>(n), -1);
+  d->h_k_off.assign(static_cast<size_t>(n), -1);
   parallel_for(static_cast<int>(items.size()), 64, [&](int qb, int qe) {
     for (int q = qb; q < qe; ++q) {
       const Item& it = items[q];
@@ -535,7 +559,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         double* B0 = base + blk;
         if (it.pass == 0) {
           int64_t jo = 0;
-          if (!leaf) {
+          if (!leaf && fz) {
+            jo = even(static_cast<int64_t>(M[c]) * W);
+          } else if (!leaf) {
             const double* d2i = f.dual_to_input.data() + static_cast<size_t>(cdo[c]) * nu;
             const double* d2c = f.dual_to_costate.data() + static_cast<size_t>(cdo[c]) * nx;
             for (int k = 0; k < M[c]; ++k) {
@@ -553,10 +579,14 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
             const double* FN = p.FNl(l);
             std::copy(FN, FN + static_cast<size_t>(mN) * nx, B0);
             jo = even(static_cast<int64_t>(mN) * nx);
-            const double* lca = f.leaf_costate_affine.data() + static_cast<size_t>(l) * nx;
-            for (int t = 0; t < nx; ++t) aff_bw[static_cast<size_t>(c) * W + nu + t] = lca[t];
+            if (!fz) {
+              const double* lca = f.leaf_costate_affine.data() + static_cast<size_t>(l) * nx;
+              for (int t = 0; t < nx; ++t) aff_bw[static_cast<size_t>(c) * W + nu + t] = lca[t];
+            }
           }
-          if (c != 0) {
+          d->h_bw_off[c] = it.off + blk;
+          d->h_bw_j[c] = it.off + blk + jo;
+          if (c != 0 && !fz) {
             double* J = B0 + jo;
             const double* c2i = f.child_to_input.data() + static_cast<size_t>(c) * nu * nx;
             const double* cl = f.closed_loop.data() + static_cast<size_t>(c) * nx * nx;
@@ -588,7 +618,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
             for (int t = 0; t < nx; ++t) aff_fw[static_cast<size_t>(c) * nx + t] = cc[t];
           }
           double* K = B0 + ko;
-          if (!leaf) {
+          d->h_k_off[c] = it.off + blk + ko;
+          if (!leaf && fz) {
+          } else if (!leaf) {
             const double* gain = f.gain.data() + static_cast<size_t>(c) * nu * nx;
             for (int j = 0; j < nu; ++j)
               for (int k = 0; k < nx; ++k) K[k + static_cast<int64_t>(j) * nxp] = gain[j + static_cast<int64_t>(k) * nu];
@@ -603,6 +635,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     }
   });
 
+  clk.mark("pack");
   // ---- launch configuration: one co-resident CTA per SM. Preference order:
   //   1. producer-staged vectors, every item's blocks in a shared-memory slot,
   //      the deepest slot ring (<= 5) that fits;
@@ -677,6 +710,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   SCN_CUDA(sweep_configure(d->dyn_smem));
   d->G = 0;
 
+  clk.mark("launch config");
   // ---- upload
   d->bw_blk = upload(*d, bw);
   d->fw_blk = upload(*d, fw);
@@ -719,7 +753,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
       }
     }
   }
+  clk.mark("upload blocks");
   pack_common(*d, p, d->sharded() ? &mine : nullptr);
+  clk.mark("pack_common");
   const int D = p.dual_dim;
   if (d->sharded()) {
     d->rank = shard->rank;

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../cuda/dual.hpp"
+#include "../cuda/factor.hpp"
 #include "../cuda/layout.hpp"
 #include "model.hpp"
 
@@ -57,6 +58,12 @@ struct DevState {
   std::vector<Launch> launches;
   int cut_stage = -1;  // CTA subtree-ownership cut of the main region (-1: all global tickets)
   bool consumer_stage = false;  // teams stage their own vectors (very wide states)
+  // node block positions in the pass arrays (doubles; -1: not on this handle)
+  std::vector<int64_t> h_bw_off, h_bw_j, h_k_off;
+  double* vq = nullptr;         // value_quad of the device factor [n][nx*nx]
+  bool device_factor = false;   // E / J / K / aff_bw computed on the device (K9)
+  FactorParams fp{};            // device-factor launch parameters (index arrays on the device)
+  bool fp_ready = false;
   int items_global = 0;         // items whose node blocks are read from HBM in place
   // ---- subtree sharding over ranks
   int rank = 0, world = 1, shard_stage = -1;
@@ -116,6 +123,17 @@ struct ShardSpec {
 std::vector<int> shard_plan(const Problem& p, int world, int* stage);
 std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* f, int device,
                                      const ShardSpec* shard = nullptr);
+// Handle whose factor is computed on the device (K9, factor.cu): the host
+// packs only problem data; the factor blocks are written by the GPU.
+std::unique_ptr<DevState> dev_create_device_factor(const Problem& p, int device);
+// (Re)compute the factor of the handle's own problem data on the device.
+void dev_factor_device(DevState& d);
+// The device factor in the FactorCache layout (riccati.hpp:38-63).
+Factor dev_factor_export(DevState& d, const Problem& p);
+// refactor_affine (riccati.hpp:187-216) on the device: upload p's linear
+// terms (q, r, c, p_N, root state; same matrices) and recompute the affine
+// factor terms in place. Requires a device-factored handle.
+void dev_refactor_affine(DevState& d, const Problem& p);
 // ncclGetUniqueId into 128 bytes
 void nccl_unique_id(void* out128);
 void nccl_comm_init(DevState& d, const void* id128);

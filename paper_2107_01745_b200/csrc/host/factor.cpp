@@ -48,6 +48,39 @@ void check_factor_shape(const Factor& f, const Problem& p, const char* who) {
     fail(SCENOPT_E_CACHE_MISMATCH, std::string(who) + ": cache was built for a different problem shape");
 }
 
+Factor factor_shape(const Problem& p, bool lite) {
+  require_valid(p);
+  const int nx = p.nx, nu = p.nu, n = p.n, Fn = p.first_leaf;
+  Factor f;
+  f.nx = nx;
+  f.nu = nu;
+  f.n = n;
+  f.first_leaf = Fn;
+  f.dual_dim = p.dual_dim;
+  f.L = p.L;
+  f.stage_total = p.stage_total;
+  f.child_dual_offset.assign(static_cast<size_t>(Fn), 0);
+  f.child_dual_rows.assign(static_cast<size_t>(Fn), 0);
+  for (int i = 0; i < Fn; ++i) {
+    const int cb = p.child_begin[i], cc = p.child_count[i];
+    int rows = 0;
+    for (int c = cb; c < cb + cc; ++c) rows += p.stage_rows[c];
+    f.child_dual_rows[i] = rows;
+    f.child_dual_offset[i] = p.dual_offset[cb];
+  }
+  if (lite) return f;  // dimensions and child offsets only (device factor layout)
+  f.gain.assign(static_cast<size_t>(Fn) * p.sxu(), 0.0);
+  f.dual_to_input.assign(static_cast<size_t>(p.stage_total) * nu, 0.0);
+  f.dual_to_costate.assign(static_cast<size_t>(p.stage_total) * nx, 0.0);
+  f.input_affine.assign(static_cast<size_t>(Fn) * nu, 0.0);
+  f.costate_affine.assign(static_cast<size_t>(Fn) * nx, 0.0);
+  f.child_to_input.assign(static_cast<size_t>(n) * p.sxu(), 0.0);
+  f.closed_loop.assign(static_cast<size_t>(n) * p.sxx(), 0.0);
+  f.value_quad.assign(static_cast<size_t>(n) * p.sxx(), 0.0);
+  f.leaf_costate_affine.assign(static_cast<size_t>(p.L) * nx, 0.0);
+  return f;
+}
+
 Factor factor(const Problem& p) {
   require_valid(p);
   const int nx = p.nx, nu = p.nu, n = p.n, Fn = p.first_leaf;

@@ -76,6 +76,8 @@ struct Factor {
 };
 
 Factor factor(const Problem& p);                // riccati.hpp:82-182
+// dimensions and child offsets; zero blocks unless lite (device factor layout)
+Factor factor_shape(const Problem& p, bool lite = false);
 void refactor_affine(Factor& f, const Problem& p);  // riccati.hpp:187-216
 void check_factor_shape(const Factor& f, const Problem& p, const char* who);
 

@@ -669,6 +669,20 @@ struct scenopt_lbfgs {
 // ------------------------------------------------------------------ C-ABI
 extern "C" {
 
+int scenopt_dev_refactor_device(scenopt_dev* h) {
+  SCN_GUARD({
+    dev_factor_device(*h->d);
+    h->w->fhat0_ready = false;  // f_hat(0) and H x(0) depend on the factor
+  });
+}
+
+int scenopt_dev_refactor_affine(scenopt_dev* h, const scenopt_problem* p) {
+  SCN_GUARD({
+    dev_refactor_affine(*h->d, p->p);
+    h->w->fhat0_ready = false;
+  });
+}
+
 int scenopt_fhat_value(scenopt_dev* h, const double* y, double* out, int flags) {
   SCN_GUARD({
     Engine e(*h);

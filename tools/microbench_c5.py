@@ -23,13 +23,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--max-nodes", type=int, default=4_000_000)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default=None, help="comma-separated indices into SHAPES")
     a = ap.parse_args()
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json"))).get("hbm_gbs", 6455.3) \
         if os.path.exists("MEASURED_PEAKS.json") else 6455.3
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     rows = []
-    for nx, nu, H, br in SHAPES:
+    sel = [SHAPES[int(i)] for i in a.only.split(",")] if a.only else SHAPES
+    for nx, nu, H, br in sel:
         n = 1
         w = 1
         for t in range(H):

@@ -615,7 +615,9 @@ struct FactorState {
   std::shared_ptr<scenopt_dev> alt_dev;
   ProblemPtr alt_prob;
 
+  bool on_device = false;  // factored by factor_device(): no host factor, one device handle
   scenopt_dev* device_for(const ProblemInstance& pi) {
+    if (on_device) return dev.get();
     if (&pi == src || src == nullptr) {
       if (!dev) {
         scenopt_dev* d = nullptr;
@@ -717,8 +719,12 @@ struct FactorCache {
     int S = 0;
     for (int i = 1; i < n; ++i) S += prob.stage_rows(i);
     std::vector<double> d2i(static_cast<size_t>(std::max(S, 1)) * nu), d2c(static_cast<size_t>(std::max(S, 1)) * nx);
-    detail::check(scenopt_factor_export(state->fac.get(), g.data(), c2i.data(), cl.data(), d2i.data(), d2c.data(),
-                                        ia.data(), ca.data(), vq.data(), lca.data()));
+    if (state->on_device)
+      detail::check(scenopt_dev_factor_export(state->dev.get(), state->prob.get(), g.data(), c2i.data(), cl.data(),
+                                              d2i.data(), d2c.data(), ia.data(), ca.data(), vq.data(), lca.data()));
+    else
+      detail::check(scenopt_factor_export(state->fac.get(), g.data(), c2i.data(), cl.data(), d2i.data(), d2c.data(),
+                                          ia.data(), ca.data(), vq.data(), lca.data()));
     auto mat = [](const double* src, int r, int c) {
       Mat m(r, c);
       std::copy(src, src + static_cast<size_t>(r) * c, m.data());
@@ -792,10 +798,38 @@ inline FactorCache factor(const ProblemInstance& prob) {
   return c;
 }
 
+/// factor() on the device (K9; B200 extension): the Riccati factor is computed
+/// by a GPU kernel directly into the sweep layout, with no host factor and no
+/// factor upload. Use with refactor_affine() for receding-horizon re-solves.
+inline FactorCache factor_device(const ProblemInstance& prob) {
+  auto st = std::make_shared<detail::FactorState>();
+  st->prob = detail::to_handle(prob);
+  st->src = &prob;
+  st->on_device = true;
+  scenopt_dev* d = nullptr;
+  detail::check(scenopt_dev_create_device_factor(st->prob.get(), 0, &d));
+  st->dev = std::shared_ptr<scenopt_dev>(d, detail::DevDeleter{});
+  FactorCache c;
+  c.nx = prob.nx;
+  c.nu = prob.nu;
+  c.num_nodes = prob.num_nodes();
+  c.first_leaf = prob.tree.first_leaf();
+  c.dual_dim = prob.dual_dim;
+  c.state = st;
+  return c;
+}
+
 /// refactor_affine(), riccati.hpp:187-216: recomputes the affine members for
-/// new q, r, c, p (same matrices) and refreshes the device handle.
+/// new q, r, c, p (same matrices) and refreshes the device handle. On a
+/// factor_device() cache only the linear terms and the root state move to
+/// the device and the affine terms are recomputed there.
 inline void refactor_affine(FactorCache& cache, const ProblemInstance& prob) {
   detail::check_shapes(cache, prob, "refactor_affine");
+  if (cache.state->on_device) {
+    auto ph = detail::to_handle(prob);
+    detail::check(scenopt_dev_refactor_affine(cache.state->dev.get(), ph.get()));
+    return;
+  }
   auto st = std::make_shared<detail::FactorState>(*cache.state);
   auto ph = detail::to_handle(prob);
   detail::check(scenopt_refactor_affine(st->fac.get(), ph.get()));
@@ -1268,7 +1302,9 @@ inline SolverReport solve(const ProblemInstance& prob, const SolverConfig& cfg, 
   const scenopt_solver_config c = detail::c_config(cfg);
   scenopt_report* r = nullptr;
   detail::check(scenopt_solve(h.get(), &c, static_cast<int>(kind),
-                              shared_cache ? shared_cache->state->fac.get() : nullptr, 0, &r));
+                              (shared_cache && !shared_cache->state->on_device) ? shared_cache->state->fac.get()
+                                                                                : nullptr,
+                              0, &r));
   return detail::take_report(r, prob);
 }
 

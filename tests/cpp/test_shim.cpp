@@ -344,6 +344,27 @@ TEST_CASE("the solver entry points agree with solve() and each other", false) {
   CHECK_THROWS_AS(scenopt::solve_minfbe(prob, cache, g, bad, y0), scenopt::InvalidParams);
 }
 
+TEST_CASE("factor_device and refactor_affine (receding horizon)", false) {
+  auto prob = small(61, 4, 2, 4, 2);
+  auto cache = scenopt::factor_device(prob);
+  const auto host = scenopt::factor(prob);
+  Rng rng(62);
+  const Vec y = rng.vector(prob.dual_dim);
+  const Vec a = flat_x(scenopt::dual_grad(cache, prob, y)), b = flat_x(scenopt::dual_grad(host, prob, y));
+  CHECK(max_abs(a - b) < 1e-10 * (1.0 + max_abs(b)));
+  // new initial state and linear costs, same matrices
+  auto prob2 = prob;
+  prob2.root_state = rng.vector(prob.nx, 0.1);
+  for (int i = 1; i < prob2.num_nodes(); ++i) prob2.cost[i].q = prob2.cost[i].q * 1.05;
+  scenopt::refactor_affine(cache, prob2);
+  const auto fresh = scenopt::factor(prob2);
+  const Vec c2 = flat_x(scenopt::dual_grad(cache, prob2, y)), d2 = flat_x(scenopt::dual_grad(fresh, prob2, y));
+  CHECK(max_abs(c2 - d2) < 1e-10 * (1.0 + max_abs(d2)));
+  CHECK(max_abs(c2.segment(prob.tree.first_leaf() * prob.nu, prob.nx) - prob2.root_state) < 1e-14);
+  cache.load_matrices(prob2);
+  CHECK(static_cast<int>(cache.gain.size()) == prob.tree.first_leaf());
+}
+
 int main(int argc, char** argv) {
   const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
   int run = 0;

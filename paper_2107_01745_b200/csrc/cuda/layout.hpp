@@ -80,6 +80,7 @@ struct SweepParams {
   int nxp, Vp;  // padded column lengths (== 2 mod 4) of J/K/TN and W
   int consumer_stage;  // 1: teams stage their own vectors (staging area per team, not per ring entry)
   int global_blocks;   // 1: some items keep their node blocks in HBM (kGlobalBlocks)
+  int small_nodes;     // 1: warp-per-node consumers (nx + nu <= 32, nx + m <= 32, mN <= 32)
   const Item* items;      // CTA-major: CTA b owns items [cta_off[b], cta_off[b+1])
   const int32_t* cta_off;
   const double* bw_blk;

@@ -64,6 +64,12 @@ static_assert(kStageQ % kProducers == 0 && kStageQ % kTeams == 0, "staging ring 
 constexpr int kDoneQ = 8 * kTeams;  // completion ring depth (publisher lag allowed); a multiple of kTeams
 constexpr int kPublisherWarp = kProducers + kTeams * kTeam / 32;
 constexpr int kIssuerWarp = kPublisherWarp + 1;
+#ifndef SCN_WARP_RELEASE
+#define SCN_WARP_RELEASE 0  /* per-warp release measured 1-2% slower than one team barrier */
+#endif
+constexpr bool kWarpRelease = SCN_WARP_RELEASE != 0;
+constexpr int kReleaseArrivals = kWarpRelease ? kTeam / 32 : 1;  // mempty / sempty / done arrivals per item
+constexpr int kScratchBufs = kWarpRelease ? 2 : 1;             // w / x scratch buffers per team
 
 #ifdef SCN_SWEEP_PROFILE
 // cycle counters: [0] prod stage-empty wait [1] prod stage round trip
@@ -73,6 +79,11 @@ __device__ unsigned long long g_prof[16];
 __device__ int g_dbg;  // timing experiments only: bit0 ignore dependencies, bit1 skip compute
 __device__ unsigned long long* g_timeline;  // per item: globaltimer at retirement (null: off)
 __device__ long long* g_trace;              // per item: 8 clock64 stamps of the consumer team (null: off)
+// light per-team counters: cycles accumulated in registers by each team's
+// thread 0, flushed once per CTA (g_prof[8..15]); SCN_DBG bit 3 enables
+#define LC_DECL() long long _lc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long _lt = clock64(); const bool _lon = (g_dbg & 8) && ttid == 0
+#define LC_MARK(slot) do { if (_lon) { const long long _n = clock64(); _lc[slot] += _n - _lt; _lt = _n; } } while (0)
+#define LC_FLUSH() do { if (_lon) for (int _i = 0; _i < 8; ++_i) atomicAdd(&g_prof[8 + _i], (unsigned long long)_lc[_i]); } while (0)
 #define TRACE_IN(i) \
   do { if (g_trace && ttid == 0 && trace_row) trace_row[i] = static_cast<long long>(gtimer()); } while (0)
 #define TRACE(i) \
@@ -94,6 +105,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #else
 #define DBG(bit) 0
+#define LC_DECL()
+#define LC_MARK(slot)
+#define LC_FLUSH()
 #define TRACE(i) (void)0
 #define TRACE_IN(i) (void)0
 #define PROF_T0() (void)0
@@ -540,10 +554,152 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   if (ttid == 0) PROF_T1(13);
 }
 
+// ---------------------------------------------------------------- small nodes
+// nx + nu <= 32 and nx + m <= 32: one warp owns a whole node (lane j computes
+// output j; the costate / state vector moves between the two phases by
+// shuffles), so a team's warps work on four nodes without any barrier.
+// Same products as consume_backward / consume_forward (tree_oracles.hpp:
+// 44-88), sequential sums in index order.
+template <int NRHS>
+__device__ void consume_bw_small(const SweepParams& P, const Item& it, const double* slot, const double* mat,
+                                 const double* st, int ttid) {
+  const int nx = P.nx, nu = P.nu, W = nx + nu, nxp = P.nxp;
+  const int lane = ttid & 31;
+  const bool leaf = it.leaf != 0;
+  const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
+  const double* Y = st;
+  const double* Cn = st + NRHS * it.v0_n;
+  const double* AF = st + NRHS * (it.v0_n + ((it.direct & kDirectContrib) ? 0 : it.v1_n * W));
+  const int ncols = leaf ? nx : W;
+  for (int ni = ttid >> 5; ni < it.count; ni += kTeam / 32) {
+    const NodeMeta& mc = meta[ni];
+    double acc[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
+    const int ja = leaf ? nu + lane : lane;
+    if (lane < ncols) {
+      const int len = leaf ? mc.mN : mc.M;
+      const double* col = mat + mc.blk + lane * len;
+      const double* yv = Y + mc.yoff;
+      for (int k = 0; k < len; ++k) {
+        const double a = col[k];
+#pragma unroll
+        for (int r = 0; r < NRHS; ++r) acc[r] = fma(a, yv[r * it.v0_n + k], acc[r]);
+      }
+      if (!leaf) {
+        if (it.direct & kDirectContrib) {
+          for (int k = 0; k < mc.nkid; ++k)
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r)
+              acc[r] += __ldcg(P.contrib[r] + static_cast<int64_t>(it.v1_lo + mc.kid0 + k) * W + lane);
+        } else {
+          for (int k = 0; k < mc.nkid; ++k)
+#pragma unroll
+            for (int r = 0; r < NRHS; ++r) acc[r] += Cn[r * it.v1_n * W + (mc.kid0 + k) * W + lane];
+        }
+      }
+      const double aff = P.affine ? AF[ni * W + ja] : 0.0;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        acc[r] += aff;
+        if (ja < nu) P.u[r][static_cast<int64_t>(mc.c) * nu + ja] = acc[r];  // u_off
+      }
+    }
+    if (mc.c == 0) continue;  // the root has no parent to contribute to
+    // phase B: contrib_c = J_c' w_c, w[t] held by lane (leaf ? t : nu + t)
+    const int e = leaf ? mc.mN * nx : mc.M * W;
+    const double* J = mat + mc.blk + ((e + 1) & ~1);
+    double b[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) b[r] = 0.0;
+    for (int t = 0; t < nx; ++t) {
+      const int src = leaf ? t : nu + t;
+      const double jt = lane < W ? J[t + lane * nxp] : 0.0;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) b[r] = fma(jt, __shfl_sync(0xffffffffu, acc[r], src), b[r]);
+    }
+    if (lane < W)
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) P.contrib[r][static_cast<int64_t>(mc.c) * W + lane] = b[r];
+  }
+}
+
+template <int NRHS>
+__device__ void consume_fw_small(const SweepParams& P, const Item& it, const double* slot, const double* mat,
+                                 const double* st, int ttid) {
+  const int nx = P.nx, nu = P.nu, Vp = P.Vp, nxp = P.nxp;
+  const int lane = ttid & 31;
+  const bool leaf = it.leaf != 0;
+  const bool root = it.first == 0;
+  const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
+  const int tot = it.v0_n * Vp;
+  const double* PV = st;
+  const double* UO = st + NRHS * tot;
+  const double* AF = st + NRHS * (tot + it.v1_n * nu);
+  for (int ni = ttid >> 5; ni < it.count; ni += kTeam / 32) {
+    const NodeMeta& mc = meta[ni];
+    const int64_t c = mc.c;
+    double xv[NRHS];
+    if (root) {  // x_0 = p (affine) or 0
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        xv[r] = (lane < nx && P.affine) ? P.root_state[lane] : 0.0;
+        if (lane < nx) P.x[r][lane] = xv[r];
+      }
+    } else {
+      // phase A: x_c = [A B] [x_a; u_a] (+c), stage rows [F G] [x_a; u_a]
+      double acc[NRHS];
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
+      if (lane < nx + mc.m) {
+        const double* col = mat + mc.blk + lane * Vp;
+        const double* v = PV + mc.par * Vp;
+        for (int k = 0; k < nx + nu; ++k) {
+          const double a = col[k];
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) acc[r] = fma(a, v[r * tot + k], acc[r]);
+        }
+        if (lane < nx) {
+          const double aff = P.affine ? AF[ni * nx + lane] : 0.0;
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) {
+            acc[r] += aff;
+            P.x[r][c * nx + lane] = acc[r];
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < NRHS; ++r) P.Hx[r][mc.doff + (lane - nx)] = acc[r];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) xv[r] = acc[r];
+    }
+    // phase B: u_c = K x_c + u_off (interior) or terminal rows F_N x_c (leaf); x[t] in lane t
+    const double* K = mat + mc.blk + (root ? 0 : Vp * (nx + mc.m));
+    const int nout = leaf ? mc.mN : nu;
+    double b[NRHS];
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) b[r] = 0.0;
+    for (int t = 0; t < nx; ++t) {
+      const double kt = lane < nout ? K[t + lane * nxp] : 0.0;
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) b[r] = fma(kt, __shfl_sync(0xffffffffu, xv[r], t), b[r]);
+    }
+    if (lane < nout)
+#pragma unroll
+      for (int r = 0; r < NRHS; ++r) {
+        if (leaf)
+          P.Hx[r][mc.tdo + lane] = b[r];
+        else
+          P.u[r][c * nu + lane] = UO[r * it.v1_n * nu + ni * nu + lane] + b[r];
+      }
+  }
+}
+
 // MODE bits (one instantiation per combination, so the common layout's
 // kernel carries no fallback code): kModeConsumerStage = teams stage their own
 // vectors; kModeGlobalBlocks = some items read their node blocks from HBM.
-constexpr int kModeConsumerStage = 1, kModeGlobalBlocks = 2;
+constexpr int kModeConsumerStage = 1, kModeGlobalBlocks = 2, kModeSmallNodes = 4;
 template <int NRHS, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P, int mmax, int mNmax) {
   extern __shared__ __align__(128) double smem[];
@@ -581,18 +737,18 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
     s_epoch = *reinterpret_cast<volatile unsigned*>(P.ctrl) + 1u;
     s_retired = 0;
     for (int s = 0; s < kTeams * NS; ++s) mbar_init(&full[s], 1);
-    for (int s = 0; s < NS; ++s) mbar_init(&mempty[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&mempty[s], kReleaseArrivals);
     for (int q = 0; q < kStageQ; ++q) {
       mbar_init(&sfull[q], 1);
-      mbar_init(&sempty[q], 1);
+      mbar_init(&sempty[q], kReleaseArrivals);
     }
     for (int q = 0; q < kDoneQ; ++q) {
-      mbar_init(&done[q], 1);
+      mbar_init(&done[q], kReleaseArrivals);
       mbar_init(&pdone[q], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = tid; i < kTeams * P.scratch_doubles; i += kThreads) scratch[i] = 0.0;  // zero pads of w / x
+  for (int i = tid; i < kScratchBufs * kTeams * P.scratch_doubles; i += kThreads) scratch[i] = 0.0;  // zero pads of w / x
   __syncthreads();
   const unsigned E = s_epoch;
   if (warp < kProducers) {
@@ -634,19 +790,26 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
     // ------------------------------------------------------------ consumer teams
     const int team = (warp - kTeamWarp0) / (kTeam / 32);
     const int ttid = tid - 32 * kTeamWarp0 - team * kTeam;
-    double* tbuf = scratch + team * P.scratch_doubles;
+    double* const tbuf0 = scratch + static_cast<int64_t>(team) * kScratchBufs * P.scratch_doubles;
+    LC_DECL();
     for (int k = team; k < K; k += kTeams) {
       const int s = k % NS;
       PROF_T0();
       TRACE(0);
+      LC_MARK(7);  // loop overhead
       mbar_wait(&full[k % (kTeams * NS)], static_cast<unsigned>((k / (kTeams * NS)) & 1));
       if (ttid == 0) PROF_T1(3);
       TRACE(1);
+      LC_MARK(0);  // wait matrices
       const int q = k % kStageQ;
       mbar_wait(&sfull[q], static_cast<unsigned>((k / kStageQ) & 1));
       if (ttid == 0) PROF_T1(4);
       TRACE(2);
+      LC_MARK(1);  // wait vectors
       const Item it = sitem[s];
+      // w / x scratch of this item: double-buffered by item parity when the
+      // team's warps release items independently (they may run one item apart)
+      double* tbuf = tbuf0 + ((kScratchBufs == 2) ? ((k / kTeams) & 1) * P.scratch_doubles : 0);
       const double* slot = slots + static_cast<int64_t>(s) * P.slot_doubles;
       // node blocks: in the slot, or (an item larger than a slot) read from
       // HBM/L2 in place; the slot then holds only the item's node headers.
@@ -667,6 +830,18 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       if (g_trace) trace_row = g_trace + 12LL * (P.cta_off[blockIdx.x] + P.items_base + k);
 #endif
       if (DBG(2)) {
+      } else if (MODE & kModeSmallNodes) {
+        if ((MODE & kModeGlobalBlocks) && gblocks) {
+          if (it.pass == 0)
+            consume_bw_small<NRHS>(P, it, slot, gmat, st, ttid);
+          else
+            consume_fw_small<NRHS>(P, it, slot, gmat, st, ttid);
+        } else {
+          if (it.pass == 0)
+            consume_bw_small<NRHS>(P, it, slot, slot, st, ttid);
+          else
+            consume_fw_small<NRHS>(P, it, slot, slot, st, ttid);
+        }
       } else if (it.pass == 0) {
         if ((MODE & kModeGlobalBlocks) && gblocks)
           consume_backward<NRHS>(P, it, slot, gmat, st, tbuf, ttid, team, trace_row);
@@ -679,21 +854,29 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
           consume_forward<NRHS>(P, it, slot, slot, st, tbuf, ttid, team, mmax, mNmax, trace_row);
       }
       TRACE(5);
-      team_sync(team);
+      LC_MARK(2);  // compute (phases A + barrier + B)
+      if (!kWarpRelease || kConsumerStage) team_sync(team);
+      LC_MARK(3);  // end barrier
       if (ttid == 0) PROF_T1(5);
       TRACE(6);
-      if (ttid == 0) {
-        mbar_arrive(&mempty[s]);  // slot reads done (team_sync) -> the issuer may refill it
+      // release: slot reads done -> the issuer may refill the slot; staging
+      // area free; item complete -> the publisher. Per warp (kWarpRelease:
+      // a warp done with phase B moves on without waiting for the others),
+      // else once per team after the barrier above.
+      if (kWarpRelease ? (lane == 0) : (ttid == 0)) {
+        mbar_arrive(&mempty[s]);
         mbar_arrive(&sempty[q]);
         // the publisher must have retired item k-kDoneQ before its DONE phase reuses
         const int dq = k % kDoneQ;
         if (k >= kDoneQ) mbar_wait(&pdone[dq], static_cast<unsigned>((k / kDoneQ - 1) & 1));
-        sdone[dq] = make_int4(it.first, it.count, it.pass, it.publish);
+        if (ttid == 0) sdone[dq] = make_int4(it.first, it.count, it.pass, it.publish);
         mbar_arrive(&done[dq]);
       }
       if (ttid == 0) PROF_T1(6);
       TRACE(7);
+      LC_MARK(4);  // release
     }
+    LC_FLUSH();
   }
   if (warp == kIssuerWarp) {
     // ------------------------------------------------------------ issuer
@@ -778,11 +961,11 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 int sweep_threads() { return kThreads; }
 int sweep_teams() { return kTeams; }
 namespace {
-const void* const kKernels[2][4] = {
-    {reinterpret_cast<const void*>(sweep_kernel<1, 0>), reinterpret_cast<const void*>(sweep_kernel<1, 1>),
-     reinterpret_cast<const void*>(sweep_kernel<1, 2>), reinterpret_cast<const void*>(sweep_kernel<1, 3>)},
-    {reinterpret_cast<const void*>(sweep_kernel<2, 0>), reinterpret_cast<const void*>(sweep_kernel<2, 1>),
-     reinterpret_cast<const void*>(sweep_kernel<2, 2>), reinterpret_cast<const void*>(sweep_kernel<2, 3>)}};
+#define SCN_K(R, M) reinterpret_cast<const void*>(sweep_kernel<R, M>)
+const void* const kKernels[2][8] = {
+    {SCN_K(1, 0), SCN_K(1, 1), SCN_K(1, 2), SCN_K(1, 3), SCN_K(1, 4), SCN_K(1, 5), SCN_K(1, 6), SCN_K(1, 7)},
+    {SCN_K(2, 0), SCN_K(2, 1), SCN_K(2, 2), SCN_K(2, 3), SCN_K(2, 4), SCN_K(2, 5), SCN_K(2, 6), SCN_K(2, 7)}};
+#undef SCN_K
 }  // namespace
 
 size_t sweep_static_smem() {
@@ -796,6 +979,7 @@ size_t sweep_static_smem() {
   return m;
 }
 int sweep_stage_queue() { return kStageQ; }
+int sweep_scratch_bufs() { return kScratchBufs; }
 
 cudaError_t sweep_trace(long long* dev_buf) {
 #ifdef SCN_SWEEP_PROFILE
@@ -878,7 +1062,8 @@ cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mm
   }();
   (void)dbg_set;
 #endif
-  const int mode = (P.consumer_stage ? kModeConsumerStage : 0) | (P.global_blocks ? kModeGlobalBlocks : 0);
+  const int mode = (P.consumer_stage ? kModeConsumerStage : 0) | (P.global_blocks ? kModeGlobalBlocks : 0) |
+                   (P.small_nodes ? kModeSmallNodes : 0);
   const void* fn = kKernels[P.nrhs == 2 ? 1 : 0][mode];
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, dyn_smem, stream);
 }

@@ -654,7 +654,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   const int64_t hdr_doubles_max = static_cast<int64_t>(d->max_count) * (sizeof(NodeMeta) / 8);
   auto smem_for = [&](int ns, int64_t slot, bool consumer) {
     return (static_cast<size_t>(ns) * slot + static_cast<size_t>(consumer ? teams : stageq) * d->stage_doubles +
-            static_cast<size_t>(teams) * d->vec_doubles) * dbl;
+            static_cast<size_t>(teams) * sweep_scratch_bufs() * d->vec_doubles) * dbl;
   };
   int best_ns = 0;
   int64_t slot = 0;
@@ -686,7 +686,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     const int ns = force_ns ? force_ns : 4;
     int64_t sl = slot_cap_env ? slot_cap_env
                               : static_cast<int64_t>((optin / dbl - static_cast<size_t>(cons ? teams : stageq) * d->stage_doubles -
-                                                      static_cast<size_t>(teams) * d->vec_doubles) / ns);
+                                                      static_cast<size_t>(teams) * sweep_scratch_bufs() * d->vec_doubles) / ns);
     sl = std::max<int64_t>(sl, hdr_doubles_max) & ~int64_t(15);
     sl = std::max<int64_t>(sl, (hdr_doubles_max + 15) & ~int64_t(15));
     if (sl > 0 && fits(ns, sl, cons)) best_ns = ns, slot = sl, consumer = cons;
@@ -704,6 +704,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
       ++n_global;
     }
   d->items_global = n_global;
+  // warp-per-node consumers (opt-in, SCENOPT_SMALL_NODES=1): measured slower than
+  // the team path on the C5 nx=10 trees (sequential per-lane dots), kept for work
+  d->small_nodes = (nx + nu <= 32) && (nx + d->max_m <= 32) && (d->max_mN <= 32) && env_int("SCENOPT_SMALL_NODES", 0) != 0;
   d->nslot = best_ns;
   d->ctas_per_sm = 1;
   d->dyn_smem = smem_for(best_ns, slot, consumer);
@@ -926,6 +929,7 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
   P.Vp = d.Vp;
   P.consumer_stage = d.consumer_stage ? 1 : 0;
   P.global_blocks = d.items_global > 0 ? 1 : 0;
+  P.small_nodes = d.small_nodes ? 1 : 0;
   P.bw_blk = d.bw_blk;
   P.fw_blk = d.fw_blk;
   P.aff_bw = d.aff_bw;

@@ -65,6 +65,7 @@ struct DevState {
   FactorParams fp{};            // device-factor launch parameters (index arrays on the device)
   bool fp_ready = false;
   int items_global = 0;         // items whose node blocks are read from HBM in place
+  bool small_nodes = false;     // warp-per-node consumers (small states)
   // ---- subtree sharding over ranks
   int rank = 0, world = 1, shard_stage = -1;
   void* comm = nullptr;         // ncclComm_t
@@ -160,6 +161,7 @@ void dev_gather_primal(DevState& d, double* x, double* u);
 int sweep_teams();
 size_t sweep_static_smem();
 int sweep_stage_queue();
+int sweep_scratch_bufs();
 cudaError_t sweep_configure(size_t dyn_smem);
 cudaError_t sweep_profile_read(unsigned long long* out, bool reset);
 cudaError_t sweep_timeline(unsigned long long* dev_buf);

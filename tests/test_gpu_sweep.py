@@ -155,13 +155,15 @@ def test_default_grid_uses_subtree_ownership_on_c3(gpu):
     assert info["cut_stage"] == 4  # 1024 subtrees >= 4 per CTA
 
 
-@pytest.mark.parametrize("mode", [dict(SCENOPT_SLOT_KB="4"), dict(SCENOPT_STAGE="consumer"),
+@pytest.mark.parametrize("mode", [dict(SCENOPT_SMALL_NODES="1"), dict(SCENOPT_SMALL_NODES="1", SCENOPT_SLOT_KB="4"),
+                                  dict(SCENOPT_SLOT_KB="4"), dict(SCENOPT_STAGE="consumer"),
                                   dict(SCENOPT_SLOT_KB="6", SCENOPT_STAGE="consumer"),
                                   dict(SCENOPT_SLOT_KB="4", SCENOPT_GRID="5", SCENOPT_MIN_SUBTREES="1")])
 def test_fallback_layouts_match_oracle(gpu, monkeypatch, mode):
     """Items larger than a shared-memory slot read their node blocks from HBM
     in place (kGlobalBlocks); very wide states stage vectors per consumer
-    team. Forced here on ordinary trees, with 1- and 2-RHS sweeps."""
+    team; small states can use warp-per-node consumers (opt-in). Forced on
+    ordinary trees, 1- and 2-RHS."""
     for k, v in mode.items():
         monkeypatch.setenv(k, v)
     rng = orc.Rng(4242)

@@ -1,5 +1,5 @@
 import sys, os, ctypes as C, numpy as np
-os.environ["SCN_DBG"] = str(int(os.environ.get("SCN_DBG", "0")) | 4)  # per-role counters on
+os.environ.setdefault("SCN_DBG", "4")  # per-role counters on unless chosen
 sys.path.insert(0, '.')
 import torch
 import paper_2107_01745_b200 as so
@@ -23,7 +23,7 @@ torch.cuda.synchronize()
 prof = (C.c_ulonglong * 16)()
 items = info['items_bw'] + info['items_fw']
 names = ["prod_sempty", "prod_stage", "prod_dep", "team_full", "team_sfull", "team_compute", "team_tail", "pub_fence",
-         "bwA", "bwA_sync", "bwB", "fwA", "fwA_sync", "fwB"]
+         "lc_wait_tma", "lc_wait_vec", "lc_compute", "lc_endbar", "lc_release", "-", "-", "lc_loop"]
 for nrhs, aff in ((1, 0), (1, 1), (2, 0)):
     Y = arr(ys[:nrhs]); H = arr(hs[:nrhs])
     for _ in range(3):
@@ -40,6 +40,6 @@ for nrhs, aff in ((1, 0), (1, 1), (2, 0)):
     ms = e0.elapsed_time(e1) / K
     b = info['sweep_bytes_aff' if aff else ('sweep_bytes_hom2' if nrhs == 2 else 'sweep_bytes_hom')]
     N.lib().scenopt_debug_sweep_profile(prof, 1)
-    per = {names[i]: prof[i] / (items * K) * (2 if i >= 8 else 1) for i in range(len(names))}
+    per = {names[i]: prof[i] / (items * K) for i in range(len(names)) if names[i] != "-"}
     print(f"{shape} nrhs={nrhs} aff={aff}: {ms*1e3:.1f} us, {b/ms/1e6:.0f} GB/s ({b/ms/1e6/6455.3:.1%}) | cyc/item " + " ".join(f"{k}={v:.0f}" for k, v in per.items()), flush=True)
 print({k: info[k] for k in ('grid_ctas', 'slots', 'items_bw', 'items_fw', 'nodes_per_item_max', 'slot_bytes')})

@@ -14,6 +14,21 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
+
+__all__ = [
+    # problem_data.hpp / generators.hpp / solvers.hpp:569-623
+    "PrimalPoint", "ProblemInstance", "gen_random_instance", "precondition",
+    # riccati.hpp (+ device factor, subtree sharding)
+    "FactorCache", "DeviceFactorCache", "factor", "factor_device", "refactor_affine", "nccl_unique_id",
+    # tree_oracles.hpp
+    "OracleStats", "dual_grad", "hessian_vec", "sweep", "grad_fhat", "fhat_value", "apply_H",
+    # prox.hpp / fbe.hpp / lbfgs.hpp
+    "Nonsmooth", "make_nonsmooth", "FbState", "fb_step", "fbe_value", "fbe_grad", "linesearch_cert",
+    "LbfgsBuffer",
+    # solvers.hpp
+    "SolverConfig", "SolverReport", "estimate_dual_lipschitz", "solve_minfbe", "solve_nama", "solve_gpad",
+    "warm_start", "solve", "verify_report",
+]
 from ._native import InvalidParams, check, dptr, iptr
 
 HOST = N.HOST_IO

@@ -402,10 +402,21 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
       SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, k.grad, e.st));
       grad_valid = true;
     }
+    // The L-BFGS direction, its image and the certificate are enqueued before
+    // the simple rule's test (solvers.hpp:279-302) is read, so one host round
+    // trip serves both. When the rule fires, the reference clears the buffer
+    // and rebuilds the state before any of that work counts; the speculative
+    // results are simply discarded (a push made by them is undone by the clear).
+    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], k.prev_y, k.grad,
+                     k.prev_g, k.grad, k.dir, k.Sb, k.Qb, e.st));
+    e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
+    const int nxt = cur ^ 1;
+    SCN_CUDA(k_cert_search(e.ctx(), cur, 0, 1, k.y[cur], k.R[cur], k.Hx[cur], k.HR, k.dir, k.Hd, k.y[nxt],
+                           e.st));
+    e.read_scalars();
     if (cfg.backtracking_rule == 1) {  // simple rule (solvers.hpp:279-302)
       bool halved = false;
       for (;;) {
-        e.read_scalars();
         const bool trigger = lambda * std::sqrt(e.S(sl::IMG2)) > cfg.eps_bt * std::sqrt(e.S(sl::R2));
         if (!trigger) break;
         lambda = halve_lambda(lambda);
@@ -415,6 +426,7 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
         e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
         ++rep.stats.hessian_vec_calls;
         SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, k.grad, e.st));
+        e.read_scalars();
         halved = true;
       }
       if (halved) {
@@ -422,15 +434,8 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
         continue;
       }
     }
-    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], k.prev_y, k.grad,
-                     k.prev_g, k.grad, k.dir, k.Sb, k.Qb, e.st));
     have_pair = false;
-    e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
     ++rep.stats.hessian_vec_calls;
-    const int nxt = cur ^ 1;
-    SCN_CUDA(k_cert_search(e.ctx(), cur, 0, 1, k.y[cur], k.R[cur], k.Hx[cur], k.HR, k.dir, k.Hd, k.y[nxt],
-                           e.st));
-    e.read_scalars();
     if (e.S(sl::STALL) != 0.0) {
       rep.stats.prox_calls += 61;
       rep.stats.conj_calls += 61;

@@ -915,19 +915,40 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       j = __shfl_sync(0xffffffffu, j, 0);
       PROF_T0();
       bool pub = false;
-      for (int q2 = k; q2 < j; ++q2) pub |= sdone[q2 % kDoneQ].w != 0;
+      for (int q2 = k; q2 < j; ++q2) pub |= (sdone[q2 % kDoneQ].w & 1) != 0;
       if (pub) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         for (int q2 = k; q2 < j; ++q2) {
           const int4 dn = sdone[q2 % kDoneQ];
-          if (!dn.w) continue;
+          if (!(dn.w & 1)) continue;
           unsigned* flags = dn.z == 0 ? P.bw_flag : P.fw_flag;
           for (int i = lane; i < dn.y; i += 32)
             asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + dn.x + i), "r"(E) : "memory");
         }
       }
       __syncwarp();
+      // forward progress for overlapped host copies: nodes of each stage
+      // finished so far (gpu-scope release, cumulative over the teams' writes
+      // observed through DONE); the host's copy stream waits on these counters
       if (lane == 0) {
+        // forward progress for overlapped host copies: when this CTA retires
+        // its last forward item of a stage, count the CTA as done with that
+        // stage (one gpu-scope fence per such batch; lane 0 observed every
+        // item of the batch through the DONE waits)
+        if (P.stage_done) {
+          bool fenced = pub;
+          for (int q2 = k; q2 < j; ++q2) {
+            const int4 dn = sdone[q2 % kDoneQ];
+            if (dn.w & 2) {
+              if (!fenced) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                fenced = true;
+              }
+              asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(P.stage_done + ((dn.w >> 2) - 1))
+                           : "memory");
+            }
+          }
+        }
         st_release_cta(&s_retired, j);
 #ifdef SCN_SWEEP_PROFILE
         if (g_timeline || g_trace) {

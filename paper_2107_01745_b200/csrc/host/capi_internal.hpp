@@ -59,4 +59,5 @@ struct scenopt_dev {
   const double* in_dual(const double* src, int flags, int slot);
   void out_copy(double* dst, const double* dev_src, size_t count, int flags);
   void sync();
+  bool overlap_ready();  // host copies overlapped with the sweep (DevState::Overlap) available
 };

@@ -11,6 +11,31 @@
 
 namespace scn {
 
+bool DevState::Overlap::init(DevState& d) {
+  cudaDriverEntryPointQueryResult q{};
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn) {
+    cudaGetLastError();
+    return false;
+  }
+  wait_fn = fn;
+  SCN_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  stage_done = d.alloc<unsigned long long>(static_cast<size_t>(d.lay.N) + 1);
+  expected.assign(static_cast<size_t>(d.lay.N) + 1, 0ull);
+  return true;
+}
+
+void DevState::Overlap::wait(cudaStream_t s, unsigned long long* addr, unsigned long long value) {
+  using Fn = int (*)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);  // CUresult(CUstream, CUdeviceptr, cuuint64_t, flags)
+  const int r = reinterpret_cast<Fn>(wait_fn)(s, reinterpret_cast<unsigned long long>(addr), value, 0u /* GEQ */);
+  if (r != 0) fail(SCENOPT_E_CUDA, "cuStreamWaitValue64 failed (" + std::to_string(r) + ")");
+}
+
+DevState::Overlap::~Overlap() {
+  if (copy_stream) cudaStreamDestroy(copy_stream);
+}
+
 DevState::~DevState() {
   if (device >= 0) cudaSetDevice(device);
   nccl_comm_destroy(comm);
@@ -448,7 +473,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     const bool leaf = ru.first >= p.first_leaf;
     it.leaf = leaf ? 1 : 0;
     it.ldep = ru.ldep;
-    it.publish = ru.publish;
+    it.publish = ru.publish | (ru.pass == 1 ? (p.node_stage[ru.first] + 1) << 2 : 0);
     int64_t stage = 0;
     if (ru.pass == 0) {
       if (leaf) {
@@ -487,6 +512,28 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     max_stage = std::max(max_stage, stage);
     max_item = std::max(max_item, tot);
     max_cnt = std::max(max_cnt, ru.count);
+  }
+  // the last forward item of each stage in every CTA's list signals the
+  // stage's completion to overlapped host copies (DevState::Overlap)
+  d->stage_ctas.assign(static_cast<size_t>(p.N) + 1, 0);
+  {
+    size_t base = 0;
+    for (const auto& off : cta_offs) {
+      for (int gg = 0; gg < G; ++gg) {
+        int last_stage = -1;
+        for (int q = off[gg + 1] - 1; q >= off[gg]; --q) {
+          Item& it = items[base + q];
+          if (it.pass != 1) continue;
+          const int st = p.node_stage[it.first];
+          if (st != last_stage) {  // scanning backwards: first seen = last of its stage
+            it.publish |= 2;
+            ++d->stage_ctas[st];
+            last_stage = st;
+          }
+        }
+      }
+      base += off[G];
+    }
   }
   // Pass-array placement in "time-major" order: item k of every CTA, then
   // item k+1, ... (SCENOPT_PACK=cta: CTA-major). CTAs advance through their
@@ -991,8 +1038,9 @@ void phase_b(DevState& d, SweepParams& P) {
 }  // namespace
 
 void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
-               double* const* u, double* const* Hx, bool gather_primal) {
+               double* const* u, double* const* Hx, bool gather_primal, unsigned long long* stage_done) {
   SweepParams P = sweep_params(d, nrhs, affine, y, x, u, Hx);
+  P.stage_done = d.sharded() ? nullptr : stage_done;
   if (!d.sharded()) {
     launch(d, P, d.launches[0]);
     return;

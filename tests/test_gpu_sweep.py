@@ -208,3 +208,22 @@ def test_wide_states_match_oracle(gpu, dims):
         assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL
     rep = so.solve(prob, so.SolverConfig(), "nama")
     assert rep.status == "converged" and rep.verified
+
+
+def test_overlapped_host_output_is_bitwise_the_serialized_copy(gpu, monkeypatch):
+    """Host outputs copied stage by stage while the forward pass runs (device
+    completion counters + a copy stream) equal the copy after the sweep."""
+    monkeypatch.setenv("SCENOPT_OVERLAP", "1")
+    monkeypatch.setenv("SCENOPT_OVERLAP_KB", "4")  # many groups
+    prob = so.gen_random_instance(2, 12, 5, 9, [3, 3, 2])
+    cache = so.factor(prob)
+    y = np.random.default_rng(4).uniform(-1, 1, prob.dual_dim)
+    runs = [so.dual_grad(cache, prob, y) for _ in range(3)]  # overlapped (opt-in)
+    monkeypatch.setenv("SCENOPT_OVERLAP", "0")
+    cache2 = so.factor(prob)
+    ref = so.dual_grad(cache2, prob, y)
+    for pt in runs:
+        assert np.array_equal(pt.x, ref.x) and np.array_equal(pt.u, ref.u)
+    pts, _ = so.sweep(cache, [y, -y], True)
+    pts2, _ = so.sweep(cache2, [y, -y], True)
+    assert np.array_equal(pts[1].x, pts2[1].x) and np.array_equal(pts[1].u, pts2[1].u)

@@ -69,6 +69,7 @@ static_assert(sizeof(Item) == 64, "Item is one 64-byte record");
 
 constexpr int kDirectContrib = 1;
 constexpr int kGlobalBlocks = 2;
+constexpr int kFlatTop = 4;  // forward top node computed from its ancestors' u_off; depth in bits 8..
 constexpr int kMaxRhs = 2;
 constexpr int kMaxSlots = 8;
 
@@ -88,7 +89,9 @@ struct SweepParams {
   const double* bw_blk;
   const double* fw_blk;
   const double* aff_bw;  // [n][nu+nx]: [input_affine; costate_affine] / [0; pi p_N]
-  const double* aff_fw;  // [n][nx]: c_c
+  const double* aff_fw;  // [n][nx]: c_c (flattened top: the constant a'_c)
+  const double* aff_fwh; // [n][mmax]: constant of the flattened top's stage rows
+  int mmax;
   const double* root_state;
   unsigned* ctrl;     // [0] epoch, [1] done-CTA counter
   unsigned* bw_flag;  // [n]
@@ -96,6 +99,7 @@ struct SweepParams {
   const double* y[kMaxRhs];
   double* x[kMaxRhs];
   double* u[kMaxRhs];
+  double* uoff[kMaxRhs];  // [first_leaf][nu] backward input offsets (the forward pass reads, never overwrites)
   double* Hx[kMaxRhs];
   double* contrib[kMaxRhs];  // [n][nu+nx] scratch
 };

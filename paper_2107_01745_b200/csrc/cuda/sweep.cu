@@ -210,7 +210,12 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 __device__ __forceinline__ const unsigned* dep_flags(const SweepParams& P, const Item& it) {
-  return (it.pass == 0 || it.first == 0) ? P.bw_flag : P.fw_flag;
+  return (it.pass == 0 || it.first == 0 || (it.direct & kFlatTop)) ? P.bw_flag : P.fw_flag;
+}
+// padded dot length of a flattened top node of depth k (== 2 mod 4, as pad2 on the host)
+__device__ __forceinline__ int flat_len(int k, int nu) {
+  const int l = k * nu;
+  return l + ((2 - l % 4) + 4) % 4;
 }
 
 __device__ __forceinline__ bool flags_ready(const unsigned* flags, const Item& it, unsigned E, int lane) {
@@ -248,6 +253,35 @@ __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, in
       double* ad = st + NRHS * (it.v0_n + ((it.direct & kDirectContrib) ? 0 : nc));
       for (int i = lane; i < na; i += nt) cp_async8(ad + i, as + i);
     }
+  } else if (it.direct & kFlatTop) {
+    // flattened top: PV_r = [u_off(root); u_off(a_1); u_off(a_2); 0-pad] shared by the
+    // item's siblings, then UO_r (own u_off), AFX (a'), AFH (stage-row constants)
+    const int k = it.direct >> 8, Lp = flat_len(k, nu), nuo = it.v1_n * nu;
+#pragma unroll
+    for (int r = 0; r < NRHS; ++r) {
+      double* pd = st + r * Lp;
+      for (int e = lane; e < Lp; e += nt) {
+        const int i = e / nu, j = e - i * nu;
+        if (i < k) {
+          const int a = i == 0 ? 0 : (i == 1 ? it.v0_lo : it.v0_n);
+          cp_async8(pd + e, P.uoff[r] + static_cast<int64_t>(a) * nu + j);
+        } else {
+          pd[e] = 0.0;
+        }
+      }
+      const double* os = P.uoff[r] + static_cast<int64_t>(it.v1_lo) * nu;
+      double* od = st + NRHS * Lp + r * nuo;
+      for (int i = lane; i < nuo; i += nt) cp_async8(od + i, os + i);
+    }
+    if (P.affine) {
+      double* ad = st + NRHS * (Lp + nuo);
+      const int na = it.count * nx;
+      const double* as = P.aff_fw + static_cast<int64_t>(it.first) * nx;
+      for (int i = lane; i < na; i += nt) cp_async8(ad + i, as + i);
+      const int nh = it.count * P.mmax;
+      const double* hs = P.aff_fwh + static_cast<int64_t>(it.first) * P.mmax;
+      for (int i = lane; i < nh; i += nt) cp_async8(ad + na + i, hs + i);
+    }
   } else {
     const int tot = it.v0_n * Vp, nuo = it.v1_n * nu;
 #pragma unroll
@@ -265,7 +299,7 @@ __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, in
             pd[e] = 0.0;
         }
       }
-      const double* os = P.u[r] + static_cast<int64_t>(it.v1_lo) * nu;
+      const double* os = P.uoff[r] + static_cast<int64_t>(it.v1_lo) * nu;
       double* od = st + NRHS * tot + r * nuo;
       for (int i = lane; i < nuo; i += nt) cp_async8(od + i, os + i);
     }
@@ -418,7 +452,7 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
       for (int r = 0; r < NRHS; ++r) {
         const double v = acc[r] + aff;
         if (ja < nu)
-          P.u[r][static_cast<int64_t>(mc.c) * nu + ja] = v;  // u_off, completed by the forward pass
+          P.uoff[r][static_cast<int64_t>(mc.c) * nu + ja] = v;  // u_off, completed by the forward pass
         else
           wbuf[(ni * NRHS + r) * nxp + (ja - nu)] = v;  // costate w_c
       }
@@ -448,6 +482,9 @@ struct FwPhaseA {
   const double* AF;
   double* xbuf;
   int nx, Vp, nxp, ncols, tot, single;
+  int flat;             // flattened top: one shared vector PV (ancestors' u_off), column stride Vp = Lp
+  const double* AFH;    // flattened top: stage-row constants [count][mmaxh]
+  int mmaxh;
   template <int S>
   __device__ __forceinline__ void run(int task, int q, bool active) const {
     int ni = 0, j = 0;
@@ -459,7 +496,7 @@ struct FwPhaseA {
       const NodeMeta& mc = meta[ni];
       active = j < nx + mc.m;
       col = slot + mc.blk + j * Vp;
-      v = PV + mc.par * Vp;
+      v = flat ? PV : PV + mc.par * Vp;
     }
     double acc[NRHS];
     dot_split<NRHS, S>(col, v, tot, active ? Vp : 0, q, acc);
@@ -475,8 +512,9 @@ struct FwPhaseA {
           P.x[r][c * nx + j] = xv;
         }
       } else {
+        const double h = (flat && P.affine) ? AFH[ni * mmaxh + (j - nx)] : 0.0;
 #pragma unroll
-        for (int r = 0; r < NRHS; ++r) P.Hx[r][mc.doff + (j - nx)] = acc[r];
+        for (int r = 0; r < NRHS; ++r) P.Hx[r][mc.doff + (j - nx)] = acc[r] + h;
       }
     }
   }
@@ -527,7 +565,9 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   const bool leaf = it.leaf != 0;
   const bool root = it.first == 0;
   const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
-  const int tot = it.v0_n * Vp;
+  const bool flat = (it.direct & kFlatTop) != 0;
+  const int cstride = flat ? flat_len(it.direct >> 8, nu) : Vp;  // phase-A column length
+  const int tot = flat ? cstride : it.v0_n * Vp;
   const double* PV = st;
   const double* UO = st + NRHS * tot;
   const double* AF = st + NRHS * (tot + it.v1_n * nu);
@@ -540,7 +580,8 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
       P.x[r][k] = v;
     }
   } else {
-    const FwPhaseA<NRHS> body{P, meta, mat, PV, AF, xbuf, nx, Vp, nxp, nx + mmax, tot, cnt == 1 ? 1 : 0};
+    const FwPhaseA<NRHS> body{P,     meta, mat, PV, AF, xbuf, nx, cstride, nxp, nx + mmax, tot, cnt == 1 ? 1 : 0,
+                              flat ? 1 : 0, AF + cnt * nx, P.mmax};
     for_tasks(cnt * (nx + mmax), ttid, body);
   }
   if (ttid == 0) PROF_T1(11);
@@ -548,7 +589,7 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   team_sync(team);
   if (ttid == 0) PROF_T1(12);
   TRACE_IN(4);
-  const FwPhaseB<NRHS> body{P, meta, mat, UO, xbuf, nx, nu, Vp, nxp, leaf ? mNmax : nu, it.v1_n * nu,
+  const FwPhaseB<NRHS> body{P, meta, mat, UO, xbuf, nx, nu, cstride, nxp, leaf ? mNmax : nu, it.v1_n * nu,
                             leaf ? 1 : 0, root ? 1 : 0, cnt == 1 ? 1 : 0};
   for_tasks(cnt * (leaf ? mNmax : nu), ttid, body);
   if (ttid == 0) PROF_T1(13);
@@ -602,7 +643,7 @@ __device__ void consume_bw_small(const SweepParams& P, const Item& it, const dou
 #pragma unroll
       for (int r = 0; r < NRHS; ++r) {
         acc[r] += aff;
-        if (ja < nu) P.u[r][static_cast<int64_t>(mc.c) * nu + ja] = acc[r];  // u_off
+        if (ja < nu) P.uoff[r][static_cast<int64_t>(mc.c) * nu + ja] = acc[r];  // u_off
       }
     }
     if (mc.c == 0) continue;  // the root has no parent to contribute to

@@ -166,6 +166,10 @@ std::unique_ptr<DevState> dev_create_bare(int device) {
 }
 
 namespace {
+struct FlatTop {  // flattened forward top node (see dev_create)
+  std::vector<double> G, L, a, h;
+};
+
 struct PhaseClock {  // SCN_SETUP_TIMING=1: phase times of dev_create on stderr
   bool on = std::getenv("SCN_SETUP_TIMING") != nullptr;
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
@@ -228,6 +232,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   }
   const Factor& f = *fptr;
   d->has_factor = true;
+  const bool fz = f.gain.empty();  // layout-only factor: the device factor writes these blocks
 
   // ---- per-node block sizes (doubles, even => 16-byte aligned); padded
   // column lengths pad2(l) == 2 (mod 4) for conflict-free 16-byte smem loads
@@ -270,7 +275,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   const int cap = std::max(1, env_int("SCENOPT_ITEM_MAX_NODES", 32));
   const int min_sub = env_int("SCENOPT_MIN_SUBTREES", 4);  // per CTA; 0 disables ownership
   const int min_items = 8;  // independent items per stage and CTA (local dependency distance)
-  struct Run { int first, count, pass, ldep, gdep, publish; };
+  struct Run { int first, count, pass, ldep, gdep, publish, flat = 0; };
   using Lists = std::vector<std::vector<Run>>;
   auto chunk = [&](int lo, int hi, int pass, int per_stage_min, std::vector<Run>& out) {
     const std::vector<int64_t>& size = pass == 0 ? bws : fws;
@@ -369,8 +374,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
           if (r.first >= p.first_leaf) continue;
           lo = p.child_begin[r.first];
           hi = p.child_begin[last] + p.child_count[last];
-        } else if (r.first == 0) {
-          lo = 0, hi = 1;  // forward root <- backward root
+        } else if (r.first == 0 || r.flat) {
+          lo = 0, hi = 1;  // forward root / flattened top <- backward root
         } else {
           lo = p.ancestor[r.first];
           hi = p.ancestor[last] + 1;
@@ -409,6 +414,36 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   if (!shard) {
     Lists bw_l, fw_l;
     d->cut_stage = region(0, p.N, full, true, true, true, bw_l, fw_l);
+    // Flattened forward top: with a host factor and a cut at
+    // stage 2..4, every node above the cut computes x / u / Hx in one level
+    // from its ancestors' u_off (affine maps precomputed below) as soon as the
+    // backward root is done, instead of a chain of per-stage dependencies.
+    const int cut = d->cut_stage;
+    d->flat_top = !fz && cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0 &&
+                  env_int("SCENOPT_SMALL_NODES", 0) == 0;
+    if (d->flat_top)
+      for (auto& lst : fw_l) {
+        std::vector<Run> out;
+        for (const Run& r : lst) {
+          const int st = p.node_stage[r.first];
+          if (r.pass != 1 || st < 1 || st >= cut) {
+            out.push_back(r);
+            continue;
+          }
+          int a = r.first;  // split at parent boundaries: an item's nodes share their ancestors
+          while (a < r.first + r.count) {
+            int b2 = a + 1;
+            while (b2 < r.first + r.count && p.ancestor[b2] == p.ancestor[a]) ++b2;
+            Run q = r;
+            q.first = a;
+            q.count = b2 - a;
+            q.flat = 1;
+            out.push_back(q);
+            a = b2;
+          }
+        }
+        lst.swap(out);
+      }
     for (int gg = 0; gg < G; ++gg) bw_l[gg].insert(bw_l[gg].end(), fw_l[gg].begin(), fw_l[gg].end());
     launch_lists.push_back(std::move(bw_l));
   } else {
@@ -453,6 +488,12 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->items_fw = static_cast<int>(runs.size()) - nbw;
 
   clk.mark("schedule");
+  // flattened top nodes: (nx + m) columns over the ancestors' u_off (k nu,
+  // padded) followed by the gain block
+  if (d->flat_top)
+    for (int c = 1; c < p.stage_offsets[d->cut_stage]; ++c)
+      fws[c] = even(static_cast<int64_t>(nx + p.stage_rows[c]) * pad2(p.node_stage[c] * nu) +
+                    static_cast<int64_t>(nxp) * nu);
   std::vector<Item> items(runs.size());
   std::vector<int64_t> item_doubles(runs.size());
   int64_t bw_total = 0, fw_total = 0, max_item = 2, max_stage = 16;
@@ -492,6 +533,18 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
       it.direct = it.v1_n > 2 * ru.count ? 1 : 0;  // > 2 children per node on average
       stage = kMaxRhs * (static_cast<int64_t>(it.v0_n) + (it.direct ? 0 : static_cast<int64_t>(it.v1_n) * W)) +
               static_cast<int64_t>(ru.count) * W;
+    } else if (ru.flat) {  // flattened top: ancestors a_1 / a_2 in v0_lo / v0_n, the root is a_0
+      const int k = p.node_stage[ru.first];
+      const int par = p.ancestor[ru.first];
+      it.dep_lo = 0;
+      it.dep_hi = 1;
+      it.v0_lo = k >= 2 ? (k == 2 ? par : p.ancestor[par]) : 0;
+      it.v0_n = k >= 3 ? par : 0;
+      it.v1_lo = ru.first;
+      it.v1_n = ru.count;
+      it.direct = kFlatTop | (k << 8);
+      stage = kMaxRhs * (static_cast<int64_t>(pad2(k * nu)) + static_cast<int64_t>(ru.count) * nu) +
+              static_cast<int64_t>(ru.count) * (nx + d->max_m);
     } else {
       if (ru.first == 0) {
         it.dep_lo = 0;
@@ -571,7 +624,67 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   // ---- pass arrays: [NodeMeta x count | node blocks] per item
   std::vector<double> bw(static_cast<size_t>(bw_total), 0.0), fw(static_cast<size_t>(fw_total), 0.0);
   std::vector<double> aff_bw(static_cast<size_t>(n) * W, 0.0), aff_fw(static_cast<size_t>(n) * nx, 0.0);
-  const bool fz = f.gain.empty();  // layout-only factor: the device factor writes these blocks
+  // flattened forward top (host factor): x_c = a'_c + sum_i G_{c,i} u_off(a_i)
+  // by the recursion x_c = CL_c x_p + B_c u_off(p) + c_c (u_p = K_p x_p + u_off(p)):
+  //   G_{c,i} = CL_c G_{p,i} (i < k-1), G_{c,k-1} = B_c, a'_c = CL_c a'_p + c_c, a'_0 = x_0;
+  // stage rows z_c = F_c x_p + G'_c u_p = (F_c + G'_c K_p) x_p + G'_c u_off(p).
+  std::vector<FlatTop> flat;
+  std::vector<double> aff_fwh(static_cast<size_t>(n) * std::max(d->max_m, 1), 0.0);
+  if (d->flat_top) {
+    flat.resize(static_cast<size_t>(p.stage_offsets[d->cut_stage]));
+    flat[0].a.assign(p.root_state.begin(), p.root_state.end());
+    for (int c = 1; c < p.stage_offsets[d->cut_stage]; ++c) {
+      const int k = p.node_stage[c], pr = p.ancestor[c], mm = p.stage_rows[c];
+      const FlatTop& fp = flat[pr];
+      FlatTop& ft = flat[c];
+      const double* CL = f.closed_loop.data() + static_cast<size_t>(c) * nx * nx;
+      const double* Bc = p.Bi(c);
+      ft.G.assign(static_cast<size_t>(k) * nu * nx, 0.0);  // k matrices nx x nu, column-major
+      for (int i = 0; i + 1 < k; ++i)
+        for (int j = 0; j < nu; ++j)
+          for (int r = 0; r < nx; ++r) {
+            double s2 = 0.0;
+            for (int z = 0; z < nx; ++z) s2 += CL[r + static_cast<size_t>(z) * nx] * fp.G[(static_cast<size_t>(i) * nu + j) * nx + z];
+            ft.G[(static_cast<size_t>(i) * nu + j) * nx + r] = s2;
+          }
+      for (int j = 0; j < nu; ++j)
+        for (int r = 0; r < nx; ++r) ft.G[(static_cast<size_t>(k - 1) * nu + j) * nx + r] = Bc[r + static_cast<size_t>(j) * nx];
+      ft.a.assign(static_cast<size_t>(nx), 0.0);
+      const double* cc = p.ci(c);
+      for (int r = 0; r < nx; ++r) {
+        double s2 = cc[r];
+        for (int z = 0; z < nx; ++z) s2 += CL[r + static_cast<size_t>(z) * nx] * fp.a[z];
+        ft.a[r] = s2;
+      }
+      // stage rows: M = F_c + G'_c K_p (m x nx)
+      const double* Fm = p.Fi(c);
+      const double* Gm = p.Gi(c);
+      const double* Kp = f.gain.data() + static_cast<size_t>(pr) * nu * nx;
+      std::vector<double> Mf(static_cast<size_t>(mm) * nx);
+      for (int z = 0; z < nx; ++z)
+        for (int q = 0; q < mm; ++q) {
+          double s2 = Fm[q + static_cast<size_t>(z) * mm];
+          for (int w = 0; w < nu; ++w) s2 += Gm[q + static_cast<size_t>(w) * mm] * Kp[w + static_cast<size_t>(z) * nu];
+          Mf[q + static_cast<size_t>(z) * mm] = s2;
+        }
+      ft.L.assign(static_cast<size_t>(k) * nu * mm, 0.0);  // k matrices m x nu
+      for (int i = 0; i + 1 < k; ++i)
+        for (int j = 0; j < nu; ++j)
+          for (int q = 0; q < mm; ++q) {
+            double s2 = 0.0;
+            for (int z = 0; z < nx; ++z) s2 += Mf[q + static_cast<size_t>(z) * mm] * fp.G[(static_cast<size_t>(i) * nu + j) * nx + z];
+            ft.L[(static_cast<size_t>(i) * nu + j) * mm + q] = s2;
+          }
+      for (int j = 0; j < nu; ++j)
+        for (int q = 0; q < mm; ++q) ft.L[(static_cast<size_t>(k - 1) * nu + j) * mm + q] = Gm[q + static_cast<size_t>(j) * mm];
+      ft.h.assign(static_cast<size_t>(mm), 0.0);
+      for (int q = 0; q < mm; ++q) {
+        double s2 = 0.0;
+        for (int z = 0; z < nx; ++z) s2 += Mf[q + static_cast<size_t>(z) * mm] * fp.a[z];
+        ft.h[q] = s2;
+      }
+    }
+  }
   // per-node block positions (the device factor writes E / J / K in place)
   d->h_bw_off.assign(static_cast<size_t>(n), -1);
   d->h_bw_j.assign(static_cast<size_t>(n), -1);
@@ -643,6 +756,27 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
             }
           }
           blk += bws[c];
+        } else if (it.direct & kFlatTop) {
+          // x_c = a'_c + sum_i G_{c,i} u_off(a_i); z_c = h'_c + sum_i L_{c,i} u_off(a_i)
+          const int k = p.node_stage[c];
+          const int Lp = pad2(k * nu);
+          const FlatTop& ft = flat[c];
+          for (int r = 0; r < nx + mm; ++r) {
+            double* col = B0 + static_cast<int64_t>(r) * Lp;
+            for (int i = 0; i < k; ++i)
+              for (int j = 0; j < nu; ++j)
+                col[i * nu + j] = r < nx ? ft.G[(static_cast<size_t>(i) * nu + j) * nx + r]
+                                         : ft.L[(static_cast<size_t>(i) * nu + j) * mm + (r - nx)];
+          }
+          for (int t = 0; t < nx; ++t) aff_fw[static_cast<size_t>(c) * nx + t] = ft.a[t];
+          for (int s2 = 0; s2 < mm; ++s2) aff_fwh[static_cast<size_t>(c) * d->max_m + s2] = ft.h[s2];
+          const int64_t ko = static_cast<int64_t>(Lp) * (nx + mm);
+          double* K = B0 + ko;
+          d->h_k_off[c] = it.off + blk + ko;
+          const double* gain = f.gain.data() + static_cast<size_t>(c) * nu * nx;
+          for (int j = 0; j < nu; ++j)
+            for (int kk = 0; kk < nx; ++kk) K[kk + static_cast<int64_t>(j) * nxp] = gain[j + static_cast<int64_t>(kk) * nu];
+          blk += fws[c];
         } else {
           int64_t ko = 0;
           if (c != 0) {
@@ -770,6 +904,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   fw.shrink_to_fit();
   d->aff_bw = upload(*d, aff_bw);
   d->aff_fw = upload(*d, aff_fw);
+  d->aff_fwh = upload(*d, aff_fwh);
   d->root_state = upload(*d, p.root_state);
   {
     size_t base = 0;
@@ -816,6 +951,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
 
   for (int r = 0; r < kMaxRhs; ++r) {
     d->contrib[r] = d->alloc<double>(static_cast<size_t>(n) * W);
+    d->uoff[r] = d->alloc<double>(static_cast<size_t>(std::max(p.first_leaf, 1)) * nu);
     d->xs[r] = d->alloc<double>(static_cast<size_t>(n) * nx);
     d->us[r] = d->alloc<double>(static_cast<size_t>(std::max(p.first_leaf, 1)) * nu);
     d->hs[r] = d->alloc<double>(static_cast<size_t>(std::max(D, 1)));
@@ -981,6 +1117,8 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
   P.fw_blk = d.fw_blk;
   P.aff_bw = d.aff_bw;
   P.aff_fw = d.aff_fw;
+  P.aff_fwh = d.aff_fwh;
+  P.mmax = d.max_m;
   P.root_state = d.root_state;
   P.ctrl = d.ctrl;
   P.bw_flag = d.bw_flag;
@@ -991,6 +1129,7 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
     P.u[r] = (u && u[r]) ? u[r] : d.us[r];
     P.Hx[r] = (Hx && Hx[r]) ? Hx[r] : d.hs[r];
     P.contrib[r] = d.contrib[r];
+    P.uoff[r] = d.uoff[r];
   }
   return P;
 }

@@ -58,6 +58,8 @@ struct DevState {
   std::vector<Launch> launches;
   int cut_stage = -1;  // CTA subtree-ownership cut of the main region (-1: all global tickets)
   bool consumer_stage = false;  // teams stage their own vectors (very wide states)
+  bool flat_top = false;        // flattened forward top (one level after the backward root)
+  double* aff_fwh = nullptr;    // [n][max_m] constant of the flattened top's stage rows
   // node block positions in the pass arrays (doubles; -1: not on this handle)
   std::vector<int64_t> h_bw_off, h_bw_j, h_k_off;
   double* vq = nullptr;         // value_quad of the device factor [n][nx*nx]
@@ -96,6 +98,7 @@ struct DevState {
   double *row_lo = nullptr, *row_hi = nullptr, *row_wg = nullptr;
   // sweep scratch (2 RHS)
   double* contrib[kMaxRhs] = {nullptr, nullptr};
+  double* uoff[kMaxRhs] = {nullptr, nullptr};  // backward input offsets
   double* xs[kMaxRhs] = {nullptr, nullptr};
   double* us[kMaxRhs] = {nullptr, nullptr};
   double* hs[kMaxRhs] = {nullptr, nullptr};

@@ -227,3 +227,26 @@ def test_overlapped_host_output_is_bitwise_the_serialized_copy(gpu, monkeypatch)
     pts, _ = so.sweep(cache, [y, -y], True)
     pts2, _ = so.sweep(cache2, [y, -y], True)
     assert np.array_equal(pts[1].x, pts2[1].x) and np.array_equal(pts[1].u, pts2[1].u)
+
+
+@pytest.mark.parametrize("flat", ["1", "0"])
+def test_flattened_forward_top_matches_oracle_on_c3(gpu, monkeypatch, flat):
+    """The forward top above the cut (stages 1..3 at C3) computed in one level
+    from the ancestors' u_off with precomputed affine maps, against the
+    oracle and against the per-stage chain (SCENOPT_FLAT_TOP=0)."""
+    monkeypatch.setenv("SCENOPT_FLAT_TOP", flat)
+    prob = so.gen_random_instance(1, 50, 20, 20, [8, 8, 8, 2])
+    po = orc.Problem.from_flat(prob.flat())
+    cache = so.factor(prob)
+    assert cache.dev_info()["cut_stage"] == 4
+    ofac = orc.Factor(po)
+    rng = np.random.default_rng(11)
+    y = rng.uniform(-1, 1, prob.dual_dim)
+    r = rng.uniform(-1, 1, prob.dual_dim)
+    for affine in (True, False):
+        pts, hs = so.sweep(cache, [y, r], affine)
+        for v, pt, h in ((y, pts[0], hs[0]), (r, pts[1], hs[1])):
+            ox, ou = ofac.sweep(v, affine)
+            assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL
+            Hx = orc.apply_H(po, ox, ou)
+            assert np.abs(h - Hx).max() <= TOL * (1 + np.abs(Hx).max())

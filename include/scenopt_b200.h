@@ -118,6 +118,8 @@ typedef struct scenopt_dev_info {
   int32_t shard_first, shard_past; /* this rank's shard-stage node ids [first, past) */
   int32_t items_global;   /* items too large for a shared-memory slot (blocks read from HBM in place) */
   int32_t consumer_stage; /* 1: vectors staged by the consumer teams (very wide states) */
+  int32_t flat_top;       /* 1: forward stages above the cut flattened into one level */
+  int32_t device_factor;  /* 1: factor computed on the device (scenopt_dev_create_device_factor) */
 } scenopt_dev_info;
 
 typedef struct scenopt_problem scenopt_problem;

@@ -327,7 +327,82 @@ __global__ void __launch_bounds__(kT) factor_affine(FactorParams F) {
   }
 }
 
+__device__ __forceinline__ int pad2d(int l) { return l + ((2 - l % 4) + 4) % 4; }
+
+// Flattened forward top of node c (stage k, parent p): x_c = a'_c + sum_i G_{c,i} u_off(a_i),
+// stage rows z_c = h'_c + sum_i L_{c,i} u_off(a_i), with (device.cpp, host variant)
+//   G_{c,i} = CL_c G_{p,i} (i < k-1), G_{c,k-1} = B_c, a'_c = CL_c a'_p + c_c,
+//   L_{c,i} = Mf G_{p,i}, L_{c,k-1} = G'_c, h'_c = Mf a'_p, Mf = F_c + G'_c K_p.
+__global__ void __launch_bounds__(kT) factor_flat(FactorParams F) {
+  const int nx = F.nx, nu = F.nu, W = nx + nu, nxp = F.nxp;
+  const int64_t xx = static_cast<int64_t>(nx) * nx, xu = static_cast<int64_t>(nx) * nu,
+                uu = static_cast<int64_t>(nu) * nu;
+  const int64_t csz = 2 * xx + 2 * xu + uu + 2 * nx + nu;
+  extern __shared__ __align__(16) double sm[];  // Mf (m x nx) | a'_p (nx)
+  for (int q = blockIdx.x; q < F.stage_count; q += gridDim.x) {
+    const int c = F.stage_first + q;
+    const int m = F.stage_rows[c];
+    const int p = F.ancestor[c];
+    int k = 0;
+    for (int a = c; a > 0; a = F.ancestor[a]) ++k;  // stage of c
+    const int Lp = pad2d(k * nu), Lpp = pad2d((k - 1) * nu);
+    double* blk = F.fw_blk + F.flat_off[c];
+    const double* pblk = k >= 2 ? F.fw_blk + F.flat_off[p] : nullptr;
+    const double* J = F.bw_blk + F.bw_j[c];  // CL[a, t] = J[a + (nu + t) nxp]
+    const double* cost = F.cost_node + static_cast<int64_t>(c - 1) * csz;
+    const double *Bc = cost + xx, *cc = Bc + xu;
+    const double* Kb = F.fw_blk + F.k_off[p];  // K_p[w, z] = Kb[z + w nxp]
+    const double* hc = F.hcoef + static_cast<int64_t>(F.dual_offset[c]) * W;
+    double* Mf = sm;
+    double* ap = sm + static_cast<int64_t>(m) * nx;
+    for (int e = threadIdx.x; e < m * nx; e += kT) {
+      const int s2 = e % m, z = e / m;
+      double v = hc[static_cast<int64_t>(s2) * W + z];
+      for (int w = 0; w < nu; ++w) v = fma(hc[static_cast<int64_t>(s2) * W + nx + w], Kb[z + static_cast<int64_t>(w) * nxp], v);
+      Mf[e] = v;
+    }
+    for (int e = threadIdx.x; e < nx; e += kT) ap[e] = p == 0 ? F.root_state[e] : F.aff_fw[static_cast<int64_t>(p) * nx + e];
+    __syncthreads();
+    if (!F.flat_consts_only) {
+      for (int e = threadIdx.x; e < (nx + m) * k * nu; e += kT) {
+        const int r = e / (k * nu), ij = e - r * (k * nu), i = ij / nu, j = ij - i * nu;
+        double v = 0.0;
+        if (i == k - 1) {
+          v = r < nx ? Bc[r + static_cast<int64_t>(j) * nx] : hc[static_cast<int64_t>(r - nx) * W + nx + j];
+        } else {
+          for (int z = 0; z < nx; ++z) {
+            const double g = pblk[static_cast<int64_t>(z) * Lpp + i * nu + j];  // G_{p,i}[z, j]
+            v = fma(r < nx ? J[r + static_cast<int64_t>(nu + z) * nxp] : Mf[(r - nx) + z * m], g, v);
+          }
+        }
+        blk[static_cast<int64_t>(r) * Lp + ij] = v;
+      }
+    }
+    for (int r = threadIdx.x; r < nx + m; r += kT) {
+      double v = r < nx ? cc[r] : 0.0;
+      for (int z = 0; z < nx; ++z) v = fma(r < nx ? J[r + static_cast<int64_t>(nu + z) * nxp] : Mf[(r - nx) + z * m], ap[z], v);
+      if (r < nx)
+        F.aff_fw[static_cast<int64_t>(c) * nx + r] = v;
+      else
+        F.aff_fwh[static_cast<int64_t>(c) * F.mmax + (r - nx)] = v;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+cudaError_t factor_run_flat(const FactorParams& F, int grid, cudaStream_t st) {
+  int mmax = F.mmax > 0 ? F.mmax : 1;
+  const size_t smem = sizeof(double) * (static_cast<size_t>(mmax) * F.nx + F.nx);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(factor_flat, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  factor_flat<<<grid, kT, smem, st>>>(F);
+  return cudaGetLastError();
+}
 
 cudaError_t factor_run_affine(const FactorParams& F, int grid, cudaStream_t st) {
   const size_t smem = sizeof(double) * (F.nu + 2 * F.nx);

@@ -235,6 +235,8 @@ int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
     info->shard_past = d.shard_hi;
     info->items_global = d.items_global;
     info->consumer_stage = d.consumer_stage ? 1 : 0;
+    info->flat_top = d.flat_top ? 1 : 0;
+    info->device_factor = d.device_factor ? 1 : 0;
   });
 }
 

@@ -45,6 +45,12 @@ FactorParams& params(DevState& d) {
   F.child_count = up(d, L.child_count);
   F.dual_offset = up(d, L.dual_offset);
   F.stage_rows = up(d, L.stage_rows);
+  F.ancestor = up(d, L.ancestor);
+  F.flat_off = d.flat_top ? up(d, d.h_flat_off) : nullptr;
+  F.aff_fw = d.aff_fw;
+  F.aff_fwh = d.aff_fwh;
+  F.mmax = d.max_m;
+  F.root_state = d.root_state;
   F.prob = d.cost.prob;
   F.cost_node = d.cost.node;
   F.cost_leaf = d.cost.leaf;
@@ -61,6 +67,18 @@ FactorParams& params(DevState& d) {
   F.bad = d.alloc<int>(1);
   d.fp_ready = true;
   return F;
+}
+// flattened forward top (device.cpp, kFlatTop): stages 1 .. cut-1 in order,
+// each reads its parents' maps
+void run_flat(DevState& d, FactorParams& F, int consts_only) {
+  if (!d.flat_top) return;
+  const Layout& L = d.lay;
+  F.flat_consts_only = consts_only;
+  for (int t = 1; t < d.cut_stage; ++t) {
+    F.stage_first = L.stage_offsets[t];
+    F.stage_count = L.stage_offsets[t + 1] - L.stage_offsets[t];
+    SCN_CUDA(factor_run_flat(F, std::min(d.sm_count * 2, F.stage_count), d.stream));
+  }
 }
 }  // namespace
 
@@ -97,6 +115,7 @@ void dev_factor_device(DevState& d) {
     F.stage_count = L.stage_offsets[t + 1] - L.stage_offsets[t];
     SCN_CUDA(factor_run_stage(F, std::min(grid_max, F.stage_count), smem, d.stream));
   }
+  run_flat(d, F, 0);
   int bad = 0;
   SCN_CUDA(cudaMemcpyAsync(&bad, F.bad, sizeof(int), cudaMemcpyDeviceToHost, d.stream));
   SCN_CUDA(cudaStreamSynchronize(d.stream));
@@ -144,6 +163,7 @@ void dev_refactor_affine(DevState& d, const Problem& p) {
   F.stage_count = L.n - L.first_leaf;
   SCN_CUDA(factor_run_leaves(F, std::min(grid, std::max(1, F.stage_count)), d.stream));
   SCN_CUDA(factor_run_affine(F, std::min(grid, std::max(1, L.first_leaf)), d.stream));
+  run_flat(d, F, 1);
   SCN_CUDA(cudaStreamSynchronize(d.stream));
 }
 

@@ -419,7 +419,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     // from its ancestors' u_off (affine maps precomputed below) as soon as the
     // backward root is done, instead of a chain of per-stage dependencies.
     const int cut = d->cut_stage;
-    d->flat_top = !fz && cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0 &&
+    d->flat_top = cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0 &&
                   env_int("SCENOPT_SMALL_NODES", 0) == 0;
     if (d->flat_top)
       for (auto& lst : fw_l) {
@@ -630,7 +630,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   // stage rows z_c = F_c x_p + G'_c u_p = (F_c + G'_c K_p) x_p + G'_c u_off(p).
   std::vector<FlatTop> flat;
   std::vector<double> aff_fwh(static_cast<size_t>(n) * std::max(d->max_m, 1), 0.0);
-  if (d->flat_top) {
+  if (d->flat_top && !fz) {  // device factor: factor_flat (cuda/factor.cu) fills these after K9
     flat.resize(static_cast<size_t>(p.stage_offsets[d->cut_stage]));
     flat[0].a.assign(p.root_state.begin(), p.root_state.end());
     for (int c = 1; c < p.stage_offsets[d->cut_stage]; ++c) {
@@ -689,6 +689,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->h_bw_off.assign(static_cast<size_t>(n), -1);
   d->h_bw_j.assign(static_cast<size_t>(n), -1);
   d->h_k_off.assign(static_cast<size_t>(n), -1);
+  d->h_flat_off.assign(static_cast<size_t>(n), -1);
   parallel_for(static_cast<int>(items.size()), 64, [&](int qb, int qe) {
     for (int q = qb; q < qe; ++q) {
       const Item& it = items[q];
@@ -760,6 +761,13 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
           // x_c = a'_c + sum_i G_{c,i} u_off(a_i); z_c = h'_c + sum_i L_{c,i} u_off(a_i)
           const int k = p.node_stage[c];
           const int Lp = pad2(k * nu);
+          d->h_flat_off[c] = it.off + blk;
+          const int64_t ko = static_cast<int64_t>(Lp) * (nx + mm);
+          d->h_k_off[c] = it.off + blk + ko;
+          if (fz) {
+            blk += fws[c];
+            continue;
+          }
           const FlatTop& ft = flat[c];
           for (int r = 0; r < nx + mm; ++r) {
             double* col = B0 + static_cast<int64_t>(r) * Lp;
@@ -770,9 +778,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
           }
           for (int t = 0; t < nx; ++t) aff_fw[static_cast<size_t>(c) * nx + t] = ft.a[t];
           for (int s2 = 0; s2 < mm; ++s2) aff_fwh[static_cast<size_t>(c) * d->max_m + s2] = ft.h[s2];
-          const int64_t ko = static_cast<int64_t>(Lp) * (nx + mm);
           double* K = B0 + ko;
-          d->h_k_off[c] = it.off + blk + ko;
           const double* gain = f.gain.data() + static_cast<size_t>(c) * nu * nx;
           for (int j = 0; j < nu; ++j)
             for (int kk = 0; kk < nx; ++kk) K[kk + static_cast<int64_t>(j) * nxp] = gain[j + static_cast<int64_t>(kk) * nu];

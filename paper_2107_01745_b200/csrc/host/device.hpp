@@ -61,7 +61,7 @@ struct DevState {
   bool flat_top = false;        // flattened forward top (one level after the backward root)
   double* aff_fwh = nullptr;    // [n][max_m] constant of the flattened top's stage rows
   // node block positions in the pass arrays (doubles; -1: not on this handle)
-  std::vector<int64_t> h_bw_off, h_bw_j, h_k_off;
+  std::vector<int64_t> h_bw_off, h_bw_j, h_k_off, h_flat_off;
   double* vq = nullptr;         // value_quad of the device factor [n][nx*nx]
   bool device_factor = false;   // E / J / K / aff_bw computed on the device (K9)
   FactorParams fp{};            // device-factor launch parameters (index arrays on the device)

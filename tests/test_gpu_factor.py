@@ -122,3 +122,34 @@ def test_mpc_style_resolve_after_refactor_affine(gpu):
         assert rep.status == "converged"
         assert abs(rep.iterations - orep["iterations"]) <= 1
         assert np.abs(rep.x.x.ravel(order="F") - orep["x"]).max() < 1e-3 * (1 + np.abs(orep["x"]).max())
+
+
+@pytest.mark.parametrize("flat", ["1", "0"])
+def test_device_factor_flattened_top_on_c3(gpu, monkeypatch, flat):
+    """Device-factored handle at C3: the flattened forward top's maps
+    (G = CL G_p, L = (F + G'K_p) G_p, a' = CL a'_p + c, h' = (F + G'K_p) a'_p)
+    computed on the device after K9 (factor_flat, cuda/factor.cu), against the
+    oracle; then refactor_affine (new c / q / r / p_N / root state) recomputes
+    the constants a' / h' and the handle sweeps the new problem."""
+    monkeypatch.setenv("SCENOPT_FLAT_TOP", flat)
+    prob = so.gen_random_instance(1, 50, 20, 20, [8, 8, 8, 2])
+    cache = so.factor_device(prob)
+    info = cache.dev_info()
+    assert info["cut_stage"] == 4 and info["device_factor"] == 1 and info["flat_top"] == int(flat)
+    rng = np.random.default_rng(12)
+    y = rng.uniform(-1, 1, prob.dual_dim)
+    r = rng.uniform(-1, 1, prob.dual_dim)
+    flat_data = prob.flat()
+    for step in range(2):
+        po = orc.Problem.from_flat(prob.flat())
+        ofac = orc.Factor(po)
+        for affine in (True, False):
+            pts, hs = so.sweep(cache, [y, r], affine)
+            for v, pt, h in ((y, pts[0], hs[0]), (r, pts[1], hs[1])):
+                ox, ou = ofac.sweep(v, affine)
+                assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < 1e-9
+                Hx = orc.apply_H(po, ox, ou)
+                assert np.abs(h - Hx).max() <= 1e-9 * (1 + np.abs(Hx).max())
+        if step == 0:
+            prob = so.ProblemInstance.from_flat(_perturbed(flat_data, orc.Rng(5)))
+            so.refactor_affine(cache, prob)

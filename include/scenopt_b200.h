@@ -140,6 +140,55 @@ int scenopt_problem_create(const scenopt_problem_view* v, scenopt_problem** out)
  * reproduce the reference's full-branching tree. */
 int scenopt_problem_gen_random(uint64_t seed, int nx, int nu, int horizon, const int32_t* branching,
                                int nbranch, scenopt_problem** out);
+/* SpringMassParams, generators.hpp:49-64. Arrays of length 0 take the
+ * reference defaults (generators.hpp:149-162); transition is row-major. */
+typedef struct scenopt_spring_mass_params {
+  double mass_kg, stiffness, damping, input_bound, velocity_bound;
+  int32_t horizon;
+  double sampling, state_weight, input_weight, terminal_weight;
+  int32_t initial_len, transition_rows, transition_cols, mode_values_len, root_state_len;
+  const double* initial_probs;
+  const double* transition;
+  const double* mode_values;
+  const double* root_state;
+} scenopt_spring_mass_params;
+/* the member defaults of SpringMassParams (generators.hpp:50-59), empty arrays */
+void scenopt_spring_mass_defaults(scenopt_spring_mass_params* par);
+/* gen_spring_mass, generators.hpp:119-218: ZOH-discretized spring-mass-damper
+ * array (nx = 2M, nu = M-1) on the Markov mode tree (build_from_markov,
+ * scenario_tree.hpp:72-126). par == NULL: defaults. */
+int scenopt_problem_gen_spring_mass(int masses, const scenopt_spring_mass_params* par, scenopt_problem** out);
+/* detail::spring_mass_continuous, generators.hpp:70-91: A (2M x 2M), B (2M x M-1), column-major */
+int scenopt_spring_mass_continuous(int masses, const scenopt_spring_mass_params* par, double* A, double* B);
+/* discretize_zoh, generators.hpp:97-112 (exp of [[A, B], [0, 0]]·period), column-major */
+int scenopt_discretize_zoh(const double* A, const double* B, int n, int m, double period, double* Ad, double* Bd);
+/* matrix exponential (Eigen MatrixBase::exp semantics: Pade scaling and squaring), column-major n x n */
+int scenopt_expm(const double* X, int n, double* out);
+/* sample_initial_state, generators.hpp:223-234: `count` consecutive draws from
+ * std::mt19937_64(seed), each 2M doubles, into out */
+int scenopt_sample_initial_states(int masses, const scenopt_spring_mass_params* par, uint64_t seed, int count,
+                                  double* out);
+/* ---- problem files, problem_io.hpp:18-559 ("scenopt-problem-v1" JSON) ---- */
+/* serialize_problem (:480): canonical text (sorted keys, 2-space indent, "\n"
+ * terminated). buf == NULL queries the length (*len, without the NUL); then
+ * call again with cap >= *len + 1. */
+int scenopt_problem_serialize(scenopt_problem* p, char* buf, size_t cap, size_t* len);
+/* parse_problem (:484) / problem_from_json (:323): SCENOPT_E_PARSE_ERROR on
+ * malformed JSON, a wrong schema, missing keys, ragged data, or an instance
+ * that fails validation (message lists every violation). */
+int scenopt_problem_parse(const char* text, size_t len, scenopt_problem** out);
+/* validate_problem_text (:512): number of violations (0: parses and
+ * validates), messages joined by '\n' into buf */
+int scenopt_problem_validate_text(const char* text, size_t len, char* buf, int buflen);
+int scenopt_problem_save(const scenopt_problem* p, const char* path);  /* save_problem (:494) */
+int scenopt_problem_load(const char* path, scenopt_problem** out);    /* load_problem (:502) */
+/* content_hash (:539) and factor_hash (:546): FNV-1a of the canonical text /
+ * of the factor-determining fields (no root state, modes or nonsmooth specs) */
+int scenopt_problem_hashes(const scenopt_problem* p, uint64_t* content, uint64_t* factor);
+/* ScenarioTree::mode (scenario_tree.hpp:41): per-node Markov mode, -1 at the
+ * root; empty when unknown. get returns the count (0: none). */
+int scenopt_problem_set_mode(scenopt_problem* p, const int32_t* mode, int n);
+int scenopt_problem_get_mode(const scenopt_problem* p, int32_t* out, int cap);
 /* Pointers into the handle's own arrays (valid until destroy). */
 int scenopt_problem_get_view(scenopt_problem* p, scenopt_problem_view* v, int32_t* dual_dim);
 /* dims = {nx, nu, num_stages, num_nodes, num_leaves, first_leaf, dual_dim, primal_dim} */
@@ -300,6 +349,47 @@ int scenopt_report_arrays(const scenopt_report* r, double* x, double* u, double*
 int scenopt_verify_report(const scenopt_problem* p, scenopt_report* r, const double* z_override,
                           int device);
 void scenopt_report_destroy(scenopt_report* r);
+
+/* ---- experiment harness, experiment.hpp:22-283 -------------------------- */
+typedef struct scenopt_experiment scenopt_experiment; /* RunReport */
+/* ExperimentRow (:63-80); strings and the trace point into the report */
+typedef struct scenopt_experiment_row {
+  const char* instance_id;
+  const char* solver;
+  const char* error; /* "" unless the factorization or the solve threw */
+  int32_t iterations;
+  uint64_t dual_grad_calls, hessian_vec_calls, prox_calls;
+  double final_residual_inf, wall_ms;
+  int32_t converged, fbe_monotone, trace_len;
+  const double* residual_trace;
+} scenopt_experiment_row;
+/* SolverSummary (:86-96) */
+typedef struct scenopt_solver_summary {
+  char solver[16];
+  int32_t count, converged, fbe_violations;
+  double median_calls, p84_calls, p95_calls, frac_within_50, total_wall_ms;
+} scenopt_solver_summary;
+/* run_experiment (:222-283): every solver ("minfbe", "nama", "pnama" = NAMA
+ * with the parallel line search, "gpad") on every instance, in order, through
+ * scenopt_solve on `device`. reuse_factors shares one factor per factor hash
+ * (not with preconditioning). A run that fails with a scenopt error is
+ * recorded in its row; CUDA / NCCL / allocation failures abort the batch. */
+int scenopt_run_experiment(const scenopt_problem* const* problems, const char* const* ids, int count,
+                           const char* const* solvers, int nsolvers, const scenopt_solver_config* cfg,
+                           int include_timing, int reuse_factors, int device, scenopt_experiment** out);
+int scenopt_experiment_row_count(const scenopt_experiment* x);
+int scenopt_experiment_row_get(const scenopt_experiment* x, int i, scenopt_experiment_row* row);
+/* which: 0 csv() (:137), 1 traces_csv() (:153), 2 summary_json().dump(2) + "\n"
+ * (:194; metadata_json: a JSON object text or NULL). buf == NULL queries the length. */
+int scenopt_experiment_text(scenopt_experiment* x, int which, const char* metadata_json, char* buf, size_t cap,
+                            size_t* len);
+/* summaries() (:163): returns the number of solvers, fills up to cap */
+int scenopt_experiment_summaries(const scenopt_experiment* x, scenopt_solver_summary* out, int cap);
+void scenopt_experiment_destroy(scenopt_experiment* x);
+/* treebench's solve report (treebench.cpp:52-85): "scenopt-solvereport-v1"
+ * JSON of one solve of problem p, dump(2) + "\n"; buf == NULL queries the length */
+int scenopt_report_json(const scenopt_report* r, const scenopt_problem* p, const char* solver, int converged,
+                        char* buf, size_t cap, size_t* len);
 
 #ifdef __cplusplus
 }

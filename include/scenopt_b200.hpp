@@ -28,6 +28,7 @@
 #include <initializer_list>
 #include <limits>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -513,7 +514,12 @@ inline ProblemPtr to_handle(const ProblemInstance& pi) {
   if (!fp.shape_errors.empty()) throw DimensionMismatch(fp.shape_errors.front());
   scenopt_problem* h = nullptr;
   check(scenopt_problem_create(&fp.view, &h));
-  return ProblemPtr(h, ProblemDeleter{});
+  ProblemPtr out(h, ProblemDeleter{});
+  if (static_cast<int>(pi.tree.mode.size()) == pi.num_nodes()) {
+    std::vector<int32_t> mode(pi.tree.mode.begin(), pi.tree.mode.end());
+    check(scenopt_problem_set_mode(h, mode.data(), static_cast<int>(mode.size())));
+  }
+  return out;
 }
 
 /// Structured instance from a C handle (inverse of to_handle).
@@ -535,6 +541,11 @@ inline ProblemInstance from_handle(scenopt_problem* h) {
     for (int i = t.stage_offsets[s]; i < t.stage_offsets[s + 1]; ++i) t.node_stage[i] = s;
   t.children.assign(static_cast<size_t>(n), {});
   for (int i = 1; i < n; ++i) t.children[static_cast<size_t>(t.ancestor[i])].push_back(i);
+  {
+    std::vector<int32_t> mode(static_cast<size_t>(n));
+    const int k = check(scenopt_problem_get_mode(h, mode.data(), n));
+    t.mode.assign(mode.begin(), mode.begin() + k);
+  }
   pi.root_state = Vec(std::vector<double>(v.root_state, v.root_state + nx));
   const int F0 = t.first_leaf(), L = n - F0;
   pi.dyn.resize(static_cast<size_t>(n));
@@ -693,6 +704,152 @@ inline ProblemInstance gen_random_instance(std::uint64_t seed, RandomDims dims, 
                                            &h));
   std::unique_ptr<scenopt_problem, detail::ProblemDeleter> hp(h);
   return detail::from_handle(h);
+}
+
+// ------------------------------------------------------------------ generators.hpp:39-234
+/// Spring-mass-damper array benchmark parameters (generators.hpp:49-64).
+/// Empty members take the reference defaults.
+struct SpringMassParams {
+  double mass_kg = 5.0;
+  double stiffness = 1.0;
+  double damping = 0.1;
+  double input_bound = 2.0;
+  double velocity_bound = 5.0;
+  int horizon = 11;
+  double sampling = 0.5;
+  double state_weight = 5.0;
+  double input_weight = 2.0;
+  double terminal_weight = 100.0;
+  Vec initial_probs;
+  Mat transition;
+  Vec mode_values;
+  Vec root_state;
+};
+namespace detail {
+struct SpringMassC {
+  scenopt_spring_mass_params c{};
+  std::vector<double> t;  // transition, row-major
+  explicit SpringMassC(const SpringMassParams& p) {
+    c.mass_kg = p.mass_kg;
+    c.stiffness = p.stiffness;
+    c.damping = p.damping;
+    c.input_bound = p.input_bound;
+    c.velocity_bound = p.velocity_bound;
+    c.horizon = p.horizon;
+    c.sampling = p.sampling;
+    c.state_weight = p.state_weight;
+    c.input_weight = p.input_weight;
+    c.terminal_weight = p.terminal_weight;
+    c.initial_len = p.initial_probs.size();
+    c.initial_probs = p.initial_probs.data();
+    c.mode_values_len = p.mode_values.size();
+    c.mode_values = p.mode_values.data();
+    c.root_state_len = p.root_state.size();
+    c.root_state = p.root_state.data();
+    if (p.transition.size() > 0) {
+      for (int i = 0; i < p.transition.rows(); ++i)
+        for (int j = 0; j < p.transition.cols(); ++j) t.push_back(p.transition(i, j));
+      c.transition_rows = p.transition.rows();
+      c.transition_cols = p.transition.cols();
+      c.transition = t.data();
+    }
+  }
+};
+/// detail::spring_mass_continuous (generators.hpp:70-91).
+inline void spring_mass_continuous(int masses, const SpringMassParams& par, Mat& A, Mat& B) {
+  SpringMassC c(par);
+  A = Mat(2 * masses, 2 * masses);
+  B = Mat(2 * masses, masses - 1);
+  check(scenopt_spring_mass_continuous(masses, &c.c, A.data(), B.data()));
+}
+}  // namespace detail
+
+/// discretize_zoh (generators.hpp:97-112).
+inline void discretize_zoh(const Mat& A, const Mat& B, double period, Mat& Ad, Mat& Bd) {
+  if (A.rows() != A.cols() || B.rows() != A.rows())
+    throw DimensionMismatch("discretize_zoh: A must be square and match B");
+  Ad = Mat(A.rows(), A.cols());
+  Bd = Mat(B.rows(), B.cols());
+  detail::check(scenopt_discretize_zoh(A.data(), B.data(), A.rows(), B.cols(), period, Ad.data(), Bd.data()));
+}
+
+/// gen_spring_mass (generators.hpp:119-218).
+inline ProblemInstance gen_spring_mass(int masses, const SpringMassParams& params = {}) {
+  detail::SpringMassC c(params);
+  scenopt_problem* h = nullptr;
+  detail::check(scenopt_problem_gen_spring_mass(masses, &c.c, &h));
+  std::unique_ptr<scenopt_problem, detail::ProblemDeleter> hp(h);
+  return detail::from_handle(h);
+}
+
+/// sample_initial_state (generators.hpp:223-234): one draw of the caller's engine per component.
+inline Vec sample_initial_state(int masses, const SpringMassParams& params, std::mt19937_64& gen) {
+  if (masses < 2) throw InvalidParams("sample_initial_state: masses must be >= 2");
+  const double half = 0.5 * params.velocity_bound, pos_box = 1.0 * params.velocity_bound;
+  auto sym = [&gen]() { return 2.0 * (static_cast<double>(gen() >> 11) * 0x1.0p-53) - 1.0; };
+  Vec state(2 * masses);
+  for (int i = 0; i < masses; ++i) state(i) = pos_box * sym();
+  for (int i = masses; i < state.size(); ++i) state(i) = half * sym();
+  return state;
+}
+
+// ------------------------------------------------------------------ problem_io.hpp:18-559
+/// Problem files: JSON documents with schema "scenopt-problem-v1" (the
+/// canonical text of the library's serializer; nlohmann DOM entry points
+/// problem_to_json / problem_from_json are text-based here).
+inline constexpr const char* kProblemSchema = "scenopt-problem-v1";
+
+inline std::string serialize_problem(const ProblemInstance& prob) {
+  auto h = detail::to_handle(prob);
+  size_t n = 0;
+  detail::check(scenopt_problem_serialize(h.get(), nullptr, 0, &n));
+  std::string out(n + 1, '\0');
+  detail::check(scenopt_problem_serialize(h.get(), out.data(), n + 1, &n));
+  out.resize(n);
+  return out;
+}
+inline ProblemInstance parse_problem(const std::string& text) {
+  scenopt_problem* h = nullptr;
+  detail::check(scenopt_problem_parse(text.data(), text.size(), &h));
+  std::unique_ptr<scenopt_problem, detail::ProblemDeleter> hp(h);
+  return detail::from_handle(h);
+}
+inline void save_problem(const ProblemInstance& prob, const std::string& path) {
+  auto h = detail::to_handle(prob);
+  detail::check(scenopt_problem_save(h.get(), path.c_str()));
+}
+inline ProblemInstance load_problem(const std::string& path) {
+  scenopt_problem* h = nullptr;
+  detail::check(scenopt_problem_load(path.c_str(), &h));
+  std::unique_ptr<scenopt_problem, detail::ProblemDeleter> hp(h);
+  return detail::from_handle(h);
+}
+inline std::vector<std::string> validate_problem_text(const std::string& text) {
+  std::vector<char> buf(1 << 16);
+  const int k = detail::check(scenopt_problem_validate_text(text.data(), text.size(), buf.data(),
+                                                            static_cast<int>(buf.size())));
+  std::vector<std::string> out;
+  std::string all(buf.data());
+  for (size_t pos = 0; k > 0 && pos < all.size();) {
+    const size_t nl = all.find('\n', pos);
+    const std::string line = all.substr(pos, nl == std::string::npos ? std::string::npos : nl - pos);
+    if (!line.empty()) out.push_back(line);
+    if (nl == std::string::npos) break;
+    pos = nl + 1;
+  }
+  return out;
+}
+inline std::uint64_t content_hash(const ProblemInstance& prob) {
+  auto h = detail::to_handle(prob);
+  std::uint64_t c = 0;
+  detail::check(scenopt_problem_hashes(h.get(), &c, nullptr));
+  return c;
+}
+inline std::uint64_t factor_hash(const ProblemInstance& prob) {
+  auto h = detail::to_handle(prob);
+  std::uint64_t f = 0;
+  detail::check(scenopt_problem_hashes(h.get(), nullptr, &f));
+  return f;
 }
 
 // ------------------------------------------------------------------ riccati.hpp:38-216
@@ -1306,6 +1463,137 @@ inline SolverReport solve(const ProblemInstance& prob, const SolverConfig& cfg, 
                                                                                 : nullptr,
                               0, &r));
   return detail::take_report(r, prob);
+}
+
+// ------------------------------------------------------------------ experiment.hpp:22-283
+/// One solver column of an experiment (p-NAMA: NAMA with the parallel line search).
+struct SolverSpec {
+  std::string name;
+  SolverKind kind = SolverKind::Nama;
+  bool parallel_linesearch = false;
+};
+inline SolverSpec solver_spec_from_name(const std::string& name) {
+  if (name == "minfbe") return {"minfbe", SolverKind::Minfbe, false};
+  if (name == "nama") return {"nama", SolverKind::Nama, false};
+  if (name == "pnama") return {"pnama", SolverKind::Nama, true};
+  if (name == "gpad") return {"gpad", SolverKind::Gpad, false};
+  throw InvalidParams("unknown solver \"" + name + "\"; expected minfbe, nama, pnama, or gpad");
+}
+inline std::vector<SolverSpec> default_solver_set() {
+  return {solver_spec_from_name("minfbe"), solver_spec_from_name("nama"), solver_spec_from_name("gpad")};
+}
+struct BatchEntry {
+  std::string id;
+  ProblemInstance prob;
+};
+struct ExperimentConfig {
+  SolverConfig solver;
+  bool include_timing = true;  ///< false zeroes wall_ms: byte-deterministic reports
+  bool reuse_factors = true;   ///< one factor per factor_hash
+};
+struct ExperimentRow {
+  std::string instance_id;
+  std::string solver;
+  int iterations = 0;
+  std::uint64_t dual_grad_calls = 0, hessian_vec_calls = 0, prox_calls = 0;
+  double final_residual_inf = std::numeric_limits<double>::infinity();
+  double wall_ms = 0.0;
+  bool converged = false;
+  bool fbe_monotone = true;
+  std::string error;
+  std::vector<double> residual_trace;
+  std::uint64_t oracle_calls() const { return dual_grad_calls + hessian_vec_calls; }
+};
+struct SolverSummary {
+  std::string solver;
+  int count = 0, converged = 0;
+  double median_calls = 0.0, p84_calls = 0.0, p95_calls = 0.0, frac_within_50 = 0.0;
+  int fbe_violations = 0;
+  double total_wall_ms = 0.0;
+};
+inline constexpr const char* kResultsCsvHeader =
+    "instance_id,solver,iterations,dual_grad_calls,hessian_vec_calls,prox_calls,final_residual_inf,wall_ms,converged";
+
+namespace detail {
+struct ExperimentDeleter { void operator()(scenopt_experiment* x) const { scenopt_experiment_destroy(x); } };
+}  // namespace detail
+
+/// RunReport (experiment.hpp:136-214). `metadata` is a JSON object text
+/// (nlohmann::json in the reference); summary_json() returns the dump(2) text.
+struct RunReport {
+  std::vector<ExperimentRow> rows;
+  std::string metadata = "{}";
+  std::shared_ptr<scenopt_experiment> native;
+
+  std::string text(int which) const {
+    size_t n = 0;
+    detail::check(scenopt_experiment_text(native.get(), which, metadata.c_str(), nullptr, 0, &n));
+    std::string out(n + 1, '\0');
+    detail::check(scenopt_experiment_text(native.get(), which, metadata.c_str(), out.data(), n + 1, &n));
+    out.resize(n);
+    return out;
+  }
+  std::string csv() const { return text(0); }
+  std::string traces_csv() const { return text(1); }
+  std::string summary_json() const {  // dump(2), no trailing newline
+    std::string t = text(2);
+    if (!t.empty() && t.back() == '\n') t.pop_back();
+    return t;
+  }
+  std::vector<SolverSummary> summaries() const {
+    std::vector<scenopt_solver_summary> raw(16);
+    const int k = detail::check(scenopt_experiment_summaries(native.get(), raw.data(), 16));
+    std::vector<SolverSummary> out;
+    for (int i = 0; i < k; ++i) {
+      const auto& s = raw[static_cast<size_t>(i)];
+      out.push_back({s.solver, s.count, s.converged, s.median_calls, s.p84_calls, s.p95_calls, s.frac_within_50,
+                     s.fbe_violations, s.total_wall_ms});
+    }
+    return out;
+  }
+};
+
+/// run_experiment (experiment.hpp:222-283): every solver on every instance, in order.
+inline RunReport run_experiment(const std::vector<BatchEntry>& instances, const std::vector<SolverSpec>& solvers,
+                                const ExperimentConfig& cfg = {}) {
+  validate_config(cfg.solver);
+  std::vector<detail::ProblemPtr> hs;
+  std::vector<const scenopt_problem*> ps;
+  std::vector<const char*> ids;
+  for (const auto& e : instances) {
+    hs.push_back(detail::to_handle(e.prob));
+    ps.push_back(hs.back().get());
+    ids.push_back(e.id.c_str());
+  }
+  std::vector<const char*> names;
+  for (const auto& s : solvers) names.push_back(s.name.c_str());
+  const scenopt_solver_config c = detail::c_config(cfg.solver);
+  scenopt_experiment* x = nullptr;
+  detail::check(scenopt_run_experiment(ps.data(), ids.data(), static_cast<int>(ps.size()), names.data(),
+                                       static_cast<int>(names.size()), &c, cfg.include_timing ? 1 : 0,
+                                       cfg.reuse_factors ? 1 : 0, 0, &x));
+  RunReport rep;
+  rep.native.reset(x, detail::ExperimentDeleter{});
+  const int k = scenopt_experiment_row_count(x);
+  for (int i = 0; i < k; ++i) {
+    scenopt_experiment_row r{};
+    detail::check(scenopt_experiment_row_get(x, i, &r));
+    ExperimentRow row;
+    row.instance_id = r.instance_id;
+    row.solver = r.solver;
+    row.iterations = r.iterations;
+    row.dual_grad_calls = r.dual_grad_calls;
+    row.hessian_vec_calls = r.hessian_vec_calls;
+    row.prox_calls = r.prox_calls;
+    row.final_residual_inf = r.final_residual_inf;
+    row.wall_ms = r.wall_ms;
+    row.converged = r.converged != 0;
+    row.fbe_monotone = r.fbe_monotone != 0;
+    row.error = r.error;
+    row.residual_trace.assign(r.residual_trace, r.residual_trace + r.trace_len);
+    rep.rows.push_back(std::move(row));
+  }
+  return rep;
 }
 
 }  // namespace scenopt

@@ -251,6 +251,78 @@ def gen_random(seed: int, nx: int, nu: int, horizon: int, branching) -> Problem:
     return Problem(h)
 
 
+class SpringMassC(C.Structure):
+    _fields_ = [
+        ("mass_kg", C.c_double), ("stiffness", C.c_double), ("damping", C.c_double),
+        ("input_bound", C.c_double), ("velocity_bound", C.c_double), ("horizon", C.c_int32),
+        ("sampling", C.c_double), ("state_weight", C.c_double), ("input_weight", C.c_double),
+        ("terminal_weight", C.c_double), ("initial_len", C.c_int32), ("transition_rows", C.c_int32),
+        ("transition_cols", C.c_int32), ("mode_values_len", C.c_int32), ("root_state_len", C.c_int32),
+        ("initial_probs", F64P), ("transition", F64P), ("mode_values", F64P), ("root_state", F64P),
+    ]
+
+
+_SM_DEFAULTS = dict(mass_kg=5.0, stiffness=1.0, damping=0.1, input_bound=2.0, velocity_bound=5.0,
+                    horizon=11, sampling=0.5, state_weight=5.0, input_weight=2.0, terminal_weight=100.0)
+
+
+def _spring_params(par):
+    """generators.hpp:49-64 from any object carrying the SpringMassParams
+    attribute names (None / missing -> defaults)."""
+    st = SpringMassC()
+    for k, v in _SM_DEFAULTS.items():
+        setattr(st, k, getattr(par, k, v) if par is not None else v)
+    keep = []
+    for name, ln in (("initial_probs", "initial_len"), ("mode_values", "mode_values_len"),
+                     ("root_state", "root_state_len")):
+        v = getattr(par, name, None) if par is not None else None
+        if v is not None:
+            a = np.ascontiguousarray(v, np.float64).ravel()
+            keep.append(a)
+            setattr(st, ln, a.size)
+            setattr(st, name, a.ctypes.data_as(F64P))
+    T = getattr(par, "transition", None) if par is not None else None
+    if T is not None:
+        T = np.ascontiguousarray(np.atleast_2d(T), np.float64)
+        keep.append(T)
+        st.transition_rows, st.transition_cols = T.shape
+        st.transition = T.ctypes.data_as(F64P)
+    return st, keep
+
+
+def gen_spring_mass(masses: int, par=None) -> Problem:
+    """generators.hpp:119-218 (series exponential for the ZOH)."""
+    st, keep = _spring_params(par)
+    h = C.c_void_p()
+    _check(lib().orc_gen_spring_mass(int(masses), C.byref(st), C.byref(h)))
+    return Problem(h)
+
+
+def spring_mass_continuous(masses: int, par=None):
+    st, keep = _spring_params(par)
+    nx, nu = 2 * masses, masses - 1
+    A, B = _buf(nx * nx), _buf(max(nx * nu, 1))
+    _check(lib().orc_spring_mass_continuous(int(masses), C.byref(st), _p(A), _p(B)))
+    return A.reshape((nx, nx), order="F"), B[:nx * nu].reshape((nx, nu), order="F")
+
+
+def expm_series(X) -> np.ndarray:
+    """test_generators.cpp:23-38."""
+    X = np.asarray(X, np.float64)
+    n = X.shape[0]
+    src = np.ascontiguousarray(X.ravel(order="F"))
+    out = _buf(n * n)
+    _check(lib().orc_expm_series(_p(src), n, _p(out)))
+    return out.reshape((n, n), order="F")
+
+
+def sample_initial_states(masses: int, par=None, seed: int = 0, count: int = 1) -> np.ndarray:
+    st, keep = _spring_params(par)
+    out = _buf(count * 2 * masses)
+    _check(lib().orc_sample_initial_states(int(masses), C.byref(st), C.c_uint64(seed), int(count), _p(out)))
+    return out.reshape(count, 2 * masses)
+
+
 @dataclass
 class InstanceOptions:
     with_box: bool = True

@@ -268,6 +268,67 @@ int orc_gen_random(uint64_t seed, int nx, int nu, int horizon, const int32_t* br
   })
 }
 
+namespace {
+SpringMassParams sm_from(const orc_spring_mass_params* c) {
+  SpringMassParams p;
+  if (!c) return p;
+  p.mass_kg = c->mass_kg;
+  p.stiffness = c->stiffness;
+  p.damping = c->damping;
+  p.input_bound = c->input_bound;
+  p.velocity_bound = c->velocity_bound;
+  p.horizon = c->horizon;
+  p.sampling = c->sampling;
+  p.state_weight = c->state_weight;
+  p.input_weight = c->input_weight;
+  p.terminal_weight = c->terminal_weight;
+  if (c->initial_len > 0) p.initial_probs.assign(c->initial_probs, c->initial_probs + c->initial_len);
+  if (c->transition_rows > 0 && c->transition_cols > 0) {
+    p.transition = Mat(c->transition_rows, c->transition_cols);
+    for (int i = 0; i < c->transition_rows; ++i)
+      for (int j = 0; j < c->transition_cols; ++j) p.transition(i, j) = c->transition[i * c->transition_cols + j];
+  }
+  if (c->mode_values_len > 0) p.mode_values.assign(c->mode_values, c->mode_values + c->mode_values_len);
+  if (c->root_state_len > 0) p.root_state.assign(c->root_state, c->root_state + c->root_state_len);
+  return p;
+}
+}  // namespace
+
+int orc_gen_spring_mass(int masses, const orc_spring_mass_params* par, orc_problem** out) {
+  ORC_GUARD({
+    auto h = std::make_unique<orc_problem>();
+    h->prob = gen_spring_mass(masses, sm_from(par));
+    *out = h.release();
+  })
+}
+int orc_expm_series(const double* X, int n, double* out) {
+  ORC_GUARD({
+    Mat M(n, n);
+    std::copy(X, X + static_cast<size_t>(n) * n, M.d.begin());
+    const Mat E = expm_series(M);
+    std::copy(E.d.begin(), E.d.end(), out);
+  })
+}
+int orc_spring_mass_continuous(int masses, const orc_spring_mass_params* par, double* A, double* B) {
+  ORC_GUARD({
+    Mat Ac, Bc;
+    spring_mass_continuous(masses, sm_from(par), Ac, Bc);
+    std::copy(Ac.d.begin(), Ac.d.end(), A);
+    std::copy(Bc.d.begin(), Bc.d.end(), B);
+  })
+}
+int orc_sample_initial_states(int masses, const orc_spring_mass_params* par, uint64_t seed, int count,
+                              double* out) {
+  ORC_GUARD({
+    std::mt19937_64 gen(seed);
+    const SpringMassParams p = sm_from(par);
+    for (int k = 0; k < count; ++k) {
+      const Vec s = sample_initial_state(masses, p, gen);
+      std::copy(s.begin(), s.end(), out + static_cast<size_t>(k) * s.size());
+    }
+  })
+}
+
 int orc_problem_validate(const orc_problem* p, char* buf, int buflen) {
   try {
     const auto bad = validate_problem(p->prob);

@@ -69,6 +69,25 @@ int orc_problem_view_get(orc_problem* p, orc_problem_view* v, int32_t* dual_dim)
 void orc_problem_free(orc_problem* p);
 int orc_gen_random(uint64_t seed, int nx, int nu, int horizon, const int32_t* branching, int nbr,
                    orc_problem** out);
+/* generators.hpp:39-234 (spring-mass benchmark). Arrays of length 0 take the defaults;
+ * transition is row-major [transition_rows x transition_cols]. */
+typedef struct orc_spring_mass_params {
+  double mass_kg, stiffness, damping, input_bound, velocity_bound;
+  int32_t horizon;
+  double sampling, state_weight, input_weight, terminal_weight;
+  int32_t initial_len, transition_rows, transition_cols, mode_values_len, root_state_len;
+  const double* initial_probs;
+  const double* transition;
+  const double* mode_values;
+  const double* root_state;
+} orc_spring_mass_params;
+int orc_gen_spring_mass(int masses, const orc_spring_mass_params* par, orc_problem** out);
+/* series exponential (test_generators.cpp:23-38), column-major n x n */
+int orc_expm_series(const double* X, int n, double* out);
+int orc_spring_mass_continuous(int masses, const orc_spring_mass_params* par, double* A, double* B);
+/* `count` consecutive sample_initial_state draws from mt19937_64(seed) */
+int orc_sample_initial_states(int masses, const orc_spring_mass_params* par, uint64_t seed, int count,
+                              double* out);
 int orc_problem_validate(const orc_problem* p, char* buf, int buflen);
 int orc_problem_layout(const orc_problem* p, int32_t* dual_offset, int32_t* tdual_offset);
 int orc_precondition(const orc_problem* p, orc_problem** out);

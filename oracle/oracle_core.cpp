@@ -1603,6 +1603,166 @@ ProblemInstance gen_random_instance(std::uint64_t seed, int nx, int nu, int hori
   return prob;
 }
 
+// ============================================================ spring-mass
+// generators.hpp:66-91: d/dt [p; v] = [[0, I], [-(k/m) T, -(b/m) T]] [p; v] + [[0], [D/m]] u
+// with T the tridiagonal (2, -1) coupling and D the signed actuator incidence.
+void spring_mass_continuous(int masses, const SpringMassParams& par, Mat& A, Mat& B) {
+  const int n = masses;
+  Mat T(n, n), D(n, n - 1);
+  for (int j = 0; j < n; ++j) {
+    T(j, j) = 2.0;
+    if (j > 0) T(j, j - 1) = -1.0;
+    if (j + 1 < n) T(j, j + 1) = -1.0;
+  }
+  for (int a = 0; a + 1 < n; ++a) {
+    D(a, a) = -1.0;
+    D(a + 1, a) = 1.0;
+  }
+  A = Mat(2 * n, 2 * n);
+  for (int j = 0; j < n; ++j) A(j, n + j) = 1.0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      A(n + i, j) = -(par.stiffness / par.mass_kg) * T(i, j);
+      A(n + i, n + j) = -(par.damping / par.mass_kg) * T(i, j);
+    }
+  B = Mat(2 * n, n - 1);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j + 1 < n; ++j) B(n + i, j) = D(i, j) / par.mass_kg;
+}
+
+namespace {
+double fro(const Mat& X) {
+  double s = 0.0;
+  for (double v : X.d) s += v * v;
+  return std::sqrt(s);
+}
+}  // namespace
+
+// test_generators.cpp:23-38: halve into ||X||_F <= 0.25, sum the series to
+// 1e-20 relative (at most 60 terms), square back.
+Mat expm_series(Mat X) {
+  int squarings = 0;
+  while (fro(X) > 0.25) {
+    for (double& v : X.d) v *= 0.5;
+    ++squarings;
+  }
+  Mat sum = Mat::identity(X.r);
+  Mat term = sum;
+  for (int k = 1; k <= 60; ++k) {
+    term = matmul(term, X);
+    for (double& v : term.d) v /= static_cast<double>(k);
+    for (size_t t = 0; t < sum.d.size(); ++t) sum.d[t] += term.d[t];
+    if (fro(term) <= 1e-20 * fro(sum)) break;
+  }
+  for (int s = 0; s < squarings; ++s) sum = matmul(sum, sum);
+  return sum;
+}
+
+// generators.hpp:97-112: exp([[A, B], [0, 0]] period) holds A_d | B_d in its top rows.
+void discretize_zoh(const Mat& A, const Mat& B, double period, Mat& Ad, Mat& Bd) {
+  if (A.r != A.c || B.r != A.r) ORC_THROW(kDimensionMismatch, "discretize_zoh: A must be square and match B");
+  if (!(period > 0.0)) ORC_THROW(kInvalidParams, "discretize_zoh: period must be > 0");
+  const int n = A.r, m = B.c;
+  Mat aug(n + m, n + m);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) aug(i, j) = A(i, j) * period;
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < n; ++i) aug(i, n + j) = B(i, j) * period;
+  const Mat big = expm_series(aug);
+  Ad = Mat(n, n);
+  Bd = Mat(n, m);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) Ad(i, j) = big(i, j);
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < n; ++i) Bd(i, j) = big(i, n + j);
+}
+
+// generators.hpp:119-218
+ProblemInstance gen_spring_mass(int masses, const SpringMassParams& params) {
+  if (masses < 2) ORC_THROW(kInvalidParams, "gen_spring_mass: masses must be >= 2");
+  if (!(params.mass_kg > 0.0)) ORC_THROW(kInvalidParams, "gen_spring_mass: mass_kg must be > 0");
+  if (!(params.input_bound > 0.0) || !(params.velocity_bound > 0.0))
+    ORC_THROW(kInvalidParams, "gen_spring_mass: bounds must be > 0");
+  if (!(params.input_weight > 0.0) || !(params.terminal_weight > 0.0))
+    ORC_THROW(kInvalidParams, "gen_spring_mass: input and terminal weights must be > 0");
+  if (params.state_weight < 0.0) ORC_THROW(kInvalidParams, "gen_spring_mass: state_weight must be >= 0");
+  SpringMassParams par = params;
+  if (par.initial_probs.empty()) par.initial_probs = {0.5, 0.5};
+  if (par.transition.d.empty()) {
+    par.transition = Mat(2, 2);
+    par.transition(0, 0) = 0.1;
+    par.transition(0, 1) = 0.9;
+    par.transition(1, 0) = 0.9;
+    par.transition(1, 1) = 0.1;
+  }
+  if (par.mode_values.empty()) {
+    par.mode_values.assign(par.initial_probs.size(), 0.0);
+    if (par.mode_values.size() > 1) par.mode_values[1] = 0.1;
+  }
+  if (par.mode_values.size() != par.initial_probs.size())
+    ORC_THROW(kDimensionMismatch, "gen_spring_mass: one mode value per Markov mode required");
+  const int nx = 2 * masses, nu = masses - 1;
+  Mat Ac, Bc, Ad, Bd;
+  spring_mass_continuous(masses, par, Ac, Bc);
+  discretize_zoh(Ac, Bc, par.sampling, Ad, Bd);
+  ProblemInstance prob;
+  prob.tree = build_from_markov(par.transition, par.initial_probs, par.horizon);
+  prob.nx = nx;
+  prob.nu = nu;
+  prob.root_state = par.root_state.empty() ? Vec(static_cast<size_t>(nx), 0.0) : par.root_state;
+  if (static_cast<int>(prob.root_state.size()) != nx)
+    ORC_THROW(kDimensionMismatch, "gen_spring_mass: root_state must have length 2M");
+  const int rows = masses + nu;
+  NodeCost cost{Mat(nx, nx), Mat(nu, nu), Mat(nu, nx), Vec(static_cast<size_t>(nx), 0.0),
+                Vec(static_cast<size_t>(nu), 0.0)};
+  for (int i = 0; i < nx; ++i) cost.Q(i, i) = par.state_weight;
+  for (int i = 0; i < nu; ++i) cost.R(i, i) = par.input_weight;
+  ConstraintBlock con{Mat(rows, nx), Mat(rows, nu), NonsmoothSpec{}};
+  for (int k = 0; k < masses; ++k) con.F(k, masses + k) = 1.0;  // velocity rows
+  for (int k = 0; k < nu; ++k) con.G(masses + k, k) = 1.0;      // input rows
+  con.g.kind = NonsmoothKind::Box;
+  con.g.zmin.assign(static_cast<size_t>(rows), 0.0);
+  for (int k = 0; k < rows; ++k) con.g.zmin[static_cast<size_t>(k)] = k < masses ? -par.velocity_bound : -par.input_bound;
+  con.g.zmax.resize(static_cast<size_t>(rows));
+  for (int k = 0; k < rows; ++k) con.g.zmax[static_cast<size_t>(k)] = -con.g.zmin[static_cast<size_t>(k)];
+  const int n = prob.num_nodes();
+  prob.dyn.resize(static_cast<size_t>(n));
+  prob.cost.resize(static_cast<size_t>(n));
+  prob.con.resize(static_cast<size_t>(n));
+  prob.dyn[0] = NodeDynamics{Mat(nx, nx), Mat(nx, nu), Vec(static_cast<size_t>(nx), 0.0)};
+  prob.cost[0] = NodeCost{Mat(nx, nx), Mat(nu, nu), Mat(nu, nx), Vec(static_cast<size_t>(nx), 0.0),
+                          Vec(static_cast<size_t>(nu), 0.0)};
+  prob.con[0] = ConstraintBlock{Mat(0, nx), Mat(0, nu), NonsmoothSpec{}};
+  for (int i = 1; i < n; ++i) {
+    const auto si = static_cast<size_t>(i);
+    prob.dyn[si] = NodeDynamics{Ad, Bd, Vec(static_cast<size_t>(nx), par.mode_values[static_cast<size_t>(prob.tree.mode[si])])};
+    prob.cost[si] = cost;
+    prob.con[si] = con;
+  }
+  const int leaves = prob.tree.num_leaves();
+  TerminalCost tc{Mat(nx, nx), Vec(static_cast<size_t>(nx), 0.0)};
+  for (int i = 0; i < nx; ++i) tc.P(i, i) = par.terminal_weight;
+  TerminalBlock tb{Mat(masses, nx), NonsmoothSpec{}};
+  for (int k = 0; k < masses; ++k) tb.F(k, masses + k) = 1.0;
+  tb.g.kind = NonsmoothKind::Box;
+  tb.g.zmin.assign(static_cast<size_t>(masses), -par.velocity_bound);
+  tb.g.zmax.assign(static_cast<size_t>(masses), par.velocity_bound);
+  prob.tcost.assign(static_cast<size_t>(leaves), tc);
+  prob.tcon.assign(static_cast<size_t>(leaves), tb);
+  prob.finalize_layout();
+  return prob;
+}
+
+// generators.hpp:223-234: positions in +-velocity_bound, velocities in +-velocity_bound / 2
+Vec sample_initial_state(int masses, const SpringMassParams& params, std::mt19937_64& gen) {
+  if (masses < 2) ORC_THROW(kInvalidParams, "sample_initial_state: masses must be >= 2");
+  const double half = 0.5 * params.velocity_bound, pos_box = params.velocity_bound;
+  Vec state(static_cast<size_t>(2 * masses));
+  for (int i = 0; i < masses; ++i) state[static_cast<size_t>(i)] = pos_box * (2.0 * unit_draw(gen) - 1.0);
+  for (int i = masses; i < 2 * masses; ++i) state[static_cast<size_t>(i)] = half * (2.0 * unit_draw(gen) - 1.0);
+  return state;
+}
+
 // ============================================================ test support
 // tests/support.hpp:33-43 (column-major draws)
 Mat Rng::matrix(int rows, int cols, double scale) {

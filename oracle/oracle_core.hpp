@@ -339,6 +339,25 @@ SolverReport solve(const ProblemInstance& prob, const SolverConfig& cfg, SolverK
 ProblemInstance gen_random_instance(std::uint64_t seed, int nx, int nu, int horizon,
                                     const std::vector<int>& branching);
 
+// generators.hpp:39-234: spring-mass-damper array benchmark. Empty vectors take
+// the reference defaults (generators.hpp:149-162).
+struct SpringMassParams {
+  double mass_kg = 5.0, stiffness = 1.0, damping = 0.1, input_bound = 2.0, velocity_bound = 5.0;
+  int horizon = 11;
+  double sampling = 0.5, state_weight = 5.0, input_weight = 2.0, terminal_weight = 100.0;
+  Vec initial_probs;
+  Mat transition;
+  Vec mode_values;
+  Vec root_state;
+};
+void spring_mass_continuous(int masses, const SpringMassParams& par, Mat& A, Mat& B);
+// matrix exponential by the series oracle of test_generators.cpp:23-38
+// (scaling and squaring around a Taylor sum), independent of the product's Pade
+Mat expm_series(Mat X);
+void discretize_zoh(const Mat& A, const Mat& B, double period, Mat& Ad, Mat& Bd);
+ProblemInstance gen_spring_mass(int masses, const SpringMassParams& params);
+Vec sample_initial_state(int masses, const SpringMassParams& params, std::mt19937_64& gen);
+
 // ---------------------------------------------------------------- test support
 // tests/support.hpp:24-209
 struct Rng {

@@ -6,7 +6,8 @@ CUDA library ``lib/libscenopt_b200.so`` (include/scenopt_b200.h).
 """
 from ._native import (  # noqa: F401
     CacheMismatch, CudaError, DimensionMismatch, Error, InfiniteConjugate, InvalidParams,
-    LineSearchStalled, NoDevice, NotStronglyConvex, ShapeChanged, StepUnderflow,
+    LineSearchStalled, NoDevice, NonStochasticMatrix, NotStronglyConvex, ParseError, ShapeChanged,
+    StageOutOfRange, StepUnderflow, UnsupportedSpec,
     ZeroProbability, build, lib,
 )
 from .api import *  # noqa: F401,F403

@@ -73,6 +73,36 @@ class DevInfoC(C.Structure):
     ]
 
 
+class ExperimentRowC(C.Structure):
+    _fields_ = [
+        ("instance_id", C.c_char_p), ("solver", C.c_char_p), ("error", C.c_char_p),
+        ("iterations", C.c_int32), ("dual_grad_calls", C.c_uint64), ("hessian_vec_calls", C.c_uint64),
+        ("prox_calls", C.c_uint64), ("final_residual_inf", C.c_double), ("wall_ms", C.c_double),
+        ("converged", C.c_int32), ("fbe_monotone", C.c_int32), ("trace_len", C.c_int32),
+        ("residual_trace", F64P),
+    ]
+
+
+class SolverSummaryC(C.Structure):
+    _fields_ = [
+        ("solver", C.c_char * 16), ("count", C.c_int32), ("converged", C.c_int32),
+        ("fbe_violations", C.c_int32), ("median_calls", C.c_double), ("p84_calls", C.c_double),
+        ("p95_calls", C.c_double), ("frac_within_50", C.c_double), ("total_wall_ms", C.c_double),
+    ]
+
+
+class SpringMassC(C.Structure):
+    """scenopt_spring_mass_params (generators.hpp:49-64)."""
+    _fields_ = [
+        ("mass_kg", C.c_double), ("stiffness", C.c_double), ("damping", C.c_double),
+        ("input_bound", C.c_double), ("velocity_bound", C.c_double), ("horizon", C.c_int32),
+        ("sampling", C.c_double), ("state_weight", C.c_double), ("input_weight", C.c_double),
+        ("terminal_weight", C.c_double), ("initial_len", C.c_int32), ("transition_rows", C.c_int32),
+        ("transition_cols", C.c_int32), ("mode_values_len", C.c_int32), ("root_state_len", C.c_int32),
+        ("initial_probs", F64P), ("transition", F64P), ("mode_values", F64P), ("root_state", F64P),
+    ]
+
+
 # errors.hpp:9-80 -> Python exception types with the reference's names.
 class Error(RuntimeError):
     code = -1

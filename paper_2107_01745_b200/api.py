@@ -18,6 +18,10 @@ from . import _native as N
 __all__ = [
     # problem_data.hpp / generators.hpp / solvers.hpp:569-623
     "PrimalPoint", "ProblemInstance", "gen_random_instance", "precondition",
+    "serialize_problem", "parse_problem", "save_problem", "load_problem", "validate_problem_text",
+    "problem_to_json", "problem_from_json", "content_hash", "factor_hash", "PROBLEM_SCHEMA",
+    "SpringMassParams", "gen_spring_mass", "spring_mass_continuous", "discretize_zoh", "expm",
+    "sample_initial_state",
     # riccati.hpp (+ device factor, subtree sharding)
     "FactorCache", "DeviceFactorCache", "factor", "factor_device", "refactor_affine", "nccl_unique_id",
     # tree_oracles.hpp
@@ -28,6 +32,9 @@ __all__ = [
     # solvers.hpp
     "SolverConfig", "SolverReport", "estimate_dual_lipschitz", "solve_minfbe", "solve_nama", "solve_gpad",
     "warm_start", "solve", "verify_report",
+    # experiment.hpp
+    "SolverSpec", "solver_spec_from_name", "default_solver_set", "BatchEntry", "ExperimentRow",
+    "SolverSummary", "RunReport", "run_experiment", "RESULTS_CSV_HEADER",
 ]
 from ._native import InvalidParams, check, dptr, iptr
 
@@ -89,6 +96,16 @@ class ProblemInstance:
     def num_nodes(self) -> int:
         return self._n
 
+    def mode(self) -> np.ndarray:
+        """ScenarioTree::mode (scenario_tree.hpp:41); empty when unknown."""
+        out = np.zeros(self._n, np.int32)
+        k = check(N.lib().scenopt_problem_get_mode(self._h, iptr(out), self._n))
+        return out[:k]
+
+    def set_mode(self, mode) -> None:
+        m = np.ascontiguousarray(mode, np.int32)
+        check(N.lib().scenopt_problem_set_mode(self._h, iptr(m) if m.size else None, m.size))
+
     def primal_dim(self) -> int:
         return self._primal_dim
 
@@ -142,6 +159,176 @@ def gen_random_instance(seed: int, nx: int = 3, nu: int = 2, horizon: int = 3,
     check(N.lib().scenopt_problem_gen_random(C.c_uint64(seed), nx, nu, horizon, iptr(b), len(b),
                                              C.byref(h)))
     return ProblemInstance(h)
+
+
+# ---------------------------------------------------------------- problem files
+PROBLEM_SCHEMA = "scenopt-problem-v1"  # problem_io.hpp:27
+
+
+def serialize_problem(prob: ProblemInstance) -> str:
+    """problem_io.hpp:480: canonical JSON text (sorted keys, 2-space indent)."""
+    n = C.c_size_t()
+    check(N.lib().scenopt_problem_serialize(prob._h, None, C.c_size_t(0), C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(N.lib().scenopt_problem_serialize(prob._h, buf, C.c_size_t(n.value + 1), C.byref(n)))
+    return buf.raw[:n.value].decode()
+
+
+def parse_problem(text: str) -> ProblemInstance:
+    """problem_io.hpp:484 (ParseError on malformed or invalid documents)."""
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    check(N.lib().scenopt_problem_parse(raw, C.c_size_t(len(raw)), C.byref(h)))
+    return ProblemInstance(h)
+
+
+def save_problem(prob: ProblemInstance, path: str) -> None:
+    check(N.lib().scenopt_problem_save(prob._h, str(path).encode()))
+
+
+def load_problem(path: str) -> ProblemInstance:
+    h = C.c_void_p()
+    check(N.lib().scenopt_problem_load(str(path).encode(), C.byref(h)))
+    return ProblemInstance(h)
+
+
+def validate_problem_text(text: str) -> list:
+    """problem_io.hpp:512-524: violation lines; empty when the document parses and validates."""
+    raw = text.encode() if isinstance(text, str) else bytes(text)
+    buf = C.create_string_buffer(1 << 16)
+    k = check(N.lib().scenopt_problem_validate_text(raw, C.c_size_t(len(raw)), buf, len(buf)))
+    return [ln for ln in buf.value.decode().split("\n") if ln][:k] if k else []
+
+
+def problem_to_json(prob: ProblemInstance) -> dict:
+    """problem_io.hpp:220 as a Python dict (the parsed canonical text)."""
+    import json
+    return json.loads(serialize_problem(prob))
+
+
+def problem_from_json(doc: dict) -> ProblemInstance:
+    """problem_io.hpp:323 from a Python dict."""
+    import json
+    return parse_problem(json.dumps(doc))
+
+
+def content_hash(prob: ProblemInstance) -> int:
+    """problem_io.hpp:539: FNV-1a of the canonical serialization."""
+    h = C.c_uint64()
+    check(N.lib().scenopt_problem_hashes(prob._h, C.byref(h), None))
+    return h.value
+
+
+def factor_hash(prob: ProblemInstance) -> int:
+    """problem_io.hpp:546: FNV-1a of the factor-determining content (no root
+    state, modes or nonsmooth specs)."""
+    h = C.c_uint64()
+    check(N.lib().scenopt_problem_hashes(prob._h, None, C.byref(h)))
+    return h.value
+
+
+@dataclass
+class SpringMassParams:
+    """generators.hpp:49-64; None arrays take the reference defaults
+    (initial (0.5, 0.5), transition [[0.1, 0.9], [0.9, 0.1]], mode values
+    (0, 0.1), zero root state)."""
+    mass_kg: float = 5.0
+    stiffness: float = 1.0
+    damping: float = 0.1
+    input_bound: float = 2.0
+    velocity_bound: float = 5.0
+    horizon: int = 11
+    sampling: float = 0.5
+    state_weight: float = 5.0
+    input_weight: float = 2.0
+    terminal_weight: float = 100.0
+    initial_probs: np.ndarray | None = None
+    transition: np.ndarray | None = None
+    mode_values: np.ndarray | None = None
+    root_state: np.ndarray | None = None
+
+    def c(self, cls=None):
+        """(struct, keep-alive arrays) for the C-ABI (or an identical layout `cls`)."""
+        cls = cls or N.SpringMassC
+        st = cls()
+        for k in ("mass_kg", "stiffness", "damping", "input_bound", "velocity_bound", "horizon",
+                  "sampling", "state_weight", "input_weight", "terminal_weight"):
+            setattr(st, k, getattr(self, k))
+        keep = []
+        for name, ln in (("initial_probs", "initial_len"), ("mode_values", "mode_values_len"),
+                         ("root_state", "root_state_len")):
+            v = getattr(self, name)
+            if v is not None:
+                a = np.ascontiguousarray(v, np.float64).ravel()
+                keep.append(a)
+                setattr(st, ln, a.size)
+                setattr(st, name, a.ctypes.data_as(N.F64P))
+        if self.transition is not None:
+            T = np.ascontiguousarray(np.atleast_2d(self.transition), np.float64)  # row-major
+            keep.append(T)
+            st.transition_rows, st.transition_cols = T.shape
+            st.transition = T.ctypes.data_as(N.F64P)
+        return st, keep
+
+
+def gen_spring_mass(masses: int, params: SpringMassParams | None = None) -> ProblemInstance:
+    """generators.hpp:119-218: ZOH-discretized spring-mass-damper array
+    (nx = 2M, nu = M-1) on the Markov mode tree, box constraints on every
+    velocity and input."""
+    st, keep = (params or SpringMassParams()).c()
+    h = C.c_void_p()
+    check(N.lib().scenopt_problem_gen_spring_mass(int(masses), C.byref(st), C.byref(h)))
+    return ProblemInstance(h)
+
+
+def _colmajor(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, np.float64).ravel(order="F"))
+
+
+def spring_mass_continuous(masses: int, params: SpringMassParams | None = None):
+    """detail::spring_mass_continuous, generators.hpp:70-91 -> (A, B)."""
+    st, keep = (params or SpringMassParams()).c()
+    nx, nu = 2 * masses, max(masses - 1, 0)
+    A, B = np.zeros(nx * nx), np.zeros(max(nx * nu, 1))
+    check(N.lib().scenopt_spring_mass_continuous(int(masses), C.byref(st), dptr(A), dptr(B)))
+    return A.reshape((nx, nx), order="F"), B[:nx * nu].reshape((nx, nu), order="F")
+
+
+def expm(X) -> np.ndarray:
+    """Matrix exponential (Pade scaling and squaring, the method of Eigen's exp())."""
+    X = np.asarray(X, np.float64)
+    if X.ndim != 2 or X.shape[0] != X.shape[1]:
+        raise N.DimensionMismatch("expm: matrix must be square")
+    n = X.shape[0]
+    out = np.zeros(n * n)
+    check(N.lib().scenopt_expm(dptr(_colmajor(X)), n, dptr(out)))
+    return out.reshape((n, n), order="F")
+
+
+def discretize_zoh(A, B, period: float):
+    """generators.hpp:97-112 -> (Ad, Bd)."""
+    A = np.atleast_2d(np.asarray(A, np.float64))
+    B = np.asarray(B, np.float64)
+    if B.ndim == 1:
+        B = B.reshape(-1, 1)
+    if A.shape[0] != A.shape[1] or B.shape[0] != A.shape[0]:
+        raise N.DimensionMismatch("discretize_zoh: A must be square and match B")
+    n, m = A.shape[0], B.shape[1]
+    Ad, Bd = np.zeros(n * n), np.zeros(max(n * m, 1))
+    check(N.lib().scenopt_discretize_zoh(dptr(_colmajor(A)), dptr(_colmajor(B) if m else np.zeros(1)), n, m,
+                                         C.c_double(period), dptr(Ad), dptr(Bd)))
+    return Ad.reshape((n, n), order="F"), Bd[:n * m].reshape((n, m), order="F")
+
+
+def sample_initial_state(masses: int, params: SpringMassParams | None = None, seed: int = 0,
+                         count: int = 1) -> np.ndarray:
+    """generators.hpp:223-234: `count` consecutive draws from
+    std::mt19937_64(seed); shape (count, 2M)."""
+    st, keep = (params or SpringMassParams()).c()
+    out = np.zeros((count, 2 * masses))
+    check(N.lib().scenopt_sample_initial_states(int(masses), C.byref(st), C.c_uint64(seed), int(count),
+                                                dptr(out)))
+    return out
 
 
 def precondition(prob: ProblemInstance) -> ProblemInstance:
@@ -689,3 +876,137 @@ def verify_report(prob: ProblemInstance, rep: SolverReport, z_override=None, dev
     if zo is not None:
         rep.z = zo.copy()
     return rep
+
+
+# ---------------------------------------------------------------- experiment.hpp
+RESULTS_CSV_HEADER = ("instance_id,solver,iterations,dual_grad_calls,hessian_vec_calls,"
+                      "prox_calls,final_residual_inf,wall_ms,converged")  # experiment.hpp:133-135
+
+
+@dataclass
+class SolverSpec:
+    """experiment.hpp:26-30; p-NAMA is NAMA with the parallel line search."""
+    name: str
+    kind: str = "nama"
+    parallel_linesearch: bool = False
+
+
+def solver_spec_from_name(name: str) -> SolverSpec:
+    """experiment.hpp:32-40."""
+    table = {"minfbe": SolverSpec("minfbe", "minfbe"), "nama": SolverSpec("nama", "nama"),
+             "pnama": SolverSpec("pnama", "nama", True), "gpad": SolverSpec("gpad", "gpad")}
+    if name not in table:
+        raise InvalidParams(f'unknown solver "{name}"; expected minfbe, nama, pnama, or gpad')
+    return table[name]
+
+
+def default_solver_set() -> list:
+    return [solver_spec_from_name(n) for n in ("minfbe", "nama", "gpad")]
+
+
+@dataclass
+class BatchEntry:
+    id: str
+    prob: ProblemInstance
+
+
+@dataclass
+class ExperimentRow:
+    """experiment.hpp:63-80."""
+    instance_id: str
+    solver: str
+    iterations: int
+    dual_grad_calls: int
+    hessian_vec_calls: int
+    prox_calls: int
+    final_residual_inf: float
+    wall_ms: float
+    converged: bool
+    fbe_monotone: bool
+    error: str
+    residual_trace: np.ndarray
+
+    def oracle_calls(self) -> int:
+        return self.dual_grad_calls + self.hessian_vec_calls
+
+
+@dataclass
+class SolverSummary:
+    """experiment.hpp:86-96."""
+    solver: str
+    count: int
+    converged: int
+    median_calls: float
+    p84_calls: float
+    p95_calls: float
+    frac_within_50: float
+    fbe_violations: int
+    total_wall_ms: float
+
+
+class RunReport:
+    """experiment.hpp:136-214 (rendered by the native library)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self.metadata: dict = {}
+        self.rows = []
+        k = N.lib().scenopt_experiment_row_count(handle)
+        r = N.ExperimentRowC()
+        for i in range(k):
+            check(N.lib().scenopt_experiment_row_get(handle, i, C.byref(r)))
+            tr = (np.ctypeslib.as_array(r.residual_trace, shape=(r.trace_len,)).copy()
+                  if r.trace_len else np.zeros(0))
+            self.rows.append(ExperimentRow(r.instance_id.decode(), r.solver.decode(), r.iterations,
+                                           r.dual_grad_calls, r.hessian_vec_calls, r.prox_calls,
+                                           r.final_residual_inf, r.wall_ms, bool(r.converged),
+                                           bool(r.fbe_monotone), r.error.decode(), tr))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and N._lib is not None:
+            N._lib.scenopt_experiment_destroy(self._h)
+            self._h = None
+
+    def _text(self, which: int, meta=None) -> str:
+        import json
+        m = json.dumps(meta).encode() if meta is not None else None
+        n = C.c_size_t()
+        check(N.lib().scenopt_experiment_text(self._h, which, m, None, C.c_size_t(0), C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(N.lib().scenopt_experiment_text(self._h, which, m, buf, C.c_size_t(n.value + 1), C.byref(n)))
+        return buf.raw[:n.value].decode()
+
+    def csv(self) -> str:
+        return self._text(0)
+
+    def traces_csv(self) -> str:
+        return self._text(1)
+
+    def summary_json(self) -> str:
+        """summary_json().dump(2) + "\\n" (the report file's text)."""
+        return self._text(2, self.metadata)
+
+    def summaries(self) -> list:
+        out = (N.SolverSummaryC * 16)()
+        k = check(N.lib().scenopt_experiment_summaries(self._h, out, 16))
+        return [SolverSummary(s.solver.decode(), s.count, s.converged, s.median_calls, s.p84_calls,
+                              s.p95_calls, s.frac_within_50, s.fbe_violations, s.total_wall_ms)
+                for s in out[:k]]
+
+
+def run_experiment(instances, solvers=None, solver: SolverConfig | None = None,
+                   include_timing: bool = True, reuse_factors: bool = True, device: int = 0) -> RunReport:
+    """experiment.hpp:222-283: every solver on every instance, in order.
+    `instances` are BatchEntry or (id, ProblemInstance) pairs; `solvers` are
+    SolverSpec or names (default: minfbe, nama, gpad)."""
+    entries = [e if isinstance(e, BatchEntry) else BatchEntry(*e) for e in instances]
+    specs = default_solver_set() if solvers is None else [
+        s if isinstance(s, SolverSpec) else solver_spec_from_name(s) for s in solvers]
+    probs = (C.c_void_p * max(len(entries), 1))(*[e.prob._h for e in entries])
+    ids = (C.c_char_p * max(len(entries), 1))(*[e.id.encode() for e in entries])
+    names = (C.c_char_p * max(len(specs), 1))(*[s.name.encode() for s in specs])
+    c = (solver or SolverConfig()).c()
+    h = C.c_void_p()
+    check(N.lib().scenopt_run_experiment(probs, ids, len(entries), names, len(specs), C.byref(c),
+                                         int(include_timing), int(reuse_factors), device, C.byref(h)))
+    return RunReport(h)

@@ -4,9 +4,11 @@
 // message for scenopt_last_error().
 #include <cstring>
 #include <memory>
+#include <random>
 #include <string>
 
 #include "capi_internal.hpp"
+#include "problem_io.hpp"
 
 using namespace scn;
 
@@ -38,6 +40,98 @@ int scenopt_problem_gen_random(uint64_t seed, int nx, int nu, int horizon, const
     auto h = std::make_unique<scenopt_problem>();
     h->p = gen_random(seed, nx, nu, horizon, br);
     *out = h.release();
+  });
+}
+
+namespace {
+SpringMass spring_from(const scenopt_spring_mass_params* c) {
+  SpringMass p;
+  if (!c) return p;
+  p.mass_kg = c->mass_kg;
+  p.stiffness = c->stiffness;
+  p.damping = c->damping;
+  p.input_bound = c->input_bound;
+  p.velocity_bound = c->velocity_bound;
+  p.horizon = c->horizon;
+  p.sampling = c->sampling;
+  p.state_weight = c->state_weight;
+  p.input_weight = c->input_weight;
+  p.terminal_weight = c->terminal_weight;
+  if (c->initial_len > 0) p.initial_probs.assign(c->initial_probs, c->initial_probs + c->initial_len);
+  if (c->transition_rows > 0 && c->transition_cols > 0) {
+    p.transition.assign(c->transition, c->transition + static_cast<size_t>(c->transition_rows) * c->transition_cols);
+    p.transition_rows = c->transition_rows;
+    p.transition_cols = c->transition_cols;
+  }
+  if (c->mode_values_len > 0) p.mode_values.assign(c->mode_values, c->mode_values + c->mode_values_len);
+  if (c->root_state_len > 0) p.root_state.assign(c->root_state, c->root_state + c->root_state_len);
+  return p;
+}
+}  // namespace
+
+void scenopt_spring_mass_defaults(scenopt_spring_mass_params* par) {
+  if (!par) return;
+  const SpringMass d;
+  *par = scenopt_spring_mass_params{};
+  par->mass_kg = d.mass_kg;
+  par->stiffness = d.stiffness;
+  par->damping = d.damping;
+  par->input_bound = d.input_bound;
+  par->velocity_bound = d.velocity_bound;
+  par->horizon = d.horizon;
+  par->sampling = d.sampling;
+  par->state_weight = d.state_weight;
+  par->input_weight = d.input_weight;
+  par->terminal_weight = d.terminal_weight;
+}
+
+int scenopt_problem_gen_spring_mass(int masses, const scenopt_spring_mass_params* par, scenopt_problem** out) {
+  SCN_GUARD({
+    if (!out) fail(SCENOPT_E_INVALID_PARAMS, "gen_spring_mass: null output");
+    auto h = std::make_unique<scenopt_problem>();
+    h->p = gen_spring_mass(masses, spring_from(par));
+    *out = h.release();
+  });
+}
+
+int scenopt_spring_mass_continuous(int masses, const scenopt_spring_mass_params* par, double* A, double* B) {
+  SCN_GUARD({
+    if (masses < 2) fail(SCENOPT_E_INVALID_PARAMS, "spring_mass_continuous: masses must be >= 2");
+    std::vector<double> a, b;
+    spring_mass_continuous(masses, spring_from(par), a, b);
+    std::copy(a.begin(), a.end(), A);
+    std::copy(b.begin(), b.end(), B);
+  });
+}
+
+int scenopt_discretize_zoh(const double* A, const double* B, int n, int m, double period, double* Ad, double* Bd) {
+  SCN_GUARD({
+    if (n < 1 || m < 0) fail(SCENOPT_E_DIMENSION_MISMATCH, "discretize_zoh: A must be square and match B");
+    discretize_zoh(A, B, n, m, period, Ad, Bd);
+  });
+}
+
+int scenopt_expm(const double* X, int n, double* out) {
+  SCN_GUARD({
+    if (n < 1) fail(SCENOPT_E_DIMENSION_MISMATCH, "expm: matrix must be square and non-empty");
+    const std::vector<double> E = expm(std::vector<double>(X, X + static_cast<size_t>(n) * n), n);
+    std::copy(E.begin(), E.end(), out);
+  });
+}
+
+int scenopt_sample_initial_states(int masses, const scenopt_spring_mass_params* par, uint64_t seed, int count,
+                                  double* out) {
+  SCN_GUARD({
+    if (masses < 2) fail(SCENOPT_E_INVALID_PARAMS, "sample_initial_state: masses must be >= 2");
+    const SpringMass p = spring_from(par);
+    const double half = 0.5 * p.velocity_bound, pos_box = 1.0 * p.velocity_bound;
+    std::mt19937_64 gen(seed);
+    auto sym = [&gen]() { return 2.0 * (static_cast<double>(gen() >> 11) * 0x1.0p-53) - 1.0; };
+    for (int k = 0; k < count; ++k) {
+      double* s = out + static_cast<size_t>(k) * 2 * masses;
+      for (int i = 0; i < masses; ++i) s[i] = pos_box * sym();
+      for (int i = masses; i < 2 * masses; ++i) s[i] = half * sym();
+    }
   });
 }
 
@@ -344,3 +438,95 @@ int scenopt_debug_items(scenopt_dev* h, int32_t* out, int cap) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- problem files (problem_io.hpp)
+namespace {
+int copy_out(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap > 0) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return 0;
+}
+}  // namespace
+
+int scenopt_problem_serialize(scenopt_problem* p, char* buf, size_t cap, size_t* len) {
+  SCN_GUARD({
+    if (!p) fail(SCENOPT_E_INVALID_PARAMS, "serialize_problem: null problem");
+    if (!buf || p->text.empty()) p->text = serialize_problem(p->p);
+    copy_out(p->text, buf, cap, len);
+    if (buf) std::string().swap(p->text);
+  });
+}
+
+int scenopt_problem_parse(const char* text, size_t len, scenopt_problem** out) {
+  SCN_GUARD({
+    if (!text || !out) fail(SCENOPT_E_INVALID_PARAMS, "parse_problem: null argument");
+    auto h = std::make_unique<scenopt_problem>();
+    h->p = parse_problem(std::string(text, len));
+    *out = h.release();
+  });
+}
+
+int scenopt_problem_validate_text(const char* text, size_t len, char* buf, int buflen) {
+  try {
+    const auto bad = validate_problem_text(std::string(text ? text : "", text ? len : 0));
+    std::string all;
+    for (const auto& b : bad) all += b + "\n";
+    if (buf && buflen > 0) {
+      std::strncpy(buf, all.c_str(), static_cast<size_t>(buflen) - 1);
+      buf[buflen - 1] = 0;
+    }
+    return static_cast<int>(bad.size());
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SCENOPT_E_ERROR;
+  }
+}
+
+int scenopt_problem_save(const scenopt_problem* p, const char* path) {
+  SCN_GUARD({
+    if (!p || !path) fail(SCENOPT_E_INVALID_PARAMS, "save_problem: null argument");
+    save_problem(p->p, path);
+  });
+}
+
+int scenopt_problem_load(const char* path, scenopt_problem** out) {
+  SCN_GUARD({
+    if (!path || !out) fail(SCENOPT_E_INVALID_PARAMS, "load_problem: null argument");
+    auto h = std::make_unique<scenopt_problem>();
+    h->p = load_problem(path);
+    *out = h.release();
+  });
+}
+
+int scenopt_problem_hashes(const scenopt_problem* p, uint64_t* content, uint64_t* factor) {
+  SCN_GUARD({
+    if (!p) fail(SCENOPT_E_INVALID_PARAMS, "problem hashes: null problem");
+    if (content) *content = content_hash(p->p);
+    if (factor) *factor = factor_hash(p->p);
+  });
+}
+
+int scenopt_problem_set_mode(scenopt_problem* p, const int32_t* mode, int n) {
+  SCN_GUARD({
+    if (!p) fail(SCENOPT_E_INVALID_PARAMS, "set_mode: null problem");
+    if (n != 0 && n != p->p.n) fail(SCENOPT_E_DIMENSION_MISMATCH, "tree: mode must be empty or one entry per node");
+    p->p.mode.assign(mode, mode + n);
+  });
+}
+
+int scenopt_problem_get_mode(const scenopt_problem* p, int32_t* out, int cap) {
+  SCN_GUARD({
+    if (!p) fail(SCENOPT_E_INVALID_PARAMS, "get_mode: null problem");
+    const int n = static_cast<int>(p->p.mode.size());
+    if (out)
+      for (int i = 0; i < std::min(n, cap); ++i) out[i] = p->p.mode[static_cast<size_t>(i)];
+    return n;
+  });
+}

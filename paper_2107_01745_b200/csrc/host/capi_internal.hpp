@@ -36,6 +36,7 @@ struct Stats {  // OracleStats, tree_oracles.hpp:14-21
 
 struct scenopt_problem {
   scn::Problem p;
+  std::string text;  // last serialization (size query, then copy)
 };
 struct scenopt_factor {
   scn::Factor f;

@@ -235,3 +235,117 @@ double spectral_radius(const double* A0, int n) {
 }
 
 }  // namespace scn
+
+namespace scn {
+namespace {
+using Dm = std::vector<double>;
+Dm mm(const Dm& A, const Dm& B, int n) {
+  Dm C(static_cast<size_t>(n) * n, 0.0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k) {
+      const double b = B[k + static_cast<size_t>(j) * n];
+      if (b == 0.0) continue;
+      for (int i = 0; i < n; ++i) C[i + static_cast<size_t>(j) * n] += A[i + static_cast<size_t>(k) * n] * b;
+    }
+  return C;
+}
+// X = P^{-1} Q by LU with partial pivoting (P overwritten)
+Dm lu_solve(Dm P, Dm Q, int n) {
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(P[i + static_cast<size_t>(k) * n]) > std::fabs(P[piv + static_cast<size_t>(k) * n])) piv = i;
+    if (piv != k) {
+      for (int j = 0; j < n; ++j) std::swap(P[k + static_cast<size_t>(j) * n], P[piv + static_cast<size_t>(j) * n]);
+      for (int j = 0; j < n; ++j) std::swap(Q[k + static_cast<size_t>(j) * n], Q[piv + static_cast<size_t>(j) * n]);
+    }
+    const double d = P[k + static_cast<size_t>(k) * n];
+    for (int i = k + 1; i < n; ++i) {
+      const double l = P[i + static_cast<size_t>(k) * n] / d;
+      if (l == 0.0) continue;
+      for (int j = k; j < n; ++j) P[i + static_cast<size_t>(j) * n] -= l * P[k + static_cast<size_t>(j) * n];
+      for (int j = 0; j < n; ++j) Q[i + static_cast<size_t>(j) * n] -= l * Q[k + static_cast<size_t>(j) * n];
+    }
+  }
+  for (int j = 0; j < n; ++j)
+    for (int i = n - 1; i >= 0; --i) {
+      double s = Q[i + static_cast<size_t>(j) * n];
+      for (int k = i + 1; k < n; ++k) s -= P[i + static_cast<size_t>(k) * n] * Q[k + static_cast<size_t>(j) * n];
+      Q[i + static_cast<size_t>(j) * n] = s / P[i + static_cast<size_t>(i) * n];
+    }
+  return Q;
+}
+}  // namespace
+
+// Matrix exponential by scaling and squaring with the [m/m] Pade approximant,
+// m in {3, 5, 7, 9, 13} chosen by the 1-norm (Higham 2005, the method behind
+// Eigen's MatrixBase::exp() that generators.hpp:108 calls).
+std::vector<double> expm(const std::vector<double>& A0, int n) {
+  static const double th[5] = {1.495585217958292e-2, 2.539398330063230e-1, 9.504178996162932e-1,
+                               2.097847961257068e0, 5.371920351148152e0};
+  static const double b3[4] = {120., 60., 12., 1.};
+  static const double b5[6] = {30240., 15120., 3360., 420., 30., 1.};
+  static const double b7[8] = {17297280., 8648640., 1995840., 277200., 25200., 1512., 56., 1.};
+  static const double b9[10] = {17643225600., 8821612800., 2075673600., 302702400., 30270240.,
+                                2162160.,     110880.,     3960.,       90.,         1.};
+  static const double b13[14] = {64764752532480000., 32382376266240000., 7771770303897600., 1187353796428800.,
+                                 129060195264000.,   10559470521600.,    670442572800.,    33522128640.,
+                                 1323241920.,        40840800.,          960960.,          16380.,
+                                 182.,               1.};
+  const size_t nn = static_cast<size_t>(n) * n;
+  double norm1 = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += std::fabs(A0[i + static_cast<size_t>(j) * n]);
+    norm1 = std::max(norm1, s);
+  }
+  Dm I(nn, 0.0);
+  for (int i = 0; i < n; ++i) I[i + static_cast<size_t>(i) * n] = 1.0;
+  auto pade = [&](const Dm& A, const double* b, int m, Dm& U, Dm& V) {  // m in {3,5,7,9}
+    const Dm A2 = mm(A, A, n);
+    Dm pw = I, Uo(nn, 0.0);
+    V.assign(nn, 0.0);
+    for (int k = 0; k <= m; k += 2) {  // even powers A^k: V += b_k A^k, Uo += b_{k+1} A^k
+      for (size_t t = 0; t < nn; ++t) {
+        V[t] += b[k] * pw[t];
+        Uo[t] += b[k + 1] * pw[t];
+      }
+      if (k + 2 <= m) pw = mm(pw, A2, n);
+    }
+    U = mm(A, Uo, n);
+  };
+  int s = 0;
+  Dm A = A0, U, V;
+  if (norm1 <= th[0]) pade(A, b3, 3, U, V);
+  else if (norm1 <= th[1]) pade(A, b5, 5, U, V);
+  else if (norm1 <= th[2]) pade(A, b7, 7, U, V);
+  else if (norm1 <= th[3]) pade(A, b9, 9, U, V);
+  else {
+    if (norm1 > th[4]) s = std::max(0, static_cast<int>(std::ceil(std::log2(norm1 / th[4]))));
+    const double sc = std::ldexp(1.0, -s);
+    for (double& v : A) v *= sc;
+    const Dm A2 = mm(A, A, n), A4 = mm(A2, A2, n), A6 = mm(A4, A2, n);
+    Dm t1(nn), t2(nn), t3(nn), t4(nn);
+    for (size_t t = 0; t < nn; ++t) {
+      t1[t] = b13[13] * A6[t] + b13[11] * A4[t] + b13[9] * A2[t];
+      t2[t] = b13[7] * A6[t] + b13[5] * A4[t] + b13[3] * A2[t] + b13[1] * I[t];
+      t3[t] = b13[12] * A6[t] + b13[10] * A4[t] + b13[8] * A2[t];
+      t4[t] = b13[6] * A6[t] + b13[4] * A4[t] + b13[2] * A2[t] + b13[0] * I[t];
+    }
+    Dm inner = mm(A6, t1, n);
+    for (size_t t = 0; t < nn; ++t) inner[t] += t2[t];
+    U = mm(A, inner, n);
+    V = mm(A6, t3, n);
+    for (size_t t = 0; t < nn; ++t) V[t] += t4[t];
+  }
+  Dm P(nn), Q(nn);
+  for (size_t t = 0; t < nn; ++t) {
+    P[t] = V[t] - U[t];
+    Q[t] = V[t] + U[t];
+  }
+  Dm X = lu_solve(std::move(P), std::move(Q), n);
+  for (int k = 0; k < s; ++k) X = mm(X, X, n);
+  return X;
+}
+
+}  // namespace scn

@@ -148,7 +148,7 @@ void problem_to_view(const Problem& p, scenopt_problem_view* v) {
 }
 
 // scenario_tree.hpp:128-240 and problem_data.hpp:233-314, over the flat model.
-std::vector<std::string> validate(const Problem& p) {
+std::vector<std::string> validate_tree(const Problem& p) {
   std::vector<std::string> bad;
   auto complain = [&bad](const std::string& m) { bad.push_back(m); };
   constexpr double kTol = 1e-9;
@@ -192,6 +192,13 @@ std::vector<std::string> validate(const Problem& p) {
     if (p.node_stage[i] == p.node_stage[i + 1] && p.ancestor[i] > p.ancestor[i + 1])
       complain("node " + std::to_string(i + 1) +
                ": siblings out of BFS order (ancestor ids must be nondecreasing within a stage)");
+  return bad;
+}
+
+std::vector<std::string> validate(const Problem& p) {
+  std::vector<std::string> bad = validate_tree(p);
+  auto complain = [&bad](const std::string& m) { bad.push_back(m); };
+  const int n = p.n;
   const int nx = p.nx, nu = p.nu;
   auto check_spec = [&](int kind, double gamma, int off, int rows, const std::string& where) {
     if (kind < 0 || kind > 2) {
@@ -318,6 +325,7 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
   p.ancestor = {-1};
   p.probability = {1.0};
   p.stage_offsets = {0, 1};
+  p.mode = {-1};
   {
     int begin = 0, end = 1;
     for (int t = 0; t < horizon; ++t) {
@@ -327,6 +335,7 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
         for (int w = 0; w < nb; ++w) {
           p.ancestor.push_back(i);
           p.probability.push_back(p.probability[i] * branch);
+          p.mode.push_back(w);
         }
       begin = end;
       end = static_cast<int>(p.ancestor.size());
@@ -448,4 +457,187 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
   return p;
 }
 
+}  // namespace scn
+
+namespace scn {
+// ---------------------------------------------------------------- spring-mass
+// generators.hpp:66-91 (column-major 2M x 2M and 2M x (M-1))
+void spring_mass_continuous(int masses, const SpringMass& par, std::vector<double>& A, std::vector<double>& B) {
+  const int M = masses, nx = 2 * M, nu = M - 1;
+  A.assign(static_cast<size_t>(nx) * nx, 0.0);
+  B.assign(static_cast<size_t>(nx) * nu, 0.0);
+  const double ks = par.stiffness / par.mass_kg, bs = par.damping / par.mass_kg;
+  auto a = [&](int i, int j) -> double& { return A[i + static_cast<size_t>(j) * nx]; };
+  for (int j = 0; j < M; ++j) {
+    a(j, M + j) = 1.0;                         // dp/dt = v
+    a(M + j, j) = -ks * 2.0;                   // -(k/m) T, T = tridiag(-1, 2, -1)
+    a(M + j, M + j) = -bs * 2.0;               // -(b/m) T
+    if (j > 0) {
+      a(M + j, j - 1) = -ks * -1.0;
+      a(M + j, M + j - 1) = -bs * -1.0;
+    }
+    if (j + 1 < M) {
+      a(M + j, j + 1) = -ks * -1.0;
+      a(M + j, M + j + 1) = -bs * -1.0;
+    }
+  }
+  for (int u = 0; u < nu; ++u) {  // actuator u: -u on mass u, +u on mass u+1
+    B[(M + u) + static_cast<size_t>(u) * nx] = -1.0 / par.mass_kg;
+    B[(M + u + 1) + static_cast<size_t>(u) * nx] = 1.0 / par.mass_kg;
+  }
+}
+
+// generators.hpp:97-112
+void discretize_zoh(const double* A, const double* B, int n, int m, double period, double* Ad, double* Bd) {
+  if (!(period > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "discretize_zoh: period must be > 0");
+  const int k = n + m;
+  std::vector<double> aug(static_cast<size_t>(k) * k, 0.0);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) aug[i + static_cast<size_t>(j) * k] = A[i + static_cast<size_t>(j) * n] * period;
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < n; ++i) aug[i + static_cast<size_t>(n + j) * k] = B[i + static_cast<size_t>(j) * n] * period;
+  const std::vector<double> E = expm(aug, k);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) Ad[i + static_cast<size_t>(j) * n] = E[i + static_cast<size_t>(j) * k];
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < n; ++i) Bd[i + static_cast<size_t>(j) * n] = E[i + static_cast<size_t>(n + j) * k];
+}
+
+// build_from_markov, scenario_tree.hpp:72-126: all positive-probability mode
+// paths in BFS order, children in mode order (fills the tree members of p)
+void markov_tree(const std::vector<double>& T, int rows, int cols, const std::vector<double>& initial, int horizon,
+                 Problem& p) {
+  const int modes = static_cast<int>(initial.size());
+  if (horizon < 1) fail(SCENOPT_E_INVALID_PARAMS, "build_from_markov: horizon must be >= 1");
+  if (rows != modes || cols != modes)
+    fail(SCENOPT_E_DIMENSION_MISMATCH,
+         "build_from_markov: transition must be square and match the initial distribution size");
+  double sum = 0.0, mn = 0.0;
+  for (double v : initial) {
+    sum += v;
+    mn = std::min(mn, v);
+  }
+  if (modes == 0 || mn < 0.0 || std::fabs(sum - 1.0) > 1e-9)
+    fail(SCENOPT_E_NON_STOCHASTIC_MATRIX, "build_from_markov: initial distribution");
+  for (int w = 0; w < modes; ++w) {
+    double rs = 0.0, rm = 0.0;
+    for (int j = 0; j < modes; ++j) {
+      rs += T[static_cast<size_t>(w) * modes + j];
+      rm = std::min(rm, T[static_cast<size_t>(w) * modes + j]);
+    }
+    if (rm < 0.0 || std::fabs(rs - 1.0) > 1e-9)
+      fail(SCENOPT_E_NON_STOCHASTIC_MATRIX, "build_from_markov: transition row " + std::to_string(w));
+  }
+  p.N = horizon;
+  p.ancestor = {-1};
+  p.probability = {1.0};
+  p.stage_offsets = {0, 1};
+  p.mode = {-1};
+  for (int t = 0, begin = 0, end = 1; t < horizon; ++t) {
+    for (int i = begin; i < end; ++i)
+      for (int w = 0; w < modes; ++w) {
+        const double branch = t == 0 ? initial[static_cast<size_t>(w)]
+                                     : T[static_cast<size_t>(p.mode[static_cast<size_t>(i)]) * modes + w];
+        if (branch <= 0.0) continue;
+        p.ancestor.push_back(i);
+        p.probability.push_back(p.probability[static_cast<size_t>(i)] * branch);
+        p.mode.push_back(w);
+      }
+    begin = end;
+    end = static_cast<int>(p.ancestor.size());
+    p.stage_offsets.push_back(end);
+  }
+  p.n = static_cast<int>(p.ancestor.size());
+}
+
+// generators.hpp:119-218 on the tree of scenario_tree.hpp:72-126 (positive-probability
+// mode paths, BFS order, children in mode order)
+Problem gen_spring_mass(int masses, const SpringMass& params) {
+  if (masses < 2) fail(SCENOPT_E_INVALID_PARAMS, "gen_spring_mass: masses must be >= 2");
+  if (!(params.mass_kg > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "gen_spring_mass: mass_kg must be > 0");
+  if (!(params.input_bound > 0.0) || !(params.velocity_bound > 0.0))
+    fail(SCENOPT_E_INVALID_PARAMS, "gen_spring_mass: bounds must be > 0");
+  if (!(params.input_weight > 0.0) || !(params.terminal_weight > 0.0))
+    fail(SCENOPT_E_INVALID_PARAMS, "gen_spring_mass: input and terminal weights must be > 0");
+  if (params.state_weight < 0.0) fail(SCENOPT_E_INVALID_PARAMS, "gen_spring_mass: state_weight must be >= 0");
+  SpringMass par = params;
+  if (par.initial_probs.empty()) par.initial_probs = {0.5, 0.5};
+  if (par.transition.empty()) {
+    par.transition = {0.1, 0.9, 0.9, 0.1};
+    par.transition_rows = par.transition_cols = 2;
+  }
+  if (par.mode_values.empty()) {
+    par.mode_values.assign(par.initial_probs.size(), 0.0);
+    if (par.mode_values.size() > 1) par.mode_values[1] = 0.1;
+  }
+  if (par.mode_values.size() != par.initial_probs.size())
+    fail(SCENOPT_E_DIMENSION_MISMATCH, "gen_spring_mass: one mode value per Markov mode required");
+  const int M = masses, nx = 2 * M, nu = M - 1;
+  std::vector<double> Ac, Bc, Ad(static_cast<size_t>(nx) * nx), Bd(static_cast<size_t>(nx) * nu);
+  spring_mass_continuous(M, par, Ac, Bc);
+  discretize_zoh(Ac.data(), Bc.data(), nx, nu, par.sampling, Ad.data(), Bd.data());
+  Problem p;
+  markov_tree(par.transition, par.transition_rows, par.transition_cols, par.initial_probs, par.horizon, p);
+  if (!par.root_state.empty() && static_cast<int>(par.root_state.size()) != nx)
+    fail(SCENOPT_E_DIMENSION_MISMATCH, "gen_spring_mass: root_state must have length 2M");
+
+  p.nx = nx;
+  p.nu = nu;
+  const std::vector<int32_t>& mode = p.mode;
+  const int n = p.n, L = n - p.stage_offsets[static_cast<size_t>(par.horizon)], rows = M + nu;
+  p.stage_rows.assign(static_cast<size_t>(n), rows);
+  p.stage_rows[0] = 0;
+  p.terminal_rows.assign(static_cast<size_t>(L), M);
+  p.finalize();
+  p.root_state = par.root_state.empty() ? std::vector<double>(static_cast<size_t>(nx), 0.0) : par.root_state;
+  const size_t sxx = p.sxx(), sxu = p.sxu(), suu = p.suu();
+  p.A.assign(n * sxx, 0.0);
+  p.B.assign(n * sxu, 0.0);
+  p.c.assign(static_cast<size_t>(n) * nx, 0.0);
+  p.Q.assign(n * sxx, 0.0);
+  p.R.assign(n * suu, 0.0);
+  p.S.assign(n * sxu, 0.0);
+  p.q.assign(static_cast<size_t>(n) * nx, 0.0);
+  p.r.assign(static_cast<size_t>(n) * nu, 0.0);
+  p.F.assign(static_cast<size_t>(p.stage_total) * nx, 0.0);
+  p.G.assign(static_cast<size_t>(p.stage_total) * nu, 0.0);
+  p.g_kind.assign(static_cast<size_t>(n), 1);
+  p.g_kind[0] = 0;
+  p.g_gamma.assign(static_cast<size_t>(n), 0.0);
+  p.zmin.assign(static_cast<size_t>(p.dual_dim), 0.0);
+  p.zmax.assign(static_cast<size_t>(p.dual_dim), 0.0);
+  p.P.assign(static_cast<size_t>(L) * sxx, 0.0);
+  p.p.assign(static_cast<size_t>(L) * nx, 0.0);
+  p.FN.assign(static_cast<size_t>(L) * M * nx, 0.0);
+  p.tg_kind.assign(static_cast<size_t>(L), 1);
+  p.tg_gamma.assign(static_cast<size_t>(L), 0.0);
+  for (int i = 1; i < n; ++i) {
+    std::copy(Ad.begin(), Ad.end(), p.A.begin() + static_cast<std::ptrdiff_t>(i * sxx));
+    std::copy(Bd.begin(), Bd.end(), p.B.begin() + static_cast<std::ptrdiff_t>(i * sxu));
+    std::fill_n(p.c.begin() + static_cast<std::ptrdiff_t>(i) * nx, nx, par.mode_values[static_cast<size_t>(mode[static_cast<size_t>(i)])]);
+    for (int k = 0; k < nx; ++k) p.Q[i * sxx + k + static_cast<size_t>(k) * nx] = par.state_weight;
+    for (int k = 0; k < nu; ++k) p.R[i * suu + k + static_cast<size_t>(k) * nu] = par.input_weight;
+    const int off = p.dual_offset[i];
+    double* F = p.F.data() + static_cast<size_t>(off) * nx;  // rows x nx column-major
+    double* G = p.G.data() + static_cast<size_t>(off) * nu;
+    for (int k = 0; k < M; ++k) F[k + static_cast<size_t>(M + k) * rows] = 1.0;  // velocity rows
+    for (int k = 0; k < nu; ++k) G[(M + k) + static_cast<size_t>(k) * rows] = 1.0;  // input rows
+    for (int k = 0; k < rows; ++k) {
+      const double bnd = k < M ? par.velocity_bound : par.input_bound;
+      p.zmin[static_cast<size_t>(off + k)] = -bnd;
+      p.zmax[static_cast<size_t>(off + k)] = bnd;
+    }
+  }
+  for (int l = 0; l < L; ++l) {
+    for (int k = 0; k < nx; ++k) p.P[l * sxx + k + static_cast<size_t>(k) * nx] = par.terminal_weight;
+    const int off = p.tdual_offset[l];
+    double* FN = p.FN.data() + static_cast<size_t>(off - p.stage_total) * nx;
+    for (int k = 0; k < M; ++k) {
+      FN[k + static_cast<size_t>(M + k) * M] = 1.0;
+      p.zmin[static_cast<size_t>(off + k)] = -par.velocity_bound;
+      p.zmax[static_cast<size_t>(off + k)] = par.velocity_bound;
+    }
+  }
+  return p;
+}
 }  // namespace scn

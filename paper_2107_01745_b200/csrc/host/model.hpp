@@ -25,6 +25,7 @@ struct Error : std::runtime_error {
 struct Problem {
   int nx = 0, nu = 0, N = 0, n = 0, L = 0, first_leaf = 0, dual_dim = 0, stage_total = 0;
   std::vector<int32_t> ancestor, stage_offsets, stage_rows, terminal_rows, g_kind, tg_kind;
+  std::vector<int32_t> mode;  // Markov mode per node (-1 root); empty when unknown (scenario_tree.hpp:41)
   std::vector<double> probability, root_state, A, B, c, Q, R, S, q, r, F, G, g_gamma, P, p, FN,
       tg_gamma, zmin, zmax;
   // derived (finalize)
@@ -55,10 +56,27 @@ struct Problem {
 Problem problem_from_view(const scenopt_problem_view& v);
 void problem_to_view(const Problem& p, scenopt_problem_view* v);
 std::vector<std::string> validate(const Problem& p);
+std::vector<std::string> validate_tree(const Problem& p);  // scenario_tree.hpp:128-240 only
+void markov_tree(const std::vector<double>& transition, int rows, int cols, const std::vector<double>& initial,
+                 int horizon, Problem& p);
 void require_valid(const Problem& p);
 Problem precondition(const Problem& p);                 // solvers.hpp:569-602
 std::vector<double> probability_roots(const Problem& p);  // solvers.hpp:608-623
 Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector<int>& br);
+
+// generators.hpp:39-234: spring-mass-damper array on the Markov mode tree.
+// Empty vectors take the reference defaults; transition is row-major.
+struct SpringMass {
+  double mass_kg = 5.0, stiffness = 1.0, damping = 0.1, input_bound = 2.0, velocity_bound = 5.0;
+  int horizon = 11;
+  double sampling = 0.5, state_weight = 5.0, input_weight = 2.0, terminal_weight = 100.0;
+  std::vector<double> initial_probs, transition, mode_values, root_state;
+  int transition_rows = 0, transition_cols = 0;
+};
+Problem gen_spring_mass(int masses, const SpringMass& par);
+void spring_mass_continuous(int masses, const SpringMass& par, std::vector<double>& A, std::vector<double>& B);
+std::vector<double> expm(const std::vector<double>& A, int n);  // column-major n x n
+void discretize_zoh(const double* A, const double* B, int n, int m, double period, double* Ad, double* Bd);
 
 struct Factor {
   int nx = 0, nu = 0, n = 0, first_leaf = 0, dual_dim = 0, L = 0, stage_total = 0;

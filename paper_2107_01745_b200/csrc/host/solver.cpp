@@ -148,6 +148,10 @@ double halve_lambda(double lambda) {
 
 }  // namespace
 
+namespace scn {
+void check_solver_config(const scenopt_solver_config& c) { validate_config(c); }  // experiment.cpp
+}  // namespace scn
+
 // Engine: the per-handle solver operations (device resident).
 struct Engine {
   scenopt_dev& h;

@@ -125,6 +125,62 @@ TEST_CASE("markov build: full two-mode chain is a binary tree", true) {
   CHECK_THROWS_AS(scenopt::build_from_markov(bad, p0, 2), scenopt::NonStochasticMatrix);
 }
 
+TEST_CASE("spring-mass defaults and documented structure (test_generators.cpp:42-93)", true) {
+  const auto def = scenopt::gen_spring_mass(5);
+  CHECK(def.nx == 10 && def.nu == 4 && def.tree.num_stages == 11);
+  CHECK(def.num_nodes() == 4095 && def.tree.num_leaves() == 2048);
+  scenopt::SpringMassParams par;
+  par.horizon = 3;
+  const auto prob = scenopt::gen_spring_mass(5, par);
+  REQUIRE(prob.num_nodes() == 15);
+  CHECK(scenopt::validate(prob).empty());
+  CHECK(prob.dual_dim == 14 * 9 + 8 * 5);
+  CHECK(prob.tree.probability[1] == 0.5 && prob.tree.probability[2] == 0.5);
+  for (int i = 1; i < prob.num_nodes(); ++i) {
+    CHECK(prob.stage_rows(i) == 9);
+    CHECK(prob.cost[i].Q(3, 3) == 5.0 && prob.cost[i].Q(3, 4) == 0.0 && prob.cost[i].R(2, 2) == 2.0);
+    const auto& g = prob.con[i].g;
+    CHECK(g.zmin(0) == -5.0 && g.zmax(4) == 5.0 && g.zmin(5) == -2.0 && g.zmax(8) == 2.0);
+  }
+  CHECK(prob.dyn[1].c.lpNormInf() == 0.0 && prob.dyn[2].c(7) == 0.1);  // modes 0 / 1 at stage 1
+  CHECK(prob.tcost[3].P(9, 9) == 100.0 && prob.terminal_rows(3) == 5);
+}
+
+TEST_CASE("spring-mass ZOH, free particles and parameter checks (test_generators.cpp:95-145)", true) {
+  scenopt::SpringMassParams par;
+  par.horizon = 1;
+  for (const int masses : {2, 3, 5}) {
+    const auto prob = scenopt::gen_spring_mass(masses, par);
+    scenopt::Mat Ac, Bc, Ad, Bd;
+    scenopt::detail::spring_mass_continuous(masses, par, Ac, Bc);
+    scenopt::discretize_zoh(Ac, Bc, par.sampling, Ad, Bd);
+    double d = 0.0;
+    for (int j = 0; j < Ad.cols(); ++j)
+      for (int i = 0; i < Ad.rows(); ++i) d = std::max(d, std::abs(Ad(i, j) - prob.dyn[1].A(i, j)));
+    CHECK(d == 0.0);
+  }
+  par.stiffness = 0.0;
+  par.damping = 0.0;
+  const auto free = scenopt::gen_spring_mass(4, par);
+  for (int i = 0; i < 4; ++i) {
+    CHECK(std::abs(free.dyn[1].A(i, i) - 1.0) < 1e-12 && std::abs(free.dyn[1].A(4 + i, 4 + i) - 1.0) < 1e-12);
+    CHECK(std::abs(free.dyn[1].A(i, 4 + i) - par.sampling) < 1e-12 && std::abs(free.dyn[1].A(4 + i, i)) < 1e-12);
+  }
+  CHECK_THROWS_AS(scenopt::gen_spring_mass(1), scenopt::InvalidParams);
+  scenopt::SpringMassParams bad;
+  bad.mass_kg = 0.0;
+  CHECK_THROWS_AS(scenopt::gen_spring_mass(5, bad), scenopt::InvalidParams);
+  bad = {};
+  bad.mode_values = Vec::Zero(3);
+  CHECK_THROWS_AS(scenopt::gen_spring_mass(5, bad), scenopt::DimensionMismatch);
+  bad = {};
+  bad.root_state = Vec::Zero(3);
+  CHECK_THROWS_AS(scenopt::gen_spring_mass(5, bad), scenopt::DimensionMismatch);
+  std::mt19937_64 ga(7), gb(7);
+  const Vec sa = scenopt::sample_initial_state(5, {}, ga), sb = scenopt::sample_initial_state(5, {}, gb);
+  CHECK(sa.size() == 10 && (sa - sb).lpNormInf() == 0.0 && sa.segment(5, 5).lpNormInf() <= 2.5);
+}
+
 TEST_CASE("validate reports broken instances", true) {
   auto prob = small(8);
   prob.tree.probability[1] = 0.9;  // children no longer sum to the parent

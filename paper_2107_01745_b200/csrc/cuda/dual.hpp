@@ -26,6 +26,7 @@ constexpr int kScalars = 192;
 // Int block slots.
 namespace il {
 constexpr int LB_COUNT = 0, LB_PUSHED = 1, SETTLED = 2, PZERO = 3;
+constexpr int PDONE = 4, PROUNDS = 5, PMAX = 6;  // batched power iteration: sticky stop flag, rounds run, cap
 constexpr int LB_ORDER = 8;  // [8, 8 + mem + 1): slot ids, oldest first, then free slots
 constexpr int kInts = 128;
 }  // namespace il
@@ -56,6 +57,7 @@ cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, 
                         cudaStream_t st);
 // MINFBE fbe_grad epilogue (fbe.hpp:89-94): grad = R + lam HR, and the simple
 // backtracking norms ||(grad - R)/lam||^2, ||R||^2 (solvers.hpp:215-222, 279-302).
+cudaError_t k_publish(const double* S, const int* I, double* hS_mapped, int* hI_mapped, cudaStream_t st);
 cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const double* HR, double* grad,
                        cudaStream_t st);
 // L-BFGS (lbfgs.hpp:33-62): optional push of (a - b, cc - dd) with scale_ref

@@ -469,6 +469,9 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
 
 // ---------------------------------------------------------------- K8
 __global__ void __launch_bounds__(kThreads) power_kernel(DualCtx c, double* v, const double* Hv, double rel_tol) {
+  // rounds are enqueued in batches: after the stopping round every later
+  // launch (and its sweep, via SweepParams::skip) does nothing
+  if (*reinterpret_cast<const volatile int*>(c.I + il::PDONE)) return;
   int ph = 0;
   double s[2] = {0, 0};
   for (int i = gtid(); i < c.D; i += gstride()) {
@@ -490,6 +493,8 @@ __global__ void __launch_bounds__(kThreads) power_kernel(DualCtx c, double* v, c
     c.S[sl::PMAG] = mag;
     c.I[il::SETTLED] = settled ? 1 : 0;
     c.I[il::PZERO] = zero ? 1 : 0;
+    c.I[il::PROUNDS] += 1;
+    if (zero || settled || c.I[il::PROUNDS] >= c.I[il::PMAX]) c.I[il::PDONE] = 1;
   }
 }
 
@@ -659,6 +664,18 @@ cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, 
   DualCtx cc = c;
   void* args[] = {&cc, &state, &mode, &y, &Hx, &Hx0, &weight, &z, &R, &T};
   return coop(reinterpret_cast<const void*>(fb_finish_kernel), c, args, st);
+}
+
+// Scalar block -> mapped pinned host memory in one launch (the host waits on
+// an event instead of two D2H copies)
+__global__ void publish_kernel(const double* S, const int* I, double* hS, int* hI) {
+  for (int t = threadIdx.x; t < sl::kScalars; t += blockDim.x) hS[t] = S[t];
+  for (int t = threadIdx.x; t < il::kInts; t += blockDim.x) hI[t] = I[t];
+}
+
+cudaError_t k_publish(const double* S, const int* I, double* hS_mapped, int* hI_mapped, cudaStream_t st) {
+  publish_kernel<<<1, 256, 0, st>>>(S, I, hS_mapped, hI_mapped);
+  return cudaGetLastError();
 }
 
 cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const double* HR, double* grad,

@@ -94,6 +94,7 @@ struct SweepParams {
   int mmax;
   const double* root_state;
   unsigned* ctrl;     // [0] epoch, [1] done-CTA counter
+  const int* skip;    // non-null and *skip != 0: the launch does nothing (batched power iteration)
   unsigned* bw_flag;  // [n]
   unsigned* fw_flag;  // [n]
   const double* y[kMaxRhs];

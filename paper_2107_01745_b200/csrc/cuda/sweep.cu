@@ -755,6 +755,9 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   __shared__ __align__(16) int4 sdone[kDoneQ];  // {first, count, pass, publish} of finished items
   __shared__ unsigned s_epoch;
   __shared__ int s_retired;  // items [0, s_retired) of this CTA are complete
+  // a skipped launch touches nothing: the epoch stays, so the next sweep is
+  // as if this one had not been enqueued (every CTA reads the same flag)
+  if (P.skip && *reinterpret_cast<const volatile int*>(P.skip)) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NS = P.nslot;  // matrix slots
   double* slots = smem;

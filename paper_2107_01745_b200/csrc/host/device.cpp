@@ -1127,6 +1127,7 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
   P.mmax = d.max_m;
   P.root_state = d.root_state;
   P.ctrl = d.ctrl;
+  P.skip = d.sweep_skip;
   P.bw_flag = d.bw_flag;
   P.fw_flag = d.fw_flag;
   for (int r = 0; r < nrhs; ++r) {

@@ -30,6 +30,12 @@ struct scenopt_dev::Work {
   unsigned* bar = nullptr;
   double* hS = nullptr;  // pinned mirrors
   int* hI = nullptr;
+  // mapped pinned copy of S / I written by k_publish; pubEv marks its completion
+  double* pS = nullptr;
+  int* pI = nullptr;
+  double* dpS = nullptr;
+  int* dpI = nullptr;
+  cudaEvent_t pubEv = nullptr;
   // pinned staging words of asynchronous scalar writes; a word is reused only
   // after a stream synchronisation has retired every copy that read it
   static constexpr int kRing = 256;
@@ -64,6 +70,9 @@ scenopt_dev::~scenopt_dev() {
     if (w->hS) cudaFreeHost(w->hS);
     if (w->hI) cudaFreeHost(w->hI);
     if (w->hRing) cudaFreeHost(w->hRing);
+    if (w->pS) cudaFreeHost(w->pS);
+    if (w->pI) cudaFreeHost(w->pI);
+    if (w->pubEv) cudaEventDestroy(w->pubEv);
   }
 }
 
@@ -85,6 +94,11 @@ void scenopt_dev::init_solver_buffers() {
   SCN_CUDA(cudaMallocHost(&k.hS, sl::kScalars * sizeof(double)));
   SCN_CUDA(cudaMallocHost(&k.hI, il::kInts * sizeof(int)));
   SCN_CUDA(cudaMallocHost(&k.hRing, scenopt_dev::Work::kRing * sizeof(double)));
+  SCN_CUDA(cudaHostAlloc(&k.pS, sl::kScalars * sizeof(double), cudaHostAllocMapped));
+  SCN_CUDA(cudaHostAlloc(&k.pI, il::kInts * sizeof(int), cudaHostAllocMapped));
+  SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpS), k.pS, 0));
+  SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpI), k.pI, 0));
+  SCN_CUDA(cudaEventCreateWithFlags(&k.pubEv, cudaEventDisableTiming));
   const size_t D = static_cast<size_t>(k.D), nxn = static_cast<size_t>(L.nx) * L.n,
                nuf = static_cast<size_t>(L.nu) * std::max(L.first_leaf, 1);
   for (int s = 0; s < 2; ++s) {
@@ -173,22 +187,48 @@ struct Engine {
     k.hS[slot] = v;  // host mirror
     SCN_CUDA(cudaMemcpyAsync(k.S + slot, w, sizeof(double), cudaMemcpyHostToDevice, st));
   }
-  void read_scalars() {
-    cudaEvent_t pre = nullptr;
+  // Host reads of the scalar block. publish() enqueues its copy into mapped
+  // host memory and marks it with an event; wait_published() waits for that
+  // event only, so work enqueued after publish() keeps the GPU busy while the
+  // host decides (speculation). read_scalars() = publish + full stream sync.
+  cudaEvent_t pub_pre = nullptr;
+  void publish() {
     if (timer.on) {
-      cudaEventCreate(&pre);
-      cudaEventRecord(pre, st);
+      cudaEventCreate(&pub_pre);
+      cudaEventRecord(pub_pre, st);
     }
-    SCN_CUDA(cudaMemcpyAsync(k.hS, k.S, sl::kScalars * sizeof(double), cudaMemcpyDeviceToHost, st));
-    SCN_CUDA(cudaMemcpyAsync(k.hI, k.I, il::kInts * sizeof(int), cudaMemcpyDeviceToHost, st));
-    SCN_CUDA(cudaStreamSynchronize(st));
-    k.ring_next = 0;
-    if (timer.on) {  // GPU-side cost of this host round trip: copies + wake-up + re-enqueue
+    SCN_CUDA(k_publish(k.S, k.I, k.dpS, k.dpI, st));
+    SCN_CUDA(cudaEventRecord(k.pubEv, st));
+    mark("read.copy");
+  }
+  void wait_published(bool full) {
+    const double h0 = timer.on ? now_ms() : 0.0;
+    if (full) {
+      SCN_CUDA(cudaStreamSynchronize(st));
+      k.ring_next = 0;  // every staging word has been consumed
+    } else {
+      SCN_CUDA(cudaEventSynchronize(k.pubEv));
+    }
+    if (timer.on) timer.host_sync_ms += now_ms() - h0;
+    std::memcpy(k.hS, k.pS, sl::kScalars * sizeof(double));
+    std::memcpy(k.hI, k.pI, il::kInts * sizeof(int));
+    if (timer.on) {  // GPU-side cost of this host round trip: copy + wake-up + re-enqueue
       cudaEvent_t post;
       cudaEventCreate(&post);
       cudaEventRecord(post, st);
-      timer.sync_ev.emplace_back(pre, post);
+      timer.sync_ev.emplace_back(pub_pre, post);
     }
+  }
+  void read_scalars() {
+    publish();
+    wait_published(true);
+  }
+  void mark(const char* tag) {
+    if (!timer.marks) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, st);
+    timer.mk.emplace_back(tag, ev);
   }
   double S(int slot) const { return k.hS[slot]; }
   int I(int slot) const { return k.hI[slot]; }
@@ -200,6 +240,7 @@ struct Engine {
     bool on = std::getenv("SCN_SOLVE_TIMING") != nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
     ~SweepTimer() {
+      report_marks();
       if (!on || ev.empty()) return;
       cudaDeviceSynchronize();
       double tot = 0.0;
@@ -220,8 +261,34 @@ struct Engine {
       if (!sync_ev.empty())
         std::fprintf(stderr, "[scn] %zu host round trips, %.3f ms (%.1f us each)\n", sync_ev.size(), st,
                      1e3 * st / sync_ev.size());
+      std::fprintf(stderr, "[scn] host: %.3f ms enqueuing sweeps (%.1f us each), %.3f ms blocked in reads\n",
+                   host_launch_ms, 1e3 * host_launch_ms / ev.size(), host_sync_ms);
     }
+    double host_launch_ms = 0.0, host_sync_ms = 0.0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sync_ev;
+    // SCN_SOLVE_TIMING=2: an event after every stream op of the loops; the
+    // time between consecutive marks (op + any idle before it) averaged per tag
+    bool marks = on && std::atoi(std::getenv("SCN_SOLVE_TIMING")) >= 2;
+    std::vector<std::pair<const char*, cudaEvent_t>> mk;
+    void report_marks() {
+      if (mk.size() < 2) return;
+      cudaDeviceSynchronize();
+      std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+      for (size_t i = 1; i < mk.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, mk[i - 1].second, mk[i].second);
+        size_t t = 0;
+        while (t < agg.size() && agg[t].first != mk[i].first) ++t;
+        if (t == agg.size()) agg.push_back({mk[i].first, {0.0, 0}});
+        agg[t].second.first += ms;
+        ++agg[t].second.second;
+      }
+      for (auto& a : agg)
+        std::fprintf(stderr, "[scn]   %-14s %4d x %8.1f us = %8.3f ms\n", a.first.c_str(), a.second.second,
+                     1e3 * a.second.first / a.second.second, a.second.first);
+      for (auto& m : mk) cudaEventDestroy(m.second);
+      mk.clear();
+    }
   } timer;
   template <class F>
   void timed(F&& f) {
@@ -230,7 +297,9 @@ struct Engine {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a, st);
+    const double h0 = now_ms();
     f();
+    timer.host_launch_ms += now_ms() - h0;  // host cost of enqueuing the sweep
     cudaEventRecord(b, st);
     timer.ev.emplace_back(a, b);
   }
@@ -307,17 +376,29 @@ struct Engine {
     for (double& a : v) a /= nn;
     SCN_CUDA(cudaMemcpy(k.v, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
     set_scalar(sl::RAYLEIGH, 0.0);
-    double rayleigh = 0.0;
-    for (int round = 0; round < max_rounds; ++round) {
-      sweep1(false, k.v, nullptr, nullptr, k.Hv);
-      if (calls) ++*calls;
-      SCN_CUDA(k_power(ctx(), k.v, k.Hv, rel_tol, st));
+    // Rounds are enqueued kBatch at a time and read once per batch: the power
+    // kernel sets a sticky stop flag at the reference's stopping round (settled,
+    // zero image or max_rounds), after which the remaining launches of the
+    // batch, sweeps included, return at once. Same rounds, same estimate.
+    const int init[3] = {0, 0, max_rounds};
+    SCN_CUDA(cudaMemcpy(k.I + il::PDONE, init, sizeof init, cudaMemcpyHostToDevice));
+    struct SkipGuard {
+      DevState& d;
+      ~SkipGuard() { d.sweep_skip = nullptr; }
+    } guard{d};
+    d.sweep_skip = k.I + il::PDONE;
+    constexpr int kBatch = 8;
+    for (int round = 0; round < max_rounds; round += kBatch) {
+      for (int b = 0; b < kBatch && round + b < max_rounds; ++b) {
+        sweep1(false, k.v, nullptr, nullptr, k.Hv);
+        SCN_CUDA(k_power(ctx(), k.v, k.Hv, rel_tol, st));
+      }
       read_scalars();
-      if (I(il::PZERO)) return 1e-12;
-      rayleigh = S(sl::PNEXT);
-      if (I(il::SETTLED)) break;
+      if (I(il::PDONE)) break;
     }
-    return std::max(rayleigh, 1e-12);
+    if (calls) *calls += static_cast<uint64_t>(I(il::PROUNDS));
+    if (I(il::PZERO)) return 1e-12;
+    return std::max(S(sl::PNEXT), 1e-12);
   }
 };
 
@@ -351,6 +432,7 @@ struct Loop {
       if (!dst.empty())
         SCN_CUDA(cudaMemcpyAsync(dst.data(), src, dst.size() * sizeof(double), cudaMemcpyDeviceToHost, e.st));
     };
+    const double f0 = now_ms();
     dev_gather_primal(e.d, e.k.x[s], e.k.u[s]);  // sharded: assemble the full point
     dl(rep.x, e.k.x[s]);
     dl(rep.u, e.k.u[s]);
@@ -358,6 +440,7 @@ struct Loop {
     dl(rep.z, e.k.z[s]);
     SCN_CUDA(cudaStreamSynchronize(e.st));
     rep.wall_ms = now_ms() - t0;
+    if (e.timer.on) std::fprintf(stderr, "[scn] finish: %.3f ms (result copies)\n", now_ms() - f0);
   }
 };
 
@@ -378,11 +461,15 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
   double lambda = resolve_lambda0(e, cfg, 0, rep);
   e.lbfgs_reset(cfg.memory);
   auto& k = e.k;
-  const size_t D = e.D();
   int cur = 0;
   e.fb_step(cur, y0dev, lambda, weight, rep.stats);
   bool grad_valid = false, have_pair = false, fresh = true;
   int iter = 0;
+  // The previous iterate and gradient of the L-BFGS pair are not copied: the
+  // previous iterate is the other state's y (overwritten only by the next
+  // certificate, after the L-BFGS kernel read it) and the gradient buffers
+  // swap roles on every accepted step.
+  double *grad = k.grad, *prev_g = k.prev_g, *prev_y = k.prev_y;
   for (;;) {
     e.read_scalars();
     const double residual = e.S(cur * sl::kStateStride + sl::RESID);
@@ -401,23 +488,35 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
       return rep;
     }
     if (!grad_valid) {  // fbe_grad (fbe.hpp:89-94)
+      e.mark("idle>grad");
       e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
+      e.mark("sweep.HR");
       ++rep.stats.hessian_vec_calls;
-      SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, k.grad, e.st));
+      SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, grad, e.st));
+      e.mark("fbe_grad");
       grad_valid = true;
     }
-    // The L-BFGS direction, its image and the certificate are enqueued before
-    // the simple rule's test (solvers.hpp:279-302) is read, so one host round
-    // trip serves both. When the rule fires, the reference clears the buffer
-    // and rebuilds the state before any of that work counts; the speculative
-    // results are simply discarded (a push made by them is undone by the clear).
-    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], k.prev_y, k.grad,
-                     k.prev_g, k.grad, k.dir, k.Sb, k.Qb, e.st));
+    // The L-BFGS direction, its image, the certificate and the FB step at the
+    // certified point are all enqueued before the simple rule's test
+    // (solvers.hpp:279-302) and the certificate's results are read; the host
+    // waits only for the published scalars while the FB step runs. When the
+    // rule fires, the reference clears the buffer and rebuilds the state
+    // before any of that work counts: the speculative results are discarded
+    // (a push made by them is undone by the clear; state nxt is rebuilt).
+    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], prev_y, grad, prev_g,
+                     grad, k.dir, k.Sb, k.Qb, e.st));
+    e.mark("lbfgs");
     e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
+    e.mark("sweep.Hd");
     const int nxt = cur ^ 1;
     SCN_CUDA(k_cert_search(e.ctx(), cur, 0, 1, k.y[cur], k.R[cur], k.Hx[cur], k.HR, k.dir, k.Hd, k.y[nxt],
                            e.st));
-    e.read_scalars();
+    e.mark("cert");
+    e.publish();
+    Stats spec;
+    e.fb_step(nxt, k.y[nxt], lambda, weight, spec);
+    e.mark("fb_step");
+    e.wait_published(false);
     if (cfg.backtracking_rule == 1) {  // simple rule (solvers.hpp:279-302)
       bool halved = false;
       for (;;) {
@@ -429,7 +528,7 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
         e.rescale(cur, lambda, weight, rep.stats);
         e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
         ++rep.stats.hessian_vec_calls;
-        SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, k.grad, e.st));
+        SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, grad, e.st));
         e.read_scalars();
         halved = true;
       }
@@ -449,7 +548,9 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     rep.stats.prox_calls += trials;
     rep.stats.conj_calls += trials;
     const double cert_fhat = e.S(sl::CERT_FHAT), hxw_rw = e.S(sl::HXW_RW), rw2 = e.S(sl::RW2);
-    e.fb_step(nxt, k.y[nxt], lambda, weight, rep.stats);
+    rep.stats.dual_grad_calls += spec.dual_grad_calls;  // the FB step at the certified point now counts
+    rep.stats.prox_calls += spec.prox_calls;
+    rep.stats.conj_calls += spec.conj_calls;
     if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:329-346)
       e.read_scalars();
       const double model = cert_fhat + lambda * hxw_rw + 0.5 * (1.0 - cfg.beta_bt) * lambda * rw2;
@@ -463,8 +564,8 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
         continue;
       }
     }
-    e.copy(k.prev_y, k.y[cur], D);
-    e.copy(k.prev_g, k.grad, D);
+    prev_y = k.y[cur];
+    std::swap(grad, prev_g);
     grad_valid = false;
     have_pair = true;
     cur = nxt;
@@ -482,11 +583,13 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
   double lambda = resolve_lambda0(e, cfg, 1, rep);
   e.lbfgs_reset(cfg.memory);
   auto& k = e.k;
-  const size_t D = e.D();
   int cur = 0;
   e.fb_step(cur, y0dev, lambda, weight, rep.stats);
   bool have_pair = false, fresh = true;
   int iter = 0;
+  // previous iterate / residual of the L-BFGS pair: the other state's y and R
+  // (intact until the next certificate and FB step, which follow the L-BFGS kernel)
+  double *prev_y = k.prev_y, *prev_res = k.prev_g;
   for (;;) {
     e.read_scalars();
     const double residual = e.S(cur * sl::kStateStride + sl::RESID);
@@ -504,8 +607,8 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
       lp.finish(1, cur, residual, lambda);
       return rep;
     }
-    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], k.prev_y, k.R[cur],
-                     k.prev_g, k.R[cur], k.dir, k.Sb, k.Qb, e.st));
+    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], prev_y, k.R[cur],
+                     prev_res, k.R[cur], k.dir, k.Sb, k.Qb, e.st));
     have_pair = false;
     // the two homogeneous images x0(r), x0(d): one 2-RHS sweep when the
     // parallel line search is on (p-NAMA), two sweeps otherwise; the
@@ -520,7 +623,12 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
     const int nxt = cur ^ 1;
     SCN_CUDA(k_cert_search(e.ctx(), cur, 1, cfg.nama_update_tlambda ? 1 : 0, k.y[cur], k.R[cur], k.Hx[cur],
                            k.HR, k.dir, k.Hd, k.y[nxt], e.st));
-    e.read_scalars();
+    // the FB step at the certified point runs while the host reads the
+    // certificate (discarded when the simple rule halves lambda)
+    e.publish();
+    Stats spec;
+    e.fb_step(nxt, k.y[nxt], lambda, weight, spec);
+    e.wait_published(false);
     if (cfg.backtracking_rule == 1) {  // simple rule (solvers.hpp:424-438)
       const bool trigger = lambda * std::sqrt(e.S(sl::HR2)) > cfg.eps_bt * std::sqrt(e.S(sl::RR2));
       if (trigger) {
@@ -543,7 +651,9 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
     rep.stats.prox_calls += trials;
     rep.stats.conj_calls += trials;
     const double cert_fhat = e.S(sl::CERT_FHAT), hxw_rw = e.S(sl::HXW_RW), rw2 = e.S(sl::RW2);
-    e.fb_step(nxt, k.y[nxt], lambda, weight, rep.stats);
+    rep.stats.dual_grad_calls += spec.dual_grad_calls;
+    rep.stats.prox_calls += spec.prox_calls;
+    rep.stats.conj_calls += spec.conj_calls;
     if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:467-483)
       e.read_scalars();
       const double model = cert_fhat + lambda * hxw_rw + 0.5 * (1.0 - cfg.beta_bt) * lambda * rw2;
@@ -556,8 +666,8 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
         continue;
       }
     }
-    e.copy(k.prev_y, k.y[cur], D);
-    e.copy(k.prev_g, k.R[cur], D);  // prev_res
+    prev_y = k.y[cur];
+    prev_res = k.R[cur];
     have_pair = true;
     cur = nxt;
     ++iter;

@@ -229,3 +229,24 @@ def test_c1_c2_small_tree_matches_oracle(gpu, kind):
     assert rep.verified and orep["verified"]
     assert np.abs(rep.x.flatten() - np.r_[orep["u"], orep["x"]]).max() <= 10 * c.eps * (
         1 + np.abs(orep["x"]).max())
+
+
+def test_lipschitz_estimate_rounds_match_oracle(gpu):
+    """estimate_dual_lipschitz (solvers.hpp:89-113): the device runs the power
+    rounds in batches with a sticky stop flag; the stopping round (and so the
+    sweep count) and the estimate must be the reference's."""
+    rng = orc.Rng(1301)
+    rounds = set()
+    for trial in range(8):
+        po, prob = fixture(rng, mixed() if trial % 2 else feasible_box(), stages=4, max_nodes=30)
+        cache = so.factor(prob)
+        est, calls = so.estimate_dual_lipschitz(cache, prob)
+        oest, ocalls = orc.Factor(po).estimate_lipschitz()
+        assert calls == ocalls, (trial, calls, ocalls)
+        assert est == pytest.approx(oest, rel=1e-9)
+        rounds.add(calls)
+    assert len(rounds) > 2  # the instances stop at different rounds (batch boundaries exercised)
+    # the solver's own count is the same rounds
+    c, oc = cfgs()
+    rep = so.solve(prob, c, "nama")
+    assert rep.lipschitz_calls == calls

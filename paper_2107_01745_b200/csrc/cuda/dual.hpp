@@ -57,7 +57,8 @@ cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, 
                         cudaStream_t st);
 // MINFBE fbe_grad epilogue (fbe.hpp:89-94): grad = R + lam HR, and the simple
 // backtracking norms ||(grad - R)/lam||^2, ||R||^2 (solvers.hpp:215-222, 279-302).
-cudaError_t k_publish(const double* S, const int* I, double* hS_mapped, int* hI_mapped, cudaStream_t st);
+cudaError_t k_publish(const double* S, const int* I, double* hS_mapped, int* hI_mapped, unsigned* seq_mapped,
+                      unsigned seq, cudaStream_t st);
 cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const double* HR, double* grad,
                        cudaStream_t st);
 // L-BFGS (lbfgs.hpp:33-62): optional push of (a - b, cc - dd) with scale_ref

@@ -668,13 +668,21 @@ cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, 
 
 // Scalar block -> mapped pinned host memory in one launch (the host waits on
 // an event instead of two D2H copies)
-__global__ void publish_kernel(const double* S, const int* I, double* hS, int* hI) {
+// A sequence number written last (after a system-scope fence) tells a host
+// spinning on the mapped word that the block is complete.
+__global__ void publish_kernel(const double* S, const int* I, double* hS, int* hI, unsigned* hseq, unsigned seq) {
   for (int t = threadIdx.x; t < sl::kScalars; t += blockDim.x) hS[t] = S[t];
   for (int t = threadIdx.x; t < il::kInts; t += blockDim.x) hI[t] = I[t];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned*>(hseq) = seq;
+  }
 }
 
-cudaError_t k_publish(const double* S, const int* I, double* hS_mapped, int* hI_mapped, cudaStream_t st) {
-  publish_kernel<<<1, 256, 0, st>>>(S, I, hS_mapped, hI_mapped);
+cudaError_t k_publish(const double* S, const int* I, double* hS_mapped, int* hI_mapped, unsigned* seq_mapped,
+                      unsigned seq, cudaStream_t st) {
+  publish_kernel<<<1, 256, 0, st>>>(S, I, hS_mapped, hI_mapped, seq_mapped, seq);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -35,6 +36,9 @@ struct scenopt_dev::Work {
   int* pI = nullptr;
   double* dpS = nullptr;
   int* dpI = nullptr;
+  unsigned* pSeq = nullptr;  // mapped: sequence number of the last completed publish
+  unsigned* dpSeq = nullptr;
+  unsigned seq = 0;
   cudaEvent_t pubEv = nullptr;
   // pinned staging words of asynchronous scalar writes; a word is reused only
   // after a stream synchronisation has retired every copy that read it
@@ -72,6 +76,7 @@ scenopt_dev::~scenopt_dev() {
     if (w->hRing) cudaFreeHost(w->hRing);
     if (w->pS) cudaFreeHost(w->pS);
     if (w->pI) cudaFreeHost(w->pI);
+    if (w->pSeq) cudaFreeHost(w->pSeq);
     if (w->pubEv) cudaEventDestroy(w->pubEv);
   }
 }
@@ -98,6 +103,9 @@ void scenopt_dev::init_solver_buffers() {
   SCN_CUDA(cudaHostAlloc(&k.pI, il::kInts * sizeof(int), cudaHostAllocMapped));
   SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpS), k.pS, 0));
   SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpI), k.pI, 0));
+  SCN_CUDA(cudaHostAlloc(&k.pSeq, sizeof(unsigned), cudaHostAllocMapped));
+  *k.pSeq = 0;
+  SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpSeq), k.pSeq, 0));
   SCN_CUDA(cudaEventCreateWithFlags(&k.pubEv, cudaEventDisableTiming));
   const size_t D = static_cast<size_t>(k.D), nxn = static_cast<size_t>(L.nx) * L.n,
                nuf = static_cast<size_t>(L.nu) * std::max(L.first_leaf, 1);
@@ -197,18 +205,26 @@ struct Engine {
       cudaEventCreate(&pub_pre);
       cudaEventRecord(pub_pre, st);
     }
-    SCN_CUDA(k_publish(k.S, k.I, k.dpS, k.dpI, st));
-    SCN_CUDA(cudaEventRecord(k.pubEv, st));
+    SCN_CUDA(k_publish(k.S, k.I, k.dpS, k.dpI, k.dpSeq, ++k.seq, st));
     mark("read.copy");
   }
+  // Spin on the mapped sequence word (no driver call, no sleep / wake-up);
+  // every 4096 polls the stream is queried so a device fault cannot hang it.
   void wait_published(bool full) {
     const double h0 = timer.on ? now_ms() : 0.0;
-    if (full) {
-      SCN_CUDA(cudaStreamSynchronize(st));
-      k.ring_next = 0;  // every staging word has been consumed
-    } else {
-      SCN_CUDA(cudaEventSynchronize(k.pubEv));
+    const volatile unsigned* seqp = k.pSeq;
+    for (unsigned spins = 1; *seqp != k.seq; ++spins) {
+      if ((spins & 4095u) == 0) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q != cudaSuccess && q != cudaErrorNotReady) SCN_CUDA(q);
+        if (q == cudaSuccess && !full && *seqp != k.seq) {  // drained without the word: fall back
+          SCN_CUDA(cudaStreamSynchronize(st));
+          break;
+        }
+      }
     }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (full) k.ring_next = 0;  // publish ran after every earlier copy: all staging words consumed
     if (timer.on) timer.host_sync_ms += now_ms() - h0;
     std::memcpy(k.hS, k.pS, sl::kScalars * sizeof(double));
     std::memcpy(k.hI, k.pI, il::kInts * sizeof(int));

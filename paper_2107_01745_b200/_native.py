@@ -152,6 +152,17 @@ def lib():
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
                 "(the scenopt_b200 hot path has no fallback implementation)")
+        if not os.environ.get("SCENOPT_NCCL_LIBRARY"):
+            # NCCL is loaded by the library on first use (sharded handles);
+            # point it at the framework's own build when one is installed, so
+            # a later `import torch` finds the libnccl.so.2 it was built against
+            import importlib.util
+            spec = importlib.util.find_spec("nvidia.nccl")
+            for loc in (spec.submodule_search_locations or []) if spec else []:
+                cand = os.path.join(loc, "lib", "libnccl.so.2")
+                if os.path.exists(cand):
+                    os.environ["SCENOPT_NCCL_LIBRARY"] = cand
+                    break
         L = C.CDLL(LIB_PATH)
         L.scenopt_last_error.restype = C.c_char_p
         if hasattr(L, "scenopt_lbfgs_gamma0"):

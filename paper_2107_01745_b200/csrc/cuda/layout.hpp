@@ -100,6 +100,10 @@ struct SweepParams {
   const double* y[kMaxRhs];
   double* x[kMaxRhs];
   double* u[kMaxRhs];
+  // optional second destination of x / u in mapped pinned host memory: the
+  // forward pass streams its results over PCIe as it computes them (host I/O)
+  double* hx[kMaxRhs];
+  double* hu[kMaxRhs];
   double* uoff[kMaxRhs];  // [first_leaf][nu] backward input offsets (the forward pass reads, never overwrites)
   double* Hx[kMaxRhs];
   double* contrib[kMaxRhs];  // [n][nu+nx] scratch

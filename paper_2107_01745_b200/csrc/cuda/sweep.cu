@@ -510,6 +510,7 @@ struct FwPhaseA {
           const double xv = acc[r] + aff;
           xbuf[(ni * NRHS + r) * nxp + j] = xv;
           P.x[r][c * nx + j] = xv;
+          if (P.hx[r]) P.hx[r][c * nx + j] = xv;
         }
       } else {
         const double h = (flat && P.affine) ? AFH[ni * mmaxh + (j - nx)] : 0.0;
@@ -547,10 +548,13 @@ struct FwPhaseB {
       const NodeMeta& mc = meta[ni];
 #pragma unroll
       for (int r = 0; r < NRHS; ++r) {
-        if (leaf)
+        if (leaf) {
           P.Hx[r][mc.tdo + j] = acc[r];
-        else
-          P.u[r][static_cast<int64_t>(mc.c) * nu + j] = UO[r * v1nu + ni * nu + j] + acc[r];
+        } else {
+          const double uv = UO[r * v1nu + ni * nu + j] + acc[r];
+          P.u[r][static_cast<int64_t>(mc.c) * nu + j] = uv;
+          if (P.hu[r]) P.hu[r][static_cast<int64_t>(mc.c) * nu + j] = uv;
+        }
       }
     }
   }
@@ -578,6 +582,7 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
       const double v = P.affine ? P.root_state[k] : 0.0;
       xbuf[r * nxp + k] = v;
       P.x[r][k] = v;
+      if (P.hx[r]) P.hx[r][k] = v;
     }
   } else {
     const FwPhaseA<NRHS> body{P,     meta, mat, PV, AF, xbuf, nx, cstride, nxp, nx + mmax, tot, cnt == 1 ? 1 : 0,
@@ -685,7 +690,10 @@ __device__ void consume_fw_small(const SweepParams& P, const Item& it, const dou
 #pragma unroll
       for (int r = 0; r < NRHS; ++r) {
         xv[r] = (lane < nx && P.affine) ? P.root_state[lane] : 0.0;
-        if (lane < nx) P.x[r][lane] = xv[r];
+        if (lane < nx) {
+          P.x[r][lane] = xv[r];
+          if (P.hx[r]) P.hx[r][lane] = xv[r];
+        }
       }
     } else {
       // phase A: x_c = [A B] [x_a; u_a] (+c), stage rows [F G] [x_a; u_a]
@@ -706,6 +714,7 @@ __device__ void consume_fw_small(const SweepParams& P, const Item& it, const dou
           for (int r = 0; r < NRHS; ++r) {
             acc[r] += aff;
             P.x[r][c * nx + lane] = acc[r];
+            if (P.hx[r]) P.hx[r][c * nx + lane] = acc[r];
           }
         } else {
 #pragma unroll
@@ -733,6 +742,7 @@ __device__ void consume_fw_small(const SweepParams& P, const Item& it, const dou
           P.Hx[r][mc.tdo + lane] = b[r];
         else
           P.u[r][c * nu + lane] = UO[r * it.v1_n * nu + ni * nu + lane] + b[r];
+          if (P.hu[r]) P.hu[r][c * nu + lane] = P.u[r][c * nu + lane];
       }
   }
 }

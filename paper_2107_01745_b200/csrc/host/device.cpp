@@ -1135,6 +1135,8 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
     P.x[r] = (x && x[r]) ? x[r] : d.xs[r];
     P.u[r] = (u && u[r]) ? u[r] : d.us[r];
     P.Hx[r] = (Hx && Hx[r]) ? Hx[r] : d.hs[r];
+    P.hx[r] = d.out_hx[r];
+    P.hu[r] = d.out_hu[r];
     P.contrib[r] = d.contrib[r];
     P.uoff[r] = d.uoff[r];
   }

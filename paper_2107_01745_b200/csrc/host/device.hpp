@@ -59,7 +59,9 @@ struct DevState {
   int cut_stage = -1;  // CTA subtree-ownership cut of the main region (-1: all global tickets)
   bool consumer_stage = false;  // teams stage their own vectors (very wide states)
   bool flat_top = false;
-  const int* sweep_skip = nullptr;  // SweepParams::skip of the next launches (power iteration batches)        // flattened forward top (one level after the backward root)
+  const int* sweep_skip = nullptr;  // SweepParams::skip of the next launches (power iteration batches)
+  double* out_hx[kMaxRhs] = {};      // SweepParams::hx / hu of the next launches (mapped host outputs)
+  double* out_hu[kMaxRhs] = {};        // flattened forward top (one level after the backward root)
   double* aff_fwh = nullptr;    // [n][max_m] constant of the flattened top's stage rows
   // node block positions in the pass arrays (doubles; -1: not on this handle)
   std::vector<int64_t> h_bw_off, h_bw_j, h_k_off, h_flat_off;

@@ -108,6 +108,26 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
     }
     return;
   }
+  // Mapped (pinned) host outputs: the forward pass writes x / u to the
+  // caller's buffers over PCIe as it computes them, overlapping the transfer
+  // with the sweep; pageable buffers take the copy after the sweep.
+  if (host && want_primal && zero_copy_ok(nrhs, x, u)) {
+    struct Reset {
+      DevState& d;
+      ~Reset() {
+        for (int r = 0; r < kMaxRhs; ++r) d.out_hx[r] = d.out_hu[r] = nullptr;
+      }
+    } reset{*d};
+    for (int r = 0; r < nrhs; ++r) {
+      d->out_hx[r] = (x && x[r]) ? mapped(x[r]) : nullptr;
+      d->out_hu[r] = (u && u[r]) ? mapped(u[r]) : nullptr;
+    }
+    dev_sweep(*d, nrhs, affine, yd, xd, ud, hd, true);
+    for (int r = 0; r < nrhs; ++r)
+      if (Hx && Hx[r]) out_copy(Hx[r], d->hs[r], static_cast<size_t>(L.dual_dim), flags);
+    sync();
+    return;
+  }
   dev_sweep(*d, nrhs, affine, yd, xd, ud, hd, want_primal);
   if (host) {
     for (int r = 0; r < nrhs; ++r) {
@@ -122,6 +142,30 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
 static int env_kb(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
+}
+
+// Device-visible address of a pinned host buffer (UVA: registered and
+// cudaHostAlloc memory is mapped), or nullptr for pageable memory.
+double* scenopt_dev::mapped(double* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? static_cast<double*>(a.devicePointer) : nullptr;
+}
+
+bool scenopt_dev::zero_copy_ok(int nrhs, double* const* x, double* const* u) {
+  static const bool off = [] {
+    const char* v = std::getenv("SCENOPT_ZERO_COPY");
+    return v && std::string(v) == "0";
+  }();
+  if (off || d->sharded()) return false;
+  for (int r = 0; r < nrhs; ++r) {
+    if (x && x[r] && !mapped(x[r])) return false;
+    if (u && u[r] && !mapped(u[r])) return false;
+  }
+  return true;
 }
 
 bool scenopt_dev::overlap_ready() {

@@ -250,3 +250,42 @@ def test_flattened_forward_top_matches_oracle_on_c3(gpu, monkeypatch, flat):
             assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL
             Hx = orc.apply_H(po, ox, ou)
             assert np.abs(h - Hx).max() <= TOL * (1 + np.abs(Hx).max())
+
+
+def test_mapped_host_outputs_are_bitwise_the_copied_ones(gpu):
+    """Pinned (mapped) host buffers: the forward pass writes x / u over PCIe
+    while it runs; pageable buffers get the copy after the sweep. Same bits,
+    1 and 2 right-hand sides, affine and homogeneous."""
+    import ctypes as C
+    import torch
+    prob = so.gen_random_instance(2, 12, 4, 6, [3, 2, 2])
+    cache = so.factor(prob)
+    dev = cache.device()
+    lib = so.lib()
+    f = prob.flat()
+    nx, nu, n, F = prob.nx, prob.nu, prob.num_nodes(), prob.first_leaf
+    P = C.POINTER(C.c_double)
+    rng = np.random.default_rng(5)
+    ys = [rng.uniform(-1, 1, prob.dual_dim) for _ in range(2)]
+
+    def ptr(a):
+        return C.cast(a.data_ptr(), P) if isinstance(a, torch.Tensor) else a.ctypes.data_as(P)
+
+    for pinned in (False, True):
+        mk = (lambda k: torch.zeros(k, dtype=torch.float64).pin_memory()) if pinned else (lambda k: np.zeros(k))
+        x1, u1 = mk(nx * n), mk(nu * F)
+        so.api.check(lib.scenopt_dual_grad(dev, ys[0].ctypes.data_as(P), ptr(x1), ptr(u1), 1))
+        X = [mk(nx * n), mk(nx * n)]
+        U = [mk(nu * F), mk(nu * F)]
+        Hs = [np.zeros(prob.dual_dim), np.zeros(prob.dual_dim)]
+        so.api.check(lib.scenopt_dev_sweep(dev, 2, 0, (P * 2)(*[y.ctypes.data_as(P) for y in ys]),
+                                           (P * 2)(*[ptr(a) for a in X]), (P * 2)(*[ptr(a) for a in U]),
+                                           (P * 2)(*[h.ctypes.data_as(P) for h in Hs]), 1))
+        res = [np.asarray(a).copy() for a in (x1, u1, *X, *U, *Hs)]
+        if not pinned:
+            ref = res
+    for a, b in zip(ref, res):
+        assert np.array_equal(a, b)
+    po = orc.Problem.from_flat(f)
+    ox, ou = orc.Factor(po).dual_grad(ys[0])
+    assert sup.rel_gap(ox, ou, res[0], res[1]) < 1e-9

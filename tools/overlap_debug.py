@@ -1,0 +1,16 @@
+"""A few host-I/O dual_grad calls with the overlap debug timeline."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2107_01745_b200 as so
+p = so.gen_random_instance(1, 50, 20, 20, [8, 8, 8, 2])
+c = so.factor(p)
+dev = c.device()
+lib = so.lib()
+y = torch.rand(p.dual_dim, dtype=torch.float64).pin_memory()
+x = torch.empty(50 * p.num_nodes(), dtype=torch.float64).pin_memory()
+u = torch.empty(20 * p.first_leaf, dtype=torch.float64).pin_memory()
+P = C.POINTER(C.c_double)
+yp, xp, up = (C.cast(t.data_ptr(), P) for t in (y, x, u))
+for _ in range(4):
+    so.api.check(lib.scenopt_dual_grad(dev, yp, xp, up, 1))

@@ -23,7 +23,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxRed = 24;  // scalars per reduction
+constexpr int kMaxRed = 32;  // scalars per reduction
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -286,6 +286,187 @@ __global__ void __launch_bounds__(kThreads) lbfgs_kernel(DualCtx c, int mem, dou
       c.S[sl::CURV + j] = curv[j];
     }
     c.S[sl::GAMMA0] = gamma0;
+  }
+}
+
+// L-BFGS direction in compact form (Byrd, Nocedal & Schnabel 1994; lbfgs.hpp
+// restated): with the pairs oldest -> newest, R = upper(S'Y), D = diag(S'Y),
+// a = S'g, b = Y'g, t = R^-1 a, u = R^-T ((D + g0 Y'Y) t - g0 b),
+//   H g = g0 g + S u - g0 Y t,     direction = -H g,
+// the same matrix as the two-loop recursion. One pass computes the new pair
+// (the curvature gate's dots), the new pair's row of S'Y and Y'Y against the
+// stored pairs, and S'g, Y'g: one grid reduction instead of 2*mem + 1. S'Y
+// and Y'Y of the stored pairs persist in Mb (slot-indexed); only the free
+// slot's row / column is written, which no block reads, so no barrier.
+constexpr int kCompactMem = 6;
+constexpr int kCompactK = 6 + 4 * kCompactMem;  // 30 <= kMaxRed
+constexpr int kMbLd = 64;                      // Mb: STY[kMbLd][kMbLd] | YTY[kMbLd][kMbLd]
+
+__global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int mem, double eps_curv, double scale_ref,
+                                                                 int do_push, const double* a, const double* b,
+                                                                 const double* cc, const double* dd, const double* gv,
+                                                                 double* out, double* Sb, double* Qb, double* Mb) {
+  int ph = 0;
+  const int64_t D = c.D;
+  __shared__ int order[kCompactMem + 1];
+  __shared__ int count_s, cnt_new, pushed_s;
+  __shared__ double coef_u[kCompactMem], coef_t[kCompactMem], gamma_s;
+  if (threadIdx.x == 0) {
+    count_s = c.I[il::LB_COUNT];
+    for (int j = 0; j <= mem; ++j) order[j] = c.I[il::LB_ORDER + j];
+  }
+  __syncthreads();
+  const int count = count_s;  // stored pairs before this call
+  const int f = order[count];  // free slot (target of a push)
+  // S'Y / Y'Y of the stored pairs (by age position), fetched in parallel now:
+  // the small solves after the reduction then read shared memory only
+  __shared__ double pSTY[kCompactMem][kCompactMem], pYTY[kCompactMem][kCompactMem];
+  __shared__ double g0_in;
+  if (threadIdx.x < kCompactMem * kCompactMem) {
+    const int i = threadIdx.x / kCompactMem, j = threadIdx.x % kCompactMem;
+    if (i < count && j < count) {
+      pSTY[i][j] = Mb[order[i] * kMbLd + order[j]];
+      pYTY[i][j] = Mb[kMbLd * kMbLd + order[i] * kMbLd + order[j]];
+    }
+  }
+  if (threadIdx.x == 64) g0_in = c.S[sl::GAMMA0];
+  // v: 0 <s,q> 1 |s|^2 2 |q|^2 3 |dd|^2 4 <s,g> 5 <q,g>; old pair j (order position):
+  //    6+j <s_j,g>, 6+M+j <y_j,g>, 6+2M+j <s_j,q>, 6+3M+j <y_j,q>   (M = kCompactMem)
+  double v[kCompactK];
+#pragma unroll
+  for (int k = 0; k < kCompactK; ++k) v[k] = 0.0;
+  const double* sj_[kCompactMem];
+  const double* yj_[kCompactMem];
+#pragma unroll
+  for (int j = 0; j < kCompactMem; ++j) {
+    sj_[j] = Sb + static_cast<int64_t>(order[j < count ? j : 0]) * D;
+    yj_[j] = Qb + static_cast<int64_t>(order[j < count ? j : 0]) * D;
+  }
+  double* sf = Sb + static_cast<int64_t>(f) * D;
+  double* qf = Qb + static_cast<int64_t>(f) * D;
+  for (int64_t i = gtid(); i < D; i += gstride()) {
+    const double gi = gv[i];
+    if (do_push) {
+      const double si = a[i] - b[i], qi = cc[i] - dd[i], di = dd[i];
+      sf[i] = si;
+      qf[i] = qi;
+      v[0] += si * qi;
+      v[1] += si * si;
+      v[2] += qi * qi;
+      v[3] += di * di;
+      v[4] += si * gi;
+      v[5] += qi * gi;
+#pragma unroll
+      for (int j = 0; j < kCompactMem; ++j)
+        if (j < count) {
+          const double sj = sj_[j][i], yj = yj_[j][i];
+          v[6 + j] += sj * gi;
+          v[6 + kCompactMem + j] += yj * gi;
+          v[6 + 2 * kCompactMem + j] += sj * qi;
+          v[6 + 3 * kCompactMem + j] += yj * qi;
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kCompactMem; ++j)
+        if (j < count) {
+          v[6 + j] += sj_[j][i] * gi;
+          v[6 + kCompactMem + j] += yj_[j][i] * gi;
+        }
+    }
+  }
+  grid_reduce<kCompactK>(c, ph, v);
+  if (threadIdx.x == 0) {  // every block: gate, pair set, small triangular solves (identical results)
+    double gamma0 = g0_in;
+    // age positions: 0..count-1 the stored pairs, count the new pair
+    int pos[kCompactMem + 1];  // active list (after the push) as age positions
+    int cnt = count, pushed = 0, first = 0;
+    if (do_push) {  // lbfgs.hpp:33-44 (strict curvature gate, FIFO eviction)
+      const double scale = scale_ref >= 0.0 ? scale_ref : v[3];
+      if ((v[0] > eps_curv * v[1] * scale) && (v[2] > 0.0)) {
+        pushed = 1;
+        gamma0 = v[0] / v[2];
+        if (cnt == mem) first = 1;  // evict the oldest
+        else ++cnt;
+        if (blockIdx.x == 0) {  // the new pair's row / column (slot f; read by no block in this launch)
+          double* STY = Mb;
+          double* YTY = Mb + kMbLd * kMbLd;
+          for (int k = 0; k < count; ++k) {
+            const int sk = order[k];
+            STY[sk * kMbLd + f] = v[6 + 2 * kCompactMem + k];  // s_k . y_new (older k)
+            YTY[sk * kMbLd + f] = v[6 + 3 * kCompactMem + k];
+            YTY[f * kMbLd + sk] = v[6 + 3 * kCompactMem + k];
+          }
+          STY[f * kMbLd + f] = v[0];
+          YTY[f * kMbLd + f] = v[2];
+          c.S[sl::CURV + f] = v[0];
+        }
+      }
+    }
+    for (int k = 0; k < cnt; ++k) pos[k] = first + k;  // the new pair (position count) is the newest
+    auto sty = [&](int pi, int pj) -> double {  // age positions, pi <= pj
+      if (pj == count) return pi == count ? v[0] : v[6 + 2 * kCompactMem + pi];
+      return pSTY[pi][pj];
+    };
+    auto yty = [&](int pi, int pj) -> double {
+      if (pi == count || pj == count) {
+        if (pi == count && pj == count) return v[2];
+        return v[6 + 3 * kCompactMem + (pi == count ? pj : pi)];
+      }
+      return pYTY[pi][pj];
+    };
+    auto ag = [&](int p) { return p == count ? v[4] : v[6 + p]; };
+    auto bg = [&](int p) { return p == count ? v[5] : v[6 + kCompactMem + p]; };
+    double t[kCompactMem], u[kCompactMem];
+    for (int i = cnt - 1; i >= 0; --i) {  // t = R^-1 a
+      double s2 = ag(pos[i]);
+      for (int j = i + 1; j < cnt; ++j) s2 -= sty(pos[i], pos[j]) * t[j];
+      t[i] = s2 / sty(pos[i], pos[i]);
+    }
+    for (int i = 0; i < cnt; ++i) {  // u = R^-T ((D + g0 Y'Y) t - g0 b)
+      double w = sty(pos[i], pos[i]) * t[i];
+      for (int j = 0; j < cnt; ++j) w += gamma0 * yty(pos[i], pos[j]) * t[j];
+      w -= gamma0 * bg(pos[i]);
+      for (int j = 0; j < i; ++j) w -= sty(pos[j], pos[i]) * u[j];
+      u[i] = w / sty(pos[i], pos[i]);
+    }
+    for (int i = 0; i < cnt; ++i) {
+      coef_u[i] = u[i];
+      coef_t[i] = t[i];
+    }
+    // slot order after the push (oldest first), spare slot last
+    int ord[kCompactMem + 1];
+    for (int k = 0; k < cnt; ++k) ord[k] = pos[k] == count ? f : order[pos[k]];
+    if (pushed && first) ord[mem] = order[0];
+    else if (!pushed) ord[cnt] = f;
+    else ord[cnt] = order[cnt];
+    for (int k = 0; k < cnt; ++k) order[k] = ord[k];
+    order[cnt] = ord[cnt];
+    cnt_new = cnt;
+    pushed_s = pushed;
+    gamma_s = gamma0;
+  }
+  __syncthreads();
+  const int cnt = cnt_new;
+  const double g0 = gamma_s;
+  const double* S_[kCompactMem];
+  const double* Y_[kCompactMem];
+#pragma unroll
+  for (int j = 0; j < kCompactMem; ++j) {
+    S_[j] = Sb + static_cast<int64_t>(order[j < cnt ? j : 0]) * D;
+    Y_[j] = Qb + static_cast<int64_t>(order[j < cnt ? j : 0]) * D;
+  }
+  for (int64_t i = gtid(); i < D; i += gstride()) {  // direction = -(g0 g + S u - g0 Y t)
+    double h = g0 * gv[i];
+#pragma unroll
+    for (int j = 0; j < kCompactMem; ++j)
+      if (j < cnt) h += coef_u[j] * S_[j][i] - g0 * coef_t[j] * Y_[j][i];
+    out[i] = -h;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c.I[il::LB_COUNT] = cnt;
+    c.I[il::LB_PUSHED] = pushed_s;
+    for (int j = 0; j <= mem; ++j) c.I[il::LB_ORDER + j] = order[j];
+    c.S[sl::GAMMA0] = g0;
   }
 }
 
@@ -695,8 +876,12 @@ cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const doubl
 
 cudaError_t k_lbfgs(const DualCtx& c, int mem, double eps_curv, double scale_ref, int do_push, const double* a,
                     const double* b, const double* cc, const double* dd, const double* gvec,
-                    double* out, double* Sbuf, double* Qbuf, cudaStream_t st) {
+                    double* out, double* Sbuf, double* Qbuf, cudaStream_t st, double* Mbuf) {
   DualCtx c2 = c;
+  if (Mbuf && mem <= kCompactMem) {
+    void* args[] = {&c2, &mem, &eps_curv, &scale_ref, &do_push, &a, &b, &cc, &dd, &gvec, &out, &Sbuf, &Qbuf, &Mbuf};
+    return coop(reinterpret_cast<const void*>(lbfgs_compact_kernel), c, args, st);
+  }
   void* args[] = {&c2, &mem, &eps_curv, &scale_ref, &do_push, &a, &b, &cc, &dd, &gvec, &out, &Sbuf, &Qbuf};
   return coop(reinterpret_cast<const void*>(lbfgs_kernel), c, args, st);
 }

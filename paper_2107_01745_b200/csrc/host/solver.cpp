@@ -52,6 +52,7 @@ struct scenopt_dev::Work {
          *HR = nullptr, *v = nullptr, *Hv = nullptr, *w = nullptr, *yp = nullptr, *weight = nullptr,
          *tmp = nullptr, *tmp2 = nullptr;
   double *Sb = nullptr, *Qb = nullptr;
+  double* Mb = nullptr;  // compact L-BFGS: S'Y and Y'Y of the stored pairs (2 x 64 x 64)
   double* small = nullptr;  // 64 doubles of API scratch
   int lb_slots = 0;
   bool fhat0_ready = false;
@@ -367,6 +368,7 @@ struct Engine {
     if (k.lb_slots < mem + 1) {
       k.Sb = d.alloc<double>(static_cast<size_t>(mem + 1) * D());
       k.Qb = d.alloc<double>(static_cast<size_t>(mem + 1) * D());
+      if (!k.Mb) k.Mb = d.alloc<double>(2 * 64 * 64);
       k.lb_slots = mem + 1;
     }
     std::vector<int> ints(il::kInts, 0);
@@ -520,7 +522,7 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     // before any of that work counts: the speculative results are discarded
     // (a push made by them is undone by the clear; state nxt is rebuilt).
     SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], prev_y, grad, prev_g,
-                     grad, k.dir, k.Sb, k.Qb, e.st));
+                     grad, k.dir, k.Sb, k.Qb, e.st, k.Mb));
     e.mark("lbfgs");
     e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
     e.mark("sweep.Hd");
@@ -624,7 +626,7 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
       return rep;
     }
     SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], prev_y, k.R[cur],
-                     prev_res, k.R[cur], k.dir, k.Sb, k.Qb, e.st));
+                     prev_res, k.R[cur], k.dir, k.Sb, k.Qb, e.st, k.Mb));
     have_pair = false;
     // the two homogeneous images x0(r), x0(d): one 2-RHS sweep when the
     // parallel line search is on (p-NAMA), two sweeps otherwise; the
@@ -799,6 +801,7 @@ struct scenopt_lbfgs {
   double eps_curv;
   DualCtx c;
   double *Sb, *Qb, *g, *out, *a, *b, *cc, *dd;
+  double* Mb;
 };
 
 // ------------------------------------------------------------------ C-ABI
@@ -1094,7 +1097,7 @@ int scenopt_lbfgs_create(scenopt_dev* h, int memory, double eps_curv, scenopt_lb
     SCN_CUDA(cudaMemcpy(b->c.I, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
     const double one = 1.0;
     SCN_CUDA(cudaMemcpy(b->c.S + sl::GAMMA0, &one, sizeof(double), cudaMemcpyHostToDevice));
-    b->Sb = b->Qb = b->g = b->out = b->a = b->b = b->cc = b->dd = nullptr;
+    b->Sb = b->Qb = b->g = b->out = b->a = b->b = b->cc = b->dd = b->Mb = nullptr;
     *out = b.release();
   });
 }
@@ -1108,6 +1111,7 @@ void lb_ensure(scenopt_lbfgs* b, int n) {
   b->c.D = n;
   b->Sb = d.alloc<double>(static_cast<size_t>(b->mem + 1) * n);
   b->Qb = d.alloc<double>(static_cast<size_t>(b->mem + 1) * n);
+  b->Mb = d.alloc<double>(2 * 64 * 64);
   for (double** p : {&b->g, &b->out, &b->a, &b->b, &b->cc, &b->dd}) *p = d.alloc<double>(n);
   SCN_CUDA(cudaMemset(b->b, 0, n * sizeof(double)));
   SCN_CUDA(cudaMemset(b->dd, 0, n * sizeof(double)));
@@ -1124,7 +1128,7 @@ int scenopt_lbfgs_push(scenopt_lbfgs* b, int n, const double* step, const double
     SCN_CUDA(cudaMemcpyAsync(b->a, step, n * sizeof(double), cudaMemcpyHostToDevice, st));
     SCN_CUDA(cudaMemcpyAsync(b->cc, change, n * sizeof(double), cudaMemcpyHostToDevice, st));
     SCN_CUDA(k_lbfgs(b->c, b->mem, b->eps_curv, scale_ref, 1, b->a, b->b, b->cc, b->dd, b->a, b->out, b->Sb,
-                     b->Qb, st));
+                     b->Qb, st, b->Mb));
     int pushed = 0;
     SCN_CUDA(cudaMemcpyAsync(&pushed, b->c.I + il::LB_PUSHED, sizeof(int), cudaMemcpyDeviceToHost, st));
     SCN_CUDA(cudaStreamSynchronize(st));
@@ -1141,7 +1145,7 @@ int scenopt_lbfgs_apply(scenopt_lbfgs* b, int n, const double* grad, double* out
     lb_ensure(b, n);
     cudaStream_t st = b->dev->stream;
     SCN_CUDA(cudaMemcpyAsync(b->g, grad, n * sizeof(double), cudaMemcpyHostToDevice, st));
-    SCN_CUDA(k_lbfgs(b->c, b->mem, b->eps_curv, -1.0, 0, nullptr, nullptr, nullptr, nullptr, b->g, b->out, b->Sb, b->Qb, st));
+    SCN_CUDA(k_lbfgs(b->c, b->mem, b->eps_curv, -1.0, 0, nullptr, nullptr, nullptr, nullptr, b->g, b->out, b->Sb, b->Qb, st, b->Mb));
     SCN_CUDA(cudaMemcpyAsync(out, b->out, n * sizeof(double), cudaMemcpyDeviceToHost, st));
     SCN_CUDA(cudaStreamSynchronize(st));
   });

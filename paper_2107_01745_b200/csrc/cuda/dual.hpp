@@ -67,7 +67,10 @@ cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const doubl
 // Mbuf (2 * 64 * 64 doubles, persistent per buffer): compact form when mem <= 6
 cudaError_t k_lbfgs(const DualCtx& c, int mem, double eps_curv, double scale_ref, int do_push, const double* a,
                     const double* b, const double* cc, const double* dd, const double* gvec,
-                    double* out, double* Sbuf, double* Qbuf, cudaStream_t st, double* Mbuf = nullptr);
+                    double* out, double* Sbuf, double* Qbuf, cudaStream_t st, double* Mbuf = nullptr,
+                    const double* fR = nullptr, const double* fHR = nullptr, int fstate = 0, double* gout = nullptr);
+// compact form (and the fused fbe_grad) applies when Mbuf is given and mem <= this
+constexpr int kLbfgsCompactMaxMem = 6;
 // Line-search certificate + speculative multi-tau search (fbe.hpp:136-231,
 // solvers.hpp:310-325 / 440-464). shifted = 0: MINFBE (anchor y); 1: NAMA
 // (anchor y - lam R, dir d + lam R). Writes y_next = T(tau*) (or

@@ -299,13 +299,18 @@ __global__ void __launch_bounds__(kThreads) lbfgs_kernel(DualCtx c, int mem, dou
 // and Y'Y of the stored pairs persist in Mb (slot-indexed); only the free
 // slot's row / column is written, which no block reads, so no barrier.
 constexpr int kCompactMem = 6;
-constexpr int kCompactK = 6 + 4 * kCompactMem;  // 30 <= kMaxRed
+constexpr int kCompactK = 6 + 4 * kCompactMem + 2;  // 32 <= kMaxRed (last two: fused fbe_grad norms)
 constexpr int kMbLd = 64;                      // Mb: STY[kMbLd][kMbLd] | YTY[kMbLd][kMbLd]
 
+// fR != nullptr: fbe_grad (fbe.hpp:89-94) fused in front: grad = R + lam HR of
+// state fstate is written to gout and used as both cc and gv; IMG2 / R2 as
+// fbe_grad_kernel computes them.
 __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int mem, double eps_curv, double scale_ref,
                                                                  int do_push, const double* a, const double* b,
                                                                  const double* cc, const double* dd, const double* gv,
-                                                                 double* out, double* Sb, double* Qb, double* Mb) {
+                                                                 double* out, double* Sb, double* Qb, double* Mb,
+                                                                 const double* fR, const double* fHR, int fstate,
+                                                                 double* gout) {
   int ph = 0;
   const int64_t D = c.D;
   __shared__ int order[kCompactMem + 1];
@@ -344,10 +349,21 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
   }
   double* sf = Sb + static_cast<int64_t>(f) * D;
   double* qf = Qb + static_cast<int64_t>(f) * D;
+  const double flam = fR ? c.S[fstate * sl::kStateStride + sl::LAM] : 0.0;
   for (int64_t i = gtid(); i < D; i += gstride()) {
-    const double gi = gv[i];
+    double gi;
+    if (fR) {
+      const double Ri = fR[i];
+      gi = Ri + flam * fHR[i];
+      gout[i] = gi;
+      const double img = (gi - Ri) / flam;
+      v[kCompactK - 2] += img * img;
+      v[kCompactK - 1] += Ri * Ri;
+    } else {
+      gi = gv[i];
+    }
     if (do_push) {
-      const double si = a[i] - b[i], qi = cc[i] - dd[i], di = dd[i];
+      const double si = a[i] - b[i], qi = (fR ? gi : cc[i]) - dd[i], di = dd[i];
       sf[i] = si;
       qf[i] = qi;
       v[0] += si * qi;
@@ -455,8 +471,9 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
     S_[j] = Sb + static_cast<int64_t>(order[j < cnt ? j : 0]) * D;
     Y_[j] = Qb + static_cast<int64_t>(order[j < cnt ? j : 0]) * D;
   }
+  const double* gvec = fR ? gout : gv;  // fused: each thread reads back its own writes
   for (int64_t i = gtid(); i < D; i += gstride()) {  // direction = -(g0 g + S u - g0 Y t)
-    double h = g0 * gv[i];
+    double h = g0 * gvec[i];
 #pragma unroll
     for (int j = 0; j < kCompactMem; ++j)
       if (j < cnt) h += coef_u[j] * S_[j][i] - g0 * coef_t[j] * Y_[j][i];
@@ -467,6 +484,10 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
     c.I[il::LB_PUSHED] = pushed_s;
     for (int j = 0; j <= mem; ++j) c.I[il::LB_ORDER + j] = order[j];
     c.S[sl::GAMMA0] = g0;
+    if (fR) {
+      c.S[sl::IMG2] = v[kCompactK - 2];
+      c.S[sl::R2] = v[kCompactK - 1];
+    }
   }
 }
 
@@ -876,10 +897,12 @@ cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const doubl
 
 cudaError_t k_lbfgs(const DualCtx& c, int mem, double eps_curv, double scale_ref, int do_push, const double* a,
                     const double* b, const double* cc, const double* dd, const double* gvec,
-                    double* out, double* Sbuf, double* Qbuf, cudaStream_t st, double* Mbuf) {
+                    double* out, double* Sbuf, double* Qbuf, cudaStream_t st, double* Mbuf, const double* fR,
+                    const double* fHR, int fstate, double* gout) {
   DualCtx c2 = c;
   if (Mbuf && mem <= kCompactMem) {
-    void* args[] = {&c2, &mem, &eps_curv, &scale_ref, &do_push, &a, &b, &cc, &dd, &gvec, &out, &Sbuf, &Qbuf, &Mbuf};
+    void* args[] = {&c2,  &mem,  &eps_curv, &scale_ref, &do_push, &a,  &b,   &cc,     &dd,  &gvec,
+                    &out, &Sbuf, &Qbuf,     &Mbuf,      &fR,      &fHR, &fstate, &gout};
     return coop(reinterpret_cast<const void*>(lbfgs_compact_kernel), c, args, st);
   }
   void* args[] = {&c2, &mem, &eps_curv, &scale_ref, &do_push, &a, &b, &cc, &dd, &gvec, &out, &Sbuf, &Qbuf};

@@ -505,12 +505,15 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
       lp.finish(1, cur, residual, lambda);
       return rep;
     }
-    if (!grad_valid) {  // fbe_grad (fbe.hpp:89-94)
+    // fbe_grad (fbe.hpp:89-94): its elementwise part and norms run inside the
+    // compact L-BFGS kernel below when that kernel is used (memory <= 6)
+    const bool fuse_grad = !grad_valid && cfg.memory <= kLbfgsCompactMaxMem;
+    if (!grad_valid) {
       e.mark("idle>grad");
       e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
       e.mark("sweep.HR");
       ++rep.stats.hessian_vec_calls;
-      SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, grad, e.st));
+      if (!fuse_grad) SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, grad, e.st));
       e.mark("fbe_grad");
       grad_valid = true;
     }
@@ -522,7 +525,7 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     // before any of that work counts: the speculative results are discarded
     // (a push made by them is undone by the clear; state nxt is rebuilt).
     SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], prev_y, grad, prev_g,
-                     grad, k.dir, k.Sb, k.Qb, e.st, k.Mb));
+                     grad, k.dir, k.Sb, k.Qb, e.st, k.Mb, fuse_grad ? k.R[cur] : nullptr, k.HR, cur, grad));
     e.mark("lbfgs");
     e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
     e.mark("sweep.Hd");

@@ -1,3 +1,4 @@
+"""Sweep timing of one shape (SHAPE=c3|c4|c5a|...); with a profiling build, per-role counters (SCN_DBG)."""
 import sys, os, ctypes as C, numpy as np
 os.environ.setdefault("SCN_DBG", "4")  # per-role counters on unless chosen
 sys.path.insert(0, '.')

@@ -507,10 +507,19 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
   const double lam = S0[sl::LAM], gp = 1.0 / lam;
   const double value = S0[sl::VALUE], fhat = S0[sl::FHAT];
   // pass 1: coefficients (fbe.hpp:136-143) and, for the shifted form, the
-  // anchor quantities (fbe.hpp:172-203)
+  // anchor quantities (fbe.hpp:172-203). In the solver path (no explicit
+  // taus) the same pass also evaluates the first batch of 8 trials and the
+  // final-pass sums and iterate for tau = 1, so when the full step is accepted
+  // (the common case) the whole search is this one pass and one reduction.
+  // Every sum keeps its own reduction tree: results are bitwise those of the
+  // separate passes.
   double s[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   // 0 <dir,Hxd> 1 |Hxd|^2 2 <Hxa, dir + lam Hxd> 3 <Hxa,dir> 4 <Hx,r> 5 <r,Hr>
   // 6 conj_a 7 |z_a|^2 8 <Hxa,res_a> 9 |res_a|^2 10 |HR|^2 11 |R|^2
+  const bool fused = ntau_explicit <= 0;
+  double fx[18];  // fused: 16 batch-0 trial sums, then <Hxw,Rw>, |Rw|^2 at tau = 1
+#pragma unroll
+  for (int q = 0; q < 18; ++q) fx[q] = 0.0;
   for (int i = gtid(); i < c.D; i += gstride()) {
     double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
     if (shifted) {
@@ -536,8 +545,44 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
     s[1] += hd * hd;
     s[2] += ha * (di + lam * hd);
     s[3] += ha * di;
+    if (fused) {
+      const double pb = an / lam + ha, ps = di / lam + hd;
+      const int kd = c.g.kind[i];
+      const double lo = c.g.lo[i], hi = c.g.hi[i], wg = c.g.wg[i];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double tau = ldexp(1.0, -q);
+        const double z = prox_row(kd, pb + tau * ps, lo, hi, gp * wg);
+        const double Rt = z - (ha + tau * hd);
+        const double Tt = (an + tau * di) - lam * Rt;
+        fx[2 * q] += conj_row(kd, Tt, lo, hi, wg);
+        fx[2 * q + 1] += z * z;
+        if (q == 0) {  // the final pass's quantities at tau = 1
+          const double hxw = ha + hd;
+          const double z1 = prox_row(kd, pb + ps, lo, hi, gp * wg);
+          const double R1 = z1 - hxw;
+          const double T1 = (an + di) - lam * R1;
+          if (y_next) y_next[i] = tlambda ? T1 : y[i] - lam * R1;
+          fx[16] += hxw * R1;
+          fx[17] += R1 * R1;
+        }
+      }
+    }
   }
-  grid_reduce<12>(c, ph, s);
+  double sv[30];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) sv[q] = s[q];
+#pragma unroll
+  for (int q = 0; q < 18; ++q) sv[12 + q] = fx[q];
+  if (fused) {
+    grid_reduce<30>(c, ph, sv);
+  } else {
+    grid_reduce<12>(c, ph, s);
+#pragma unroll
+    for (int q = 0; q < 12; ++q) sv[q] = s[q];
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) s[q] = sv[q];
   const double quad = s[0];
   const double alpha2 = -0.5 * quad - 0.5 * lam * s[1];
   const double alpha1 = -s[2];
@@ -568,6 +613,10 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
       const int kk = base + q;
       tq[q] = ntau_explicit > 0 ? (kk < ntau ? taus.t[kk < 16 ? kk : 15] : 0.0) : ldexp(1.0, -kk);
     }
+    if (fused && base == 0) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = sv[12 + q];
+    } else {
     for (int i = gtid(); i < c.D; i += gstride()) {
       double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
       if (shifted) {
@@ -592,6 +641,7 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
       }
     }
     grid_reduce<16>(c, ph, acc);
+    }
     for (int q = 0; q < 8 && base + q < ntau; ++q) {
       const double tau = tq[q];
       const double delta =
@@ -616,9 +666,14 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
     kstar = ntau - 1;
     tau_star = taus.t[ntau - 1];
   }
-  // final pass at tau*: next iterate and the original-rule probes
+  // final pass at tau*: next iterate and the original-rule probes (tau = 1
+  // came with the fused first pass)
   double f2[2] = {0, 0};
-  if (kstar >= 0) {
+  const bool have_f2 = fused && kstar == 0;
+  if (have_f2) {
+    f2[0] = sv[28];
+    f2[1] = sv[29];
+  } else if (kstar >= 0) {
     const double tau = tau_star;
     for (int i = gtid(); i < c.D; i += gstride()) {
       double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
@@ -649,7 +704,7 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
       f2[1] += Rt * Rt;
     }
   }
-  grid_reduce<2>(c, ph, f2);
+  if (!have_f2) grid_reduce<2>(c, ph, f2);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     c.S[sl::TAU] = tau_star;
     c.S[sl::KSTAR] = kstar;

@@ -82,6 +82,34 @@ T* upload(DevState& d, const std::vector<T>& h) {
   return p;
 }
 
+// Host staging array of doubles without value-initialisation (the multi-GB
+// pack buffers of large trees are zeroed in parallel where padding needs it,
+// or fully overwritten).
+struct HostArray {
+  std::unique_ptr<double[]> p;
+  size_t n = 0;
+  explicit HostArray(size_t count, bool zero) : p(new double[std::max<size_t>(count, 1)]), n(count) {
+    if (zero)
+      parallel_for(static_cast<int>((count + (1 << 20) - 1) >> 20), 1, [&](int b, int e) {
+        for (int k = b; k < e; ++k) {
+          const size_t lo = static_cast<size_t>(k) << 20, hi = std::min(count, lo + (size_t(1) << 20));
+          std::fill(p.get() + lo, p.get() + hi, 0.0);
+        }
+      });
+  }
+  double* data() { return p.get(); }
+  void release() {
+    p.reset();
+    n = 0;
+  }
+};
+
+double* upload(DevState& d, const HostArray& h) {
+  double* q = d.alloc<double>(std::max<size_t>(h.n, 1));
+  if (h.n) SCN_CUDA(cudaMemcpy(q, h.p.get(), h.n * sizeof(double), cudaMemcpyHostToDevice));
+  return q;
+}
+
 }  // namespace
 
 namespace {
@@ -622,7 +650,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
 
   clk.mark("items");
   // ---- pass arrays: [NodeMeta x count | node blocks] per item
-  std::vector<double> bw(static_cast<size_t>(bw_total), 0.0), fw(static_cast<size_t>(fw_total), 0.0);
+  HostArray bw(static_cast<size_t>(bw_total), true), fw(static_cast<size_t>(fw_total), true);
   std::vector<double> aff_bw(static_cast<size_t>(n) * W, 0.0), aff_fw(static_cast<size_t>(n) * nx, 0.0);
   // flattened forward top (host factor): x_c = a'_c + sum_i G_{c,i} u_off(a_i)
   // by the recursion x_c = CL_c x_p + B_c u_off(p) + c_c (u_p = K_p x_p + u_off(p)):
@@ -904,10 +932,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   // ---- upload
   d->bw_blk = upload(*d, bw);
   d->fw_blk = upload(*d, fw);
-  bw.clear();
-  bw.shrink_to_fit();
-  fw.clear();
-  fw.shrink_to_fit();
+  bw.release();
+  fw.release();
   d->aff_bw = upload(*d, aff_bw);
   d->aff_fw = upload(*d, aff_fw);
   d->aff_fwh = upload(*d, aff_fwh);
@@ -1046,7 +1072,7 @@ void pack_common(DevState& dd, const Problem& p, const std::vector<char>* mine) 
   for (int l = 0; l < p.L; ++l)
     if (!mine || (*mine)[p.first_leaf + l]) leaves.push_back(p.first_leaf + l);
   const size_t csz = 2 * p.sxx() + 2 * p.sxu() + p.suu() + 2 * static_cast<size_t>(nx) + nu;
-  std::vector<double> cn(std::max<size_t>(nodes.size(), 1) * csz, 0.0);
+  HostArray cn(std::max<size_t>(nodes.size(), 1) * csz, nodes.empty());  // every block fully written below
   parallel_for(static_cast<int>(nodes.size()), 256, [&](int b, int e) {
     for (int t = b; t < e; ++t) {
       const int i = nodes[t];
@@ -1062,7 +1088,7 @@ void pack_common(DevState& dd, const Problem& p, const std::vector<char>* mine) 
     }
   });
   const size_t lsz = p.sxx() + static_cast<size_t>(nx);
-  std::vector<double> cl(std::max<size_t>(leaves.size(), 1) * lsz, 0.0);
+  HostArray cl(std::max<size_t>(leaves.size(), 1) * lsz, leaves.empty());
   for (size_t t = 0; t < leaves.size(); ++t) {
     const int l = leaves[t] - p.first_leaf;
     double* o = cl.data() + t * lsz;

@@ -472,6 +472,70 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         }
         lst.swap(out);
       }
+    // The flattened items of stage cut-1 go to the CTA that owns their first
+    // child's subtree: that child's first local forward item then waits on a
+    // CTA-local retire counter instead of a cross-CTA flag, and each CTA
+    // computes exactly the parents its own subtrees need before starting its
+    // local forward (round-robin tickets delayed CTAs holding four of them).
+    if (d->flat_top && env_int("SCENOPT_FLAT_OWNER", 1) != 0) {
+      std::vector<int> owner(static_cast<size_t>(n), -1);
+      for (int gg = 0; gg < G; ++gg)
+        for (const Run& r : fw_l[gg])
+          if (r.pass == 1 && p.node_stage[r.first] == cut)
+            for (int c = r.first; c < r.first + r.count; ++c) owner[c] = gg;
+      std::vector<std::vector<Run>> moved(static_cast<size_t>(G));
+      for (int gg = 0; gg < G; ++gg) {
+        std::vector<Run> out;
+        for (const Run& r : fw_l[gg]) {
+          if (r.flat && p.node_stage[r.first] == cut - 1) {
+            const int g2 = owner[p.child_begin[r.first]];
+            moved[g2 >= 0 ? g2 : gg].push_back(r);
+          } else {
+            out.push_back(r);
+          }
+        }
+        fw_l[gg].swap(out);
+      }
+      for (int gg = 0; gg < G; ++gg) {  // rank order: after the CTA's top tickets, before its local forward
+        auto& mv = moved[gg];
+        std::sort(mv.begin(), mv.end(), [](const Run& x, const Run& y) { return x.first < y.first; });
+        auto& lst = fw_l[gg];
+        size_t pos = 0;
+        while (pos < lst.size() && p.node_stage[lst[pos].first] < cut) ++pos;
+        lst.insert(lst.begin() + static_cast<std::ptrdiff_t>(pos), mv.begin(), mv.end());
+      }
+    }
+    // Likewise the backward tickets of stage cut-1: a parent's children are
+    // consecutive cut-stage nodes, mostly of one CTA, so the parent placed on
+    // that CTA right after its local backward waits on the retire counter.
+    if (cut >= 1 && env_int("SCENOPT_BW_OWNER", 1) != 0) {
+      std::vector<int> owner(static_cast<size_t>(n), -1);
+      for (int gg = 0; gg < G; ++gg)
+        for (const Run& r : bw_l[gg])
+          if (r.pass == 0 && p.node_stage[r.first] == cut)
+            for (int c = r.first; c < r.first + r.count; ++c) owner[c] = gg;
+      std::vector<std::vector<Run>> moved(static_cast<size_t>(G));
+      for (int gg = 0; gg < G; ++gg) {
+        std::vector<Run> out;
+        for (const Run& r : bw_l[gg]) {
+          if (r.pass == 0 && p.node_stage[r.first] == cut - 1) {
+            const int g2 = owner[p.child_begin[r.first]];
+            moved[g2 >= 0 ? g2 : gg].push_back(r);
+          } else {
+            out.push_back(r);
+          }
+        }
+        bw_l[gg].swap(out);
+      }
+      for (int gg = 0; gg < G; ++gg) {  // rank order: after the local backward, before the upper tickets
+        auto& mv = moved[gg];
+        std::sort(mv.begin(), mv.end(), [](const Run& x, const Run& y) { return x.first < y.first; });
+        auto& lst = bw_l[gg];
+        size_t pos = 0;
+        while (pos < lst.size() && p.node_stage[lst[pos].first] >= cut) ++pos;
+        lst.insert(lst.begin() + static_cast<std::ptrdiff_t>(pos), mv.begin(), mv.end());
+      }
+    }
     for (int gg = 0; gg < G; ++gg) bw_l[gg].insert(bw_l[gg].end(), fw_l[gg].begin(), fw_l[gg].end());
     launch_lists.push_back(std::move(bw_l));
   } else {

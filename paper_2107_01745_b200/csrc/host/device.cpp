@@ -508,17 +508,19 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     // Likewise the backward tickets of stage cut-1: a parent's children are
     // consecutive cut-stage nodes, mostly of one CTA, so the parent placed on
     // that CTA right after its local backward waits on the retire counter.
-    if (cut >= 1 && env_int("SCENOPT_BW_OWNER", 1) != 0) {
+    // SCENOPT_BW_OWNER=2 applies the rule level by level up to the root.
+    const int bw_owner = env_int("SCENOPT_BW_OWNER", 1);
+    for (int lvl = cut - 1; lvl >= (bw_owner >= 2 ? 0 : cut - 1) && lvl >= 0 && bw_owner != 0; --lvl) {
       std::vector<int> owner(static_cast<size_t>(n), -1);
       for (int gg = 0; gg < G; ++gg)
         for (const Run& r : bw_l[gg])
-          if (r.pass == 0 && p.node_stage[r.first] == cut)
+          if (r.pass == 0 && p.node_stage[r.first] == lvl + 1)
             for (int c = r.first; c < r.first + r.count; ++c) owner[c] = gg;
       std::vector<std::vector<Run>> moved(static_cast<size_t>(G));
       for (int gg = 0; gg < G; ++gg) {
         std::vector<Run> out;
         for (const Run& r : bw_l[gg]) {
-          if (r.pass == 0 && p.node_stage[r.first] == cut - 1) {
+          if (r.pass == 0 && p.node_stage[r.first] == lvl) {
             const int g2 = owner[p.child_begin[r.first]];
             moved[g2 >= 0 ? g2 : gg].push_back(r);
           } else {
@@ -527,12 +529,12 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         }
         bw_l[gg].swap(out);
       }
-      for (int gg = 0; gg < G; ++gg) {  // rank order: after the local backward, before the upper tickets
+      for (int gg = 0; gg < G; ++gg) {  // rank order: after the deeper backward items, before the upper tickets
         auto& mv = moved[gg];
         std::sort(mv.begin(), mv.end(), [](const Run& x, const Run& y) { return x.first < y.first; });
         auto& lst = bw_l[gg];
         size_t pos = 0;
-        while (pos < lst.size() && p.node_stage[lst[pos].first] >= cut) ++pos;
+        while (pos < lst.size() && p.node_stage[lst[pos].first] > lvl) ++pos;
         lst.insert(lst.begin() + static_cast<std::ptrdiff_t>(pos), mv.begin(), mv.end());
       }
     }

@@ -40,8 +40,15 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
   double* ud[kMaxRhs] = {nullptr, nullptr};
   double* hd[kMaxRhs] = {nullptr, nullptr};
   const bool host = (flags & SCENOPT_HOST_IO) != 0;
+  static const bool mapped_y_on = [] {
+    const char* v = std::getenv("SCENOPT_MAPPED_Y");
+    return !(v && std::string(v) == "0");
+  }();
+  const bool mapped_y = host && (x || u) && mapped_y_on && !d->sharded() && zero_copy_ok(nrhs, x, u);
   for (int r = 0; r < nrhs; ++r) {
-    yd[r] = in_dual(y[r], flags, r);
+    // a pinned dual input can be read in place by the backward's staging copies
+    double* m = mapped_y && y[r] ? mapped(const_cast<double*>(y[r])) : nullptr;
+    yd[r] = m ? m : in_dual(y[r], flags, r);
     if (!host) {
       xd[r] = x ? x[r] : nullptr;
       ud[r] = u ? u[r] : nullptr;

@@ -273,12 +273,14 @@ def test_mapped_host_outputs_are_bitwise_the_copied_ones(gpu):
 
     for pinned in (False, True):
         mk = (lambda k: torch.zeros(k, dtype=torch.float64).pin_memory()) if pinned else (lambda k: np.zeros(k))
+        # pinned inputs are read in place by the sweep (no H2D copy)
+        yin = [torch.from_numpy(v).pin_memory() if pinned else v for v in ys]
         x1, u1 = mk(nx * n), mk(nu * F)
-        so.api.check(lib.scenopt_dual_grad(dev, ys[0].ctypes.data_as(P), ptr(x1), ptr(u1), 1))
+        so.api.check(lib.scenopt_dual_grad(dev, ptr(yin[0]), ptr(x1), ptr(u1), 1))
         X = [mk(nx * n), mk(nx * n)]
         U = [mk(nu * F), mk(nu * F)]
         Hs = [np.zeros(prob.dual_dim), np.zeros(prob.dual_dim)]
-        so.api.check(lib.scenopt_dev_sweep(dev, 2, 0, (P * 2)(*[y.ctypes.data_as(P) for y in ys]),
+        so.api.check(lib.scenopt_dev_sweep(dev, 2, 0, (P * 2)(*[ptr(v) for v in yin]),
                                            (P * 2)(*[ptr(a) for a in X]), (P * 2)(*[ptr(a) for a in U]),
                                            (P * 2)(*[h.ctypes.data_as(P) for h in Hs]), 1))
         res = [np.asarray(a).copy() for a in (x1, u1, *X, *U, *Hs)]

@@ -473,7 +473,7 @@ __device__ void consume_backward(const SweepParams& P, const Item& it, const dou
 // ---------------------------------------------------------------- forward
 // tree_oracles.hpp:75-88 + apply_H, phase A: [x_c; z_c] = W_c' [x_a; u_a]
 // (+[c_c; 0]) for non-root c.
-template <int NRHS>
+template <int NRHS, bool HOST = false>
 struct FwPhaseA {
   const SweepParams& P;
   const NodeMeta* meta;
@@ -510,7 +510,8 @@ struct FwPhaseA {
           const double xv = acc[r] + aff;
           xbuf[(ni * NRHS + r) * nxp + j] = xv;
           P.x[r][c * nx + j] = xv;
-          if (P.hx[r]) P.hx[r][c * nx + j] = xv;
+          if constexpr (!HOST)
+            if (P.hx[r]) P.hx[r][c * nx + j] = xv;  // host-output kernels write whole rows instead
         }
       } else {
         const double h = (flat && P.affine) ? AFH[ni * mmaxh + (j - nx)] : 0.0;
@@ -560,7 +561,7 @@ struct FwPhaseB {
   }
 };
 
-template <int NRHS>
+template <int NRHS, bool HOST = false>
 __device__ void consume_forward(const SweepParams& P, const Item& it, const double* slot, const double* mat,
                                 const double* st, double* xbuf, int ttid, int team, int mmax,
                                 int mNmax, long long* trace_row) {
@@ -585,8 +586,8 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
       if (P.hx[r]) P.hx[r][k] = v;
     }
   } else {
-    const FwPhaseA<NRHS> body{P,     meta, mat, PV, AF, xbuf, nx, cstride, nxp, nx + mmax, tot, cnt == 1 ? 1 : 0,
-                              flat ? 1 : 0, AF + cnt * nx, P.mmax};
+    const FwPhaseA<NRHS, HOST> body{P,    meta, mat, PV, AF, xbuf, nx, cstride, nxp, nx + mmax, tot,
+                                    cnt == 1 ? 1 : 0, flat ? 1 : 0, AF + cnt * nx, P.mmax};
     for_tasks(cnt * (nx + mmax), ttid, body);
   }
   if (ttid == 0) PROF_T1(11);
@@ -594,6 +595,25 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   team_sync(team);
   if (ttid == 0) PROF_T1(12);
   TRACE_IN(4);
+  // mapped host output (host I/O): the item's x rows leave shared memory as
+  // whole 16-byte stores (full PCIe write transactions), alongside phase B
+  if constexpr (HOST)
+  if (!root && (P.hx[0] || (NRHS > 1 && P.hx[NRHS - 1]))) {
+    if ((nx & 1) == 0) {
+      const int n2 = nx >> 1;
+      for (int idx = ttid; idx < NRHS * cnt * n2; idx += kTeam) {
+        const int r = idx / (cnt * n2), rem = idx - r * cnt * n2, ni = rem / n2, k = rem - ni * n2;
+        if (P.hx[r])
+          reinterpret_cast<double2*>(P.hx[r] + static_cast<int64_t>(meta[ni].c) * nx)[k] =
+              *reinterpret_cast<const double2*>(xbuf + (ni * NRHS + r) * nxp + 2 * k);
+      }
+    } else {
+      for (int idx = ttid; idx < NRHS * cnt * nx; idx += kTeam) {
+        const int r = idx / (cnt * nx), rem = idx - r * cnt * nx, ni = rem / nx, k = rem - ni * nx;
+        if (P.hx[r]) P.hx[r][static_cast<int64_t>(meta[ni].c) * nx + k] = xbuf[(ni * NRHS + r) * nxp + k];
+      }
+    }
+  }
   const FwPhaseB<NRHS> body{P, meta, mat, UO, xbuf, nx, nu, cstride, nxp, leaf ? mNmax : nu, it.v1_n * nu,
                             leaf ? 1 : 0, root ? 1 : 0, cnt == 1 ? 1 : 0};
   for_tasks(cnt * (leaf ? mNmax : nu), ttid, body);
@@ -751,6 +771,9 @@ __device__ void consume_fw_small(const SweepParams& P, const Item& it, const dou
 // kernel carries no fallback code): kModeConsumerStage = teams stage their own
 // vectors; kModeGlobalBlocks = some items read their node blocks from HBM.
 constexpr int kModeConsumerStage = 1, kModeGlobalBlocks = 2, kModeSmallNodes = 4;
+// kModeHostOut: forward x rows to mapped host memory as 16-byte row stores
+// (only instantiated for the default layout; other layouts store per element)
+constexpr int kModeHostOut = 8;
 template <int NRHS, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P, int mmax, int mNmax) {
   extern __shared__ __align__(128) double smem[];
@@ -903,9 +926,11 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
           consume_backward<NRHS>(P, it, slot, slot, st, tbuf, ttid, team, trace_row);
       } else {
         if ((MODE & kModeGlobalBlocks) && gblocks)
-          consume_forward<NRHS>(P, it, slot, gmat, st, tbuf, ttid, team, mmax, mNmax, trace_row);
+          consume_forward<NRHS, (MODE & kModeHostOut) != 0>(P, it, slot, gmat, st, tbuf, ttid, team, mmax, mNmax,
+                                                          trace_row);
         else
-          consume_forward<NRHS>(P, it, slot, slot, st, tbuf, ttid, team, mmax, mNmax, trace_row);
+          consume_forward<NRHS, (MODE & kModeHostOut) != 0>(P, it, slot, slot, st, tbuf, ttid, team, mmax, mNmax,
+                                                          trace_row);
       }
       TRACE(5);
       LC_MARK(2);  // compute (phases A + barrier + B)
@@ -1037,9 +1062,11 @@ int sweep_threads() { return kThreads; }
 int sweep_teams() { return kTeams; }
 namespace {
 #define SCN_K(R, M) reinterpret_cast<const void*>(sweep_kernel<R, M>)
-const void* const kKernels[2][8] = {
+const void* const kKernels[3][8] = {
     {SCN_K(1, 0), SCN_K(1, 1), SCN_K(1, 2), SCN_K(1, 3), SCN_K(1, 4), SCN_K(1, 5), SCN_K(1, 6), SCN_K(1, 7)},
-    {SCN_K(2, 0), SCN_K(2, 1), SCN_K(2, 2), SCN_K(2, 3), SCN_K(2, 4), SCN_K(2, 5), SCN_K(2, 6), SCN_K(2, 7)}};
+    {SCN_K(2, 0), SCN_K(2, 1), SCN_K(2, 2), SCN_K(2, 3), SCN_K(2, 4), SCN_K(2, 5), SCN_K(2, 6), SCN_K(2, 7)},
+    // host-output variants of the default layout (row [nrhs-1]); the rest of the row repeats them
+    {SCN_K(1, 8), SCN_K(2, 8), SCN_K(1, 8), SCN_K(2, 8), SCN_K(1, 8), SCN_K(2, 8), SCN_K(1, 8), SCN_K(2, 8)}};
 #undef SCN_K
 }  // namespace
 
@@ -1139,7 +1166,8 @@ cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mm
 #endif
   const int mode = (P.consumer_stage ? kModeConsumerStage : 0) | (P.global_blocks ? kModeGlobalBlocks : 0) |
                    (P.small_nodes ? kModeSmallNodes : 0);
-  const void* fn = kKernels[P.nrhs == 2 ? 1 : 0][mode];
+  const bool host_out = P.hx[0] || (P.nrhs == 2 && P.hx[1]);
+  const void* fn = (host_out && mode == 0) ? kKernels[2][P.nrhs == 2 ? 1 : 0] : kKernels[P.nrhs == 2 ? 1 : 0][mode];
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, dyn_smem, stream);
 }
 

@@ -710,8 +710,20 @@ Report solve_gpad(Engine& e, const scenopt_solver_config& cfg, const double* y0d
   int cur = 0;
   e.fb_step(cur, y0dev, lambda, weight, rep.stats);
   int iter = 0;
+  // The next extrapolation and FB step are enqueued before the host reads the
+  // current residual (the GPU keeps working during the read); they are
+  // discarded when the loop stops, and counted only when it continues.
   for (;;) {
-    e.read_scalars();
+    e.publish();
+    const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
+    const int nxt = cur ^ 1;
+    Stats spec;
+    const bool more = iter < cfg.max_iters;
+    if (more) {
+      SCN_CUDA(k_extrapolate(e.ctx(), k.T[cur], k.yp, k.w, (t - 1.0) / t_next, e.st));
+      e.fb_step(nxt, k.w, lambda, weight, spec);
+    }
+    e.wait_published(false);
     const double residual = e.S(cur * sl::kStateStride + sl::RESID);
     lp.push_trace(cur);
     if (residual <= cfg.eps) {
@@ -719,16 +731,15 @@ Report solve_gpad(Engine& e, const scenopt_solver_config& cfg, const double* y0d
       lp.finish(0, cur, residual, lambda);
       return rep;
     }
-    if (iter >= cfg.max_iters) {
+    if (!more) {
       rep.iterations = iter;
       lp.finish(1, cur, residual, lambda);
       return rep;
     }
-    const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));
-    SCN_CUDA(k_extrapolate(e.ctx(), k.T[cur], k.yp, k.w, (t - 1.0) / t_next, e.st));
+    rep.stats.dual_grad_calls += spec.dual_grad_calls;
+    rep.stats.prox_calls += spec.prox_calls;
+    rep.stats.conj_calls += spec.conj_calls;
     t = t_next;
-    const int nxt = cur ^ 1;
-    e.fb_step(nxt, k.w, lambda, weight, rep.stats);
     cur = nxt;
     ++iter;
   }

@@ -181,6 +181,43 @@ TEST_CASE("spring-mass ZOH, free particles and parameter checks (test_generators
   CHECK(sa.size() == 10 && (sa - sb).lpNormInf() == 0.0 && sa.segment(5, 5).lpNormInf() <= 2.5);
 }
 
+TEST_CASE("problem files: canonical round trip, shared fields, hashes (test_io.cpp)", true) {
+  const std::string chain = R"json({
+  "schema": "scenopt-problem-v1", "dims": {"nx": 2, "nu": 1}, "root_state": [0.25, -0.5],
+  "tree": {"stage": [0, 1, 2], "ancestor": [-1, 0, 1], "probability": [1.0, 1.0, 1.0]},
+  "dynamics": {"A": [[0.9, 0.1], [0.0, 0.8]], "B": [[0.5], [1.0]], "c": [0.0, 0.0]},
+  "cost": {"Q": [[1.0, 0.0], [0.0, 1.0]], "R": [[1.0]], "S": [[0.0, 0.0]], "q": [0.0, 0.0], "r": [0.0]},
+  "constraints": {"F": [[1.0, 0.0]], "G": [[1.0]], "kind": "box", "zmin": [[-1.0], [-2.0]],
+                  "zmax": [[1.0], [2.0]], "gamma": 0.0},
+  "terminal_cost": {"P": [[1.0, 0.0], [0.0, 1.0]], "p": [0.0, 0.0]},
+  "terminal_constraints": {"F": [[0.0, 1.0]], "kind": "box", "zmin": [-1.0], "zmax": [1.0], "gamma": 0.0}})json";
+  const auto prob = scenopt::parse_problem(chain);
+  REQUIRE(prob.num_nodes() == 3 && prob.tree.num_leaves() == 1);
+  CHECK(prob.root_state(0) == 0.25 && prob.dyn[1].A(0, 0) == 0.9 && prob.dyn[2].A(0, 1) == 0.1);
+  CHECK(prob.con[1].g.zmin(0) == -1.0 && prob.con[2].g.zmax(0) == 2.0);
+  CHECK(scenopt::validate(prob).empty());
+  for (const auto& p : {small(7), scenopt::gen_spring_mass(3, [] {
+                          scenopt::SpringMassParams par;
+                          par.horizon = 3;
+                          return par;
+                        }())}) {
+    const std::string first = scenopt::serialize_problem(p);
+    CHECK(scenopt::serialize_problem(scenopt::parse_problem(first)) == first);
+  }
+  CHECK_THROWS_AS(scenopt::parse_problem("not json at all"), scenopt::ParseError);
+  CHECK(!scenopt::validate_problem_text("{\"schema\": 3}").empty());
+  CHECK(scenopt::validate_problem_text(chain).empty());
+  const auto base = small(5);
+  auto moved = base;
+  moved.root_state = Vec::Constant(base.nx, 0.01);
+  CHECK(scenopt::content_hash(moved) != scenopt::content_hash(base));
+  CHECK(scenopt::factor_hash(moved) == scenopt::factor_hash(base));
+  auto redyn = base;
+  redyn.dyn[1].A(0, 0) += 0.125;
+  CHECK(scenopt::factor_hash(redyn) != scenopt::factor_hash(base));
+  CHECK(scenopt::content_hash(base) == scenopt::content_hash(small(5)));
+}
+
 TEST_CASE("validate reports broken instances", true) {
   auto prob = small(8);
   prob.tree.probability[1] = 0.9;  // children no longer sum to the parent
@@ -419,6 +456,27 @@ TEST_CASE("factor_device and refactor_affine (receding horizon)", false) {
   CHECK(max_abs(c2.segment(prob.tree.first_leaf() * prob.nu, prob.nx) - prob2.root_state) < 1e-14);
   cache.load_matrices(prob2);
   CHECK(static_cast<int>(cache.gain.size()) == prob.tree.first_leaf());
+}
+
+TEST_CASE("run_experiment: rows, pinned csv header, byte-stable reports (test_experiment.cpp)", false) {
+  std::vector<scenopt::BatchEntry> batch;
+  for (int k = 0; k < 3; ++k) batch.push_back({"r" + std::to_string(k + 1), small(static_cast<uint64_t>(k + 1))});
+  scenopt::ExperimentConfig cfg;
+  cfg.include_timing = false;
+  const auto a = scenopt::run_experiment(batch, scenopt::default_solver_set(), cfg);
+  const auto b = scenopt::run_experiment(batch, scenopt::default_solver_set(), cfg);
+  REQUIRE(a.rows.size() == 9);
+  for (const auto& r : a.rows) {
+    CHECK(r.converged && r.error.empty());
+    if (r.solver != "gpad") CHECK(r.fbe_monotone);  // GPAD records the envelope too, not monotone (solvers.hpp:518)
+  }
+  const std::string csv = a.csv();
+  CHECK(csv.substr(0, csv.find('\n')) == scenopt::kResultsCsvHeader);
+  CHECK(csv == b.csv() && a.traces_csv() == b.traces_csv() && a.summary_json() == b.summary_json());
+  const auto sums = a.summaries();
+  REQUIRE(sums.size() == 3);
+  CHECK(sums[0].solver == "minfbe" && sums[0].count == 3 && sums[0].converged == 3);
+  CHECK_THROWS_AS(scenopt::solver_spec_from_name("bfgs"), scenopt::InvalidParams);
 }
 
 int main(int argc, char** argv) {

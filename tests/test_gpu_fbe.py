@@ -163,6 +163,30 @@ def test_lbfgs_two_loop_matches_dense_bfgs(gpu):
             assert np.abs(buf.apply_direction(g) - expected).max() < 1e-11 * (1 + np.abs(expected).max())
 
 
+@pytest.mark.parametrize("memory", [1, 6, 7, 9])
+def test_lbfgs_direction_both_kernels_match_dense_bfgs(gpu, memory):
+    """memory <= 6: compact-form kernel; above: the two-loop kernel. Both are
+    the dense BFGS inverse of the stored pairs, with and without eviction."""
+    rng = orc.Rng(84 + memory)
+    prob = so.gen_random_instance(1, 3, 2, 2, 2)
+    cache = so.factor(prob)
+    dim = 14
+    buf = so.LbfgsBuffer(memory, 1e-12, cache)
+    root = rng.matrix(dim, dim)
+    spd = root @ root.T + 0.5 * np.eye(dim)
+    accepted = []
+    for k in range(memory + 3):
+        step = rng.vector(dim)
+        change = spd @ step
+        assert buf.push(step, change, 1.0)
+        accepted = (accepted + [(step, change)])[-memory:]
+        s_, q_ = accepted[-1]
+        inv = sup.dense_bfgs_inverse(accepted, dim, s_ @ q_ / (q_ @ q_))
+        g = rng.vector(dim)
+        expected = -(inv @ g)
+        assert np.abs(buf.apply_direction(g) - expected).max() < 1e-11 * (1 + np.abs(expected).max())
+
+
 def test_lbfgs_gate_is_strict_and_clear_resets(gpu):
     prob = so.gen_random_instance(1, 3, 2, 2, 2)
     cache = so.factor(prob)

@@ -11,6 +11,7 @@
 // step, power-iteration stop) are taken on the device without a host round
 // trip.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <cmath>
 #include <cstdint>
@@ -955,7 +956,11 @@ cudaError_t k_lbfgs(const DualCtx& c, int mem, double eps_curv, double scale_ref
                     double* out, double* Sbuf, double* Qbuf, cudaStream_t st, double* Mbuf, const double* fR,
                     const double* fHR, int fstate, double* gout) {
   DualCtx c2 = c;
-  if (Mbuf && mem <= kCompactMem) {
+  static const bool compact_on = [] {
+    const char* v = std::getenv("SCENOPT_LBFGS_COMPACT");
+    return !(v && v[0] == '0');
+  }();
+  if (Mbuf && mem <= kCompactMem && compact_on) {
     void* args[] = {&c2,  &mem,  &eps_curv, &scale_ref, &do_push, &a,  &b,   &cc,     &dd,  &gvec,
                     &out, &Sbuf, &Qbuf,     &Mbuf,      &fR,      &fHR, &fstate, &gout};
     return coop(reinterpret_cast<const void*>(lbfgs_compact_kernel), c, args, st);

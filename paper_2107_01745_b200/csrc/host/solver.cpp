@@ -507,7 +507,11 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     }
     // fbe_grad (fbe.hpp:89-94): its elementwise part and norms run inside the
     // compact L-BFGS kernel below when that kernel is used (memory <= 6)
-    const bool fuse_grad = !grad_valid && cfg.memory <= kLbfgsCompactMaxMem;
+    static const bool compact_on = [] {
+      const char* v = std::getenv("SCENOPT_LBFGS_COMPACT");
+      return !(v && v[0] == '0');
+    }();
+    const bool fuse_grad = !grad_valid && cfg.memory <= kLbfgsCompactMaxMem && compact_on;
     if (!grad_valid) {
       e.mark("idle>grad");
       e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);

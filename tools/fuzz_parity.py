@@ -12,6 +12,9 @@ from tests import support as sup
 
 trials = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 rng = orc.Rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
+max_nodes = int(sys.argv[3]) if len(sys.argv) > 3 else 400  # >= ~600 per stage exercises the subtree cut
+solves = (sys.argv[4] != "0") if len(sys.argv) > 4 else True
+cuts = {}
 worst = {"dual_grad": 0.0, "hessian_vec": 0.0, "two_rhs": 0.0}
 fails, iters_off = [], 0
 t0 = time.time()
@@ -21,10 +24,21 @@ for t in range(trials):
     opt = orc.InstanceOptions(with_box=True, with_l1=rng.integer(0, 1) == 1, with_none=rng.integer(0, 1) == 1,
                               affine=rng.integer(0, 3) > 0, feasible_boxes=True,
                               stage_rows_lo=rng.integer(0, 1), stage_rows_hi=rng.integer(1, 4))
-    po = rng.random_instance(stages, rng.integer(2, 400), nx, nu, opt)
-    prob = so.ProblemInstance.from_flat(po.flat())
+    if max_nodes > 0:
+        po = rng.random_instance(stages, rng.integer(2, max_nodes), nx, nu, opt)
+        prob = so.ProblemInstance.from_flat(po.flat())
+    else:  # full-branching trees with stages of 500-5000 nodes: the subtree cut, flat top, owners
+        depth = rng.integer(2, 5)
+        br = [rng.integer(3, 9) for _ in range(depth)]
+        br[0] = rng.integer(3, 40)  # wide first stages put the cut at stage 2 or 3
+        horizon = depth + rng.integer(0, 4)
+        prob = so.gen_random_instance(rng.integer(1, 10 ** 6), nx, nu, horizon, br)
+        po = orc.Problem.from_flat(prob.flat())
     ofac = orc.Factor(po)
     cache = so.factor(prob)
+    info = cache.dev_info()
+    key = (info["cut_stage"], info["flat_top"])
+    cuts[key] = cuts.get(key, 0) + 1
     y = rng.vector(prob.dual_dim, 1.0)
     r = rng.vector(prob.dual_dim, 1.0)
     try:
@@ -42,7 +56,7 @@ for t in range(trials):
             worst[k] = max(worst[k], g)
             if not g < 1e-9:
                 fails.append((t, k, g, stages, nx, nu, prob.num_nodes()))
-        if t % 3 == 0:
+        if solves and t % 3 == 0:
             for kind, code in (("minfbe", 0), ("nama", 1), ("gpad", 2)):
                 rep = so.solve(prob, so.SolverConfig(eps=1e-5), kind)
                 orep = orc.solve(po, orc.SolverConfig(eps=1e-5), code)
@@ -60,6 +74,7 @@ for t in range(trials):
     except Exception as e:  # noqa: BLE001 - report and continue
         fails.append((t, "exception", repr(e)[:200], stages, nx, nu))
 print(f"{trials} trials in {time.time() - t0:.0f} s; worst rel gaps {worst}; solves off by one: {iters_off}")
+print("(cut stage, flat top) -> trees:", cuts)
 print("failures:", len(fails))
 for f in fails[:20]:
     print("  ", f)

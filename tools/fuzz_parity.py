@@ -14,6 +14,7 @@ trials = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 rng = orc.Rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
 max_nodes = int(sys.argv[3]) if len(sys.argv) > 3 else 400  # >= ~600 per stage exercises the subtree cut
 solves = (sys.argv[4] != "0") if len(sys.argv) > 4 else True
+device_factor = len(sys.argv) > 5 and sys.argv[5] == "dev"  # factor on the GPU (K9 + flattened-top maps)
 cuts = {}
 worst = {"dual_grad": 0.0, "hessian_vec": 0.0, "two_rhs": 0.0}
 fails, iters_off = [], 0
@@ -35,7 +36,7 @@ for t in range(trials):
         prob = so.gen_random_instance(rng.integer(1, 10 ** 6), nx, nu, horizon, br)
         po = orc.Problem.from_flat(prob.flat())
     ofac = orc.Factor(po)
-    cache = so.factor(prob)
+    cache = so.factor_device(prob) if device_factor else so.factor(prob)
     info = cache.dev_info()
     key = (info["cut_stage"], info["flat_top"])
     cuts[key] = cuts.get(key, 0) + 1

@@ -9,7 +9,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2107_01745_b200 as so
 from paper_2107_01745_b200 import _native as N
-shapes = {"c3": (50, 20, 20, [8, 8, 8, 2]), "c4": (50, 20, 20, [8, 8, 8, 8, 4])}
+shapes = {"c3": (50, 20, 20, [8, 8, 8, 2]), "c4": (50, 20, 20, [8, 8, 8, 8, 4]), "c1": (10, 5, 10, [2, 2, 2]), "c5_1k": (10, 5, 20, [2] * 6)}
 nx, nu, H, br = shapes[sys.argv[1] if len(sys.argv) > 1 else "c3"]
 p = so.gen_random_instance(1, nx, nu, H, br)
 c = so.factor(p)

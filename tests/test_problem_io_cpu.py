@@ -222,3 +222,33 @@ def test_treebench_cli_generates_and_validates(tmp_path):
     assert r.returncode == 1 and "schema must be" in r.stderr
     assert subprocess.run([exe, "frobnicate"], capture_output=True).returncode == 2
     assert subprocess.run([exe, "gen", "random"], capture_output=True).returncode == 2  # --out required
+
+
+def test_json_reader_edge_cases():
+    """The in-house reader (csrc/host/json.cpp): escapes, number forms, whitespace,
+    duplicate keys (the last wins, as std::map assignment), and malformed input."""
+    base = json.loads(CHAIN_FILE)
+    text = json.dumps(base)
+    # whitespace and key order do not matter; unicode escapes in strings are decoded
+    spaced = text.replace(":", " :\n\t").replace(",", " ,\r\n ")
+    assert so.serialize_problem(so.parse_problem(spaced)) == so.serialize_problem(so.parse_problem(text))
+    doc = dict(base)
+    doc["constraints"] = dict(base["constraints"], kind="\\u0062ox")  # "box" spelled with an escape
+    assert so.parse_problem(json.dumps(doc).replace("\\\\u0062", "\\u0062")).flat()["g_kind"][1] == 1
+    # number forms: exponents, negative zero, integers where doubles are expected
+    doc = json.loads(CHAIN_FILE)
+    doc["root_state"] = [2.5e-1, -5E-1]
+    doc["dims"] = {"nx": 2, "nu": 1.0}  # dims accept numbers
+    t = json.dumps(doc).replace("0.25", "2.5e-1")
+    assert list(so.parse_problem(t).flat()["root_state"]) == [0.25, -0.5]
+    # duplicate keys: the last one is used
+    dup = text[:-1] + ', "root_state": [1.0, 2.0]}'
+    assert list(so.parse_problem(dup).flat()["root_state"]) == [1.0, 2.0]
+    # malformed documents name a byte position
+    for bad in ('{"schema": "scenopt-problem-v1",}', '{"a": [1, 2,]}', '{"a": 01}', '{"a": "x\\q"}',
+                '{"a": .5}', '{"a": tru}', '["unterminated]', '{"a": 1} trailing', '', '   '):
+        with pytest.raises(so.ParseError, match="not valid JSON"):
+            so.parse_problem(bad)
+    # deep nesting is bounded, not a stack overflow
+    with pytest.raises(so.ParseError):
+        so.parse_problem("[" * 100000)

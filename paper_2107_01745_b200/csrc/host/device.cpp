@@ -455,18 +455,10 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   std::vector<Lists> launch_lists;
   std::vector<std::pair<int, int>> full(static_cast<size_t>(p.N) + 1);
   for (int t = 0; t <= p.N; ++t) full[t] = {p.stage_offsets[t], p.stage_offsets[t + 1]};
-  if (!shard) {
-    Lists bw_l, fw_l;
-    d->cut_stage = region(0, p.N, full, true, true, true, bw_l, fw_l);
-    // Flattened forward top (DESIGN.md §3.1): with a host factor and a cut at
-    // stage 2..4, every node above the cut computes x / u / Hx in one level
-    // from its ancestors' u_off (affine maps precomputed below) as soon as the
-    // backward root is done, instead of a chain of per-stage dependencies.
-    const int cut = d->cut_stage;
-    d->flat_top = cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0 &&
-                  env_int("SCENOPT_SMALL_NODES", 0) == 0;
-    if (d->flat_top)
-      for (auto& lst : fw_l) {
+  // Flattened forward top, and the owner rules (stage cut-1 items on the CTA
+  // owning their first child); shared by the single-launch and sharded schedules.
+  auto mark_flat = [&](Lists& fw_l, int cut) {
+    for (auto& lst : fw_l) {
         std::vector<Run> out;
         for (const Run& r : lst) {
           const int st = p.node_stage[r.first];
@@ -488,6 +480,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         }
         lst.swap(out);
       }
+  };
+  auto owner_fw = [&](Lists& fw_l, int cut) {
     // The flattened items of stage cut-1 go to the CTA that owns their first
     // child's subtree: that child's first local forward item then waits on a
     // CTA-local retire counter instead of a cross-CTA flag, and each CTA
@@ -521,6 +515,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         lst.insert(lst.begin() + static_cast<std::ptrdiff_t>(pos), mv.begin(), mv.end());
       }
     }
+  };
+  auto owner_bw = [&](Lists& bw_l, int cut) {
     // Likewise the backward tickets of stage cut-1: a parent's children are
     // consecutive cut-stage nodes, mostly of one CTA, so the parent placed on
     // that CTA right after its local backward waits on the retire counter.
@@ -554,6 +550,22 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         lst.insert(lst.begin() + static_cast<std::ptrdiff_t>(pos), mv.begin(), mv.end());
       }
     }
+  };
+  if (!shard) {
+    Lists bw_l, fw_l;
+    d->cut_stage = region(0, p.N, full, true, true, true, bw_l, fw_l);
+    // Flattened forward top (DESIGN.md §3.1): with a host factor and a cut at
+    // stage 2..4, every node above the cut computes x / u / Hx in one level
+    // from its ancestors' u_off (affine maps precomputed below) as soon as the
+    // backward root is done, instead of a chain of per-stage dependencies.
+    const int cut = d->cut_stage;
+    d->flat_top = cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0 &&
+                  env_int("SCENOPT_SMALL_NODES", 0) == 0;
+    if (d->flat_top) {
+      mark_flat(fw_l, cut);
+      owner_fw(fw_l, cut);
+    }
+    owner_bw(bw_l, cut);
     for (int gg = 0; gg < G; ++gg) bw_l[gg].insert(bw_l[gg].end(), fw_l[gg].begin(), fw_l[gg].end());
     launch_lists.push_back(std::move(bw_l));
   } else {
@@ -568,9 +580,19 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     const auto own = descend(d->shard_lo, d->shard_hi, s, p.N);
     Lists a_bw, a_fw, t_bw, t_fw, o_bw, o_fw;
     d->cut_stage = region(s, p.N, own, true, true, false, a_bw, a_fw);
+    const int cut = d->cut_stage;
+    if (env_int("SCENOPT_SHARD_OWNER", 1) != 0) owner_bw(a_bw, cut);
     launch_lists.push_back(std::move(a_bw));
     region(0, s - 1, full, false, true, true, t_bw, t_fw);
     region(s, p.N, own, true, false, true, o_bw, o_fw);
+    // launch B: every flattened node waits on the (replicated) backward root
+    d->flat_top = cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0 &&
+                  env_int("SCENOPT_SHARD_FLAT", 1) != 0 && env_int("SCENOPT_SMALL_NODES", 0) == 0;
+    if (d->flat_top) {
+      mark_flat(t_fw, cut);
+      mark_flat(o_fw, cut);
+      owner_fw(o_fw, cut);
+    }
     for (int gg = 0; gg < G; ++gg) {
       t_bw[gg].insert(t_bw[gg].end(), t_fw[gg].begin(), t_fw[gg].end());
       t_bw[gg].insert(t_bw[gg].end(), o_fw[gg].begin(), o_fw[gg].end());

@@ -578,6 +578,37 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     d->sstage_hi = p.stage_offsets[s + 1];
     d->dual_top = p.dual_offset[p.stage_offsets[s]];
     const auto own = descend(d->shard_lo, d->shard_hi, s, p.N);
+    {
+      auto add = [](std::vector<std::pair<int64_t, int64_t>>& v, int64_t a, int64_t b) {
+        if (b <= a) return;
+        if (!v.empty() && v.back().second == a)
+          v.back().second = b;
+        else
+          v.push_back({a, b});
+      };
+      auto rows = [&](int a, int b) {  // stage rows of nodes [a, b), and terminal rows of leaves
+        if (b <= a) return;
+        add(d->zero_x, static_cast<int64_t>(a) * nx, static_cast<int64_t>(b) * nx);
+        if (a < p.first_leaf)
+          add(d->zero_u, static_cast<int64_t>(a) * nu, static_cast<int64_t>(std::min(b, p.first_leaf)) * nu);
+        add(d->zero_hx, p.dual_offset[a], p.dual_offset[b - 1] + p.stage_rows[b - 1]);
+      };
+      for (int t = s; t <= p.N; ++t) {
+        const int lo = p.stage_offsets[t], hi = p.stage_offsets[t + 1];
+        const int olo = own[t].first < own[t].second ? own[t].first : hi, ohi = own[t].first < own[t].second ? own[t].second : hi;
+        rows(lo, olo);
+        rows(ohi, hi);
+      }
+      auto trows = [&](int a, int b) {
+        if (b > a)
+          add(d->zero_hx, p.tdual_offset[a - p.first_leaf],
+              p.tdual_offset[b - 1 - p.first_leaf] + p.terminal_rows[b - 1 - p.first_leaf]);
+      };
+      const int lo = p.stage_offsets[p.N], hi = p.stage_offsets[p.N + 1];
+      const bool any = own[p.N].first < own[p.N].second;
+      trows(lo, any ? own[p.N].first : hi);
+      if (any) trows(own[p.N].second, hi);
+    }
     Lists a_bw, a_fw, t_bw, t_fw, o_bw, o_fw;
     d->cut_stage = region(s, p.N, own, true, true, false, a_bw, a_fw);
     const int cut = d->cut_stage;
@@ -1285,11 +1316,16 @@ void phase_a(DevState& d, SweepParams& P, bool gather_primal) {
   const Layout& L = d.lay;
   const int W = L.nx + L.nu;
   const size_t ns = static_cast<size_t>(d.sstage_hi - d.sstage_lo);
+  // only the rows of other ranks' subtrees: this rank's launches write the rest
+  auto zero = [&](double* v, const std::vector<std::pair<int64_t, int64_t>>& rg) {
+    for (const auto& q : rg)
+      SCN_CUDA(cudaMemsetAsync(v + q.first, 0, sizeof(double) * (q.second - q.first), d.stream));
+  };
   for (int r = 0; r < P.nrhs; ++r) {
-    SCN_CUDA(cudaMemsetAsync(P.Hx[r], 0, sizeof(double) * L.dual_dim, d.stream));
+    zero(P.Hx[r], d.zero_hx);
     if (gather_primal) {
-      SCN_CUDA(cudaMemsetAsync(P.x[r], 0, sizeof(double) * L.nx * L.n, d.stream));
-      SCN_CUDA(cudaMemsetAsync(P.u[r], 0, sizeof(double) * L.nu * L.first_leaf, d.stream));
+      zero(P.x[r], d.zero_x);
+      zero(P.u[r], d.zero_u);
     }
   }
   launch(d, P, d.launches[0]);

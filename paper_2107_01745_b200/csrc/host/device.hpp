@@ -92,6 +92,9 @@ struct DevState {
   int sstage_lo = 0, sstage_hi = 0;  // all shard-stage nodes [stage_offsets[s], stage_offsets[s+1])
   int64_t dual_top = 0;          // dual rows of the replicated top stages (a prefix)
   double* xbuf = nullptr;        // exchange buffer: shard-stage contributions, kMaxRhs x ns x (nu+nx)
+  // [begin, end) element ranges of x / u / Hx that no launch of this rank
+  // writes (other ranks' subtrees), zeroed before the sweep's allreduces
+  std::vector<std::pair<int64_t, int64_t>> zero_x, zero_u, zero_hx;
   bool sharded() const { return shard_stage >= 0; }
   unsigned *ctrl = nullptr, *bw_flag = nullptr, *fw_flag = nullptr;
   int64_t bw_doubles = 0, fw_doubles = 0;

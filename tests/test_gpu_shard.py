@@ -128,6 +128,7 @@ def test_emulated_ranks_reassemble_the_unsharded_sweep(gpu, monkeypatch, world, 
             for rk in ranks:
                 for k in range(nrhs):
                     rk.put(rk.y[k], ys[k])
+                    rk.put(rk.h[k], np.full(prob.dual_dim, np.nan))  # rows nobody zeroes or writes show up
                 rk.phase(0, nrhs, affine)
             total = sum(rk.get(rk.xbuf, nrhs * rk.nx) for rk in ranks)
             for rk in ranks:

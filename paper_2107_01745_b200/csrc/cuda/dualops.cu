@@ -392,7 +392,15 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
     }
   }
   grid_reduce<kCompactK>(c, ph, v);
+  // the serial part indexes the totals at run time: from shared memory, so
+  // that v stays in registers through the accumulation above
+  __shared__ double vs[kCompactK];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k2 = 0; k2 < kCompactK; ++k2) vs[k2] = v[k2];
+  }
   if (threadIdx.x == 0) {  // every block: gate, pair set, small triangular solves (identical results)
+    const double* v = vs;
     double gamma0 = g0_in;
     // age positions: 0..count-1 the stored pairs, count the new pair
     int pos[kCompactMem + 1];  // active list (after the push) as age positions
@@ -496,6 +504,15 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
 struct Taus {
   double t[16];
 };
+// taus.t[k] by unrolled select: a run-time index into a kernel parameter
+// would copy the whole array to local memory in every thread
+__device__ __forceinline__ double tau_at(const Taus& taus, int k) {
+  double t = taus.t[15];
+#pragma unroll
+  for (int m = 0; m < 16; ++m)
+    if (m == k) t = taus.t[m];
+  return t;
+}
 
 __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int shifted, int tlambda,
                                                         const double* y, const double* R, const double* Hx,
@@ -612,7 +629,7 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int kk = base + q;
-      tq[q] = ntau_explicit > 0 ? (kk < ntau ? taus.t[kk < 16 ? kk : 15] : 0.0) : ldexp(1.0, -kk);
+      tq[q] = ntau_explicit > 0 ? (kk < ntau ? tau_at(taus, kk) : 0.0) : ldexp(1.0, -kk);
     }
     if (fused && base == 0) {
 #pragma unroll
@@ -665,7 +682,7 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
   }
   if (ntau_explicit > 0) {  // vectors of the last tau (test path)
     kstar = ntau - 1;
-    tau_star = taus.t[ntau - 1];
+    tau_star = tau_at(taus, ntau - 1);
   }
   // final pass at tau*: next iterate and the original-rule probes (tau = 1
   // came with the fused first pass)

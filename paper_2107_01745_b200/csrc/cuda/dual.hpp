@@ -20,6 +20,10 @@ constexpr int TAU = 40, KSTAR = 41, STALL = 42, CERT_FHAT = 43, HXW_RW = 44, RW2
               CONJ_A = 47, ZN2_A = 48, FHAT_A = 49, ALPHA1 = 50, ALPHA2 = 51, HR2 = 52, RR2 = 53,
               DELTA = 54;
 constexpr int EVALF = 56, EVALF_INF = 57, RED0 = 58, RED1 = 59;  // API reductions
+// fb_finish's skip word I[CONV] for a speculative MINFBE sweep: 1 when the
+// step met the stop tolerance or the backtracking rule in S[GATE_RULE]
+// (0 original, 1 simple) would reject it (solvers.hpp:279-302, 329-346)
+constexpr int EPS_STOP = 60, GATE_RULE = 61, BETA_BT = 62, EPS_BT = 63;
 constexpr int CURV = 64;  // L-BFGS curvatures [64, 64 + mem + 1)
 constexpr int kScalars = 192;
 }  // namespace sl
@@ -27,6 +31,7 @@ constexpr int kScalars = 192;
 namespace il {
 constexpr int LB_COUNT = 0, LB_PUSHED = 1, SETTLED = 2, PZERO = 3;
 constexpr int PDONE = 4, PROUNDS = 5, PMAX = 6;  // batched power iteration: sticky stop flag, rounds run, cap
+constexpr int CONV = 7;  // last fb_finish met the stop tolerance: skip word of a speculative sweep
 constexpr int LB_ORDER = 8;  // [8, 8 + mem + 1): slot ids, oldest first, then free slots
 constexpr int kInts = 128;
 }  // namespace il

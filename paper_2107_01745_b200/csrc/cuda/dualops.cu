@@ -147,6 +147,19 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
     S[sl::ZN2] = s[1];
     S[sl::VALUE] = fhat + s[0] + lam * s[2] + 0.5 * lam * s[3];
     S[sl::RESID] = m[0];
+    // skip word of a speculative sweep after this step (the host reads it
+    // with the step's scalars and re-sweeps if it skipped an accepted step)
+    int skip = m[0] <= c.S[sl::EPS_STOP] ? 1 : 0;
+    const int rule = static_cast<int>(c.S[sl::GATE_RULE]);
+    if (rule == 0) {  // original rule: candidate fhat above the model
+      const double model = __dadd_rn(__dadd_rn(c.S[sl::CERT_FHAT], __dmul_rn(lam, c.S[sl::HXW_RW])),
+                                     __dmul_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(1.0, -c.S[sl::BETA_BT])), lam),
+                                               c.S[sl::RW2]));
+      if (fhat > model) skip = 1;
+    } else if (rule == 1) {  // simple rule: lambda |img| > eps_bt |R| halves lambda
+      if (__dmul_rn(lam, sqrt(c.S[sl::IMG2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::R2]))) skip = 1;
+    }
+    c.I[il::CONV] = skip;
   }
 }
 

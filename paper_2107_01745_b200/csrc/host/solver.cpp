@@ -323,6 +323,18 @@ struct Engine {
   void sweep1(bool affine, const double* y, double* x, double* u, double* Hx) {
     timed([&] { dev_sweep(d, 1, affine, &y, x ? &x : nullptr, u ? &u : nullptr, &Hx); });
   }
+  // H x0(r) launched only if the last fb_finish missed the stop tolerance
+  // (I[CONV], see k_fb_finish): a speculative sweep costs a launch at convergence
+  void sweep1_unless_converged(const double* r, double* Hr) {
+    d.sweep_skip = k.I + il::CONV;
+    try {
+      sweep1(false, r, nullptr, nullptr, Hr);
+    } catch (...) {
+      d.sweep_skip = nullptr;
+      throw;
+    }
+    d.sweep_skip = nullptr;
+  }
   void sweep2(const double* a, const double* b, double* Ha, double* Hb) {
     const double* ys[2] = {a, b};
     double* hs[2] = {Ha, Hb};
@@ -488,8 +500,22 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
   // certificate, after the L-BFGS kernel read it) and the gradient buffers
   // swap roles on every accepted step.
   double *grad = k.grad, *prev_g = k.prev_g, *prev_y = k.prev_y;
+  // Speculative FBE-gradient sweep: after an FB step at the certified point
+  // the next iteration's H x0(R) is enqueued before the host has read the
+  // step's results (skipped on the device when the step converged), so the
+  // host decides while it runs. A rejected step (lambda halving) discards it.
+  static const bool spec_on = [] {
+    const char* v = std::getenv("SCENOPT_SPEC_HR");
+    return !(v && v[0] == '0');
+  }();
+  e.set_scalar(sl::EPS_STOP, cfg.eps);
+  e.set_scalar(sl::GATE_RULE, cfg.backtracking_rule);
+  e.set_scalar(sl::BETA_BT, cfg.beta_bt);
+  e.set_scalar(sl::EPS_BT, cfg.eps_bt);
+  bool scalars_fresh = false, hr_ready = false;
   for (;;) {
-    e.read_scalars();
+    if (!scalars_fresh) e.read_scalars();
+    scalars_fresh = false;
     const double residual = e.S(cur * sl::kStateStride + sl::RESID);
     if (fresh) {
       lp.push_trace(cur);
@@ -514,7 +540,8 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     const bool fuse_grad = !grad_valid && cfg.memory <= kLbfgsCompactMaxMem && compact_on;
     if (!grad_valid) {
       e.mark("idle>grad");
-      e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
+      if (!hr_ready) e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
+      hr_ready = false;
       e.mark("sweep.HR");
       ++rep.stats.hessian_vec_calls;
       if (!fuse_grad) SCN_CUDA(k_fbe_grad(e.ctx(), cur, k.R[cur], k.HR, grad, e.st));
@@ -537,11 +564,18 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     SCN_CUDA(k_cert_search(e.ctx(), cur, 0, 1, k.y[cur], k.R[cur], k.Hx[cur], k.HR, k.dir, k.Hd, k.y[nxt],
                            e.st));
     e.mark("cert");
-    e.publish();
     Stats spec;
+    const bool spec_hr = spec_on && iter + 1 < cfg.max_iters;
+    if (!spec_hr) e.publish();
     e.fb_step(nxt, k.y[nxt], lambda, weight, spec);
     e.mark("fb_step");
-    e.wait_published(false);
+    if (spec_hr) {
+      e.publish();  // certificate and FB-step scalars; the host reads them while HR runs
+      e.sweep1_unless_converged(k.R[nxt], k.HR);
+      e.wait_published(true);
+    } else {
+      e.wait_published(false);
+    }
     if (cfg.backtracking_rule == 1) {  // simple rule (solvers.hpp:279-302)
       bool halved = false;
       for (;;) {
@@ -577,7 +611,7 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     rep.stats.prox_calls += spec.prox_calls;
     rep.stats.conj_calls += spec.conj_calls;
     if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:329-346)
-      e.read_scalars();
+      if (!spec_hr) e.read_scalars();
       const double model = cert_fhat + lambda * hxw_rw + 0.5 * (1.0 - cfg.beta_bt) * lambda * rw2;
       if (e.S(nxt * sl::kStateStride + sl::FHAT) > model) {
         lambda = halve_lambda(lambda);
@@ -596,6 +630,8 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     cur = nxt;
     ++iter;
     fresh = true;
+    hr_ready = spec_hr && e.I(il::CONV) == 0;  // H x0(R) of the new iterate is in flight
+    scalars_fresh = spec_hr;   // and its scalars were read after its FB step
   }
 }
 

@@ -22,7 +22,8 @@ constexpr int TAU = 40, KSTAR = 41, STALL = 42, CERT_FHAT = 43, HXW_RW = 44, RW2
 constexpr int EVALF = 56, EVALF_INF = 57, RED0 = 58, RED1 = 59;  // API reductions
 // fb_finish's skip word I[CONV] for a speculative MINFBE sweep: 1 when the
 // step met the stop tolerance or the backtracking rule in S[GATE_RULE]
-// (0 original, 1 simple) would reject it (solvers.hpp:279-302, 329-346)
+// (0 original, 1 MINFBE simple, 3 NAMA simple; 2 none) would reject it
+// (solvers.hpp:279-302, 329-346, 424-438, 467-483)
 constexpr int EPS_STOP = 60, GATE_RULE = 61, BETA_BT = 62, EPS_BT = 63;
 constexpr int CURV = 64;  // L-BFGS curvatures [64, 64 + mem + 1)
 constexpr int kScalars = 192;
@@ -52,6 +53,7 @@ struct DualCtx {
   int* I;          // int block
   double* part;    // partial sums [2][64][nblk]
   unsigned* bar;   // grid barrier {count, generation}
+  const int* skip = nullptr;  // L-BFGS kernels: non-null and *skip != 0 -> return at once (speculation)
 };
 
 // fb_step / rescale_state finish (fbe.hpp:38-67). mode 0: fhat from the

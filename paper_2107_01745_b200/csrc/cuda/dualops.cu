@@ -156,8 +156,10 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
                                      __dmul_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(1.0, -c.S[sl::BETA_BT])), lam),
                                                c.S[sl::RW2]));
       if (fhat > model) skip = 1;
-    } else if (rule == 1) {  // simple rule: lambda |img| > eps_bt |R| halves lambda
+    } else if (rule == 1) {  // MINFBE simple rule: lambda |img| > eps_bt |R| halves lambda
       if (__dmul_rn(lam, sqrt(c.S[sl::IMG2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::R2]))) skip = 1;
+    } else if (rule == 3) {  // NAMA simple rule on the certificate's norms
+      if (__dmul_rn(lam, sqrt(c.S[sl::HR2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::RR2]))) skip = 1;
     }
     c.I[il::CONV] = skip;
   }
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(kThreads) lbfgs_kernel(DualCtx c, int mem, dou
                                                          const double* a, const double* b, const double* cc,
                                                          const double* dd, const double* gv, double* out,
                                                          double* Sb, double* Qb) {
+  if (c.skip && *reinterpret_cast<const volatile int*>(c.skip)) return;  // speculative launch, not needed
   int ph = 0;
   const int64_t D = c.D;
   __shared__ int order[64];
@@ -325,6 +328,7 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
                                                                  double* out, double* Sb, double* Qb, double* Mb,
                                                                  const double* fR, const double* fHR, int fstate,
                                                                  double* gout) {
+  if (c.skip && *reinterpret_cast<const volatile int*>(c.skip)) return;  // speculative launch, not needed
   int ph = 0;
   const int64_t D = c.D;
   __shared__ int order[kCompactMem + 1];

@@ -325,15 +325,21 @@ struct Engine {
   }
   // H x0(r) launched only if the last fb_finish missed the stop tolerance
   // (I[CONV], see k_fb_finish): a speculative sweep costs a launch at convergence
+  struct SkipScope {  // sweeps launched in scope return at once when I[CONV] != 0
+    DevState& d;
+    SkipScope(DevState& dd, const int* w) : d(dd) { d.sweep_skip = w; }
+    ~SkipScope() { d.sweep_skip = nullptr; }
+  };
   void sweep1_unless_converged(const double* r, double* Hr) {
-    d.sweep_skip = k.I + il::CONV;
-    try {
-      sweep1(false, r, nullptr, nullptr, Hr);
-    } catch (...) {
-      d.sweep_skip = nullptr;
-      throw;
-    }
-    d.sweep_skip = nullptr;
+    SkipScope g(d, k.I + il::CONV);
+    sweep1(false, r, nullptr, nullptr, Hr);
+  }
+  // the GATE_RULE code of fb_finish's skip word for solver kind (0 MINFBE, 1 NAMA)
+  void set_gate(const scenopt_solver_config& cfg, int kind) {
+    set_scalar(sl::EPS_STOP, cfg.eps);
+    set_scalar(sl::GATE_RULE, cfg.backtracking_rule == 1 && kind == 1 ? 3 : cfg.backtracking_rule);
+    set_scalar(sl::BETA_BT, cfg.beta_bt);
+    set_scalar(sl::EPS_BT, cfg.eps_bt);
   }
   void sweep2(const double* a, const double* b, double* Ha, double* Hb) {
     const double* ys[2] = {a, b};
@@ -482,6 +488,15 @@ double resolve_lambda0(Engine& e, const scenopt_solver_config& cfg, int kind, Re
   return (fixed ? 0.95 : 0.9) / rep.lipschitz_estimate;
 }
 
+// Speculative next-iteration sweeps in MINFBE / NAMA (SCENOPT_SPEC_HR=0 disables)
+bool spec_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("SCENOPT_SPEC_HR");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 // solve_minfbe, solvers.hpp:234-356
 Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y0dev, const double* weight) {
   validate_config(cfg);
@@ -504,14 +519,7 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
   // the next iteration's H x0(R) is enqueued before the host has read the
   // step's results (skipped on the device when the step converged), so the
   // host decides while it runs. A rejected step (lambda halving) discards it.
-  static const bool spec_on = [] {
-    const char* v = std::getenv("SCENOPT_SPEC_HR");
-    return !(v && v[0] == '0');
-  }();
-  e.set_scalar(sl::EPS_STOP, cfg.eps);
-  e.set_scalar(sl::GATE_RULE, cfg.backtracking_rule);
-  e.set_scalar(sl::BETA_BT, cfg.beta_bt);
-  e.set_scalar(sl::EPS_BT, cfg.eps_bt);
+  e.set_gate(cfg, 0);
   bool scalars_fresh = false, hr_ready = false;
   for (;;) {
     if (!scalars_fresh) e.read_scalars();
@@ -565,7 +573,7 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
                            e.st));
     e.mark("cert");
     Stats spec;
-    const bool spec_hr = spec_on && iter + 1 < cfg.max_iters;
+    const bool spec_hr = spec_on() && iter + 1 < cfg.max_iters;
     if (!spec_hr) e.publish();
     e.fb_step(nxt, k.y[nxt], lambda, weight, spec);
     e.mark("fb_step");
@@ -651,8 +659,15 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
   // previous iterate / residual of the L-BFGS pair: the other state's y and R
   // (intact until the next certificate and FB step, which follow the L-BFGS kernel)
   double *prev_y = k.prev_y, *prev_res = k.prev_g;
+  // As in MINFBE: after the FB step at the certified point, the next
+  // iteration's L-BFGS direction and its two homogeneous images are enqueued
+  // before the host reads the step, gated by fb_finish's skip word; a rejected
+  // step clears the L-BFGS buffer, which undoes the speculative push.
+  e.set_gate(cfg, 1);
+  bool scalars_fresh = false, next_ready = false;
   for (;;) {
-    e.read_scalars();
+    if (!scalars_fresh) e.read_scalars();
+    scalars_fresh = false;
     const double residual = e.S(cur * sl::kStateStride + sl::RESID);
     if (fresh) {
       lp.push_trace(cur);
@@ -668,28 +683,42 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
       lp.finish(1, cur, residual, lambda);
       return rep;
     }
-    SCN_CUDA(k_lbfgs(e.ctx(), cfg.memory, cfg.eps_curv, -1.0, have_pair ? 1 : 0, k.y[cur], prev_y, k.R[cur],
-                     prev_res, k.R[cur], k.dir, k.Sb, k.Qb, e.st, k.Mb));
+    // the L-BFGS direction, then the two homogeneous images x0(r), x0(d): one
+    // 2-RHS sweep when the parallel line search is on (p-NAMA), two sweeps
+    // otherwise; the arithmetic is identical either way (solvers.hpp:410-422)
+    auto direction_and_images = [&](DualCtx c, int s, int push, const double* py, const double* pr) {
+      SCN_CUDA(k_lbfgs(c, cfg.memory, cfg.eps_curv, -1.0, push, k.y[s], py, k.R[s], pr, k.R[s], k.dir, k.Sb,
+                       k.Qb, e.st, k.Mb));
+      if (cfg.nama_parallel_linesearch)
+        e.sweep2(k.R[s], k.dir, k.HR, k.Hd);
+      else {
+        e.sweep1(false, k.R[s], nullptr, nullptr, k.HR);
+        e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
+      }
+    };
+    if (!next_ready) direction_and_images(e.ctx(), cur, have_pair ? 1 : 0, prev_y, prev_res);
+    next_ready = false;
     have_pair = false;
-    // the two homogeneous images x0(r), x0(d): one 2-RHS sweep when the
-    // parallel line search is on (p-NAMA), two sweeps otherwise; the
-    // arithmetic is identical either way (solvers.hpp:410-422)
-    if (cfg.nama_parallel_linesearch)
-      e.sweep2(k.R[cur], k.dir, k.HR, k.Hd);
-    else {
-      e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
-      e.sweep1(false, k.dir, nullptr, nullptr, k.Hd);
-    }
     rep.stats.hessian_vec_calls += 2;
     const int nxt = cur ^ 1;
     SCN_CUDA(k_cert_search(e.ctx(), cur, 1, cfg.nama_update_tlambda ? 1 : 0, k.y[cur], k.R[cur], k.Hx[cur],
                            k.HR, k.dir, k.Hd, k.y[nxt], e.st));
     // the FB step at the certified point runs while the host reads the
     // certificate (discarded when the simple rule halves lambda)
-    e.publish();
+    const bool spec_next = spec_on() && iter + 1 < cfg.max_iters;
+    if (!spec_next) e.publish();
     Stats spec;
     e.fb_step(nxt, k.y[nxt], lambda, weight, spec);
-    e.wait_published(false);
+    if (spec_next) {
+      e.publish();
+      DualCtx cs = e.ctx();
+      cs.skip = k.I + il::CONV;
+      Engine::SkipScope g(e.d, k.I + il::CONV);
+      direction_and_images(cs, nxt, 1, k.y[cur], k.R[cur]);
+      e.wait_published(true);
+    } else {
+      e.wait_published(false);
+    }
     if (cfg.backtracking_rule == 1) {  // simple rule (solvers.hpp:424-438)
       const bool trigger = lambda * std::sqrt(e.S(sl::HR2)) > cfg.eps_bt * std::sqrt(e.S(sl::RR2));
       if (trigger) {
@@ -716,7 +745,7 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
     rep.stats.prox_calls += spec.prox_calls;
     rep.stats.conj_calls += spec.conj_calls;
     if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:467-483)
-      e.read_scalars();
+      if (!spec_next) e.read_scalars();
       const double model = cert_fhat + lambda * hxw_rw + 0.5 * (1.0 - cfg.beta_bt) * lambda * rw2;
       if (e.S(nxt * sl::kStateStride + sl::FHAT) > model) {
         lambda = halve_lambda(lambda);
@@ -733,6 +762,8 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
     cur = nxt;
     ++iter;
     fresh = true;
+    next_ready = spec_next && e.I(il::CONV) == 0;  // direction and images of the new iterate in flight
+    scalars_fresh = spec_next;
   }
 }
 

@@ -16,6 +16,7 @@
 #include <limits>
 #include <random>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "capi_internal.hpp"
@@ -146,6 +147,34 @@ struct Report {  // SolverReport, solvers.hpp:66-84
   double verify_subdiff_dist = std::numeric_limits<double>::infinity();
   std::vector<double> residual_trace, fbe_trace, x, u, y, z;
 };
+
+// Result arrays of destroyed reports, kept resident for the next solve's
+// download: a fresh 10.5 MB std::vector costs ~2.7 ms of page faults and
+// zero-fill on the host at C3, inside wall_ms; a recycled one costs nothing.
+namespace {
+std::mutex g_arrays_mu;
+std::vector<std::vector<double>> g_arrays;
+constexpr size_t kArraysKept = 16, kArrayMinBytes = 1 << 16;
+void array_take(std::vector<double>& dst, size_t n) {
+  {
+    std::lock_guard<std::mutex> lk(g_arrays_mu);
+    size_t best = g_arrays.size();
+    for (size_t i = 0; i < g_arrays.size(); ++i)  // the smallest that fits
+      if (g_arrays[i].capacity() >= n && (best == g_arrays.size() || g_arrays[i].capacity() < g_arrays[best].capacity()))
+        best = i;
+    if (best < g_arrays.size()) {
+      dst.swap(g_arrays[best]);
+      g_arrays.erase(g_arrays.begin() + static_cast<std::ptrdiff_t>(best));
+    }
+  }
+  dst.resize(n);  // every element is overwritten by the download
+}
+void array_give(std::vector<double>& v) {
+  if (v.capacity() * sizeof(double) < kArrayMinBytes) return;
+  std::lock_guard<std::mutex> lk(g_arrays_mu);
+  if (g_arrays.size() < kArraysKept) g_arrays.push_back(std::move(v));
+}
+}  // namespace
 
 // solvers.hpp:48-60
 void validate_config(const scenopt_solver_config& c) {
@@ -460,10 +489,10 @@ struct Loop {
     rep.residual_inf = residual;
     rep.lambda_final = lambda;
     const Layout& L = e.d.lay;
-    rep.x.resize(static_cast<size_t>(L.nx) * L.n);
-    rep.u.resize(static_cast<size_t>(L.nu) * L.first_leaf);
-    rep.y.resize(static_cast<size_t>(L.dual_dim));
-    rep.z.resize(static_cast<size_t>(L.dual_dim));
+    array_take(rep.x, static_cast<size_t>(L.nx) * L.n);
+    array_take(rep.u, static_cast<size_t>(L.nu) * L.first_leaf);
+    array_take(rep.y, static_cast<size_t>(L.dual_dim));
+    array_take(rep.z, static_cast<size_t>(L.dual_dim));
     auto dl = [&](std::vector<double>& dst, const double* src) {
       if (!dst.empty())
         SCN_CUDA(cudaMemcpyAsync(dst.data(), src, dst.size() * sizeof(double), cudaMemcpyDeviceToHost, e.st));
@@ -1144,7 +1173,11 @@ int scenopt_report_arrays(const scenopt_report* rr, double* x, double* u, double
   });
 }
 
-void scenopt_report_destroy(scenopt_report* r) { delete r; }
+void scenopt_report_destroy(scenopt_report* r) {
+  if (r)
+    for (auto* v : {&r->r.x, &r->r.u, &r->r.y, &r->r.z}) array_give(*v);
+  delete r;
+}
 
 // ------------------------------------------------------------------ L-BFGS handle (lbfgs.hpp)
 int scenopt_lbfgs_create(scenopt_dev* h, int memory, double eps_curv, scenopt_lbfgs** out) {

@@ -50,8 +50,9 @@ __device__ void grid_sync(unsigned* bar) {
 }
 
 // Deterministic grid reduction of K per-thread values (sum, or max when
-// MAX). Every thread of every block receives the totals in v.
-template <int K, bool MAX = false>
+// MAX; values from index MAXFROM on are max-reduced, the rest summed). Every
+// thread of every block receives the totals in v.
+template <int K, bool MAX = false, int MAXFROM = (MAX ? 0 : K)>
 __device__ void grid_reduce(const DualCtx& c, int& ph, double (&v)[K]) {
   __shared__ double sh[kWarps][kMaxRed];
   __shared__ double tot[kMaxRed];
@@ -59,17 +60,19 @@ __device__ void grid_reduce(const DualCtx& c, int& ph, double (&v)[K]) {
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     double t = v[k];
+    const bool mx = k >= MAXFROM;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double u = __shfl_xor_sync(0xffffffffu, t, o);
-      t = MAX ? fmax(t, u) : t + u;
+      t = mx ? fmax(t, u) : t + u;
     }
     if (lane == 0) sh[warp][k] = t;
   }
   __syncthreads();
   if (threadIdx.x < K) {
+    const bool mx = static_cast<int>(threadIdx.x) >= MAXFROM;
     double t = sh[0][threadIdx.x];
-    for (int w = 1; w < kWarps; ++w) t = MAX ? fmax(t, sh[w][threadIdx.x]) : t + sh[w][threadIdx.x];
+    for (int w = 1; w < kWarps; ++w) t = mx ? fmax(t, sh[w][threadIdx.x]) : t + sh[w][threadIdx.x];
     c.part[(static_cast<int64_t>(ph) * 64 + threadIdx.x) * c.nblk + blockIdx.x] = t;
   }
   grid_sync(c.bar);
@@ -78,12 +81,13 @@ __device__ void grid_reduce(const DualCtx& c, int& ph, double (&v)[K]) {
   {
     for (int k = warp; k < K; k += kWarps) {
       const double* p = c.part + (static_cast<int64_t>(ph) * 64 + k) * c.nblk;
-      double t = MAX ? -INFINITY : 0.0;
-      for (int b = lane; b < c.nblk; b += 32) t = MAX ? fmax(t, __ldcg(p + b)) : t + __ldcg(p + b);
+      const bool mx = k >= MAXFROM;
+      double t = mx ? -INFINITY : 0.0;
+      for (int b = lane; b < c.nblk; b += 32) t = mx ? fmax(t, __ldcg(p + b)) : t + __ldcg(p + b);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double u = __shfl_xor_sync(0xffffffffu, t, o);
-        t = MAX ? fmax(t, u) : t + u;
+        t = mx ? fmax(t, u) : t + u;
       }
       if (lane == 0) tot[k] = t;
     }
@@ -120,8 +124,7 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
   double* S = c.S + st * sl::kStateStride;
   const double lam = S[sl::LAM];
   const double gp = 1.0 / lam;
-  double s[5] = {0, 0, 0, 0, 0};  // conj, z2, Hx.R, R2, (Hx0+Hx).y
-  double m[1] = {0.0};            // weighted inf residual
+  double s[6] = {0, 0, 0, 0, 0, 0};  // conj, z2, Hx.R, R2, (Hx0+Hx).y; [5] weighted inf residual (max)
   for (int i = gtid(); i < c.D; i += gstride()) {
     const int kd = c.g.kind[i];
     const double yi = y[i], hi = Hx[i];
@@ -136,10 +139,10 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
     s[2] += hi * Ri;
     s[3] += Ri * Ri;
     if (mode == 0) s[4] += (Hx0[i] + hi) * yi;
-    m[0] = fmax(m[0], fabs(weight ? Ri * weight[i] : Ri));
+    s[5] = fmax(s[5], fabs(weight ? Ri * weight[i] : Ri));
   }
-  grid_reduce<5>(c, ph, s);
-  grid_reduce<1, true>(c, ph, m);
+  grid_reduce<6, false, 5>(c, ph, s);  // one barrier: five sums and the max
+  const double m[1] = {s[5]};
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const double fhat = mode == 0 ? c.S[sl::FHAT0] - 0.5 * s[4] : S[sl::FHAT];
     S[sl::FHAT] = fhat;

@@ -90,7 +90,11 @@ void scenopt_dev::init_solver_buffers() {
   Work& k = *w;
   const Layout& L = ds.lay;
   k.D = std::max(L.dual_dim, 1);
-  k.nblk = ds.sm_count;
+  k.nblk = ds.sm_count;  // SCENOPT_DUAL_BLOCKS: grid of the dual-space kernels (<= SMs, co-resident)
+  if (const char* ev = std::getenv("SCENOPT_DUAL_BLOCKS")) {
+    const int b = std::atoi(ev);
+    if (b > 0 && b < ds.sm_count) k.nblk = b;
+  }
   k.S = ds.alloc<double>(sl::kScalars);
   k.I = ds.alloc<int>(il::kInts);
   k.part = ds.alloc<double>(static_cast<size_t>(2) * 64 * k.nblk);

@@ -54,6 +54,12 @@ struct DualCtx {
   double* part;    // partial sums [2][64][nblk]
   unsigned* bar;   // grid barrier {count, generation}
   const int* skip = nullptr;  // L-BFGS kernels: non-null and *skip != 0 -> return at once (speculation)
+  // fb_finish: when pubS is set, block 0 also publishes S / I into mapped
+  // host memory and writes seq last (publish_kernel's protocol, one launch fewer)
+  double* pubS = nullptr;
+  int* pubI = nullptr;
+  unsigned* pubSeq = nullptr;
+  unsigned seq = 0;
 };
 
 // fb_step / rescale_state finish (fbe.hpp:38-67). mode 0: fhat from the

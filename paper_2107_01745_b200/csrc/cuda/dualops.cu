@@ -166,6 +166,16 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
     }
     c.I[il::CONV] = skip;
   }
+  if (c.pubS && blockIdx.x == 0) {  // thread 0's S / I writes are visible to the block after the barrier
+    __syncthreads();
+    for (int t = threadIdx.x; t < sl::kScalars; t += blockDim.x) c.pubS[t] = c.S[t];
+    for (int t = threadIdx.x; t < il::kInts; t += blockDim.x) c.pubI[t] = c.I[t];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned*>(c.pubSeq) = c.seq;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- K7

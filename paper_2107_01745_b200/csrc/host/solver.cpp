@@ -396,14 +396,27 @@ struct Engine {
   }
 
   // fb_step (fbe.hpp:55-67) into state s: dual_grad sweep + fused finish
-  void fb_step(int s, const double* ydev, double lambda, const double* weight, Stats& stats) {
+  // publish_after: fb_finish also publishes the scalar block (= publish() right after it)
+  void fb_step(int s, const double* ydev, double lambda, const double* weight, Stats& stats,
+               bool publish_after = false) {
     if (!(lambda > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "fb_step: lambda must be > 0");
     ensure_fhat0();
     if (ydev != k.y[s]) copy(k.y[s], ydev, D());
     set_scalar(s * sl::kStateStride + sl::LAM, lambda);
     sweep1(true, k.y[s], k.x[s], k.u[s], k.Hx[s]);
     ++stats.dual_grad_calls;
-    SCN_CUDA(k_fb_finish(ctx(), s, 0, k.y[s], k.Hx[s], k.Hx0, weight, k.z[s], k.R[s], k.T[s], st));
+    DualCtx c = ctx();
+    if (publish_after) {
+      if (timer.on) {
+        cudaEventCreate(&pub_pre);
+        cudaEventRecord(pub_pre, st);
+      }
+      c.pubS = k.dpS;
+      c.pubI = k.dpI;
+      c.pubSeq = k.dpSeq;
+      c.seq = ++k.seq;
+    }
+    SCN_CUDA(k_fb_finish(c, s, 0, k.y[s], k.Hx[s], k.Hx0, weight, k.z[s], k.R[s], k.T[s], st));
     ++stats.prox_calls;
     ++stats.conj_calls;
   }
@@ -608,10 +621,9 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     Stats spec;
     const bool spec_hr = spec_on() && iter + 1 < cfg.max_iters;
     if (!spec_hr) e.publish();
-    e.fb_step(nxt, k.y[nxt], lambda, weight, spec);
+    e.fb_step(nxt, k.y[nxt], lambda, weight, spec, spec_hr);  // spec: fb_finish publishes
     e.mark("fb_step");
-    if (spec_hr) {
-      e.publish();  // certificate and FB-step scalars; the host reads them while HR runs
+    if (spec_hr) {  // certificate and FB-step scalars published; the host reads them while HR runs
       e.sweep1_unless_converged(k.R[nxt], k.HR);
       e.wait_published(true);
     } else {
@@ -741,9 +753,8 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
     const bool spec_next = spec_on() && iter + 1 < cfg.max_iters;
     if (!spec_next) e.publish();
     Stats spec;
-    e.fb_step(nxt, k.y[nxt], lambda, weight, spec);
+    e.fb_step(nxt, k.y[nxt], lambda, weight, spec, spec_next);  // spec: fb_finish publishes
     if (spec_next) {
-      e.publish();
       DualCtx cs = e.ctx();
       cs.skip = k.I + il::CONV;
       Engine::SkipScope g(e.d, k.I + il::CONV);

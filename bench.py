@@ -107,19 +107,66 @@ def dist_setup():
     return world, rank, local
 
 
-def cpu_baseline(flat, target_s=12.0):
-    """The CPU oracle (restatement of the reference, single thread, as the
-    reference's serial node loops) on a bounded sample of the workload."""
+def host_cpu():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
+def cpu_solves(orc, po, fac, lam0s, gpu_ttt=None):
+    """The CPU oracle's MINFBE and NAMA (p-NAMA: the reference's second thread,
+    solvers.hpp:411-418) from y0 = 0 at the given lambda0, with the
+    reference's wall_ms semantics (solvers.hpp:240, 166-168)."""
+    out = {}
+    for kind, code in (("minfbe", 0), ("nama", 1)):
+        cfg = orc.SolverConfig(lambda0=lam0s[kind], nama_parallel_linesearch=(kind == "nama"))
+        rep = orc.solve_direct(po, fac, cfg, code)
+        row = {"ms": rep["wall_ms"], "iterations": rep["iterations"],
+               "status": "converged" if rep["status"] == 0 else "max_iters_exceeded",
+               "dual_grad_calls": rep["dual_grad_calls"], "hessian_vec_calls": rep["hessian_vec_calls"],
+               "residual_inf": rep["residual_inf"], "lambda0": lam0s[kind],
+               "threads": 2 if kind == "nama" else 1}
+        if gpu_ttt and kind in gpu_ttt:
+            g = gpu_ttt[kind]
+            row["gpu_iterations"] = g["iterations"]
+            row["iterations_within_1"] = abs(g["iterations"] - rep["iterations"]) <= 1
+            if "y" in g:
+                yo = rep["y"]
+                row["y_gap_inf"] = float(np.abs(g.pop("y") - yo).max())
+                row["y_gap_bound"] = 10 * cfg.eps * (1 + float(np.abs(yo).max()))
+            row["gpu_speedup"] = rep["wall_ms"] / g["ms"] if g.get("ms") else None
+        out[kind] = row
+    return out
+
+
+def cpu_baseline(flat, lam0s=None, gpu_ttt=None, target_s=10.0):
+    """The CPU oracle (restatement of the reference, built -O3 -march=native
+    on this host; single thread, as the reference's serial node loops) on a
+    bounded sample of the workload, plus its MINFBE / NAMA time-to-tolerance
+    at the device's lambda0."""
     from oracle import oracle as orc
 
+    native = orc.use_native()
     po = orc.Problem.from_flat(flat)
     fac = orc.Factor(po)
     t1 = fac.time_sweeps(1, True)
     n = max(2, min(200, int(math.ceil(target_s / max(t1, 1e-6)))))
     t = fac.time_sweeps(n, True)
-    return {"value": 1.0 / t, "unit": "dual-grad evals/s", "cores": 1, "kind": "port",
-            "sample": f"{n} affine sweeps (dual_grad) of the same instance on one host thread, "
-                      f"{t * 1e3:.1f} ms each"}
+    out = {"value": 1.0 / t, "unit": "dual-grad evals/s", "cores": 1, "kind": "port",
+           "build": "g++ -O3 -march=native (built on this host)" if native else "portable -O3 (native build failed)",
+           "host_cpu": host_cpu(),
+           "sample": f"{n} affine sweeps (dual_grad) of the same instance on one host thread, "
+                     f"{t * 1e3:.1f} ms each; MINFBE and NAMA solved to tolerance once each"}
+    if lam0s:
+        out["time_to_tolerance"] = cpu_solves(orc, po, fac, lam0s, gpu_ttt)
+    return out
 
 
 def run_reference(args, world, rank):
@@ -129,6 +176,7 @@ def run_reference(args, world, rank):
         return
     from oracle import oracle as orc
 
+    native = orc.use_native()
     nx, nu, N, br, label = CONFIGS[args.config]
     t0 = time.time()
     po = orc.gen_random(1, nx, nu, N, br)
@@ -152,7 +200,7 @@ def run_reference(args, world, rank):
             th.join()
         return time.perf_counter() - tt
 
-    budget = 90.0  # seconds of timed CPU work
+    budget = 60.0  # seconds of timed CPU work
     w = min(args.warmup, 1)
     round_of(w)
     tr = round_of(1)  # one concurrent sweep per thread
@@ -160,6 +208,14 @@ def run_reference(args, world, rank):
     wall = round_of(k)
     t = wall / (k * threads)  # seconds per evaluation, aggregate
     value = 1.0 / t
+    # time-to-tolerance as solve() runs it (solvers.hpp:668-679): L by power
+    # iteration once (reported apart), then each solver from y0 = 0
+    ttt = None
+    if args.config in ("c1", "c3"):
+        tl = time.perf_counter()
+        L, lip_sweeps = fac.estimate_lipschitz()
+        ttt = {"lipschitz": {"ms": (time.perf_counter() - tl) * 1e3, "sweeps": lip_sweeps, "estimate": L}}
+        ttt.update(cpu_solves(orc, po, fac, {"minfbe": 0.9 / L, "nama": 0.9 / L}))
     out = {"metric": METRIC, "value": value, "unit": "dual-grad evals/s", "impl": "reference",
            "n_gpus": world, "steps": k, "warmup": w, "ms_per_step": t * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -167,10 +223,13 @@ def run_reference(args, world, rank):
            "config": {"workload": label, "nodes": po.flat()["num_nodes"], "dual_dim": po.dual_dim,
                       "setup_s": setup_s},
            "cpu_baseline": {"value": value, "unit": "dual-grad evals/s", "cores": threads, "kind": "port",
+                            "build": "g++ -O3 -march=native (built on this host)" if native else "portable -O3",
+                            "host_cpu": host_cpu(),
                             "sample": f"{k} rounds of {threads} concurrent affine sweeps (one per host "
                                       f"thread, {wall / k * 1e3:.0f} ms per round) of the CPU oracle "
                                       "(Eigen-free restatement of the reference; serial single-thread "
                                       f"sweep {t1 * 1e3:.1f} ms)"},
+           "time_to_tolerance": ttt,
            "e2e": {"value": value, "unit": "dual-grad evals/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -247,7 +306,8 @@ def main():
     H = (P * 2)(C.cast(hx.data_ptr(), P), None)
 
     def step():
-        so.api.check(lib.scenopt_dev_sweep_async(dev, 1, 1, Y, X, U, H))
+        # sharded: the primal stays on its owners (no gather inside the step)
+        so.api.check(lib.scenopt_dev_sweep_async(dev, 1, 1, Y, None if sharded else X, None if sharded else U, H))
 
     for _ in range(args.warmup):
         step()
@@ -292,6 +352,7 @@ def main():
     # report's wall_ms (solvers.hpp:240, 166-168) then covers the iterations
     # only, and the power iteration is reported beside it.
     ttt = {}
+    y_last = {}
     if not args.no_solve:
         so.estimate_dual_lipschitz(cache, prob)  # untimed: module load
         torch.cuda.synchronize()
@@ -315,6 +376,7 @@ def main():
                          "hessian_vec_calls": rep.stats.hessian_vec_calls,
                          "residual_inf": rep.residual_inf,
                          "lambda0": cfg.lambda0}
+            y_last[kind] = rep.y.copy()
 
     peaks, peak_src = measured_peaks()
     bytes_step = info["sweep_bytes_aff"]  # algorithmic bytes of the whole tree
@@ -353,7 +415,11 @@ def main():
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(prob.flat())
+        # CPU solver at the device's lambda0; compared with the device's
+        # iterates (iterations within 1, y within 10 eps), then dropped
+        gpu = {k: dict(v, y=y_last[k]) for k, v in ttt.items() if k in y_last}
+        lam0s = {k: v["lambda0"] for k, v in ttt.items() if k in ("minfbe", "nama")}
+        out["cpu_baseline"] = cpu_baseline(prob.flat(), lam0s or None, gpu)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -92,6 +92,24 @@ def build() -> str:
 
 
 _lib = None
+_NATIVE_PATH = os.path.join(_HERE, "_build", "native", "liboracle.so")
+
+
+def use_native() -> bool:
+    """Timed CPU baseline only (bench.py): build the oracle with -O3
+    -march=native on THIS host (``make native``, ~15 s) and load it instead of
+    the portable parity build. Must run before the first lib() call. Returns
+    False (portable build kept) when the build fails."""
+    global _LIB_PATH
+    if _lib is not None:
+        return _LIB_PATH == _NATIVE_PATH
+    try:
+        subprocess.run(["make", "-s", "-C", _HERE, "native"], check=True,
+                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    except (OSError, subprocess.CalledProcessError):
+        return False
+    _LIB_PATH = _NATIVE_PATH
+    return True
 
 
 def lib():

@@ -34,6 +34,7 @@ constexpr int LB_COUNT = 0, LB_PUSHED = 1, SETTLED = 2, PZERO = 3;
 constexpr int PDONE = 4, PROUNDS = 5, PMAX = 6;  // batched power iteration: sticky stop flag, rounds run, cap
 constexpr int CONV = 7;  // last fb_finish met the stop tolerance: skip word of a speculative sweep
 constexpr int LB_ORDER = 8;  // [8, 8 + mem + 1): slot ids, oldest first, then free slots
+constexpr int REJECT = 100;  // last fb_finish: the backtracking rule in S[GATE_RULE] rejects the step
 constexpr int kInts = 128;
 }  // namespace il
 

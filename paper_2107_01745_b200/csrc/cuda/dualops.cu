@@ -11,7 +11,6 @@
 // step, power-iteration stop) are taken on the device without a host round
 // trip.
 #include <cuda_runtime.h>
-#include <cstdlib>
 
 #include <cmath>
 #include <cstdint>
@@ -152,19 +151,20 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
     S[sl::RESID] = m[0];
     // skip word of a speculative sweep after this step (the host reads it
     // with the step's scalars and re-sweeps if it skipped an accepted step)
-    int skip = m[0] <= c.S[sl::EPS_STOP] ? 1 : 0;
     const int rule = static_cast<int>(c.S[sl::GATE_RULE]);
-    if (rule == 0) {  // original rule: candidate fhat above the model
+    int reject = 0;
+    if (rule == 0) {  // original rule: candidate fhat above the model (the host takes this verdict)
       const double model = __dadd_rn(__dadd_rn(c.S[sl::CERT_FHAT], __dmul_rn(lam, c.S[sl::HXW_RW])),
                                      __dmul_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(1.0, -c.S[sl::BETA_BT])), lam),
                                                c.S[sl::RW2]));
-      if (fhat > model) skip = 1;
+      reject = fhat > model;
     } else if (rule == 1) {  // MINFBE simple rule: lambda |img| > eps_bt |R| halves lambda
-      if (__dmul_rn(lam, sqrt(c.S[sl::IMG2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::R2]))) skip = 1;
+      reject = __dmul_rn(lam, sqrt(c.S[sl::IMG2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::R2]));
     } else if (rule == 3) {  // NAMA simple rule on the certificate's norms
-      if (__dmul_rn(lam, sqrt(c.S[sl::HR2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::RR2]))) skip = 1;
+      reject = __dmul_rn(lam, sqrt(c.S[sl::HR2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::RR2]));
     }
-    c.I[il::CONV] = skip;
+    c.I[il::REJECT] = reject;
+    c.I[il::CONV] = (m[0] <= c.S[sl::EPS_STOP] || reject) ? 1 : 0;
   }
   if (c.pubS && blockIdx.x == 0) {  // thread 0's S / I writes are visible to the block after the barrier
     __syncthreads();
@@ -1003,11 +1003,7 @@ cudaError_t k_lbfgs(const DualCtx& c, int mem, double eps_curv, double scale_ref
                     double* out, double* Sbuf, double* Qbuf, cudaStream_t st, double* Mbuf, const double* fR,
                     const double* fHR, int fstate, double* gout) {
   DualCtx c2 = c;
-  static const bool compact_on = [] {
-    const char* v = std::getenv("SCENOPT_LBFGS_COMPACT");
-    return !(v && v[0] == '0');
-  }();
-  if (Mbuf && mem <= kCompactMem && compact_on) {
+  if (Mbuf && mem <= kCompactMem) {
     void* args[] = {&c2,  &mem,  &eps_curv, &scale_ref, &do_push, &a,  &b,   &cc,     &dd,  &gvec,
                     &out, &Sbuf, &Qbuf,     &Mbuf,      &fR,      &fHR, &fstate, &gout};
     return coop(reinterpret_cast<const void*>(lbfgs_compact_kernel), c, args, st);

@@ -62,8 +62,7 @@ struct Item {
   int32_t direct;   // flags: kDirectContrib (bw: contributions read from L2, many children),
                     //        kGlobalBlocks (node blocks stay in HBM; only the headers are copied)
   int32_t ldep;     // local index (same CTA) of the last item this one depends on, -1: none
-  int32_t publish;  // bit 0: release the nodes' flags at gpu scope (consumed by other CTAs);
-                    // bit 1: the CTA's last forward item of its stage; bits 2..: forward stage + 1
+  int32_t publish;  // bit 0: release the nodes' flags at gpu scope (consumed by other CTAs)
 };
 static_assert(sizeof(Item) == 64, "Item is one 64-byte record");
 
@@ -82,8 +81,6 @@ struct SweepParams {
   int nxp, Vp;  // padded column lengths (== 2 mod 4) of J/K/TN and W
   int consumer_stage;  // 1: teams stage their own vectors (staging area per team, not per ring entry)
   int global_blocks;   // 1: some items keep their node blocks in HBM (kGlobalBlocks)
-  int small_nodes;     // 1: warp-per-node consumers (nx + nu <= 32, nx + m <= 32, mN <= 32)
-  unsigned long long* stage_done;  // [N+1] CTAs done with each forward stage (cumulative), or null
   const Item* items;      // CTA-major: CTA b owns items [cta_off[b], cta_off[b+1])
   const int32_t* cta_off;
   const double* bw_blk;

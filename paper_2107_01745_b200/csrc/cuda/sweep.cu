@@ -620,160 +620,13 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   if (ttid == 0) PROF_T1(13);
 }
 
-// ---------------------------------------------------------------- small nodes
-// nx + nu <= 32 and nx + m <= 32: one warp owns a whole node (lane j computes
-// output j; the costate / state vector moves between the two phases by
-// shuffles), so a team's warps work on four nodes without any barrier.
-// Same products as consume_backward / consume_forward (tree_oracles.hpp:
-// 44-88), sequential sums in index order.
-template <int NRHS>
-__device__ void consume_bw_small(const SweepParams& P, const Item& it, const double* slot, const double* mat,
-                                 const double* st, int ttid) {
-  const int nx = P.nx, nu = P.nu, W = nx + nu, nxp = P.nxp;
-  const int lane = ttid & 31;
-  const bool leaf = it.leaf != 0;
-  const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
-  const double* Y = st;
-  const double* Cn = st + NRHS * it.v0_n;
-  const double* AF = st + NRHS * (it.v0_n + ((it.direct & kDirectContrib) ? 0 : it.v1_n * W));
-  const int ncols = leaf ? nx : W;
-  for (int ni = ttid >> 5; ni < it.count; ni += kTeam / 32) {
-    const NodeMeta& mc = meta[ni];
-    double acc[NRHS];
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
-    const int ja = leaf ? nu + lane : lane;
-    if (lane < ncols) {
-      const int len = leaf ? mc.mN : mc.M;
-      const double* col = mat + mc.blk + lane * len;
-      const double* yv = Y + mc.yoff;
-      for (int k = 0; k < len; ++k) {
-        const double a = col[k];
-#pragma unroll
-        for (int r = 0; r < NRHS; ++r) acc[r] = fma(a, yv[r * it.v0_n + k], acc[r]);
-      }
-      if (!leaf) {
-        if (it.direct & kDirectContrib) {
-          for (int k = 0; k < mc.nkid; ++k)
-#pragma unroll
-            for (int r = 0; r < NRHS; ++r)
-              acc[r] += __ldcg(P.contrib[r] + static_cast<int64_t>(it.v1_lo + mc.kid0 + k) * W + lane);
-        } else {
-          for (int k = 0; k < mc.nkid; ++k)
-#pragma unroll
-            for (int r = 0; r < NRHS; ++r) acc[r] += Cn[r * it.v1_n * W + (mc.kid0 + k) * W + lane];
-        }
-      }
-      const double aff = P.affine ? AF[ni * W + ja] : 0.0;
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) {
-        acc[r] += aff;
-        if (ja < nu) P.uoff[r][static_cast<int64_t>(mc.c) * nu + ja] = acc[r];  // u_off
-      }
-    }
-    if (mc.c == 0) continue;  // the root has no parent to contribute to
-    // phase B: contrib_c = J_c' w_c, w[t] held by lane (leaf ? t : nu + t)
-    const int e = leaf ? mc.mN * nx : mc.M * W;
-    const double* J = mat + mc.blk + ((e + 1) & ~1);
-    double b[NRHS];
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) b[r] = 0.0;
-    for (int t = 0; t < nx; ++t) {
-      const int src = leaf ? t : nu + t;
-      const double jt = lane < W ? J[t + lane * nxp] : 0.0;
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) b[r] = fma(jt, __shfl_sync(0xffffffffu, acc[r], src), b[r]);
-    }
-    if (lane < W)
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) P.contrib[r][static_cast<int64_t>(mc.c) * W + lane] = b[r];
-  }
-}
-
-template <int NRHS>
-__device__ void consume_fw_small(const SweepParams& P, const Item& it, const double* slot, const double* mat,
-                                 const double* st, int ttid) {
-  const int nx = P.nx, nu = P.nu, Vp = P.Vp, nxp = P.nxp;
-  const int lane = ttid & 31;
-  const bool leaf = it.leaf != 0;
-  const bool root = it.first == 0;
-  const NodeMeta* meta = reinterpret_cast<const NodeMeta*>(slot);
-  const int tot = it.v0_n * Vp;
-  const double* PV = st;
-  const double* UO = st + NRHS * tot;
-  const double* AF = st + NRHS * (tot + it.v1_n * nu);
-  for (int ni = ttid >> 5; ni < it.count; ni += kTeam / 32) {
-    const NodeMeta& mc = meta[ni];
-    const int64_t c = mc.c;
-    double xv[NRHS];
-    if (root) {  // x_0 = p (affine) or 0
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) {
-        xv[r] = (lane < nx && P.affine) ? P.root_state[lane] : 0.0;
-        if (lane < nx) {
-          P.x[r][lane] = xv[r];
-          if (P.hx[r]) P.hx[r][lane] = xv[r];
-        }
-      }
-    } else {
-      // phase A: x_c = [A B] [x_a; u_a] (+c), stage rows [F G] [x_a; u_a]
-      double acc[NRHS];
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) acc[r] = 0.0;
-      if (lane < nx + mc.m) {
-        const double* col = mat + mc.blk + lane * Vp;
-        const double* v = PV + mc.par * Vp;
-        for (int k = 0; k < nx + nu; ++k) {
-          const double a = col[k];
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) acc[r] = fma(a, v[r * tot + k], acc[r]);
-        }
-        if (lane < nx) {
-          const double aff = P.affine ? AF[ni * nx + lane] : 0.0;
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) {
-            acc[r] += aff;
-            P.x[r][c * nx + lane] = acc[r];
-            if (P.hx[r]) P.hx[r][c * nx + lane] = acc[r];
-          }
-        } else {
-#pragma unroll
-          for (int r = 0; r < NRHS; ++r) P.Hx[r][mc.doff + (lane - nx)] = acc[r];
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) xv[r] = acc[r];
-    }
-    // phase B: u_c = K x_c + u_off (interior) or terminal rows F_N x_c (leaf); x[t] in lane t
-    const double* K = mat + mc.blk + (root ? 0 : Vp * (nx + mc.m));
-    const int nout = leaf ? mc.mN : nu;
-    double b[NRHS];
-#pragma unroll
-    for (int r = 0; r < NRHS; ++r) b[r] = 0.0;
-    for (int t = 0; t < nx; ++t) {
-      const double kt = lane < nout ? K[t + lane * nxp] : 0.0;
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) b[r] = fma(kt, __shfl_sync(0xffffffffu, xv[r], t), b[r]);
-    }
-    if (lane < nout)
-#pragma unroll
-      for (int r = 0; r < NRHS; ++r) {
-        if (leaf)
-          P.Hx[r][mc.tdo + lane] = b[r];
-        else
-          P.u[r][c * nu + lane] = UO[r * it.v1_n * nu + ni * nu + lane] + b[r];
-          if (P.hu[r]) P.hu[r][c * nu + lane] = P.u[r][c * nu + lane];
-      }
-  }
-}
-
 // MODE bits (one instantiation per combination, so the common layout's
 // kernel carries no fallback code): kModeConsumerStage = teams stage their own
 // vectors; kModeGlobalBlocks = some items read their node blocks from HBM.
-constexpr int kModeConsumerStage = 1, kModeGlobalBlocks = 2, kModeSmallNodes = 4;
+constexpr int kModeConsumerStage = 1, kModeGlobalBlocks = 2;
 // kModeHostOut: forward x rows to mapped host memory as 16-byte row stores
 // (only instantiated for the default layout; other layouts store per element)
-constexpr int kModeHostOut = 8;
+constexpr int kModeHostOut = 4;
 template <int NRHS, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P, int mmax, int mNmax) {
   extern __shared__ __align__(128) double smem[];
@@ -907,18 +760,6 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
       if (g_trace) trace_row = g_trace + 12LL * (P.cta_off[blockIdx.x] + P.items_base + k);
 #endif
       if (DBG(2)) {
-      } else if (MODE & kModeSmallNodes) {
-        if ((MODE & kModeGlobalBlocks) && gblocks) {
-          if (it.pass == 0)
-            consume_bw_small<NRHS>(P, it, slot, gmat, st, ttid);
-          else
-            consume_fw_small<NRHS>(P, it, slot, gmat, st, ttid);
-        } else {
-          if (it.pass == 0)
-            consume_bw_small<NRHS>(P, it, slot, slot, st, ttid);
-          else
-            consume_fw_small<NRHS>(P, it, slot, slot, st, ttid);
-        }
       } else if (it.pass == 0) {
         if ((MODE & kModeGlobalBlocks) && gblocks)
           consume_backward<NRHS>(P, it, slot, gmat, st, tbuf, ttid, team, trace_row);
@@ -1006,28 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
         }
       }
       __syncwarp();
-      // forward progress for overlapped host copies: nodes of each stage
-      // finished so far (gpu-scope release, cumulative over the teams' writes
-      // observed through DONE); the host's copy stream waits on these counters
       if (lane == 0) {
-        // forward progress for overlapped host copies: when this CTA retires
-        // its last forward item of a stage, count the CTA as done with that
-        // stage (one gpu-scope fence per such batch; lane 0 observed every
-        // item of the batch through the DONE waits)
-        if (P.stage_done) {
-          bool fenced = pub;
-          for (int q2 = k; q2 < j; ++q2) {
-            const int4 dn = sdone[q2 % kDoneQ];
-            if (dn.w & 2) {
-              if (!fenced) {
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                fenced = true;
-              }
-              asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(P.stage_done + ((dn.w >> 2) - 1))
-                           : "memory");
-            }
-          }
-        }
         st_release_cta(&s_retired, j);
 #ifdef SCN_SWEEP_PROFILE
         if (g_timeline || g_trace) {
@@ -1062,11 +882,11 @@ int sweep_threads() { return kThreads; }
 int sweep_teams() { return kTeams; }
 namespace {
 #define SCN_K(R, M) reinterpret_cast<const void*>(sweep_kernel<R, M>)
-const void* const kKernels[3][8] = {
-    {SCN_K(1, 0), SCN_K(1, 1), SCN_K(1, 2), SCN_K(1, 3), SCN_K(1, 4), SCN_K(1, 5), SCN_K(1, 6), SCN_K(1, 7)},
-    {SCN_K(2, 0), SCN_K(2, 1), SCN_K(2, 2), SCN_K(2, 3), SCN_K(2, 4), SCN_K(2, 5), SCN_K(2, 6), SCN_K(2, 7)},
+const void* const kKernels[3][4] = {
+    {SCN_K(1, 0), SCN_K(1, 1), SCN_K(1, 2), SCN_K(1, 3)},
+    {SCN_K(2, 0), SCN_K(2, 1), SCN_K(2, 2), SCN_K(2, 3)},
     // host-output variants of the default layout (row [nrhs-1]); the rest of the row repeats them
-    {SCN_K(1, 8), SCN_K(2, 8), SCN_K(1, 8), SCN_K(2, 8), SCN_K(1, 8), SCN_K(2, 8), SCN_K(1, 8), SCN_K(2, 8)}};
+    {SCN_K(1, 4), SCN_K(2, 4), SCN_K(1, 4), SCN_K(2, 4)}};
 #undef SCN_K
 }  // namespace
 
@@ -1164,8 +984,7 @@ cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mm
   }();
   (void)dbg_set;
 #endif
-  const int mode = (P.consumer_stage ? kModeConsumerStage : 0) | (P.global_blocks ? kModeGlobalBlocks : 0) |
-                   (P.small_nodes ? kModeSmallNodes : 0);
+  const int mode = (P.consumer_stage ? kModeConsumerStage : 0) | (P.global_blocks ? kModeGlobalBlocks : 0);
   const bool host_out = P.hx[0] || (P.nrhs == 2 && P.hx[1]);
   const void* fn = (host_out && mode == 0) ? kKernels[2][P.nrhs == 2 ? 1 : 0] : kKernels[P.nrhs == 2 ? 1 : 0][mode];
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, dyn_smem, stream);

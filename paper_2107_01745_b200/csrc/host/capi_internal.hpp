@@ -60,7 +60,6 @@ struct scenopt_dev {
   const double* in_dual(const double* src, int flags, int slot);
   void out_copy(double* dst, const double* dev_src, size_t count, int flags);
   void sync();
-  bool overlap_ready();  // host copies overlapped with the sweep (DevState::Overlap) available
   static double* mapped(double* p);  // device address of a pinned host buffer, or nullptr
   bool zero_copy_ok(int nrhs, double* const* x, double* const* u);
 };

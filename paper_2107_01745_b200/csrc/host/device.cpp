@@ -11,31 +11,6 @@
 
 namespace scn {
 
-bool DevState::Overlap::init(DevState& d) {
-  cudaDriverEntryPointQueryResult q{};
-  void* fn = nullptr;
-  if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-      q != cudaDriverEntryPointSuccess || !fn) {
-    cudaGetLastError();
-    return false;
-  }
-  wait_fn = fn;
-  SCN_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
-  stage_done = d.alloc<unsigned long long>(static_cast<size_t>(d.lay.N) + 1);
-  expected.assign(static_cast<size_t>(d.lay.N) + 1, 0ull);
-  return true;
-}
-
-void DevState::Overlap::wait(cudaStream_t s, unsigned long long* addr, unsigned long long value) {
-  using Fn = int (*)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);  // CUresult(CUstream, CUdeviceptr, cuuint64_t, flags)
-  const int r = reinterpret_cast<Fn>(wait_fn)(s, reinterpret_cast<unsigned long long>(addr), value, 0u /* GEQ */);
-  if (r != 0) fail(SCENOPT_E_CUDA, "cuStreamWaitValue64 failed (" + std::to_string(r) + ")");
-}
-
-DevState::Overlap::~Overlap() {
-  if (copy_stream) cudaStreamDestroy(copy_stream);
-}
-
 DevState::~DevState() {
   if (device >= 0) cudaSetDevice(device);
   nccl_comm_destroy(comm);
@@ -300,7 +275,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   const int min_sub_cfg = env_int("SCENOPT_MIN_SUBTREES", 4);
   if (const int g = env_int("SCENOPT_GRID", 0)) {
     d->grid = std::min(g, d->grid);  // experiments only
-  } else if (min_sub_cfg > 0 && env_int("SCENOPT_SMALL_GRID", 1) != 0) {  // whole-tree widths (conservative per rank)
+  } else if (min_sub_cfg > 0) {  // whole-tree widths (conservative per rank)
     // A latency-bound tree (no stage reaches min_sub * SMs nodes, and little
     // data) runs on the largest grid that still gets a subtree cut: its
     // dependencies are then CTA-local instead of cross-CTA flags at every
@@ -487,7 +462,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     // CTA-local retire counter instead of a cross-CTA flag, and each CTA
     // computes exactly the parents its own subtrees need before starting its
     // local forward (round-robin tickets delayed CTAs holding four of them).
-    if (d->flat_top && env_int("SCENOPT_FLAT_OWNER", 1) != 0) {
+    if (d->flat_top) {
       std::vector<int> owner(static_cast<size_t>(n), -1);
       for (int gg = 0; gg < G; ++gg)
         for (const Run& r : fw_l[gg])
@@ -520,9 +495,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     // Likewise the backward tickets of stage cut-1: a parent's children are
     // consecutive cut-stage nodes, mostly of one CTA, so the parent placed on
     // that CTA right after its local backward waits on the retire counter.
-    // SCENOPT_BW_OWNER=2 applies the rule level by level up to the root.
-    const int bw_owner = env_int("SCENOPT_BW_OWNER", 1);
-    for (int lvl = cut - 1; lvl >= (bw_owner >= 2 ? 0 : cut - 1) && lvl >= 0 && bw_owner != 0; --lvl) {
+    // (Applying the rule level by level up to the root measured no faster.)
+    if (cut >= 1) {
+      const int lvl = cut - 1;
       std::vector<int> owner(static_cast<size_t>(n), -1);
       for (int gg = 0; gg < G; ++gg)
         for (const Run& r : bw_l[gg])
@@ -559,8 +534,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     // from its ancestors' u_off (affine maps precomputed below) as soon as the
     // backward root is done, instead of a chain of per-stage dependencies.
     const int cut = d->cut_stage;
-    d->flat_top = cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0 &&
-                  env_int("SCENOPT_SMALL_NODES", 0) == 0;
+    d->flat_top = cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0;
     if (d->flat_top) {
       mark_flat(fw_l, cut);
       owner_fw(fw_l, cut);
@@ -612,13 +586,12 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     Lists a_bw, a_fw, t_bw, t_fw, o_bw, o_fw;
     d->cut_stage = region(s, p.N, own, true, true, false, a_bw, a_fw);
     const int cut = d->cut_stage;
-    if (env_int("SCENOPT_SHARD_OWNER", 1) != 0) owner_bw(a_bw, cut);
+    owner_bw(a_bw, cut);
     launch_lists.push_back(std::move(a_bw));
     region(0, s - 1, full, false, true, true, t_bw, t_fw);
     region(s, p.N, own, true, false, true, o_bw, o_fw);
     // launch B: every flattened node waits on the (replicated) backward root
-    d->flat_top = cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0 &&
-                  env_int("SCENOPT_SHARD_FLAT", 1) != 0 && env_int("SCENOPT_SMALL_NODES", 0) == 0;
+    d->flat_top = cut >= 2 && cut <= 4 && env_int("SCENOPT_FLAT_TOP", 1) != 0;
     if (d->flat_top) {
       mark_flat(t_fw, cut);
       mark_flat(o_fw, cut);
@@ -729,34 +702,11 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     max_item = std::max(max_item, tot);
     max_cnt = std::max(max_cnt, ru.count);
   }
-  // the last forward item of each stage in every CTA's list signals the
-  // stage's completion to overlapped host copies (DevState::Overlap)
-  d->stage_ctas.assign(static_cast<size_t>(p.N) + 1, 0);
-  {
-    size_t base = 0;
-    for (const auto& off : cta_offs) {
-      for (int gg = 0; gg < G; ++gg) {
-        int last_stage = -1;
-        for (int q = off[gg + 1] - 1; q >= off[gg]; --q) {
-          Item& it = items[base + q];
-          if (it.pass != 1) continue;
-          const int st = p.node_stage[it.first];
-          if (st != last_stage) {  // scanning backwards: first seen = last of its stage
-            it.publish |= 2;
-            ++d->stage_ctas[st];
-            last_stage = st;
-          }
-        }
-      }
-      base += off[G];
-    }
-  }
   // Pass-array placement in "time-major" order: item k of every CTA, then
-  // item k+1, ... (SCENOPT_PACK=cta: CTA-major). CTAs advance through their
-  // lists at about the same rate, so the blocks streamed concurrently by the
-  // grid are neighbours in HBM instead of 148 far-apart streams.
+  // item k+1, ... CTAs advance through their lists at about the same rate, so
+  // the blocks streamed concurrently by the grid are neighbours in HBM instead
+  // of 148 far-apart streams.
   {
-    const bool cta_major = std::getenv("SCENOPT_PACK") && std::string(std::getenv("SCENOPT_PACK")) == "cta";
     size_t base = 0;
     for (const auto& off : cta_offs) {
       int longest = 0;
@@ -767,13 +717,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         it.off = total;
         total += item_doubles[q];
       };
-      if (cta_major) {
-        for (int q = 0; q < off[G]; ++q) place(base + q);
-      } else {
-        for (int k = 0; k < longest; ++k)
-          for (int gg = 0; gg < G; ++gg)
-            if (off[gg] + k < off[gg + 1]) place(base + off[gg] + k);
-      }
+      for (int k = 0; k < longest; ++k)
+        for (int gg = 0; gg < G; ++gg)
+          if (off[gg] + k < off[gg + 1]) place(base + off[gg] + k);
       base += off[G];
     }
   }
@@ -1009,7 +955,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   int best_ns = 0;
   int64_t slot = 0;
   bool consumer = false;
-  const int ns_max = std::min(kMaxSlots, std::max(2, env_int("SCENOPT_NSLOT_MAX", 5)));
+  const int ns_max = std::min(kMaxSlots, 5);
   auto fits = [&](int ns, int64_t sl, bool cons) {
     const size_t smem = smem_for(ns, sl, cons);
     if (smem > optin) return false;
@@ -1054,9 +1000,6 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
       ++n_global;
     }
   d->items_global = n_global;
-  // warp-per-node consumers (opt-in, SCENOPT_SMALL_NODES=1): measured slower than
-  // the team path on the C5 nx=10 trees (sequential per-lane dots), kept for work
-  d->small_nodes = (nx + nu <= 32) && (nx + d->max_m <= 32) && (d->max_mN <= 32) && env_int("SCENOPT_SMALL_NODES", 0) != 0;
   d->nslot = best_ns;
   d->ctas_per_sm = 1;
   d->dyn_smem = smem_for(best_ns, slot, consumer);
@@ -1279,7 +1222,6 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
   P.Vp = d.Vp;
   P.consumer_stage = d.consumer_stage ? 1 : 0;
   P.global_blocks = d.items_global > 0 ? 1 : 0;
-  P.small_nodes = d.small_nodes ? 1 : 0;
   P.bw_blk = d.bw_blk;
   P.fw_blk = d.fw_blk;
   P.aff_bw = d.aff_bw;
@@ -1352,9 +1294,8 @@ void phase_b(DevState& d, SweepParams& P) {
 }  // namespace
 
 void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
-               double* const* u, double* const* Hx, bool gather_primal, unsigned long long* stage_done) {
+               double* const* u, double* const* Hx, bool gather_primal) {
   SweepParams P = sweep_params(d, nrhs, affine, y, x, u, Hx);
-  P.stage_done = d.sharded() ? nullptr : stage_done;
   if (!d.sharded()) {
     launch(d, P, d.launches[0]);
     return;

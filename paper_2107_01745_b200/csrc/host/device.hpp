@@ -69,22 +69,7 @@ struct DevState {
   bool device_factor = false;   // E / J / K / aff_bw computed on the device (K9)
   FactorParams fp{};            // device-factor launch parameters (index arrays on the device)
   bool fp_ready = false;
-  // Overlapped host output: per-stage forward completion counters (device,
-  // cumulative) waited on by a copy stream (cuStreamWaitValue64 through the
-  // runtime's driver entry point, so the library needs no libcuda link).
-  struct Overlap {
-    int state = 0;  // 0 untried, 1 ready, -1 unavailable
-    cudaStream_t copy_stream = nullptr;
-    unsigned long long* stage_done = nullptr;
-    std::vector<unsigned long long> expected;
-    void* wait_fn = nullptr;
-    bool init(DevState& d);
-    void wait(cudaStream_t s, unsigned long long* addr, unsigned long long value);
-    ~Overlap();
-  } overlap;
   int items_global = 0;         // items whose node blocks are read from HBM in place
-  std::vector<int> stage_ctas;  // per forward stage: CTAs holding items of it (stage signals per sweep)
-  bool small_nodes = false;     // warp-per-node consumers (small states)
   // ---- subtree sharding over ranks
   int rank = 0, world = 1, shard_stage = -1;
   void* comm = nullptr;         // ncclComm_t
@@ -171,8 +156,7 @@ int device_count_sm100();
 // Sharded handles: Hx is assembled on every rank; x/u hold this rank's nodes
 // plus the replicated top unless gather_primal assembles them in full.
 void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
-               double* const* u, double* const* Hx, bool gather_primal = false,
-               unsigned long long* stage_done = nullptr);
+               double* const* u, double* const* Hx, bool gather_primal = false);
 // One phase of a sharded sweep with the exchange left to the caller (phase 0:
 // zero Hx, local backward, own contributions into d.xbuf; phase 1: xbuf
 // (summed over ranks by the caller) back, top backward + forward, top rows

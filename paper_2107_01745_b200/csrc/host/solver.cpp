@@ -46,6 +46,8 @@ struct scenopt_dev::Work {
   static constexpr int kRing = 256;
   double* hRing = nullptr;
   int ring_next = 0;
+  int* hIRing = nullptr;  // the same for int-block writes (kRing words)
+  int iring_next = 0;
   // two FbStates (ping-pong)
   double *y[2] = {}, *Hx[2] = {}, *z[2] = {}, *R[2] = {}, *T[2] = {}, *x[2] = {}, *u[2] = {};
   double *Hx0 = nullptr, *x0 = nullptr, *u0 = nullptr;
@@ -76,6 +78,7 @@ scenopt_dev::~scenopt_dev() {
     if (w->hS) cudaFreeHost(w->hS);
     if (w->hI) cudaFreeHost(w->hI);
     if (w->hRing) cudaFreeHost(w->hRing);
+    if (w->hIRing) cudaFreeHost(w->hIRing);
     if (w->pS) cudaFreeHost(w->pS);
     if (w->pI) cudaFreeHost(w->pI);
     if (w->pSeq) cudaFreeHost(w->pSeq);
@@ -90,11 +93,7 @@ void scenopt_dev::init_solver_buffers() {
   Work& k = *w;
   const Layout& L = ds.lay;
   k.D = std::max(L.dual_dim, 1);
-  k.nblk = ds.sm_count;  // SCENOPT_DUAL_BLOCKS: grid of the dual-space kernels (<= SMs, co-resident)
-  if (const char* ev = std::getenv("SCENOPT_DUAL_BLOCKS")) {
-    const int b = std::atoi(ev);
-    if (b > 0 && b < ds.sm_count) k.nblk = b;
-  }
+  k.nblk = ds.sm_count;  // grid of the dual-space kernels: one co-resident block per SM
   k.S = ds.alloc<double>(sl::kScalars);
   k.I = ds.alloc<int>(il::kInts);
   k.part = ds.alloc<double>(static_cast<size_t>(2) * 64 * k.nblk);
@@ -105,6 +104,7 @@ void scenopt_dev::init_solver_buffers() {
   SCN_CUDA(cudaMallocHost(&k.hS, sl::kScalars * sizeof(double)));
   SCN_CUDA(cudaMallocHost(&k.hI, il::kInts * sizeof(int)));
   SCN_CUDA(cudaMallocHost(&k.hRing, scenopt_dev::Work::kRing * sizeof(double)));
+  SCN_CUDA(cudaMallocHost(&k.hIRing, scenopt_dev::Work::kRing * sizeof(int)));
   SCN_CUDA(cudaHostAlloc(&k.pS, sl::kScalars * sizeof(double), cudaHostAllocMapped));
   SCN_CUDA(cudaHostAlloc(&k.pI, il::kInts * sizeof(int), cudaHostAllocMapped));
   SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpS), k.pS, 0));
@@ -158,15 +158,20 @@ struct Report {  // SolverReport, solvers.hpp:66-84
 namespace {
 std::mutex g_arrays_mu;
 std::vector<std::vector<double>> g_arrays;
-constexpr size_t kArraysKept = 16, kArrayMinBytes = 1 << 16;
+size_t g_arrays_bytes = 0;
+// at most 16 arrays and 256 MB are kept; a request takes the smallest array
+// that fits, and only one at most twice its size
+constexpr size_t kArraysKept = 16, kArrayMinBytes = 1 << 16, kArraysMaxBytes = size_t(256) << 20;
 void array_take(std::vector<double>& dst, size_t n) {
   {
     std::lock_guard<std::mutex> lk(g_arrays_mu);
     size_t best = g_arrays.size();
     for (size_t i = 0; i < g_arrays.size(); ++i)  // the smallest that fits
-      if (g_arrays[i].capacity() >= n && (best == g_arrays.size() || g_arrays[i].capacity() < g_arrays[best].capacity()))
+      if (g_arrays[i].capacity() >= n && g_arrays[i].capacity() <= 2 * n &&
+          (best == g_arrays.size() || g_arrays[i].capacity() < g_arrays[best].capacity()))
         best = i;
     if (best < g_arrays.size()) {
+      g_arrays_bytes -= g_arrays[best].capacity() * sizeof(double);
       dst.swap(g_arrays[best]);
       g_arrays.erase(g_arrays.begin() + static_cast<std::ptrdiff_t>(best));
     }
@@ -174,9 +179,13 @@ void array_take(std::vector<double>& dst, size_t n) {
   dst.resize(n);  // every element is overwritten by the download
 }
 void array_give(std::vector<double>& v) {
-  if (v.capacity() * sizeof(double) < kArrayMinBytes) return;
+  const size_t bytes = v.capacity() * sizeof(double);
+  if (bytes < kArrayMinBytes) return;
   std::lock_guard<std::mutex> lk(g_arrays_mu);
-  if (g_arrays.size() < kArraysKept) g_arrays.push_back(std::move(v));
+  if (g_arrays.size() < kArraysKept && g_arrays_bytes + bytes <= kArraysMaxBytes) {
+    g_arrays_bytes += bytes;
+    g_arrays.push_back(std::move(v));
+  }
 }
 }  // namespace
 
@@ -229,6 +238,19 @@ struct Engine {
     k.hS[slot] = v;  // host mirror
     SCN_CUDA(cudaMemcpyAsync(k.S + slot, w, sizeof(double), cudaMemcpyHostToDevice, st));
   }
+  // Stream-ordered write of n ints at I[slot..] from pinned staging words
+  // (ordered with every kernel of the handle's stream, no host synchronisation).
+  void set_ints(int slot, const int* v, int n) {
+    if (k.iring_next + n > scenopt_dev::Work::kRing) {  // every staging word may still be in flight
+      SCN_CUDA(cudaStreamSynchronize(st));
+      k.iring_next = 0;
+    }
+    int* w = k.hIRing + k.iring_next;
+    k.iring_next += n;
+    std::memcpy(w, v, n * sizeof(int));
+    std::memcpy(k.hI + slot, v, n * sizeof(int));  // host mirror
+    SCN_CUDA(cudaMemcpyAsync(k.I + slot, w, n * sizeof(int), cudaMemcpyHostToDevice, st));
+  }
   // Host reads of the scalar block. publish() enqueues its copy into mapped
   // host memory and marks it with an event; wait_published() waits for that
   // event only, so work enqueued after publish() keeps the GPU busy while the
@@ -258,7 +280,7 @@ struct Engine {
       }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
-    if (full) k.ring_next = 0;  // publish ran after every earlier copy: all staging words consumed
+    if (full) k.ring_next = k.iring_next = 0;  // publish ran after every earlier copy: all staging words consumed
     if (timer.on) timer.host_sync_ms += now_ms() - h0;
     std::memcpy(k.hS, k.pS, sl::kScalars * sizeof(double));
     std::memcpy(k.hI, k.pI, il::kInts * sizeof(int));
@@ -311,6 +333,10 @@ struct Engine {
       if (!sync_ev.empty())
         std::fprintf(stderr, "[scn] %zu host round trips, %.3f ms (%.1f us each)\n", sync_ev.size(), st,
                      1e3 * st / sync_ev.size());
+      for (auto& p : sync_ev) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+      }
       std::fprintf(stderr, "[scn] host: %.3f ms enqueuing sweeps (%.1f us each), %.3f ms blocked in reads\n",
                    host_launch_ms, 1e3 * host_launch_ms / ev.size(), host_sync_ms);
     }
@@ -435,14 +461,15 @@ struct Engine {
       if (!k.Mb) k.Mb = d.alloc<double>(2 * 64 * 64);
       k.lb_slots = mem + 1;
     }
-    std::vector<int> ints(il::kInts, 0);
+    int ints[il::LB_ORDER + 64] = {};
     for (int j = 0; j <= mem; ++j) ints[il::LB_ORDER + j] = j;
-    SCN_CUDA(cudaMemcpy(k.I, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice));
+    set_ints(il::LB_COUNT, ints + il::LB_COUNT, 2);                   // count, pushed
+    set_ints(il::LB_ORDER, ints + il::LB_ORDER, mem + 1);
     set_scalar(sl::GAMMA0, 1.0);
   }
   void lbfgs_clear() {  // lbfgs.hpp:64-67
     const int zero = 0;
-    SCN_CUDA(cudaMemcpy(k.I + il::LB_COUNT, &zero, sizeof(int), cudaMemcpyHostToDevice));
+    set_ints(il::LB_COUNT, &zero, 1);
     set_scalar(sl::GAMMA0, 1.0);
   }
 
@@ -456,14 +483,15 @@ struct Engine {
     for (double a : v) nn += a * a;
     nn = std::sqrt(nn);
     for (double& a : v) a /= nn;
-    SCN_CUDA(cudaMemcpy(k.v, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+    // pageable source: the copy is stream-ordered and v is staged before the call returns
+    SCN_CUDA(cudaMemcpyAsync(k.v, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, st));
     set_scalar(sl::RAYLEIGH, 0.0);
     // Rounds are enqueued kBatch at a time and read once per batch: the power
     // kernel sets a sticky stop flag at the reference's stopping round (settled,
     // zero image or max_rounds), after which the remaining launches of the
     // batch, sweeps included, return at once. Same rounds, same estimate.
     const int init[3] = {0, 0, max_rounds};
-    SCN_CUDA(cudaMemcpy(k.I + il::PDONE, init, sizeof init, cudaMemcpyHostToDevice));
+    set_ints(il::PDONE, init, 3);
     struct SkipGuard {
       DevState& d;
       ~SkipGuard() { d.sweep_skip = nullptr; }
@@ -587,11 +615,7 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     }
     // fbe_grad (fbe.hpp:89-94): its elementwise part and norms run inside the
     // compact L-BFGS kernel below when that kernel is used (memory <= 6)
-    static const bool compact_on = [] {
-      const char* v = std::getenv("SCENOPT_LBFGS_COMPACT");
-      return !(v && v[0] == '0');
-    }();
-    const bool fuse_grad = !grad_valid && cfg.memory <= kLbfgsCompactMaxMem && compact_on;
+    const bool fuse_grad = !grad_valid && cfg.memory <= kLbfgsCompactMaxMem;
     if (!grad_valid) {
       e.mark("idle>grad");
       if (!hr_ready) e.sweep1(false, k.R[cur], nullptr, nullptr, k.HR);
@@ -659,14 +683,14 @@ Report solve_minfbe(Engine& e, const scenopt_solver_config& cfg, const double* y
     const uint64_t trials = static_cast<uint64_t>(e.S(sl::KSTAR)) + 1;
     rep.stats.prox_calls += trials;
     rep.stats.conj_calls += trials;
-    const double cert_fhat = e.S(sl::CERT_FHAT), hxw_rw = e.S(sl::HXW_RW), rw2 = e.S(sl::RW2);
     rep.stats.dual_grad_calls += spec.dual_grad_calls;  // the FB step at the certified point now counts
     rep.stats.prox_calls += spec.prox_calls;
     rep.stats.conj_calls += spec.conj_calls;
     if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:329-346)
       if (!spec_hr) e.read_scalars();
-      const double model = cert_fhat + lambda * hxw_rw + 0.5 * (1.0 - cfg.beta_bt) * lambda * rw2;
-      if (e.S(nxt * sl::kStateStride + sl::FHAT) > model) {
+      // f_hat(T(w)) > f_hat(w) + lam <Hx(w), R(w)> + (1 - beta)/2 lam |R(w)|^2, evaluated
+      // once, by fb_finish on the device (I[REJECT]); the host never re-rounds it
+      if (e.I(il::REJECT)) {
         lambda = halve_lambda(lambda);
         e.lbfgs_clear();
         have_pair = false;
@@ -784,14 +808,12 @@ Report solve_nama(Engine& e, const scenopt_solver_config& cfg, const double* y0d
     const uint64_t trials = static_cast<uint64_t>(e.S(sl::KSTAR)) + 1;
     rep.stats.prox_calls += trials;
     rep.stats.conj_calls += trials;
-    const double cert_fhat = e.S(sl::CERT_FHAT), hxw_rw = e.S(sl::HXW_RW), rw2 = e.S(sl::RW2);
     rep.stats.dual_grad_calls += spec.dual_grad_calls;
     rep.stats.prox_calls += spec.prox_calls;
     rep.stats.conj_calls += spec.conj_calls;
-    if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:467-483)
+    if (cfg.backtracking_rule == 0) {  // original rule (solvers.hpp:467-483), decided on the device
       if (!spec_next) e.read_scalars();
-      const double model = cert_fhat + lambda * hxw_rw + 0.5 * (1.0 - cfg.beta_bt) * lambda * rw2;
-      if (e.S(nxt * sl::kStateStride + sl::FHAT) > model) {
+      if (e.I(il::REJECT)) {
         lambda = halve_lambda(lambda);
         e.lbfgs_clear();
         have_pair = false;

@@ -155,15 +155,13 @@ def test_default_grid_uses_subtree_ownership_on_c3(gpu):
     assert info["cut_stage"] == 4  # 1024 subtrees >= 4 per CTA
 
 
-@pytest.mark.parametrize("mode", [dict(SCENOPT_SMALL_NODES="1"), dict(SCENOPT_SMALL_NODES="1", SCENOPT_SLOT_KB="4"),
-                                  dict(SCENOPT_SLOT_KB="4"), dict(SCENOPT_STAGE="consumer"),
+@pytest.mark.parametrize("mode", [dict(SCENOPT_SLOT_KB="4"), dict(SCENOPT_STAGE="consumer"),
                                   dict(SCENOPT_SLOT_KB="6", SCENOPT_STAGE="consumer"),
                                   dict(SCENOPT_SLOT_KB="4", SCENOPT_GRID="5", SCENOPT_MIN_SUBTREES="1")])
 def test_fallback_layouts_match_oracle(gpu, monkeypatch, mode):
     """Items larger than a shared-memory slot read their node blocks from HBM
     in place (kGlobalBlocks); very wide states stage vectors per consumer
-    team; small states can use warp-per-node consumers (opt-in). Forced on
-    ordinary trees, 1- and 2-RHS."""
+    team. Forced on ordinary trees, 1- and 2-RHS."""
     for k, v in mode.items():
         monkeypatch.setenv(k, v)
     rng = orc.Rng(4242)
@@ -210,23 +208,37 @@ def test_wide_states_match_oracle(gpu, dims):
     assert rep.status == "converged" and rep.verified
 
 
-def test_overlapped_host_output_is_bitwise_the_serialized_copy(gpu, monkeypatch):
-    """Host outputs copied stage by stage while the forward pass runs (device
-    completion counters + a copy stream) equal the copy after the sweep."""
-    monkeypatch.setenv("SCENOPT_OVERLAP", "1")
-    monkeypatch.setenv("SCENOPT_OVERLAP_KB", "4")  # many groups
+def test_pinned_host_outputs_match_pageable_and_stay_in_bounds(gpu):
+    """Pinned (mapped) caller buffers: the forward pass writes x / u into them
+    over PCIe while it runs. The result must equal the pageable path bit for
+    bit, and nothing may be written past u's nu*first_leaf elements (leaves
+    carry no input) or past x's nx*n elements: guard zones around both
+    buffers keep their sentinel."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2107_01745_b200 import _native as N
+
     prob = so.gen_random_instance(2, 12, 5, 9, [3, 3, 2])
     cache = so.factor(prob)
     y = np.random.default_rng(4).uniform(-1, 1, prob.dual_dim)
-    runs = [so.dual_grad(cache, prob, y) for _ in range(3)]  # overlapped (opt-in)
-    monkeypatch.setenv("SCENOPT_OVERLAP", "0")
-    cache2 = so.factor(prob)
-    ref = so.dual_grad(cache2, prob, y)
-    for pt in runs:
-        assert np.array_equal(pt.x, ref.x) and np.array_equal(pt.u, ref.u)
-    pts, _ = so.sweep(cache, [y, -y], True)
-    pts2, _ = so.sweep(cache2, [y, -y], True)
-    assert np.array_equal(pts[1].x, pts2[1].x) and np.array_equal(pts[1].u, pts2[1].u)
+    ref = so.dual_grad(cache, prob, y)
+    nx, nu, n, F = prob.nx, prob.nu, prob.num_nodes(), prob.first_leaf
+    guard = 64
+    P = C.POINTER(C.c_double)
+    for _ in range(3):
+        xb = torch.full((nx * n + 2 * guard,), 7.25, dtype=torch.float64).pin_memory()
+        ub = torch.full((nu * F + 2 * guard,), 7.25, dtype=torch.float64).pin_memory()
+        yb = torch.from_numpy(y.copy()).pin_memory()
+        xp = C.cast(xb.data_ptr() + 8 * guard, P)
+        up = C.cast(ub.data_ptr() + 8 * guard, P)
+        so.api.check(N.lib().scenopt_dual_grad(cache.device(), C.cast(yb.data_ptr(), P), xp, up, 1))
+        xs, us = xb.numpy(), ub.numpy()
+        assert np.all(xs[:guard] == 7.25) and np.all(xs[guard + nx * n:] == 7.25)
+        assert np.all(us[:guard] == 7.25) and np.all(us[guard + nu * F:] == 7.25)
+        assert np.array_equal(xs[guard:guard + nx * n], ref.x.ravel(order="F"))
+        assert np.array_equal(us[guard:guard + nu * F], ref.u.ravel(order="F"))
 
 
 @pytest.mark.parametrize("flat", ["1", "0"])

@@ -240,14 +240,20 @@ int scenopt_dev_create(const scenopt_problem* p, const scenopt_factor* f, int de
  * (one per GPU, all calling this concurrently) owns the subtrees of a
  * contiguous, byte-balanced range of the shard-stage nodes (shard_stage < 0:
  * the smallest stage with >= world nodes) and replicates the stages above.
- * Dual vectors are replicated on every rank; every sweep exchanges the
- * shard-stage contributions and assembles Hx with NCCL sum-allreduces on the
- * handle's stream; x/u outputs of the public entry points and solver reports
- * are assembled in full. nccl_id: 128 bytes from scenopt_nccl_unique_id() on
- * one rank, shared with the others (NULL: no communicator, see the phase
- * API below; world == 1 needs none). The same problem and factor must be
- * passed on every rank. Replaces nothing in the reference (single-process);
- * every other entry point accepts the sharded handle unchanged. */
+ * Primal and dual vectors are sharded the same way: a rank holds valid
+ * values on its own nodes / rows and on the replicated top. Every sweep
+ * sum-allreduces one exchange buffer (the shard-stage nodes' contributions
+ * to their parents and their dual rows); every reduction of the dual-space
+ * kernels allgathers the ranks' partial sums (a few dozen doubles) and
+ * combines them in rank order on the device, so every rank takes identical
+ * decisions. Device outputs of scenopt_dev_sweep[_async] are rank-local;
+ * host outputs of the public entry points and solver reports are assembled
+ * in full. nccl_id: 128 bytes from scenopt_nccl_unique_id() on one rank,
+ * shared with the others (NULL: no communicator, see the phase API below;
+ * world == 1 needs none). The same problem and factor must be passed on
+ * every rank. Replaces nothing in the reference (single-process); every
+ * other entry point accepts the sharded handle (solvers: memory <= 6;
+ * scenopt_linesearch_cert with explicit trials: unsharded handles only). */
 int scenopt_nccl_unique_id(void* out128);
 /* Host-only plan of the above: the shard stage actually used and the
  * world + 1 bounds of the ranks' shard-stage node ranges. */
@@ -255,13 +261,24 @@ int scenopt_shard_plan(const scenopt_problem* p, int world, int shard_stage, int
                        int32_t* bounds);
 int scenopt_dev_create_sharded(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
                                int world, int shard_stage, const void* nccl_id, scenopt_dev** out);
+/* Emulated shard group: `world` sharded handles of ONE process, driven by one
+ * host thread per rank, exchange through host memory after a stream
+ * synchronisation (no NCCL; kernels of different ranks never wait on one
+ * another, so several ranks can share one GPU). For tests of the sharded
+ * solver on one device. */
+typedef struct scenopt_shard_group scenopt_shard_group;
+int scenopt_shard_group_create(int world, scenopt_shard_group** out);
+void scenopt_shard_group_destroy(scenopt_shard_group* g);
+int scenopt_dev_create_sharded_group(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
+                                     scenopt_shard_group* g, int shard_stage, scenopt_dev** out);
 /* Sharded handles created with nccl_id == NULL leave the exchange to the
- * caller (emulating ranks on one device, tests): phase 0 zeroes Hx, runs the
- * local backward and writes this rank's shard-stage contributions into the
- * exchange buffer (zeros elsewhere); the caller sums the buffers over ranks
- * into every rank's buffer; phase 1 runs the top backward and all forward
- * work and zeroes the replicated top rows of Hx on ranks != 0, so the sum of
- * the ranks' Hx is the full Hx. Device pointers, handle stream. */
+ * caller (emulating ranks on one device, tests): phase 0 zeroes the Hx rows
+ * this rank does not write, runs the local backward and writes this rank's
+ * shard-stage contributions and dual rows into the exchange buffer (zeros
+ * elsewhere); the caller sums the buffers over ranks into every rank's
+ * buffer; phase 1 runs the top backward and all forward work and zeroes the
+ * replicated top rows of Hx on ranks != 0, so the sum of the ranks' Hx is
+ * the full Hx. Device pointers, handle stream. */
 int scenopt_shard_sweep_phase(scenopt_dev* d, int phase, int nrhs, int affine, const double* const* y,
                               double* const* Hx);
 int scenopt_shard_exchange_buffer(scenopt_dev* d, double** buf, size_t* doubles_per_rhs);

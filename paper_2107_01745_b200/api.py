@@ -24,6 +24,7 @@ __all__ = [
     "sample_initial_state",
     # riccati.hpp (+ device factor, subtree sharding)
     "FactorCache", "DeviceFactorCache", "factor", "factor_device", "refactor_affine", "nccl_unique_id",
+    "ShardGroup",
     # tree_oracles.hpp
     "OracleStats", "dual_grad", "hessian_vec", "sweep", "grad_fhat", "fhat_value", "apply_H",
     # prox.hpp / fbe.hpp / lbfgs.hpp
@@ -384,6 +385,18 @@ class FactorCache:
         self._dev = h
         return h
 
+    def shard_emulated(self, rank: int, group: "ShardGroup", device: int = 0, stage: int = -1):
+        """As shard(), for a rank of an emulated group (one process, one host
+        thread per rank; exchanges through host memory, no NCCL): tests of
+        the sharded solver with several ranks on one GPU."""
+        if self._dev is not None:
+            raise InvalidParams("shard_emulated(): the cache already has a device handle")
+        h = C.c_void_p()
+        check(N.lib().scenopt_dev_create_sharded_group(self._prob._h, self._h, device, rank, group._h, stage,
+                                                       C.byref(h)))
+        self._dev = h
+        return h
+
     def dev_info(self) -> dict:
         info = N.DevInfoC()
         check(N.lib().scenopt_dev_info_get(self.device(), C.byref(info)))
@@ -403,6 +416,21 @@ class FactorCache:
             "gain", "child_to_input", "closed_loop", "dual_to_input", "dual_to_costate",
             "input_affine", "costate_affine", "value_quad", "leaf_costate_affine")]))
         return out
+
+
+class ShardGroup:
+    """Emulated shard group of `world` ranks in this process
+    (scenopt_shard_group_create); see FactorCache.shard_emulated."""
+
+    def __init__(self, world: int):
+        self._h = C.c_void_p()
+        check(N.lib().scenopt_shard_group_create(world, C.byref(self._h)))
+        self.world = world
+
+    def __del__(self):
+        if getattr(self, "_h", None) and N._lib is not None:
+            N._lib.scenopt_shard_group_destroy(self._h)
+            self._h = None
 
 
 def nccl_unique_id() -> bytes:

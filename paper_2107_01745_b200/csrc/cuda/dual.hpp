@@ -26,6 +26,7 @@ constexpr int EVALF = 56, EVALF_INF = 57, RED0 = 58, RED1 = 59;  // API reductio
 // (solvers.hpp:279-302, 329-346, 424-438, 467-483)
 constexpr int EPS_STOP = 60, GATE_RULE = 61, BETA_BT = 62, EPS_BT = 63;
 constexpr int CURV = 64;  // L-BFGS curvatures [64, 64 + mem + 1)
+constexpr int CERT_S = 120;  // sharded certificate: coefficient totals [120, 132) between phases
 constexpr int kScalars = 192;
 }  // namespace sl
 // Int block slots.
@@ -35,6 +36,8 @@ constexpr int PDONE = 4, PROUNDS = 5, PMAX = 6;  // batched power iteration: sti
 constexpr int CONV = 7;  // last fb_finish met the stop tolerance: skip word of a speculative sweep
 constexpr int LB_ORDER = 8;  // [8, 8 + mem + 1): slot ids, oldest first, then free slots
 constexpr int REJECT = 100;  // last fb_finish: the backtracking rule in S[GATE_RULE] rejects the step
+constexpr int CSTATE = 101;  // sharded certificate: state after phase k at CSTATE + k - 1 (k = 1..3)
+constexpr int CKSTAR = 105;  // sharded certificate: accepted trial between phases
 constexpr int kInts = 128;
 }  // namespace il
 
@@ -61,7 +64,22 @@ struct DualCtx {
   int* pubI = nullptr;
   unsigned* pubSeq = nullptr;
   unsigned seq = 0;
+  // Subtree-sharded handles. Reductions count only the rows
+  // with cnt[i] != 0 (this rank's own rows; the replicated top on rank 0),
+  // and every reduction becomes a phase boundary: phase 0 ends with this
+  // rank's totals in xs, the launcher allgathers them over the ranks (xc,
+  // a Comm*), and phase 1 combines xr in rank order and carries on. Every
+  // rank then holds bitwise-identical scalars.
+  const uint8_t* cnt = nullptr;
+  void* xc = nullptr;     // host: the handle's communicator (null: single-launch kernels)
+  int world = 1;
+  double* xs = nullptr;   // [kXMax] this rank's totals
+  double* xr = nullptr;   // [world][kXMax] gathered totals
+  int phase = -1;         // set by the launchers
 };
+constexpr int kXMax = 160;  // doubles exchanged per rank and phase
+// allgather of n doubles per rank through a Comm* (comm.cpp), on st
+void dual_allgather(void* xc, const double* send, double* recv, size_t n, cudaStream_t st);
 
 // fb_step / rescale_state finish (fbe.hpp:38-67). mode 0: fhat from the
 // quadratic identity fhat(y) = fhat(0) - 1/2 <Hx(0) + Hx(y), y>; mode 1: keep

@@ -97,6 +97,57 @@ __device__ void grid_reduce(const DualCtx& c, int& ph, double (&v)[K]) {
   ph ^= 1;
 }
 
+// ---- sharded handles (DualCtx: cnt / xs / xr / phase)
+__device__ __forceinline__ bool counted(const DualCtx& c, int64_t i) { return !c.cnt || c.cnt[i]; }
+
+// This rank's totals of K per-thread values into xs[off, off + K) (every
+// block takes part in the grid reduction; block 0 writes).
+template <int K, int MAXFROM = K>
+__device__ void xsend(const DualCtx& c, int& ph, double (&v)[K], int off) {
+  grid_reduce<K, false, MAXFROM>(c, ph, v);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) c.xs[off + k] = v[k];
+  }
+}
+// The ranks' totals gathered in xr, combined in rank order (sum; max from
+// MAXFROM on): bitwise the same on every rank and every block.
+template <int K, int MAXFROM = K>
+__device__ void xrecv(const DualCtx& c, double (&v)[K], int off) {
+  __shared__ double tot[kMaxRed];
+  static_assert(K <= kMaxRed, "xrecv: at most kMaxRed values");
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int k = threadIdx.x;
+    const bool mx = k >= MAXFROM;
+    double t = c.xr[off + k];
+    for (int q = 1; q < c.world; ++q) {
+      const double u = c.xr[q * kXMax + off + k];
+      t = mx ? fmax(t, u) : t + u;
+    }
+    tot[k] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = tot[k];
+}
+// One reduction point of a kernel. Unsharded: the grid reduction. Sharded
+// phase 0: this rank's totals go to xs and the kernel must return (false);
+// phase 1: the totals of all ranks from xr.
+template <int K, bool MAX = false, int MAXFROM = (MAX ? 0 : K)>
+__device__ bool xreduce(const DualCtx& c, int& ph, double (&v)[K]) {
+  if (c.phase < 0) {
+    grid_reduce<K, MAX, MAXFROM>(c, ph, v);
+    return true;
+  }
+  if (c.phase == 0) {
+    xsend<K, MAXFROM>(c, ph, v, 0);
+    return false;
+  }
+  xrecv<K, MAXFROM>(c, v, 0);
+  return true;
+}
+
 // prox of gamma_prox * g on one row (prox.hpp:58-81).
 __device__ __forceinline__ double prox_row(int kind, double v, double lo, double hi, double thr) {
   if (kind == 1) return fmin(fmax(v, lo), hi);
@@ -124,23 +175,27 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
   const double lam = S[sl::LAM];
   const double gp = 1.0 / lam;
   double s[6] = {0, 0, 0, 0, 0, 0};  // conj, z2, Hx.R, R2, (Hx0+Hx).y; [5] weighted inf residual (max)
-  for (int i = gtid(); i < c.D; i += gstride()) {
-    const int kd = c.g.kind[i];
-    const double yi = y[i], hi = Hx[i];
-    const double zi = prox_row(kd, yi / lam + hi, c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
-    const double Ri = zi - hi;
-    const double Ti = yi - lam * Ri;
-    z[i] = zi;
-    R[i] = Ri;
-    T[i] = Ti;
-    s[0] += conj_row(kd, Ti, c.g.lo[i], c.g.hi[i], c.g.wg[i]);
-    s[1] += zi * zi;
-    s[2] += hi * Ri;
-    s[3] += Ri * Ri;
-    if (mode == 0) s[4] += (Hx0[i] + hi) * yi;
-    s[5] = fmax(s[5], fabs(weight ? Ri * weight[i] : Ri));
-  }
-  grid_reduce<6, false, 5>(c, ph, s);  // one barrier: five sums and the max
+  if (c.phase <= 0)
+    for (int i = gtid(); i < c.D; i += gstride()) {
+      const int kd = c.g.kind[i];
+      const double yi = y[i], hi = Hx[i];
+      const double zi = prox_row(kd, yi / lam + hi, c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
+      const double Ri = zi - hi;
+      const double Ti = yi - lam * Ri;
+      z[i] = zi;
+      R[i] = Ri;
+      T[i] = Ti;
+      if (counted(c, i)) {
+        s[0] += conj_row(kd, Ti, c.g.lo[i], c.g.hi[i], c.g.wg[i]);
+        s[1] += zi * zi;
+        s[2] += hi * Ri;
+        s[3] += Ri * Ri;
+        if (mode == 0) s[4] += (Hx0[i] + hi) * yi;
+        s[5] = fmax(s[5], fabs(weight ? Ri * weight[i] : Ri));
+      }
+    }
+  if (c.phase == 1 && blockIdx.x != 0) return;  // block 0 finishes
+  if (!xreduce<6, false, 5>(c, ph, s)) return;  // one barrier: five sums and the max
   const double m[1] = {s[5]};
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const double fhat = mode == 0 ? c.S[sl::FHAT0] - 0.5 * s[4] : S[sl::FHAT];
@@ -184,15 +239,18 @@ __global__ void __launch_bounds__(kThreads) fbe_grad_kernel(DualCtx c, int st, c
   int ph = 0;
   const double lam = c.S[st * sl::kStateStride + sl::LAM];
   double s[2] = {0, 0};
-  for (int i = gtid(); i < c.D; i += gstride()) {
-    const double Ri = R[i];
-    const double gi = Ri + lam * HR[i];
-    grad[i] = gi;
-    const double img = (gi - Ri) / lam;
-    s[0] += img * img;
-    s[1] += Ri * Ri;
-  }
-  grid_reduce<2>(c, ph, s);
+  if (c.phase <= 0)
+    for (int i = gtid(); i < c.D; i += gstride()) {
+      const double Ri = R[i];
+      const double gi = Ri + lam * HR[i];
+      grad[i] = gi;
+      const double img = (gi - Ri) / lam;
+      if (counted(c, i)) {
+        s[0] += img * img;
+        s[1] += Ri * Ri;
+      }
+    }
+  if (!xreduce<2>(c, ph, s)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     c.S[sl::IMG2] = s[0];
     c.S[sl::R2] = s[1];
@@ -381,17 +439,27 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
   double* sf = Sb + static_cast<int64_t>(f) * D;
   double* qf = Qb + static_cast<int64_t>(f) * D;
   const double flam = fR ? c.S[fstate * sl::kStateStride + sl::LAM] : 0.0;
-  for (int64_t i = gtid(); i < D; i += gstride()) {
+  for (int64_t i = gtid(); c.phase <= 0 && i < D; i += gstride()) {
+    const bool ci = counted(c, i);
     double gi;
     if (fR) {
       const double Ri = fR[i];
       gi = Ri + flam * fHR[i];
       gout[i] = gi;
       const double img = (gi - Ri) / flam;
-      v[kCompactK - 2] += img * img;
-      v[kCompactK - 1] += Ri * Ri;
+      if (ci) {
+        v[kCompactK - 2] += img * img;
+        v[kCompactK - 1] += Ri * Ri;
+      }
     } else {
       gi = gv[i];
+    }
+    if (!ci) {  // not this rank's row: the new pair's entries only
+      if (do_push) {
+        sf[i] = a[i] - b[i];
+        qf[i] = (fR ? gi : cc[i]) - dd[i];
+      }
+      continue;
     }
     if (do_push) {
       const double si = a[i] - b[i], qi = (fR ? gi : cc[i]) - dd[i], di = dd[i];
@@ -421,7 +489,7 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
         }
     }
   }
-  grid_reduce<kCompactK>(c, ph, v);
+  if (!xreduce<kCompactK>(c, ph, v)) return;
   // the serial part indexes the totals at run time: from shared memory, so
   // that v stays in registers through the accumulation above
   __shared__ double vs[kCompactK];
@@ -531,6 +599,11 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
 }
 
 // ---------------------------------------------------------------- K4 / K6
+// Line-search certificate (fbe.hpp:105-231) and the tau search of
+// solvers.hpp:310-325 / 440-464. The row arithmetic and the scalar decisions
+// live in shared helpers so that the single-launch kernel and the sharded
+// phase kernel compute bit-identical values (a world-1 sharded solve equals
+// the unsharded one bitwise).
 struct Taus {
   double t[16];
 };
@@ -544,6 +617,217 @@ __device__ __forceinline__ double tau_at(const Taus& taus, int k) {
   return t;
 }
 
+// Row arithmetic of the certificate with explicit round-to-nearest
+// operations (no FMA contraction): the single-launch and the sharded kernel
+// inline these into different code, and the compiler must not be free to
+// fuse them differently. This is also the CPU oracle's arithmetic
+// (-ffp-contract=off).
+__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a, b); }
+
+struct CertRow {
+  double an, di, ha, hd;  // anchor, direction, Hx(anchor), Hx0(direction)
+};
+// shifted (NAMA, fbe.hpp:172-203): anchor y - lam R, direction d + lam R
+__device__ __forceinline__ CertRow cert_row(int shifted, double lam, const double* y, const double* R,
+                                            const double* Hx, const double* HR, const double* d,
+                                            const double* Hd, int64_t i) {
+  CertRow r{y[i], d[i], Hx[i], Hd[i]};
+  if (shifted) {
+    const double rr = mul_(-lam, R[i]);
+    const double hr = mul_(-lam, HR[i]);
+    r.an = add_(r.an, rr);
+    r.di = sub_(r.di, rr);
+    r.ha = add_(r.ha, hr);
+    r.hd = sub_(r.hd, hr);
+  }
+  return r;
+}
+// trial tau of one row: z = prox(pb + tau ps), R = z - (ha + tau hd), T = (an + tau di) - lam R
+struct CertTrial {
+  double z, Rt, Tt, hxw;
+};
+__device__ __forceinline__ CertTrial cert_trial(const CertRow& r, int kd, double lo, double hi, double wg,
+                                                double lam, double gp, double pb, double ps, double tau) {
+  CertTrial t;
+  t.z = prox_row(kd, add_(pb, mul_(tau, ps)), lo, hi, gp * wg);
+  t.hxw = add_(r.ha, mul_(tau, r.hd));
+  t.Rt = sub_(t.z, t.hxw);
+  t.Tt = sub_(add_(r.an, mul_(tau, r.di)), mul_(lam, t.Rt));
+  return t;
+}
+// Row i of the first pass: coefficient sums s[0..12) (fbe.hpp:136-143 and the
+// shifted anchor quantities, fbe.hpp:172-203) and, when fused, the 8 trials
+// tau = 2^-q (conj, |z|^2 at fx[2q], fx[2q+1]) plus the tau = 1 final-pass
+// sums fx[16], fx[17] and the tau = 1 iterate into y_next.
+__device__ __forceinline__ void cert_first_row(const DualCtx& c, int shifted, int tlambda, double lam, double gp,
+                                               const double* y, const double* R, const double* Hx,
+                                               const double* HR, const double* d, const double* Hd,
+                                               double* y_next, int64_t i, bool ci, bool fused, double (&s)[12],
+                                               double (&fx)[18]) {
+  const CertRow r = cert_row(shifted, lam, y, R, Hx, HR, d, Hd, i);
+  const int kd = c.g.kind[i];
+  const double lo = c.g.lo[i], hi = c.g.hi[i], wg = c.g.wg[i];
+  if (shifted && ci) {
+    const double rr = mul_(-lam, R[i]);
+    const double hr = mul_(-lam, HR[i]);
+    s[4] = add_(s[4], mul_(Hx[i], rr));
+    s[5] = add_(s[5], mul_(rr, hr));
+    const double za = prox_row(kd, add_(r.an / lam, r.ha), lo, hi, gp * wg);
+    const double ra = sub_(za, r.ha);
+    s[6] = add_(s[6], conj_row(kd, sub_(r.an, mul_(lam, ra)), lo, hi, wg));
+    s[7] = add_(s[7], mul_(za, za));
+    s[8] = add_(s[8], mul_(r.ha, ra));
+    s[9] = add_(s[9], mul_(ra, ra));
+    s[10] = add_(s[10], mul_(HR[i], HR[i]));
+    s[11] = add_(s[11], mul_(R[i], R[i]));
+  }
+  if (ci) {
+    s[0] = add_(s[0], mul_(r.di, r.hd));
+    s[1] = add_(s[1], mul_(r.hd, r.hd));
+    s[2] = add_(s[2], mul_(r.ha, add_(r.di, mul_(lam, r.hd))));
+    s[3] = add_(s[3], mul_(r.ha, r.di));
+  }
+  if (!fused) return;
+  const double pb = add_(r.an / lam, r.ha), ps = add_(r.di / lam, r.hd);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const CertTrial t = cert_trial(r, kd, lo, hi, wg, lam, gp, pb, ps, ldexp(1.0, -q));
+    if (q == 0) {  // the final pass's quantities at tau = 1
+      if (y_next) y_next[i] = tlambda ? t.Tt : sub_(y[i], mul_(lam, t.Rt));
+      if (ci) {
+        fx[16] = add_(fx[16], mul_(t.hxw, t.Rt));
+        fx[17] = add_(fx[17], mul_(t.Rt, t.Rt));
+      }
+    }
+    if (ci) {
+      fx[2 * q] = add_(fx[2 * q], conj_row(kd, t.Tt, lo, hi, wg));
+      fx[2 * q + 1] = add_(fx[2 * q + 1], mul_(t.z, t.z));
+    }
+  }
+}
+// Row i of a batch of 8 trials tq[q] (evaluate_cert, fbe.hpp:214-231)
+__device__ __forceinline__ void cert_batch_row(const DualCtx& c, int shifted, double lam, double gp,
+                                               const double* y, const double* R, const double* Hx,
+                                               const double* HR, const double* d, const double* Hd, int64_t i,
+                                               const double (&tq)[8], double (&acc)[16]) {
+  const CertRow r = cert_row(shifted, lam, y, R, Hx, HR, d, Hd, i);
+  const int kd = c.g.kind[i];
+  const double lo = c.g.lo[i], hi = c.g.hi[i], wg = c.g.wg[i];
+  const double pb = add_(r.an / lam, r.ha), ps = add_(r.di / lam, r.hd);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const CertTrial t = cert_trial(r, kd, lo, hi, wg, lam, gp, pb, ps, tq[q]);
+    acc[2 * q] = add_(acc[2 * q], conj_row(kd, t.Tt, lo, hi, wg));
+    acc[2 * q + 1] = add_(acc[2 * q + 1], mul_(t.z, t.z));
+  }
+}
+// Row i of the final pass at tau*: the next iterate (and the trial vectors
+// on the test path), and the sums <Hx(w), R(w)>, |R(w)|^2
+__device__ __forceinline__ void cert_final_row(const DualCtx& c, int shifted, int tlambda, double lam, double gp,
+                                               const double* y, const double* R, const double* Hx,
+                                               const double* HR, const double* d, const double* Hd,
+                                               double* y_next, double* ow, double* oHxw, double* oz, double* oR,
+                                               double* oT, int64_t i, bool ci, double tau, double (&f2)[2]) {
+  const CertRow r = cert_row(shifted, lam, y, R, Hx, HR, d, Hd, i);
+  const double pb = add_(r.an / lam, r.ha), ps = add_(r.di / lam, r.hd);
+  const int kd = c.g.kind[i];
+  const CertTrial t = cert_trial(r, kd, c.g.lo[i], c.g.hi[i], c.g.wg[i], lam, gp, pb, ps, tau);
+  if (y_next) y_next[i] = tlambda ? t.Tt : sub_(y[i], mul_(lam, t.Rt));
+  if (ow) {
+    ow[i] = add_(r.an, mul_(tau, r.di));
+    oHxw[i] = t.hxw;
+    oz[i] = t.z;
+    oR[i] = t.Rt;
+    oT[i] = t.Tt;
+  }
+  if (ci) {
+    f2[0] = add_(f2[0], mul_(t.hxw, t.Rt));
+    f2[1] = add_(f2[1], mul_(t.Rt, t.Rt));
+  }
+}
+
+// Scalar decisions, written with explicit round-to-nearest operations (no
+// FMA contraction) so that both kernels, inlined anywhere, round alike; the
+// operation order is C++'s left-to-right order of the reference's formulas
+// (fbe.hpp:136-143, 189, 214-231; solvers.hpp:313-325).
+struct CertScalars {
+  double quad, alpha1, alpha2, fhat_a, conj_a, zn2_a, value_a, value, slack, lam;
+};
+__device__ __forceinline__ CertScalars cert_scalars(const double* S0, int shifted, const double* s) {
+  CertScalars k;
+  k.lam = S0[sl::LAM];
+  k.value = S0[sl::VALUE];
+  const double fhat = S0[sl::FHAT];
+  const double hl = __dmul_rn(0.5, k.lam);
+  k.quad = s[0];
+  k.alpha2 = __dsub_rn(__dmul_rn(-0.5, k.quad), __dmul_rn(hl, s[1]));  // -q/2 - lam |Hd|^2 / 2
+  k.alpha1 = -s[2];
+  if (shifted) {
+    k.fhat_a = __dsub_rn(__dsub_rn(fhat, s[4]), __dmul_rn(0.5, s[5]));
+    k.conj_a = s[6];
+    k.zn2_a = s[7];
+    k.value_a = __dadd_rn(__dadd_rn(__dadd_rn(k.fhat_a, k.conj_a), __dmul_rn(k.lam, s[8])), __dmul_rn(hl, s[9]));
+  } else {
+    k.fhat_a = fhat;
+    k.conj_a = S0[sl::CONJ];
+    k.zn2_a = S0[sl::ZN2];
+    k.value_a = k.value;
+  }
+  k.slack = __dmul_rn(1e-12, __dadd_rn(1.0, fabs(k.value)));
+  return k;
+}
+__device__ __forceinline__ double cert_delta(const CertScalars& k, double tau, double conj, double z2) {
+  const double quad = __dadd_rn(__dmul_rn(__dmul_rn(k.alpha2, tau), tau), __dmul_rn(k.alpha1, tau));
+  return __dadd_rn(__dsub_rn(__dadd_rn(quad, conj), k.conj_a),
+                   __dmul_rn(__dmul_rn(0.5, k.lam), __dsub_rn(z2, k.zn2_a)));
+}
+__device__ __forceinline__ double cert_fhat(const CertScalars& k, double s3, double tau) {
+  return __dsub_rn(__dsub_rn(k.fhat_a, __dmul_rn(tau, s3)), __dmul_rn(__dmul_rn(__dmul_rn(0.5, tau), tau), k.quad));
+}
+// first accepted trial tau = 2^-(base+q), q < nq, of one batch (acc: conj,
+// |z|^2 per trial); -1: none. The slack is 1e-12 (1 + |phi(y)|).
+__device__ __forceinline__ int cert_pick(const CertScalars& k, int shifted, int base, int nq, const double* acc,
+                                         double& tau_out, double& delta_out) {
+  for (int q = 0; q < nq; ++q) {
+    const double tau = ldexp(1.0, -(base + q));
+    const double delta = cert_delta(k, tau, acc[2 * q], acc[2 * q + 1]);
+    const bool ok = shifted ? (__dadd_rn(k.value_a, delta) <= __dadd_rn(k.value, k.slack)) : (delta <= k.slack);
+    if (ok) {
+      tau_out = tau;
+      delta_out = delta;
+      return base + q;
+    }
+  }
+  return -1;
+}
+__device__ __forceinline__ void cert_finalize(const DualCtx& c, const CertScalars& k, const double* s, int kstar,
+                                              double tau_star, double delta_star, double f20, double f21) {
+  c.S[sl::TAU] = tau_star;
+  c.S[sl::KSTAR] = kstar;
+  c.S[sl::STALL] = kstar < 0 ? 1.0 : 0.0;
+  c.S[sl::CERT_FHAT] = cert_fhat(k, s[3], tau_star);
+  c.S[sl::HXW_RW] = f20;
+  c.S[sl::RW2] = f21;
+  c.S[sl::VALUE_A] = k.value_a;
+  c.S[sl::CONJ_A] = k.conj_a;
+  c.S[sl::ZN2_A] = k.zn2_a;
+  c.S[sl::FHAT_A] = k.fhat_a;
+  c.S[sl::ALPHA1] = k.alpha1;
+  c.S[sl::ALPHA2] = k.alpha2;
+  c.S[sl::DELTA] = delta_star;
+  c.S[sl::HR2] = s[10];
+  c.S[sl::RR2] = s[11];
+}
+
+// Single-launch certificate + tau search. In the solver path (no explicit
+// taus) the first pass also evaluates the first batch of 8 trials and the
+// final-pass sums and iterate for tau = 1, so when the full step is accepted
+// (the common case) the whole search is this one pass and one reduction.
+// Every sum keeps its own reduction tree: results are bitwise those of
+// separate passes. Explicit taus (test / API path): deltas and f_hat of each
+// trial, the last trial's vectors.
 __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int shifted, int tlambda,
                                                         const double* y, const double* R, const double* Hx,
                                                         const double* HR, const double* d, const double* Hd,
@@ -553,70 +837,15 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
   int ph = 0;
   const double* S0 = c.S + st * sl::kStateStride;
   const double lam = S0[sl::LAM], gp = 1.0 / lam;
-  const double value = S0[sl::VALUE], fhat = S0[sl::FHAT];
-  // pass 1: coefficients (fbe.hpp:136-143) and, for the shifted form, the
-  // anchor quantities (fbe.hpp:172-203). In the solver path (no explicit
-  // taus) the same pass also evaluates the first batch of 8 trials and the
-  // final-pass sums and iterate for tau = 1, so when the full step is accepted
-  // (the common case) the whole search is this one pass and one reduction.
-  // Every sum keeps its own reduction tree: results are bitwise those of the
-  // separate passes.
-  double s[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  // 0 <dir,Hxd> 1 |Hxd|^2 2 <Hxa, dir + lam Hxd> 3 <Hxa,dir> 4 <Hx,r> 5 <r,Hr>
-  // 6 conj_a 7 |z_a|^2 8 <Hxa,res_a> 9 |res_a|^2 10 |HR|^2 11 |R|^2
   const bool fused = ntau_explicit <= 0;
-  double fx[18];  // fused: 16 batch-0 trial sums, then <Hxw,Rw>, |Rw|^2 at tau = 1
+  double s[12], fx[18];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) s[q] = 0.0;
 #pragma unroll
   for (int q = 0; q < 18; ++q) fx[q] = 0.0;
-  for (int i = gtid(); i < c.D; i += gstride()) {
-    double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
-    if (shifted) {
-      const double r = -lam * R[i];
-      const double hr = -lam * HR[i];
-      s[4] += Hx[i] * r;
-      s[5] += r * hr;
-      an = an + r;
-      di = di - r;
-      ha = ha + hr;
-      hd = hd - hr;
-      const int kd = c.g.kind[i];
-      const double za = prox_row(kd, an / lam + ha, c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
-      const double ra = za - ha;
-      s[6] += conj_row(kd, an - lam * ra, c.g.lo[i], c.g.hi[i], c.g.wg[i]);
-      s[7] += za * za;
-      s[8] += ha * ra;
-      s[9] += ra * ra;
-      s[10] += HR[i] * HR[i];
-      s[11] += R[i] * R[i];
-    }
-    s[0] += di * hd;
-    s[1] += hd * hd;
-    s[2] += ha * (di + lam * hd);
-    s[3] += ha * di;
-    if (fused) {
-      const double pb = an / lam + ha, ps = di / lam + hd;
-      const int kd = c.g.kind[i];
-      const double lo = c.g.lo[i], hi = c.g.hi[i], wg = c.g.wg[i];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double tau = ldexp(1.0, -q);
-        const double z = prox_row(kd, pb + tau * ps, lo, hi, gp * wg);
-        const double Rt = z - (ha + tau * hd);
-        const double Tt = (an + tau * di) - lam * Rt;
-        fx[2 * q] += conj_row(kd, Tt, lo, hi, wg);
-        fx[2 * q + 1] += z * z;
-        if (q == 0) {  // the final pass's quantities at tau = 1
-          const double hxw = ha + hd;
-          const double z1 = prox_row(kd, pb + ps, lo, hi, gp * wg);
-          const double R1 = z1 - hxw;
-          const double T1 = (an + di) - lam * R1;
-          if (y_next) y_next[i] = tlambda ? T1 : y[i] - lam * R1;
-          fx[16] += hxw * R1;
-          fx[17] += R1 * R1;
-        }
-      }
-    }
-  }
+  for (int64_t i = gtid(); i < c.D; i += gstride())
+    cert_first_row(c, shifted, tlambda, lam, gp, y, R, Hx, HR, d, Hd, fused ? y_next : nullptr, i, true, fused, s,
+                   fx);
   double sv[30];
 #pragma unroll
   for (int q = 0; q < 12; ++q) sv[q] = s[q];
@@ -631,23 +860,7 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
   }
 #pragma unroll
   for (int q = 0; q < 12; ++q) s[q] = sv[q];
-  const double quad = s[0];
-  const double alpha2 = -0.5 * quad - 0.5 * lam * s[1];
-  const double alpha1 = -s[2];
-  double fhat_a, conj_a, zn2_a, value_a;
-  if (shifted) {
-    fhat_a = fhat - s[4] - 0.5 * s[5];
-    conj_a = s[6];
-    zn2_a = s[7];
-    value_a = fhat_a + conj_a + lam * s[8] + 0.5 * lam * s[9];
-  } else {
-    fhat_a = fhat;
-    conj_a = S0[sl::CONJ];
-    zn2_a = S0[sl::ZN2];
-    value_a = value;
-  }
-  const double slack = 1e-12 * (1.0 + fabs(value));
-  // tau search: batches of 8 speculative trials (evaluate_cert, fbe.hpp:214-231)
+  const CertScalars k = cert_scalars(S0, shifted, s);
   int kstar = -1;
   double tau_star = 0.0, delta_star = 0.0;
   const int ntau = ntau_explicit > 0 ? ntau_explicit : 61;
@@ -665,50 +878,18 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
 #pragma unroll
       for (int q = 0; q < 16; ++q) acc[q] = sv[12 + q];
     } else {
-    for (int i = gtid(); i < c.D; i += gstride()) {
-      double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
-      if (shifted) {
-        const double r = -lam * R[i];
-        const double hr = -lam * HR[i];
-        an = an + r;
-        di = di - r;
-        ha = ha + hr;
-        hd = hd - hr;
-      }
-      const double pb = an / lam + ha, ps = di / lam + hd;
-      const int kd = c.g.kind[i];
-      const double lo = c.g.lo[i], hi = c.g.hi[i], wg = c.g.wg[i];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double tau = tq[q];
-        const double z = prox_row(kd, pb + tau * ps, lo, hi, gp * wg);
-        const double Rt = z - (ha + tau * hd);
-        const double Tt = (an + tau * di) - lam * Rt;
-        acc[2 * q] += conj_row(kd, Tt, lo, hi, wg);
-        acc[2 * q + 1] += z * z;
-      }
+      for (int64_t i = gtid(); i < c.D; i += gstride()) cert_batch_row(c, shifted, lam, gp, y, R, Hx, HR, d, Hd, i, tq, acc);
+      grid_reduce<16>(c, ph, acc);
     }
-    grid_reduce<16>(c, ph, acc);
-    }
-    for (int q = 0; q < 8 && base + q < ntau; ++q) {
-      const double tau = tq[q];
-      const double delta =
-          alpha2 * tau * tau + alpha1 * tau + acc[2 * q] - conj_a + 0.5 * lam * (acc[2 * q + 1] - zn2_a);
-      if (ntau_explicit > 0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-          deltas[base + q] = delta;
-          cfh[base + q] = fhat_a - tau * s[3] - 0.5 * tau * tau * quad;
+    if (ntau_explicit > 0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int q = 0; q < 8 && base + q < ntau; ++q) {
+          deltas[base + q] = cert_delta(k, tq[q], acc[2 * q], acc[2 * q + 1]);
+          cfh[base + q] = cert_fhat(k, s[3], tq[q]);
         }
-        continue;
-      }
-      const bool ok = shifted ? (value_a + delta <= value + slack) : (delta <= slack);
-      if (ok) {
-        kstar = base + q;
-        tau_star = tau;
-        delta_star = delta;
-        break;
-      }
+      continue;
     }
+    kstar = cert_pick(k, shifted, base, ntau - base < 8 ? ntau - base : 8, acc, tau_star, delta_star);
   }
   if (ntau_explicit > 0) {  // vectors of the last tau (test path)
     kstar = ntau - 1;
@@ -722,53 +903,140 @@ __global__ void __launch_bounds__(kThreads) cert_kernel(DualCtx c, int st, int s
     f2[0] = sv[28];
     f2[1] = sv[29];
   } else if (kstar >= 0) {
-    const double tau = tau_star;
-    for (int i = gtid(); i < c.D; i += gstride()) {
-      double an = y[i], di = d[i], ha = Hx[i], hd = Hd[i];
-      if (shifted) {
-        const double r = -lam * R[i];
-        const double hr = -lam * HR[i];
-        an = an + r;
-        di = di - r;
-        ha = ha + hr;
-        hd = hd - hr;
-      }
-      const double pb = an / lam + ha, ps = di / lam + hd;
-      const int kd = c.g.kind[i];
-      const double z = prox_row(kd, pb + tau * ps, c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
-      const double w = an + tau * di;
-      const double hxw = ha + tau * hd;
-      const double Rt = z - hxw;
-      const double Tt = w - lam * Rt;
-      if (y_next) y_next[i] = tlambda ? Tt : y[i] - lam * Rt;
-      if (ow) {
-        ow[i] = w;
-        oHxw[i] = hxw;
-        oz[i] = z;
-        oR[i] = Rt;
-        oT[i] = Tt;
-      }
-      f2[0] += hxw * Rt;
-      f2[1] += Rt * Rt;
-    }
+    for (int64_t i = gtid(); i < c.D; i += gstride())
+      cert_final_row(c, shifted, tlambda, lam, gp, y, R, Hx, HR, d, Hd, y_next, ow, oHxw, oz, oR, oT, i, true,
+                     tau_star, f2);
   }
   if (!have_f2) grid_reduce<2>(c, ph, f2);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    c.S[sl::TAU] = tau_star;
-    c.S[sl::KSTAR] = kstar;
-    c.S[sl::STALL] = kstar < 0 ? 1.0 : 0.0;
-    c.S[sl::CERT_FHAT] = fhat_a - tau_star * s[3] - 0.5 * tau_star * tau_star * quad;
-    c.S[sl::HXW_RW] = f2[0];
-    c.S[sl::RW2] = f2[1];
-    c.S[sl::VALUE_A] = value_a;
-    c.S[sl::CONJ_A] = conj_a;
-    c.S[sl::ZN2_A] = zn2_a;
-    c.S[sl::FHAT_A] = fhat_a;
-    c.S[sl::ALPHA1] = alpha1;
-    c.S[sl::ALPHA2] = alpha2;
-    c.S[sl::DELTA] = delta_star;
-    c.S[sl::HR2] = s[10];
-    c.S[sl::RR2] = s[11];
+  if (blockIdx.x == 0 && threadIdx.x == 0) cert_finalize(c, k, s, kstar, tau_star, delta_star, f2[0], f2[1]);
+}
+
+// ---------------------------------------------------------------- K4 / K6, sharded handles
+// The same certificate and tau search with every reduction a cross-rank
+// phase boundary (DualCtx). Phases (the launcher always issues four, with an
+// allgather after each of the first three):
+//   0: cert_kernel's fused first pass over this rank's rows;
+//   1: decide in batch 0. tau* = 1 -> done. tau* in batch 0 -> final pass at
+//      tau*, its two sums sent. No accept -> the sums of trials 8..60 sent;
+//   2: no accept in batch 0: decide among 8..60, final pass at tau* (or
+//      stall). Else finish the pending final pass;
+//   3: finish a final pass started in phase 2.
+// The state after phase k is I[CSTATE + k - 1]; phase k reads the previous
+// one, so no block can observe a state written in its own launch. The
+// coefficient totals persist in S[CERT_S ..] between phases.
+constexpr int kCertDone = 0, kCertNeedF2 = 1, kCertNeedBatches = 2;
+
+__global__ void __launch_bounds__(kThreads) cert_shard_kernel(DualCtx c, int st, int shifted, int tlambda,
+                                                              const double* y, const double* R, const double* Hx,
+                                                              const double* HR, const double* d, const double* Hd,
+                                                              double* y_next) {
+  int ph = 0;
+  const double* S0 = c.S + st * sl::kStateStride;
+  const double lam = S0[sl::LAM], gp = 1.0 / lam;
+  const int stage = c.phase;
+  const bool b0 = blockIdx.x == 0 && threadIdx.x == 0;
+  auto final_pass = [&](double tau) {  // this rank's f2 sums go out
+    double f2[2] = {0, 0};
+    for (int64_t i = gtid(); i < c.D; i += gstride())
+      cert_final_row(c, shifted, tlambda, lam, gp, y, R, Hx, HR, d, Hd, y_next, nullptr, nullptr, nullptr, nullptr,
+                     nullptr, i, counted(c, i), tau, f2);
+    xsend<2>(c, ph, f2, 0);
+  };
+  if (stage == 0) {
+    double s[12], fx[18];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) s[q] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 18; ++q) fx[q] = 0.0;
+    for (int64_t i = gtid(); i < c.D; i += gstride())
+      cert_first_row(c, shifted, tlambda, lam, gp, y, R, Hx, HR, d, Hd, y_next, i, counted(c, i), true, s, fx);
+    double sv[30];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) sv[q] = s[q];
+#pragma unroll
+    for (int q = 0; q < 18; ++q) sv[12 + q] = fx[q];
+    xsend<30>(c, ph, sv, 0);
+    return;
+  }
+  if (stage == 1) {
+    double sv[30];
+    xrecv<30>(c, sv, 0);
+    const CertScalars k = cert_scalars(S0, shifted, sv);
+    double tau = 0.0, delta = 0.0;
+    const int kstar = cert_pick(k, shifted, 0, 8, sv + 12, tau, delta);
+    if (b0)
+      for (int q = 0; q < 12; ++q) c.S[sl::CERT_S + q] = sv[q];
+    if (kstar == 0) {
+      if (b0) {
+        cert_finalize(c, k, sv, 0, tau, delta, sv[28], sv[29]);
+        c.I[il::CSTATE] = kCertDone;
+      }
+      return;
+    }
+    if (kstar > 0) {
+      final_pass(tau);
+      if (b0) {
+        c.I[il::CSTATE] = kCertNeedF2;
+        c.I[il::CKSTAR] = kstar;
+        c.S[sl::TAU] = tau;
+        c.S[sl::DELTA] = delta;
+      }
+      return;
+    }
+    // no accept in batch 0: this rank's sums of trials 8..60, 8 per pass
+    for (int chunk = 0; chunk < 7; ++chunk) {
+      double acc[16], tq[8];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) tq[q] = ldexp(1.0, -(8 + chunk * 8 + q));
+      for (int64_t i = gtid(); i < c.D; i += gstride())
+        if (counted(c, i)) cert_batch_row(c, shifted, lam, gp, y, R, Hx, HR, d, Hd, i, tq, acc);
+      xsend<16>(c, ph, acc, chunk * 16);
+    }
+    if (b0) c.I[il::CSTATE] = kCertNeedBatches;
+    return;
+  }
+  // stages 2 and 3
+  const int state = c.I[il::CSTATE + stage - 2];  // after the previous phase
+  if (state == kCertDone) {
+    if (b0) c.I[il::CSTATE + stage - 1] = kCertDone;
+    return;
+  }
+  double s[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) s[q] = c.S[sl::CERT_S + q];
+  const CertScalars k = cert_scalars(S0, shifted, s);
+  if (state == kCertNeedF2) {
+    double f2[2];
+    xrecv<2>(c, f2, 0);
+    if (b0) {
+      cert_finalize(c, k, s, c.I[il::CKSTAR], c.S[sl::TAU], c.S[sl::DELTA], f2[0], f2[1]);
+      c.I[il::CSTATE + stage - 1] = kCertDone;
+    }
+    return;
+  }
+  // kCertNeedBatches (stage 2): trials 8..60 in order
+  int kstar = -1;
+  double tau = 0.0, delta = 0.0;
+  for (int chunk = 0; chunk < 7 && kstar < 0; ++chunk) {
+    double acc[16];
+    xrecv<16>(c, acc, chunk * 16);
+    kstar = cert_pick(k, shifted, 8 + chunk * 8, chunk == 6 ? 5 : 8, acc, tau, delta);
+  }
+  if (kstar < 0) {  // stall (solvers.hpp:315-325): no trial decreases the envelope
+    if (b0) {
+      cert_finalize(c, k, s, -1, 0.0, 0.0, 0.0, 0.0);
+      c.I[il::CSTATE + stage - 1] = kCertDone;
+    }
+    return;
+  }
+  final_pass(tau);
+  if (b0) {
+    c.I[il::CSTATE + stage - 1] = kCertNeedF2;
+    c.I[il::CKSTAR] = kstar;
+    c.S[sl::TAU] = tau;
+    c.S[sl::DELTA] = delta;
   }
 }
 
@@ -779,12 +1047,14 @@ __global__ void __launch_bounds__(kThreads) power_kernel(DualCtx c, double* v, c
   if (*reinterpret_cast<const volatile int*>(c.I + il::PDONE)) return;
   int ph = 0;
   double s[2] = {0, 0};
-  for (int i = gtid(); i < c.D; i += gstride()) {
-    const double img = -Hv[i];
-    s[0] += v[i] * img;
-    s[1] += img * img;
-  }
-  grid_reduce<2>(c, ph, s);
+  if (c.phase <= 0)
+    for (int i = gtid(); i < c.D; i += gstride()) {
+      if (!counted(c, i)) continue;
+      const double img = -Hv[i];
+      s[0] += v[i] * img;
+      s[1] += img * img;
+    }
+  if (!xreduce<2>(c, ph, s)) return;
   const double next = s[0], mag = sqrt(s[1]);
   const bool zero = !(mag > 0.0);
   const double rayleigh = c.S[sl::RAYLEIGH];
@@ -820,8 +1090,10 @@ __global__ void prox_kernel(DualCtx c, const double* v, double gp, double* out) 
 __global__ void __launch_bounds__(kThreads) conj_kernel(DualCtx c, const double* w) {
   int ph = 0;
   double s[1] = {0.0};
-  for (int i = gtid(); i < c.D; i += gstride()) s[0] += conj_row(c.g.kind[i], w[i], c.g.lo[i], c.g.hi[i], c.g.wg[i]);
-  grid_reduce<1>(c, ph, s);
+  if (c.phase <= 0)
+    for (int i = gtid(); i < c.D; i += gstride())
+      if (counted(c, i)) s[0] += conj_row(c.g.kind[i], w[i], c.g.lo[i], c.g.hi[i], c.g.wg[i]);
+  if (!xreduce<1>(c, ph, s)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) c.S[sl::RED0] = s[0];
 }
 
@@ -829,7 +1101,8 @@ __global__ void __launch_bounds__(kThreads) conj_kernel(DualCtx c, const double*
 __global__ void __launch_bounds__(kThreads) dist_kernel(DualCtx c, const double* y, const double* z) {
   int ph = 0;
   double m[1] = {0.0};
-  for (int i = gtid(); i < c.D; i += gstride()) {
+  for (int i = gtid(); c.phase <= 0 && i < c.D; i += gstride()) {
+    if (!counted(c, i)) continue;
     const int kd = c.g.kind[i];
     const double yi = y[i], zi = z[i];
     double dv = 0.0;
@@ -846,23 +1119,27 @@ __global__ void __launch_bounds__(kThreads) dist_kernel(DualCtx c, const double*
     }
     m[0] = fmax(m[0], dv);
   }
-  grid_reduce<1, true>(c, ph, m);
+  if (!xreduce<1, true>(c, ph, m)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) c.S[sl::RED0] = m[0];
 }
 
 __global__ void __launch_bounds__(kThreads) maxdiff_kernel(DualCtx c, const double* a, const double* b) {
   int ph = 0;
   double m[1] = {0.0};
-  for (int i = gtid(); i < c.D; i += gstride()) m[0] = fmax(m[0], fabs(a[i] - b[i]));
-  grid_reduce<1, true>(c, ph, m);
+  if (c.phase <= 0)
+    for (int i = gtid(); i < c.D; i += gstride())
+      if (counted(c, i)) m[0] = fmax(m[0], fabs(a[i] - b[i]));
+  if (!xreduce<1, true>(c, ph, m)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) c.S[sl::RED0] = m[0];
 }
 
 __global__ void __launch_bounds__(kThreads) dot_kernel(DualCtx c, const double* a, const double* b) {
   int ph = 0;
   double s[1] = {0.0};
-  for (int i = gtid(); i < c.D; i += gstride()) s[0] += a[i] * b[i];
-  grid_reduce<1>(c, ph, s);
+  if (c.phase <= 0)
+    for (int i = gtid(); i < c.D; i += gstride())
+      if (counted(c, i)) s[0] += a[i] * b[i];
+  if (!xreduce<1>(c, ph, s)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) c.S[sl::RED0] = s[0];
 }
 
@@ -898,7 +1175,7 @@ __global__ void __launch_bounds__(kThreads) eval_f_kernel(DualCtx c, CostPack cp
   const int64_t lsz = static_cast<int64_t>(nx) * nx + nx;
   double s[1] = {0.0}, bad[1] = {0.0};
   const int NN = cp.nnodes, NL = cp.nleaves;
-  for (int t = gw; t < NN + NL + 1; t += nw) {
+  for (int t = gw; c.phase <= 0 && t < NN + NL + 1; t += nw) {
     if (t == NN + NL) {  // root state check
       if (cp.check_root)
         for (int k = lane; k < nx; k += 32)
@@ -947,16 +1224,33 @@ __global__ void __launch_bounds__(kThreads) eval_f_kernel(DualCtx c, CostPack cp
       s[0] += cp.prob[nd] * part;
     }
   }
-  grid_reduce<1>(c, ph, s);
-  grid_reduce<1, true>(c, ph, bad);
+  double v[2] = {s[0], bad[0]};  // the sum and the infeasibility flag (max), one barrier
+  if (!xreduce<2, false, 1>(c, ph, v)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    c.S[sl::EVALF] = s[0];
-    c.S[sl::EVALF_INF] = bad[0];
+    c.S[sl::EVALF] = v[0];
+    c.S[sl::EVALF_INF] = v[1];
   }
 }
 
 cudaError_t coop(const void* fn, const DualCtx& c, void** args, cudaStream_t st) {
   return cudaLaunchCooperativeKernel(fn, dim3(c.nblk), dim3(kThreads), args, 0, st);
+}
+
+// Launch of a kernel whose args[0] is &cc. Unsharded: one launch. Sharded:
+// `phases` launches (cc.phase = 0, 1, ...) with an allgather of the ranks'
+// totals after each but the last.
+cudaError_t phased(const void* fn, DualCtx& cc, void** args, cudaStream_t st, int phases = 2) {
+  if (!cc.xc) {
+    cc.phase = -1;
+    return coop(fn, cc, args, st);
+  }
+  for (int p = 0; p < phases; ++p) {
+    cc.phase = p;
+    const cudaError_t e = coop(fn, cc, args, st);
+    if (e != cudaSuccess) return e;
+    if (p + 1 < phases) dual_allgather(cc.xc, cc.xs, cc.xr, kXMax, st);
+  }
+  return cudaSuccess;
 }
 
 }  // namespace
@@ -968,7 +1262,7 @@ cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, 
                         cudaStream_t st) {
   DualCtx cc = c;
   void* args[] = {&cc, &state, &mode, &y, &Hx, &Hx0, &weight, &z, &R, &T};
-  return coop(reinterpret_cast<const void*>(fb_finish_kernel), c, args, st);
+  return phased(reinterpret_cast<const void*>(fb_finish_kernel), cc, args, st);
 }
 
 // Scalar block -> mapped pinned host memory in one launch (the host waits on
@@ -995,7 +1289,7 @@ cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const doubl
                        cudaStream_t st) {
   DualCtx cc = c;
   void* args[] = {&cc, &state, &R, &HR, &grad};
-  return coop(reinterpret_cast<const void*>(fbe_grad_kernel), c, args, st);
+  return phased(reinterpret_cast<const void*>(fbe_grad_kernel), cc, args, st);
 }
 
 cudaError_t k_lbfgs(const DualCtx& c, int mem, double eps_curv, double scale_ref, int do_push, const double* a,
@@ -1006,8 +1300,9 @@ cudaError_t k_lbfgs(const DualCtx& c, int mem, double eps_curv, double scale_ref
   if (Mbuf && mem <= kCompactMem) {
     void* args[] = {&c2,  &mem,  &eps_curv, &scale_ref, &do_push, &a,  &b,   &cc,     &dd,  &gvec,
                     &out, &Sbuf, &Qbuf,     &Mbuf,      &fR,      &fHR, &fstate, &gout};
-    return coop(reinterpret_cast<const void*>(lbfgs_compact_kernel), c, args, st);
+    return phased(reinterpret_cast<const void*>(lbfgs_compact_kernel), c2, args, st);
   }
+  if (c2.xc) return cudaErrorNotSupported;  // sharded handles: compact form only (memory <= 6)
   void* args[] = {&c2, &mem, &eps_curv, &scale_ref, &do_push, &a, &b, &cc, &dd, &gvec, &out, &Sbuf, &Qbuf};
   return coop(reinterpret_cast<const void*>(lbfgs_kernel), c, args, st);
 }
@@ -1016,6 +1311,10 @@ cudaError_t k_cert_search(const DualCtx& c, int state, int shifted, int tlambda,
                           const double* R, const double* Hx, const double* HR, const double* d,
                           const double* Hd, double* y_next, cudaStream_t st) {
   DualCtx cc = c;
+  if (cc.xc) {  // sharded: four phases (cert_shard_kernel)
+    void* args[] = {&cc, &state, &shifted, &tlambda, &y, &R, &Hx, &HR, &d, &Hd, &y_next};
+    return phased(reinterpret_cast<const void*>(cert_shard_kernel), cc, args, st, 4);
+  }
   int ntau = 0;
   Taus taus{};
   double* nul = nullptr;
@@ -1029,6 +1328,7 @@ cudaError_t k_cert_eval(const DualCtx& c, int state, int shifted, const double* 
                         int ntau, const double* taus_host, double* deltas, double* cfh, double* w,
                         double* Hxw, double* zz, double* RR, double* TT, cudaStream_t st) {
   if (ntau < 1 || ntau > 16) return cudaErrorInvalidValue;
+  if (c.xc) return cudaErrorNotSupported;  // explicit trials: unsharded handles
   DualCtx cc = c;
   Taus taus{};
   for (int k = 0; k < ntau; ++k) taus.t[k] = taus_host[k];
@@ -1042,7 +1342,7 @@ cudaError_t k_cert_eval(const DualCtx& c, int state, int shifted, const double* 
 cudaError_t k_power(const DualCtx& c, double* v, const double* Hv, double rel_tol, cudaStream_t st) {
   DualCtx cc = c;
   void* args[] = {&cc, &v, &Hv, &rel_tol};
-  return coop(reinterpret_cast<const void*>(power_kernel), c, args, st);
+  return phased(reinterpret_cast<const void*>(power_kernel), cc, args, st);
 }
 
 cudaError_t k_extrapolate(const DualCtx& c, const double* yn, double* yp, double* w, double mom,
@@ -1059,25 +1359,25 @@ cudaError_t k_prox(const DualCtx& c, const double* v, double gamma_prox, double*
 cudaError_t k_conj(const DualCtx& c, const double* w, cudaStream_t st) {
   DualCtx cc = c;
   void* args[] = {&cc, &w};
-  return coop(reinterpret_cast<const void*>(conj_kernel), c, args, st);
+  return phased(reinterpret_cast<const void*>(conj_kernel), cc, args, st);
 }
 
 cudaError_t k_dist_subdiff(const DualCtx& c, const double* y, const double* z, cudaStream_t st) {
   DualCtx cc = c;
   void* args[] = {&cc, &y, &z};
-  return coop(reinterpret_cast<const void*>(dist_kernel), c, args, st);
+  return phased(reinterpret_cast<const void*>(dist_kernel), cc, args, st);
 }
 
 cudaError_t k_max_abs_diff(const DualCtx& c, const double* a, const double* b, cudaStream_t st) {
   DualCtx cc = c;
   void* args[] = {&cc, &a, &b};
-  return coop(reinterpret_cast<const void*>(maxdiff_kernel), c, args, st);
+  return phased(reinterpret_cast<const void*>(maxdiff_kernel), cc, args, st);
 }
 
 cudaError_t k_dot(const DualCtx& c, const double* a, const double* b, cudaStream_t st) {
   DualCtx cc = c;
   void* args[] = {&cc, &a, &b};
-  return coop(reinterpret_cast<const void*>(dot_kernel), c, args, st);
+  return phased(reinterpret_cast<const void*>(dot_kernel), cc, args, st);
 }
 
 cudaError_t k_scale(const DualCtx& c, int n, double alpha, const double* x, double beta, const double* y0,
@@ -1097,7 +1397,7 @@ cudaError_t k_eval_f(const DualCtx& c, const CostPack& cp, const double* x, cons
   DualCtx cc = c;
   CostPack p = cp;
   void* args[] = {&cc, &p, &x, &u, &feas_tol};
-  return coop(reinterpret_cast<const void*>(eval_f_kernel), c, args, st);
+  return phased(reinterpret_cast<const void*>(eval_f_kernel), cc, args, st);
 }
 
 }  // namespace scn

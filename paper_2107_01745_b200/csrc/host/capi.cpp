@@ -258,6 +258,38 @@ int scenopt_dev_create_sharded(const scenopt_problem* p, const scenopt_factor* f
   });
 }
 
+struct scenopt_shard_group {
+  std::shared_ptr<EmuGroup> g;
+};
+
+int scenopt_shard_group_create(int world, scenopt_shard_group** out) {
+  SCN_GUARD({
+    auto g = std::make_unique<scenopt_shard_group>();
+    g->g = emu_group_create(world);
+    *out = g.release();
+  });
+}
+
+void scenopt_shard_group_destroy(scenopt_shard_group* g) { delete g; }
+
+int scenopt_dev_create_sharded_group(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
+                                     scenopt_shard_group* g, int shard_stage, scenopt_dev** out) {
+  SCN_GUARD({
+    if (!f) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: a factor cache is required");
+    if (!g) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: null shard group");
+    ShardSpec spec;
+    spec.rank = rank;
+    spec.world = emu_group_world(*g->g);
+    spec.stage = shard_stage;
+    spec.emu = g->g;
+    if (rank < 0 || rank >= spec.world) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: bad rank/world");
+    auto h = std::make_unique<scenopt_dev>();
+    h->d = dev_create(p->p, &f->f, device, &spec);
+    h->init_solver_buffers();
+    *out = h.release();
+  });
+}
+
 int scenopt_shard_sweep_phase(scenopt_dev* h, int phase, int nrhs, int affine, const double* const* y,
                               double* const* Hx) {
   SCN_GUARD({
@@ -271,7 +303,7 @@ int scenopt_shard_exchange_buffer(scenopt_dev* h, double** buf, size_t* doubles_
     const DevState& d = *h->d;
     if (!d.sharded()) fail(SCENOPT_E_INVALID_PARAMS, "exchange buffer: handle is not sharded");
     *buf = d.xbuf;
-    *doubles_per_rhs = static_cast<size_t>(d.sstage_hi - d.sstage_lo) * (d.lay.nx + d.lay.nu);
+    *doubles_per_rhs = static_cast<size_t>(d.xbuf_rhs);
   });
 }
 

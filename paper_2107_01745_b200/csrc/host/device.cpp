@@ -13,7 +13,7 @@ namespace scn {
 
 DevState::~DevState() {
   if (device >= 0) cudaSetDevice(device);
-  nccl_comm_destroy(comm);
+  comm.reset();
   for (void* p : owned) cudaFree(p);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -1055,8 +1055,43 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   if (d->sharded()) {
     d->rank = shard->rank;
     d->world = shard->world;
-    d->xbuf = d->alloc<double>(static_cast<size_t>(kMaxRhs) * (d->sstage_hi - d->sstage_lo) * W);
-    if (shard->nccl_id) nccl_comm_init(*d, shard->nccl_id);  // else: exchange left to the caller (phase API)
+    // rows / nodes this rank owns (counted in reductions and gathers): its
+    // subtrees' stage and terminal rows, and the replicated top on rank 0
+    std::vector<uint8_t> cnt(static_cast<size_t>(std::max(D, 1)), 0);
+    auto add = [](std::vector<std::pair<int64_t, int64_t>>& v, int64_t a, int64_t b) {
+      if (b <= a) return;
+      if (!v.empty() && v.back().second == a)
+        v.back().second = b;
+      else
+        v.push_back({a, b});
+    };
+    for (int c = 1; c < n; ++c)
+      if (mine[c])
+        for (int k = 0; k < p.stage_rows[c]; ++k) cnt[p.dual_offset[c] + k] = 1;
+    for (int l = 0; l < p.L; ++l)
+      if (mine[p.first_leaf + l])
+        for (int k = 0; k < p.terminal_rows[l]; ++k) cnt[p.tdual_offset[l] + k] = 1;
+    for (int i = 0; i < D; ++i)
+      if (cnt[i]) add(d->keep_y, i, i + 1);
+    for (int c = 0; c < n; ++c)
+      if (mine[c]) {
+        add(d->keep_x, static_cast<int64_t>(c) * nx, static_cast<int64_t>(c + 1) * nx);
+        if (c < p.first_leaf) add(d->keep_u, static_cast<int64_t>(c) * nu, static_cast<int64_t>(c + 1) * nu);
+      }
+    d->row_counted = upload(*d, cnt);
+    const int last = d->sstage_hi - 1;
+    d->dual_s_end = p.dual_offset[last] + p.stage_rows[last];
+    d->xbuf_rhs = static_cast<int64_t>(d->sstage_hi - d->sstage_lo) * W + (d->dual_s_end - d->dual_top);
+    d->xbuf = d->alloc<double>(static_cast<size_t>(kMaxRhs) * d->xbuf_rhs);
+    for (int r = 0; r < kMaxRhs; ++r) d->ycomp[r] = d->alloc<double>(static_cast<size_t>(std::max(D, 1)));
+    d->gx = d->alloc<double>(static_cast<size_t>(n) * nx);
+    d->gu = d->alloc<double>(static_cast<size_t>(std::max(p.first_leaf, 1)) * nu);
+    d->gy = d->alloc<double>(static_cast<size_t>(std::max(D, 1)));
+    if (shard->emu)
+      d->comm = emu_comm(shard->emu, shard->rank);
+    else if (shard->nccl_id)
+      d->comm = nccl_comm(device, shard->rank, shard->world, shard->nccl_id);
+    // else: exchange left to the caller (phase API)
   }
 
   for (int r = 0; r < kMaxRhs; ++r) {
@@ -1252,84 +1287,102 @@ void launch(DevState& d, SweepParams& P, const DevState::Launch& ln) {
   P.items_total = ln.count;
   SCN_CUDA(sweep_launch(P, d.grid, d.dyn_smem, d.max_m, d.max_mN, d.stream));
 }
-// sharded phase A: zero the outputs this rank does not own, local backward,
-// own shard-stage contributions into the (zeroed) exchange buffer
-void phase_a(DevState& d, SweepParams& P, bool gather_primal) {
+// sharded phase A: local backward; this rank's shard-stage contributions
+// and shard-stage dual rows into the (zeroed) exchange buffer. zero_rows
+// (phase API only) also zeroes the Hx rows this rank does not write.
+void phase_a(DevState& d, SweepParams& P, bool zero_rows) {
   const Layout& L = d.lay;
   const int W = L.nx + L.nu;
-  const size_t ns = static_cast<size_t>(d.sstage_hi - d.sstage_lo);
-  // only the rows of other ranks' subtrees: this rank's launches write the rest
-  auto zero = [&](double* v, const std::vector<std::pair<int64_t, int64_t>>& rg) {
-    for (const auto& q : rg)
-      SCN_CUDA(cudaMemsetAsync(v + q.first, 0, sizeof(double) * (q.second - q.first), d.stream));
-  };
-  for (int r = 0; r < P.nrhs; ++r) {
-    zero(P.Hx[r], d.zero_hx);
-    if (gather_primal) {
-      zero(P.x[r], d.zero_x);
-      zero(P.u[r], d.zero_u);
-    }
-  }
+  const int64_t ns = d.sstage_hi - d.sstage_lo;
+  if (zero_rows)
+    for (int r = 0; r < P.nrhs; ++r)
+      for (const auto& q : d.zero_hx)
+        SCN_CUDA(cudaMemsetAsync(P.Hx[r] + q.first, 0, sizeof(double) * (q.second - q.first), d.stream));
   launch(d, P, d.launches[0]);
-  SCN_CUDA(cudaMemsetAsync(d.xbuf, 0, sizeof(double) * P.nrhs * ns * W, d.stream));
-  for (int r = 0; r < P.nrhs; ++r)
-    SCN_CUDA(cudaMemcpyAsync(d.xbuf + (r * ns + (d.shard_lo - d.sstage_lo)) * W,
-                             P.contrib[r] + static_cast<size_t>(d.shard_lo) * W,
-                             sizeof(double) * (d.shard_hi - d.shard_lo) * W, cudaMemcpyDeviceToDevice, d.stream));
+  SCN_CUDA(cudaMemsetAsync(d.xbuf, 0, sizeof(double) * P.nrhs * d.xbuf_rhs, d.stream));
+  const int64_t own_lo = d.shard_lo, own_hi = d.shard_hi;
+  if (own_hi <= own_lo) return;  // no shard-stage node on this rank
+  const int64_t ylo = L.dual_offset[own_lo], yhi = L.dual_offset[own_hi - 1] + L.stage_rows[own_hi - 1];
+  for (int r = 0; r < P.nrhs; ++r) {
+    double* xb = d.xbuf + r * d.xbuf_rhs;
+    SCN_CUDA(cudaMemcpyAsync(xb + (own_lo - d.sstage_lo) * W, P.contrib[r] + own_lo * W,
+                             sizeof(double) * (own_hi - own_lo) * W, cudaMemcpyDeviceToDevice, d.stream));
+    SCN_CUDA(cudaMemcpyAsync(xb + ns * W + (ylo - d.dual_top), P.y[r] + ylo, sizeof(double) * (yhi - ylo),
+                             cudaMemcpyDeviceToDevice, d.stream));
+  }
 }
-// sharded phase B: summed contributions back, top backward + forward, and
-// the replicated top rows of Hx kept on rank 0 only
-void phase_b(DevState& d, SweepParams& P) {
+// sharded phase B: summed contributions back; launch B reads the top rows of
+// y and every rank's shard-stage rows (ycomp); top backward + forward, local
+// forward. zero_rows (phase API only): the replicated top rows of Hx are kept
+// on rank 0 only.
+void phase_b(DevState& d, SweepParams& P, bool zero_rows) {
   const Layout& L = d.lay;
   const int W = L.nx + L.nu;
-  const size_t ns = static_cast<size_t>(d.sstage_hi - d.sstage_lo);
-  for (int r = 0; r < P.nrhs; ++r)
-    SCN_CUDA(cudaMemcpyAsync(P.contrib[r] + static_cast<size_t>(d.sstage_lo) * W, d.xbuf + r * ns * W,
-                             sizeof(double) * ns * W, cudaMemcpyDeviceToDevice, d.stream));
+  const int64_t ns = d.sstage_hi - d.sstage_lo, nys = d.dual_s_end - d.dual_top;
+  for (int r = 0; r < P.nrhs; ++r) {
+    const double* xb = d.xbuf + r * d.xbuf_rhs;
+    SCN_CUDA(cudaMemcpyAsync(P.contrib[r] + static_cast<int64_t>(d.sstage_lo) * W, xb, sizeof(double) * ns * W,
+                             cudaMemcpyDeviceToDevice, d.stream));
+    if (d.dual_top > 0)
+      SCN_CUDA(cudaMemcpyAsync(d.ycomp[r], P.y[r], sizeof(double) * d.dual_top, cudaMemcpyDeviceToDevice, d.stream));
+    SCN_CUDA(cudaMemcpyAsync(d.ycomp[r] + d.dual_top, xb + ns * W, sizeof(double) * nys, cudaMemcpyDeviceToDevice,
+                             d.stream));
+    P.y[r] = d.ycomp[r];
+  }
   launch(d, P, d.launches[1]);
-  if (d.rank != 0)
+  if (zero_rows && d.rank != 0)
     for (int r = 0; r < P.nrhs; ++r)
       SCN_CUDA(cudaMemsetAsync(P.Hx[r], 0, d.dual_top * sizeof(double), d.stream));
 }
 }  // namespace
 
 void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
-               double* const* u, double* const* Hx, bool gather_primal) {
+               double* const* u, double* const* Hx) {
   SweepParams P = sweep_params(d, nrhs, affine, y, x, u, Hx);
   if (!d.sharded()) {
     launch(d, P, d.launches[0]);
     return;
   }
-  // sharded: A (local backward) | allreduce contributions | B (top + local forward) | allreduce Hx
-  const int W = d.lay.nx + d.lay.nu;
-  const size_t ns = static_cast<size_t>(d.sstage_hi - d.sstage_lo);
-  phase_a(d, P, gather_primal);
-  dev_allreduce(d, d.xbuf, static_cast<size_t>(nrhs) * ns * W);
-  phase_b(d, P);
-  for (int r = 0; r < nrhs; ++r) dev_allreduce(d, P.Hx[r], static_cast<size_t>(d.lay.dual_dim));
-  if (gather_primal)
-    for (int r = 0; r < nrhs; ++r) dev_gather_primal(d, P.x[r], P.u[r]);
+  // sharded: A (local backward) | allreduce of the shard-stage exchange | B (top + local forward).
+  // x / u / Hx stay on their owners: no other collective.
+  phase_a(d, P, false);
+  dev_allreduce(d, d.xbuf, static_cast<size_t>(nrhs) * d.xbuf_rhs);
+  phase_b(d, P, false);
 }
 
 void dev_sweep_phase(DevState& d, int phase, int nrhs, bool affine, const double* const* y, double* const* Hx) {
   if (!d.sharded()) fail(SCENOPT_E_INVALID_PARAMS, "sweep phase: handle is not sharded");
   SweepParams P = sweep_params(d, nrhs, affine, y, nullptr, nullptr, Hx);
   if (phase == 0)
-    phase_a(d, P, false);
+    phase_a(d, P, true);
   else
-    phase_b(d, P);
+    phase_b(d, P, true);
 }
 
-void dev_gather_primal(DevState& d, double* x, double* u) {
-  if (!d.sharded()) return;
+namespace {
+// dst = src on the ranges, 0 elsewhere; then the sum over ranks
+void gather_into(DevState& d, const double* src, double* dst, size_t total,
+                 const std::vector<std::pair<int64_t, int64_t>>& keep) {
+  SCN_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * total, d.stream));
+  for (const auto& q : keep)
+    SCN_CUDA(cudaMemcpyAsync(dst + q.first, src + q.first, sizeof(double) * (q.second - q.first),
+                             cudaMemcpyDeviceToDevice, d.stream));
+  dev_allreduce(d, dst, total);
+}
+}  // namespace
+
+std::pair<const double*, const double*> dev_gather_primal(DevState& d, const double* x, const double* u) {
+  if (!d.sharded()) return {x, u};
   const Layout& L = d.lay;
-  // top nodes [0, sstage_lo) are replicated: keep rank 0's copy only
-  if (d.rank != 0) {
-    SCN_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * L.nx * d.sstage_lo, d.stream));
-    SCN_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * L.nu * d.sstage_lo, d.stream));
-  }
-  dev_allreduce(d, x, static_cast<size_t>(L.nx) * L.n);
-  dev_allreduce(d, u, static_cast<size_t>(L.nu) * L.first_leaf);
+  if (x) gather_into(d, x, d.gx, static_cast<size_t>(L.nx) * L.n, d.keep_x);
+  if (u) gather_into(d, u, d.gu, static_cast<size_t>(L.nu) * L.first_leaf, d.keep_u);
+  return {x ? d.gx : nullptr, u ? d.gu : nullptr};
+}
+
+const double* dev_gather_dual(DevState& d, const double* y) {
+  if (!d.sharded()) return y;
+  gather_into(d, y, d.gy, static_cast<size_t>(d.lay.dual_dim), d.keep_y);
+  return d.gy;
 }
 
 }  // namespace scn

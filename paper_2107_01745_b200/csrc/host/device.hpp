@@ -30,6 +30,15 @@ struct DBuf {
   size_t n = 0;
 };
 
+// Collectives of a sharded handle on its stream (comm.cpp): NCCL, or an
+// emulated group of handles in one process (tests on one GPU).
+struct Comm {
+  virtual ~Comm() = default;
+  virtual void allreduce_sum(double* buf, size_t n, cudaStream_t st) = 0;
+  virtual void allgather(const double* send, double* recv, size_t n, cudaStream_t st) = 0;  // recv: world x n
+};
+struct EmuGroup;
+
 struct Layout {  // host copy of the layout numbers the device code needs
   int nx = 0, nu = 0, N = 0, n = 0, L = 0, first_leaf = 0, dual_dim = 0, stage_total = 0;
   std::vector<int32_t> ancestor, stage_offsets, stage_rows, terminal_rows, child_begin,
@@ -72,11 +81,21 @@ struct DevState {
   int items_global = 0;         // items whose node blocks are read from HBM in place
   // ---- subtree sharding over ranks
   int rank = 0, world = 1, shard_stage = -1;
-  void* comm = nullptr;         // ncclComm_t
+  std::unique_ptr<Comm> comm;   // null: exchange left to the caller (phase API)
   int shard_lo = 0, shard_hi = 0;  // this rank's shard-stage nodes
   int sstage_lo = 0, sstage_hi = 0;  // all shard-stage nodes [stage_offsets[s], stage_offsets[s+1])
   int64_t dual_top = 0;          // dual rows of the replicated top stages (a prefix)
-  double* xbuf = nullptr;        // exchange buffer: shard-stage contributions, kMaxRhs x ns x (nu+nx)
+  int64_t dual_s_end = 0;        // end of the shard-stage nodes' dual rows ([dual_top, dual_s_end))
+  // exchange buffer, per right-hand side: [shard-stage contributions ns x (nu+nx) | shard-stage y rows]
+  double* xbuf = nullptr;
+  int64_t xbuf_rhs = 0;          // doubles per right-hand side
+  double* ycomp[kMaxRhs] = {};   // launch B's dual input: top rows + every rank's shard-stage rows
+  // Row / node ownership. Rank r holds valid values on its own rows (its
+  // subtrees' stage and terminal rows) and on the replicated top rows;
+  // reductions count the own rows, and the top rows on rank 0 only.
+  uint8_t* row_counted = nullptr;  // [dual_dim] (device)
+  std::vector<std::pair<int64_t, int64_t>> keep_x, keep_u, keep_y;  // element ranges counted on this rank
+  double *gx = nullptr, *gu = nullptr, *gy = nullptr;               // gather scratch
   // [begin, end) element ranges of x / u / Hx that no launch of this rank
   // writes (other ranks' subtrees), zeroed before the sweep's allreduces
   std::vector<std::pair<int64_t, int64_t>> zero_x, zero_u, zero_hx;
@@ -126,6 +145,7 @@ struct ShardSpec {
   int rank = 0, world = 1;
   int stage = -1;              // shard cut stage (-1: smallest stage with >= world nodes)
   const void* nccl_id = nullptr;  // 128-byte ncclUniqueId shared by all ranks
+  std::shared_ptr<EmuGroup> emu;  // or: an emulated group (one process, one host thread per rank)
 };
 // Host-only shard plan: *stage (in: -1 = auto) and the world+1 bounds of the
 // ranks' contiguous shard-stage node ranges, balanced by subtree bytes.
@@ -145,25 +165,31 @@ Factor dev_factor_export(DevState& d, const Problem& p);
 void dev_refactor_affine(DevState& d, const Problem& p);
 // ncclGetUniqueId into 128 bytes
 void nccl_unique_id(void* out128);
-void nccl_comm_init(DevState& d, const void* id128);
-void nccl_comm_destroy(void* comm);
+std::unique_ptr<Comm> nccl_comm(int device, int rank, int world, const void* id128);
+std::shared_ptr<EmuGroup> emu_group_create(int world);
+int emu_group_world(const EmuGroup& g);
+std::unique_ptr<Comm> emu_comm(const std::shared_ptr<EmuGroup>& g, int rank);
 // Sum-allreduce of n doubles on the handle's stream (no-op unsharded).
 void dev_allreduce(DevState& d, double* buf, size_t n);
 int device_count_sm100();
 
 // One fused sweep over nrhs right-hand sides; y/x/u/Hx are device pointers
 // (x/u/Hx may be null: the handle's scratch is used). Enqueued on d.stream.
-// Sharded handles: Hx is assembled on every rank; x/u hold this rank's nodes
-// plus the replicated top unless gather_primal assembles them in full.
+// Sharded handles: y must be valid on this rank's own and top rows; x/u/Hx
+// come out valid on this rank's own and top nodes / rows only (the
+// dev_gather_* calls assemble full vectors).
 void dev_sweep(DevState& d, int nrhs, bool affine, const double* const* y, double* const* x,
-               double* const* u, double* const* Hx, bool gather_primal = false);
+               double* const* u, double* const* Hx);
 // One phase of a sharded sweep with the exchange left to the caller (phase 0:
 // zero Hx, local backward, own contributions into d.xbuf; phase 1: xbuf
 // (summed over ranks by the caller) back, top backward + forward, top rows
 // of Hx zeroed on ranks != 0). Emulation / tests of handles without NCCL.
 void dev_sweep_phase(DevState& d, int phase, int nrhs, bool affine, const double* const* y, double* const* Hx);
-// Assemble a sharded primal point in full on every rank (x: nx*n, u: nu*F).
-void dev_gather_primal(DevState& d, double* x, double* u);
+// Assemble a sharded primal point / dual vector in full on every rank, into
+// the handle's gather scratch (returned; the inputs are not modified). An
+// unsharded handle returns the inputs.
+std::pair<const double*, const double*> dev_gather_primal(DevState& d, const double* x, const double* u);
+const double* dev_gather_dual(DevState& d, const double* y);
 
 // kernel launchers (cuda/*.cu)
 int sweep_teams();

@@ -60,18 +60,21 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
       d->out_hx[r] = (x && x[r]) ? mapped(x[r]) : nullptr;
       d->out_hu[r] = (u && u[r]) ? mapped(u[r]) : nullptr;
     }
-    dev_sweep(*d, nrhs, affine, yd, xd, ud, hd, true);
+    dev_sweep(*d, nrhs, affine, yd, xd, ud, hd);
     for (int r = 0; r < nrhs; ++r)
       if (Hx && Hx[r]) out_copy(Hx[r], d->hs[r], static_cast<size_t>(L.dual_dim), flags);
     sync();
     return;
   }
-  dev_sweep(*d, nrhs, affine, yd, xd, ud, hd, want_primal);
+  dev_sweep(*d, nrhs, affine, yd, xd, ud, hd);
   if (host) {
+    // sharded: host outputs are assembled over the ranks (device outputs stay rank-local)
     for (int r = 0; r < nrhs; ++r) {
-      if (x && x[r]) out_copy(x[r], d->xs[r], static_cast<size_t>(L.nx) * L.n, flags);
-      if (u && u[r]) out_copy(u[r], d->us[r], static_cast<size_t>(L.nu) * L.first_leaf, flags);
-      if (Hx && Hx[r]) out_copy(Hx[r], d->hs[r], static_cast<size_t>(L.dual_dim), flags);
+      const auto xu = dev_gather_primal(*d, (x && x[r]) ? d->xs[r] : nullptr, (u && u[r]) ? d->us[r] : nullptr);
+      if (x && x[r]) out_copy(x[r], xu.first, static_cast<size_t>(L.nx) * L.n, flags);
+      if (u && u[r]) out_copy(u[r], xu.second, static_cast<size_t>(L.nu) * L.first_leaf, flags);
+      if (Hx && Hx[r]) out_copy(Hx[r], dev_gather_dual(*d, d->hs[r]), static_cast<size_t>(L.dual_dim), flags);
+      if (d->sharded()) sync();  // the gather scratch is reused by the next right-hand side
     }
   }
   if (sync_after || host) sync();

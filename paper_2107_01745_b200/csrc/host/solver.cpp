@@ -57,6 +57,7 @@ struct scenopt_dev::Work {
   double *Sb = nullptr, *Qb = nullptr;
   double* Mb = nullptr;  // compact L-BFGS: S'Y and Y'Y of the stored pairs (2 x 64 x 64)
   double* small = nullptr;  // 64 doubles of API scratch
+  double *xs = nullptr, *xr = nullptr;  // sharded: per-phase totals of this rank / of all ranks
   int lb_slots = 0;
   bool fhat0_ready = false;
   DualCtx ctx(const DevState& d) const {
@@ -68,6 +69,13 @@ struct scenopt_dev::Work {
     c.I = I;
     c.part = part;
     c.bar = bar;
+    if (d.sharded()) {  // reductions over this rank's rows, combined across ranks (DualCtx)
+      c.cnt = d.row_counted;
+      c.xc = d.comm.get();
+      c.world = d.world;
+      c.xs = xs;
+      c.xr = xr;
+    }
     return c;
   }
 };
@@ -125,6 +133,10 @@ void scenopt_dev::init_solver_buffers() {
     k.u[s] = ds.alloc<double>(nuf);
   }
   k.small = ds.alloc<double>(64);
+  if (ds.sharded()) {
+    k.xs = ds.alloc<double>(kXMax);
+    k.xr = ds.alloc<double>(static_cast<size_t>(kXMax) * ds.world);
+  }
   k.Hx0 = ds.alloc<double>(D);
   k.x0 = ds.alloc<double>(nxn);
   k.u0 = ds.alloc<double>(nuf);
@@ -189,6 +201,7 @@ void array_give(std::vector<double>& v) {
 }
 }  // namespace
 
+void validate_for(const scenopt_solver_config& c, const DevState& d);
 // solvers.hpp:48-60
 void validate_config(const scenopt_solver_config& c) {
   if (c.lambda0 < 0.0) fail(SCENOPT_E_INVALID_PARAMS, "lambda0 must be >= 0");
@@ -202,6 +215,13 @@ void validate_config(const scenopt_solver_config& c) {
   if (c.warm_start_iters < 0) fail(SCENOPT_E_INVALID_PARAMS, "warm_start_iters must be >= 0");
   if (c.backtracking_rule < 0 || c.backtracking_rule > 2)
     fail(SCENOPT_E_INVALID_PARAMS, "unknown backtracking rule");
+}
+
+// a sharded handle runs the compact L-BFGS form only (one reduction per direction)
+void validate_for(const scenopt_solver_config& c, const DevState& d) {
+  validate_config(c);
+  if (d.sharded() && c.memory > kLbfgsCompactMaxMem)
+    fail(SCENOPT_E_INVALID_PARAMS, "memory must be <= 6 on a sharded handle");
 }
 
 // solvers.hpp:122-127
@@ -411,8 +431,7 @@ struct Engine {
     if (k.fhat0_ready) return;
     SCN_CUDA(cudaMemsetAsync(k.tmp, 0, D() * sizeof(double), st));
     sweep1(true, k.tmp, k.x0, k.u0, k.Hx0);
-    SCN_CUDA(k_eval_f(ctx(), d.cost, k.x0, k.u0, 1e-8, st));
-    dev_allreduce(d, k.S + sl::EVALF, 2);  // sharded: partial f and infeasibility count
+    SCN_CUDA(k_eval_f(ctx(), d.cost, k.x0, k.u0, 1e-8, st));  // sharded: own nodes, summed over ranks
     read_scalars();
     const double f0 = S(sl::EVALF);
     if (S(sl::EVALF_INF) != 0.0 || !std::isfinite(f0))
@@ -543,11 +562,12 @@ struct Loop {
         SCN_CUDA(cudaMemcpyAsync(dst.data(), src, dst.size() * sizeof(double), cudaMemcpyDeviceToHost, e.st));
     };
     const double f0 = now_ms();
-    dev_gather_primal(e.d, e.k.x[s], e.k.u[s]);  // sharded: assemble the full point
-    dl(rep.x, e.k.x[s]);
-    dl(rep.u, e.k.u[s]);
-    dl(rep.y, e.k.y[s]);
-    dl(rep.z, e.k.z[s]);
+    // sharded: assemble the full point (the gathers read the states, never write them)
+    const auto xu = dev_gather_primal(e.d, e.k.x[s], e.k.u[s]);
+    dl(rep.x, xu.first);
+    dl(rep.u, xu.second);
+    dl(rep.y, dev_gather_dual(e.d, e.k.y[s]));
+    dl(rep.z, dev_gather_dual(e.d, e.k.z[s]));
     SCN_CUDA(cudaStreamSynchronize(e.st));
     rep.wall_ms = now_ms() - t0;
     if (e.timer.on) std::fprintf(stderr, "[scn] finish: %.3f ms (result copies)\n", now_ms() - f0);
@@ -979,7 +999,6 @@ int scenopt_fhat_value(scenopt_dev* h, const double* y, double* out, int flags) 
     e.sweep1(true, yd, e.k.x[1], e.k.u[1], e.k.Hx[1]);
     ++h->stats.dual_grad_calls;
     SCN_CUDA(k_eval_f(e.ctx(), h->d->cost, e.k.x[1], e.k.u[1], 1e-8, e.st));
-    dev_allreduce(*h->d, e.k.S + sl::EVALF, 2);
     SCN_CUDA(k_dot(e.ctx(), e.k.Hx[1], yd, e.st));
     e.read_scalars();
     const double f = e.S(sl::EVALF_INF) != 0.0 ? std::numeric_limits<double>::infinity() : e.S(sl::EVALF);
@@ -1045,13 +1064,15 @@ int scenopt_fb_step(scenopt_dev* h, const double* y, double lambda, double* x, d
     auto& k = e.k;
     e.fb_step(0, h->in_dual(y, flags, 0), lambda, nullptr, h->stats);
     const Layout& L = h->d->lay;
-    if (x || u) dev_gather_primal(*h->d, k.x[0], k.u[0]);
-    h->out_copy(x, k.x[0], static_cast<size_t>(L.nx) * L.n, flags);
-    h->out_copy(u, k.u[0], static_cast<size_t>(L.nu) * L.first_leaf, flags);
-    h->out_copy(Hx, k.Hx[0], e.D(), flags);
-    h->out_copy(z, k.z[0], e.D(), flags);
-    h->out_copy(R, k.R[0], e.D(), flags);
-    h->out_copy(T, k.T[0], e.D(), flags);
+    DevState& d = *h->d;  // sharded: outputs assembled over the ranks
+    const auto xu = dev_gather_primal(d, x ? k.x[0] : nullptr, u ? k.u[0] : nullptr);
+    h->out_copy(x, xu.first, static_cast<size_t>(L.nx) * L.n, flags);
+    h->out_copy(u, xu.second, static_cast<size_t>(L.nu) * L.first_leaf, flags);
+    for (auto [dst, src] : {std::pair<double*, double*>{Hx, k.Hx[0]}, {z, k.z[0]}, {R, k.R[0]}, {T, k.T[0]}})
+      if (dst) {
+        h->out_copy(dst, dev_gather_dual(d, src), e.D(), flags);
+        if (d.sharded()) SCN_CUDA(cudaStreamSynchronize(e.st));  // the gather scratch is reused next
+      }
     e.read_scalars();
     if (scalars) {
       scalars[0] = e.S(sl::FHAT);
@@ -1071,7 +1092,7 @@ int scenopt_fbe_grad(scenopt_dev* h, const double* R, double lambda, double* gra
     e.sweep1(false, Rd, nullptr, nullptr, k.HR);
     ++h->stats.hessian_vec_calls;
     SCN_CUDA(k_fbe_grad(e.ctx(), 0, Rd, k.HR, k.grad, e.st));
-    h->out_copy(grad, k.grad, e.D(), flags);
+    h->out_copy(grad, dev_gather_dual(*h->d, k.grad), e.D(), flags);
     h->sync();
   });
 }
@@ -1083,6 +1104,7 @@ int scenopt_linesearch_cert(scenopt_dev* h, const double* y, const double* Hx, d
   SCN_GUARD({
     if (!(lambda > 0.0)) fail(SCENOPT_E_INVALID_PARAMS, "linesearch_cert: lambda must be > 0");
     if (ntau < 1 || ntau > 16) fail(SCENOPT_E_INVALID_PARAMS, "linesearch_cert: 1..16 taus");
+    if (h->d->sharded()) fail(SCENOPT_E_INVALID_PARAMS, "linesearch_cert: explicit trials need an unsharded handle");
     Engine e(*h);
     auto& k = e.k;
     const size_t D = e.D();
@@ -1143,7 +1165,7 @@ int scenopt_estimate_lipschitz(scenopt_dev* h, uint64_t* calls, double* out) {
 int scenopt_dev_solve(scenopt_dev* h, const scenopt_solver_config* cfg, int kind, const double* y0,
                       const double* weight, scenopt_report** out) {
   SCN_GUARD({
-    validate_config(*cfg);
+    validate_for(*cfg, *h->d);
     Engine e(*h);
     const size_t D = e.D();
     if (y0)

@@ -1,16 +1,20 @@
 """Subtree sharding on one B200.
 
 * world = 1 with a real NCCL communicator: the two-launch sharded sweep
-  (local backward | contribution allreduce | top + forward | Hx allreduce)
-  must reproduce the single-launch handle bitwise, and so must whole solves.
-* W emulated ranks (handles without a communicator, exchange done here on
-  the host through the phase API): each rank packs only its own subtrees;
+  (local backward | exchange allreduce | top + forward) must reproduce the
+  single-launch handle bitwise, and so must whole solves (every reduction
+  of the dual-space kernels goes through the phase / allgather path).
+* W emulated ranks on the phase API (handles without a communicator,
+  exchange done here on the host): each rank packs only its own subtrees;
   summing the ranks' exchange buffers and Hx must reproduce the unsharded
-  Hx (every row is nonzero on exactly one rank, so the exchange itself is
-  exact; the per-item summation order depends on how a shard's nodes are
-  grouped into items, hence 1e-12 rather than bitwise). Kernels of
-  different ranks never wait on one another: the exchange sits between
-  launches."""
+  Hx (1e-12: the per-item summation order depends on how a shard's nodes
+  are grouped into items).
+* W emulated ranks of a shard group (one host thread per rank, exchanges
+  through host memory after stream synchronisation): the whole sharded
+  solver, dual vectors sharded by row ownership, against the unsharded
+  solver and the oracle.
+Kernels of different ranks never wait on one another: every exchange sits
+between launches."""
 import ctypes as C
 
 import numpy as np
@@ -139,3 +143,84 @@ def test_emulated_ranks_reassemble_the_unsharded_sweep(gpu, monkeypatch, world, 
                 got = sum(rk.get(rk.h[k], prob.dual_dim) for rk in ranks)
                 err = np.abs(got - want[k]).max() / (1.0 + np.abs(want[k]).max())
                 assert err < 1e-12, (world, st, nrhs, affine, err)
+
+
+def _emulated_solve(prob, world, stage, kind, cfg):
+    """W sharded handles of one emulated group (one host thread per rank,
+    exchanges through host memory), all solving the same problem."""
+    import threading
+
+    group = so.ShardGroup(world)
+    caches = []
+    for r in range(world):
+        c = so.factor(prob)
+        c.shard_emulated(r, group, 0, stage)
+        caches.append(c)
+    reps, errs = [None] * world, []
+
+    def run(r):
+        try:
+            reps[r] = so.api._solve_direct(kind, prob, caches[r], cfg)
+        except Exception as e:  # noqa: BLE001 - re-raised below
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    return reps, caches
+
+
+@pytest.mark.parametrize("world,stage", [(2, -1), (3, 2), (4, 1)])
+def test_emulated_ranks_solve_like_the_unsharded_handle(gpu, world, stage):
+    """The sharded solver with W ranks on one GPU (emulated group): dual and
+    primal vectors sharded by subtree, one exchange allreduce per sweep and
+    one allgather of partial sums per reduction. Every rank takes the same
+    decisions (bitwise-identical reports), and the result is the unsharded
+    solver's: iterations within 1, iterates within the tolerance, oracle
+    counts equal when the iterations are."""
+    prob = so.gen_random_instance(5, 6, 3, 8, [4, 3, 2])
+    po = orc.Problem.from_flat(prob.flat())
+    full = so.factor(prob)
+    for kind in ("minfbe", "nama"):
+        cfg = so.SolverConfig(eps=1e-6, nama_parallel_linesearch=(kind == "nama"))
+        ref = so.api._solve_direct(kind, prob, full, cfg)
+        reps, caches = _emulated_solve(prob, world, stage, kind, cfg)
+        assert caches[0].dev_info()["world"] == world
+        for rep in reps[1:]:
+            assert rep.iterations == reps[0].iterations
+            assert np.array_equal(rep.y, reps[0].y) and np.array_equal(rep.x.x, reps[0].x.x)
+        rep = reps[0]
+        assert rep.status == ref.status == "converged"
+        assert abs(rep.iterations - ref.iterations) <= 1
+        if rep.iterations == ref.iterations:
+            assert rep.stats.dual_grad_calls == ref.stats.dual_grad_calls
+            assert rep.stats.hessian_vec_calls == ref.stats.hessian_vec_calls
+        assert rep.lipschitz_estimate == pytest.approx(ref.lipschitz_estimate, rel=1e-9)
+        assert np.abs(rep.y - ref.y).max() <= 10 * cfg.eps * (1 + np.abs(ref.y).max())
+        assert np.abs(rep.x.x - ref.x.x).max() <= 10 * cfg.eps * (1 + np.abs(ref.x.x).max())
+        # and the CPU oracle's iteration count
+        orep = orc.solve(po, orc.SolverConfig(eps=1e-6, nama_parallel_linesearch=cfg.nama_parallel_linesearch),
+                         {"minfbe": 0, "nama": 1}[kind])
+        assert abs(rep.iterations - orep["iterations"]) <= 1
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_ranks_solve_c3(gpu, world):
+    """C3 (1.24M variables) sharded at stage 1 over 2 / 3 emulated ranks:
+    NAMA (p-NAMA, 2-RHS sweeps) and MINFBE reach the unsharded handle's
+    iterates with the same iteration counts."""
+    prob = so.gen_random_instance(1, 50, 20, 20, [8, 8, 8, 2])
+    full = so.factor(prob)
+    L, _ = so.estimate_dual_lipschitz(full, prob)
+    for kind in ("nama", "minfbe"):
+        cfg = so.SolverConfig(lambda0=0.9 / L, nama_parallel_linesearch=(kind == "nama"))
+        ref = so.api._solve_direct(kind, prob, full, cfg)
+        reps, _ = _emulated_solve(prob, world, 1, kind, cfg)
+        rep = reps[0]
+        assert rep.status == "converged" and abs(rep.iterations - ref.iterations) <= 1
+        assert np.abs(rep.y - ref.y).max() <= 10 * cfg.eps * (1 + np.abs(ref.y).max())
+        assert rep.residual_inf <= cfg.eps

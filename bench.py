@@ -247,6 +247,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-shard", action="store_true",
                     help="use the sharded (NCCL) handle even at one GPU (exercises the N>1 path)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = one tree of N config-sized subtrees (default); strong = the "
+                         "config's own tree sharded over N GPUs (BASELINE config 4: --config c4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -254,6 +257,9 @@ def main():
         run_reference(args, world, rank)
         return
 
+    # NCCL's version banner goes to stdout, where only the JSON line belongs
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     import torch
     import torch.distributed as dist
 
@@ -267,17 +273,20 @@ def main():
     torch.cuda.set_device(device)
 
     nx, nu, N, br, label = CONFIGS[args.config]
-    units = 1  # C3-sized evaluations per sweep of the benchmarked tree
+    units = 1  # config-sized evaluations per sweep of the benchmarked tree
     sharded = world > 1 or args.force_shard
-    if sharded:
+    if sharded and args.scaling == "weak":
         # Weak scaling over subtree shards: N GPUs solve ONE tree
-        # of N C3-sized subtrees, branching [8N, 8, 8, 2] (N = 1 is exactly
-        # C3), sharded at stage 1 -- each rank owns 8 of the 8N stage-1
-        # subtrees and replicates the root; every sweep exchanges the stage-1
-        # contributions and assembles Hx with NCCL allreduces.
+        # of N config-sized subtrees, branching [8N, ...] (N = 1 is exactly the
+        # config), sharded at stage 1 -- each rank owns 8 of the 8N stage-1
+        # subtrees and replicates the root. Per sweep: one NCCL allreduce of
+        # the stage-1 exchange buffer; per dual-kernel reduction: one
+        # allgather of the ranks' partial sums. x / u / Hx stay on their owners.
         br = [br[0] * world] + list(br[1:])
         units = world
         label = f"{label}; x{world} sharded: one tree [{', '.join(map(str, br))}] over {world} GPUs"
+    elif sharded:
+        label = f"{label}; strong scaling: the same tree sharded over {world} GPUs"
     t0 = time.time()
     prob = so.gen_random_instance(1, nx, nu, N, br)
     cache = so.factor(prob)
@@ -392,12 +401,13 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "dual-grad evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded gen_random_instance, seed 1; random-system tree)",
         "config": {"workload": label, "nodes": prob.num_nodes(), "primal_dim": prob.primal_dim(),
                    "dual_dim": D,
-                   "parallelism": (f"subtree shards x{world} (stage 1, NCCL allreduce of stage-1 "
-                                   f"contributions + Hx per sweep)") if sharded else "1 GPU",
+                   "parallelism": (f"subtree shards x{world} (stage {info['shard_stage']}; per sweep one NCCL "
+                                   f"allreduce of {8 * info.get('exchange_doubles', 0)} B; per dual-kernel "
+                                   "reduction one allgather of partial sums)") if sharded else "1 GPU",
                    "value_units": ("C3-sized dual-grad evaluations (a sweep of the x{0} tree counts {0})"
                                    .format(units)) if sharded else "dual-grad evaluations of the tree",
                    "l2": "inputs larger than L2 (packed matrices %.2f GB vs 126 MB L2)"

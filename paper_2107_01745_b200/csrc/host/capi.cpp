@@ -338,6 +338,7 @@ int scenopt_dev_factor_export(scenopt_dev* h, const scenopt_problem* p, double* 
 int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
   SCN_GUARD({
     const DevState& d = *h->d;
+    *info = scenopt_dev_info{};
     info->device = d.device;
     info->sm_count = d.sm_count;
     info->grid_ctas = d.grid;
@@ -359,6 +360,7 @@ int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
     info->world = d.world;
     info->shard_first = d.shard_lo;
     info->shard_past = d.shard_hi;
+    info->exchange_doubles = d.sharded() ? d.xbuf_rhs : 0;
     info->items_global = d.items_global;
     info->consumer_stage = d.consumer_stage ? 1 : 0;
     info->flat_top = d.flat_top ? 1 : 0;

@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported():
 
 def test_abi_version_and_no_device_here():
     lib = so.lib()
-    assert lib.scenopt_abi_version() == 1
+    assert lib.scenopt_abi_version() == 2
     if so.device_count() == 0:
         prob = so.gen_random_instance(1, 3, 2, 2, 2)
         cache = so.factor(prob)

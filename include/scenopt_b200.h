@@ -261,6 +261,10 @@ int scenopt_nccl_unique_id(void* out128);
  * world + 1 bounds of the ranks' shard-stage node ranges. */
 int scenopt_shard_plan(const scenopt_problem* p, int world, int shard_stage, int32_t* stage_out,
                        int32_t* bounds);
+/* Host-only: the dual rows rank `rank` counts in the sharded reductions
+ * (counted[i] = 1: a stage or terminal row of its subtrees, or a top row on
+ * rank 0), dual_dim bytes. */
+int scenopt_shard_rows(const scenopt_problem* p, int world, int shard_stage, int rank, uint8_t* counted);
 int scenopt_dev_create_sharded(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
                                int world, int shard_stage, const void* nccl_id, scenopt_dev** out);
 /* Emulated shard group: `world` sharded handles of ONE process, driven by one

@@ -241,6 +241,16 @@ int scenopt_shard_plan(const scenopt_problem* p, int world, int shard_stage, int
   });
 }
 
+int scenopt_shard_rows(const scenopt_problem* p, int world, int shard_stage, int rank, uint8_t* counted) {
+  SCN_GUARD({
+    if (world < 1 || rank < 0 || rank >= world) fail(SCENOPT_E_INVALID_PARAMS, "shard rows: bad rank/world");
+    int s = shard_stage;
+    const std::vector<int> b = shard_plan(p->p, world, &s);
+    const std::vector<uint8_t> cnt = shard_rows(p->p, shard_nodes(p->p, s, b[rank], b[rank + 1], rank));
+    std::copy(cnt.begin(), cnt.end(), counted);
+  });
+}
+
 int scenopt_dev_create_sharded(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
                                int world, int shard_stage, const void* nccl_id, scenopt_dev** out) {
   SCN_GUARD({

@@ -150,6 +150,31 @@ std::vector<int> shard_plan(const Problem& p, int world, int* stage) {
   return balanced_split(subtree_bytes(p, bws, fws), p.stage_offsets[s], p.stage_offsets[s + 1], world);
 }
 
+std::vector<char> shard_nodes(const Problem& p, int stage, int lo, int hi, int rank) {
+  std::vector<char> mine(static_cast<size_t>(p.n), 0);
+  for (int c = 0; c < p.stage_offsets[stage]; ++c) mine[c] = rank == 0;
+  for (int t = stage; t <= p.N; ++t) {
+    for (int c = lo; c < hi; ++c) mine[c] = 1;
+    if (t < p.N && lo < hi) {
+      const int nlo = p.child_begin[lo], nhi = p.child_begin[hi - 1] + p.child_count[hi - 1];
+      lo = nlo;
+      hi = nhi;
+    }
+  }
+  return mine;
+}
+
+std::vector<uint8_t> shard_rows(const Problem& p, const std::vector<char>& mine) {
+  std::vector<uint8_t> cnt(static_cast<size_t>(p.dual_dim), 0);
+  for (int c = 1; c < p.n; ++c)
+    if (mine[c])
+      for (int k = 0; k < p.stage_rows[c]; ++k) cnt[p.dual_offset[c] + k] = 1;
+  for (int l = 0; l < p.L; ++l)
+    if (mine[p.first_leaf + l])
+      for (int k = 0; k < p.terminal_rows[l]; ++k) cnt[p.tdual_offset[l] + k] = 1;
+  return cnt;
+}
+
 std::unique_ptr<DevState> dev_create_bare(int device) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -1035,19 +1060,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   SCN_CUDA(cudaMemset(d->fw_flag, 0, static_cast<size_t>(n) * sizeof(unsigned)));
 
   std::vector<char> mine;
-  if (d->sharded()) {  // nodes whose cost this rank evaluates: own subtrees, top on rank 0
-    mine.assign(static_cast<size_t>(n), 0);
-    for (int c = 0; c < p.stage_offsets[d->shard_stage]; ++c) mine[c] = shard->rank == 0;
-    int lo = d->shard_lo, hi = d->shard_hi;
-    for (int t = d->shard_stage; t <= p.N; ++t) {
-      for (int c = lo; c < hi; ++c) mine[c] = 1;
-      if (t < p.N && lo < hi) {
-        const int nlo = p.child_begin[lo], nhi = p.child_begin[hi - 1] + p.child_count[hi - 1];
-        lo = nlo;
-        hi = nhi;
-      }
-    }
-  }
+  if (d->sharded())  // nodes whose cost this rank evaluates: own subtrees, top on rank 0
+    mine = shard_nodes(p, d->shard_stage, d->shard_lo, d->shard_hi, shard->rank);
   clk.mark("upload blocks");
   pack_common(*d, p, d->sharded() ? &mine : nullptr);
   clk.mark("pack_common");
@@ -1057,7 +1071,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     d->world = shard->world;
     // rows / nodes this rank owns (counted in reductions and gathers): its
     // subtrees' stage and terminal rows, and the replicated top on rank 0
-    std::vector<uint8_t> cnt(static_cast<size_t>(std::max(D, 1)), 0);
+    std::vector<uint8_t> cnt = shard_rows(p, mine);
+    if (cnt.empty()) cnt.push_back(0);
     auto add = [](std::vector<std::pair<int64_t, int64_t>>& v, int64_t a, int64_t b) {
       if (b <= a) return;
       if (!v.empty() && v.back().second == a)
@@ -1065,12 +1080,6 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
       else
         v.push_back({a, b});
     };
-    for (int c = 1; c < n; ++c)
-      if (mine[c])
-        for (int k = 0; k < p.stage_rows[c]; ++k) cnt[p.dual_offset[c] + k] = 1;
-    for (int l = 0; l < p.L; ++l)
-      if (mine[p.first_leaf + l])
-        for (int k = 0; k < p.terminal_rows[l]; ++k) cnt[p.tdual_offset[l] + k] = 1;
     for (int i = 0; i < D; ++i)
       if (cnt[i]) add(d->keep_y, i, i + 1);
     for (int c = 0; c < n; ++c)

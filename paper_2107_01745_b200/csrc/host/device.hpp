@@ -150,6 +150,11 @@ struct ShardSpec {
 // Host-only shard plan: *stage (in: -1 = auto) and the world+1 bounds of the
 // ranks' contiguous shard-stage node ranges, balanced by subtree bytes.
 std::vector<int> shard_plan(const Problem& p, int world, int* stage);
+// Host-only ownership of rank `rank` whose shard-stage nodes are [lo, hi):
+// node mask (its subtrees; the top stages on rank 0) and the dual rows it
+// counts in reductions (stage and terminal rows of its nodes).
+std::vector<char> shard_nodes(const Problem& p, int stage, int lo, int hi, int rank);
+std::vector<uint8_t> shard_rows(const Problem& p, const std::vector<char>& mine);
 std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* f, int device,
                                      const ShardSpec* shard = nullptr);
 // Handle whose factor is computed on the device (K9, factor.cu): the host

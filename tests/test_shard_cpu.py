@@ -1,9 +1,13 @@
 """Host logic of subtree sharding over world_size 2 on CPU
 (gloo): both ranks derive the same shard plan from the C-ABI
 (scenopt_shard_plan, host-only), their node sets partition the tree below
-the shard stage with the top replicated, and the exchange the sharded sweep
-performs -- a sum-allreduce of disjoint row sets with the replicated top kept
-on rank 0 -- reassembles the oracle's full x, u and Hx exactly."""
+the shard stage with the top replicated, and the row ownership the library
+uses (scenopt_shard_rows) is that partition. On the oracle's vectors: the
+gathers of sharded results (sum-allreduce of disjoint row sets, top on rank
+0) reassemble the full x, u and Hx exactly; the sweep's exchange of the
+shard-stage dual rows gives every rank all of them; and a dual-kernel
+reduction done the sharded way (partial sums over counted rows, allgather,
+rank-order combine) gives every rank the same bits, equal to the full sum."""
 import ctypes as C
 import os
 import socket
@@ -79,6 +83,41 @@ def _worker(rank, world, port, out):
                 part = torch.from_numpy(np.where(mask, full, 0.0))
                 dist.all_reduce(part)
                 assert np.array_equal(part.numpy(), full)
+            # the library's own row ownership (scenopt_shard_rows) is this mask
+            counted = np.zeros(prob.dual_dim, np.uint8)
+            so.api.check(so.lib().scenopt_shard_rows(prob._h, world, stage, rank,
+                                                     counted.ctypes.data_as(C.POINTER(C.c_uint8))))
+            assert np.array_equal(counted.astype(bool), rows)
+            # the sweep's exchange also carries the shard-stage nodes' dual rows:
+            # owners write theirs, the sum is every rank's copy of those rows
+            lo_s, hi_s = so_[s], so_[s + 1]
+            r0, r1 = doff[lo_s - 1], doff[hi_s - 1]
+            ysec = np.where(rows[r0:r1], y[r0:r1], 0.0)
+            t = torch.from_numpy(ysec.copy())
+            dist.all_reduce(t)
+            assert np.array_equal(t.numpy(), y[r0:r1])
+            # a dual-kernel reduction: each rank's partial sums over its counted
+            # rows (the FB step's conj / |z|^2 / <Hx,R> / |R|^2, and max |R|),
+            # allgathered and combined in rank order -- the same bits on
+            # every rank, equal to the full reduction
+            g = orc.Nonsmooth.from_problem(po)
+            st_ = orc.fb_step(fac, g, y, 0.37)
+            z, R, T = st_["z"], st_["R"], st_["T"]
+            conj_rows = np.array([g.conj(np.where(np.arange(len(T)) == i, T, 0.0)) for i in range(len(T))])
+            terms = np.stack([conj_rows, z * z, st_["Hx"] * R, R * R])
+            part = np.concatenate([np.where(rows, terms, 0.0).sum(axis=1), [np.abs(np.where(rows, R, 0.0)).max()]])
+            gathered = [torch.zeros(5, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(gathered, torch.from_numpy(part))
+            tot = gathered[0].numpy().copy()
+            for q in range(1, world):
+                tot[:4] += gathered[q].numpy()[:4]
+                tot[4] = max(tot[4], gathered[q].numpy()[4])
+            every = [torch.zeros(5, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(every, torch.from_numpy(tot))
+            assert all(np.array_equal(e.numpy(), tot) for e in every)
+            full = np.concatenate([terms.sum(axis=1), [np.abs(R).max()]])
+            assert np.allclose(tot, full, rtol=1e-12, atol=1e-12)
+            assert tot[0] == pytest.approx(st_["conj_T"], rel=1e-12, abs=1e-12)
         out.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         out.put((rank, repr(e)))

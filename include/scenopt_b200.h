@@ -352,6 +352,10 @@ void scenopt_lbfgs_destroy(scenopt_lbfgs* b);
 /* ---- solvers: solvers.hpp:89-720 ---------------------------------------- */
 /* estimate_dual_lipschitz, solvers.hpp:89-113 */
 int scenopt_estimate_lipschitz(scenopt_dev* d, uint64_t* calls, double* out);
+/* The same with the reference's optional arguments (solvers.hpp:88-93):
+ * stop when the Rayleigh quotient moves by <= rel_tol relative, or after
+ * max_rounds sweeps (max_rounds <= 0: no sweep, 1e-12). */
+int scenopt_estimate_lipschitz_ex(scenopt_dev* d, double rel_tol, int max_rounds, uint64_t* calls, double* out);
 /* solve_minfbe (kind 0) / solve_nama (1) / solve_gpad (2) from y0 (host,
  * NULL = zeros), optional residual weight (host, NULL = none). */
 int scenopt_dev_solve(scenopt_dev* d, const scenopt_solver_config* cfg, int kind, const double* y0,

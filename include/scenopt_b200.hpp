@@ -1366,16 +1366,13 @@ inline SolverReport run_solver(const ProblemInstance& prob, const FactorCache& c
 }
 }  // namespace detail
 
-/// estimate_dual_lipschitz, solvers.hpp:89-113 (power iteration on the
-/// device; the reference's defaults rel_tol 1e-6, max_rounds 100).
+/// estimate_dual_lipschitz, solvers.hpp:89-113 (power iteration on the device).
 inline double estimate_dual_lipschitz(const FactorCache& cache, const ProblemInstance& prob,
                                       std::uint64_t* calls = nullptr, double rel_tol = 1e-6, int max_rounds = 100) {
-  if (rel_tol != 1e-6 || max_rounds != 100)
-    throw InvalidParams("estimate_dual_lipschitz: the device path implements rel_tol 1e-6, max_rounds 100");
   detail::check_shapes(cache, prob, "estimate_dual_lipschitz");
   std::uint64_t n = 0;
   double L = 0.0;
-  detail::check(scenopt_estimate_lipschitz(cache.state->device_for(prob), &n, &L));
+  detail::check(scenopt_estimate_lipschitz_ex(cache.state->device_for(prob), rel_tol, max_rounds, &n, &L));
   if (calls) *calls += n;
   return L;
 }

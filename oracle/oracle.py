@@ -473,10 +473,11 @@ class Factor:
                                     C.byref(out)))
         return out.value
 
-    def estimate_lipschitz(self):
+    def estimate_lipschitz(self, rel_tol: float = 1e-6, max_rounds: int = 100):
         calls = C.c_uint64()
         out = C.c_double()
-        _check(lib().orc_estimate_lipschitz(self.h, self.prob.h, C.byref(calls), C.byref(out)))
+        _check(lib().orc_estimate_lipschitz_ex(self.h, self.prob.h, C.c_double(rel_tol), int(max_rounds),
+                                               C.byref(calls), C.byref(out)))
         return out.value, int(calls.value)
 
     def time_sweeps(self, nsweeps: int, affine: bool = True) -> float:

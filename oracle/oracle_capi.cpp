@@ -632,6 +632,10 @@ double orc_lbfgs_gamma0(const orc_lbfgs* b) { return b->buf.gamma0(); }
 int orc_estimate_lipschitz(const orc_factor* f, const orc_problem* p, uint64_t* calls, double* out) {
   ORC_GUARD(*out = estimate_dual_lipschitz(f->cache, p->prob, calls))
 }
+int orc_estimate_lipschitz_ex(const orc_factor* f, const orc_problem* p, double rel_tol, int max_rounds,
+                              uint64_t* calls, double* out) {
+  ORC_GUARD(*out = estimate_dual_lipschitz(f->cache, p->prob, calls, rel_tol, max_rounds))
+}
 
 int orc_solve(const orc_problem* p, const orc_solver_config* cfg, int kind, const orc_factor* shared,
               orc_report** out) {

@@ -167,6 +167,8 @@ double orc_lbfgs_gamma0(const orc_lbfgs* b);
 
 /* solvers: kind 0 MINFBE, 1 NAMA, 2 GPAD */
 int orc_estimate_lipschitz(const orc_factor* f, const orc_problem* p, uint64_t* calls, double* out);
+int orc_estimate_lipschitz_ex(const orc_factor* f, const orc_problem* p, double rel_tol, int max_rounds,
+                              uint64_t* calls, double* out);
 int orc_solve(const orc_problem* p, const orc_solver_config* cfg, int kind, const orc_factor* shared,
               orc_report** out);
 int orc_solve_direct(const orc_problem* p, const orc_factor* f, const orc_solver_config* cfg,

@@ -836,12 +836,14 @@ def _report(prob: ProblemInstance, h) -> SolverReport:
         verify_subdiff_dist=s.verify_subdiff_dist, _h=h)
 
 
-def estimate_dual_lipschitz(cache: FactorCache, prob: ProblemInstance):
+def estimate_dual_lipschitz(cache: FactorCache, prob: ProblemInstance, rel_tol: float = 1e-6,
+                            max_rounds: int = 100):
     """solvers.hpp:89-113 -> (estimate, sweeps)."""
     _check_shapes(cache, prob, "estimate_dual_lipschitz")
     calls = C.c_uint64()
     out = C.c_double()
-    check(N.lib().scenopt_estimate_lipschitz(cache.device(), C.byref(calls), C.byref(out)))
+    check(N.lib().scenopt_estimate_lipschitz_ex(cache.device(), C.c_double(rel_tol), int(max_rounds),
+                                                C.byref(calls), C.byref(out)))
     return out.value, int(calls.value)
 
 

@@ -494,6 +494,7 @@ struct Engine {
 
   // estimate_dual_lipschitz (solvers.hpp:89-113)
   double lipschitz(uint64_t* calls, double rel_tol = 1e-6, int max_rounds = 100) {
+    if (max_rounds <= 0) return 1e-12;  // no round: the Rayleigh quotient stays 0 (solvers.hpp:99-112)
     const int n = d.lay.dual_dim;
     std::vector<double> v(static_cast<size_t>(n));
     std::mt19937_64 gen(0x5eed5eed5eed5eedULL);
@@ -1159,6 +1160,13 @@ int scenopt_estimate_lipschitz(scenopt_dev* h, uint64_t* calls, double* out) {
   SCN_GUARD({
     Engine e(*h);
     *out = e.lipschitz(calls);
+  });
+}
+
+int scenopt_estimate_lipschitz_ex(scenopt_dev* h, double rel_tol, int max_rounds, uint64_t* calls, double* out) {
+  SCN_GUARD({
+    Engine e(*h);
+    *out = e.lipschitz(calls, rel_tol, max_rounds);
   });
 }
 

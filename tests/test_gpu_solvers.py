@@ -250,3 +250,17 @@ def test_lipschitz_estimate_rounds_match_oracle(gpu):
     c, oc = cfgs()
     rep = so.solve(prob, c, "nama")
     assert rep.lipschitz_calls == calls
+
+
+@pytest.mark.parametrize("rel_tol,max_rounds", [(1e-3, 100), (0.0, 7), (1e-9, 13), (1e-6, 0), (1e-6, 1)])
+def test_lipschitz_optional_arguments_match_oracle(gpu, rel_tol, max_rounds):
+    """estimate_dual_lipschitz(cache, prob, calls, rel_tol, max_rounds)
+    (solvers.hpp:88-93): other tolerances and caps stop at the reference's
+    round with the reference's estimate (max_rounds <= 0: no sweep, 1e-12)."""
+    rng = orc.Rng(1302)
+    for trial in range(3):
+        po, prob = fixture(rng, feasible_box(), stages=4, max_nodes=30)
+        est, calls = so.estimate_dual_lipschitz(so.factor(prob), prob, rel_tol, max_rounds)
+        oest, ocalls = orc.Factor(po).estimate_lipschitz(rel_tol, max_rounds)
+        assert calls == ocalls and calls <= max(max_rounds, 0)
+        assert est == pytest.approx(oest, rel=1e-9)

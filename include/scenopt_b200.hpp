@@ -10,8 +10,9 @@
 //   * Mat / Vec are small in-house column-major types with the subset of the
 //     Eigen API the callers use (the reference's Eigen types are not
 //     available in this image).
-//   * FactorCache keeps the factor on the C side; its matrices are copied
-//     into the reference's fields only by load_matrices() (1.2 GB at C3).
+//   * factor() fills FactorCache's matrix members as the reference does;
+//     factor(prob, FactorMembers::on_demand) keeps the factor on the C side
+//     only (no host copy: 1.2 GB at C3) until load_matrices() is called.
 //   * The device handle of a (ProblemInstance, FactorCache) pair is created
 //     on first use and snapshots the instance. After changing an instance's
 //     affine data call refactor_affine(cache, prob), as with the reference.
@@ -866,6 +867,7 @@ struct FactorCache {
   std::vector<Vec> leaf_costate_affine;
 
   std::shared_ptr<detail::FactorState> state;
+  bool members_loaded = false;  // the fields above hold the current factor
 
   /// Copies the factor's matrices into the reference's fields.
   void load_matrices(const ProblemInstance& prob) {
@@ -920,8 +922,12 @@ struct FactorCache {
     }
     leaf_costate_affine.assign(static_cast<size_t>(L), Vec());
     for (int l = 0; l < L; ++l) leaf_costate_affine[l] = vec(lca.data() + static_cast<size_t>(l) * nx, nx);
+    members_loaded = true;
   }
 };
+
+/// Whether factor() copies the factor into FactorCache's matrix members.
+enum class FactorMembers { full, on_demand };
 
 namespace detail {
 /// riccati.hpp:67-74
@@ -938,7 +944,7 @@ inline void need_dual(const ProblemInstance& prob, const Vec& y, const char* who
 
 /// factor(), riccati.hpp:82-182 (host, offline; the device handle is built
 /// on first use).
-inline FactorCache factor(const ProblemInstance& prob) {
+inline FactorCache factor(const ProblemInstance& prob, FactorMembers members = FactorMembers::full) {
   auto st = std::make_shared<detail::FactorState>();
   st->prob = detail::to_handle(prob);
   st->src = &prob;
@@ -952,6 +958,7 @@ inline FactorCache factor(const ProblemInstance& prob) {
   c.first_leaf = prob.tree.first_leaf();
   c.dual_dim = prob.dual_dim;
   c.state = st;
+  if (members == FactorMembers::full) c.load_matrices(prob);
   return c;
 }
 
@@ -985,6 +992,7 @@ inline void refactor_affine(FactorCache& cache, const ProblemInstance& prob) {
   if (cache.state->on_device) {
     auto ph = detail::to_handle(prob);
     detail::check(scenopt_dev_refactor_affine(cache.state->dev.get(), ph.get()));
+    if (cache.members_loaded) cache.load_matrices(prob);
     return;
   }
   auto st = std::make_shared<detail::FactorState>(*cache.state);
@@ -996,6 +1004,7 @@ inline void refactor_affine(FactorCache& cache, const ProblemInstance& prob) {
   st->alt_dev.reset();
   st->alt_src = nullptr;
   cache.state = st;
+  if (cache.members_loaded) cache.load_matrices(prob);  // the affine members changed
 }
 
 // ------------------------------------------------------------------ tree_oracles.hpp:14-129

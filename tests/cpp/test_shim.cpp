@@ -251,6 +251,37 @@ TEST_CASE("configuration and buffer parameters are validated", true) {
   CHECK_THROWS_AS(scenopt::gen_random_instance(1, scenopt::RandomDims{0, 2}), scenopt::InvalidParams);
 }
 
+TEST_CASE("factor() fills the reference's FactorCache members; refactor_affine refreshes them", true) {
+  const auto prob = small(10);
+  auto cache = scenopt::factor(prob);
+  const int F = prob.tree.first_leaf(), nx = prob.nx, nu = prob.nu;
+  REQUIRE(static_cast<int>(cache.gain.size()) == F && cache.members_loaded);
+  REQUIRE(static_cast<int>(cache.closed_loop.size()) == prob.num_nodes());
+  // closed_loop_c = A_c + B_c gain_parent (riccati.hpp:171)
+  double gap = 0.0;
+  for (int c = 1; c < prob.num_nodes(); ++c) {
+    const int a = prob.tree.ancestor[static_cast<size_t>(c)];
+    for (int i = 0; i < nx; ++i)
+      for (int j = 0; j < nx; ++j) {
+        double v = prob.dyn[c].A(i, j);
+        for (int k = 0; k < nu; ++k) v += prob.dyn[c].B(i, k) * cache.gain[a](k, j);
+        gap = std::max(gap, std::abs(v - cache.closed_loop[c](i, j)));
+      }
+  }
+  CHECK(gap < 1e-12);
+  const auto lazy = scenopt::factor(prob, scenopt::FactorMembers::on_demand);
+  CHECK(lazy.gain.empty() && !lazy.members_loaded);
+  const Vec before = cache.costate_affine[0];
+  auto prob2 = prob;
+  for (int i = 1; i < prob2.num_nodes(); ++i) prob2.cost[i].q = prob2.cost[i].q * 1.5;
+  scenopt::refactor_affine(cache, prob2);
+  const auto fresh = scenopt::factor(prob2);
+  double agap = 0.0;
+  for (int i = 0; i < F; ++i) agap = std::max(agap, max_abs(cache.costate_affine[i] - fresh.costate_affine[i]));
+  CHECK(agap < 1e-12);
+  CHECK(max_abs(cache.costate_affine[0] - before) > 1e-9);  // the members moved with the affine data
+}
+
 // ---------------------------------------------------------------- device
 TEST_CASE("dual_grad output is dynamics-feasible", false) {
   Rng rng(41);

@@ -152,6 +152,120 @@ double now_ms() {
       .count();
 }
 
+// Result arrays of a report (x, u, y, z): page-locked host memory from a
+// process-wide pool, so the final download runs at full PCIe rate (a fresh
+// pageable 10.5 MB vector costs ~2.7 ms of page faults and zero-fill at C3,
+// and pageable D2H copies are staged at a fraction of the pinned rate; both
+// sit inside wall_ms). Destroyed reports return their arrays to the pool
+// (at most 16 arrays and 256 MB; a request takes the smallest array that
+// fits, and only one at most twice its size). Falls back to pageable memory
+// when page-locked memory is unavailable.
+class ResultArray {
+ public:
+  ResultArray() = default;
+  ResultArray(const ResultArray&) = delete;
+  ResultArray& operator=(const ResultArray&) = delete;
+  ResultArray(ResultArray&& o) noexcept { swap(o); }
+  ResultArray& operator=(ResultArray&& o) noexcept {
+    swap(o);
+    return *this;
+  }
+  ~ResultArray() { give(); }
+  void take(size_t n);  // n elements, contents unspecified (overwritten by the download)
+  void give();          // back to the pool
+  void assign(size_t n, double v) {
+    take(n);
+    std::fill(p_, p_ + n_, v);
+  }
+  size_t size() const { return n_; }
+  bool empty() const { return n_ == 0; }
+  double* data() { return p_; }
+  const double* data() const { return p_; }
+  double& operator[](size_t i) { return p_[i]; }
+  double operator[](size_t i) const { return p_[i]; }
+  double* begin() { return p_; }
+  double* end() { return p_ + n_; }
+
+ private:
+  void swap(ResultArray& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    std::swap(cap_, o.cap_);
+    std::swap(pinned_, o.pinned_);
+  }
+  double* p_ = nullptr;
+  size_t n_ = 0, cap_ = 0;
+  bool pinned_ = false;
+};
+
+namespace {
+struct PoolBlock {
+  double* p;
+  size_t cap;
+  bool pinned;
+};
+std::mutex g_arrays_mu;
+std::vector<PoolBlock> g_arrays;
+size_t g_arrays_bytes = 0;
+constexpr size_t kArraysKept = 16, kArraysMaxBytes = size_t(256) << 20;
+void free_block(const PoolBlock& b) {
+  if (b.pinned)
+    cudaFreeHost(b.p);
+  else
+    std::free(b.p);
+}
+}  // namespace
+
+void ResultArray::take(size_t n) {
+  give();
+  if (n == 0) return;
+  {
+    std::lock_guard<std::mutex> lk(g_arrays_mu);
+    size_t best = g_arrays.size();
+    for (size_t i = 0; i < g_arrays.size(); ++i)  // the smallest that fits, at most 2n
+      if (g_arrays[i].cap >= n && g_arrays[i].cap <= 2 * n &&
+          (best == g_arrays.size() || g_arrays[i].cap < g_arrays[best].cap))
+        best = i;
+    if (best < g_arrays.size()) {
+      const PoolBlock b = g_arrays[best];
+      g_arrays_bytes -= b.cap * sizeof(double);
+      g_arrays.erase(g_arrays.begin() + static_cast<std::ptrdiff_t>(best));
+      p_ = b.p;
+      cap_ = b.cap;
+      pinned_ = b.pinned;
+      n_ = n;
+      return;
+    }
+  }
+  void* q = nullptr;
+  if (cudaMallocHost(&q, n * sizeof(double)) == cudaSuccess) {
+    pinned_ = true;
+  } else {
+    cudaGetLastError();
+    q = std::malloc(n * sizeof(double));
+    if (!q) throw std::bad_alloc();
+    pinned_ = false;
+  }
+  p_ = static_cast<double*>(q);
+  cap_ = n_ = n;
+}
+
+void ResultArray::give() {
+  if (!p_) return;
+  const PoolBlock b{p_, cap_, pinned_};
+  p_ = nullptr;
+  n_ = cap_ = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_arrays_mu);
+    if (g_arrays.size() < kArraysKept && g_arrays_bytes + b.cap * sizeof(double) <= kArraysMaxBytes) {
+      g_arrays_bytes += b.cap * sizeof(double);
+      g_arrays.push_back(b);
+      return;
+    }
+  }
+  free_block(b);
+}
+
 struct Report {  // SolverReport, solvers.hpp:66-84
   int status = 1, iterations = 0;
   Stats stats;
@@ -161,47 +275,10 @@ struct Report {  // SolverReport, solvers.hpp:66-84
   bool verified = false;
   double verify_residual_inf = std::numeric_limits<double>::infinity();
   double verify_subdiff_dist = std::numeric_limits<double>::infinity();
-  std::vector<double> residual_trace, fbe_trace, x, u, y, z;
+  std::vector<double> residual_trace, fbe_trace;
+  ResultArray x, u, y, z;
 };
 
-// Result arrays of destroyed reports, kept resident for the next solve's
-// download: a fresh 10.5 MB std::vector costs ~2.7 ms of page faults and
-// zero-fill on the host at C3, inside wall_ms; a recycled one costs nothing.
-namespace {
-std::mutex g_arrays_mu;
-std::vector<std::vector<double>> g_arrays;
-size_t g_arrays_bytes = 0;
-// at most 16 arrays and 256 MB are kept; a request takes the smallest array
-// that fits, and only one at most twice its size
-constexpr size_t kArraysKept = 16, kArrayMinBytes = 1 << 16, kArraysMaxBytes = size_t(256) << 20;
-void array_take(std::vector<double>& dst, size_t n) {
-  {
-    std::lock_guard<std::mutex> lk(g_arrays_mu);
-    size_t best = g_arrays.size();
-    for (size_t i = 0; i < g_arrays.size(); ++i)  // the smallest that fits
-      if (g_arrays[i].capacity() >= n && g_arrays[i].capacity() <= 2 * n &&
-          (best == g_arrays.size() || g_arrays[i].capacity() < g_arrays[best].capacity()))
-        best = i;
-    if (best < g_arrays.size()) {
-      g_arrays_bytes -= g_arrays[best].capacity() * sizeof(double);
-      dst.swap(g_arrays[best]);
-      g_arrays.erase(g_arrays.begin() + static_cast<std::ptrdiff_t>(best));
-    }
-  }
-  dst.resize(n);  // every element is overwritten by the download
-}
-void array_give(std::vector<double>& v) {
-  const size_t bytes = v.capacity() * sizeof(double);
-  if (bytes < kArrayMinBytes) return;
-  std::lock_guard<std::mutex> lk(g_arrays_mu);
-  if (g_arrays.size() < kArraysKept && g_arrays_bytes + bytes <= kArraysMaxBytes) {
-    g_arrays_bytes += bytes;
-    g_arrays.push_back(std::move(v));
-  }
-}
-}  // namespace
-
-void validate_for(const scenopt_solver_config& c, const DevState& d);
 // solvers.hpp:48-60
 void validate_config(const scenopt_solver_config& c) {
   if (c.lambda0 < 0.0) fail(SCENOPT_E_INVALID_PARAMS, "lambda0 must be >= 0");
@@ -554,11 +631,11 @@ struct Loop {
     rep.residual_inf = residual;
     rep.lambda_final = lambda;
     const Layout& L = e.d.lay;
-    array_take(rep.x, static_cast<size_t>(L.nx) * L.n);
-    array_take(rep.u, static_cast<size_t>(L.nu) * L.first_leaf);
-    array_take(rep.y, static_cast<size_t>(L.dual_dim));
-    array_take(rep.z, static_cast<size_t>(L.dual_dim));
-    auto dl = [&](std::vector<double>& dst, const double* src) {
+    rep.x.take(static_cast<size_t>(L.nx) * L.n);
+    rep.u.take(static_cast<size_t>(L.nu) * L.first_leaf);
+    rep.y.take(static_cast<size_t>(L.dual_dim));
+    rep.z.take(static_cast<size_t>(L.dual_dim));
+    auto dl = [&](ResultArray& dst, const double* src) {
       if (!dst.empty())
         SCN_CUDA(cudaMemcpyAsync(dst.data(), src, dst.size() * sizeof(double), cudaMemcpyDeviceToHost, e.st));
     };
@@ -1228,7 +1305,7 @@ int scenopt_report_arrays(const scenopt_report* rr, double* x, double* u, double
                           double* ft) {
   SCN_GUARD({
     const Report& r = rr->r;
-    auto cp = [](const std::vector<double>& v, double* dst) {
+    auto cp = [](const auto& v, double* dst) {
       if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
     };
     cp(r.x, x);
@@ -1240,11 +1317,7 @@ int scenopt_report_arrays(const scenopt_report* rr, double* x, double* u, double
   });
 }
 
-void scenopt_report_destroy(scenopt_report* r) {
-  if (r)
-    for (auto* v : {&r->r.x, &r->r.u, &r->r.y, &r->r.z}) array_give(*v);
-  delete r;
-}
+void scenopt_report_destroy(scenopt_report* r) { delete r; }  // result arrays go back to the pool
 
 // ------------------------------------------------------------------ L-BFGS handle (lbfgs.hpp)
 int scenopt_lbfgs_create(scenopt_dev* h, int memory, double eps_curv, scenopt_lbfgs** out) {

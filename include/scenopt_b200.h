@@ -255,7 +255,11 @@ int scenopt_dev_create(const scenopt_problem* p, const scenopt_factor* f, int de
  * world == 1 needs none). The same problem and factor must be passed on
  * every rank. Replaces nothing in the reference (single-process); every
  * other entry point accepts the sharded handle (solvers: memory <= 6;
- * scenopt_linesearch_cert with explicit trials: unsharded handles only). */
+ * scenopt_linesearch_cert with explicit trials: unsharded handles only).
+ * f == NULL: the factor is computed on the device (K9): each rank factors
+ * its own subtrees, the shard-stage value matrices are exchanged in one
+ * sum-allreduce, and every rank factors the replicated top; no rank needs a
+ * host factor. */
 int scenopt_nccl_unique_id(void* out128);
 /* Host-only plan of the above: the shard stage actually used and the
  * world + 1 bounds of the ranks' shard-stage node ranges. */

@@ -446,11 +446,31 @@ class DeviceFactorCache(FactorCache):
     sweep layout by a per-stage GPU kernel; export() reads it back in the
     FactorCache layout."""
 
-    def __init__(self, prob: ProblemInstance, device: int = 0):
+    def __init__(self, prob: ProblemInstance, device: int = 0, _handle=None):
         super().__init__(None, prob)
-        h = C.c_void_p()
-        check(N.lib().scenopt_dev_create_device_factor(prob._h, device, C.byref(h)))
+        h = _handle
+        if h is None:
+            h = C.c_void_p()
+            check(N.lib().scenopt_dev_create_device_factor(prob._h, device, C.byref(h)))
         self._dev = h
+
+    @classmethod
+    def sharded(cls, prob: ProblemInstance, rank: int, world: int = 1, nccl_id: bytes | None = None,
+                group: "ShardGroup | None" = None, device: int = 0, stage: int = -1) -> "DeviceFactorCache":
+        """A subtree-sharded handle whose factor is computed on the device
+        (each rank factors its own subtrees and the replicated top; no host
+        factor): one rank of an NCCL group (nccl_id) or of an emulated
+        ShardGroup (group)."""
+        h = C.c_void_p()
+        if group is not None:
+            check(N.lib().scenopt_dev_create_sharded_group(prob._h, None, device, rank, group._h, stage,
+                                                           C.byref(h)))
+        else:
+            if nccl_id is not None and len(nccl_id) != 128:
+                raise InvalidParams("sharded(): nccl_id must be 128 bytes")
+            buf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+            check(N.lib().scenopt_dev_create_sharded(prob._h, None, device, rank, world, stage, buf, C.byref(h)))
+        return cls(prob, device, _handle=h)
 
     def device(self, device: int = 0):
         return self._dev

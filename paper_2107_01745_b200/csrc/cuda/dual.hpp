@@ -150,10 +150,12 @@ struct CostPack {
   const double* prob;
   const int32_t* nodes;  // non-root nodes evaluated here (all, or a rank's share)
   int nnodes;
-  const double* node;    // per listed node: [A | B | c | Q | S | R | q | r]
+  const double* node;    // cost blocks [A | B | c | Q | S | R | q | r] of the handle's nodes
+  const int32_t* slot;   // [n]: block of node i in `node` (-1: not on this handle)
   const int32_t* leaves; // leaves evaluated here
   int nleaves;
-  const double* leaf;    // per listed leaf: [P | p]
+  const double* leaf;    // blocks [P | p] of the handle's leaves
+  const int32_t* lslot;  // [L]: block of leaf l in `leaf` (-1: not on this handle)
   const double* root_state;
   int check_root;        // 1: include the x^0 = p check
 };

@@ -1185,7 +1185,7 @@ __global__ void __launch_bounds__(kThreads) eval_f_kernel(DualCtx c, CostPack cp
     if (t < NN) {
       const int nd = cp.nodes[t];
       const int64_t a = cp.anc[nd];
-      const double* blk = cp.node + static_cast<int64_t>(t) * csz;
+      const double* blk = cp.node + static_cast<int64_t>(cp.slot[nd]) * csz;
       const double *A = blk, *B = A + nx * nx, *cv = B + nx * nu, *Q = cv + nx, *Sm = Q + nx * nx,
                    *Rm = Sm + nu * nx, *q = Rm + nu * nu, *r = q + nx;
       const double* xa = x + a * nx;
@@ -1212,7 +1212,7 @@ __global__ void __launch_bounds__(kThreads) eval_f_kernel(DualCtx c, CostPack cp
     } else {
       const int l = t - NN;
       const int nd = cp.leaves[l];
-      const double* P = cp.leaf + static_cast<int64_t>(l) * lsz;
+      const double* P = cp.leaf + static_cast<int64_t>(cp.lslot[nd - cp.first_leaf]) * lsz;
       const double* p = P + nx * nx;
       const double* xc = x + static_cast<int64_t>(nd) * nx;
       double part = 0.0;

@@ -90,13 +90,19 @@ __device__ void chol_solve(const double* L, int n, double* X, int ldx, int ncol,
   }
 }
 
+// problem data of node c / leaf l on this handle (a sharded handle holds its
+// own nodes, the replicated top and the shard-stage nodes)
+__device__ __forceinline__ const double* cost_of(const FactorParams& F, int c, int64_t csz) {
+  return F.cost_node + static_cast<int64_t>(F.cost_slot[c]) * csz;
+}
+
 __global__ void __launch_bounds__(kT) factor_leaves(FactorParams F) {
   const int nx = F.nx, nu = F.nu, W = nx + nu;
   const int64_t lsz = static_cast<int64_t>(nx) * nx + nx;
   for (int l = blockIdx.x; l < F.stage_count; l += gridDim.x) {  // riccati.hpp:106-113
-    const int c = F.first_leaf + l;
+    const int c = F.stage_first + l;
     const double pi = F.prob[c];
-    const double* P = F.cost_leaf + l * lsz;
+    const double* P = F.cost_leaf + static_cast<int64_t>(F.leaf_slot[F.stage_first - F.first_leaf + l]) * lsz;
     if (!F.affine_only)
       for (int e = threadIdx.x; e < nx * nx; e += kT) F.vq[static_cast<int64_t>(c) * nx * nx + e] = pi * P[e];
     for (int e = threadIdx.x; e < W; e += kT)
@@ -126,7 +132,7 @@ __global__ void __launch_bounds__(kT) factor_stage(FactorParams F) {
     // riccati.hpp:127-141: accumulate over the children
     for (int c = cb; c < cb + cc; ++c) {
       const double pc = F.prob[c];
-      const double* blk = F.cost_node + static_cast<int64_t>(c - 1) * csz;
+      const double* blk = cost_of(F, c, csz);
       const double *Ag = blk, *Bg = Ag + xx, *cg = Bg + xu, *Qg = cg + nx, *Sg = Qg + xx, *Rg = Sg + xu,
                    *qg = Rg + uu, *rg = qg + nx;
       for (int e = threadIdx.x; e < xx; e += kT) {
@@ -237,7 +243,9 @@ __global__ void __launch_bounds__(kT) factor_stage(FactorParams F) {
         E[(col + rr) + static_cast<int64_t>(nu + z) * M] = s;
       }
       // child_to_input_c = -1/2 H^{-1} B_c' ; closed_loop_c = A_c + B_c K  -> J_c (nxp x W)
-      const double* blk = F.cost_node + static_cast<int64_t>(c - 1) * csz;
+      // (a sharded handle's top node writes the J blocks of its own children only)
+      if (F.bw_j[c] < 0) continue;
+      const double* blk = cost_of(F, c, csz);
       const double *Ag = blk, *Bg = Ag + xx;
       __syncthreads();
       for (int e = threadIdx.x; e < xu; e += kT) {
@@ -273,13 +281,15 @@ __global__ void __launch_bounds__(kT) factor_affine(FactorParams F) {
   const int64_t csz = 2 * xx + 2 * xu + uu + 2 * nx + nu;
   extern __shared__ __align__(16) double sm[];  // su (nu) | sx (nx) | pc2 (nx)
   double *su = sm, *sx = su + nu, *pc2 = sx + nx;
-  for (int i = blockIdx.x; i < F.first_leaf; i += gridDim.x) {
+  const int count = F.aff_nodes ? F.n_aff_nodes : F.first_leaf;
+  for (int q = blockIdx.x; q < count; q += gridDim.x) {
+    const int i = F.aff_nodes ? F.aff_nodes[q] : q;
     for (int e = threadIdx.x; e < nu; e += kT) su[e] = 0.0;
     for (int e = threadIdx.x; e < nx; e += kT) sx[e] = 0.0;
     __syncthreads();
     for (int c = F.child_begin[i]; c < F.child_begin[i] + F.child_count[i]; ++c) {
       const double pc = F.prob[c];
-      const double* blk = F.cost_node + static_cast<int64_t>(c - 1) * csz;
+      const double* blk = cost_of(F, c, csz);
       const double *Ag = blk, *Bg = Ag + xx, *cg = Bg + xu, *qg = cg + nx + xx + xu + uu, *rg = qg + nx;
       const double* V = F.vq + static_cast<int64_t>(c) * xx;
       for (int e = threadIdx.x; e < nx; e += kT) {
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(kT) factor_flat(FactorParams F) {
     double* blk = F.fw_blk + F.flat_off[c];
     const double* pblk = k >= 2 ? F.fw_blk + F.flat_off[p] : nullptr;
     const double* J = F.bw_blk + F.bw_j[c];  // CL[a, t] = J[a + (nu + t) nxp]
-    const double* cost = F.cost_node + static_cast<int64_t>(c - 1) * csz;
+    const double* cost = cost_of(F, c, csz);
     const double *Bc = cost + xx, *cc = Bc + xu;
     const double* Kb = F.fw_blk + F.k_off[p];  // K_p[w, z] = Kb[z + w nxp]
     const double* hc = F.hcoef + static_cast<int64_t>(F.dual_offset[c]) * W;

@@ -16,8 +16,12 @@ struct FactorParams {
   const int32_t* stage_rows;      // per node
   const int32_t* ancestor;        // per node (-1 root)
   const double* prob;
-  const double* cost_node;        // per non-root node i at (i-1)*csz (unsharded handles)
-  const double* cost_leaf;        // per leaf l at l*lsz
+  const double* cost_node;        // per non-root node i at cost_slot[i]*csz
+  const double* cost_leaf;        // per leaf l at leaf_slot[l]*lsz
+  const int32_t* cost_slot;       // [n] block of node i in cost_node (-1: not on this handle)
+  const int32_t* leaf_slot;       // [L] block of leaf l in cost_leaf (-1: not on this handle)
+  const int32_t* aff_nodes;       // factor_affine: the non-leaf nodes of this handle (null: all)
+  int n_aff_nodes;
   const double* hcoef;            // per dual row: [F row | G row]
   const int64_t* bw_off;          // per node: E / leaf F_N block start in the bw pass array
   const int64_t* bw_j;            // per non-root node: J block start

@@ -254,7 +254,6 @@ int scenopt_shard_rows(const scenopt_problem* p, int world, int shard_stage, int
 int scenopt_dev_create_sharded(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
                                int world, int shard_stage, const void* nccl_id, scenopt_dev** out) {
   SCN_GUARD({
-    if (!f) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: a factor cache is required");
     if (world < 1 || rank < 0 || rank >= world) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: bad rank/world");
     ShardSpec spec;
     spec.rank = rank;
@@ -262,7 +261,7 @@ int scenopt_dev_create_sharded(const scenopt_problem* p, const scenopt_factor* f
     spec.stage = shard_stage;
     spec.nccl_id = nccl_id;
     auto h = std::make_unique<scenopt_dev>();
-    h->d = dev_create(p->p, &f->f, device, &spec);
+    h->d = f ? dev_create(p->p, &f->f, device, &spec) : dev_create_device_factor(p->p, device, &spec);
     h->init_solver_buffers();
     *out = h.release();
   });
@@ -285,7 +284,6 @@ void scenopt_shard_group_destroy(scenopt_shard_group* g) { delete g; }
 int scenopt_dev_create_sharded_group(const scenopt_problem* p, const scenopt_factor* f, int device, int rank,
                                      scenopt_shard_group* g, int shard_stage, scenopt_dev** out) {
   SCN_GUARD({
-    if (!f) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: a factor cache is required");
     if (!g) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: null shard group");
     ShardSpec spec;
     spec.rank = rank;
@@ -294,7 +292,7 @@ int scenopt_dev_create_sharded_group(const scenopt_problem* p, const scenopt_fac
     spec.emu = g->g;
     if (rank < 0 || rank >= spec.world) fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: bad rank/world");
     auto h = std::make_unique<scenopt_dev>();
-    h->d = dev_create(p->p, &f->f, device, &spec);
+    h->d = f ? dev_create(p->p, &f->f, device, &spec) : dev_create_device_factor(p->p, device, &spec);
     h->init_solver_buffers();
     *out = h.release();
   });

@@ -21,9 +21,9 @@ T* up(DevState& d, const std::vector<T>& h) {
 }
 }  // namespace
 
-std::unique_ptr<DevState> dev_create_device_factor(const Problem& p, int device) {
+std::unique_ptr<DevState> dev_create_device_factor(const Problem& p, int device, const ShardSpec* shard) {
   const Factor shape = factor_shape(p, true);  // layout only: the GPU writes the factor blocks
-  auto d = dev_create(p, &shape, device);
+  auto d = dev_create(p, &shape, device, shard);
   dev_factor_device(*d);
   return d;
 }
@@ -54,6 +54,8 @@ FactorParams& params(DevState& d) {
   F.prob = d.cost.prob;
   F.cost_node = d.cost.node;
   F.cost_leaf = d.cost.leaf;
+  F.cost_slot = d.cost.slot;
+  F.leaf_slot = d.cost.lslot;
   F.hcoef = d.hrows.coef;
   F.bw_off = up(d, d.h_bw_off);
   F.bw_j = up(d, d.h_bw_j);
@@ -68,23 +70,30 @@ FactorParams& params(DevState& d) {
   d.fp_ready = true;
   return F;
 }
+// the nodes of stage t this handle holds: all, or a sharded rank's own range
+// below the shard stage (the replicated top above it)
+std::pair<int, int> held_range(const DevState& d, int t) {
+  if (d.sharded()) return d.own_range[t];
+  return {d.lay.stage_offsets[t], d.lay.stage_offsets[t + 1]};
+}
 // flattened forward top (device.cpp, kFlatTop): stages 1 .. cut-1 in order,
 // each reads its parents' maps
 void run_flat(DevState& d, FactorParams& F, int consts_only) {
   if (!d.flat_top) return;
-  const Layout& L = d.lay;
   F.flat_consts_only = consts_only;
   for (int t = 1; t < d.cut_stage; ++t) {
-    F.stage_first = L.stage_offsets[t];
-    F.stage_count = L.stage_offsets[t + 1] - L.stage_offsets[t];
-    SCN_CUDA(factor_run_flat(F, std::min(d.sm_count * 2, F.stage_count), d.stream));
+    const auto r = held_range(d, t);
+    F.stage_first = r.first;
+    F.stage_count = r.second - r.first;
+    if (F.stage_count > 0) SCN_CUDA(factor_run_flat(F, std::min(d.sm_count * 2, F.stage_count), d.stream));
   }
 }
 }  // namespace
 
 void dev_factor_device(DevState& d) {
   if (!d.has_factor) fail(SCENOPT_E_CACHE_MISMATCH, "device factor: handle has no sweep layout");
-  if (d.sharded()) fail(SCENOPT_E_UNSUPPORTED_SPEC, "device factor: not available on sharded handles");
+  if (d.sharded() && d.world > 1 && !d.comm)
+    fail(SCENOPT_E_INVALID_PARAMS, "device factor: a sharded handle needs its communicator");
   const Layout& L = d.lay;
   const int nx = L.nx, nu = L.nu, n = L.n;
   SCN_CUDA(cudaSetDevice(d.device));
@@ -105,23 +114,56 @@ void dev_factor_device(DevState& d) {
     F.ws_global = d.alloc<double>(static_cast<size_t>(grid_max) * ws);
   }
   SCN_CUDA(cudaMemsetAsync(F.bad, 0, sizeof(int), d.stream));
-  // riccati.hpp:106-113: leaves; then stages N-1 .. 0 (each needs the stage below)
+  auto check_bad = [&](double others) {
+    int bad = 0;
+    SCN_CUDA(cudaMemcpyAsync(&bad, F.bad, sizeof(int), cudaMemcpyDeviceToHost, d.stream));
+    SCN_CUDA(cudaStreamSynchronize(d.stream));
+    if (bad)
+      fail(SCENOPT_E_NOT_STRONGLY_CONVEX, "factor: eliminated input Hessian at node " + std::to_string(bad - 1) +
+                                              " has min eigenvalue below 1e-10");
+    if (others > 0.0)
+      fail(SCENOPT_E_NOT_STRONGLY_CONVEX, "factor: an eliminated input Hessian of another rank's subtrees has "
+                                          "min eigenvalue below 1e-10");
+  };
+  // riccati.hpp:106-113: leaves; then stages N-1 .. 0 (each needs the stage below).
+  // A sharded rank factors its own subtrees up to the shard stage, then every
+  // rank factors the replicated top from the shard-stage nodes' value
+  // matrices, exchanged in one sum-allreduce (owners write their rows).
   F.affine_only = 0;
-  F.stage_first = L.first_leaf;
-  F.stage_count = L.n - L.first_leaf;
-  SCN_CUDA(factor_run_leaves(F, std::min(grid_max, std::max(1, F.stage_count)), d.stream));
+  const int s = d.sharded() ? d.shard_stage : -1;
+  const auto leaves = held_range(d, L.N);
+  F.stage_first = leaves.first;
+  F.stage_count = leaves.second - leaves.first;
+  if (F.stage_count > 0) SCN_CUDA(factor_run_leaves(F, std::min(grid_max, F.stage_count), d.stream));
   for (int t = L.N - 1; t >= 0; --t) {
-    F.stage_first = L.stage_offsets[t];
-    F.stage_count = L.stage_offsets[t + 1] - L.stage_offsets[t];
-    SCN_CUDA(factor_run_stage(F, std::min(grid_max, F.stage_count), smem, d.stream));
+    if (t == s - 1) {  // the shard-stage exchange
+      const int ns = d.sstage_hi - d.sstage_lo;
+      const size_t xx = static_cast<size_t>(nx) * nx;
+      if (!d.vx) d.vx = d.alloc<double>(static_cast<size_t>(ns) * xx + 1);
+      SCN_CUDA(cudaMemsetAsync(d.vx, 0, sizeof(double) * (ns * xx + 1), d.stream));
+      if (d.shard_hi > d.shard_lo)
+        SCN_CUDA(cudaMemcpyAsync(d.vx + (d.shard_lo - d.sstage_lo) * xx, d.vq + static_cast<size_t>(d.shard_lo) * xx,
+                                 sizeof(double) * (d.shard_hi - d.shard_lo) * xx, cudaMemcpyDeviceToDevice, d.stream));
+      int bad = 0;  // this rank's verdict travels with the exchange, so every rank stops together
+      SCN_CUDA(cudaMemcpyAsync(&bad, F.bad, sizeof(int), cudaMemcpyDeviceToHost, d.stream));
+      SCN_CUDA(cudaStreamSynchronize(d.stream));
+      const double flag = bad ? 1.0 : 0.0;
+      SCN_CUDA(cudaMemcpyAsync(d.vx + ns * xx, &flag, sizeof(double), cudaMemcpyHostToDevice, d.stream));
+      dev_allreduce(d, d.vx, ns * xx + 1);
+      SCN_CUDA(cudaMemcpyAsync(d.vq + static_cast<size_t>(d.sstage_lo) * xx, d.vx, sizeof(double) * ns * xx,
+                               cudaMemcpyDeviceToDevice, d.stream));
+      double all = 0.0;
+      SCN_CUDA(cudaMemcpyAsync(&all, d.vx + ns * xx, sizeof(double), cudaMemcpyDeviceToHost, d.stream));
+      SCN_CUDA(cudaStreamSynchronize(d.stream));
+      check_bad(all - flag);
+    }
+    const auto r = held_range(d, t);
+    F.stage_first = r.first;
+    F.stage_count = r.second - r.first;
+    if (F.stage_count > 0) SCN_CUDA(factor_run_stage(F, std::min(grid_max, F.stage_count), smem, d.stream));
   }
   run_flat(d, F, 0);
-  int bad = 0;
-  SCN_CUDA(cudaMemcpyAsync(&bad, F.bad, sizeof(int), cudaMemcpyDeviceToHost, d.stream));
-  SCN_CUDA(cudaStreamSynchronize(d.stream));
-  if (bad)
-    fail(SCENOPT_E_NOT_STRONGLY_CONVEX, "factor: eliminated input Hessian at node " + std::to_string(bad - 1) +
-                                            " has min eigenvalue below 1e-10");
+  check_bad(0.0);
   d.device_factor = true;
 }
 
@@ -131,6 +173,7 @@ void dev_refactor_affine(DevState& d, const Problem& p) {
     fail(SCENOPT_E_SHAPE_CHANGED, "refactor_affine: problem shape changed since factor()");
   if (!d.device_factor)
     fail(SCENOPT_E_INVALID_PARAMS, "refactor_affine on the device needs a device-factored handle");
+  if (d.sharded()) fail(SCENOPT_E_INVALID_PARAMS, "refactor_affine: not available on sharded handles");
   const int nx = L.nx, nu = L.nu, n = L.n;
   const size_t dbl = sizeof(double);
   const size_t xx = static_cast<size_t>(nx) * nx, xu = static_cast<size_t>(nx) * nu, uu = static_cast<size_t>(nu) * nu;
@@ -169,6 +212,7 @@ void dev_refactor_affine(DevState& d, const Problem& p) {
 
 Factor dev_factor_export(DevState& d, const Problem& p) {
   if (!d.device_factor || !d.vq) fail(SCENOPT_E_INVALID_PARAMS, "factor export: handle has no device factor");
+  if (d.sharded()) fail(SCENOPT_E_INVALID_PARAMS, "factor export: not available on sharded handles");
   Factor f = factor_shape(p);
   const int nx = p.nx, nu = p.nu, n = p.n, W = nx + nu, nxp = d.nxp;
   std::vector<double> bw(static_cast<size_t>(d.bw_doubles)), fw(static_cast<size_t>(d.fw_doubles)),

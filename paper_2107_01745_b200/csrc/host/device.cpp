@@ -88,7 +88,8 @@ double* upload(DevState& d, const HostArray& h) {
 }  // namespace
 
 namespace {
-void pack_common(DevState& d, const Problem& p, const std::vector<char>* mine = nullptr);
+void pack_common(DevState& d, const Problem& p, const std::vector<char>* mine = nullptr,
+                 const std::vector<char>* held = nullptr);
 }
 
 // Per-node packed block sizes (doubles) of the backward / forward pass
@@ -577,6 +578,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     d->sstage_hi = p.stage_offsets[s + 1];
     d->dual_top = p.dual_offset[p.stage_offsets[s]];
     const auto own = descend(d->shard_lo, d->shard_hi, s, p.N);
+    d->own_range.assign(static_cast<size_t>(p.N) + 1, {0, 0});
+    for (int t = 0; t <= p.N; ++t)
+      d->own_range[t] = t < s ? std::make_pair(p.stage_offsets[t], p.stage_offsets[t + 1]) : own[t];
     {
       auto add = [](std::vector<std::pair<int64_t, int64_t>>& v, int64_t a, int64_t b) {
         if (b <= a) return;
@@ -1063,7 +1067,12 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   if (d->sharded())  // nodes whose cost this rank evaluates: own subtrees, top on rank 0
     mine = shard_nodes(p, d->shard_stage, d->shard_lo, d->shard_hi, shard->rank);
   clk.mark("upload blocks");
-  pack_common(*d, p, d->sharded() ? &mine : nullptr);
+  std::vector<char> held;  // cost blocks kept: own subtrees, the top and every shard-stage node
+  if (d->sharded()) {
+    held = mine;
+    for (int c = 0; c < d->sstage_hi; ++c) held[c] = 1;
+  }
+  pack_common(*d, p, d->sharded() ? &mine : nullptr, d->sharded() ? &held : nullptr);
   clk.mark("pack_common");
   const int D = p.dual_dim;
   if (d->sharded()) {
@@ -1135,7 +1144,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
 namespace {
 // Per-dual-row nonsmooth data, apply_H rows and eval_f cost blocks: what
 // every handle needs, with or without the sweep layout.
-void pack_common(DevState& dd, const Problem& p, const std::vector<char>* mine) {
+// mine: the nodes whose cost this handle evaluates (eval_f); held: the nodes
+// whose cost blocks it keeps (the device factor's inputs). Null: all nodes.
+void pack_common(DevState& dd, const Problem& p, const std::vector<char>* mine, const std::vector<char>* held) {
   DevState* d = &dd;
   const int n = p.n, nx = p.nx, nu = p.nu, D = p.dual_dim, V = nx + nu;
   std::vector<int8_t> kind(static_cast<size_t>(D), 0);
@@ -1185,19 +1196,32 @@ void pack_common(DevState& dd, const Problem& p, const std::vector<char>* mine) 
   d->hrows.row_node = upload(*d, rnode);
   d->hrows.row_term = upload(*d, rterm);
   d->hrows.coef = upload(*d, coef);
-  // eval_f blocks: [A | B | c | Q | S | R | q | r] per non-root node, [P | p] per leaf
-  // (a sharded handle keeps only the nodes it evaluates: its subtrees, and
-  // the replicated top on rank 0; the partial sums are allreduced)
-  std::vector<int32_t> nodes, leaves;
-  for (int i = 1; i < n; ++i)
+  // cost blocks: [A | B | c | Q | S | R | q | r] per non-root node, [P | p] per
+  // leaf. A sharded handle holds its subtrees, the replicated top and the
+  // shard-stage nodes (the device factor of the top reads them), and
+  // evaluates f over its subtrees (plus the top on rank 0); the partial sums
+  // are reduced over the ranks.
+  std::vector<int32_t> nodes, leaves, hnodes, hleaves;
+  std::vector<int32_t> slot(static_cast<size_t>(n), -1), lslot(static_cast<size_t>(std::max(p.L, 1)), -1);
+  for (int i = 1; i < n; ++i) {
     if (!mine || (*mine)[i]) nodes.push_back(i);
-  for (int l = 0; l < p.L; ++l)
+    if (!held || (*held)[i]) {
+      slot[i] = static_cast<int32_t>(hnodes.size());
+      hnodes.push_back(i);
+    }
+  }
+  for (int l = 0; l < p.L; ++l) {
     if (!mine || (*mine)[p.first_leaf + l]) leaves.push_back(p.first_leaf + l);
+    if (!held || (*held)[p.first_leaf + l]) {
+      lslot[l] = static_cast<int32_t>(hleaves.size());
+      hleaves.push_back(p.first_leaf + l);
+    }
+  }
   const size_t csz = 2 * p.sxx() + 2 * p.sxu() + p.suu() + 2 * static_cast<size_t>(nx) + nu;
-  HostArray cn(std::max<size_t>(nodes.size(), 1) * csz, nodes.empty());  // every block fully written below
-  parallel_for(static_cast<int>(nodes.size()), 256, [&](int b, int e) {
+  HostArray cn(std::max<size_t>(hnodes.size(), 1) * csz, hnodes.empty());  // every block fully written below
+  parallel_for(static_cast<int>(hnodes.size()), 256, [&](int b, int e) {
     for (int t = b; t < e; ++t) {
-      const int i = nodes[t];
+      const int i = hnodes[t];
       double* o = cn.data() + static_cast<size_t>(t) * csz;
       o = std::copy(p.Ai(i), p.Ai(i) + p.sxx(), o);
       o = std::copy(p.Bi(i), p.Bi(i) + p.sxu(), o);
@@ -1210,9 +1234,9 @@ void pack_common(DevState& dd, const Problem& p, const std::vector<char>* mine) 
     }
   });
   const size_t lsz = p.sxx() + static_cast<size_t>(nx);
-  HostArray cl(std::max<size_t>(leaves.size(), 1) * lsz, leaves.empty());
-  for (size_t t = 0; t < leaves.size(); ++t) {
-    const int l = leaves[t] - p.first_leaf;
+  HostArray cl(std::max<size_t>(hleaves.size(), 1) * lsz, hleaves.empty());
+  for (size_t t = 0; t < hleaves.size(); ++t) {
+    const int l = hleaves[t] - p.first_leaf;
     double* o = cl.data() + t * lsz;
     o = std::copy(p.Pl(l), p.Pl(l) + p.sxx(), o);
     std::copy(p.pl(l), p.pl(l) + nx, o);
@@ -1226,9 +1250,11 @@ void pack_common(DevState& dd, const Problem& p, const std::vector<char>* mine) 
   d->cost.nodes = upload(*d, nodes);
   d->cost.nnodes = static_cast<int>(nodes.size());
   d->cost.node = upload(*d, cn);
+  d->cost.slot = upload(*d, slot);
   d->cost.leaves = upload(*d, leaves);
   d->cost.nleaves = static_cast<int>(leaves.size());
   d->cost.leaf = upload(*d, cl);
+  d->cost.lslot = upload(*d, lslot);
   d->cost.check_root = (!mine || (*mine)[0]) ? 1 : 0;
   d->cost.root_state = upload(*d, p.root_state);
   if (!d->root_state) d->root_state = const_cast<double*>(d->cost.root_state);

@@ -75,6 +75,7 @@ struct DevState {
   // node block positions in the pass arrays (doubles; -1: not on this handle)
   std::vector<int64_t> h_bw_off, h_bw_j, h_k_off, h_flat_off;
   double* vq = nullptr;         // value_quad of the device factor [n][nx*nx]
+  double* vx = nullptr;         // sharded device factor: shard-stage value matrices exchanged (+ a flag)
   bool device_factor = false;   // E / J / K / aff_bw computed on the device (K9)
   FactorParams fp{};            // device-factor launch parameters (index arrays on the device)
   bool fp_ready = false;
@@ -83,6 +84,7 @@ struct DevState {
   int rank = 0, world = 1, shard_stage = -1;
   std::unique_ptr<Comm> comm;   // null: exchange left to the caller (phase API)
   int shard_lo = 0, shard_hi = 0;  // this rank's shard-stage nodes
+  std::vector<std::pair<int, int>> own_range;  // per stage: the nodes this rank holds (all above the shard stage)
   int sstage_lo = 0, sstage_hi = 0;  // all shard-stage nodes [stage_offsets[s], stage_offsets[s+1])
   int64_t dual_top = 0;          // dual rows of the replicated top stages (a prefix)
   int64_t dual_s_end = 0;        // end of the shard-stage nodes' dual rows ([dual_top, dual_s_end))
@@ -159,7 +161,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* f, int devi
                                      const ShardSpec* shard = nullptr);
 // Handle whose factor is computed on the device (K9, factor.cu): the host
 // packs only problem data; the factor blocks are written by the GPU.
-std::unique_ptr<DevState> dev_create_device_factor(const Problem& p, int device);
+std::unique_ptr<DevState> dev_create_device_factor(const Problem& p, int device, const ShardSpec* shard = nullptr);
 // (Re)compute the factor of the handle's own problem data on the device.
 void dev_factor_device(DevState& d);
 // The device factor in the FactorCache layout (riccati.hpp:38-63).

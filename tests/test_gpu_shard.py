@@ -224,3 +224,82 @@ def test_emulated_ranks_solve_c3(gpu, world):
         assert rep.status == "converged" and abs(rep.iterations - ref.iterations) <= 1
         assert np.abs(rep.y - ref.y).max() <= 10 * cfg.eps * (1 + np.abs(ref.y).max())
         assert rep.residual_inf <= cfg.eps
+
+
+def test_world1_sharded_device_factor_is_bitwise_the_device_factor(gpu):
+    """K9 on a sharded handle (world 1, NCCL): own subtrees, the exchange of
+    the shard-stage value matrices, the replicated top -- the same factor,
+    sweeps and solves as the unsharded device factor, bit for bit."""
+    prob = so.gen_random_instance(5, 6, 3, 8, [3, 3, 2])
+    full = so.factor_device(prob)
+    shard = so.DeviceFactorCache.sharded(prob, 0, 1, so.nccl_unique_id())
+    assert shard.dev_info()["device_factor"] == 1 and shard.dev_info()["world"] == 1
+    y = np.random.default_rng(2).uniform(-1, 1, prob.dual_dim)
+    a, b = so.dual_grad(full, prob, y), so.dual_grad(shard, prob, y)
+    assert np.array_equal(a.x, b.x) and np.array_equal(a.u, b.u)
+    for kind in ("minfbe", "nama"):
+        cfg = so.SolverConfig(nama_parallel_linesearch=(kind == "nama"))
+        ra = so.api._solve_direct(kind, prob, full, cfg)
+        rb = so.api._solve_direct(kind, prob, shard, cfg)
+        assert ra.iterations == rb.iterations and np.array_equal(ra.y, rb.y)
+
+
+@pytest.mark.parametrize("world,stage,shape", [(2, -1, (5, 6, 3, 8, [4, 3, 2])), (3, 2, (5, 6, 3, 8, [4, 3, 2])),
+                                               (4, 1, (7, 5, 2, 9, [4, 2, 2, 2]))])
+def test_emulated_ranks_factor_on_the_device(gpu, world, stage, shape):
+    """Every rank factors only its own subtrees plus the replicated top on
+    the device (no host factor anywhere): sweeps reassemble the host
+    factor's, and the sharded solves match the unsharded solver."""
+    import threading
+
+    prob = so.gen_random_instance(*shape)
+    full = so.factor(prob)
+    group = so.ShardGroup(world)
+    caches = [None] * world
+    errs = []
+
+    def make(r):
+        try:
+            caches[r] = so.DeviceFactorCache.sharded(prob, r, group=group, stage=stage)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=make, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    y = np.random.default_rng(world).uniform(-1, 1, prob.dual_dim)
+    ref = so.dual_grad(full, prob, y)
+    outs = [None] * world
+
+    def grad(r):
+        outs[r] = so.dual_grad(caches[r], prob, y)
+
+    ts = [threading.Thread(target=grad, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for pt in outs:
+        scale = 1 + np.abs(ref.x).max()
+        assert np.abs(pt.x - ref.x).max() <= 1e-9 * scale and np.abs(pt.u - ref.u).max() <= 1e-9 * scale
+    for kind in ("minfbe", "nama"):
+        cfg = so.SolverConfig(eps=1e-6, nama_parallel_linesearch=(kind == "nama"))
+        want = so.api._solve_direct(kind, prob, full, cfg)
+        reps = [None] * world
+
+        def run(r):
+            reps[r] = so.api._solve_direct(kind, prob, caches[r], cfg)
+
+        ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert all(rp is not None for rp in reps)
+        rep = reps[0]
+        assert rep.status == "converged" and abs(rep.iterations - want.iterations) <= 1
+        assert np.abs(rep.y - want.y).max() <= 10 * cfg.eps * (1 + np.abs(want.y).max())

@@ -288,13 +288,19 @@ def main():
     elif sharded:
         label = f"{label}; strong scaling: the same tree sharded over {world} GPUs"
     t0 = time.time()
-    prob = so.gen_random_instance(1, nx, nu, N, br)
-    cache = so.factor(prob)
     if sharded:
+        # each rank builds only its part of the instance (its subtrees, the
+        # top and the stage-1 nodes; bit-identical to the full instance there)
+        # and factors it on the device: no rank holds the whole tree or a
+        # host factor
+        prob = so.gen_random_instance_shard(1, nx, nu, N, br, rank, world, 1)
         nid = [so.nccl_unique_id() if rank == 0 else None]
         if world > 1:
             dist.broadcast_object_list(nid, src=0)
-        cache.shard(rank, world, nid[0], device=device, stage=1)
+        cache = so.DeviceFactorCache.sharded(prob, rank, world, nid[0], device=device, stage=1)
+    else:
+        prob = so.gen_random_instance(1, nx, nu, N, br)
+        cache = so.factor(prob)
     dev = cache.device(device)
     setup_s = time.time() - t0
     info = cache.dev_info()

@@ -142,6 +142,15 @@ int scenopt_problem_create(const scenopt_problem_view* v, scenopt_problem** out)
  * reproduce the reference's full-branching tree. */
 int scenopt_problem_gen_random(uint64_t seed, int nx, int nu, int horizon, const int32_t* branching,
                                int nbranch, scenopt_problem** out);
+/* One shard's part of the same instance (B200 extension for subtree-sharded
+ * runs): the random stream is drawn in full in the reference's order, but
+ * only the nodes rank `rank` of `world` holds (its subtrees under the plan
+ * of scenopt_shard_plan, the stages above and the shard-stage nodes) are
+ * built; their values equal the full instance's bit for bit. Every dual row
+ * is complete. The result can only build that rank's sharded handle with a
+ * device factor (scenopt_dev_create_sharded[_group] with f == NULL). */
+int scenopt_problem_gen_random_shard(uint64_t seed, int nx, int nu, int horizon, const int32_t* branching,
+                                     int nbranch, int world, int rank, int shard_stage, scenopt_problem** out);
 /* SpringMassParams, generators.hpp:49-64. Arrays of length 0 take the
  * reference defaults (generators.hpp:149-162); transition is row-major. */
 typedef struct scenopt_spring_mass_params {

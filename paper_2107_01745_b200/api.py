@@ -17,7 +17,7 @@ from . import _native as N
 
 __all__ = [
     # problem_data.hpp / generators.hpp / solvers.hpp:569-623
-    "PrimalPoint", "ProblemInstance", "gen_random_instance", "precondition",
+    "PrimalPoint", "ProblemInstance", "gen_random_instance", "gen_random_instance_shard", "precondition",
     "serialize_problem", "parse_problem", "save_problem", "load_problem", "validate_problem_text",
     "problem_to_json", "problem_from_json", "content_hash", "factor_hash", "PROBLEM_SCHEMA",
     "SpringMassParams", "gen_spring_mass", "spring_mass_continuous", "discretize_zoh", "expm",
@@ -159,6 +159,20 @@ def gen_random_instance(seed: int, nx: int = 3, nu: int = 2, horizon: int = 3,
     h = C.c_void_p()
     check(N.lib().scenopt_problem_gen_random(C.c_uint64(seed), nx, nu, horizon, iptr(b), len(b),
                                              C.byref(h)))
+    return ProblemInstance(h)
+
+
+def gen_random_instance_shard(seed: int, nx: int, nu: int, horizon: int, branching, rank: int, world: int,
+                              stage: int = -1) -> ProblemInstance:
+    """One rank's part of gen_random_instance(seed, ...) for a subtree-sharded
+    run (scenopt_problem_gen_random_shard): only the nodes the rank holds are
+    built, bit-identical to the full instance; use it with
+    DeviceFactorCache.sharded(...) on that rank."""
+    br = [branching] * horizon if isinstance(branching, int) else list(branching)
+    b = np.asarray(br, np.int32)
+    h = C.c_void_p()
+    check(N.lib().scenopt_problem_gen_random_shard(C.c_uint64(seed), nx, nu, horizon, iptr(b), len(b), world,
+                                                   rank, stage, C.byref(h)))
     return ProblemInstance(h)
 
 

@@ -43,6 +43,22 @@ int scenopt_problem_gen_random(uint64_t seed, int nx, int nu, int horizon, const
   });
 }
 
+int scenopt_problem_gen_random_shard(uint64_t seed, int nx, int nu, int horizon, const int32_t* branching,
+                                     int nbranch, int world, int rank, int shard_stage, scenopt_problem** out) {
+  SCN_GUARD({
+    if (world < 1 || rank < 0 || rank >= world) fail(SCENOPT_E_INVALID_PARAMS, "gen_random_instance: bad rank/world");
+    std::vector<int> br(branching, branching + (nbranch > 0 ? nbranch : 0));
+    const Problem tree = gen_random_tree(nx, nu, horizon, br);
+    int s = shard_stage;
+    const std::vector<int> b = shard_plan(tree, world, &s);
+    std::vector<char> keep = shard_nodes(tree, s, b[rank], b[rank + 1], rank);
+    for (int c = 0; c < tree.stage_offsets[s + 1]; ++c) keep[c] = 1;  // the top and every shard-stage node
+    auto h = std::make_unique<scenopt_problem>();
+    h->p = gen_random(seed, nx, nu, horizon, br, &keep);
+    *out = h.release();
+  });
+}
+
 namespace {
 SpringMass spring_from(const scenopt_spring_mass_params* c) {
   SpringMass p;

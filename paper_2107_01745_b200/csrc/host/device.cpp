@@ -215,6 +215,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   PhaseClock clk;
   if (fptr) check_factor_shape(*fptr, p, "dev_create");
   require_valid(p);
+  if (!shard) require_full(p, "dev_create");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -1071,6 +1072,11 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   if (d->sharded()) {
     held = mine;
     for (int c = 0; c < d->sstage_hi; ++c) held[c] = 1;
+    if (!p.held.empty())  // a shard's instance must hold what this rank packs
+      for (int c = 0; c < n; ++c)
+        if (held[c] && !p.held[c])
+          fail(SCENOPT_E_INVALID_PARAMS, "dev_create_sharded: the instance does not hold node " + std::to_string(c) +
+                                             " of this rank's shard (generated for another rank or plan?)");
   }
   pack_common(*d, p, d->sharded() ? &mine : nullptr, d->sharded() ? &held : nullptr);
   clk.mark("pack_common");

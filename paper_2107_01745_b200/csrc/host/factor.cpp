@@ -82,6 +82,7 @@ Factor factor_shape(const Problem& p, bool lite) {
 }
 
 Factor factor(const Problem& p) {
+  require_full(p, "factor");
   require_valid(p);
   const int nx = p.nx, nu = p.nu, n = p.n, Fn = p.first_leaf;
   const size_t sxx = p.sxx(), sxu = p.sxu(), suu = p.suu();

@@ -313,7 +313,7 @@ std::vector<double> probability_roots(const Problem& p) {
 // G, box pairs; leaves W_P, p, F_N, box), so it is drawn sequentially into
 // the node arrays first; the spectral rescaling of A and the W W' + 0.1 I
 // blocks consume no draws and run on the worker pool afterwards.
-Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector<int>& br) {
+Problem gen_random_tree(int nx, int nu, int horizon, const std::vector<int>& br) {
   if (nx < 1 || nu < 1) fail(SCENOPT_E_INVALID_PARAMS, "gen_random_instance: dims must be positive");
   if (horizon < 1) fail(SCENOPT_E_INVALID_PARAMS, "gen_random_instance: tree shape must be positive");
   for (int b : br)
@@ -349,6 +349,24 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
   p.stage_rows[0] = 0;
   p.terminal_rows.assign(static_cast<size_t>(L), 1);
   p.finalize();
+  return p;
+}
+
+void require_full(const Problem& p, const char* who) {
+  if (!p.held.empty())
+    fail(SCENOPT_E_INVALID_PARAMS, std::string(who) + ": the instance holds only one shard's nodes");
+}
+
+Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector<int>& br,
+                   const std::vector<char>* keep) {
+  Problem p = gen_random_tree(nx, nu, horizon, br);
+  const int n = p.n;
+  const int L = p.L;
+  if (keep) {
+    if (static_cast<int>(keep->size()) != n) fail(SCENOPT_E_INVALID_PARAMS, "gen_random_instance: keep mask size");
+    if (std::find(keep->begin(), keep->end(), 0) != keep->end()) p.held = *keep;  // else: the full instance
+  }
+  auto kept = [&](int i) { return !keep || (*keep)[i]; };
   p.root_state.assign(static_cast<size_t>(nx), 0.0);
   const size_t sxx = p.sxx(), sxu = p.sxu(), suu = p.suu();
   const int nw = nx + nu;
@@ -377,16 +395,24 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
   std::mt19937_64 gen(seed);
   auto unit = [&gen]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
   auto sym = [&unit]() { return 2.0 * unit() - 1.0; };
-  // raw W roots for every node (consumed by the parallel pass)
-  std::vector<double> wroot(static_cast<size_t>(n - 1) * sww);
+  // raw W roots of the kept nodes (consumed by the parallel pass); the
+  // draws of other nodes go to scratch
+  std::vector<int> wslot(static_cast<size_t>(n), -1), knodes;
+  for (int i = 1; i < n; ++i)
+    if (kept(i)) {
+      wslot[i] = static_cast<int>(knodes.size());
+      knodes.push_back(i);
+    }
+  std::vector<double> wroot(std::max<size_t>(knodes.size(), 1) * sww), scratch(sxx + sxu + sww);
   for (int i = 1; i < n; ++i) {
-    double* A = p.A.data() + i * sxx;
+    const bool k = kept(i);
+    double* A = k ? p.A.data() + i * sxx : scratch.data();
     for (int a = 0; a < nx; ++a)
       for (int b = 0; b < nx; ++b) A[a + b * nx] = sym();  // row-major draw order
-    double* B = p.B.data() + i * sxu;
+    double* B = k ? p.B.data() + i * sxu : scratch.data() + sxx;
     for (int a = 0; a < nx; ++a)
       for (int b = 0; b < nu; ++b) B[a + b * nx] = sym();
-    double* W = wroot.data() + (i - 1) * sww;
+    double* W = k ? wroot.data() + static_cast<size_t>(wslot[i]) * sww : scratch.data() + sxx + sxu;
     for (int a = 0; a < nw; ++a)
       for (int b = 0; b < nw; ++b) W[a + b * nw] = sym();
     for (int a = 0; a < nx; ++a) p.q[static_cast<size_t>(i) * nx + a] = 1.5 * sym();
@@ -405,7 +431,7 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
   }
   std::vector<double> proot(static_cast<size_t>(L) * sxx);
   for (int l = 0; l < L; ++l) {
-    double* W = proot.data() + l * sxx;
+    double* W = kept(p.first_leaf + l) ? proot.data() + l * sxx : scratch.data();
     for (int a = 0; a < nx; ++a)
       for (int b = 0; b < nx; ++b) W[a + b * nx] = sym();
     for (int a = 0; a < nx; ++a) p.p[static_cast<size_t>(l) * nx + a] = 1.5 * sym();
@@ -414,10 +440,10 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
     p.zmin[off] = -(0.05 + 0.3 * unit());
     p.zmax[off] = 0.05 + 0.3 * unit();
   }
-  parallel_for(n - 1, 64, [&](int b, int e) {
+  parallel_for(static_cast<int>(knodes.size()), 64, [&](int b, int e) {
     std::vector<double> blk(sww);
     for (int k = b; k < e; ++k) {
-      const int i = k + 1;
+      const int i = knodes[k];
       double* A = p.A.data() + i * sxx;
       const double radius = spectral_radius(A, nx);
       if (radius > 0.0) {
@@ -444,6 +470,7 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
   });
   parallel_for(L, 64, [&](int b, int e) {
     for (int l = b; l < e; ++l) {
+      if (!kept(p.first_leaf + l)) continue;
       const double* W = proot.data() + l * sxx;
       double* P = p.P.data() + l * sxx;
       for (int cidx = 0; cidx < nx; ++cidx)

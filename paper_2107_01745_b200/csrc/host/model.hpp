@@ -30,6 +30,11 @@ struct Problem {
       tg_gamma, zmin, zmax;
   // derived (finalize)
   std::vector<int32_t> node_stage, child_begin, child_count, dual_offset, tdual_offset;
+  // Nodes whose problem data this instance holds (empty: all). A shard's
+  // instance (gen_random with a keep mask) holds its subtrees, the top and
+  // the shard-stage nodes; the dual-row data (F, G, bounds, F_N) are always
+  // complete. Such an instance can only build that shard's handle.
+  std::vector<char> held;
 
   void finalize();  // layout + child ranges (problem_data.hpp:126-140)
   size_t sxx() const { return static_cast<size_t>(nx) * nx; }
@@ -62,7 +67,15 @@ void markov_tree(const std::vector<double>& transition, int rows, int cols, cons
 void require_valid(const Problem& p);
 Problem precondition(const Problem& p);                 // solvers.hpp:569-602
 std::vector<double> probability_roots(const Problem& p);  // solvers.hpp:608-623
-Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector<int>& br);
+// keep: the nodes whose data are built (null: all); the random stream is
+// drawn in full either way, so kept nodes get the full instance's values.
+Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector<int>& br,
+                   const std::vector<char>* keep = nullptr);
+// the tree of gen_random (shapes and layout only, no data)
+Problem gen_random_tree(int nx, int nu, int horizon, const std::vector<int>& br);
+// an instance holding every node (a shard's instance cannot be factored,
+// saved or packed into an unsharded handle)
+void require_full(const Problem& p, const char* who);
 
 // generators.hpp:39-234: spring-mass-damper array on the Markov mode tree.
 // Empty vectors take the reference defaults; transition is row-major.

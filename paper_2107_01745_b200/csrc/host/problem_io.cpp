@@ -217,7 +217,10 @@ std::string write_problem(const Problem& p, int indent, bool factor_only) {
   return std::move(w.out);
 }
 
-std::string serialize_problem(const Problem& p) { return write_problem(p, 2, false) + "\n"; }
+std::string serialize_problem(const Problem& p) {
+  require_full(p, "serialize_problem");
+  return write_problem(p, 2, false) + "\n";
+}
 
 namespace {
 // ---------------------------------------------------------------- document -> instance

@@ -303,3 +303,50 @@ def test_emulated_ranks_factor_on_the_device(gpu, world, stage, shape):
         rep = reps[0]
         assert rep.status == "converged" and abs(rep.iterations - want.iterations) <= 1
         assert np.abs(rep.y - want.y).max() <= 10 * cfg.eps * (1 + np.abs(want.y).max())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_ranks_with_per_rank_instances(gpu, world):
+    """Each rank builds only its part of the instance
+    (gen_random_instance_shard) and factors it on the device; nobody holds
+    the whole tree. The sharded solves reach the full instance's iterates."""
+    import threading
+
+    shape = (5, 6, 3, 8, [4, 3, 2])
+    full_prob = so.gen_random_instance(*shape)
+    want_cache = so.factor(full_prob)
+    group = so.ShardGroup(world)
+    parts = [so.gen_random_instance_shard(*shape, rank=r, world=world) for r in range(world)]
+    caches, errs = [None] * world, []
+
+    def make(r):
+        try:
+            caches[r] = so.DeviceFactorCache.sharded(parts[r], r, group=group)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=make, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    for kind in ("minfbe", "nama"):
+        cfg = so.SolverConfig(eps=1e-6, nama_parallel_linesearch=(kind == "nama"))
+        want = so.api._solve_direct(kind, full_prob, want_cache, cfg)
+        reps = [None] * world
+
+        def run(r):
+            reps[r] = so.api._solve_direct(kind, parts[r], caches[r], cfg)
+
+        ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        rep = reps[0]
+        assert rep is not None and rep.status == "converged"
+        assert abs(rep.iterations - want.iterations) <= 1
+        assert np.abs(rep.y - want.y).max() <= 10 * cfg.eps * (1 + np.abs(want.y).max())
+        assert np.abs(rep.x.x - want.x.x).max() <= 10 * cfg.eps * (1 + np.abs(want.x.x).max())

@@ -157,9 +157,11 @@ double now_ms() {
 // pageable 10.5 MB vector costs ~2.7 ms of page faults and zero-fill at C3,
 // and pageable D2H copies are staged at a fraction of the pinned rate; both
 // sit inside wall_ms). Destroyed reports return their arrays to the pool
-// (at most 16 arrays and 256 MB; a request takes the smallest array that
-// fits, and only one at most twice its size). Falls back to pageable memory
-// when page-locked memory is unavailable.
+// (at most 16 arrays and 1 GB; a request takes the smallest array that
+// fits, and only one at most twice its size; 1 GB holds the results of two
+// C4-sized solves, whose fresh page-locked allocation would cost more than
+// the faster copy saves). Falls back to pageable memory when page-locked
+// memory is unavailable.
 class ResultArray {
  public:
   ResultArray() = default;
@@ -207,7 +209,7 @@ struct PoolBlock {
 std::mutex g_arrays_mu;
 std::vector<PoolBlock> g_arrays;
 size_t g_arrays_bytes = 0;
-constexpr size_t kArraysKept = 16, kArraysMaxBytes = size_t(256) << 20;
+constexpr size_t kArraysKept = 16, kArraysMaxBytes = size_t(1) << 30;
 void free_block(const PoolBlock& b) {
   if (b.pinned)
     cudaFreeHost(b.p);

@@ -133,6 +133,7 @@ cudaError_t k_dot(const DualCtx& c, const double* a, const double* b, cudaStream
 cudaError_t k_scale(const DualCtx& c, int n, double alpha, const double* x, double beta, const double* y0,
                     double* y, cudaStream_t st);
 int dual_block_threads();
+int dual_max_blocks();  // grid_reduce's bound on the dual kernels' grid
 
 // apply_H over packed rows (problem_data.hpp:144-162): z = H [x; u].
 struct HRows {

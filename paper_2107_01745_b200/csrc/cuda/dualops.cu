@@ -24,6 +24,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxRed = 32;  // scalars per reduction
+constexpr int kMaxBlocks = 160;  // dual-kernel grid (one block per SM; B200: 148)
+constexpr int kPartsPerLane = kMaxBlocks / 32;
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -75,20 +77,37 @@ __device__ void grid_reduce(const DualCtx& c, int& ph, double (&v)[K]) {
     c.part[(static_cast<int64_t>(ph) * 64 + threadIdx.x) * c.nblk + blockIdx.x] = t;
   }
   grid_sync(c.bar);
-  // the K totals are spread over the block's warps (one L2 round trip each
-  // instead of K in a row); each total keeps the same summation order
+  // The K totals are spread over the block's warps; a warp first issues every
+  // load of its values' block partials (one L2 round trip instead of one per
+  // partial and value), then combines them in the fixed order (lane-strided
+  // over the blocks, then the xor tree): the same bits as a sequential loop.
   {
-    for (int k = warp; k < K; k += kWarps) {
+    constexpr int KW = (K + kWarps - 1) / kWarps;  // values per warp
+    double ld[KW][kPartsPerLane];
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      const int k = warp + j * kWarps;
       const double* p = c.part + (static_cast<int64_t>(ph) * 64 + k) * c.nblk;
+#pragma unroll
+      for (int u = 0; u < kPartsPerLane; ++u) {
+        const int b = lane + 32 * u;
+        ld[j][u] = (k < K && b < c.nblk) ? __ldcg(p + b) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KW; ++j) {
+      const int k = warp + j * kWarps;
       const bool mx = k >= MAXFROM;
       double t = mx ? -INFINITY : 0.0;
-      for (int b = lane; b < c.nblk; b += 32) t = mx ? fmax(t, __ldcg(p + b)) : t + __ldcg(p + b);
+#pragma unroll
+      for (int u = 0; u < kPartsPerLane; ++u)
+        if (lane + 32 * u < c.nblk) t = mx ? fmax(t, ld[j][u]) : t + ld[j][u];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const double u = __shfl_xor_sync(0xffffffffu, t, o);
-        t = mx ? fmax(t, u) : t + u;
+        const double v2 = __shfl_xor_sync(0xffffffffu, t, o);
+        t = mx ? fmax(t, v2) : t + v2;
       }
-      if (lane == 0) tot[k] = t;
+      if (lane == 0 && k < K) tot[k] = t;
     }
   }
   __syncthreads();
@@ -497,79 +516,115 @@ __global__ void __launch_bounds__(kThreads) lbfgs_compact_kernel(DualCtx c, int 
 #pragma unroll
     for (int k2 = 0; k2 < kCompactK; ++k2) vs[k2] = v[k2];
   }
-  if (threadIdx.x == 0) {  // every block: gate, pair set, small triangular solves (identical results)
-    const double* v = vs;
-    double gamma0 = g0_in;
-    // age positions: 0..count-1 the stored pairs, count the new pair
-    int pos[kCompactMem + 1];  // active list (after the push) as age positions
-    int cnt = count, pushed = 0, first = 0;
-    if (do_push) {  // lbfgs.hpp:33-44 (strict curvature gate, FIFO eviction)
-      const double scale = scale_ref >= 0.0 ? scale_ref : v[3];
-      if ((v[0] > eps_curv * v[1] * scale) && (v[2] > 0.0)) {
-        pushed = 1;
-        gamma0 = v[0] / v[2];
-        if (cnt == mem) first = 1;  // evict the oldest
-        else ++cnt;
-        if (blockIdx.x == 0) {  // the new pair's row / column (slot f; read by no block in this launch)
-          double* STY = Mb;
-          double* YTY = Mb + kMbLd * kMbLd;
-          for (int k = 0; k < count; ++k) {
-            const int sk = order[k];
-            STY[sk * kMbLd + f] = v[6 + 2 * kCompactMem + k];  // s_k . y_new (older k)
-            YTY[sk * kMbLd + f] = v[6 + 3 * kCompactMem + k];
-            YTY[f * kMbLd + sk] = v[6 + 3 * kCompactMem + k];
-          }
-          STY[f * kMbLd + f] = v[0];
-          YTY[f * kMbLd + f] = v[2];
-          c.S[sl::CURV + f] = v[0];
-        }
-      }
+  __syncthreads();
+  // every block: gate, pair set, small triangular solves (identical results).
+  // The gate is evaluated by every thread; the active pairs' S'Y / Y'Y / S'g /
+  // Y'g entries are gathered into shared memory in parallel, so thread 0's
+  // solves (fully unrolled over kCompactMem, predicated) run on registers and
+  // shared memory only.
+  const double* vv = vs;
+  double gamma0 = g0_in;
+  int cnt = count, pushed = 0, first = 0;
+  if (do_push) {  // lbfgs.hpp:33-44 (strict curvature gate, FIFO eviction)
+    const double scale = scale_ref >= 0.0 ? scale_ref : vv[3];
+    if ((vv[0] > eps_curv * vv[1] * scale) && (vv[2] > 0.0)) {
+      pushed = 1;
+      gamma0 = vv[0] / vv[2];
+      if (cnt == mem) first = 1;  // evict the oldest
+      else ++cnt;
     }
-    for (int k = 0; k < cnt; ++k) pos[k] = first + k;  // the new pair (position count) is the newest
-    auto sty = [&](int pi, int pj) -> double {  // age positions, pi <= pj
-      if (pj == count) return pi == count ? v[0] : v[6 + 2 * kCompactMem + pi];
-      return pSTY[pi][pj];
-    };
-    auto yty = [&](int pi, int pj) -> double {
-      if (pi == count || pj == count) {
-        if (pi == count && pj == count) return v[2];
-        return v[6 + 3 * kCompactMem + (pi == count ? pj : pi)];
-      }
-      return pYTY[pi][pj];
-    };
-    auto ag = [&](int p) { return p == count ? v[4] : v[6 + p]; };
-    auto bg = [&](int p) { return p == count ? v[5] : v[6 + kCompactMem + p]; };
+  }
+  // age positions: 0..count-1 the stored pairs, count the new pair; active k -> first + k
+  auto sty = [&](int pi, int pj) -> double {  // age positions, pi <= pj
+    if (pj == count) return pi == count ? vv[0] : vv[6 + 2 * kCompactMem + pi];
+    return pSTY[pi][pj];
+  };
+  auto yty = [&](int pi, int pj) -> double {
+    if (pi == count || pj == count) {
+      if (pi == count && pj == count) return vv[2];
+      return vv[6 + 3 * kCompactMem + (pi == count ? pj : pi)];
+    }
+    return pYTY[pi][pj];
+  };
+  __shared__ double aR[kCompactMem][kCompactMem], aY[kCompactMem][kCompactMem], aA[kCompactMem], aB[kCompactMem];
+  if (threadIdx.x < kCompactMem * kCompactMem) {
+    const int i = threadIdx.x / kCompactMem, j = threadIdx.x % kCompactMem;
+    if (i < cnt && j < cnt) {
+      if (i <= j) aR[i][j] = sty(first + i, first + j);
+      aY[i][j] = yty(first + i, first + j);
+    }
+  } else if (threadIdx.x < kCompactMem * kCompactMem + kCompactMem) {
+    const int i = threadIdx.x - kCompactMem * kCompactMem, p2 = first + i;
+    if (i < cnt) {
+      aA[i] = p2 == count ? vv[4] : vv[6 + p2];
+      aB[i] = p2 == count ? vv[5] : vv[6 + kCompactMem + p2];
+    }
+  }
+  if (pushed && blockIdx.x == 0 && threadIdx.x == 64) {  // the new pair's row / column (slot f; read by no block)
+    double* STY = Mb;
+    double* YTY = Mb + kMbLd * kMbLd;
+    for (int k = 0; k < count; ++k) {
+      const int sk = order[k];
+      STY[sk * kMbLd + f] = vv[6 + 2 * kCompactMem + k];  // s_k . y_new (older k)
+      YTY[sk * kMbLd + f] = vv[6 + 3 * kCompactMem + k];
+      YTY[f * kMbLd + sk] = vv[6 + 3 * kCompactMem + k];
+    }
+    STY[f * kMbLd + f] = vv[0];
+    YTY[f * kMbLd + f] = vv[2];
+    c.S[sl::CURV + f] = vv[0];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     double t[kCompactMem], u[kCompactMem];
-    for (int i = cnt - 1; i >= 0; --i) {  // t = R^-1 a
-      double s2 = ag(pos[i]);
-      for (int j = i + 1; j < cnt; ++j) s2 -= sty(pos[i], pos[j]) * t[j];
-      t[i] = s2 / sty(pos[i], pos[i]);
+#pragma unroll
+    for (int i = kCompactMem - 1; i >= 0; --i) {  // t = R^-1 a
+      if (i < cnt) {
+        double s2 = aA[i];
+#pragma unroll
+        for (int j = i + 1; j < kCompactMem; ++j)
+          if (j < cnt) s2 -= aR[i][j] * t[j];
+        t[i] = s2 / aR[i][i];
+      }
     }
-    for (int i = 0; i < cnt; ++i) {  // u = R^-T ((D + g0 Y'Y) t - g0 b)
-      double w = sty(pos[i], pos[i]) * t[i];
-      for (int j = 0; j < cnt; ++j) w += gamma0 * yty(pos[i], pos[j]) * t[j];
-      w -= gamma0 * bg(pos[i]);
-      for (int j = 0; j < i; ++j) w -= sty(pos[j], pos[i]) * u[j];
-      u[i] = w / sty(pos[i], pos[i]);
+#pragma unroll
+    for (int i = 0; i < kCompactMem; ++i) {  // u = R^-T ((D + g0 Y'Y) t - g0 b)
+      if (i < cnt) {
+        double w = aR[i][i] * t[i];
+#pragma unroll
+        for (int j = 0; j < kCompactMem; ++j)
+          if (j < cnt) w += gamma0 * aY[i][j] * t[j];
+        w -= gamma0 * aB[i];
+#pragma unroll
+        for (int j = 0; j < kCompactMem; ++j)
+          if (j < i) w -= aR[j][i] * u[j];
+        u[i] = w / aR[i][i];
+      }
     }
-    for (int i = 0; i < cnt; ++i) {
-      coef_u[i] = u[i];
-      coef_t[i] = t[i];
-    }
+#pragma unroll
+    for (int i = 0; i < kCompactMem; ++i)
+      if (i < cnt) {
+        coef_u[i] = u[i];
+        coef_t[i] = t[i];
+      }
     // slot order after the push (oldest first), spare slot last
     int ord[kCompactMem + 1];
-    for (int k = 0; k < cnt; ++k) ord[k] = pos[k] == count ? f : order[pos[k]];
-    if (pushed && first) ord[mem] = order[0];
-    else if (!pushed) ord[cnt] = f;
-    else ord[cnt] = order[cnt];
-    for (int k = 0; k < cnt; ++k) order[k] = ord[k];
-    order[cnt] = ord[cnt];
+#pragma unroll
+    for (int k = 0; k < kCompactMem; ++k)
+      if (k < cnt) ord[k] = first + k == count ? f : order[first + k];
+    int spare;
+    if (pushed && first) spare = order[0];
+    else if (!pushed) spare = f;
+    else spare = order[cnt];
+#pragma unroll
+    for (int k = 0; k < kCompactMem; ++k)
+      if (k < cnt) order[k] = ord[k];
+    order[cnt] = spare;
     cnt_new = cnt;
     pushed_s = pushed;
     gamma_s = gamma0;
   }
   __syncthreads();
-  const int cnt = cnt_new;
+  cnt = cnt_new;
   const double g0 = gamma_s;
   const double* S_[kCompactMem];
   const double* Y_[kCompactMem];
@@ -1256,6 +1311,7 @@ cudaError_t phased(const void* fn, DualCtx& cc, void** args, cudaStream_t st, in
 }  // namespace
 
 int dual_block_threads() { return kThreads; }
+int dual_max_blocks() { return kMaxBlocks; }
 
 cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, const double* Hx,
                         const double* Hx0, const double* weight, double* z, double* R, double* T,

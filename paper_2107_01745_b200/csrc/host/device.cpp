@@ -1008,14 +1008,19 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
         }
       }
     if (best_ns) break;
-    // small items in smem, large ones from HBM
+    // small items in smem, large ones from HBM. What the staging areas and
+    // scratch leave is computed signed: when the (producer) staging ring alone
+    // exceeds shared memory this pass cannot work (pass 1 stages per team);
+    // a slot must hold at least the node headers of the largest item.
     const int ns = force_ns ? force_ns : 4;
-    int64_t sl = slot_cap_env ? slot_cap_env
-                              : static_cast<int64_t>((optin / dbl - static_cast<size_t>(cons ? teams : stageq) * d->stage_doubles -
-                                                      static_cast<size_t>(teams) * sweep_scratch_bufs() * d->vec_doubles) / ns);
-    sl = std::max<int64_t>(sl, hdr_doubles_max) & ~int64_t(15);
-    sl = std::max<int64_t>(sl, (hdr_doubles_max + 15) & ~int64_t(15));
-    if (sl > 0 && fits(ns, sl, cons)) best_ns = ns, slot = sl, consumer = cons;
+    const int64_t left = static_cast<int64_t>(optin / dbl) -
+                         static_cast<int64_t>(cons ? teams : stageq) * d->stage_doubles -
+                         static_cast<int64_t>(teams) * sweep_scratch_bufs() * d->vec_doubles;
+    const int64_t hdr_slot = (hdr_doubles_max + 15) & ~int64_t(15);
+    int64_t sl = slot_cap_env ? slot_cap_env : (left / ns) & ~int64_t(15);
+    sl = std::max<int64_t>(sl, hdr_slot);
+    if (sl <= (int64_t(1) << 26) && static_cast<int64_t>(ns) * sl <= left && fits(ns, sl, cons))
+      best_ns = ns, slot = sl, consumer = cons;
   }
   if (best_ns == 0)
     fail(SCENOPT_E_INVALID_PARAMS, "dev_create: the per-item staging vectors do not fit in shared memory (" +

@@ -303,3 +303,29 @@ def test_mapped_host_outputs_are_bitwise_the_copied_ones(gpu):
     po = orc.Problem.from_flat(f)
     ox, ou = orc.Factor(po).dual_grad(ys[0])
     assert sup.rel_gap(ox, ou, res[0], res[1]) < 1e-9
+
+
+@pytest.mark.parametrize("shape,item_kb", [((10, 5, 9, [2] * 7), 48), ((10, 5, 9, [2] * 7), 96),
+                                           ((12, 4, 6, [2] * 6), 96)])
+def test_oversized_staging_ring_falls_back_to_team_staging(gpu, monkeypatch, shape, item_kb):
+    """Items of many small nodes whose staged vectors make the 12-deep
+    producer staging ring larger than shared memory (found by
+    tools/layout_fuzz.py: the fallback slot size used to wrap around in
+    unsigned arithmetic, giving a negative slot and an illegal access). The
+    layout must fall back to per-team staging and match the oracle."""
+    monkeypatch.setenv("SCENOPT_ITEM_KB", str(item_kb))
+    monkeypatch.setenv("SCENOPT_ITEM_MAX_NODES", "64")
+    nx, nu, N, br = shape
+    prob = so.gen_random_instance(3, nx, nu, N, br)
+    po = orc.Problem.from_flat(prob.flat())
+    cache = so.factor(prob)
+    info = cache.dev_info()
+    assert info["slot_bytes"] > 0
+    ofac = orc.Factor(po)
+    rng = np.random.default_rng(5)
+    y, r = rng.uniform(-1, 1, prob.dual_dim), rng.uniform(-1, 1, prob.dual_dim)
+    for affine in (True, False):
+        pts, _ = so.sweep(cache, [y, r], affine)
+        for v, pt in ((y, pts[0]), (r, pts[1])):
+            ox, ou = ofac.sweep(v, affine)
+            assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL

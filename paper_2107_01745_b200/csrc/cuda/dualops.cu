@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "dual.hpp"
+#include "fbrow.cuh"
 
 namespace scn {
 
@@ -167,19 +168,8 @@ __device__ bool xreduce(const DualCtx& c, int& ph, double (&v)[K]) {
   return true;
 }
 
-// prox of gamma_prox * g on one row (prox.hpp:58-81).
-__device__ __forceinline__ double prox_row(int kind, double v, double lo, double hi, double thr) {
-  if (kind == 1) return fmin(fmax(v, lo), hi);
-  if (kind == 2) return v > thr ? v - thr : (v < -thr ? v + thr : 0.0);
-  return v;
-}
-// g* on one row (prox.hpp:90-113); +inf where the conjugate is infinite.
-__device__ __forceinline__ double conj_row(int kind, double w, double lo, double hi, double wg) {
-  constexpr double slack = 1e-9;
-  if (kind == 1) return fmax(w * lo, w * hi);
-  if (kind == 2) return fabs(w) > wg * (1.0 + slack) + slack ? INFINITY : 0.0;
-  return fabs(w) > slack ? INFINITY : 0.0;
-}
+using fbrow::conj_row;
+using fbrow::prox_row;
 
 __device__ __forceinline__ int gtid() { return blockIdx.x * kThreads + threadIdx.x; }
 __device__ __forceinline__ int gstride() { return gridDim.x * kThreads; }
@@ -190,66 +180,18 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
                                                              const double* weight, double* z, double* R,
                                                              double* T) {
   int ph = 0;
-  double* S = c.S + st * sl::kStateStride;
-  const double lam = S[sl::LAM];
+  const double lam = c.S[st * sl::kStateStride + sl::LAM];
   const double gp = 1.0 / lam;
   double s[6] = {0, 0, 0, 0, 0, 0};  // conj, z2, Hx.R, R2, (Hx0+Hx).y; [5] weighted inf residual (max)
   if (c.phase <= 0)
-    for (int i = gtid(); i < c.D; i += gstride()) {
-      const int kd = c.g.kind[i];
-      const double yi = y[i], hi = Hx[i];
-      const double zi = prox_row(kd, yi / lam + hi, c.g.lo[i], c.g.hi[i], gp * c.g.wg[i]);
-      const double Ri = zi - hi;
-      const double Ti = yi - lam * Ri;
-      z[i] = zi;
-      R[i] = Ri;
-      T[i] = Ti;
-      if (counted(c, i)) {
-        s[0] += conj_row(kd, Ti, c.g.lo[i], c.g.hi[i], c.g.wg[i]);
-        s[1] += zi * zi;
-        s[2] += hi * Ri;
-        s[3] += Ri * Ri;
-        if (mode == 0) s[4] += (Hx0[i] + hi) * yi;
-        s[5] = fmax(s[5], fabs(weight ? Ri * weight[i] : Ri));
-      }
-    }
+    for (int i = gtid(); i < c.D; i += gstride())
+      fbrow::fb_row(i, c.g.kind[i], y[i], Hx[i], c.g.lo[i], c.g.hi[i], c.g.wg[i], lam, gp, mode, Hx0, weight, z, R,
+                    T, counted(c, i), s);
   if (c.phase == 1 && blockIdx.x != 0) return;  // block 0 finishes
   if (!xreduce<6, false, 5>(c, ph, s)) return;  // one barrier: five sums and the max
-  const double m[1] = {s[5]};
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const double fhat = mode == 0 ? c.S[sl::FHAT0] - 0.5 * s[4] : S[sl::FHAT];
-    S[sl::FHAT] = fhat;
-    S[sl::CONJ] = s[0];
-    S[sl::ZN2] = s[1];
-    S[sl::VALUE] = fhat + s[0] + lam * s[2] + 0.5 * lam * s[3];
-    S[sl::RESID] = m[0];
-    // skip word of a speculative sweep after this step (the host reads it
-    // with the step's scalars and re-sweeps if it skipped an accepted step)
-    const int rule = static_cast<int>(c.S[sl::GATE_RULE]);
-    int reject = 0;
-    if (rule == 0) {  // original rule: candidate fhat above the model (the host takes this verdict)
-      const double model = __dadd_rn(__dadd_rn(c.S[sl::CERT_FHAT], __dmul_rn(lam, c.S[sl::HXW_RW])),
-                                     __dmul_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(1.0, -c.S[sl::BETA_BT])), lam),
-                                               c.S[sl::RW2]));
-      reject = fhat > model;
-    } else if (rule == 1) {  // MINFBE simple rule: lambda |img| > eps_bt |R| halves lambda
-      reject = __dmul_rn(lam, sqrt(c.S[sl::IMG2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::R2]));
-    } else if (rule == 3) {  // NAMA simple rule on the certificate's norms
-      reject = __dmul_rn(lam, sqrt(c.S[sl::HR2])) > __dmul_rn(c.S[sl::EPS_BT], sqrt(c.S[sl::RR2]));
-    }
-    c.I[il::REJECT] = reject;
-    c.I[il::CONV] = (m[0] <= c.S[sl::EPS_STOP] || reject) ? 1 : 0;
-  }
-  if (c.pubS && blockIdx.x == 0) {  // thread 0's S / I writes are visible to the block after the barrier
-    __syncthreads();
-    for (int t = threadIdx.x; t < sl::kScalars; t += blockDim.x) c.pubS[t] = c.S[t];
-    for (int t = threadIdx.x; t < il::kInts; t += blockDim.x) c.pubI[t] = c.I[t];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      *reinterpret_cast<volatile unsigned*>(c.pubSeq) = c.seq;
-    }
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) fbrow::fb_finalize(c.S, c.I, st, mode, s);
+  // thread 0's S / I writes are visible to the block after publish_block's barrier
+  if (c.pubS && blockIdx.x == 0) fbrow::publish_block(c.S, c.I, c.pubS, c.pubI, c.pubSeq, c.seq);
 }
 
 // ---------------------------------------------------------------- K7

@@ -104,6 +104,32 @@ struct SweepParams {
   double* uoff[kMaxRhs];  // [first_leaf][nu] backward input offsets (the forward pass reads, never overwrites)
   double* Hx[kMaxRhs];
   double* contrib[kMaxRhs];  // [n][nu+nx] scratch
+  // Fused finish of an FB step (fbe.hpp:38-50) on a 1-RHS affine sweep of an
+  // unsharded handle (fb_S == nullptr: off). At the end of the sweep every
+  // CTA finishes the dual rows its own forward items wrote (z, R, T and the
+  // step's partial sums), and the last CTA to finish combines the CTAs'
+  // partials in CTA order, writes the step's scalars and publishes them.
+  double* fb_S;              // scalar block (dual.hpp sl::); the state's scalars at fb_S + fb_state * kStateStride
+  int* fb_I;
+  int fb_state;
+  const double* fb_Hx0;
+  const double* fb_weight;   // residual weights or null
+  double* fb_z;
+  double* fb_R;
+  double* fb_T;
+  const int8_t* fb_kind;     // per dual row: nonsmooth kind, box bounds, l1 radius
+  const double* fb_lo;
+  const double* fb_hi;
+  const double* fb_wg;
+  const int32_t* row_first;  // per node: first stage row and count; per leaf: first terminal row and count
+  const int32_t* row_count;
+  const int32_t* trow_first;
+  const int32_t* trow_count;
+  double* fb_part;           // [grid][8] per-CTA partial sums
+  double* pub_S;             // non-null: the last CTA also publishes S / I (mapped host memory, seq last)
+  int* pub_I;
+  unsigned* pub_seq;
+  unsigned seq;
 };
 
 }  // namespace scn

@@ -43,6 +43,7 @@
 #include <cstdint>
 #include <mutex>
 
+#include "fbrow.cuh"
 #include "layout.hpp"
 
 namespace scn {
@@ -636,6 +637,79 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   if (ttid == 0) PROF_T1(13);
 }
 
+// ---------------------------------------------------------------- fused FB-step finish
+// The dual rows of this CTA's forward items (each row's Hx was written by one
+// of this CTA's teams; visible after the block barrier), one item per thread
+// in list order, then a fixed-order block reduction into this CTA's partial.
+__device__ void fb_epilogue_cta(const SweepParams& P, const Item* items, int K) {
+  __shared__ double red[kThreads / 32][8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double lam = P.fb_S[P.fb_state * sl::kStateStride + sl::LAM];
+  const double gp = 1.0 / lam;
+  const double* y = P.y[0];
+  const double* Hx = P.Hx[0];
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  auto rows = [&](int lo, int hi) {
+    for (int i = lo; i < hi; ++i)
+      fbrow::fb_row(i, P.fb_kind[i], y[i], Hx[i], P.fb_lo[i], P.fb_hi[i], P.fb_wg[i], lam, gp, 0, P.fb_Hx0,
+                    P.fb_weight, P.fb_z, P.fb_R, P.fb_T, true, s);
+  };
+  for (int k = tid; k < K; k += kThreads) {
+    const Item it = items[k];
+    if (it.pass != 1) continue;
+    const int first = it.first, last = it.first + it.count - 1;
+    if (first > 0) rows(P.row_first[first], P.row_first[last] + P.row_count[last]);  // stage rows
+    if (it.leaf) {  // terminal rows
+      const int a = first - P.first_leaf, z = last - P.first_leaf;
+      rows(P.trow_first[a], P.trow_first[z] + P.trow_count[z]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    double t = s[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, t, o);
+      t = q == 5 ? fmax(t, u) : t + u;
+    }
+    if (lane == 0) red[warp][q] = t;
+  }
+  __syncthreads();
+  if (tid < 6) {
+    double t = red[0][tid];
+    for (int w = 1; w < kThreads / 32; ++w) t = tid == 5 ? fmax(t, red[w][tid]) : t + red[w][tid];
+    P.fb_part[static_cast<int64_t>(blockIdx.x) * 8 + tid] = t;
+    __threadfence();  // before thread 0's arrival on the grid counter
+  }
+}
+
+// The last CTA: the grid's partials combined in CTA order (the order of
+// grid_reduce's second stage), the step's scalars, the publish.
+__device__ void fb_epilogue_last(const SweepParams& P) {
+  __shared__ double tot[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp < 6) {
+    const int q = warp;
+    double t = q == 5 ? -INFINITY : 0.0;
+    for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) {
+      const double v = __ldcg(P.fb_part + static_cast<int64_t>(b) * 8 + q);
+      t = q == 5 ? fmax(t, v) : t + v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, t, o);
+      t = q == 5 ? fmax(t, u) : t + u;
+    }
+    if (lane == 0) tot[q] = t;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const double s[6] = {tot[0], tot[1], tot[2], tot[3], tot[4], tot[5]};
+    fbrow::fb_finalize(P.fb_S, P.fb_I, P.fb_state, 0, s);
+  }
+  if (P.pub_S) fbrow::publish_block(P.fb_S, P.fb_I, P.pub_S, P.pub_I, P.pub_seq, P.seq);
+}
+
 // MODE bits (one instantiation per combination, so the common layout's
 // kernel carries no fallback code): kModeConsumerStage = teams stage their own
 // vectors; kModeGlobalBlocks = some items read their node blocks from HBM.
@@ -893,10 +967,22 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
     }
   }
   __syncthreads();
+  const bool fb = P.fb_S != nullptr;
+  if (fb) fb_epilogue_cta(P, items, K);  // this CTA's partial, written by threads < 6 (after a barrier)
+  __shared__ int s_last;
+  if (fb) __syncthreads();
   if (tid == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(P.ctrl + 1, 1u);
-    if (prev == gridDim.x - 1) {
+    s_last = prev == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    if (fb) {
+      __threadfence();
+      fb_epilogue_last(P);
+    }
+    if (tid == 0) {
       P.ctrl[1] = 0u;
       __threadfence();
       atomicExch(P.ctrl, E);

@@ -1123,6 +1123,24 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     // else: exchange left to the caller (phase API)
   }
 
+  // fused FB-step finish (SweepParams::fb_*): row ranges of nodes and leaves, per-CTA partials
+  {
+    std::vector<int32_t> rf(static_cast<size_t>(n), 0), rc(static_cast<size_t>(n), 0),
+        tf(static_cast<size_t>(std::max(p.L, 1)), 0), tc(static_cast<size_t>(std::max(p.L, 1)), 0);
+    for (int c = 1; c < n; ++c) {
+      rf[c] = p.dual_offset[c];
+      rc[c] = p.stage_rows[c];
+    }
+    for (int l = 0; l < p.L; ++l) {
+      tf[l] = p.tdual_offset[l];
+      tc[l] = p.terminal_rows[l];
+    }
+    d->row_first = upload(*d, rf);
+    d->row_count = upload(*d, rc);
+    d->trow_first = upload(*d, tf);
+    d->trow_count = upload(*d, tc);
+    d->fb_part = d->alloc<double>(static_cast<size_t>(G) * 8);
+  }
   for (int r = 0; r < kMaxRhs; ++r) {
     d->contrib[r] = d->alloc<double>(static_cast<size_t>(n) * W);
     d->uoff[r] = d->alloc<double>(static_cast<size_t>(std::max(p.first_leaf, 1)) * nu);
@@ -1314,6 +1332,32 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
   P.skip = d.sweep_skip;
   P.bw_flag = d.bw_flag;
   P.fw_flag = d.fw_flag;
+  if (d.fb_next) {
+    if (nrhs != 1 || !affine || d.sharded() || !d.fb_part)
+      fail(SCENOPT_E_INVALID_PARAMS, "sweep: the fused FB finish needs a 1-RHS affine sweep of an unsharded handle");
+    const DevState::FbFuse& f = *d.fb_next;
+    P.fb_S = f.S;
+    P.fb_I = f.I;
+    P.fb_state = f.state;
+    P.fb_Hx0 = f.Hx0;
+    P.fb_weight = f.weight;
+    P.fb_z = f.z;
+    P.fb_R = f.R;
+    P.fb_T = f.T;
+    P.fb_kind = d.row_kind;
+    P.fb_lo = d.row_lo;
+    P.fb_hi = d.row_hi;
+    P.fb_wg = d.row_wg;
+    P.row_first = d.row_first;
+    P.row_count = d.row_count;
+    P.trow_first = d.trow_first;
+    P.trow_count = d.trow_count;
+    P.fb_part = d.fb_part;
+    P.pub_S = f.pubS;
+    P.pub_I = f.pubI;
+    P.pub_seq = f.pubSeq;
+    P.seq = f.seq;
+  }
   for (int r = 0; r < nrhs; ++r) {
     P.y[r] = y[r];
     P.x[r] = (x && x[r]) ? x[r] : d.xs[r];

@@ -69,6 +69,22 @@ struct DevState {
   bool consumer_stage = false;  // teams stage their own vectors (very wide states)
   bool flat_top = false;
   const int* sweep_skip = nullptr;  // SweepParams::skip of the next launches (power iteration batches)
+  // Fused FB-step finish of the next launch (SweepParams::fb_*; set by the
+  // solver engine around one affine 1-RHS sweep of an unsharded handle)
+  struct FbFuse {
+    double* S = nullptr;
+    int* I = nullptr;
+    int state = 0;
+    const double *Hx0 = nullptr, *weight = nullptr;
+    double *z = nullptr, *R = nullptr, *T = nullptr;
+    double* pubS = nullptr;
+    int* pubI = nullptr;
+    unsigned* pubSeq = nullptr;
+    unsigned seq = 0;
+  };
+  const FbFuse* fb_next = nullptr;
+  int32_t *row_first = nullptr, *row_count = nullptr, *trow_first = nullptr, *trow_count = nullptr;
+  double* fb_part = nullptr;  // [grid][8]
   double* out_hx[kMaxRhs] = {};      // SweepParams::hx / hu of the next launches (mapped host outputs)
   double* out_hu[kMaxRhs] = {};        // flattened forward top (one level after the backward root)
   double* aff_fwh = nullptr;    // [n][max_m] constant of the flattened top's stage rows

@@ -543,20 +543,46 @@ struct Engine {
     ensure_fhat0();
     if (ydev != k.y[s]) copy(k.y[s], ydev, D());
     set_scalar(s * sl::kStateStride + sl::LAM, lambda);
-    sweep1(true, k.y[s], k.x[s], k.u[s], k.Hx[s]);
-    ++stats.dual_grad_calls;
-    DualCtx c = ctx();
-    if (publish_after) {
-      if (timer.on) {
-        cudaEventCreate(&pub_pre);
-        cudaEventRecord(pub_pre, st);
-      }
-      c.pubS = k.dpS;
-      c.pubI = k.dpI;
-      c.pubSeq = k.dpSeq;
-      c.seq = ++k.seq;
+    if (publish_after && timer.on) {
+      cudaEventCreate(&pub_pre);
+      cudaEventRecord(pub_pre, st);
     }
-    SCN_CUDA(k_fb_finish(c, s, 0, k.y[s], k.Hx[s], k.Hx0, weight, k.z[s], k.R[s], k.T[s], st));
+    if (!d.sharded() && d.fb_part) {
+      // finish_fb_fields fused into the sweep: its last CTA writes the step's
+      // scalars (and publishes them) once every CTA has finished its rows
+      DevState::FbFuse f;
+      f.S = k.S;
+      f.I = k.I;
+      f.state = s;
+      f.Hx0 = k.Hx0;
+      f.weight = weight;
+      f.z = k.z[s];
+      f.R = k.R[s];
+      f.T = k.T[s];
+      if (publish_after) {
+        f.pubS = k.dpS;
+        f.pubI = k.dpI;
+        f.pubSeq = k.dpSeq;
+        f.seq = ++k.seq;
+      }
+      struct Reset {
+        DevState& d;
+        ~Reset() { d.fb_next = nullptr; }
+      } reset{d};
+      d.fb_next = &f;
+      sweep1(true, k.y[s], k.x[s], k.u[s], k.Hx[s]);
+    } else {
+      sweep1(true, k.y[s], k.x[s], k.u[s], k.Hx[s]);
+      DualCtx c = ctx();
+      if (publish_after) {
+        c.pubS = k.dpS;
+        c.pubI = k.dpI;
+        c.pubSeq = k.dpSeq;
+        c.seq = ++k.seq;
+      }
+      SCN_CUDA(k_fb_finish(c, s, 0, k.y[s], k.Hx[s], k.Hx0, weight, k.z[s], k.R[s], k.T[s], st));
+    }
+    ++stats.dual_grad_calls;
     ++stats.prox_calls;
     ++stats.conj_calls;
   }

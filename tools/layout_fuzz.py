@@ -37,6 +37,11 @@ shapes = [(10, 5, 9, [2] * 7), (10, 5, 8, [4, 4, 4]), (6, 3, 7, [3, 3, 2, 2]), (
 knobs = [dict(SCENOPT_ITEM_KB=kb, SCENOPT_ITEM_MAX_NODES=mn, **({"SCENOPT_SLOT_KB": sk} if sk else {}),
               **({"SCENOPT_STAGE": "consumer"} if cons else {}))
          for kb, mn, sk, cons in itertools.product([24, 48, 96], [32, 64, 128], [0, 4, 16], [False, True])]
+if os.environ.get("FUZZ_SET") == "extremes":  # default knobs, extreme shapes
+    shapes = [(1, 1, 8, [2] * 8), (2, 1, 6, [8, 8]), (1, 2, 5, [16, 4]), (3, 1, 12, [2] * 4), (4, 4, 3, [32, 2]),
+              (2, 2, 10, [3] * 6), (5, 1, 4, [64]), (8, 8, 2, [50]), (1, 1, 20, [2, 2]), (16, 2, 4, [6, 6, 2]),
+              (30, 30, 3, [4, 2]), (64, 8, 3, [3, 3])]
+    knobs = [{}, {"SCENOPT_GRID": 7, "SCENOPT_MIN_SUBTREES": 1}, {"SCENOPT_GRID": 148, "SCENOPT_MIN_SUBTREES": 1}]
 if len(sys.argv) > 1:  # focused rerun: python tools/layout_fuzz.py SHAPE_JSON KNOBS_JSON
     shapes, knobs = [tuple(json.loads(sys.argv[1]))], [json.loads(sys.argv[2])]
 for shape in shapes:

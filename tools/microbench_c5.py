@@ -3,7 +3,7 @@
 CUDA events on the handle's stream, algorithmic bytes (§8d formula) / time
 vs the measured HBM peak. Trees whose packed matrices fit in L2 are flagged.
 
-  python tools/microbench_c5.py [--max-nodes N] [--out profiles/c5_microbench_r01.json]
+  python tools/microbench_c5.py [--max-nodes N] [--device-factor] [--out profiles/c5_microbench_r02.json]
 """
 import argparse, ctypes as C, json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--max-nodes", type=int, default=4_000_000)
     ap.add_argument("--out", default=None)
     ap.add_argument("--only", default=None, help="comma-separated indices into SHAPES")
+    ap.add_argument("--device-factor", action="store_true",
+                    help="factor on the device (no host factor: the 11.9M-node point needs ~110 GB of host RAM "
+                         "with it)")
     a = ap.parse_args()
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json"))).get("hbm_gbs", 6455.3) \
@@ -41,7 +44,7 @@ def main():
             continue
         t0 = time.time()
         p = so.gen_random_instance(1, nx, nu, H, br)
-        c = so.factor(p)
+        c = so.factor_device(p) if a.device_factor else so.factor(p)
         dev = c.device()
         info = c.dev_info()
         setup = time.time() - t0
@@ -70,7 +73,8 @@ def main():
         row = dict(nx=nx, nu=nu, horizon=H, branching=br, nodes=p.num_nodes(), sweeps=k, us_per_sweep=ms * 1e3,
                    algorithmic_bytes=bytes_, gbs=gbs, frac_of_peak=gbs / peak, l2_resident=packed < l2,
                    nodes_per_item_max=info["nodes_per_item_max"], slots=info["slots"],
-                   items_global=info["items_global"], setup_s=round(setup, 1))
+                   items_global=info["items_global"], setup_s=round(setup, 1),
+                   factor="device" if a.device_factor else "host")
         rows.append(row)
         print(json.dumps(row), flush=True)
         del c, p

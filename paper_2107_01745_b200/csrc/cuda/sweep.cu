@@ -50,7 +50,10 @@ namespace scn {
 
 namespace {
 
-constexpr int kTeam = 128;  // threads per consumer team
+#ifndef SCN_TEAM_THREADS
+#define SCN_TEAM_THREADS 128
+#endif
+constexpr int kTeam = SCN_TEAM_THREADS;  // threads per consumer team
 #ifndef SCN_TEAMS
 #define SCN_TEAMS 3
 #endif
@@ -58,7 +61,7 @@ constexpr int kTeams = SCN_TEAMS;  // consumer teams (items k = team mod kTeams)
 constexpr int kProducers = 4;  // producer warps (== slots), warp p stages items k = p (mod 4)
 constexpr int kThreads = 32 * kProducers + kTeams * kTeam + 64;  // producers, teams, publisher, issuer
 constexpr int kTeamWarp0 = kProducers;
-constexpr int kStageQ = kTeams == 3 ? 12 : 8;  // staging ring depth (items staged ahead); a multiple of kProducers
+constexpr int kStageQ = (kTeams == 3 || kTeams == 6) ? 12 : 8;  // staging ring depth (items staged ahead); a multiple of kProducers
                             // and even, so each staging area always serves the same producer
                             // warp and the same team in order
 static_assert(kStageQ % kProducers == 0 && kStageQ % kTeams == 0, "staging ring vs producers / teams");
@@ -333,13 +336,25 @@ __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, in
 // by S consecutive threads (q = 0..S-1) taking interleaved 16-byte chunks,
 // two accumulators each, then an xor-shuffle reduction. All threads of a
 // warp call it (inactive ones with lenp = 0).
+#ifndef SCN_DOT_UNROLL
+#define SCN_DOT_UNROLL 4
+#endif
+// Dot tasks are split over at most SCN_TASK_S_MAX threads: the 8-way split's
+// extra instantiations cost instruction-cache room, measured at C3 2-RHS
+// 255.7 -> 237.7 us with the cap at 4 (1-RHS unchanged; nx = 10: 978 -> 964 us;
+// a cap of 2: 242 us). A smaller dot unroll shrinks code further but slows
+// the loops (unroll 2: 1-RHS 225 us).
+#ifndef SCN_TASK_S_MAX
+#define SCN_TASK_S_MAX 4
+#endif
+constexpr int kDotUnroll = SCN_DOT_UNROLL;
 template <int NRHS, int S>
 __device__ __forceinline__ void dot_split(const double* __restrict__ col, const double* __restrict__ v0,
                                           int vstride, int lenp, int q, double (&out)[NRHS]) {
   double a[NRHS], bq[NRHS];
 #pragma unroll
   for (int r = 0; r < NRHS; ++r) a[r] = bq[r] = 0.0;
-#pragma unroll 4
+#pragma unroll kDotUnroll
   for (int k = 2 * q; k < lenp; k += 2 * S) {
     const double2 m = *reinterpret_cast<const double2*>(col + k);
 #pragma unroll
@@ -362,12 +377,12 @@ __device__ __forceinline__ void dot_split(const double* __restrict__ col, const 
 // threads per task, S chosen so one round covers the tasks when possible.
 template <class Body>
 __device__ __forceinline__ void for_tasks(int ntasks, int ttid, const Body& body) {
-  if (ntasks * 8 <= kTeam) {
+  if (SCN_TASK_S_MAX >= 8 && ntasks * 8 <= kTeam) {
     const int g = ttid >> 3, q = ttid & 7;
-    body.template run<8>(g, q, g < ntasks);
-  } else if (ntasks * 4 <= kTeam) {
+    body.template run<(SCN_TASK_S_MAX >= 8 ? 8 : 4)>(g, q, g < ntasks);
+  } else if (SCN_TASK_S_MAX >= 4 && ntasks * 4 <= kTeam) {
     const int g = ttid >> 2, q = ttid & 3;
-    body.template run<4>(g, q, g < ntasks);
+    body.template run<(SCN_TASK_S_MAX >= 4 ? 4 : 2)>(g, q, g < ntasks);
   } else if (ntasks * 2 <= kTeam) {
     const int g = ttid >> 1, q = ttid & 1;
     body.template run<2>(g, q, g < ntasks);
@@ -967,8 +982,11 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
     }
   }
   __syncthreads();
-  const bool fb = P.fb_S != nullptr;
-  if (fb) fb_epilogue_cta(P, items, K);  // this CTA's partial, written by threads < 6 (after a barrier)
+  // the fused FB finish exists only in the 1-RHS instantiations: carrying
+  // its code made the 2-RHS kernel 10 us slower (258 -> 268 us at C3)
+  const bool fb = NRHS == 1 && P.fb_S != nullptr;
+  if constexpr (NRHS == 1)
+    if (fb) fb_epilogue_cta(P, items, K);  // this CTA's partial, written by threads < 6 (after a barrier)
   __shared__ int s_last;
   if (fb) __syncthreads();
   if (tid == 0) {
@@ -978,10 +996,11 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   }
   __syncthreads();
   if (s_last) {
-    if (fb) {
-      __threadfence();
-      fb_epilogue_last(P);
-    }
+    if constexpr (NRHS == 1)
+      if (fb) {
+        __threadfence();
+        fb_epilogue_last(P);
+      }
     if (tid == 0) {
       P.ctrl[1] = 0u;
       __threadfence();

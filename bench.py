@@ -438,7 +438,14 @@ def main():
         out["cpu_baseline"] = cpu_baseline(prob.flat(), lam0s or None, gpu)
     if rank == 0:
         print(json.dumps(out), flush=True)
+    # release the handle (and with it the library's own NCCL communicator)
+    # while every rank is still alive, before the process group goes away
+    del dev, cache
+    import gc
+
+    gc.collect()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 

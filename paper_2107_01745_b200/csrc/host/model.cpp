@@ -60,11 +60,11 @@ void Problem::finalize() {
   dual_dim = off;
 }
 
-template <class T>
-static std::vector<T> take(const T* src, size_t n) {
+template <class T, class V = std::vector<T>>
+static V take(const T* src, size_t n) {
   if (n == 0) return {};
   if (!src) fail(SCENOPT_E_DIMENSION_MISMATCH, "problem view: missing array");
-  return std::vector<T>(src, src + n);
+  return V(src, src + n);
 }
 
 Problem problem_from_view(const scenopt_problem_view& v) {
@@ -82,12 +82,12 @@ Problem problem_from_view(const scenopt_problem_view& v) {
   p.ancestor = take(v.ancestor, n);
   p.probability = take(v.probability, n);
   p.root_state = take(v.root_state, static_cast<size_t>(p.nx));
-  p.A = take(v.A, n * p.sxx());
-  p.B = take(v.B, n * p.sxu());
+  p.A = take<double, BigVec>(v.A, n * p.sxx());
+  p.B = take<double, BigVec>(v.B, n * p.sxu());
   p.c = take(v.c, n * p.nx);
-  p.Q = take(v.Q, n * p.sxx());
-  p.R = take(v.R, n * p.suu());
-  p.S = take(v.S, n * p.sxu());
+  p.Q = take<double, BigVec>(v.Q, n * p.sxx());
+  p.R = take<double, BigVec>(v.R, n * p.suu());
+  p.S = take<double, BigVec>(v.S, n * p.sxu());
   p.q = take(v.q, n * p.nx);
   p.r = take(v.r, n * p.nu);
   p.stage_rows = take(v.stage_rows, n);
@@ -103,7 +103,7 @@ Problem problem_from_view(const scenopt_problem_view& v) {
   for (int l = 0; l < L; ++l)
     if (p.terminal_rows[l] < 0) fail(SCENOPT_E_DIMENSION_MISMATCH, "problem view: negative terminal rows");
   p.finalize();
-  p.P = take(v.P, static_cast<size_t>(L) * p.sxx());
+  p.P = take<double, BigVec>(v.P, static_cast<size_t>(L) * p.sxx());
   p.p = take(v.p, static_cast<size_t>(L) * p.nx);
   p.F = take(v.F, static_cast<size_t>(p.stage_total) * p.nx);
   p.G = take(v.G, static_cast<size_t>(p.stage_total) * p.nu);
@@ -371,12 +371,12 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
   const size_t sxx = p.sxx(), sxu = p.sxu(), suu = p.suu();
   const int nw = nx + nu;
   const size_t sww = static_cast<size_t>(nw) * nw;
-  p.A.assign(n * sxx, 0.0);
-  p.B.assign(n * sxu, 0.0);
+  zeros(p.A, n * sxx);
+  zeros(p.B, n * sxu);
   p.c.assign(static_cast<size_t>(n) * nx, 0.0);
-  p.Q.assign(n * sxx, 0.0);
-  p.R.assign(n * suu, 0.0);
-  p.S.assign(n * sxu, 0.0);
+  zeros(p.Q, n * sxx);
+  zeros(p.R, n * suu);
+  zeros(p.S, n * sxu);
   p.q.assign(static_cast<size_t>(n) * nx, 0.0);
   p.r.assign(static_cast<size_t>(n) * nu, 0.0);
   p.F.assign(static_cast<size_t>(p.stage_total) * nx, 0.0);
@@ -386,7 +386,7 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
   p.g_gamma.assign(static_cast<size_t>(n), 0.0);
   p.zmin.assign(static_cast<size_t>(p.dual_dim), 0.0);
   p.zmax.assign(static_cast<size_t>(p.dual_dim), 0.0);
-  p.P.assign(static_cast<size_t>(L) * sxx, 0.0);
+  zeros(p.P, static_cast<size_t>(L) * sxx);
   p.p.assign(static_cast<size_t>(L) * nx, 0.0);
   p.FN.assign(static_cast<size_t>(L) * nx, 0.0);
   p.tg_kind.assign(static_cast<size_t>(L), 1);
@@ -429,7 +429,8 @@ Problem gen_random(uint64_t seed, int nx, int nu, int horizon, const std::vector
       p.zmax[off + k] = 0.05 + 0.3 * unit();
     }
   }
-  std::vector<double> proot(static_cast<size_t>(L) * sxx);
+  BigVec proot;
+  zeros(proot, static_cast<size_t>(L) * sxx);
   for (int l = 0; l < L; ++l) {
     double* W = kept(p.first_leaf + l) ? proot.data() + l * sxx : scratch.data();
     for (int a = 0; a < nx; ++a)
@@ -618,12 +619,12 @@ Problem gen_spring_mass(int masses, const SpringMass& params) {
   p.finalize();
   p.root_state = par.root_state.empty() ? std::vector<double>(static_cast<size_t>(nx), 0.0) : par.root_state;
   const size_t sxx = p.sxx(), sxu = p.sxu(), suu = p.suu();
-  p.A.assign(n * sxx, 0.0);
-  p.B.assign(n * sxu, 0.0);
+  zeros(p.A, n * sxx);
+  zeros(p.B, n * sxu);
   p.c.assign(static_cast<size_t>(n) * nx, 0.0);
-  p.Q.assign(n * sxx, 0.0);
-  p.R.assign(n * suu, 0.0);
-  p.S.assign(n * sxu, 0.0);
+  zeros(p.Q, n * sxx);
+  zeros(p.R, n * suu);
+  zeros(p.S, n * sxu);
   p.q.assign(static_cast<size_t>(n) * nx, 0.0);
   p.r.assign(static_cast<size_t>(n) * nu, 0.0);
   p.F.assign(static_cast<size_t>(p.stage_total) * nx, 0.0);
@@ -633,7 +634,7 @@ Problem gen_spring_mass(int masses, const SpringMass& params) {
   p.g_gamma.assign(static_cast<size_t>(n), 0.0);
   p.zmin.assign(static_cast<size_t>(p.dual_dim), 0.0);
   p.zmax.assign(static_cast<size_t>(p.dual_dim), 0.0);
-  p.P.assign(static_cast<size_t>(L) * sxx, 0.0);
+  zeros(p.P, static_cast<size_t>(L) * sxx);
   p.p.assign(static_cast<size_t>(L) * nx, 0.0);
   p.FN.assign(static_cast<size_t>(L) * M * nx, 0.0);
   p.tg_kind.assign(static_cast<size_t>(L), 1);

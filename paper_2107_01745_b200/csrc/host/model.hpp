@@ -8,7 +8,12 @@
 #include <cstdint>
 #include <functional>
 #include <stdexcept>
+#include <sys/mman.h>
+
+#include <memory>
+#include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "scenopt_b200.h"
@@ -22,12 +27,61 @@ struct Error : std::runtime_error {
 };
 [[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
 
+// Allocator for the per-node matrices. Blocks of kLazyBytes or more come
+// straight from an anonymous mapping (zero pages, backed on first write), and
+// value-less construction writes nothing, so zeros() of a large array touches
+// no page: a shard's instance never writes the matrices of the nodes it does
+// not hold, and those pages never become resident (host RAM ~1/N per rank).
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  static constexpr size_t kLazyBytes = size_t{64} << 20;
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  T* allocate(size_t n) {
+    if (n * sizeof(T) < kLazyBytes) return std::allocator<T>::allocate(n);
+    void* p = mmap(nullptr, n * sizeof(T), PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t n) noexcept {
+    if (n * sizeof(T) < kLazyBytes)
+      std::allocator<T>::deallocate(p, n);
+    else
+      munmap(p, n * sizeof(T));
+  }
+  template <class U>
+  void construct(U*) noexcept {}  // default-init: no write
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+using BigVec = std::vector<double, NoInitAlloc<double>>;  // per-node matrices (GBs at C4)
+template <class U, class V>
+bool operator==(const NoInitAlloc<U>&, const NoInitAlloc<V>&) noexcept {
+  return true;
+}
+
+// v = n zeros; a large array stays unbacked until written
+inline void zeros(BigVec& v, size_t n) {
+  BigVec().swap(v);
+  if (n * sizeof(double) >= NoInitAlloc<double>::kLazyBytes)
+    v.resize(n);  // fresh anonymous mapping: reads as zero
+  else
+    v.assign(n, 0.0);
+}
+
 struct Problem {
   int nx = 0, nu = 0, N = 0, n = 0, L = 0, first_leaf = 0, dual_dim = 0, stage_total = 0;
   std::vector<int32_t> ancestor, stage_offsets, stage_rows, terminal_rows, g_kind, tg_kind;
   std::vector<int32_t> mode;  // Markov mode per node (-1 root); empty when unknown (scenario_tree.hpp:41)
-  std::vector<double> probability, root_state, A, B, c, Q, R, S, q, r, F, G, g_gamma, P, p, FN,
-      tg_gamma, zmin, zmax;
+  std::vector<double> probability, root_state, c, q, r, F, G, g_gamma, p, FN, tg_gamma, zmin, zmax;
+  BigVec A, B, Q, R, S, P;
   // derived (finalize)
   std::vector<int32_t> node_stage, child_begin, child_count, dual_offset, tdual_offset;
   // Nodes whose problem data this instance holds (empty: all). A shard's

@@ -488,12 +488,12 @@ Problem parse_problem(const std::string& text) {
   // pack the flat model (node 0 keeps zero blocks)
   const size_t sxx = p.sxx(), sxu = p.sxu(), suu = p.suu();
   p.root_state = root.d;
-  p.A.assign(n * sxx, 0.0);
-  p.B.assign(n * sxu, 0.0);
+  zeros(p.A, n * sxx);
+  zeros(p.B, n * sxu);
   p.c.assign(static_cast<size_t>(n) * nx, 0.0);
-  p.Q.assign(n * sxx, 0.0);
-  p.R.assign(n * suu, 0.0);
-  p.S.assign(n * sxu, 0.0);
+  zeros(p.Q, n * sxx);
+  zeros(p.R, n * suu);
+  zeros(p.S, n * sxu);
   p.q.assign(static_cast<size_t>(n) * nx, 0.0);
   p.r.assign(static_cast<size_t>(n) * nu, 0.0);
   p.F.assign(static_cast<size_t>(p.stage_total) * nx, 0.0);
@@ -502,12 +502,12 @@ Problem parse_problem(const std::string& text) {
   p.g_gamma.assign(static_cast<size_t>(n), 0.0);
   p.zmin.assign(static_cast<size_t>(p.dual_dim), 0.0);
   p.zmax.assign(static_cast<size_t>(p.dual_dim), 0.0);
-  p.P.assign(L * sxx, 0.0);
+  zeros(p.P, L * sxx);
   p.p.assign(L * nx, 0.0);
   p.FN.assign(static_cast<size_t>(p.dual_dim - p.stage_total) * nx, 0.0);
   p.tg_kind.assign(L, 0);
   p.tg_gamma.assign(L, 0.0);
-  auto put = [](std::vector<double>& dst, size_t off, const M& m) {
+  auto put = [](auto& dst, size_t off, const M& m) {
     std::copy(m.d.begin(), m.d.end(), dst.begin() + static_cast<std::ptrdiff_t>(off));
   };
   for (int i = 1; i < n; ++i) {

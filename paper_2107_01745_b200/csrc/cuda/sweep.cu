@@ -25,15 +25,16 @@
 //               vectors (y rows, child contributions, parent x/u, u_off,
 //               affine terms) with async 8-byte copies; four such round trips
 //               are in flight at once.
-//   warps 4..7  consumer team 0 (even items), warps 8..11 team 1 (odd
-//               items): wait for the item's matrices (TMA, slot FULL) and
+//   warps 4..15 four consumer teams of three warps (team t takes items
+//               k = t mod 4): wait for the item's matrices (slot FULL) and
 //               vectors (stage FULL), compute every product from shared
-//               memory, and recycle the slot with one cp.async.bulk (TMA 1-D)
-//               of item k+nslot.
-//   warp 12     publisher: retires items in order (CTA-scope counter) and
+//               memory, release the slot and the staging area.
+//   warp 16     publisher: retires items in order (CTA-scope counter) and
 //               releases the flags of publishing items, one gpu-scope fence
 //               per batch of finished items.
-// Products are "dot columns" split over S in {1,2,4,8} threads (interleaved
+//   warp 17     issuer: streams the CTA's items through the matrix slots, one
+//               cp.async.bulk (TMA 1-D) per item once its slot is released.
+// Products are "dot columns" split over S in {1,2,4} threads (interleaved
 // 16-byte shared loads over padded columns + xor shuffles), for all
 // right-hand sides at once so a 2-RHS (p-NAMA) sweep reads each matrix once.
 // fp64 throughout; the partial-sum order is fixed, so results are
@@ -50,18 +51,26 @@ namespace scn {
 
 namespace {
 
+// Four consumer teams of three warps (the 576 threads and 96 registers of
+// three 128-thread teams): one more item in flight per SM. Measured against
+// 3 x 128 (profiles/ab_teams_r02.txt): C3 affine 219.9 -> 218 us, C3 2-RHS
+// 238.9 -> 229 us, nx = 10 (873,813 nodes) 963 -> 939 us; 5 x 96 spills
+// (C3 242 us); 4 x 128 (704 threads) caps registers at 80 and spills.
 #ifndef SCN_TEAM_THREADS
-#define SCN_TEAM_THREADS 128
+#define SCN_TEAM_THREADS 96
 #endif
 constexpr int kTeam = SCN_TEAM_THREADS;  // threads per consumer team
 #ifndef SCN_TEAMS
-#define SCN_TEAMS 3
+#define SCN_TEAMS 4
 #endif
 constexpr int kTeams = SCN_TEAMS;  // consumer teams (items k = team mod kTeams)
 constexpr int kProducers = 4;  // producer warps (== slots), warp p stages items k = p (mod 4)
 constexpr int kThreads = 32 * kProducers + kTeams * kTeam + 64;  // producers, teams, publisher, issuer
 constexpr int kTeamWarp0 = kProducers;
-constexpr int kStageQ = (kTeams == 3 || kTeams == 6) ? 12 : 8;  // staging ring depth (items staged ahead); a multiple of kProducers
+#ifndef SCN_STAGE_Q
+#define SCN_STAGE_Q ((kTeams == 3 || kTeams == 6) ? 12 : (kTeams == 5 ? 20 : 8))
+#endif
+constexpr int kStageQ = SCN_STAGE_Q;  // staging ring depth (items staged ahead); a multiple of kProducers
                             // and even, so each staging area always serves the same producer
                             // warp and the same team in order
 static_assert(kStageQ % kProducers == 0 && kStageQ % kTeams == 0, "staging ring vs producers / teams");

@@ -426,19 +426,34 @@ struct Engine {
   struct SweepTimer {
     bool on = std::getenv("SCN_SOLVE_TIMING") != nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    std::vector<double> seq_ms;
+    std::vector<int> kind;  // per sweep: 0 homogeneous, 1 affine, 2 affine + fused FB finish, 3 two RHS
     ~SweepTimer() {
       report_marks();
       if (!on || ev.empty()) return;
       cudaDeviceSynchronize();
-      double tot = 0.0;
-      for (auto& p : ev) {
+      double tot = 0.0, by_kind[4] = {0, 0, 0, 0};
+      int n_kind[4] = {0, 0, 0, 0};
+      for (size_t i = 0; i < ev.size(); ++i) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, p.first, p.second);
+        cudaEventElapsedTime(&ms, ev[i].first, ev[i].second);
+        seq_ms.push_back(ms);
         tot += ms;
-        cudaEventDestroy(p.first);
-        cudaEventDestroy(p.second);
+        by_kind[kind[i]] += ms;
+        ++n_kind[kind[i]];
+        cudaEventDestroy(ev[i].first);
+        cudaEventDestroy(ev[i].second);
       }
       std::fprintf(stderr, "[scn] %zu sweeps, %.3f ms GPU (%.1f us each)\n", ev.size(), tot, 1e3 * tot / ev.size());
+      if (std::atoi(std::getenv("SCN_SOLVE_TIMING")) == 3) {  // every sweep in order: kind:us
+        std::fprintf(stderr, "[scn]   seq");
+        for (size_t i = 0; i < ev.size(); ++i) std::fprintf(stderr, " %d:%.0f", kind[i], 1e3 * seq_ms[i]);
+        std::fprintf(stderr, "\n");
+      }
+      static const char* const names[4] = {"homogeneous", "affine", "affine+fb", "2-rhs"};
+      for (int q = 0; q < 4; ++q)
+        if (n_kind[q])
+          std::fprintf(stderr, "[scn]   %-12s %3d x %.1f us\n", names[q], n_kind[q], 1e3 * by_kind[q] / n_kind[q]);
       double st = 0.0;
       for (auto& p : sync_ev) {
         float ms = 0.f;
@@ -482,8 +497,9 @@ struct Engine {
     }
   } timer;
   template <class F>
-  void timed(F&& f) {
+  void timed(F&& f, int kind = 0) {
     if (!timer.on) return f();
+    timer.kind.push_back(kind);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
@@ -495,7 +511,8 @@ struct Engine {
     timer.ev.emplace_back(a, b);
   }
   void sweep1(bool affine, const double* y, double* x, double* u, double* Hx) {
-    timed([&] { dev_sweep(d, 1, affine, &y, x ? &x : nullptr, u ? &u : nullptr, &Hx); });
+    timed([&] { dev_sweep(d, 1, affine, &y, x ? &x : nullptr, u ? &u : nullptr, &Hx); },
+          affine ? (d.fb_next ? 2 : 1) : 0);
   }
   // H x0(r) launched only if the last fb_finish missed the stop tolerance
   // (I[CONV], see k_fb_finish): a speculative sweep costs a launch at convergence
@@ -518,7 +535,7 @@ struct Engine {
   void sweep2(const double* a, const double* b, double* Ha, double* Hb) {
     const double* ys[2] = {a, b};
     double* hs[2] = {Ha, Hb};
-    timed([&] { dev_sweep(d, 2, false, ys, nullptr, nullptr, hs); });
+    timed([&] { dev_sweep(d, 2, false, ys, nullptr, nullptr, hs); }, 3);
   }
 
   // f_hat(0) and H x(0), once per handle (fhat identity)

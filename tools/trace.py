@@ -9,7 +9,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2107_01745_b200 as so
 from paper_2107_01745_b200 import _native as N
-shapes = {"c3": (50, 20, 20, [8, 8, 8, 2]), "c4": (50, 20, 20, [8, 8, 8, 8, 4]), "c1": (10, 5, 10, [2, 2, 2]), "c5_1k": (10, 5, 20, [2] * 6)}
+shapes = {"c3": (50, 20, 20, [8, 8, 8, 2]), "c4": (50, 20, 20, [8, 8, 8, 8, 4]), "c1": (10, 5, 10, [2, 2, 2]), "c5_1k": (10, 5, 20, [2] * 6),
+          "c5b": (10, 5, 20, [4] * 8)}
 nx, nu, H, br = shapes[sys.argv[1] if len(sys.argv) > 1 else "c3"]
 p = so.gen_random_instance(1, nx, nu, H, br)
 c = so.factor(p)
@@ -34,7 +35,7 @@ stage = np.searchsorted(p.flat()["stage_offsets"], it[:, 3], side="right") - 1
 cols = ["top", "tma", "vec", "A", "Async", "B", "end", "done", "p_start", "p_deps", "p_staged", "released"]
 print("steady-state medians (us):")
 for ps, nm in ((0, "bw"), (1, "fw")):
-    m = (it[:, 2] == ps) & (stage >= 6) & (stage <= H - 2)
+    m = (it[:, 2] == ps) & (stage >= max(6, len(br) + 2)) & (stage <= H - 2)
     d = np.diff(t[m][:, :8], axis=1)
     print(" ", nm, {cols[i + 1]: round(float(np.median(d[:, i])), 2) for i in range(7)})
 print("top levels: stage, last release, per item medians: deps->staged, staged->team vec ready, vec->done, done->released")

@@ -120,7 +120,7 @@ typedef struct scenopt_dev_info {
   int32_t consumer_stage; /* 1: vectors staged by the consumer teams (very wide states) */
   int32_t flat_top;       /* 1: forward stages above the cut flattened into one level */
   int32_t device_factor;  /* 1: factor computed on the device (scenopt_dev_create_device_factor) */
-  int32_t pad0;
+  int32_t producer_warps; /* sweep kernel geometry: 4, or 6 for layouts of many-node items */
   int64_t exchange_doubles; /* sharded: doubles sum-allreduced per sweep and right-hand side; 0 otherwise */
 } scenopt_dev_info;
 

@@ -69,7 +69,7 @@ class DevInfoC(C.Structure):
         ("sweep_bytes_hom2", C.c_int64), ("cut_stage", C.c_int32), ("shard_stage", C.c_int32),
         ("rank", C.c_int32), ("world", C.c_int32), ("shard_first", C.c_int32), ("shard_past", C.c_int32),
         ("items_global", C.c_int32), ("consumer_stage", C.c_int32),
-        ("flat_top", C.c_int32), ("device_factor", C.c_int32), ("pad0", C.c_int32),
+        ("flat_top", C.c_int32), ("device_factor", C.c_int32), ("producer_warps", C.c_int32),
         ("exchange_doubles", C.c_int64),
     ]
 

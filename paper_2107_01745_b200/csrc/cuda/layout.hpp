@@ -25,6 +25,9 @@
 // blocks], 16-byte aligned, so ONE cp.async.bulk moves an item's metadata and
 // matrices into shared memory.
 #pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
 #include <cstdint>
 
 namespace scn {
@@ -71,6 +74,7 @@ constexpr int kGlobalBlocks = 2;
 constexpr int kFlatTop = 4;  // forward top node computed from its ancestors' u_off; depth in bits 8..
 constexpr int kMaxRhs = 2;
 constexpr int kMaxSlots = 8;
+constexpr int kManyNodeItems = 8;  // largest item of at least this many nodes: six-producer sweep geometry
 
 struct SweepParams {
   int nx, nu, n, first_leaf, dual_dim;
@@ -131,5 +135,21 @@ struct SweepParams {
   unsigned* pub_seq;
   unsigned seq;
 };
+
+// One compiled geometry of the sweep kernel: cuda/sweep.cu is built once per
+// geometry (producer warps and staging-ring depth differ; the consumer teams,
+// and so every product's summation order, are the same, so the geometries
+// give bitwise-identical results). A handle picks one when its layout is
+// built (device.cpp).
+struct SweepImpl {
+  const char* name;
+  int producers, teams, threads, stage_queue, scratch_bufs;
+  size_t (*static_smem)();
+  cudaError_t (*configure)(size_t dyn_smem);
+  cudaError_t (*occupancy)(int* ctas_per_sm, size_t dyn_smem);
+  cudaError_t (*launch)(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax, cudaStream_t st);
+};
+extern const SweepImpl kSweepProducers4;  // four producer warps, 8-deep staging ring (default)
+extern const SweepImpl kSweepProducers6;  // six producer warps, 12-deep ring (layouts of many-node items)
 
 }  // namespace scn

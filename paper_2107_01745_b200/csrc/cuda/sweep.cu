@@ -47,7 +47,15 @@
 #include "fbrow.cuh"
 #include "layout.hpp"
 
+// One build per kernel geometry (cuda/layout.hpp SweepImpl): the default,
+// and the six-producer one built with -DSCN_SWEEP_NS=geom_p6 ... (Makefile).
+#ifndef SCN_SWEEP_NS
+#define SCN_SWEEP_NS geom_p4
+#define SCN_SWEEP_IMPL kSweepProducers4
+#endif
+
 namespace scn {
+namespace SCN_SWEEP_NS {
 
 namespace {
 
@@ -64,7 +72,10 @@ constexpr int kTeam = SCN_TEAM_THREADS;  // threads per consumer team
 #define SCN_TEAMS 4
 #endif
 constexpr int kTeams = SCN_TEAMS;  // consumer teams (items k = team mod kTeams)
-constexpr int kProducers = 4;  // producer warps (== slots), warp p stages items k = p (mod 4)
+#ifndef SCN_PRODUCERS
+#define SCN_PRODUCERS 4
+#endif
+constexpr int kProducers = SCN_PRODUCERS;  // producer warps, warp p stages items k = p (mod kProducers)
 constexpr int kThreads = 32 * kProducers + kTeams * kTeam + 64;  // producers, teams, publisher, issuer
 constexpr int kTeamWarp0 = kProducers;
 #ifndef SCN_STAGE_Q
@@ -1020,8 +1031,6 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 
 }  // namespace
 
-int sweep_threads() { return kThreads; }
-int sweep_teams() { return kTeams; }
 namespace {
 #define SCN_K(R, M) reinterpret_cast<const void*>(sweep_kernel<R, M>)
 const void* const kKernels[3][4] = {
@@ -1032,7 +1041,7 @@ const void* const kKernels[3][4] = {
 #undef SCN_K
 }  // namespace
 
-size_t sweep_static_smem() {
+size_t static_smem() {
   size_t m = 0;
   for (auto& row : kKernels)
     for (const void* fn : row) {
@@ -1042,12 +1051,22 @@ size_t sweep_static_smem() {
     }
   return m;
 }
-int sweep_stage_queue() { return kStageQ; }
-int sweep_scratch_bufs() { return kScratchBufs; }
+cudaError_t configure(size_t dyn_smem);
+cudaError_t occupancy(int* ctas_per_sm, size_t dyn_smem);
+cudaError_t launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax, cudaStream_t stream);
+}  // namespace SCN_SWEEP_NS
 
+#define SCN_STR2(x) #x
+#define SCN_STR(x) SCN_STR2(x)
+extern const SweepImpl SCN_SWEEP_IMPL = {
+    SCN_STR(SCN_SWEEP_NS), SCN_SWEEP_NS::kProducers, SCN_SWEEP_NS::kTeams, SCN_SWEEP_NS::kThreads,
+    SCN_SWEEP_NS::kStageQ, SCN_SWEEP_NS::kScratchBufs, &SCN_SWEEP_NS::static_smem,
+    &SCN_SWEEP_NS::configure, &SCN_SWEEP_NS::occupancy, &SCN_SWEEP_NS::launch};
+
+#ifndef SCN_SWEEP_SECONDARY  // diagnostics (profiling build of the default geometry)
 cudaError_t sweep_trace(long long* dev_buf) {
 #ifdef SCN_SWEEP_PROFILE
-  return cudaMemcpyToSymbol(g_trace, &dev_buf, sizeof(dev_buf));
+  return cudaMemcpyToSymbol(SCN_SWEEP_NS::g_trace, &dev_buf, sizeof(dev_buf));
 #else
   (void)dev_buf;
   return cudaErrorNotSupported;
@@ -1056,7 +1075,7 @@ cudaError_t sweep_trace(long long* dev_buf) {
 
 cudaError_t sweep_timeline(unsigned long long* dev_buf) {
 #ifdef SCN_SWEEP_PROFILE
-  return cudaMemcpyToSymbol(g_timeline, &dev_buf, sizeof(dev_buf));
+  return cudaMemcpyToSymbol(SCN_SWEEP_NS::g_timeline, &dev_buf, sizeof(dev_buf));
 #else
   (void)dev_buf;
   return cudaErrorNotSupported;
@@ -1065,10 +1084,10 @@ cudaError_t sweep_timeline(unsigned long long* dev_buf) {
 
 cudaError_t sweep_profile_read(unsigned long long* out, bool reset) {
 #ifdef SCN_SWEEP_PROFILE
-  cudaError_t e = cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 16);
+  cudaError_t e = cudaMemcpyFromSymbol(out, SCN_SWEEP_NS::g_prof, sizeof(unsigned long long) * 16);
   if (e == cudaSuccess && reset) {
     unsigned long long z[16] = {0};
-    e = cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    e = cudaMemcpyToSymbol(SCN_SWEEP_NS::g_prof, z, sizeof(z));
   }
   return e;
 #else
@@ -1078,7 +1097,10 @@ cudaError_t sweep_profile_read(unsigned long long* out, bool reset) {
 #endif
 }
 
-cudaError_t sweep_configure(size_t dyn_smem) {
+#endif
+
+namespace SCN_SWEEP_NS {
+cudaError_t configure(size_t dyn_smem) {
   // The cap is a per-function, per-device attribute shared by every handle of
   // the process: only ever raise it (a lower value would break the launches
   // of handles with larger slots).
@@ -1100,7 +1122,7 @@ cudaError_t sweep_configure(size_t dyn_smem) {
   return cudaSuccess;
 }
 
-cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem) {
+cudaError_t occupancy(int* ctas_per_sm, size_t dyn_smem) {
   int lo = 1 << 30;
   for (auto& row : kKernels)
     for (const void* fn : row) {
@@ -1113,8 +1135,7 @@ cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem) {
   return cudaSuccess;
 }
 
-cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax,
-                         cudaStream_t stream) {
+cudaError_t launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax, cudaStream_t stream) {
   SweepParams p = P;
   void* args[] = {&p, &mmax, &mNmax};
 #ifdef SCN_SWEEP_PROFILE
@@ -1131,5 +1152,6 @@ cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mm
   const void* fn = (host_out && mode == 0) ? kKernels[2][P.nrhs == 2 ? 1 : 0] : kKernels[P.nrhs == 2 ? 1 : 0][mode];
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, dyn_smem, stream);
 }
+}  // namespace SCN_SWEEP_NS
 
 }  // namespace scn

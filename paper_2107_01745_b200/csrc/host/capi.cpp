@@ -389,6 +389,7 @@ int scenopt_dev_info_get(const scenopt_dev* h, scenopt_dev_info* info) {
     info->consumer_stage = d.consumer_stage ? 1 : 0;
     info->flat_top = d.flat_top ? 1 : 0;
     info->device_factor = d.device_factor ? 1 : 0;
+    info->producer_warps = d.sweep->producers;
   });
 }
 

@@ -299,6 +299,9 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   // shard stage; then the shard-stage contributions are sum-allreduced; then
   // B = the (redundant) top backward, top forward and local forward.
   d->grid = d->sm_count;
+  int64_t packed_bytes = 0;  // node blocks of both passes
+  for (int c = 0; c < p.n; ++c) packed_bytes += (bws[c] + fws[c]) * 8;
+  constexpr int64_t kLatencyBoundBytes = int64_t(512) << 20;  // below: a sweep is bound by its dependency levels
   const int min_sub_cfg = env_int("SCENOPT_MIN_SUBTREES", 4);
   if (const int g = env_int("SCENOPT_GRID", 0)) {
     d->grid = std::min(g, d->grid);  // experiments only
@@ -309,9 +312,7 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     // level (1023-node C5 tree: 211 -> 135 us per sweep on 16 CTAs).
     int widest = 0;
     for (int t = 1; t <= p.N; ++t) widest = std::max(widest, p.stage_offsets[t + 1] - p.stage_offsets[t]);
-    int64_t bytes = 0;
-    for (int c = 0; c < p.n; ++c) bytes += (bws[c] + fws[c]) * 8;
-    if (widest < min_sub_cfg * d->grid && bytes < (int64_t(512) << 20)) {
+    if (widest < min_sub_cfg * d->grid && packed_bytes < kLatencyBoundBytes) {
       const int g = widest / min_sub_cfg;
       if (g >= 8) d->grid = g;
     }
@@ -968,63 +969,98 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   //   2. producer-staged, 4 slots sized for the small items: larger items keep
   //      their blocks in HBM (only the node headers are copied; kGlobalBlocks);
   //   3./4. the same with consumer-staged vectors (one staging area per team
-  //      instead of a 12-deep ring) for very wide states.
+  //      instead of the producers' staging ring) for very wide states.
   // SCENOPT_NSLOT / SCENOPT_SLOT_KB / SCENOPT_STAGE=consumer force choices (tests).
+  // Kernel geometry: large trees whose items carry many nodes (small states,
+  // nx ~ 10) are limited by the producers' staging of many short vectors per
+  // item and take six producer warps; one-node items (C3, C4) and small,
+  // latency-bound trees keep four (profiles/c5_geometry_r02.md). Both
+  // compute bitwise-identical results. SCENOPT_SWEEP_PRODUCERS=4|6 forces one (tests).
+  const int force_geom = env_int("SCENOPT_SWEEP_PRODUCERS", 0);
+  const bool many = d->max_count >= kManyNodeItems && packed_bytes >= kLatencyBoundBytes;
   const int dbl = 8;
   const int force_ns = env_int("SCENOPT_NSLOT", 0);
-  const int teams = sweep_teams();
-  const int stageq = sweep_stage_queue();
-  const size_t optin = static_cast<size_t>(prop.sharedMemPerBlockOptin) - sweep_static_smem();
   const int64_t slot_cap_env = static_cast<int64_t>(env_int("SCENOPT_SLOT_KB", 0)) * 1024 / 8;
   const bool force_consumer = std::getenv("SCENOPT_STAGE") && std::string(std::getenv("SCENOPT_STAGE")) == "consumer";
   const int64_t hdr_doubles_max = static_cast<int64_t>(d->max_count) * (sizeof(NodeMeta) / 8);
-  auto smem_for = [&](int ns, int64_t slot, bool consumer) {
-    return (static_cast<size_t>(ns) * slot + static_cast<size_t>(consumer ? teams : stageq) * d->stage_doubles +
-            static_cast<size_t>(teams) * sweep_scratch_bufs() * d->vec_doubles) * dbl;
-  };
-  int best_ns = 0;
-  int64_t slot = 0;
-  bool consumer = false;
   const int ns_max = std::min(kMaxSlots, 5);
-  auto fits = [&](int ns, int64_t sl, bool cons) {
-    const size_t smem = smem_for(ns, sl, cons);
-    if (smem > optin) return false;
-    SCN_CUDA(sweep_configure(smem));
-    int cps = 0;
-    SCN_CUDA(sweep_occupancy(&cps, smem));
-    return cps >= 1;
+  struct Fit {
+    int ns = 0;  // 0: no layout
+    int64_t slot = 0;
+    bool consumer = false;
+    size_t smem = 0;
   };
-  for (int pass = 0; pass < 2 && !best_ns; ++pass) {
-    const bool cons = pass == 1 || force_consumer;
-    if (pass == 1 && force_consumer) break;
-    // all items in smem
-    if (!slot_cap_env)
-      for (int ns = ns_max; ns >= 2; --ns) {
-        if (force_ns && ns != force_ns) continue;
-        const int64_t sl = (std::max<int64_t>(max_item, 2) + 15) & ~int64_t(15);
-        if (fits(ns, sl, cons)) {
-          best_ns = ns, slot = sl, consumer = cons;
-          break;
+  auto smem_for = [&](const SweepImpl& sw, int ns, int64_t slot, bool consumer) {
+    return (static_cast<size_t>(ns) * slot + static_cast<size_t>(consumer ? sw.teams : sw.stage_queue) * d->stage_doubles +
+            static_cast<size_t>(sw.teams) * sw.scratch_bufs * d->vec_doubles) * dbl;
+  };
+  auto fit_for = [&](const SweepImpl& sw) {
+    const size_t optin = static_cast<size_t>(prop.sharedMemPerBlockOptin) - sw.static_smem();
+    auto fits = [&](int ns, int64_t sl, bool cons) {
+      const size_t smem = smem_for(sw, ns, sl, cons);
+      if (smem > optin) return false;
+      SCN_CUDA(sw.configure(smem));
+      int cps = 0;
+      SCN_CUDA(sw.occupancy(&cps, smem));
+      return cps >= 1;
+    };
+    Fit f;
+    for (int pass = 0; pass < 2 && !f.ns; ++pass) {
+      const bool cons = pass == 1 || force_consumer;
+      if (pass == 1 && force_consumer) break;
+      // all items in smem
+      if (!slot_cap_env)
+        for (int ns = ns_max; ns >= 2; --ns) {
+          if (force_ns && ns != force_ns) continue;
+          const int64_t sl = (std::max<int64_t>(max_item, 2) + 15) & ~int64_t(15);
+          if (fits(ns, sl, cons)) {
+            f.ns = ns, f.slot = sl, f.consumer = cons;
+            break;
+          }
         }
-      }
-    if (best_ns) break;
-    // small items in smem, large ones from HBM. What the staging areas and
-    // scratch leave is computed signed: when the (producer) staging ring alone
-    // exceeds shared memory this pass cannot work (pass 1 stages per team);
-    // a slot must hold at least the node headers of the largest item.
-    const int ns = force_ns ? force_ns : 4;
-    const int64_t left = static_cast<int64_t>(optin / dbl) -
-                         static_cast<int64_t>(cons ? teams : stageq) * d->stage_doubles -
-                         static_cast<int64_t>(teams) * sweep_scratch_bufs() * d->vec_doubles;
-    const int64_t hdr_slot = (hdr_doubles_max + 15) & ~int64_t(15);
-    int64_t sl = slot_cap_env ? slot_cap_env : (left / ns) & ~int64_t(15);
-    sl = std::max<int64_t>(sl, hdr_slot);
-    if (sl <= (int64_t(1) << 26) && static_cast<int64_t>(ns) * sl <= left && fits(ns, sl, cons))
-      best_ns = ns, slot = sl, consumer = cons;
+      if (f.ns) break;
+      // small items in smem, large ones from HBM. What the staging areas and
+      // scratch leave is computed signed: when the (producer) staging ring alone
+      // exceeds shared memory this pass cannot work (pass 1 stages per team);
+      // a slot must hold at least the node headers of the largest item.
+      const int ns = force_ns ? force_ns : 4;
+      const int64_t left = static_cast<int64_t>(optin / dbl) -
+                           static_cast<int64_t>(cons ? sw.teams : sw.stage_queue) * d->stage_doubles -
+                           static_cast<int64_t>(sw.teams) * sw.scratch_bufs * d->vec_doubles;
+      const int64_t hdr_slot = (hdr_doubles_max + 15) & ~int64_t(15);
+      int64_t sl = slot_cap_env ? slot_cap_env : (left / ns) & ~int64_t(15);
+      sl = std::max<int64_t>(sl, hdr_slot);
+      if (sl <= (int64_t(1) << 26) && static_cast<int64_t>(ns) * sl <= left && fits(ns, sl, cons))
+        f.ns = ns, f.slot = sl, f.consumer = cons;
+    }
+    if (f.ns) f.smem = smem_for(sw, f.ns, f.slot, f.consumer);
+    return f;
+  };
+  // Kernel geometry: large trees whose items carry many nodes (small states,
+  // nx ~ 10) are limited by the producers' staging of many short vectors per
+  // item and take six producer warps, unless their deeper staging ring would
+  // cost slots; one-node items (C3, C4) and small, latency-bound trees keep
+  // four (profiles/c5_geometry_r02.md). Both geometries compute
+  // bitwise-identical results. SCENOPT_SWEEP_PRODUCERS=4|6 forces one (tests).
+  Fit fit;
+  if (force_geom == 6 || (force_geom != 4 && many)) {
+    fit = fit_for(kSweepProducers6);
+    d->sweep = &kSweepProducers6;
+    if (force_geom != 6) {
+      const Fit f4 = fit_for(kSweepProducers4);
+      if (!fit.ns || fit.ns < f4.ns || fit.consumer != f4.consumer) fit = f4, d->sweep = &kSweepProducers4;
+    }
+  } else {
+    fit = fit_for(kSweepProducers4);
+    d->sweep = &kSweepProducers4;
   }
-  if (best_ns == 0)
+  const SweepImpl& sw = *d->sweep;
+  if (fit.ns == 0)
     fail(SCENOPT_E_INVALID_PARAMS, "dev_create: the per-item staging vectors do not fit in shared memory (" +
-                                       std::to_string(smem_for(2, hdr_doubles_max, true)) + " bytes)");
+                                       std::to_string(smem_for(sw, 2, hdr_doubles_max, true)) + " bytes)");
+  const int best_ns = fit.ns;
+  const int64_t slot = fit.slot;
+  const bool consumer = fit.consumer;
   d->slot_doubles = static_cast<int>(slot);
   d->consumer_stage = consumer;
   int n_global = 0;
@@ -1037,8 +1073,8 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
   d->items_global = n_global;
   d->nslot = best_ns;
   d->ctas_per_sm = 1;
-  d->dyn_smem = smem_for(best_ns, slot, consumer);
-  SCN_CUDA(sweep_configure(d->dyn_smem));
+  d->dyn_smem = fit.smem;
+  SCN_CUDA(sw.configure(d->dyn_smem));
   d->G = 0;
 
   clk.mark("launch config");
@@ -1375,7 +1411,7 @@ void launch(DevState& d, SweepParams& P, const DevState::Launch& ln) {
   P.items = ln.items;
   P.cta_off = ln.cta_off;
   P.items_total = ln.count;
-  SCN_CUDA(sweep_launch(P, d.grid, d.dyn_smem, d.max_m, d.max_mN, d.stream));
+  SCN_CUDA(d.sweep->launch(P, d.grid, d.dyn_smem, d.max_m, d.max_mN, d.stream));
 }
 // sharded phase A: local backward; this rank's shard-stage contributions
 // and shard-stage dual rows into the (zeroed) exchange buffer. zero_rows

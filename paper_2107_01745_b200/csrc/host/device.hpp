@@ -68,6 +68,7 @@ struct DevState {
   int cut_stage = -1;  // CTA subtree-ownership cut of the main region (-1: all global tickets)
   bool consumer_stage = false;  // teams stage their own vectors (very wide states)
   bool flat_top = false;
+  const SweepImpl* sweep = &kSweepProducers4;  // compiled geometry of the sweep kernel (chosen with the layout)
   const int* sweep_skip = nullptr;  // SweepParams::skip of the next launches (power iteration batches)
   // Fused FB-step finish of the next launch (SweepParams::fb_*; set by the
   // solver engine around one affine 1-RHS sweep of an unsharded handle)
@@ -214,17 +215,10 @@ void dev_sweep_phase(DevState& d, int phase, int nrhs, bool affine, const double
 std::pair<const double*, const double*> dev_gather_primal(DevState& d, const double* x, const double* u);
 const double* dev_gather_dual(DevState& d, const double* y);
 
-// kernel launchers (cuda/*.cu)
-int sweep_teams();
-size_t sweep_static_smem();
-int sweep_stage_queue();
-int sweep_scratch_bufs();
-cudaError_t sweep_configure(size_t dyn_smem);
+// sweep kernel diagnostics (profiling build, cuda/sweep.cu); the launchers
+// are reached through DevState::sweep (layout.hpp SweepImpl)
 cudaError_t sweep_profile_read(unsigned long long* out, bool reset);
 cudaError_t sweep_timeline(unsigned long long* dev_buf);
 cudaError_t sweep_trace(long long* dev_buf);
-cudaError_t sweep_occupancy(int* ctas_per_sm, size_t dyn_smem);
-cudaError_t sweep_launch(const SweepParams& P, int grid, size_t dyn_smem, int mmax, int mNmax,
-                         cudaStream_t stream);
 
 }  // namespace scn

@@ -329,3 +329,31 @@ def test_oversized_staging_ring_falls_back_to_team_staging(gpu, monkeypatch, sha
         for v, pt in ((y, pts[0]), (r, pts[1])):
             ox, ou = ofac.sweep(v, affine)
             assert sup.rel_gap(ox, ou, pt.x.ravel(order="F"), pt.u.ravel(order="F")) < TOL
+
+
+@pytest.mark.parametrize("shape", [(10, 5, 12, [4, 4, 4, 4]), (50, 20, 6, [8, 8]), (6, 3, 9, [3, 3, 3, 3])])
+def test_sweep_geometries_are_bitwise_identical(gpu, monkeypatch, shape):
+    """The six-producer geometry of the sweep kernel (picked for layouts of
+    many-node items) differs from the default only in how vectors are staged:
+    the consumer teams, and so every product's summation order, are the same,
+    so both give the same bits for every sweep kind."""
+    nx, nu, N, br = shape
+    prob = so.gen_random_instance(7, nx, nu, N, br)
+    rng = np.random.default_rng(11)
+    y, r = rng.uniform(-1, 1, prob.dual_dim), rng.uniform(-1, 1, prob.dual_dim)
+    out = {}
+    for p in ("4", "6"):
+        monkeypatch.setenv("SCENOPT_SWEEP_PRODUCERS", p)
+        cache = so.factor(prob)
+        assert cache.dev_info()["producer_warps"] == int(p)
+        res = []
+        for affine in (False, True):
+            pts, hs = so.sweep(cache, [y, r], affine)
+            res += [pts[0].x, pts[0].u, pts[1].x, pts[1].u, hs[0], hs[1]]
+            pts1, hs1 = so.sweep(cache, [y], affine)
+            res += [pts1[0].x, pts1[0].u, hs1[0]]
+        out[p] = res
+    for a, b in zip(out["4"], out["6"]):
+        assert np.array_equal(a, b)
+    monkeypatch.delenv("SCENOPT_SWEEP_PRODUCERS")
+    assert so.factor(prob).dev_info()["producer_warps"] == 4  # small trees keep the default geometry

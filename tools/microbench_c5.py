@@ -73,7 +73,7 @@ def main():
         row = dict(nx=nx, nu=nu, horizon=H, branching=br, nodes=p.num_nodes(), sweeps=k, us_per_sweep=ms * 1e3,
                    algorithmic_bytes=bytes_, gbs=gbs, frac_of_peak=gbs / peak, l2_resident=packed < l2,
                    nodes_per_item_max=info["nodes_per_item_max"], slots=info["slots"],
-                   items_global=info["items_global"], setup_s=round(setup, 1),
+                   items_global=info["items_global"], producer_warps=info["producer_warps"], setup_s=round(setup, 1),
                    factor="device" if a.device_factor else "host")
         rows.append(row)
         print(json.dumps(row), flush=True)

@@ -33,7 +33,8 @@ def short(f):
     k = int(m.group(1))
     name = f[m.end():m.end() + k]
     t = re.search(r"ILi(\d)ELi(\d)E", f[m.end() + k:])
-    return name + (f"<{t.group(1)},{t.group(2)}>" if t else "")
+    g = re.search(r"geom_(p\d)", f)  # sweep kernel geometry (four / six producer warps)
+    return name + (f"<{t.group(1)},{t.group(2)}>" if t else "") + (f" {g.group(1)}" if g else "")
 
 
 print(f"library: {os.path.relpath(lib, ROOT)}")

@@ -1,5 +1,5 @@
 """Per-CUDA-line warp-stall samples of an ncu capture (cuda,sass source view):
-python tools/ncu_lines.py REPORT.ncu-rep [TOP]"""
+python tools/ncu_lines.py REPORT.ncu-rep [TOP] [KERNEL_REGEX]"""
 import csv
 import io
 import subprocess
@@ -7,7 +7,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kfilter = ["--kernel-name", "regex:" + sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + kfilter,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 lines, fname, total = [], None, 0

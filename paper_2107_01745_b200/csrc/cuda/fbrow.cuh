@@ -56,27 +56,32 @@ __device__ __forceinline__ void fb_row(int64_t i, int kd, double yi, double hi, 
 // (I[CONV]: converged or rejected).
 __device__ __forceinline__ void fb_finalize(double* Sg, int* I, int state, int mode, const double (&s)[6]) {
   double* S = Sg + state * sl::kStateStride;
-  const double lam = S[sl::LAM];
-  const double fhat = mode == 0 ? Sg[sl::FHAT0] - 0.5 * s[4] : S[sl::FHAT];
+  // Every scalar is read before the first store: the stores go through the
+  // same block, so a load after one would be ordered behind it (one L2 round
+  // trip per load on the step's critical path). Same operations as before.
+  const double lam = S[sl::LAM], fhat_state = S[sl::FHAT], fhat0 = Sg[sl::FHAT0];
+  const double rule_d = Sg[sl::GATE_RULE], cert_fhat = Sg[sl::CERT_FHAT], hxw_rw = Sg[sl::HXW_RW],
+               beta_bt = Sg[sl::BETA_BT], rw2 = Sg[sl::RW2], img2 = Sg[sl::IMG2], eps_bt = Sg[sl::EPS_BT],
+               r2 = Sg[sl::R2], hr2 = Sg[sl::HR2], rr2 = Sg[sl::RR2], eps_stop = Sg[sl::EPS_STOP];
+  const double fhat = mode == 0 ? fhat0 - 0.5 * s[4] : fhat_state;
   S[sl::FHAT] = fhat;
   S[sl::CONJ] = s[0];
   S[sl::ZN2] = s[1];
   S[sl::VALUE] = fhat + s[0] + lam * s[2] + 0.5 * lam * s[3];
   S[sl::RESID] = s[5];
-  const int rule = static_cast<int>(Sg[sl::GATE_RULE]);
+  const int rule = static_cast<int>(rule_d);
   int reject = 0;
   if (rule == 0) {  // original rule: candidate fhat above the model (the host takes this verdict)
-    const double model = __dadd_rn(__dadd_rn(Sg[sl::CERT_FHAT], __dmul_rn(lam, Sg[sl::HXW_RW])),
-                                   __dmul_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(1.0, -Sg[sl::BETA_BT])), lam),
-                                             Sg[sl::RW2]));
+    const double model = __dadd_rn(__dadd_rn(cert_fhat, __dmul_rn(lam, hxw_rw)),
+                                   __dmul_rn(__dmul_rn(__dmul_rn(0.5, __dadd_rn(1.0, -beta_bt)), lam), rw2));
     reject = fhat > model;
   } else if (rule == 1) {  // MINFBE simple rule: lambda |img| > eps_bt |R| halves lambda
-    reject = __dmul_rn(lam, sqrt(Sg[sl::IMG2])) > __dmul_rn(Sg[sl::EPS_BT], sqrt(Sg[sl::R2]));
+    reject = __dmul_rn(lam, sqrt(img2)) > __dmul_rn(eps_bt, sqrt(r2));
   } else if (rule == 3) {  // NAMA simple rule on the certificate's norms
-    reject = __dmul_rn(lam, sqrt(Sg[sl::HR2])) > __dmul_rn(Sg[sl::EPS_BT], sqrt(Sg[sl::RR2]));
+    reject = __dmul_rn(lam, sqrt(hr2)) > __dmul_rn(eps_bt, sqrt(rr2));
   }
   I[il::REJECT] = reject;
-  I[il::CONV] = (s[5] <= Sg[sl::EPS_STOP] || reject) ? 1 : 0;
+  I[il::CONV] = (s[5] <= eps_stop || reject) ? 1 : 0;
 }
 
 // S / I into mapped host memory, sequence word last (all threads of one block)

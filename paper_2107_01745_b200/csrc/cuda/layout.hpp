@@ -125,10 +125,8 @@ struct SweepParams {
   const double* fb_lo;
   const double* fb_hi;
   const double* fb_wg;
-  const int32_t* row_first;  // per node: first stage row and count; per leaf: first terminal row and count
-  const int32_t* row_count;
-  const int32_t* trow_first;
-  const int32_t* trow_count;
+  const int32_t* fb_rows;      // dual rows finished by each CTA: [fb_rows_off[b], fb_rows_off[b + 1])
+  const int32_t* fb_rows_off;  // (the stage and terminal rows of the CTA's forward items)
   double* fb_part;           // [grid][8] per-CTA partial sums
   double* pub_S;             // non-null: the last CTA also publishes S / I (mapped host memory, seq last)
   int* pub_I;

@@ -674,9 +674,10 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
 
 // ---------------------------------------------------------------- fused FB-step finish
 // The dual rows of this CTA's forward items (each row's Hx was written by one
-// of this CTA's teams; visible after the block barrier), one item per thread
-// in list order, then a fixed-order block reduction into this CTA's partial.
-__device__ void fb_epilogue_cta(const SweepParams& P, const Item* items, int K) {
+// of this CTA's teams; visible after the block barrier), listed per CTA by the
+// host (P.fb_rows): one row per thread, so every row's loads are in flight at
+// once, then a fixed-order block reduction into this CTA's partial.
+__device__ void fb_epilogue_cta(const SweepParams& P) {
   __shared__ double red[kThreads / 32][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double lam = P.fb_S[P.fb_state * sl::kStateStride + sl::LAM];
@@ -684,20 +685,11 @@ __device__ void fb_epilogue_cta(const SweepParams& P, const Item* items, int K) 
   const double* y = P.y[0];
   const double* Hx = P.Hx[0];
   double s[6] = {0, 0, 0, 0, 0, 0};
-  auto rows = [&](int lo, int hi) {
-    for (int i = lo; i < hi; ++i)
-      fbrow::fb_row(i, P.fb_kind[i], y[i], Hx[i], P.fb_lo[i], P.fb_hi[i], P.fb_wg[i], lam, gp, 0, P.fb_Hx0,
-                    P.fb_weight, P.fb_z, P.fb_R, P.fb_T, true, s);
-  };
-  for (int k = tid; k < K; k += kThreads) {
-    const Item it = items[k];
-    if (it.pass != 1) continue;
-    const int first = it.first, last = it.first + it.count - 1;
-    if (first > 0) rows(P.row_first[first], P.row_first[last] + P.row_count[last]);  // stage rows
-    if (it.leaf) {  // terminal rows
-      const int a = first - P.first_leaf, z = last - P.first_leaf;
-      rows(P.trow_first[a], P.trow_first[z] + P.trow_count[z]);
-    }
+  const int lo = P.fb_rows_off[blockIdx.x], hi = P.fb_rows_off[blockIdx.x + 1];
+  for (int q = lo + tid; q < hi; q += kThreads) {
+    const int64_t i = P.fb_rows[q];
+    fbrow::fb_row(i, P.fb_kind[i], y[i], Hx[i], P.fb_lo[i], P.fb_hi[i], P.fb_wg[i], lam, gp, 0, P.fb_Hx0,
+                  P.fb_weight, P.fb_z, P.fb_R, P.fb_T, true, s);
   }
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
@@ -1006,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
   // its code made the 2-RHS kernel 10 us slower (258 -> 268 us at C3)
   const bool fb = NRHS == 1 && P.fb_S != nullptr;
   if constexpr (NRHS == 1)
-    if (fb) fb_epilogue_cta(P, items, K);  // this CTA's partial, written by threads < 6 (after a barrier)
+    if (fb) fb_epilogue_cta(P);  // this CTA's partial, written by threads < 6 (after a barrier)
   __shared__ int s_last;
   if (fb) __syncthreads();
   if (tid == 0) {

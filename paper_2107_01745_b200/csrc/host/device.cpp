@@ -1159,22 +1159,32 @@ std::unique_ptr<DevState> dev_create(const Problem& p, const Factor* fptr, int d
     // else: exchange left to the caller (phase API)
   }
 
-  // fused FB-step finish (SweepParams::fb_*): row ranges of nodes and leaves, per-CTA partials
-  {
-    std::vector<int32_t> rf(static_cast<size_t>(n), 0), rc(static_cast<size_t>(n), 0),
-        tf(static_cast<size_t>(std::max(p.L, 1)), 0), tc(static_cast<size_t>(std::max(p.L, 1)), 0);
-    for (int c = 1; c < n; ++c) {
-      rf[c] = p.dual_offset[c];
-      rc[c] = p.stage_rows[c];
+  // fused FB-step finish (SweepParams::fb_*): per CTA, the stage rows of the
+  // nodes of its forward items and the terminal rows of its leaves (each dual
+  // row once over the grid), in item order; per-CTA partials
+  if (d->launches.size() == 1) {
+    const std::vector<int>& off = cta_offs[0];
+    std::vector<int32_t> rows, roff(static_cast<size_t>(G) + 1, 0);
+    rows.reserve(static_cast<size_t>(std::max(D, 0)));
+    for (int gg = 0; gg < G; ++gg) {
+      for (int q = off[gg]; q < off[gg + 1]; ++q) {
+        const Item& it = items[q];
+        if (it.pass != 1) continue;
+        for (int c = it.first; c < it.first + it.count; ++c) {
+          if (c > 0)
+            for (int r = 0; r < p.stage_rows[c]; ++r) rows.push_back(p.dual_offset[c] + r);
+          if (c >= p.first_leaf) {
+            const int l = c - p.first_leaf;
+            for (int r = 0; r < p.terminal_rows[l]; ++r) rows.push_back(p.tdual_offset[l] + r);
+          }
+        }
+      }
+      roff[gg + 1] = static_cast<int32_t>(rows.size());
     }
-    for (int l = 0; l < p.L; ++l) {
-      tf[l] = p.tdual_offset[l];
-      tc[l] = p.terminal_rows[l];
-    }
-    d->row_first = upload(*d, rf);
-    d->row_count = upload(*d, rc);
-    d->trow_first = upload(*d, tf);
-    d->trow_count = upload(*d, tc);
+    if (static_cast<int64_t>(rows.size()) != static_cast<int64_t>(D))
+      fail(SCENOPT_E_ERROR, "dev_create: the forward items do not cover every dual row once");
+    d->fb_rows = upload(*d, rows);
+    d->fb_rows_off = upload(*d, roff);
     d->fb_part = d->alloc<double>(static_cast<size_t>(G) * 8);
   }
   for (int r = 0; r < kMaxRhs; ++r) {
@@ -1384,10 +1394,8 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
     P.fb_lo = d.row_lo;
     P.fb_hi = d.row_hi;
     P.fb_wg = d.row_wg;
-    P.row_first = d.row_first;
-    P.row_count = d.row_count;
-    P.trow_first = d.trow_first;
-    P.trow_count = d.trow_count;
+    P.fb_rows = d.fb_rows;
+    P.fb_rows_off = d.fb_rows_off;
     P.fb_part = d.fb_part;
     P.pub_S = f.pubS;
     P.pub_I = f.pubI;

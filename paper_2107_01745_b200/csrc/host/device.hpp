@@ -84,7 +84,7 @@ struct DevState {
     unsigned seq = 0;
   };
   const FbFuse* fb_next = nullptr;
-  int32_t *row_first = nullptr, *row_count = nullptr, *trow_first = nullptr, *trow_count = nullptr;
+  int32_t *fb_rows = nullptr, *fb_rows_off = nullptr;  // fused FB finish: dual rows per CTA (SweepParams)
   double* fb_part = nullptr;  // [grid][8]
   double* out_hx[kMaxRhs] = {};      // SweepParams::hx / hu of the next launches (mapped host outputs)
   double* out_hu[kMaxRhs] = {};        // flattened forward top (one level after the backward root)

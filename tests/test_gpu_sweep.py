@@ -357,3 +357,25 @@ def test_sweep_geometries_are_bitwise_identical(gpu, monkeypatch, shape):
         assert np.array_equal(a, b)
     monkeypatch.delenv("SCENOPT_SWEEP_PRODUCERS")
     assert so.factor(prob).dev_info()["producer_warps"] == 4  # small trees keep the default geometry
+
+
+def test_large_small_state_tree_takes_six_producers_bitwise(gpu, monkeypatch):
+    """On a bandwidth-bound nx = 10 tree (873,813 nodes, 3.4 GB of packed
+    matrices, items of up to 18 nodes) the default rule picks the
+    six-producer geometry, and its sweeps equal the four-producer
+    geometry's bit for bit (device factor, so no host factor is built)."""
+    prob = so.gen_random_instance(1, 10, 5, 20, [4] * 8)
+    rng = np.random.default_rng(3)
+    y = rng.uniform(-1, 1, prob.dual_dim)
+    out = {}
+    for force in (None, "4"):
+        if force:
+            monkeypatch.setenv("SCENOPT_SWEEP_PRODUCERS", force)
+        cache = so.factor_device(prob)
+        info = cache.dev_info()
+        assert info["producer_warps"] == (4 if force else 6), info["producer_warps"]
+        pts, hs = so.sweep(cache, [y], True)
+        out[force] = (pts[0].x, pts[0].u, hs[0])
+        del cache
+    for a, b in zip(out[None], out["4"]):
+        assert np.array_equal(a, b)

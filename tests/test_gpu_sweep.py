@@ -352,6 +352,10 @@ def test_sweep_geometries_are_bitwise_identical(gpu, monkeypatch, shape):
             res += [pts[0].x, pts[0].u, pts[1].x, pts[1].u, hs[0], hs[1]]
             pts1, hs1 = so.sweep(cache, [y], affine)
             res += [pts1[0].x, pts1[0].u, hs1[0]]
+        for kind in ("minfbe", "nama"):  # the fused FB finish and the 2-RHS sweep in whole solves
+            rep = so.api._solve_direct(kind, prob, cache, so.SolverConfig(nama_parallel_linesearch=kind == "nama"))
+            assert rep.status == "converged"
+            res += [rep.y, rep.x.x, rep.x.u, np.array([rep.iterations, rep.wall_ms * 0])]
         out[p] = res
     for a, b in zip(out["4"], out["6"]):
         assert np.array_equal(a, b)

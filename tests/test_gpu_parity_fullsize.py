@@ -11,6 +11,7 @@ iteration estimate (solve() computes L once and passes lambda0 explicitly,
 solvers.hpp:668-679), so the CPU run spends no time on its own power
 iteration. The CPU side takes ~15 s per test on the GPU box's host.
 
+GPAD is compared the same way at C3 (its fixed step 0.95 / L).
 C4 (NAMA on the 18.35M-variable tree, ~3 min of CPU time) runs when
 SCENOPT_PARITY_C4=1; its committed log is profiles/parity_c4_r02.txt.
 """
@@ -69,6 +70,16 @@ def test_c3_solver_matches_cpu_oracle(gpu, c3, kind):
     par = kind == "nama"
     rep = so.api._solve_direct(kind, prob, cache, so.SolverConfig(lambda0=lam0, nama_parallel_linesearch=par))
     orep = orc.solve_direct(po, ofac, orc.SolverConfig(lambda0=lam0, nama_parallel_linesearch=par), KIND[kind])
+    _compare(prob, rep, orep, 5e-4)
+
+
+def test_c3_gpad_matches_cpu_oracle(gpu, c3):
+    """GPAD (solvers.hpp:498-540, fixed step 0.95/L as solve() uses for it)
+    at C3: 39 iterations on both sides (~11 s of CPU)."""
+    prob, cache, po, ofac, L = c3
+    lam0 = 0.95 / L
+    rep = so.api._solve_direct("gpad", prob, cache, so.SolverConfig(lambda0=lam0))
+    orep = orc.solve_direct(po, ofac, orc.SolverConfig(lambda0=lam0), 2)
     _compare(prob, rep, orep, 5e-4)
 
 

@@ -1530,27 +1530,30 @@ int scenopt_solve(const scenopt_problem* p, const scenopt_solver_config* cfg, in
       return r;
     };
     auto rep = std::make_unique<scenopt_report>();
+    // Without a shared factor the instance is factored on the device (K9,
+    // DESIGN.md §3.3) straight into the sweep layout: at C3 0.4 s for the
+    // handle against 0.75 s of host factor plus 0.6-0.8 s of packing and
+    // upload, all inside wall_ms as in the reference (solvers.hpp:646-717).
     if (!cfg->precondition) {
-      Factor local;
       const Factor* f = shared ? scenopt_factor_ptr(shared) : nullptr;
-      if (!f) {
-        local = factor(prob);
-        f = &local;
-      }
       scenopt_dev h;
-      h.d = dev_create(prob, f, device);
+      h.d = f ? dev_create(prob, f, device) : dev_create_device_factor(prob, device);
       h.init_solver_buffers();
+      const double t1 = now_ms();
       rep->r = run(h, nullptr);
+      const double t2 = now_ms();
       verify(h, rep->r);
+      if (std::getenv("SCN_SOLVE_TIMING"))
+        std::fprintf(stderr, "[scn] solve(): handle %.1f ms, lipschitz + warm start + solver %.1f ms, verify %.1f ms\n",
+                     t1 - t0, t2 - t1, now_ms() - t2);
     } else {
       const Problem scaled = precondition(prob);
-      const Factor fs = factor(scaled);
       const std::vector<double> roots = probability_roots(prob);
       std::vector<double> weight(roots.size());
       for (size_t i = 0; i < roots.size(); ++i) weight[i] = 1.0 / roots[i];
       {
         scenopt_dev h;
-        h.d = dev_create(scaled, &fs, device);
+        h.d = dev_create_device_factor(scaled, device);
         h.init_solver_buffers();
         SCN_CUDA(cudaMemcpy(h.w->weight, weight.data(), weight.size() * sizeof(double), cudaMemcpyHostToDevice));
         rep->r = run(h, h.w->weight);

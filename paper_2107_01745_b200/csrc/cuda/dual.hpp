@@ -30,6 +30,12 @@ constexpr int CERT_S = 120;  // sharded certificate: coefficient totals [120, 13
 constexpr int kScalars = 192;
 }  // namespace sl
 // Int block slots.
+// Host publication of the scalar block (mapped pinned memory), in the manner
+// of NCCL's low-latency protocol: every 8-byte word carries 4 bytes of data in
+// its low half and the publish sequence number in its high half, written as
+// one store, so the host validates each word by its own flag and the device
+// needs no system-scope fence before it can move on. Layout: S as two words
+// per double (low, high 32 bits), then I one word per int.
 namespace il {
 constexpr int LB_COUNT = 0, LB_PUSHED = 1, SETTLED = 2, PZERO = 3;
 constexpr int PDONE = 4, PROUNDS = 5, PMAX = 6;  // batched power iteration: sticky stop flag, rounds run, cap
@@ -40,6 +46,7 @@ constexpr int CSTATE = 101;  // sharded certificate: state after phase k at CSTA
 constexpr int CKSTAR = 105;  // sharded certificate: accepted trial between phases
 constexpr int kInts = 128;
 }  // namespace il
+constexpr int kPubWords = 2 * sl::kScalars + il::kInts;
 
 // Per-dual-row nonsmooth data (prox.hpp:15-52 flattened).
 struct RowG {
@@ -58,11 +65,9 @@ struct DualCtx {
   double* part;    // partial sums [2][64][nblk]
   unsigned* bar;   // grid barrier {count, generation}
   const int* skip = nullptr;  // L-BFGS kernels: non-null and *skip != 0 -> return at once (speculation)
-  // fb_finish: when pubS is set, block 0 also publishes S / I into mapped
-  // host memory and writes seq last (publish_kernel's protocol, one launch fewer)
-  double* pubS = nullptr;
-  int* pubI = nullptr;
-  unsigned* pubSeq = nullptr;
+  // fb_finish: when pub is set, block 0 also publishes S / I into mapped
+  // host memory (publish_kernel's protocol, one launch fewer)
+  unsigned long long* pub = nullptr;
   unsigned seq = 0;
   // Subtree-sharded handles. Reductions count only the rows
   // with cnt[i] != 0 (this rank's own rows; the replicated top on rank 0),
@@ -87,10 +92,9 @@ void dual_allgather(void* xc, const double* send, double* recv, size_t n, cudaSt
 cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, const double* Hx,
                         const double* Hx0, const double* weight, double* z, double* R, double* T,
                         cudaStream_t st);
+cudaError_t k_publish(const double* S, const int* I, unsigned long long* pub_mapped, unsigned seq, cudaStream_t st);
 // MINFBE fbe_grad epilogue (fbe.hpp:89-94): grad = R + lam HR, and the simple
 // backtracking norms ||(grad - R)/lam||^2, ||R||^2 (solvers.hpp:215-222, 279-302).
-cudaError_t k_publish(const double* S, const int* I, double* hS_mapped, int* hI_mapped, unsigned* seq_mapped,
-                      unsigned seq, cudaStream_t st);
 cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const double* HR, double* grad,
                        cudaStream_t st);
 // L-BFGS (lbfgs.hpp:33-62): optional push of (a - b, cc - dd) with scale_ref

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kThreads) fb_finish_kernel(DualCtx c, int st, 
   if (!xreduce<6, false, 5>(c, ph, s)) return;  // one barrier: five sums and the max
   if (blockIdx.x == 0 && threadIdx.x == 0) fbrow::fb_finalize(c.S, c.I, st, mode, s);
   // thread 0's S / I writes are visible to the block after publish_block's barrier
-  if (c.pubS && blockIdx.x == 0) fbrow::publish_block(c.S, c.I, c.pubS, c.pubI, c.pubSeq, c.seq);
+  if (c.pub && blockIdx.x == 0) fbrow::publish_block(c.S, c.I, c.pub, c.seq);
 }
 
 // ---------------------------------------------------------------- K7
@@ -1263,23 +1263,14 @@ cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, 
   return phased(reinterpret_cast<const void*>(fb_finish_kernel), cc, args, st);
 }
 
-// Scalar block -> mapped pinned host memory in one launch (the host waits on
-// an event instead of two D2H copies)
-// A sequence number written last (after a system-scope fence) tells a host
-// spinning on the mapped word that the block is complete.
-__global__ void publish_kernel(const double* S, const int* I, double* hS, int* hI, unsigned* hseq, unsigned seq) {
-  for (int t = threadIdx.x; t < sl::kScalars; t += blockDim.x) hS[t] = S[t];
-  for (int t = threadIdx.x; t < il::kInts; t += blockDim.x) hI[t] = I[t];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    *reinterpret_cast<volatile unsigned*>(hseq) = seq;
-  }
+// Scalar block -> mapped pinned host memory in one launch, as flagged words
+// (dual.hpp kPubWords): the host spins on the words themselves.
+__global__ void publish_kernel(const double* S, const int* I, unsigned long long* pub, unsigned seq) {
+  fbrow::publish_block(S, I, pub, seq);
 }
 
-cudaError_t k_publish(const double* S, const int* I, double* hS_mapped, int* hI_mapped, unsigned* seq_mapped,
-                      unsigned seq, cudaStream_t st) {
-  publish_kernel<<<1, 256, 0, st>>>(S, I, hS_mapped, hI_mapped, seq_mapped, seq);
+cudaError_t k_publish(const double* S, const int* I, unsigned long long* pub_mapped, unsigned seq, cudaStream_t st) {
+  publish_kernel<<<1, 256, 0, st>>>(S, I, pub_mapped, seq);
   return cudaGetLastError();
 }
 

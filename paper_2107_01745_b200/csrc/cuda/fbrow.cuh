@@ -84,17 +84,20 @@ __device__ __forceinline__ void fb_finalize(double* Sg, int* I, int state, int m
   I[il::CONV] = (s[5] <= eps_stop || reject) ? 1 : 0;
 }
 
-// S / I into mapped host memory, sequence word last (all threads of one block)
-__device__ __forceinline__ void publish_block(const double* S, const int* I, double* pubS, int* pubI,
-                                              unsigned* pubSeq, unsigned seq) {
+// S / I into mapped host memory as flagged words (dual.hpp kPubWords; all
+// threads of one block). The barrier makes thread 0's scalar writes visible
+// to the block; no fence follows: each word carries its own flag.
+__device__ __forceinline__ void publish_block(const double* S, const int* I, unsigned long long* pub, unsigned seq) {
   __syncthreads();
-  for (int t = threadIdx.x; t < sl::kScalars; t += blockDim.x) pubS[t] = S[t];
-  for (int t = threadIdx.x; t < il::kInts; t += blockDim.x) pubI[t] = I[t];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    *reinterpret_cast<volatile unsigned*>(pubSeq) = seq;
+  volatile unsigned long long* w = pub;
+  const unsigned long long f = static_cast<unsigned long long>(seq) << 32;
+  for (int t = threadIdx.x; t < sl::kScalars; t += blockDim.x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(S[t]));
+    w[2 * t] = f | (b & 0xffffffffull);
+    w[2 * t + 1] = f | (b >> 32);
   }
+  for (int t = threadIdx.x; t < il::kInts; t += blockDim.x)
+    w[2 * sl::kScalars + t] = f | static_cast<unsigned>(I[t]);
 }
 
 }  // namespace fbrow

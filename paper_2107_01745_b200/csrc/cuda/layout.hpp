@@ -128,9 +128,7 @@ struct SweepParams {
   const int32_t* fb_rows;      // dual rows finished by each CTA: [fb_rows_off[b], fb_rows_off[b + 1])
   const int32_t* fb_rows_off;  // (the stage and terminal rows of the CTA's forward items)
   double* fb_part;           // [grid][8] per-CTA partial sums
-  double* pub_S;             // non-null: the last CTA also publishes S / I (mapped host memory, seq last)
-  int* pub_I;
-  unsigned* pub_seq;
+  unsigned long long* pub;   // non-null: the last CTA also publishes S / I (mapped flagged words, dual.hpp)
   unsigned seq;
 };
 

@@ -734,7 +734,7 @@ __device__ void fb_epilogue_last(const SweepParams& P) {
     const double s[6] = {tot[0], tot[1], tot[2], tot[3], tot[4], tot[5]};
     fbrow::fb_finalize(P.fb_S, P.fb_I, P.fb_state, 0, s);
   }
-  if (P.pub_S) fbrow::publish_block(P.fb_S, P.fb_I, P.pub_S, P.pub_I, P.pub_seq, P.seq);
+  if (P.pub) fbrow::publish_block(P.fb_S, P.fb_I, P.pub, P.seq);
 }
 
 // MODE bits (one instantiation per combination, so the common layout's

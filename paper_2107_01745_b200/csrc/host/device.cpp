@@ -1397,9 +1397,7 @@ SweepParams sweep_params(DevState& d, int nrhs, bool affine, const double* const
     P.fb_rows = d.fb_rows;
     P.fb_rows_off = d.fb_rows_off;
     P.fb_part = d.fb_part;
-    P.pub_S = f.pubS;
-    P.pub_I = f.pubI;
-    P.pub_seq = f.pubSeq;
+    P.pub = f.pub;
     P.seq = f.seq;
   }
   for (int r = 0; r < nrhs; ++r) {

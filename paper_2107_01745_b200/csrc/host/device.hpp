@@ -78,9 +78,7 @@ struct DevState {
     int state = 0;
     const double *Hx0 = nullptr, *weight = nullptr;
     double *z = nullptr, *R = nullptr, *T = nullptr;
-    double* pubS = nullptr;
-    int* pubI = nullptr;
-    unsigned* pubSeq = nullptr;
+    unsigned long long* pub = nullptr;  // mapped flagged words (dual.hpp kPubWords)
     unsigned seq = 0;
   };
   const FbFuse* fb_next = nullptr;

@@ -32,13 +32,10 @@ struct scenopt_dev::Work {
   unsigned* bar = nullptr;
   double* hS = nullptr;  // pinned mirrors
   int* hI = nullptr;
-  // mapped pinned copy of S / I written by k_publish; pubEv marks its completion
-  double* pS = nullptr;
-  int* pI = nullptr;
-  double* dpS = nullptr;
-  int* dpI = nullptr;
-  unsigned* pSeq = nullptr;  // mapped: sequence number of the last completed publish
-  unsigned* dpSeq = nullptr;
+  // mapped pinned flagged words of S / I written by k_publish or a fused FB
+  // finish (dual.hpp kPubWords); seq is the number of the last publish issued
+  unsigned long long* pLL = nullptr;
+  unsigned long long* dpLL = nullptr;
   unsigned seq = 0;
   cudaEvent_t pubEv = nullptr;
   // pinned staging words of asynchronous scalar writes; a word is reused only
@@ -91,9 +88,7 @@ scenopt_dev::~scenopt_dev() {
     if (w->hI) cudaFreeHost(w->hI);
     if (w->hRing) cudaFreeHost(w->hRing);
     if (w->hIRing) cudaFreeHost(w->hIRing);
-    if (w->pS) cudaFreeHost(w->pS);
-    if (w->pI) cudaFreeHost(w->pI);
-    if (w->pSeq) cudaFreeHost(w->pSeq);
+    if (w->pLL) cudaFreeHost(w->pLL);
     if (w->pubEv) cudaEventDestroy(w->pubEv);
   }
 }
@@ -117,13 +112,9 @@ void scenopt_dev::init_solver_buffers() {
   SCN_CUDA(cudaMallocHost(&k.hI, il::kInts * sizeof(int)));
   SCN_CUDA(cudaMallocHost(&k.hRing, scenopt_dev::Work::kRing * sizeof(double)));
   SCN_CUDA(cudaMallocHost(&k.hIRing, scenopt_dev::Work::kRing * sizeof(int)));
-  SCN_CUDA(cudaHostAlloc(&k.pS, sl::kScalars * sizeof(double), cudaHostAllocMapped));
-  SCN_CUDA(cudaHostAlloc(&k.pI, il::kInts * sizeof(int), cudaHostAllocMapped));
-  SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpS), k.pS, 0));
-  SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpI), k.pI, 0));
-  SCN_CUDA(cudaHostAlloc(&k.pSeq, sizeof(unsigned), cudaHostAllocMapped));
-  *k.pSeq = 0;
-  SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpSeq), k.pSeq, 0));
+  SCN_CUDA(cudaHostAlloc(&k.pLL, kPubWords * sizeof(unsigned long long), cudaHostAllocMapped));
+  std::memset(k.pLL, 0, kPubWords * sizeof(unsigned long long));  // flag 0: no publish yet
+  SCN_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&k.dpLL), k.pLL, 0));
   SCN_CUDA(cudaEventCreateWithFlags(&k.pubEv, cudaEventDisableTiming));
   const size_t D = static_cast<size_t>(k.D), nxn = static_cast<size_t>(L.nx) * L.n,
                nuf = static_cast<size_t>(L.nu) * std::max(L.first_leaf, 1);
@@ -376,19 +367,27 @@ struct Engine {
       cudaEventCreate(&pub_pre);
       cudaEventRecord(pub_pre, st);
     }
-    SCN_CUDA(k_publish(k.S, k.I, k.dpS, k.dpI, k.dpSeq, ++k.seq, st));
+    SCN_CUDA(k_publish(k.S, k.I, k.dpLL, ++k.seq, st));
     mark("read.copy");
   }
-  // Spin on the mapped sequence word (no driver call, no sleep / wake-up);
-  // every 4096 polls the stream is queried so a device fault cannot hang it.
+  // Spin on the mapped flagged words (no driver call, no sleep / wake-up):
+  // word by word until each carries this publish's flag, then decode them
+  // into the host mirrors. Every 4096 polls the stream is queried so a device
+  // fault cannot hang it.
   void wait_published(bool full) {
     const double h0 = timer.on ? now_ms() : 0.0;
-    const volatile unsigned* seqp = k.pSeq;
-    for (unsigned spins = 1; *seqp != k.seq; ++spins) {
-      if ((spins & 4095u) == 0) {
+    const volatile unsigned long long* w = k.pLL;
+    const unsigned long long want = k.seq;
+    unsigned spins = 0;
+    for (int i = 0; i < kPubWords;) {
+      if ((w[i] >> 32) == want) {
+        ++i;
+        continue;
+      }
+      if ((++spins & 4095u) == 0) {
         const cudaError_t q = cudaStreamQuery(st);
         if (q != cudaSuccess && q != cudaErrorNotReady) SCN_CUDA(q);
-        if (q == cudaSuccess && !full && *seqp != k.seq) {  // drained without the word: fall back
+        if (q == cudaSuccess && !full && (w[i] >> 32) != want) {  // drained without the words: fall back
           SCN_CUDA(cudaStreamSynchronize(st));
           break;
         }
@@ -397,8 +396,11 @@ struct Engine {
     std::atomic_thread_fence(std::memory_order_acquire);
     if (full) k.ring_next = k.iring_next = 0;  // publish ran after every earlier copy: all staging words consumed
     if (timer.on) timer.host_sync_ms += now_ms() - h0;
-    std::memcpy(k.hS, k.pS, sl::kScalars * sizeof(double));
-    std::memcpy(k.hI, k.pI, il::kInts * sizeof(int));
+    for (int t = 0; t < sl::kScalars; ++t) {
+      const unsigned long long b = (w[2 * t] & 0xffffffffull) | ((w[2 * t + 1] & 0xffffffffull) << 32);
+      std::memcpy(&k.hS[t], &b, sizeof(double));
+    }
+    for (int t = 0; t < il::kInts; ++t) k.hI[t] = static_cast<int>(static_cast<unsigned>(w[2 * sl::kScalars + t]));
     if (timer.on) {  // GPU-side cost of this host round trip: copy + wake-up + re-enqueue
       cudaEvent_t post;
       cudaEventCreate(&post);
@@ -577,9 +579,7 @@ struct Engine {
       f.R = k.R[s];
       f.T = k.T[s];
       if (publish_after) {
-        f.pubS = k.dpS;
-        f.pubI = k.dpI;
-        f.pubSeq = k.dpSeq;
+        f.pub = k.dpLL;
         f.seq = ++k.seq;
       }
       struct Reset {
@@ -592,9 +592,7 @@ struct Engine {
       sweep1(true, k.y[s], k.x[s], k.u[s], k.Hx[s]);
       DualCtx c = ctx();
       if (publish_after) {
-        c.pubS = k.dpS;
-        c.pubI = k.dpI;
-        c.pubSeq = k.dpSeq;
+        c.pub = k.dpLL;
         c.seq = ++k.seq;
       }
       SCN_CUDA(k_fb_finish(c, s, 0, k.y[s], k.Hx[s], k.Hx0, weight, k.z[s], k.R[s], k.T[s], st));

@@ -61,5 +61,4 @@ struct scenopt_dev {
   void out_copy(double* dst, const double* dev_src, size_t count, int flags);
   void sync();
   static double* mapped(double* p);  // device address of a pinned host buffer, or nullptr
-  bool zero_copy_ok(int nrhs, double* const* x, double* const* u);
 };

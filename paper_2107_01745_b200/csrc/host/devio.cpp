@@ -34,7 +34,16 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
   double* ud[kMaxRhs] = {nullptr, nullptr};
   double* hd[kMaxRhs] = {nullptr, nullptr};
   const bool host = (flags & SCENOPT_HOST_IO) != 0;
-  const bool mapped_y = host && (x || u) && !d->sharded() && zero_copy_ok(nrhs, x, u);
+  // device addresses of pinned host outputs, resolved once per call (nullptr:
+  // pageable); zero copy needs every requested output pinned
+  double* mx[kMaxRhs] = {nullptr, nullptr};
+  double* mu[kMaxRhs] = {nullptr, nullptr};
+  bool zero_copy = host && (x || u) && !d->sharded();
+  for (int r = 0; zero_copy && r < nrhs; ++r) {
+    if (x && x[r]) zero_copy = (mx[r] = mapped(x[r])) != nullptr;
+    if (zero_copy && u && u[r]) zero_copy = (mu[r] = mapped(u[r])) != nullptr;
+  }
+  const bool mapped_y = zero_copy;
   for (int r = 0; r < nrhs; ++r) {
     // a pinned dual input can be read in place by the backward's staging copies
     double* m = mapped_y && y[r] ? mapped(const_cast<double*>(y[r])) : nullptr;
@@ -45,11 +54,10 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
       hd[r] = Hx ? Hx[r] : nullptr;
     }
   }
-  const bool want_primal = (x != nullptr) || (u != nullptr);
   // Mapped (pinned) host outputs: the forward pass writes x / u to the
   // caller's buffers over PCIe as it computes them, overlapping the transfer
   // with the sweep; pageable buffers take the copy after the sweep.
-  if (host && want_primal && zero_copy_ok(nrhs, x, u)) {
+  if (zero_copy) {
     struct Reset {
       DevState& d;
       ~Reset() {
@@ -57,8 +65,8 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
       }
     } reset{*d};
     for (int r = 0; r < nrhs; ++r) {
-      d->out_hx[r] = (x && x[r]) ? mapped(x[r]) : nullptr;
-      d->out_hu[r] = (u && u[r]) ? mapped(u[r]) : nullptr;
+      d->out_hx[r] = mx[r];
+      d->out_hu[r] = mu[r];
     }
     dev_sweep(*d, nrhs, affine, yd, xd, ud, hd);
     for (int r = 0; r < nrhs; ++r)
@@ -89,13 +97,4 @@ double* scenopt_dev::mapped(double* p) {
     return nullptr;
   }
   return a.type == cudaMemoryTypeHost ? static_cast<double*>(a.devicePointer) : nullptr;
-}
-
-bool scenopt_dev::zero_copy_ok(int nrhs, double* const* x, double* const* u) {
-  if (d->sharded()) return false;
-  for (int r = 0; r < nrhs; ++r) {
-    if (x && x[r] && !mapped(x[r])) return false;
-    if (u && u[r] && !mapped(u[r])) return false;
-  }
-  return true;
 }

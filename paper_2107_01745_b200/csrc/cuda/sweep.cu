@@ -575,12 +575,18 @@ struct FwPhaseA {
 };
 
 // phase B: interior u_c = u_off_c + K_c x_c ; leaf z_N,c = F_N x_c.
-template <int NRHS>
+// Host-output kernels (HOST) also leave u in the staged u_off entry it was
+// computed from (each task reads and overwrites its own entry), so whole u
+// rows can go to the caller's mapped buffer after the phase (16-byte stores).
+#ifndef SCN_HOST_U_ROWS
+#define SCN_HOST_U_ROWS 1
+#endif
+template <int NRHS, bool HOST = false>
 struct FwPhaseB {
   const SweepParams& P;
   const NodeMeta* meta;
   const double* slot;
-  const double* UO;
+  double* UO;
   const double* xbuf;
   int nx, nu, Vp, nxp, ncols, v1nu, leaf, root, single;
   template <int S>
@@ -606,7 +612,12 @@ struct FwPhaseB {
         } else {
           const double uv = UO[r * v1nu + ni * nu + j] + acc[r];
           P.u[r][static_cast<int64_t>(mc.c) * nu + j] = uv;
-          if (P.hu[r]) P.hu[r][static_cast<int64_t>(mc.c) * nu + j] = uv;
+          if constexpr (HOST) {
+            if (SCN_HOST_U_ROWS)
+              UO[r * v1nu + ni * nu + j] = uv;  // whole rows leave after the phase (consume_forward)
+            else if (P.hu[r])
+              P.hu[r][static_cast<int64_t>(mc.c) * nu + j] = uv;
+          }
         }
       }
     }
@@ -626,7 +637,7 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
   const int cstride = flat ? flat_len(it.direct >> 8, nu) : Vp;  // phase-A column length
   const int tot = flat ? cstride : it.v0_n * Vp;
   const double* PV = st;
-  const double* UO = st + NRHS * tot;
+  double* UO = const_cast<double*>(st) + NRHS * tot;  // host-output kernels leave u here (FwPhaseB)
   const double* AF = st + NRHS * (tot + it.v1_n * nu);
   PROF_T0();
   if (root) {  // x_0 = p (affine) or 0
@@ -666,9 +677,28 @@ __device__ void consume_forward(const SweepParams& P, const Item& it, const doub
       }
     }
   }
-  const FwPhaseB<NRHS> body{P, meta, mat, UO, xbuf, nx, nu, cstride, nxp, leaf ? mNmax : nu, it.v1_n * nu,
-                            leaf ? 1 : 0, root ? 1 : 0, cnt == 1 ? 1 : 0};
+  const FwPhaseB<NRHS, HOST> body{P,  meta, mat, UO, xbuf, nx, nu, cstride, nxp, leaf ? mNmax : nu, it.v1_n * nu,
+                                  leaf ? 1 : 0, root ? 1 : 0, cnt == 1 ? 1 : 0};
   for_tasks(cnt * (leaf ? mNmax : nu), ttid, body);
+  if constexpr (HOST)
+  if (SCN_HOST_U_ROWS && !leaf && (P.hu[0] || (NRHS > 1 && P.hu[NRHS - 1]))) {
+    team_sync(team);  // every u of the item is in UO
+    const int v1nu = it.v1_n * nu;
+    if ((nu & 1) == 0) {
+      const int n2 = nu >> 1;
+      for (int idx = ttid; idx < NRHS * cnt * n2; idx += kTeam) {
+        const int r = idx / (cnt * n2), rem = idx - r * cnt * n2, ni = rem / n2, k = rem - ni * n2;
+        if (P.hu[r])
+          reinterpret_cast<double2*>(P.hu[r] + static_cast<int64_t>(meta[ni].c) * nu)[k] =
+              *reinterpret_cast<const double2*>(UO + r * v1nu + ni * nu + 2 * k);
+      }
+    } else {
+      for (int idx = ttid; idx < NRHS * cnt * nu; idx += kTeam) {
+        const int r = idx / (cnt * nu), rem = idx - r * cnt * nu, ni = rem / nu, k = rem - ni * nu;
+        if (P.hu[r]) P.hu[r][static_cast<int64_t>(meta[ni].c) * nu + k] = UO[r * v1nu + ni * nu + k];
+      }
+    }
+  }
   if (ttid == 0) PROF_T1(13);
 }
 

@@ -1,6 +1,7 @@
 // SPDX-License-Identifier: MIT
 // Host/device I/O helpers of the scenopt_dev handle.
 #include <algorithm>
+#include <cstdint>
 
 #include "capi_internal.hpp"
 
@@ -35,13 +36,15 @@ void scenopt_dev::sweep(int nrhs, bool affine, const double* const* y, double* c
   double* hd[kMaxRhs] = {nullptr, nullptr};
   const bool host = (flags & SCENOPT_HOST_IO) != 0;
   // device addresses of pinned host outputs, resolved once per call (nullptr:
-  // pageable); zero copy needs every requested output pinned
+  // pageable); zero copy needs every requested output pinned and 16-byte
+  // aligned (the forward pass writes whole rows with 16-byte stores)
   double* mx[kMaxRhs] = {nullptr, nullptr};
   double* mu[kMaxRhs] = {nullptr, nullptr};
+  auto usable = [](double* m) { return m != nullptr && (reinterpret_cast<uintptr_t>(m) & 15u) == 0; };
   bool zero_copy = host && (x || u) && !d->sharded();
   for (int r = 0; zero_copy && r < nrhs; ++r) {
-    if (x && x[r]) zero_copy = (mx[r] = mapped(x[r])) != nullptr;
-    if (zero_copy && u && u[r]) zero_copy = (mu[r] = mapped(u[r])) != nullptr;
+    if (x && x[r]) zero_copy = usable(mx[r] = mapped(x[r]));
+    if (zero_copy && u && u[r]) zero_copy = usable(mu[r] = mapped(u[r]));
   }
   const bool mapped_y = zero_copy;
   for (int r = 0; r < nrhs; ++r) {

@@ -241,6 +241,38 @@ def test_pinned_host_outputs_match_pageable_and_stay_in_bounds(gpu):
         assert np.array_equal(us[guard:guard + nu * F], ref.u.ravel(order="F"))
 
 
+@pytest.mark.parametrize("shift", [1, 2])
+def test_pinned_outputs_of_any_alignment(gpu, shift):
+    """The forward pass writes mapped x / u rows with 16-byte stores, so zero
+    copy needs 16-byte-aligned buffers: a pinned buffer shifted by one double
+    (8-byte aligned) takes the copy path instead; both give the pageable
+    path's bits and stay inside their buffers."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2107_01745_b200 import _native as N
+
+    prob = so.gen_random_instance(2, 12, 6, 9, [3, 3, 2])
+    cache = so.factor(prob)
+    y = np.random.default_rng(4).uniform(-1, 1, prob.dual_dim)
+    ref = so.dual_grad(cache, prob, y)
+    nx, nu, n, F = prob.nx, prob.nu, prob.num_nodes(), prob.first_leaf
+    guard = 64
+    P = C.POINTER(C.c_double)
+    xb = torch.full((nx * n + 2 * guard + 2,), 7.25, dtype=torch.float64).pin_memory()
+    ub = torch.full((nu * F + 2 * guard + 2,), 7.25, dtype=torch.float64).pin_memory()
+    yb = torch.from_numpy(y.copy()).pin_memory()
+    off = guard + shift
+    so.api.check(N.lib().scenopt_dual_grad(cache.device(), C.cast(yb.data_ptr(), P),
+                                           C.cast(xb.data_ptr() + 8 * off, P), C.cast(ub.data_ptr() + 8 * off, P), 1))
+    xs, us = xb.numpy(), ub.numpy()
+    assert np.all(xs[:off] == 7.25) and np.all(xs[off + nx * n:] == 7.25)
+    assert np.all(us[:off] == 7.25) and np.all(us[off + nu * F:] == 7.25)
+    assert np.array_equal(xs[off:off + nx * n], ref.x.ravel(order="F"))
+    assert np.array_equal(us[off:off + nu * F], ref.u.ravel(order="F"))
+
+
 @pytest.mark.parametrize("flat", ["1", "0"])
 def test_flattened_forward_top_matches_oracle_on_c3(gpu, monkeypatch, flat):
     """The forward top above the cut (stages 1..3 at C3) computed in one level

@@ -270,8 +270,12 @@ __device__ __forceinline__ bool flags_ready(const unsigned* flags, const Item& i
 //       AFF at NRHS*(v0n*Vp + v1n*nu)  (count*nx)
 // Issued as asynchronous 8-byte copies (LDGSTS) program-ordered after the
 // acquire that observed this item's flags (ld.acquire.gpu also invalidates
-// L1), so they read the published values.
-template <int NRHS, int nt = 32>
+// L1), so they read the published values. PART: 3 stages everything; the
+// host-output kernels split a backward item into 1 (the y rows and affine
+// terms, which no item produces, issued before the dependency wait so their
+// PCIe reads from the caller's pinned y overlap it) and 2 (the children's
+// contributions; a forward item stages everything as 2).
+template <int NRHS, int nt = 32, int PART = 3>
 __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, int lane) {
   const int nx = P.nx, nu = P.nu, W = nx + nu, Vp = P.Vp;
   if (it.pass == 0) {
@@ -280,19 +284,22 @@ __device__ void stage_issue(const SweepParams& P, const Item& it, double* st, in
     for (int r = 0; r < NRHS; ++r) {
       const double* ys = P.y[r] + it.v0_lo;
       double* yd = st + r * it.v0_n;
-      for (int i = lane; i < it.v0_n; i += nt) cp_async8(yd + i, ys + i);
-      if (!(it.direct & kDirectContrib)) {
+      if (PART & 1)
+        for (int i = lane; i < it.v0_n; i += nt) cp_async8(yd + i, ys + i);
+      if ((PART & 2) && !(it.direct & kDirectContrib)) {
         const double* cs = P.contrib[r] + static_cast<int64_t>(it.v1_lo) * W;
         double* cd = st + NRHS * it.v0_n + r * nc;
         for (int i = lane; i < nc; i += nt) cp_async8(cd + i, cs + i);
       }
     }
-    if (P.affine) {
+    if ((PART & 1) && P.affine) {
       const int na = it.count * W;
       const double* as = P.aff_bw + static_cast<int64_t>(it.first) * W;
       double* ad = st + NRHS * (it.v0_n + ((it.direct & kDirectContrib) ? 0 : nc));
       for (int i = lane; i < na; i += nt) cp_async8(ad + i, as + i);
     }
+  } else if (!(PART & 2)) {
+    return;
   } else if (it.direct & kFlatTop) {
     // flattened top: PV_r = [u_off(root); u_off(a_1); u_off(a_2); 0-pad] shared by the
     // item's siblings, then UO_r (own u_off), AFX (a'), AFH (stage-row constants)
@@ -844,6 +851,11 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 #ifdef SCN_SWEEP_PROFILE
       if (g_trace && lane == 0) g_trace[12LL * (P.cta_off[blockIdx.x] + P.items_base + k) + 8] = static_cast<long long>(gtimer());
 #endif
+      // host-output kernels: a backward item's y rows (the caller's pinned
+      // memory, over PCIe) and affine terms go out before the dependency wait
+      constexpr bool kSplitStage = (MODE & kModeHostOut) != 0 && !kConsumerStage;
+      if constexpr (kSplitStage)
+        if (it.pass == 0) stage_issue<NRHS, 32, 1>(P, it, stages + static_cast<int64_t>(q) * P.stage_doubles, lane);
       if (!DBG(1)) {
         if (it.ldep >= 0)
           while (ld_acquire_cta(&s_retired) <= it.ldep) __nanosleep(16);
@@ -854,7 +866,11 @@ __global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const SweepParams P,
 #ifdef SCN_SWEEP_PROFILE
       if (g_trace && lane == 0) g_trace[12LL * (P.cta_off[blockIdx.x] + P.items_base + k) + 9] = static_cast<long long>(gtimer());
 #endif
-      if (!kConsumerStage) stage_issue<NRHS>(P, it, stages + static_cast<int64_t>(q) * P.stage_doubles, lane);
+      if constexpr (kSplitStage) {
+        stage_issue<NRHS, 32, 2>(P, it, stages + static_cast<int64_t>(q) * P.stage_doubles, lane);
+      } else if (!kConsumerStage) {
+        stage_issue<NRHS>(P, it, stages + static_cast<int64_t>(q) * P.stage_doubles, lane);
+      }
       cp_async_wait_all();
       __syncwarp();
 #ifdef SCN_SWEEP_PROFILE

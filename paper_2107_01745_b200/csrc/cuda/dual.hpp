@@ -93,6 +93,23 @@ cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, 
                         const double* Hx0, const double* weight, double* z, double* R, double* T,
                         cudaStream_t st);
 cudaError_t k_publish(const double* S, const int* I, unsigned long long* pub_mapped, unsigned seq, cudaStream_t st);
+// Sharded sweep exchange (device.cpp phase_a / phase_b). Per right-hand side
+// the exchange buffer is [ns_w contributions of the shard-stage nodes | nys
+// dual rows of those nodes]. Pack (after launch A): this rank's own entries,
+// zero elsewhere, ready for the sum-allreduce. Unpack (before launch B): the
+// summed contributions into the contribution array, and launch B's dual input
+// = the top rows of y followed by the summed shard-stage rows.
+struct ExchangeDims {
+  int64_t ns_w, nys, xbuf_rhs, contrib_off, dual_top;
+  int64_t own_c_lo, own_c_hi;  // this rank's contributions, buffer coordinates
+  int64_t own_y_lo, own_y_hi;  // this rank's shard-stage dual rows, y coordinates
+  int nrhs;
+  double* contrib[2];
+  const double* y[2];
+  double* ycomp[2];
+};
+cudaError_t k_exchange_pack(const ExchangeDims& e, double* xbuf, cudaStream_t st);
+cudaError_t k_exchange_unpack(const ExchangeDims& e, const double* xbuf, cudaStream_t st);
 // MINFBE fbe_grad epilogue (fbe.hpp:89-94): grad = R + lam HR, and the simple
 // backtracking norms ||(grad - R)/lam||^2, ||R||^2 (solvers.hpp:215-222, 279-302).
 cudaError_t k_fbe_grad(const DualCtx& c, int state, const double* R, const double* HR, double* grad,

@@ -12,6 +12,7 @@
 // trip.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -1267,6 +1268,52 @@ cudaError_t k_fb_finish(const DualCtx& c, int state, int mode, const double* y, 
 // (dual.hpp kPubWords): the host spins on the words themselves.
 __global__ void publish_kernel(const double* S, const int* I, unsigned long long* pub, unsigned seq) {
   fbrow::publish_block(S, I, pub, seq);
+}
+
+namespace {
+__global__ void exchange_pack_kernel(ExchangeDims e, double* xbuf) {
+  const int64_t per = e.xbuf_rhs, total = e.nrhs * per;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx / per);
+    const int64_t i = idx - r * per;
+    double v = 0.0;
+    if (i < e.ns_w) {
+      if (i >= e.own_c_lo && i < e.own_c_hi) v = e.contrib[r][e.contrib_off + i];
+    } else if (i < e.ns_w + e.nys) {
+      const int64_t row = e.dual_top + (i - e.ns_w);
+      if (row >= e.own_y_lo && row < e.own_y_hi) v = e.y[r][row];
+    }
+    xbuf[idx] = v;
+  }
+}
+__global__ void exchange_unpack_kernel(ExchangeDims e, const double* xbuf) {
+  const int64_t per = e.ns_w + e.dual_top + e.nys, total = e.nrhs * per;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(idx / per);
+    const int64_t i = idx - r * per;
+    const double* xb = xbuf + r * e.xbuf_rhs;
+    if (i < e.ns_w)
+      e.contrib[r][e.contrib_off + i] = xb[i];
+    else if (i < e.ns_w + e.dual_top)
+      e.ycomp[r][i - e.ns_w] = e.y[r][i - e.ns_w];
+    else
+      e.ycomp[r][i - e.ns_w] = xb[e.ns_w + (i - e.ns_w - e.dual_top)];
+  }
+}
+int exchange_blocks(int64_t n) { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 1184)); }
+}  // namespace
+
+cudaError_t k_exchange_pack(const ExchangeDims& e, double* xbuf, cudaStream_t st) {
+  const int64_t n = e.nrhs * e.xbuf_rhs;
+  if (n > 0) exchange_pack_kernel<<<exchange_blocks(n), 256, 0, st>>>(e, xbuf);
+  return cudaGetLastError();
+}
+cudaError_t k_exchange_unpack(const ExchangeDims& e, const double* xbuf, cudaStream_t st) {
+  const int64_t n = e.nrhs * (e.ns_w + e.dual_top + e.nys);
+  if (n > 0) exchange_unpack_kernel<<<exchange_blocks(n), 256, 0, st>>>(e, xbuf);
+  return cudaGetLastError();
 }
 
 cudaError_t k_publish(const double* S, const int* I, unsigned long long* pub_mapped, unsigned seq, cudaStream_t st) {

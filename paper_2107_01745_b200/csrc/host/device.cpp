@@ -1419,48 +1419,50 @@ void launch(DevState& d, SweepParams& P, const DevState::Launch& ln) {
   P.items_total = ln.count;
   SCN_CUDA(d.sweep->launch(P, d.grid, d.dyn_smem, d.max_m, d.max_mN, d.stream));
 }
-// sharded phase A: local backward; this rank's shard-stage contributions
-// and shard-stage dual rows into the (zeroed) exchange buffer. zero_rows
-// (phase API only) also zeroes the Hx rows this rank does not write.
-void phase_a(DevState& d, SweepParams& P, bool zero_rows) {
+// The exchange buffer's geometry for this rank (dual.hpp ExchangeDims).
+ExchangeDims exchange_dims(const DevState& d, const SweepParams& P) {
   const Layout& L = d.lay;
   const int W = L.nx + L.nu;
-  const int64_t ns = d.sstage_hi - d.sstage_lo;
+  ExchangeDims e{};
+  e.ns_w = static_cast<int64_t>(d.sstage_hi - d.sstage_lo) * W;
+  e.nys = d.dual_s_end - d.dual_top;
+  e.xbuf_rhs = d.xbuf_rhs;
+  e.contrib_off = static_cast<int64_t>(d.sstage_lo) * W;
+  e.dual_top = d.dual_top;
+  if (d.shard_hi > d.shard_lo) {  // else this rank has no shard-stage node: its buffer is all zeros
+    e.own_c_lo = static_cast<int64_t>(d.shard_lo - d.sstage_lo) * W;
+    e.own_c_hi = static_cast<int64_t>(d.shard_hi - d.sstage_lo) * W;
+    e.own_y_lo = L.dual_offset[d.shard_lo];
+    e.own_y_hi = L.dual_offset[d.shard_hi - 1] + L.stage_rows[d.shard_hi - 1];
+  }
+  e.nrhs = P.nrhs;
+  for (int r = 0; r < P.nrhs; ++r) {
+    e.contrib[r] = P.contrib[r];
+    e.y[r] = P.y[r];
+    e.ycomp[r] = d.ycomp[r];
+  }
+  return e;
+}
+// sharded phase A: local backward; then one kernel packs this rank's
+// shard-stage contributions and shard-stage dual rows into the exchange
+// buffer (zero elsewhere). zero_rows (phase API only) also zeroes the Hx
+// rows this rank does not write.
+void phase_a(DevState& d, SweepParams& P, bool zero_rows) {
   if (zero_rows)
     for (int r = 0; r < P.nrhs; ++r)
       for (const auto& q : d.zero_hx)
         SCN_CUDA(cudaMemsetAsync(P.Hx[r] + q.first, 0, sizeof(double) * (q.second - q.first), d.stream));
   launch(d, P, d.launches[0]);
-  SCN_CUDA(cudaMemsetAsync(d.xbuf, 0, sizeof(double) * P.nrhs * d.xbuf_rhs, d.stream));
-  const int64_t own_lo = d.shard_lo, own_hi = d.shard_hi;
-  if (own_hi <= own_lo) return;  // no shard-stage node on this rank
-  const int64_t ylo = L.dual_offset[own_lo], yhi = L.dual_offset[own_hi - 1] + L.stage_rows[own_hi - 1];
-  for (int r = 0; r < P.nrhs; ++r) {
-    double* xb = d.xbuf + r * d.xbuf_rhs;
-    SCN_CUDA(cudaMemcpyAsync(xb + (own_lo - d.sstage_lo) * W, P.contrib[r] + own_lo * W,
-                             sizeof(double) * (own_hi - own_lo) * W, cudaMemcpyDeviceToDevice, d.stream));
-    SCN_CUDA(cudaMemcpyAsync(xb + ns * W + (ylo - d.dual_top), P.y[r] + ylo, sizeof(double) * (yhi - ylo),
-                             cudaMemcpyDeviceToDevice, d.stream));
-  }
+  SCN_CUDA(k_exchange_pack(exchange_dims(d, P), d.xbuf, d.stream));
 }
-// sharded phase B: summed contributions back; launch B reads the top rows of
-// y and every rank's shard-stage rows (ycomp); top backward + forward, local
-// forward. zero_rows (phase API only): the replicated top rows of Hx are kept
-// on rank 0 only.
+// sharded phase B: one kernel unpacks the summed buffer (contributions back;
+// launch B's dual input = the top rows of y and every rank's shard-stage
+// rows, ycomp); then the top backward + forward and the local forward.
+// zero_rows (phase API only): the replicated top rows of Hx are kept on
+// rank 0 only.
 void phase_b(DevState& d, SweepParams& P, bool zero_rows) {
-  const Layout& L = d.lay;
-  const int W = L.nx + L.nu;
-  const int64_t ns = d.sstage_hi - d.sstage_lo, nys = d.dual_s_end - d.dual_top;
-  for (int r = 0; r < P.nrhs; ++r) {
-    const double* xb = d.xbuf + r * d.xbuf_rhs;
-    SCN_CUDA(cudaMemcpyAsync(P.contrib[r] + static_cast<int64_t>(d.sstage_lo) * W, xb, sizeof(double) * ns * W,
-                             cudaMemcpyDeviceToDevice, d.stream));
-    if (d.dual_top > 0)
-      SCN_CUDA(cudaMemcpyAsync(d.ycomp[r], P.y[r], sizeof(double) * d.dual_top, cudaMemcpyDeviceToDevice, d.stream));
-    SCN_CUDA(cudaMemcpyAsync(d.ycomp[r] + d.dual_top, xb + ns * W, sizeof(double) * nys, cudaMemcpyDeviceToDevice,
-                             d.stream));
-    P.y[r] = d.ycomp[r];
-  }
+  SCN_CUDA(k_exchange_unpack(exchange_dims(d, P), d.xbuf, d.stream));
+  for (int r = 0; r < P.nrhs; ++r) P.y[r] = d.ycomp[r];
   launch(d, P, d.launches[1]);
   if (zero_rows && d.rank != 0)
     for (int r = 0; r < P.nrhs; ++r)

@@ -20,20 +20,21 @@
 // Every per-item step is latency-bound (measured on B200: L2 hit ~280
 // cycles, st.release ~760, dependent DFMA 8), so the kernel overlaps items
 // in every role instead of shortening one item:
-//   warps 0..3  producers (one per staging slot, items k = p mod 4): poll
-//               the item's dependency flags (ld.acquire) and stage its small
-//               vectors (y rows, child contributions, parent x/u, u_off,
-//               affine terms) with async 8-byte copies; four such round trips
-//               are in flight at once.
-//   warps 4..15 four consumer teams of three warps (team t takes items
-//               k = t mod 4): wait for the item's matrices (slot FULL) and
-//               vectors (stage FULL), compute every product from shared
-//               memory, release the slot and the staging area.
-//   warp 16     publisher: retires items in order (CTA-scope counter) and
+//   producers   warps 0..P-1 (P = 4; 6 in the geom_p6 build), items
+//               k = p mod P: poll the item's dependency flags (ld.acquire)
+//               and stage its small vectors (y rows, child contributions,
+//               parent x/u, u_off, affine terms) with async 8-byte copies;
+//               P such round trips are in flight at once.
+//   teams       the next 12 warps: four consumer teams of three warps (team t
+//               takes items k = t mod 4): wait for the item's matrices (slot
+//               FULL) and vectors (stage FULL), compute every product from
+//               shared memory, release the slot and the staging area.
+//   publisher   the next warp: retires items in order (CTA-scope counter) and
 //               releases the flags of publishing items, one gpu-scope fence
 //               per batch of finished items.
-//   warp 17     issuer: streams the CTA's items through the matrix slots, one
-//               cp.async.bulk (TMA 1-D) per item once its slot is released.
+//   issuer      the last warp: streams the CTA's items through the matrix
+//               slots, one cp.async.bulk (TMA 1-D) per item once its slot is
+//               released.
 // Products are "dot columns" split over S in {1,2,4} threads (interleaved
 // 16-byte shared loads over padded columns + xor shuffles), for all
 // right-hand sides at once so a 2-RHS (p-NAMA) sweep reads each matrix once.

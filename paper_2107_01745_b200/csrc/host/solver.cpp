@@ -379,17 +379,24 @@ struct Engine {
     const volatile unsigned long long* w = k.pLL;
     const unsigned long long want = k.seq;
     unsigned spins = 0;
+    double drained_at = -1.0;  // the stream has finished while words were missing
     for (int i = 0; i < kPubWords;) {
       if ((w[i] >> 32) == want) {
         ++i;
         continue;
       }
       if ((++spins & 4095u) == 0) {
-        const cudaError_t q = cudaStreamQuery(st);
-        if (q != cudaSuccess && q != cudaErrorNotReady) SCN_CUDA(q);
-        if (q == cudaSuccess && !full && (w[i] >> 32) != want) {  // drained without the words: fall back
-          SCN_CUDA(cudaStreamSynchronize(st));
-          break;
+        if (drained_at < 0.0) {
+          const cudaError_t q = cudaStreamQuery(st);
+          if (q != cudaSuccess && q != cudaErrorNotReady) SCN_CUDA(q);
+          if (q == cudaSuccess) drained_at = now_ms();
+        } else if (now_ms() - drained_at > 100.0) {
+          // a finished kernel's posted writes land within microseconds: after
+          // the grace period the words are not coming
+          if (full || static_cast<int>(static_cast<unsigned>(w[i] >> 32) - static_cast<unsigned>(want)) > 0)
+            fail(SCENOPT_E_ERROR, "scalar publish " + std::to_string(want) + " never arrived (word " +
+                                      std::to_string(i) + " carries " + std::to_string(w[i] >> 32) + ")");
+          break;  // no publish was enqueued: the mirrors keep what the words hold
         }
       }
     }

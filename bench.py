@@ -201,7 +201,7 @@ def run_reference(args, world, rank):
         return time.perf_counter() - tt
 
     budget = 60.0  # seconds of timed CPU work
-    w = min(args.warmup, 1)
+    w = min(args.warmup, 3)  # warm-up rounds (the arm's own W >= 3, bounded: each round is ~0.15 s)
     round_of(w)
     tr = round_of(1)  # one concurrent sweep per thread
     k = min(args.steps, max(2, int(budget / max(tr, 1e-6))))

@@ -1340,7 +1340,9 @@ int scenopt_warm_start(scenopt_dev* h, const scenopt_solver_config* cfg, double 
     Engine e(*h);
     Stats st;
     warm_start(e, *cfg, lambda, st);
-    SCN_CUDA(cudaMemcpy(y_out, e.k.tmp2, e.D() * sizeof(double), cudaMemcpyDeviceToHost));
+    // stream-ordered: warm_start may return with its zero fill still queued (no iterations)
+    SCN_CUDA(cudaMemcpyAsync(y_out, e.k.tmp2, e.D() * sizeof(double), cudaMemcpyDeviceToHost, e.st));
+    SCN_CUDA(cudaStreamSynchronize(e.st));
     if (dual_grad_calls) *dual_grad_calls = st.dual_grad_calls;
   });
 }
@@ -1480,8 +1482,10 @@ int scenopt_lbfgs_clear(scenopt_lbfgs* b) {
     const int zero = 0;
     const double one = 1.0;
     SCN_CUDA(cudaSetDevice(b->dev->device));
-    SCN_CUDA(cudaMemcpy(b->c.I + il::LB_COUNT, &zero, sizeof(int), cudaMemcpyHostToDevice));
-    SCN_CUDA(cudaMemcpy(b->c.S + sl::GAMMA0, &one, sizeof(double), cudaMemcpyHostToDevice));
+    cudaStream_t st = b->dev->stream;  // ordered with the buffer's kernels
+    SCN_CUDA(cudaMemcpyAsync(b->c.I + il::LB_COUNT, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
+    SCN_CUDA(cudaMemcpyAsync(b->c.S + sl::GAMMA0, &one, sizeof(double), cudaMemcpyHostToDevice, st));
+    SCN_CUDA(cudaStreamSynchronize(st));  // the sources are on this frame
   });
 }
 
